@@ -1,0 +1,143 @@
+"""ctypes binding of libpcnn.so (include/pcnn.h).
+
+The structures below mirror the C declarations field for field (every field
+is int64 or double, so there is no padding to disagree about).  The library
+is built in-tree by ``__graft_entry__.build()`` / ``make``; importing the
+package without it is fine on a CPU-only box, but every device entry point
+raises ``PcnnError`` if the library or an sm_100 device is missing -- there
+is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import pathlib
+from typing import Optional
+
+LIB_PATH = pathlib.Path(__file__).resolve().parent / "libpcnn.so"
+
+c_i64 = ctypes.c_int64
+c_f64 = ctypes.c_double
+
+PCNN_OK = 0
+PCNN_ERR_TRANSFORM = -4
+
+# unit kinds
+UNIT_INGEST, UNIT_CONV, UNIT_LINEAR, UNIT_POLY, UNIT_ADD, UNIT_POLYSKIP = 1, 2, 3, 4, 5, 6
+UNIT_AFFINE, UNIT_LOCALPOOL, UNIT_BIPOOL, UNIT_GLOBALPOOL, UNIT_FLATTEN, UNIT_COPYOUT = 7, 8, 9, 10, 11, 12
+# fused pool kinds
+POOL_NONE, POOL_SUM2, POOL_BI2, POOL_GLOBAL = 0, 1, 2, 3
+# pack kinds
+PACK_CAST, PACK_BN_AFFINE, PACK_TC_WEIGHTS = 1, 2, 3
+# scale opcodes
+(OP_FILL, OP_LOAD, OP_MUL, OP_DIV, OP_SUB, OP_POWI, OP_SROOT, OP_AROOT, OP_RECIP, OP_SOLVE,
+ OP_CHECK_UNIFORM, OP_CHECK_NONZERO, OP_CHECK_NONNEG, OP_CHECK_CLOSE, OP_CHECK_ALLONE,
+ OP_SQRT, OP_STORE) = range(1, 18)
+
+MAX_FACTORS = 6
+
+
+class PcnnError(RuntimeError):
+    """A libpcnn call failed (message from pcnn_last_error)."""
+
+
+class TensorDesc(ctypes.Structure):
+    _fields_ = [(n, c_i64) for n in ("c", "h", "w", "cb", "nblk", "is_vector", "offset", "reserved")]
+
+
+_UNIT_FIELDS = ("kind", "in_", "in2", "out", "cin", "cout", "kh", "kw", "stride", "pad",
+                "w_off", "b_off", "affine_off", "residual", "res_off", "poly_deg", "poly_off",
+                "pool", "pool_off", "pool_deg", "pool_order", "in_mode", "in_div_off", "impl",
+                "tc_off", "npad")
+
+
+class UnitDesc(ctypes.Structure):
+    _fields_ = [(n, c_i64) for n in _UNIT_FIELDS] + [("reserved", c_i64 * 5)]
+
+    def __init__(self, **kw):
+        defaults = {"in_": -1, "in2": -1, "out": -1, "w_off": -1, "b_off": -1, "affine_off": -1,
+                    "res_off": -1, "poly_off": -1, "pool_off": -1, "in_div_off": -1, "tc_off": -1}
+        defaults.update(kw)
+        super().__init__(**defaults)
+
+
+class PackDesc(ctypes.Structure):
+    _fields_ = [(n, c_i64) for n in ("kind", "src", "dst", "n", "rows", "k", "r0", "r1")]
+
+
+class ScaleOp(ctypes.Structure):
+    _fields_ = [(n, c_i64) for n in ("op", "n", "dst", "a", "b", "sa", "sb", "p", "err")] + \
+               [(n, c_f64) for n in ("imm", "rtol", "atol")]
+
+
+class Factor(ctypes.Structure):
+    _fields_ = [(n, c_i64) for n in ("slot", "divide", "d1", "m1", "s1", "d2", "m2", "reserved")]
+
+
+class RewriteDesc(ctypes.Structure):
+    _fields_ = [(n, c_i64) for n in ("dst", "src", "n", "src_arena", "set_const", "n_factors")] + \
+               [("value", c_f64), ("f", Factor * MAX_FACTORS)]
+
+
+_lib: Optional[ctypes.CDLL] = None
+
+SYMBOLS = {
+    "pcnn_abi_version": ([], ctypes.c_int),
+    "pcnn_last_error": ([], ctypes.c_char_p),
+    "pcnn_device_ok": ([], ctypes.c_int),
+    "pcnn_workspace_bytes": ([ctypes.POINTER(TensorDesc), ctypes.c_int, ctypes.c_int], ctypes.c_size_t),
+    "pcnn_plan_create": ([ctypes.POINTER(UnitDesc), ctypes.c_int, ctypes.POINTER(TensorDesc), ctypes.c_int,
+                          ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                          ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "pcnn_plan_destroy": ([ctypes.c_void_p], ctypes.c_int),
+    "pcnn_plan_num_launches": ([ctypes.c_void_p], ctypes.c_int),
+    "pcnn_plan_unit_impl": ([ctypes.c_void_p, ctypes.c_int], ctypes.c_int),
+    "pcnn_forward": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int],
+                     ctypes.c_int),
+    "pcnn_forward_host": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                           ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "pcnn_forward_unit": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p],
+                          ctypes.c_int),
+    "pcnn_pack": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(PackDesc), ctypes.c_int, ctypes.c_void_p],
+                  ctypes.c_int),
+    "pcnn_redistribute": ([ctypes.c_void_p, ctypes.c_void_p, c_i64, ctypes.POINTER(ScaleOp), ctypes.c_int,
+                           ctypes.POINTER(RewriteDesc), ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                           ctypes.c_void_p], ctypes.c_int),
+}
+
+
+def lib() -> ctypes.CDLL:
+    """Load libpcnn.so (once); raise PcnnError if it was not built."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise PcnnError(f"{LIB_PATH} not built; run `make` or __graft_entry__.build()")
+        handle = ctypes.CDLL(str(LIB_PATH))
+        for name, (args, res) in SYMBOLS.items():
+            fn = getattr(handle, name)
+            fn.argtypes = args
+            fn.restype = res
+        if handle.pcnn_abi_version() != 1:
+            raise PcnnError("libpcnn ABI version mismatch")
+        _lib = handle
+    return _lib
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc != PCNN_OK:
+        msg = lib().pcnn_last_error().decode(errors="replace")
+        raise PcnnError(f"{what or 'libpcnn'} failed ({rc}): {msg}")
+
+
+def require_device() -> None:
+    """Fail loudly unless the library is built and a B200-class GPU is visible."""
+    if not lib().pcnn_device_ok():
+        raise PcnnError("no compute-capability 10.x (B200) device visible; the B200 path has no CPU fallback")
+
+
+def array(ctype, items):
+    arr = (ctype * max(len(items), 1))()
+    for i, it in enumerate(items):
+        arr[i] = it
+    return arr

@@ -1,0 +1,399 @@
+// C ABI of libpcnn: plans, forward (CUDA-graph replay), packing and
+// redistribution launches.  See include/pcnn.h for the contract.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "tc_layout.cuh"
+
+namespace pcnn {
+__global__ void redistribute_kernel(double*, double*, const pcnn_scale_op*, int, const pcnn_rewrite_desc*,
+                                    int, int64_t*, int64_t*);
+__global__ void pack_kernel(const double*, float*, const pcnn_pack_desc*, int);
+}  // namespace pcnn
+
+using namespace pcnn;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define PCNN_CUDA(call)                                                                    \
+  do {                                                                                     \
+    cudaError_t _e = (call);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      return fail(PCNN_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e));      \
+  } while (0)
+
+struct GraphEntry {
+  const float* x;
+  float* logits;
+  cudaGraphExec_t exec;
+};
+
+}  // namespace
+
+struct pcnn_plan {
+  std::vector<pcnn_unit_desc> units;
+  std::vector<pcnn_tensor_desc> tensors;
+  std::vector<TensorView> views;
+  std::vector<int> impl;  // per unit: 1 SIMT, 2 tcgen05
+  std::vector<ConvArgs> conv_args;
+  int batch = 0, input = 0, output = 0;
+  const float* params = nullptr;
+  float* ws = nullptr;
+  size_t ws_bytes = 0;
+  cudaStream_t capture_stream = nullptr;
+  std::vector<GraphEntry> graphs;
+  int launches = 0;
+};
+
+namespace {
+
+TensorView make_view(const pcnn_tensor_desc& t, float* ws) {
+  TensorView v;
+  v.base = ws + t.offset;
+  v.c = (int)t.c;
+  v.h = (int)t.h;
+  v.w = (int)t.w;
+  v.cb = (int)t.cb;
+  v.nblk = (int)t.nblk;
+  v.is_vector = (int)t.is_vector;
+  return v;
+}
+
+int64_t tensor_floats(const pcnn_tensor_desc& t, int batch) {
+  return (int64_t)batch * t.nblk * t.cb * t.h * t.w;
+}
+
+const float* P(const pcnn_plan* p, int64_t off) { return off < 0 ? nullptr : p->params + off; }
+
+int build_conv(pcnn_plan* p, int ui, ConvArgs& a) {
+  const pcnn_unit_desc& u = p->units[ui];
+  const TensorView& in = p->views[u.in];
+  const TensorView& out = p->views[u.out];
+  a.in = in;
+  a.batch = p->batch;
+  a.kh = (int)u.kh;
+  a.kw = (int)u.kw;
+  a.stride = (int)u.stride;
+  a.pad = (int)u.pad;
+  a.kp = in.nblk * a.kh * a.kw * in.cb;
+  int ho = (in.h + 2 * a.pad - a.kh) / a.stride + 1;
+  int wo = (in.w + 2 * a.pad - a.kw) / a.stride + 1;
+  a.pm.ho = ho;
+  a.pm.wo = wo;
+  a.pm.hp = ho / 2;
+  a.pm.wp = wo / 2;
+  a.pm.order = (u.pool == PCNN_POOL_SUM2 || u.pool == PCNN_POOL_BI2) ? kWindow : kPlain;
+  a.w = P(p, u.w_off);
+  a.tcw = P(p, u.tc_off);
+  EpiParams& e = a.epi;
+  e.cout = (int)u.cout;
+  e.npad = out.cpad();
+  if (u.pool == PCNN_POOL_GLOBAL) {
+    if (out.h != 1 || out.w != 1 || out.c != u.cout)
+      return fail(PCNN_ERR_INVALID, "global-pool conv needs a (cout,) output");
+  } else {
+    int ho_o = a.pm.order == kWindow ? a.pm.hp : ho, wo_o = a.pm.order == kWindow ? a.pm.wp : wo;
+    if (out.h != ho_o || out.w != wo_o || out.c != u.cout)
+      return fail(PCNN_ERR_INVALID, "conv unit " + std::to_string(ui) + ": output tensor shape mismatch");
+  }
+  a.npad = e.npad;
+  if (u.npad && u.npad != e.npad) return fail(PCNN_ERR_INVALID, "unit npad disagrees with its output tensor");
+  e.bias = P(p, u.b_off);
+  e.aff = P(p, u.affine_off);
+  e.residual = (int)u.residual;
+  e.res = P(p, u.res_off);
+  e.poly_deg = (int)u.poly_deg;
+  e.poly = P(p, u.poly_off);
+  e.pool = (int)u.pool;
+  e.pool_p = P(p, u.pool_off);
+  e.pool_deg = (int)u.pool_deg;
+  e.pool_order = (int)u.pool_order;
+  e.out = out;
+  if (u.residual) {
+    if (u.in2 < 0) return fail(PCNN_ERR_INVALID, "residual unit without skip tensor");
+    e.skip = p->views[u.in2];
+    if (e.skip.h != ho || e.skip.w != wo) return fail(PCNN_ERR_INVALID, "skip tensor shape mismatch");
+  }
+  if (u.poly_deg > kMaxPolyDeg) return fail(PCNN_ERR_UNSUPPORTED, "polynomial degree > 8");
+  if (u.pool == PCNN_POOL_BI2 && u.pool_deg > kMaxBiDeg) return fail(PCNN_ERR_UNSUPPORTED, "bivariate degree > 4");
+  if (!a.w || !e.bias) return fail(PCNN_ERR_INVALID, "conv unit without weights");
+  return PCNN_OK;
+}
+
+void enqueue_unit(pcnn_plan* p, int ui, const float* x, float* logits, cudaStream_t s) {
+  const pcnn_unit_desc& u = p->units[ui];
+  switch (u.kind) {
+    case PCNN_UNIT_INGEST:
+      launch_ingest(x, p->views[u.out], p->batch, s);
+      break;
+    case PCNN_UNIT_CONV: {
+      const ConvArgs& a = p->conv_args[ui];
+      if (u.pool == PCNN_POOL_GLOBAL)
+        cudaMemsetAsync(a.epi.out.base, 0, sizeof(float) * (size_t)p->batch * a.epi.out.cpad(), s);
+      if (p->impl[ui] == 2) launch_conv_tc(a, s);
+      else launch_conv_simt(a, s);
+      break;
+    }
+    case PCNN_UNIT_LINEAR: {
+      LinearArgs a;
+      a.in = p->views[u.in];
+      a.in_mode = (int)u.in_mode;
+      a.batch = p->batch;
+      a.n_in = (int)u.cin;
+      a.n_out = (int)u.cout;
+      a.in_div = P(p, u.in_div_off);
+      a.w = P(p, u.w_off);
+      a.bias = P(p, u.b_off);
+      a.poly_deg = (int)u.poly_deg;
+      a.poly = P(p, u.poly_off);
+      a.poly_stride = p->views[u.out].cpad();
+      a.out = p->views[u.out].base;
+      a.out_stride = p->views[u.out].cpad();
+      launch_linear(a, s);
+      break;
+    }
+    case PCNN_UNIT_COPYOUT: {
+      launch_copyout(p->views[u.in], logits, p->batch, s);
+      break;
+    }
+    default: {
+      EltArgs a;
+      a.kind = (int)u.kind;
+      a.batch = p->batch;
+      a.in = p->views[u.in];
+      if (u.in2 >= 0) a.in2 = p->views[u.in2];
+      a.out = p->views[u.out];
+      a.p = P(p, u.pool_off >= 0 ? u.pool_off : (u.poly_off >= 0 ? u.poly_off : (u.res_off >= 0 ? u.res_off : u.affine_off)));
+      a.stride = a.out.cpad();
+      a.deg = (int)(u.kind == PCNN_UNIT_POLY ? u.poly_deg : u.pool_deg);
+      a.k = (int)u.kh;
+      a.st = (int)u.stride;
+      a.pad = (int)u.pad;
+      a.axis = (int)u.pool_order;
+      launch_eltwise(a, s);
+      break;
+    }
+  }
+}
+
+void enqueue_all(pcnn_plan* p, const float* x, float* logits, cudaStream_t s) {
+  for (int i = 0; i < (int)p->units.size(); ++i) enqueue_unit(p, i, x, logits, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+int pcnn_abi_version(void) { return PCNN_ABI_VERSION; }
+
+const char* pcnn_last_error(void) { return g_last_error.c_str(); }
+
+int pcnn_device_ok(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return 0;
+  int dev = 0, major = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  return major == 10 ? 1 : 0;
+}
+
+size_t pcnn_workspace_bytes(const pcnn_tensor_desc* tensors, int n_tensors, int batch) {
+  int64_t end = 0;
+  for (int i = 0; i < n_tensors; ++i) end = std::max(end, tensors[i].offset + tensor_floats(tensors[i], batch));
+  return (size_t)end * sizeof(float);
+}
+
+int pcnn_plan_create(const pcnn_unit_desc* units, int n_units, const pcnn_tensor_desc* tensors, int n_tensors,
+                     int batch, int input_tensor, int output_tensor, const float* params, void* workspace,
+                     size_t ws_bytes, pcnn_plan** plan_out) {
+  if (!units || !tensors || n_units <= 0 || n_tensors <= 0 || batch <= 0 || !plan_out || !params || !workspace)
+    return fail(PCNN_ERR_INVALID, "pcnn_plan_create: null or empty argument");
+  if (!pcnn_device_ok()) return fail(PCNN_ERR_NO_DEVICE, "no compute capability 10.x device");
+  if (pcnn_workspace_bytes(tensors, n_tensors, batch) > ws_bytes)
+    return fail(PCNN_ERR_INVALID, "workspace too small");
+  pcnn_plan* p = new pcnn_plan();
+  p->units.assign(units, units + n_units);
+  p->tensors.assign(tensors, tensors + n_tensors);
+  p->batch = batch;
+  p->input = input_tensor;
+  p->output = output_tensor;
+  p->params = params;
+  p->ws = static_cast<float*>(workspace);
+  p->ws_bytes = ws_bytes;
+  for (auto& t : p->tensors) {
+    if (!(t.cb == 4 || t.cb == 8 || t.cb == 16 || t.cb == 32) || t.nblk * t.cb < t.c ||
+        (t.is_vector && (t.h != 1 || t.w != 1))) {
+      delete p;
+      return fail(PCNN_ERR_INVALID, "tensor block size must be 4, 8, 16 or 32");
+    }
+    p->views.push_back(make_view(t, p->ws));
+  }
+  p->impl.assign(n_units, 1);
+  p->conv_args.resize(n_units);
+  for (int i = 0; i < n_units; ++i) {
+    const pcnn_unit_desc& u = p->units[i];
+    auto bad = [&](int64_t id) { return id < -1 || id >= n_tensors; };
+    if (bad(u.in) || bad(u.in2) || bad(u.out)) {
+      delete p;
+      return fail(PCNN_ERR_INVALID, "unit " + std::to_string(i) + ": tensor id out of range");
+    }
+    if (u.kind == PCNN_UNIT_CONV) {
+      int rc = build_conv(p, i, p->conv_args[i]);
+      if (rc != PCNN_OK) {
+        delete p;
+        return rc;
+      }
+      bool want_tc = u.impl != 1;
+      if (want_tc && conv_tc_supported(p->conv_args[i]) && p->conv_args[i].tcw) p->impl[i] = 2;
+      else if (u.impl == 2) {
+        delete p;
+        return fail(PCNN_ERR_UNSUPPORTED, "unit " + std::to_string(i) + ": tcgen05 conv requested but unsupported");
+      }
+    }
+    p->launches += 1;
+  }
+  if (cudaStreamCreateWithFlags(&p->capture_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete p;
+    return fail(PCNN_ERR_CUDA, "cudaStreamCreate failed");
+  }
+  *plan_out = p;
+  return PCNN_OK;
+}
+
+int pcnn_plan_destroy(pcnn_plan* p) {
+  if (!p) return PCNN_OK;
+  for (auto& g : p->graphs) cudaGraphExecDestroy(g.exec);
+  if (p->capture_stream) cudaStreamDestroy(p->capture_stream);
+  delete p;
+  return PCNN_OK;
+}
+
+int pcnn_plan_num_launches(const pcnn_plan* p) { return p ? p->launches : -1; }
+
+int pcnn_plan_unit_impl(const pcnn_plan* p, int unit) {
+  if (!p || unit < 0 || unit >= (int)p->units.size()) return -1;
+  return p->impl[unit];
+}
+
+int pcnn_forward(pcnn_plan* p, const float* x, float* logits, void* stream, int use_graph) {
+  if (!p || !x || !logits) return fail(PCNN_ERR_INVALID, "pcnn_forward: null argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!use_graph) {
+    enqueue_all(p, x, logits, s);
+    PCNN_CUDA(cudaGetLastError());
+    return PCNN_OK;
+  }
+  for (auto& g : p->graphs)
+    if (g.x == x && g.logits == logits) {
+      PCNN_CUDA(cudaGraphLaunch(g.exec, s));
+      return PCNN_OK;
+    }
+  // capture on the plan's own stream (the legacy default stream cannot be
+  // captured), then replay on the caller's stream
+  cudaGraph_t graph;
+  PCNN_CUDA(cudaStreamBeginCapture(p->capture_stream, cudaStreamCaptureModeThreadLocal));
+  enqueue_all(p, x, logits, p->capture_stream);
+  cudaError_t le = cudaGetLastError();
+  PCNN_CUDA(cudaStreamEndCapture(p->capture_stream, &graph));
+  if (le != cudaSuccess) {
+    cudaGraphDestroy(graph);
+    return fail(PCNN_ERR_CUDA, std::string("launch during capture: ") + cudaGetErrorString(le));
+  }
+  cudaGraphExec_t exec;
+  cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ie != cudaSuccess) return fail(PCNN_ERR_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ie));
+  if (p->graphs.size() >= 4) {
+    cudaGraphExecDestroy(p->graphs.front().exec);
+    p->graphs.erase(p->graphs.begin());
+  }
+  p->graphs.push_back({x, logits, exec});
+  PCNN_CUDA(cudaGraphLaunch(exec, s));
+  return PCNN_OK;
+}
+
+int pcnn_forward_host(pcnn_plan* p, const float* x_host, float* logits_host, float* x_dev, float* logits_dev,
+                      void* stream) {
+  if (!p || !x_host || !logits_host || !x_dev || !logits_dev) return fail(PCNN_ERR_INVALID, "null argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const pcnn_tensor_desc& ti = p->tensors[p->input];
+  size_t in_bytes = sizeof(float) * (size_t)p->batch * ti.c * ti.h * ti.w;
+  const pcnn_tensor_desc& to = p->tensors[p->output];
+  size_t out_bytes = sizeof(float) * (size_t)p->batch * to.c * to.h * to.w;
+  PCNN_CUDA(cudaMemcpyAsync(x_dev, x_host, in_bytes, cudaMemcpyHostToDevice, s));
+  int rc = pcnn_forward(p, x_dev, logits_dev, stream, 1);
+  if (rc != PCNN_OK) return rc;
+  PCNN_CUDA(cudaMemcpyAsync(logits_host, logits_dev, out_bytes, cudaMemcpyDeviceToHost, s));
+  return PCNN_OK;
+}
+
+int pcnn_forward_unit(pcnn_plan* p, int unit, const float* x, float* logits, void* stream) {
+  if (!p || unit < 0 || unit >= (int)p->units.size()) return fail(PCNN_ERR_INVALID, "bad unit");
+  enqueue_unit(p, unit, x, logits, static_cast<cudaStream_t>(stream));
+  PCNN_CUDA(cudaGetLastError());
+  return PCNN_OK;
+}
+
+int pcnn_pack(const double* master, float* packed, const pcnn_pack_desc* ops, int n_ops, void* stream) {
+  if (!master || !packed || (!ops && n_ops)) return fail(PCNN_ERR_INVALID, "pcnn_pack: null argument");
+  if (n_ops == 0) return PCNN_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  pcnn_pack_desc* d_ops = nullptr;
+  PCNN_CUDA(cudaMallocAsync(&d_ops, sizeof(pcnn_pack_desc) * n_ops, s));
+  PCNN_CUDA(cudaMemcpyAsync(d_ops, ops, sizeof(pcnn_pack_desc) * n_ops, cudaMemcpyHostToDevice, s));
+  pack_kernel<<<148 * 4, 256, 0, s>>>(master, packed, d_ops, n_ops);
+  cudaError_t le = cudaGetLastError();
+  PCNN_CUDA(cudaFreeAsync(d_ops, s));
+  if (le != cudaSuccess) return fail(PCNN_ERR_CUDA, std::string("pack_kernel: ") + cudaGetErrorString(le));
+  return PCNN_OK;
+}
+
+int pcnn_redistribute(double* master, double* arena, int64_t arena_len, const pcnn_scale_op* ops, int n_ops,
+                      const pcnn_rewrite_desc* rewrites, int n_rewrites, int64_t* status_dev, int64_t* flags_dev,
+                      void* stream) {
+  if (!master || !arena || !status_dev || (!ops && n_ops) || (!rewrites && n_rewrites))
+    return fail(PCNN_ERR_INVALID, "pcnn_redistribute: null argument");
+  for (int i = 0; i < n_ops; ++i) {
+    const pcnn_scale_op& o = ops[i];
+    if (o.op < PCNN_OP_FILL || o.op > PCNN_OP_STORE || o.n < 0 || o.dst < 0)
+      return fail(PCNN_ERR_INVALID, "bad scale op " + std::to_string(i));
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  size_t ob = sizeof(pcnn_scale_op) * (size_t)std::max(n_ops, 1);
+  size_t rb = sizeof(pcnn_rewrite_desc) * (size_t)std::max(n_rewrites, 1);
+  char* d = nullptr;
+  PCNN_CUDA(cudaMallocAsync((void**)&d, ob + rb, s));
+  pcnn_scale_op* d_ops = reinterpret_cast<pcnn_scale_op*>(d);
+  pcnn_rewrite_desc* d_rw = reinterpret_cast<pcnn_rewrite_desc*>(d + ob);
+  if (n_ops) PCNN_CUDA(cudaMemcpyAsync(d_ops, ops, sizeof(pcnn_scale_op) * n_ops, cudaMemcpyHostToDevice, s));
+  if (n_rewrites)
+    PCNN_CUDA(cudaMemcpyAsync(d_rw, rewrites, sizeof(pcnn_rewrite_desc) * n_rewrites, cudaMemcpyHostToDevice, s));
+  PCNN_CUDA(cudaMemsetAsync(status_dev, 0, 4 * sizeof(int64_t), s));
+  int dev = 0, nsm = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, redistribute_kernel, 256, 0);
+  int blocks = std::max(1, nsm * std::min(per_sm, 4));
+  int64_t* flags = flags_dev ? flags_dev : status_dev + 2;
+  void* args[] = {&master, &arena, &d_ops, &n_ops, &d_rw, &n_rewrites, &status_dev, &flags};
+  cudaError_t le = cudaLaunchCooperativeKernel((void*)redistribute_kernel, dim3(blocks), dim3(256), args, 0, s);
+  cudaFreeAsync(d, s);
+  if (le != cudaSuccess) return fail(PCNN_ERR_CUDA, std::string("redistribute_kernel: ") + cudaGetErrorString(le));
+  (void)arena_len;
+  return PCNN_OK;
+}
+
+}  // extern "C"

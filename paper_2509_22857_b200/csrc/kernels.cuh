@@ -1,0 +1,58 @@
+// Kernel argument blocks and launchers (internal to libpcnn).
+#pragma once
+
+#include <algorithm>
+
+#include "epilogue.cuh"
+
+namespace pcnn {
+
+struct ConvArgs {
+  TensorView in;
+  PixelMap pm;
+  int batch;
+  int kh, kw, stride, pad;
+  int kp;            // padded K = in.nblk * kh * kw * in.cb
+  int npad;          // padded output channels
+  const float* w;    // [npad][kp] float32
+  const float* tcw;  // tcgen05 weight image or null
+  EpiParams epi;
+};
+
+struct LinearArgs {
+  TensorView in;
+  int in_mode, batch, n_in, n_out;
+  const float* in_div;
+  const float* w;
+  const float* bias;
+  int poly_deg;
+  const float* poly;
+  int64_t poly_stride;
+  float* out;
+  int64_t out_stride;
+};
+
+struct EltArgs {
+  int kind, batch;
+  TensorView in, in2, out;
+  const float* p;
+  int64_t stride;
+  int deg, k, st, pad, axis;
+};
+
+inline int64_t host_pixel_count(const PixelMap& pm, int batch) {
+  return pm.order == kPlain ? (int64_t)batch * pm.ho * pm.wo : (int64_t)batch * pm.hp * pm.wp * 4;
+}
+
+void launch_ingest(const float* x, const TensorView& t, int batch, cudaStream_t s);
+void launch_conv_simt(const ConvArgs& a, cudaStream_t s);
+void launch_linear(const LinearArgs& a, cudaStream_t s);
+void launch_eltwise(const EltArgs& a, cudaStream_t s);
+void launch_copyout(const TensorView& t, float* dst, int batch, cudaStream_t s);
+
+// tcgen05 path (conv_tc.cu); returns false if the shape is not supported
+bool conv_tc_supported(const ConvArgs& a);
+void launch_conv_tc(const ConvArgs& a, cudaStream_t s);
+void tc_weight_image_dims(int npad, int kp, int64_t* floats);
+
+}  // namespace pcnn

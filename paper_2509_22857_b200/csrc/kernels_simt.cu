@@ -1,0 +1,386 @@
+// SIMT float32 kernels: input ingest, implicit-GEMM conv with the fused
+// epilogue (used for small/odd layers and as the tcgen05 cross-check), the
+// dense layer, and standalone elementwise/pool kernels so every node kind of
+// the graph IR runs on the GPU even when it is not fused.
+#include "kernels.cuh"
+
+namespace pcnn {
+
+// ---------------------------------------------------------------------------
+// ingest: user NCHW float32 -> channel-blocked [B][nblk][H][W][cb], pad = 0
+// ---------------------------------------------------------------------------
+__global__ void ingest_kernel(const float* __restrict__ x, TensorView t, int batch) {
+  int64_t total = (int64_t)batch * t.nblk * t.h * t.w * t.cb;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int ci = (int)(i % t.cb);
+    int64_t r = i / t.cb;
+    int xw = (int)(r % t.w); r /= t.w;
+    int yh = (int)(r % t.h); r /= t.h;
+    int blk = (int)(r % t.nblk);
+    int b = (int)(r / t.nblk);
+    int ch = blk * t.cb + ci;
+    float v = 0.f;
+    if (ch < t.c) v = __ldg(x + (((int64_t)b * t.c + ch) * t.h + yh) * t.w + xw);
+    t.base[i] = v;
+  }
+}
+
+void launch_ingest(const float* x, const TensorView& t, int batch, cudaStream_t s) {
+  int64_t total = (int64_t)batch * t.nblk * t.h * t.w * t.cb;
+  int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  ingest_kernel<<<blocks, 256, 0, s>>>(x, t, batch);
+}
+
+// ---------------------------------------------------------------------------
+// SIMT implicit-GEMM conv.  Tile BM pixels x BN channels, 256 threads, each
+// thread 4 consecutive pixel rows x 4 consecutive channels, K staged by 16.
+// ---------------------------------------------------------------------------
+template <int BN>
+__global__ void __launch_bounds__(256) conv_simt_kernel(ConvArgs a) {
+  constexpr int TN = 4, TM = 4, BK = 16;
+  constexpr int NTX = BN / TN;          // threads along N
+  constexpr int NTY = 256 / NTX;        // threads along M
+  constexpr int BM = NTY * TM;
+  __shared__ __align__(16) float As[BK][BM];
+  __shared__ __align__(16) float Bs[BK][BN];
+  __shared__ int pb[BM], piy[BM], pix_[BM];
+  __shared__ int kky[BK], kkx[BK];
+  __shared__ int64_t koff[BK];
+
+  const int tid = threadIdx.x;
+  const int tx = tid % NTX, ty = tid / NTX;
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int n0 = blockIdx.y * BN;
+  const TensorView& in = a.in;
+  const int64_t M = a.pm.count(a.batch);
+  const int KP = a.kp;
+
+  for (int i = tid; i < BM; i += 256) {
+    int64_t m = m0 + i;
+    int b = -1, oy = 0, ox = 0;
+    if (m < M) a.pm.decode(m, b, oy, ox);
+    pb[i] = b;
+    piy[i] = oy * a.stride - a.pad;
+    pix_[i] = ox * a.stride - a.pad;
+  }
+  float acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
+
+  const int64_t plane = (int64_t)in.h * in.w * in.cb;
+  const int taps_cb = a.kh * a.kw * in.cb;
+  for (int k0 = 0; k0 < KP; k0 += BK) {
+    __syncthreads();
+    if (tid < BK) {
+      int k = k0 + tid;
+      if (k < KP) {
+        int blk = k / taps_cb;
+        int r = k - blk * taps_cb;
+        int tap = r / in.cb, ci = r - tap * in.cb;
+        int ky = tap / a.kw, kx = tap - ky * a.kw;
+        kky[tid] = ky;
+        kkx[tid] = kx;
+        koff[tid] = blk * plane + ((int64_t)ky * in.w + kx) * in.cb + ci;
+      } else {
+        kky[tid] = -100000;
+        kkx[tid] = 0;
+        koff[tid] = 0;
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < BK * BM; e += 256) {
+      int kk = e / BM, mm = e - kk * BM;
+      float v = 0.f;
+      int b = pb[mm];
+      if (b >= 0) {
+        int iy = piy[mm] + kky[kk], ix = pix_[mm] + kkx[kk];
+        if (iy >= 0 && iy < in.h && ix >= 0 && ix < in.w)
+          v = __ldg(in.base + (int64_t)b * in.nblk * plane + koff[kk] + ((int64_t)piy[mm] * in.w + pix_[mm]) * in.cb);
+      }
+      As[kk][mm] = v;
+    }
+    for (int e = tid; e < BK * BN; e += 256) {
+      int nn = e / BK, kk = e - nn * BK;
+      int n = n0 + nn, k = k0 + kk;
+      Bs[kk][nn] = (n < a.npad && k < KP) ? __ldg(a.w + (int64_t)n * KP + k) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float4 av = *reinterpret_cast<const float4*>(&As[kk][ty * TM]);
+      float4 bv = *reinterpret_cast<const float4*>(&Bs[kk][tx * TN]);
+      float ar[4] = {av.x, av.y, av.z, av.w}, br[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(ar[i], br[j], acc[i][j]);
+    }
+  }
+
+  // epilogue
+  const EpiParams& e = a.epi;
+  const int nb = n0 + tx * TN;
+  if (nb >= a.npad) return;
+  float v[TM][TN];
+  int bs[TM], oys[TM], oxs[TM];
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    int64_t m = m0 + ty * TM + i;
+    bs[i] = -1;
+    if (m < M) a.pm.decode(m, bs[i], oys[i], oxs[i]);
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      int ch = nb + j;
+      v[i][j] = (bs[i] >= 0 && ch < e.cout) ? epi_point(e, acc[i][j], bs[i], oys[i], oxs[i], ch) : 0.f;
+    }
+  }
+  if (e.pool == PCNN_POOL_NONE) {
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      if (bs[i] < 0) continue;
+      float4 o = make_float4(v[i][0], v[i][1], v[i][2], v[i][3]);
+      *reinterpret_cast<float4*>(e.out.pix(bs[i], nb, oys[i], oxs[i])) = o;
+    }
+  } else if (e.pool == PCNN_POOL_GLOBAL) {
+    const float div = __ldg(e.pool_p);
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      if (bs[i] < 0) continue;
+#pragma unroll
+      for (int j = 0; j < TN; ++j)
+        if (nb + j < e.cout) atomicAdd(e.out.base + (int64_t)bs[i] * e.npad + nb + j, v[i][j] * div);
+    }
+  } else {
+    // rows ty*4..ty*4+3 are one 2x2 window (WINDOW order, BM % 4 == 0)
+    if (bs[0] < 0) return;
+    float o[TN];
+#pragma unroll
+    for (int j = 0; j < TN; ++j)
+      o[j] = (nb + j < e.cout) ? epi_pool4(e, nb + j, v[0][j], v[1][j], v[2][j], v[3][j]) : 0.f;
+    *reinterpret_cast<float4*>(e.out.pix(bs[0], nb, oys[0] >> 1, oxs[0] >> 1)) =
+        make_float4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+void launch_conv_simt(const ConvArgs& a, cudaStream_t s) {
+  int64_t M = host_pixel_count(a.pm, a.batch);
+  int bn = a.npad >= 64 ? 64 : (a.npad >= 32 ? 32 : (a.npad >= 16 ? 16 : 8));
+  int bm = 4 * 256 / (bn / 4);
+  dim3 grid((unsigned)((M + bm - 1) / bm), (unsigned)((a.npad + bn - 1) / bn));
+  switch (bn) {
+    case 64: conv_simt_kernel<64><<<grid, 256, 0, s>>>(a); break;
+    case 32: conv_simt_kernel<32><<<grid, 256, 0, s>>>(a); break;
+    case 16: conv_simt_kernel<16><<<grid, 256, 0, s>>>(a); break;
+    default: conv_simt_kernel<8><<<grid, 256, 0, s>>>(a); break;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// dense layer: out[b][k] = W[k] . view(b) + bias[k]  [-> poly]
+// view: vector, flatten of a blocked spatial tensor (C-major), or global sum.
+// Block = 8 warps over 32 outputs x 16 images; X tile staged in smem.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) linear_kernel(LinearArgs a) {
+  extern __shared__ float xs[];  // [16][n_in]
+  constexpr int BB = 16;
+  const int b0 = blockIdx.y * BB;
+  const int n = a.n_in;
+  const TensorView& in = a.in;
+  const int hw = in.h * in.w;
+  const float div = a.in_div ? __ldg(a.in_div) : 1.f;
+  for (int e = threadIdx.x; e < BB * n; e += blockDim.x) {
+    int bb = e / n, j = e - bb * n;
+    int b = b0 + bb;
+    float v = 0.f;
+    if (b < a.batch) {
+      if (a.in_mode == 0) {
+        v = __ldg(in.base + (int64_t)b * in.cpad() + j);
+      } else if (a.in_mode == 1) {
+        int c = j / hw, r = j - c * hw;
+        int y = r / in.w, xw = r - y * in.w;
+        v = *in.at(b, c, y, xw);
+      } else {
+        const float* p = in.at(b, j, 0, 0);
+        float s = 0.f;
+        for (int q = 0; q < hw; ++q) s += p[(int64_t)q * in.cb];
+        v = s * div;
+      }
+    }
+    xs[e] = v;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int kk = warp; kk < 32; kk += 8) {
+    int k = blockIdx.x * 32 + kk;
+    if (k >= a.out_stride) break;
+    if (k >= a.n_out) {  // zero the padded channels
+      if (lane < BB && b0 + lane < a.batch) a.out[(int64_t)(b0 + lane) * a.out_stride + k] = 0.f;
+      continue;
+    }
+    const float* wr = a.w + (int64_t)k * n;
+    float acc[BB];
+#pragma unroll
+    for (int i = 0; i < BB; ++i) acc[i] = 0.f;
+    for (int j = lane; j < n; j += 32) {
+      float wv = __ldg(wr + j);
+#pragma unroll
+      for (int i = 0; i < BB; ++i) acc[i] = fmaf(wv, xs[i * n + j], acc[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < BB; ++i) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+    }
+    if (lane < BB) {
+      float v = acc[0];
+#pragma unroll
+      for (int i = 1; i < BB; ++i)
+        if (lane == i) v = acc[i];
+      int b = b0 + lane;
+      if (b < a.batch) {
+        v += __ldg(a.bias + k);
+        if (a.poly_deg) v = horner(a.poly, a.poly_stride, a.poly_deg, k, v);
+        a.out[(int64_t)b * a.out_stride + k] = v;
+      }
+    }
+  }
+}
+
+void launch_linear(const LinearArgs& a, cudaStream_t s) {
+  dim3 grid((unsigned)((a.out_stride + 31) / 32), (unsigned)((a.batch + 15) / 16));
+  size_t smem = (size_t)16 * a.n_in * sizeof(float);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(linear_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  linear_kernel<<<grid, 256, smem, s>>>(a);
+}
+
+// ---------------------------------------------------------------------------
+// standalone elementwise / pool kernels (one thread per 4-channel group)
+// ---------------------------------------------------------------------------
+__global__ void eltwise_kernel(EltArgs a) {
+  const TensorView& o = a.out;
+  const int groups = o.cpad() / 4;
+  const int64_t total = (int64_t)a.batch * groups * o.h * o.w;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int xw = (int)(i % o.w);
+    int64_t r = i / o.w;
+    int y = (int)(r % o.h); r /= o.h;
+    int g = (int)(r % groups);
+    int b = (int)(r / groups);
+    int ch0 = g * 4;
+    float res[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int ch = ch0 + j;
+      float v = 0.f;
+      if (ch < o.c) {
+        switch (a.kind) {
+          case PCNN_UNIT_POLY: v = horner(a.p, a.stride, a.deg, ch, *a.in.at(b, ch, y, xw)); break;
+          case PCNN_UNIT_ADD: v = *a.in.at(b, ch, y, xw) + *a.in2.at(b, ch, y, xw); break;
+          case PCNN_UNIT_POLYSKIP:
+            v = polyskip(a.p, a.stride, ch, *a.in.at(b, ch, y, xw), *a.in2.at(b, ch, y, xw));
+            break;
+          case PCNN_UNIT_AFFINE:
+            v = fmaf(*a.in.at(b, ch, y, xw), __ldg(a.p + ch), __ldg(a.p + a.stride + ch));
+            break;
+          case PCNN_UNIT_LOCALPOOL: {
+            float s = 0.f;
+            for (int dy = 0; dy < a.k; ++dy) {
+              int iy = y * a.st - a.pad + dy;
+              if (iy < 0 || iy >= a.in.h) continue;
+              for (int dx = 0; dx < a.k; ++dx) {
+                int ix = xw * a.st - a.pad + dx;
+                if (ix < 0 || ix >= a.in.w) continue;
+                s += *a.in.at(b, ch, iy, ix);
+              }
+            }
+            v = s * __ldg(a.p);
+            break;
+          }
+          case PCNN_UNIT_BIPOOL: {
+            float xv, yv;
+            if (a.axis == 0) { xv = *a.in.at(b, ch, y, 2 * xw); yv = *a.in.at(b, ch, y, 2 * xw + 1); }
+            else { xv = *a.in.at(b, ch, 2 * y, xw); yv = *a.in.at(b, ch, 2 * y + 1, xw); }
+            v = bivariate(a.p, a.stride, a.deg, ch, xv, yv);
+            break;
+          }
+          default: break;
+        }
+      }
+      res[j] = v;
+    }
+    *reinterpret_cast<float4*>(o.pix(b, ch0, y, xw)) = make_float4(res[0], res[1], res[2], res[3]);
+  }
+}
+
+// global pool / flatten: spatial -> vector [B][c] or [B][c*h*w]
+__global__ void to_vector_kernel(EltArgs a) {
+  const TensorView& in = a.in;
+  const int hw = in.h * in.w;
+  if (a.kind == PCNN_UNIT_GLOBALPOOL) {
+    // one warp per (b, channel)
+    const int64_t warps = (int64_t)a.batch * in.c;
+    const int lane = threadIdx.x & 31;
+    const float div = __ldg(a.p);
+    for (int64_t wi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; wi < warps;
+         wi += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+      int b = (int)(wi / in.c), ch = (int)(wi % in.c);
+      const float* p = in.at(b, ch, 0, 0);
+      float s = 0.f;
+      for (int q = lane; q < hw; q += 32) s += p[(int64_t)q * in.cb];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) a.out.base[(int64_t)b * a.out.cpad() + ch] = s * div;
+    }
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)a.batch * a.out.cpad();
+         i += (int64_t)gridDim.x * blockDim.x)
+      if ((int)(i % a.out.cpad()) >= in.c) a.out.base[i] = 0.f;
+  } else {
+    const int64_t n = (int64_t)in.c * hw;
+    const int64_t np = a.out.cpad();
+    const int64_t total = (int64_t)a.batch * np;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      int b = (int)(i / np);
+      int64_t j = i - (int64_t)b * np;
+      float v = 0.f;
+      if (j < n) {
+        int c = (int)(j / hw), r = (int)(j - (int64_t)c * hw);
+        v = *in.at(b, c, r / in.w, r % in.w);
+      }
+      a.out.base[i] = v;
+    }
+  }
+}
+
+void launch_eltwise(const EltArgs& a, cudaStream_t s) {
+  if (a.kind == PCNN_UNIT_GLOBALPOOL || a.kind == PCNN_UNIT_FLATTEN) {
+    to_vector_kernel<<<148 * 8, 256, 0, s>>>(a);
+    return;
+  }
+  int64_t total = (int64_t)a.batch * (a.out.cpad() / 4) * a.out.h * a.out.w;
+  int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  eltwise_kernel<<<std::max(blocks, 1), 256, 0, s>>>(a);
+}
+
+// blocked tensor -> user output [B][C][H][W] (logits [B][K] when H = W = 1)
+__global__ void copyout_kernel(TensorView t, float* __restrict__ dst, int batch) {
+  const int64_t hw = (int64_t)t.h * t.w;
+  const int64_t n = (int64_t)batch * t.c * hw;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i % hw, bc = i / hw;
+    int c = (int)(bc % t.c), b = (int)(bc / t.c);
+    dst[i] = *t.at(b, c, (int)(r / t.w), (int)(r % t.w));
+  }
+}
+
+void launch_copyout(const TensorView& t, float* dst, int batch, cudaStream_t s) {
+  int64_t n = (int64_t)batch * t.c * t.h * t.w;
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  copyout_kernel<<<std::max(blocks, 1), 256, 0, s>>>(t, dst, batch);
+}
+
+}  // namespace pcnn

@@ -1,0 +1,152 @@
+// Weight redistribution as one cooperative kernel, and parameter packing.
+//
+// Phase (a), block 0 only: run the straight-line scale program (pcnn_scale_op)
+// over float64 vectors in the arena, in order -- update terms upsilon
+// (reference transforms.py:296-318), their powers/roots/reciprocals, and the
+// channelwise scale solve of redistribute_pass (transforms.py:515-659).
+// Refusals the reference raises as TransformError are value checks here
+// (CHECK_* ops); the first failure is written to status and phase (b) is
+// skipped.
+// Phase (b), all blocks after a grid barrier: every rewrite descriptor
+// rescales one float64 parameter tensor in place, applying its factor chain
+// in order (transforms.py:374-485 per donor, :661-704 channelwise).
+#include <cooperative_groups.h>
+
+#include <cmath>
+
+#include "kernels.cuh"
+#include "tc_layout.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace pcnn {
+
+__device__ __forceinline__ double ipow(double x, long long p) {
+  // exact repeated squaring for small positive p matches x*x*... closely;
+  // use pow() like numpy for the general case
+  if (p == 1) return x;
+  if (p == 2) return x * x;  // numpy's square fast path
+  if (p == 0) return 1.0;
+  return pow(x, (double)p);
+}
+
+__device__ void run_program(const double* __restrict__ master_ro, double* master, double* arena,
+                            const pcnn_scale_op* ops, int n_ops, int64_t* status, int64_t* flags) {
+  __shared__ int failed;
+  __shared__ int bad;
+  if (threadIdx.x == 0) failed = 0;
+  __syncthreads();
+  for (int k = 0; k < n_ops; ++k) {
+    const pcnn_scale_op o = ops[k];
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < o.n; i += blockDim.x) {
+      double A = 0.0, B = 0.0;
+      if (o.op != PCNN_OP_FILL && o.op != PCNN_OP_LOAD) A = arena[o.a + i * o.sa];
+      if (o.op == PCNN_OP_MUL || o.op == PCNN_OP_DIV || o.op == PCNN_OP_SUB || o.op == PCNN_OP_SOLVE ||
+          o.op == PCNN_OP_CHECK_CLOSE)
+        B = arena[o.b + i * o.sb];
+      switch (o.op) {
+        case PCNN_OP_FILL: arena[o.dst + i] = o.imm; break;
+        case PCNN_OP_LOAD: arena[o.dst + i] = master[o.a + i * o.sa]; break;
+        case PCNN_OP_MUL: arena[o.dst + i] = A * B; break;
+        case PCNN_OP_DIV: arena[o.dst + i] = A / B; break;
+        case PCNN_OP_SUB: arena[o.dst + i] = A - B; break;
+        case PCNN_OP_POWI: arena[o.dst + i] = o.p >= 0 ? ipow(A, o.p) : pow(A, (double)o.p); break;
+        case PCNN_OP_SROOT: arena[o.dst + i] = copysign(pow(fabs(A), 1.0 / (double)o.p), A); break;
+        case PCNN_OP_AROOT: arena[o.dst + i] = pow(fabs(A), 1.0 / (double)o.p); break;
+        case PCNN_OP_RECIP: arena[o.dst + i] = 1.0 / A; break;
+        case PCNN_OP_SQRT: arena[o.dst + i] = sqrt(A); break;
+        case PCNN_OP_SOLVE: {
+          double r = B / A;
+          if ((o.p % 2) == 0 && r < 0) bad = 1;
+          double s = (r > 0) ? 1.0 : ((r < 0) ? -1.0 : 0.0);
+          arena[o.dst + i] = s * pow(fabs(r), 1.0 / (double)o.p);
+          break;
+        }
+        case PCNN_OP_CHECK_UNIFORM:
+          if (A != arena[o.a]) bad = 1;
+          break;
+        case PCNN_OP_CHECK_NONZERO:
+          if (A == 0.0) bad = 1;
+          break;
+        case PCNN_OP_CHECK_NONNEG:
+          if (A < 0.0) bad = 1;
+          break;
+        case PCNN_OP_CHECK_CLOSE:
+          if (!(fabs(A - B) <= o.atol + o.rtol * fabs(B))) bad = 1;
+          break;
+        case PCNN_OP_CHECK_ALLONE:
+          if (A != 1.0) bad = 1;
+          break;
+        case PCNN_OP_STORE: master[o.dst + i * o.sa] = A; break;
+        default: bad = 2; break;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (o.op == PCNN_OP_CHECK_ALLONE) {
+        flags[o.p] = bad ? 0 : 1;
+      } else if (bad) {
+        status[0] = bad == 2 ? -1 : o.err;
+        status[1] = k;
+        failed = 1;
+      }
+    }
+    __syncthreads();
+    if (failed) return;
+  }
+}
+
+__global__ void redistribute_kernel(double* master, double* arena, const pcnn_scale_op* ops, int n_ops,
+                                    const pcnn_rewrite_desc* rw, int n_rw, int64_t* status,
+                                    int64_t* flags) {
+  cg::grid_group grid = cg::this_grid();
+  if (blockIdx.x == 0) run_program(master, master, arena, ops, n_ops, status, flags);
+  grid.sync();
+  if (status[0] != 0) return;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  for (int d = 0; d < n_rw; ++d) {
+    const pcnn_rewrite_desc& r = rw[d];
+    const double* src = r.src_arena ? arena + r.src : master + r.src;
+    for (int64_t e = tid; e < r.n; e += nthreads) {
+      double v;
+      if (r.set_const) {
+        v = r.value;
+      } else {
+        v = src[e];
+        for (int f = 0; f < r.n_factors; ++f) {
+          const pcnn_factor& F = r.f[f];
+          int64_t idx = ((e / F.d1) % F.m1) * F.s1 + (e / F.d2) % F.m2;
+          double fv = arena[F.slot + idx];
+          v = F.divide ? v / fv : v * fv;
+        }
+      }
+      master[r.dst + e] = v;
+    }
+  }
+}
+
+__global__ void pack_kernel(const double* __restrict__ master, float* __restrict__ packed,
+                            const pcnn_pack_desc* ops, int n_ops) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  for (int k = 0; k < n_ops; ++k) {
+    const pcnn_pack_desc o = ops[k];
+    if (o.kind == PCNN_PACK_CAST) {
+      for (int64_t i = tid; i < o.n; i += nthreads) packed[o.dst + i] = (float)master[o.src + i];
+    } else if (o.kind == PCNN_PACK_BN_AFFINE) {
+      const double* g = master + o.src;
+      for (int64_t i = tid; i < o.n; i += nthreads) {
+        double s = g[i] / g[3 * o.n + i];
+        packed[o.dst + i] = (float)s;
+        packed[o.dst + o.n + i] = (float)(g[o.n + i] - s * g[2 * o.n + i]);
+      }
+    } else if (o.kind == PCNN_PACK_TC_WEIGHTS) {
+      pack_tc_weights_device(master + o.src, packed + o.dst, (int)o.rows, (int)o.k, tid, nthreads);
+    }
+  }
+}
+
+}  // namespace pcnn

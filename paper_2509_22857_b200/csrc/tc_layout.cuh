@@ -1,0 +1,61 @@
+// Weight image of the tcgen05 conv kernel.
+//
+// The B operand (weights, N = output channels, K = im2col depth) is split
+// into tf32 hi and lo parts (3xTF32: a*b ~ ahi*bhi + ahi*blo + alo*bhi) and
+// stored exactly as the kernel's shared-memory tiles: K-major, 128-byte
+// swizzle (UMMA layout SWIZZLE_128B, 8-row atoms of 1024 B, 16-byte chunk c
+// of row r at chunk position c ^ (r & 7)).  One K-block = 32 tf32 of every
+// row.  Global order: [n_tile][k_block][hi, lo][NT rows x 32], so one bulk
+// copy of 2*NT*128 bytes brings both parts of a K-block.
+#pragma once
+
+#include <stdint.h>
+
+namespace pcnn {
+
+constexpr int kTcBK = 32;  // tf32 elements per K-block (128 bytes per row)
+
+__host__ __device__ inline int tc_ntile(int npad) { return npad <= 128 ? npad : 128; }
+__host__ __device__ inline int tc_kblocks(int kp) { return (kp + kTcBK - 1) / kTcBK; }
+
+__device__ __forceinline__ uint32_t f32_to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+// float index of (row n, depth k, part) inside the image
+__host__ __device__ inline int64_t tc_image_index(int n, int k, int part, int npad, int kp) {
+  const int nt_rows = tc_ntile(npad);
+  const int nkb = tc_kblocks(kp);
+  const int nt = n / nt_rows, r = n % nt_rows;
+  const int kb = k / kTcBK, kk = k % kTcBK;
+  const int chunk = (kk >> 2) ^ (r & 7);
+  const int64_t base = ((int64_t)(nt * nkb + kb) * 2 + part) * nt_rows * kTcBK;
+  return base + (int64_t)r * kTcBK + chunk * 4 + (kk & 3);
+}
+
+__host__ __device__ inline int64_t tc_image_floats(int npad, int kp) {
+  const int nt_rows = tc_ntile(npad);
+  const int ntiles = (npad + nt_rows - 1) / nt_rows;
+  return (int64_t)ntiles * tc_kblocks(kp) * 2 * nt_rows * kTcBK;
+}
+
+// pack src [rows][k] float64 into the image (zero K padding)
+__device__ inline void pack_tc_weights_device(const double* src, float* dst, int rows, int k,
+                                              int64_t tid, int64_t nthreads) {
+  const int kpad = tc_kblocks(k) * kTcBK;
+  const int64_t total = (int64_t)rows * kpad;
+  for (int64_t i = tid; i < total; i += nthreads) {
+    int n = (int)(i / kpad), kk = (int)(i % kpad);
+    double w = kk < k ? src[(int64_t)n * k + kk] : 0.0;
+    float wf = (float)w;
+    uint32_t hi = f32_to_tf32(wf);
+    float lo_f = (float)(w - (double)__uint_as_float(hi));
+    uint32_t lo = f32_to_tf32(lo_f);
+    dst[tc_image_index(n, kk, 0, rows, k)] = __uint_as_float(hi);
+    dst[tc_image_index(n, kk, 1, rows, k)] = __uint_as_float(lo);
+  }
+}
+
+}  // namespace pcnn

@@ -1,0 +1,172 @@
+"""Device-resident engine: float64 master parameters, packed float32 images,
+execution plans, and the batched GPU forward.
+
+``Engine(g)`` uploads a graph once; ``forward`` runs the fused network on the
+GPU (CUDA-graph replay inside libpcnn); ``redistribute`` runs a compiled
+redistribution program in place on the device master and re-packs; and
+``to_graph`` downloads the parameters into a new ``ModelGraph``.
+
+Drop-in functions with the reference's names live here too:
+``reference_eval(g, image)`` (reference graph.py:413-426) and the batched
+``forward(g, x)``.  They run on the GPU -- there is no CPU fallback; without
+libpcnn.so or a B200 they raise ``PcnnError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Dict, Optional, Tuple
+
+import numpy as np
+
+from . import _lib as L
+from .graph import GraphError, ModelGraph
+from .lowering import Lowered, graph_from_master, lower, master_array
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream_handle(stream=None) -> ctypes.c_void_p:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+class Plan:
+    """A libpcnn plan for one batch size: workspace + unit table."""
+
+    def __init__(self, engine: "Engine", batch: int, impl: int = 0):
+        torch = _torch()
+        lw = engine.lw
+        self.batch = batch
+        tdescs, floats = lw.tensor_descs(batch)
+        self.ws = torch.zeros(max(floats, 1), dtype=torch.float32, device=engine.device)
+        self.units = lw.unit_descs(impl)
+        self.tdescs = tdescs
+        handle = ctypes.c_void_p()
+        L.check(L.lib().pcnn_plan_create(self.units, len(lw.units), tdescs, len(lw.tensors), batch,
+                                         lw.input_tensor, lw.output_tensor,
+                                         ctypes.c_void_p(engine.packed.data_ptr()),
+                                         ctypes.c_void_p(self.ws.data_ptr()),
+                                         self.ws.numel() * 4, ctypes.byref(handle)),
+                "pcnn_plan_create")
+        self.handle = handle
+        self.n_units = len(lw.units)
+
+    def launches(self) -> int:
+        return L.lib().pcnn_plan_num_launches(self.handle)
+
+    def unit_impl(self, i: int) -> int:
+        return L.lib().pcnn_plan_unit_impl(self.handle, i)
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and L._lib is not None:
+            L._lib.pcnn_plan_destroy(h)
+            self.handle = None
+
+
+class Engine:
+    """One graph resident on the GPU."""
+
+    def __init__(self, g: ModelGraph, device=None, use_tc: bool = True, impl: int = 0,
+                 lowered: Optional[Lowered] = None):
+        torch = _torch()
+        L.require_device()
+        self.device = torch.device(device or "cuda")
+        self.lw = lowered or lower(g, use_tc=use_tc)
+        self.impl = impl
+        m = master_array(self.lw._chunks, self.lw.master_size)
+        self.master = torch.from_numpy(m).to(self.device)
+        self.packed = torch.zeros(self.lw.packed_size, dtype=torch.float32, device=self.device)
+        self._packs = self.lw.pack_descs()
+        self.repack()
+        self.plans: Dict[int, Plan] = {}
+
+    # -- parameters -----------------------------------------------------------
+    def repack(self, stream=None) -> None:
+        L.check(L.lib().pcnn_pack(ctypes.c_void_p(self.master.data_ptr()),
+                                  ctypes.c_void_p(self.packed.data_ptr()),
+                                  self._packs, len(self.lw.pack_ops), _stream_handle(stream)), "pcnn_pack")
+
+    def master_numpy(self) -> np.ndarray:
+        return self.master.cpu().numpy()
+
+    def to_graph(self, vector_keys=(), scalar_keys=None) -> ModelGraph:
+        return graph_from_master(self.lw, self.master_numpy(), vector_keys, scalar_keys)
+
+    # -- forward ----------------------------------------------------------------
+    def plan(self, batch: int) -> Plan:
+        p = self.plans.get(batch)
+        if p is None:
+            p = self.plans[batch] = Plan(self, batch, self.impl)
+        return p
+
+    def out_shape(self, batch: int) -> Tuple[int, ...]:
+        return (batch,) + tuple(self.lw.out_shape)
+
+    def forward(self, x, out=None, use_graph: bool = True, stream=None):
+        """x: (B, C, H, W) float32 CUDA tensor -> (B, K) float32 CUDA tensor."""
+        torch = _torch()
+        if x.dtype != torch.float32 or not x.is_cuda:
+            raise GraphError("forward expects a float32 CUDA tensor; use forward_host for host data")
+        x = x.contiguous()
+        b = x.shape[0]
+        want = tuple(self.lw.shapes[self.lw.graph.input_id()])
+        if tuple(x.shape[1:]) != want:
+            raise GraphError(f"input shape {tuple(x.shape[1:])} != graph input {want}")
+        if out is None:
+            out = torch.empty(self.out_shape(b), dtype=torch.float32, device=self.device)
+        p = self.plan(b)
+        L.check(L.lib().pcnn_forward(p.handle, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                     _stream_handle(stream), int(use_graph)), "pcnn_forward")
+        return out
+
+    def forward_host(self, x_host: np.ndarray, x_dev=None, out_dev=None, out_host=None, stream=None):
+        """Host in, host out: H2D copy, forward, D2H copy inside libpcnn."""
+        torch = _torch()
+        b = x_host.shape[0]
+        if x_dev is None:
+            x_dev = torch.empty(x_host.shape, dtype=torch.float32, device=self.device)
+        if out_dev is None:
+            out_dev = torch.empty(self.out_shape(b), dtype=torch.float32, device=self.device)
+        if out_host is None:
+            out_host = np.empty(self.out_shape(b), dtype=np.float32)
+        xh = np.ascontiguousarray(x_host, dtype=np.float32)
+        p = self.plan(b)
+        L.check(L.lib().pcnn_forward_host(p.handle, xh.ctypes.data_as(ctypes.c_void_p),
+                                          out_host.ctypes.data_as(ctypes.c_void_p),
+                                          ctypes.c_void_p(x_dev.data_ptr()), ctypes.c_void_p(out_dev.data_ptr()),
+                                          _stream_handle(stream)), "pcnn_forward_host")
+        (stream or torch.cuda.current_stream()).synchronize()
+        return out_host
+
+    def forward_unit(self, batch: int, i: int, x, out, stream=None) -> None:
+        p = self.plan(batch)
+        L.check(L.lib().pcnn_forward_unit(p.handle, i, ctypes.c_void_p(x.data_ptr()),
+                                          ctypes.c_void_p(out.data_ptr()), _stream_handle(stream)),
+                "pcnn_forward_unit")
+
+
+def forward(g: ModelGraph, x, **kw):
+    """Batched GPU forward of a graph: numpy or torch (B, C, H, W) -> same kind (B, K)."""
+    torch = _torch()
+    eng = Engine(g, **kw)
+    if isinstance(x, np.ndarray):
+        xt = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(eng.device)
+        return eng.forward(xt).cpu().numpy().astype(np.float64)
+    return eng.forward(x)
+
+
+def reference_eval(g: ModelGraph, image) -> np.ndarray:
+    """Drop-in for levnet.graph.reference_eval (graph.py:413-426): one image
+    (C, H, W) -> logits, computed by the B200 kernels (float32 compute,
+    returned as float64 like the reference)."""
+    shapes = g.validate()
+    image = np.asarray(image, dtype=np.float64)
+    if image.shape != shapes[g.input_id()]:
+        raise GraphError(f"input shape {image.shape} != graph input {shapes[g.input_id()]}")
+    return forward(g, image[None])[0]

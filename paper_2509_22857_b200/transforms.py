@@ -1,0 +1,1081 @@
+"""Weight redistribution on the GPU, with the reference's transform API.
+
+Same public surface as ``levnet.transforms`` (reference transforms.py):
+``redistribute_forward`` / ``redistribute_backward`` (per donor, :423-485),
+``redistribute_pass`` (channelwise, :575-705), ``apply_pipeline`` (:712-742),
+``check_equivalence`` (:753-778), the fusion rules (:62-277) and the
+``TransformError`` / ``UpdateTerm`` / ``PassReport`` / ``EquivReport`` types.
+
+How the work is split:
+
+* host (this module): graph walks that decide *which* tensors a rewrite
+  touches -- receiver discovery through pools (transforms.py:321-371), the
+  structural part of the channelwise solver (which conv scale is free,
+  pinned or solved at each join, transforms.py:515-572) -- compiled into a
+  straight-line **scale program** plus one **rewrite descriptor** per
+  parameter tensor;
+* device (``pcnn_redistribute``, one cooperative kernel): every numeric step
+  -- update terms upsilon (c_d, its d-th root, pool divisors), their
+  powers, the per-channel scale solve, the refusal checks on values, and the
+  rescaling of every weight, bias and coefficient in float64.
+
+Refusals keep the reference's wording.  Structural ones are raised on the
+host before launch; value-dependent ones (negative even-degree leading
+coefficient, per-channel leading coefficients, zero update term, sign
+conflicts, non-square joins) are checked on the device and re-raised here.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Dict, List, NamedTuple, Optional, Sequence, Tuple, Union
+
+import numpy as np
+
+from . import _lib as L
+from .graph import (AddNode, AvgPoolNode, BatchNormNode, BiPoolNode, ConvNode, FlattenNode,
+                    InputNode, LinearNode, LocalPoolNode, ModelGraph, Node, OutputNode,
+                    PolyActNode, PolySkipNode, PS_KEYS)
+from .lowering import Lowered, graph_from_master
+
+PIPELINES = ("P4", "P2", "P2F", "P2R", "P2FR")
+
+
+class TransformError(Exception):
+    pass
+
+
+@dataclass(frozen=True)
+class UpdateTerm:
+    """Scalar factor moved between a donor and its receivers (transforms.py:36-47)."""
+    upsilon: float
+    direction: str
+    donor: str
+
+    def __post_init__(self):
+        if self.upsilon == 0:
+            raise TransformError("update term must be nonzero")
+        if self.direction not in ("forward", "backward"):
+            raise TransformError(f"bad update direction {self.direction!r}")
+
+
+@dataclass
+class PassReport:
+    rewrites: List[Tuple[str, Tuple[str, ...]]]
+    nodes_removed: int
+    depth_before: int
+    depth_after: int
+
+
+@dataclass
+class EquivReport:
+    n_inputs: int
+    max_rel_err: float
+    argmax_match_rate: float
+    passed: bool
+
+
+# ---------------------------------------------------------------------------
+# receiver discovery (host; transforms.py:284, :321-371)
+# ---------------------------------------------------------------------------
+
+RECEIVERS = (ConvNode, LinearNode, PolyActNode, PolySkipNode, BatchNormNode, BiPoolNode)
+PASS_THROUGH = (AvgPoolNode, LocalPoolNode, FlattenNode)
+DONORS = (PolyActNode, PolySkipNode, AvgPoolNode, LocalPoolNode, BiPoolNode)
+
+
+def forward_targets(g: ModelGraph, donor: str) -> List[Tuple[str, int]]:
+    out: List[Tuple[str, int]] = []
+    queue = list(g.consumer_edges(donor))
+    if not queue:
+        raise TransformError(f"donor {donor!r} has no consumers")
+    while queue:
+        nid, pos = queue.pop(0)
+        node = g.nodes[nid]
+        if isinstance(node, RECEIVERS):
+            out.append((nid, pos))
+        elif isinstance(node, PASS_THROUGH):
+            more = g.consumer_edges(nid)
+            if not more:
+                raise TransformError(f"path through pool {nid!r} reaches no receiver")
+            queue.extend(more)
+        else:
+            raise TransformError(f"no eligible receiver on the path through {nid!r} ({node.kind})")
+    return out
+
+
+def backward_targets(g: ModelGraph, donor: str, branch: Optional[int]) -> List[str]:
+    preds = g.inputs_of(donor)
+    if branch is not None:
+        if len(set(preds)) != len(preds):
+            raise TransformError(f"donor {donor!r} takes the same node on both branches")
+        preds = [preds[branch]]
+    found: List[str] = []
+    walked: List[str] = []
+    queue = list(preds)
+    while queue:
+        nid = queue.pop(0)
+        node = g.nodes[nid]
+        if isinstance(node, RECEIVERS):
+            found.append(nid)
+        elif isinstance(node, PASS_THROUGH):
+            walked.append(nid)
+            queue.extend(g.inputs_of(nid))
+        else:
+            raise TransformError(f"no eligible receiver upstream through {nid!r} ({node.kind})")
+    scope = set(found) | set(walked) | {donor}
+    for nid in found + walked:
+        for c, _ in g.consumer_edges(nid):
+            if c not in scope:
+                raise TransformError(f"{nid!r} also feeds {c!r}; scaling it would change that path")
+    return found
+
+
+# ---------------------------------------------------------------------------
+# scale programs
+# ---------------------------------------------------------------------------
+
+class Vec(NamedTuple):
+    """An arena vector: slot offset, valid length n, allocated length."""
+    slot: int
+    n: int
+    alloc: int
+
+    @property
+    def stride(self) -> int:
+        return 0 if self.alloc == 1 else 1
+
+
+# index specs for rewrite factors: (d1, m1, s1, d2, m2)
+SCALAR = (1, 1, 0, 1, 1)
+
+
+def vec_spec(cpad: int):
+    return (1, cpad, 1, 1, 1)
+
+
+class Program:
+    """Straight-line float64 program + per-tensor factor chains for one
+    pcnn_redistribute launch over an Engine's master layout."""
+
+    def __init__(self, lw: Lowered):
+        self.lw = lw
+        self.ops: List[L.ScaleOp] = []
+        self.arena = 0
+        self.errors: List[str] = []
+        self.nflags = 0
+        self.chain: Dict[int, List[Tuple]] = {}
+        self.n_of: Dict[int, int] = {}
+        self.consts: Dict[int, Tuple[int, float]] = {}
+        self.from_arena: Dict[int, Tuple[int, Vec]] = {}
+        self.flag_names: List[str] = []
+
+    # -- raw ops ---------------------------------------------------------------
+    def _op(self, op, n, dst=0, a=0, b=0, sa=1, sb=1, p=0, err=0, imm=0.0, rtol=0.0, atol=0.0):
+        self.ops.append(L.ScaleOp(op=op, n=n, dst=dst, a=a, b=b, sa=sa, sb=sb, p=p, err=err,
+                                  imm=imm, rtol=rtol, atol=atol))
+
+    def alloc(self, n: int, alloc: Optional[int] = None) -> Vec:
+        alloc = alloc or n
+        slot = self.arena
+        self.arena += alloc
+        self._op(L.OP_FILL, alloc, dst=slot, imm=1.0)
+        return Vec(slot, n, alloc)
+
+    def err(self, msg: str) -> int:
+        self.errors.append(msg)
+        return len(self.errors)
+
+    # -- vector algebra (result length = max of operands) ----------------------
+    def fill(self, value: float, n: int = 1, alloc: Optional[int] = None) -> Vec:
+        v = self.alloc(n, alloc)
+        self._op(L.OP_FILL, n, dst=v.slot, imm=float(value))
+        return v
+
+    def load(self, off: int, n: int, alloc: Optional[int] = None) -> Vec:
+        v = self.alloc(n, alloc)
+        self._op(L.OP_LOAD, n, dst=v.slot, a=off, sa=1)
+        return v
+
+    def _bin(self, op, a: Vec, b: Vec) -> Vec:
+        n = max(a.n, b.n)
+        out = self.alloc(n, max(a.alloc, b.alloc))
+        self._op(op, n, dst=out.slot, a=a.slot, b=b.slot, sa=a.stride, sb=b.stride)
+        return out
+
+    def mul(self, a, b):
+        return self._bin(L.OP_MUL, a, b)
+
+    def div(self, a, b):
+        return self._bin(L.OP_DIV, a, b)
+
+    def sub(self, a, b):
+        return self._bin(L.OP_SUB, a, b)
+
+    def _un(self, op, a: Vec, p: int = 0) -> Vec:
+        out = self.alloc(a.n, a.alloc)
+        self._op(op, a.n, dst=out.slot, a=a.slot, sa=a.stride, p=p)
+        return out
+
+    def powi(self, a, p):
+        return self._un(L.OP_POWI, a, p)
+
+    def sroot(self, a, p):
+        return self._un(L.OP_SROOT, a, p)
+
+    def aroot(self, a, p):
+        return self._un(L.OP_AROOT, a, p)
+
+    def recip(self, a):
+        return self._un(L.OP_RECIP, a)
+
+    def sqrt(self, a):
+        return self._un(L.OP_SQRT, a)
+
+    def first(self, a: Vec) -> Vec:
+        return Vec(a.slot, 1, 1)
+
+    def solve(self, coeff: Vec, target: Vec, power: int, msg: str) -> Vec:
+        n = max(coeff.n, target.n)
+        out = self.alloc(n, max(coeff.alloc, target.alloc))
+        self._op(L.OP_SOLVE, n, dst=out.slot, a=coeff.slot, b=target.slot, sa=coeff.stride,
+                 sb=target.stride, p=power, err=self.err(msg))
+        return out
+
+    def check(self, op, a: Vec, msg: str, b: Optional[Vec] = None, rtol=0.0, atol=0.0) -> None:
+        n = max(a.n, b.n if b else 0)
+        self._op(op, n, a=a.slot, b=b.slot if b else 0, sa=a.stride, sb=b.stride if b else 0,
+                 err=self.err(msg), rtol=rtol, atol=atol)
+
+    def flag_allone(self, a: Vec, name: str) -> None:
+        self._op(L.OP_CHECK_ALLONE, a.n, a=a.slot, sa=a.stride, p=self.nflags)
+        self.nflags += 1
+        self.flag_names.append(name)
+
+    # -- tensor rewrites -----------------------------------------------------------
+    def factor(self, off: int, n: int, v: Vec, divide: bool, spec) -> None:
+        self.chain.setdefault(off, []).append((v.slot, int(divide)) + tuple(spec))
+        self.n_of[off] = n
+
+    def set_const(self, off: int, n: int, value: float) -> None:
+        self.consts[off] = (n, float(value))
+
+    def set_from(self, off: int, n: int, v: Vec) -> None:
+        self.from_arena[off] = (n, v)
+
+    def current(self, off: int, n: int, alloc: int) -> Vec:
+        """Value of a coefficient vector after the factors recorded so far
+        (donor updates compose in order, like sequential reference calls)."""
+        v = self.load(off, n, alloc)
+        for slot, divide, d1, m1, s1, d2, m2 in self.chain.get(off, []):
+            fv = Vec(slot, 1, 1) if s1 == 0 else Vec(slot, n, alloc)
+            v = self.div(v, fv) if divide else self.mul(v, fv)
+        return v
+
+    def rewrite_descs(self):
+        out = []
+        for off, chain in self.chain.items():
+            if off in self.consts or off in self.from_arena:
+                continue
+            if len(chain) > L.MAX_FACTORS:
+                raise TransformError(f"tensor at {off} collects {len(chain)} factors (max {L.MAX_FACTORS})")
+            d = L.RewriteDesc(dst=off, src=off, n=self.n_of[off], n_factors=len(chain))
+            for i, (slot, divide, d1, m1, s1, d2, m2) in enumerate(chain):
+                d.f[i] = L.Factor(slot=slot, divide=divide, d1=d1, m1=m1, s1=s1, d2=d2, m2=m2, reserved=0)
+            out.append(d)
+        for off, (n, value) in self.consts.items():
+            out.append(L.RewriteDesc(dst=off, src=off, n=n, set_const=1, value=value))
+        for off, (n, v) in self.from_arena.items():
+            out.append(L.RewriteDesc(dst=off, src=v.slot, n=n, src_arena=1))
+        return out
+
+
+def run_program(engine, prog: Program, stream=None) -> np.ndarray:
+    """Launch pcnn_redistribute; raise TransformError with the reference's
+    message if a device-side check failed; return the flag array."""
+    import torch
+    from .runtime import _stream_handle
+    dev = engine.device
+    arena = torch.empty(max(prog.arena, 1), dtype=torch.float64, device=dev)
+    status = torch.zeros(4, dtype=torch.int64, device=dev)
+    flags = torch.zeros(max(prog.nflags, 1), dtype=torch.int64, device=dev)
+    ops = L.array(L.ScaleOp, prog.ops)
+    rws = prog.rewrite_descs()
+    L.check(L.lib().pcnn_redistribute(ctypes.c_void_p(engine.master.data_ptr()), ctypes.c_void_p(arena.data_ptr()),
+                                      prog.arena, ops, len(prog.ops), L.array(L.RewriteDesc, rws), len(rws),
+                                      ctypes.c_void_p(status.data_ptr()), ctypes.c_void_p(flags.data_ptr()),
+                                      _stream_handle(stream)), "pcnn_redistribute")
+    st = status.cpu().numpy()
+    if st[0] != 0:
+        code = int(st[0])
+        msg = prog.errors[code - 1] if 0 < code <= len(prog.errors) else f"device status {code}"
+        raise TransformError(msg)
+    engine.repack(stream)
+    return flags.cpu().numpy()[:prog.nflags]
+
+
+# ---------------------------------------------------------------------------
+# per-donor compilation (transforms.py:296-318, :374-485)
+# ---------------------------------------------------------------------------
+
+def _coeff_offsets(lw: Lowered, nid: str) -> Tuple[List[int], int, int]:
+    """Offsets of each coefficient vector of a polynomial-like node, its cpad, C."""
+    s = lw.slots[nid]["coeffs"]
+    cp, c = s.meta["cpad"], s.meta["c"]
+    k = s.n // cp
+    return [s.offset + i * cp for i in range(k)], cp, c
+
+
+def _leading(prog: Program, g: ModelGraph, nid: str) -> Tuple[Vec, int, int]:
+    """Current leading-coefficient vector (logical channels) of a donor."""
+    lw = prog.lw
+    node = g.nodes[nid]
+    offs, cp, c = _coeff_offsets(lw, nid)
+    if isinstance(node, PolyActNode):
+        return prog.current(offs[-1], c, cp), node.degree, cp
+    if isinstance(node, PolySkipNode):
+        return prog.current(offs[PS_KEYS.index("x2")], c, cp), 2, cp
+    d = node.degree
+    return prog.current(offs[d * (d + 1)], c, cp), d, cp
+
+
+def _donor_upsilon(prog: Program, g: ModelGraph, donor: str, direction: str,
+                   allow_negative_leading: bool) -> Vec:
+    node = g.nodes[donor]
+    if isinstance(node, (AvgPoolNode, LocalPoolNode)):
+        return prog.current(prog.lw.slots[donor]["divisor"].offset, 1, 1)
+    if not isinstance(node, (PolyActNode, PolySkipNode, BiPoolNode)):
+        raise TransformError(f"donor must be a polynomial or pool node, got {node.kind!r}")
+    lead, d, _ = _leading(prog, g, donor)
+    prog.check(L.OP_CHECK_UNIFORM, lead,
+               f"donor {donor!r} has per-channel leading coefficients; "
+               "use the pipeline's channelwise scaling instead")
+    c = prog.first(lead)
+    if direction == "forward":
+        return c
+    if isinstance(node, PolySkipNode):
+        prog.check(L.OP_CHECK_NONNEG, c, f"donor {donor!r} has negative x^2 coefficient; no real root")
+        return prog.sqrt(c)
+    if d % 2 == 0:
+        if allow_negative_leading:  # EXTENSION: |c_d|^(1/d), leading coeff -> -1
+            return prog.aroot(c, d)
+        prog.check(L.OP_CHECK_NONNEG, c,
+                   f"donor {donor!r} has negative leading coefficient with even degree; no real root")
+    return prog.sroot(c, d)
+
+
+def _absorb(prog: Program, g: ModelGraph, nid: str, u: Vec, direction: str, pos: Optional[int]) -> None:
+    lw = prog.lw
+    node = g.nodes[nid]
+    sl = lw.slots[nid]
+    if isinstance(node, (ConvNode, LinearNode)):
+        w, b = sl["weight"], sl["bias"]
+        prog.factor(w.offset, w.n, u, False, SCALAR)
+        if direction == "backward":
+            prog.factor(b.offset, b.n, u, False, SCALAR)
+    elif isinstance(node, BatchNormNode):
+        s = sl["bn"]
+        cp = s.meta["cpad"]
+        prog.factor(s.offset, cp, u, False, SCALAR)              # gamma * u
+        if direction == "forward":
+            prog.factor(s.offset + 2 * cp, cp, u, True, SCALAR)  # mean / u
+        else:
+            prog.factor(s.offset + cp, cp, u, False, SCALAR)     # beta * u
+    elif isinstance(node, PolyActNode):
+        offs, cp, _ = _coeff_offsets(lw, nid)
+        for i, off in enumerate(offs):
+            if direction == "backward":
+                prog.factor(off, cp, u, False, SCALAR)
+            elif i > 0:  # u ** 0 == 1 leaves c_0 unchanged
+                prog.factor(off, cp, u if i == 1 else prog.powi(u, i), False, SCALAR)
+    elif isinstance(node, PolySkipNode):
+        offs, cp, _ = _coeff_offsets(lw, nid)
+        if direction == "backward":
+            for off in offs:
+                prog.factor(off, cp, u, False, SCALAR)
+        else:
+            powers = {"x2": 2, "xy": 1, "x": 1} if pos == 0 else {"y2": 2, "xy": 1, "y": 1}
+            for k, off in zip(PS_KEYS, offs):
+                p = powers.get(k, 0)
+                if p:
+                    prog.factor(off, cp, u if p == 1 else prog.powi(u, p), False, SCALAR)
+    elif isinstance(node, BiPoolNode):  # EXTENSION: both branches carry u
+        offs, cp, _ = _coeff_offsets(lw, nid)
+        d = node.degree
+        for i in range(d + 1):
+            for j in range(d + 1):
+                off = offs[i * (d + 1) + j]
+                if direction == "backward":
+                    prog.factor(off, cp, u, False, SCALAR)
+                elif i + j > 0:
+                    prog.factor(off, cp, u if i + j == 1 else prog.powi(u, i + j), False, SCALAR)
+    else:
+        raise TransformError(f"{nid!r} cannot absorb a {direction} update")
+
+
+def compile_forward(prog: Program, g: ModelGraph, donor: str, upsilon: Optional[float] = None,
+                    targets=None) -> None:
+    if donor not in g.nodes:
+        raise TransformError(f"no node {donor!r}")
+    node = g.nodes[donor]
+    if upsilon is not None:
+        UpdateTerm(float(upsilon), "forward", donor)
+        u = prog.fill(float(upsilon))
+    else:
+        u = _donor_upsilon(prog, g, donor, "forward", False)
+        prog.check(L.OP_CHECK_NONZERO, u, "update term must be nonzero")
+    targets = forward_targets(g, donor) if targets is None else targets
+    lw = prog.lw
+    if isinstance(node, (PolyActNode, BiPoolNode)):
+        r = prog.recip(u)  # reference multiplies by 1/u
+        offs, cp, _ = _coeff_offsets(lw, donor)
+        for off in offs:
+            prog.factor(off, cp, r, False, SCALAR)
+    elif isinstance(node, PolySkipNode):
+        offs, cp, _ = _coeff_offsets(lw, donor)
+        for off in offs:
+            prog.factor(off, cp, u, True, SCALAR)
+    else:
+        s = lw.slots[donor]["divisor"]
+        prog.factor(s.offset, 1, u, True, SCALAR)
+    for nid, pos in targets:
+        _absorb(prog, g, nid, u, "forward", pos)
+
+
+def compile_backward(prog: Program, g: ModelGraph, donor: str, upsilon: Optional[float] = None,
+                     allow_negative_leading: bool = False, targets=None) -> None:
+    if donor not in g.nodes:
+        raise TransformError(f"no node {donor!r}")
+    node = g.nodes[donor]
+    if upsilon is not None:
+        UpdateTerm(float(upsilon), "backward", donor)
+        u = prog.fill(float(upsilon))
+    else:
+        u = _donor_upsilon(prog, g, donor, "backward", allow_negative_leading)
+        prog.check(L.OP_CHECK_NONZERO, u, "update term must be nonzero")
+    if targets is None:
+        branch = 0 if isinstance(node, PolySkipNode) else None
+        targets = backward_targets(g, donor, branch)
+    lw = prog.lw
+    if isinstance(node, PolyActNode):
+        offs, cp, _ = _coeff_offsets(lw, donor)
+        for i, off in enumerate(offs):
+            if i:
+                prog.factor(off, cp, prog.powi(u, -i), False, SCALAR)
+    elif isinstance(node, PolySkipNode):
+        offs, cp, _ = _coeff_offsets(lw, donor)
+        for k, p in (("x2", -2), ("xy", -1), ("x", -1)):
+            prog.factor(offs[PS_KEYS.index(k)], cp, prog.powi(u, p), False, SCALAR)
+    elif isinstance(node, BiPoolNode):
+        offs, cp, _ = _coeff_offsets(lw, donor)
+        d = node.degree
+        for i in range(d + 1):
+            for j in range(d + 1):
+                if i + j:
+                    prog.factor(offs[i * (d + 1) + j], cp, prog.powi(u, -(i + j)), False, SCALAR)
+    elif isinstance(node, (AvgPoolNode, LocalPoolNode)):
+        s = lw.slots[donor]["divisor"]
+        prog.factor(s.offset, 1, u, True, SCALAR)
+    else:
+        raise TransformError(f"donor must be a polynomial or pool node, got {node.kind!r}")
+    for nid in targets:
+        _absorb(prog, g, nid, u, "backward", None)
+
+
+# ---------------------------------------------------------------------------
+# channelwise pass (transforms.py:492-705)
+# ---------------------------------------------------------------------------
+
+class _Pending(NamedTuple):
+    conv: str
+    coeff: Vec
+    power: int
+
+
+class _Solver:
+    """Structural mirror of the reference _ScaleSolver; values live on the device."""
+
+    def __init__(self, prog: Program, g: ModelGraph, shapes):
+        self.p = prog
+        self.g = g
+        self.shapes = shapes
+        self.scale: Dict[str, Union[Vec, _Pending]] = {}
+        self.free: Dict[str, Optional[Vec]] = {}
+        self.memo: Dict[str, Vec] = {}
+
+    def cpad(self, nid):
+        from .lowering import cpad_for
+        return cpad_for(self.shapes[nid][0])
+
+    def ones(self, nid) -> Vec:
+        return self.p.fill(1.0, self.shapes[nid][0], self.cpad(nid))
+
+    def resolve(self, nid):
+        t = self.scale[nid]
+        if isinstance(t, _Pending) and self.free.get(t.conv) is not None:
+            if nid not in self.memo:
+                f = self.free[t.conv]
+                self.memo[nid] = self.p.mul(t.coeff, f if t.power == 1 else self.p.powi(f, t.power))
+            return self.memo[nid]
+        return t
+
+    def concrete(self, nid) -> Vec:
+        t = self.resolve(nid)
+        if isinstance(t, _Pending):
+            raise TransformError(f"scale of {nid!r} is unresolved")
+        return t
+
+    def pin_default(self, conv: str) -> None:
+        if self.free.get(conv) is not None:
+            return
+        g, p = self.g, self.p
+        val = self.ones(conv)
+        cons = g.consumers_of(conv)
+        if len(cons) == 1:
+            node = g.nodes[cons[0]]
+            if isinstance(node, PolyActNode):
+                offs, cp, c = _coeff_offsets(p.lw, cons[0])
+                val = p.mul(val, p.aroot(p.load(offs[-1], c, cp), node.degree))
+            elif isinstance(node, BatchNormNode):
+                val = p.mul(val, _bn_b1(p, cons[0]))
+        self.free[conv] = val
+
+    def bind(self, x: str, y: str, ratio: Vec) -> Vec:
+        tx, ty = self.resolve(x), self.resolve(y)
+        if isinstance(tx, _Pending) and isinstance(ty, _Pending):
+            if tx.conv == ty.conv:
+                raise TransformError("cannot bind two branches driven by the same free scale")
+            self.pin_default(ty.conv)
+            ty = self.resolve(y)
+        p = self.p
+        if isinstance(tx, _Pending):
+            self.free[tx.conv] = p.solve(tx.coeff, p.mul(ratio, ty), tx.power,
+                                         "channelwise scaling hit a sign conflict (even power, negative ratio)")
+            return self.concrete(x)
+        if isinstance(ty, _Pending):
+            self.free[ty.conv] = p.solve(p.mul(ty.coeff, ratio), tx, ty.power,
+                                         "channelwise scaling hit a sign conflict (even power, negative ratio)")
+            return tx
+        p.check(L.OP_CHECK_CLOSE, tx, "branch scales disagree at a join and no free scale remains",
+                b=p.mul(ratio, ty), rtol=1e-9, atol=1e-12)
+        return tx
+
+
+def _bn_b1(p: Program, nid: str) -> Vec:
+    s = p.lw.slots[nid]["bn"]
+    cp, c = s.meta["cpad"], s.meta["c"]
+    return p.div(p.load(s.offset, c, cp), p.load(s.offset + 3 * cp, c, cp))
+
+
+def compile_pass(prog: Program, g: ModelGraph):
+    """Emit the channelwise pass; returns a finisher that builds the
+    reference's ``rewrites`` list from the device flags."""
+    shapes = g.validate()
+    s = _Solver(prog, g, shapes)
+    order = g.topo_order()
+    preds = {nid: g.inputs_of(nid) for nid in g.nodes}
+    p = prog
+    lw = prog.lw
+    for nid in order:
+        node = g.nodes[nid]
+        pr = preds[nid]
+        if isinstance(node, (InputNode, LinearNode)):
+            s.scale[nid] = s.ones(nid)
+        elif isinstance(node, ConvNode):
+            cons = g.consumers_of(nid)
+            if len(cons) == 1 and isinstance(g.nodes[cons[0]], OutputNode):
+                s.scale[nid] = s.ones(nid)
+            else:
+                s.free[nid] = None
+                s.scale[nid] = _Pending(nid, s.ones(nid), 1)
+        elif isinstance(node, BatchNormNode):
+            t = s.resolve(pr[0])
+            b1 = _bn_b1(p, nid)
+            s.scale[nid] = (_Pending(t.conv, p.div(t.coeff, b1), t.power)
+                            if isinstance(t, _Pending) else p.div(t, b1))
+        elif isinstance(node, AvgPoolNode):
+            div = p.load(lw.slots[nid]["divisor"].offset, 1, 1)
+            t = s.resolve(pr[0])
+            s.scale[nid] = (_Pending(t.conv, p.div(t.coeff, div), t.power)
+                            if isinstance(t, _Pending) else p.div(t, div))
+        elif isinstance(node, PolyActNode):
+            d = node.degree
+            offs, cp, c = _coeff_offsets(lw, nid)
+            cd = p.load(offs[-1], c, cp)
+            p.check(L.OP_CHECK_NONZERO, cd, f"activation {nid!r} has a zero leading coefficient")
+            t = s.resolve(pr[0])
+            if isinstance(t, _Pending):
+                s.scale[nid] = _Pending(t.conv, p.div(p.powi(t.coeff, d), cd), t.power * d)
+            else:
+                s.scale[nid] = p.div(p.powi(t, d), cd)
+        elif isinstance(node, AddNode):
+            s.scale[nid] = s.bind(pr[0], pr[1], s.ones(nid))
+        elif isinstance(node, PolySkipNode):
+            offs, cp, c = _coeff_offsets(lw, nid)
+            dx2, dy2, dxy = (p.load(offs[PS_KEYS.index(k)], c, cp) for k in ("x2", "y2", "xy"))
+            p.check(L.OP_CHECK_NONZERO, dx2, f"join {nid!r} has degenerate quadratic coefficients")
+            p.check(L.OP_CHECK_NONZERO, dxy, f"join {nid!r} has degenerate quadratic coefficients")
+            four = p.fill(4.0)
+            p.check(L.OP_CHECK_CLOSE, p.mul(dxy, dxy),
+                    f"join {nid!r} cannot be made monic: its quadratic form is not a perfect square",
+                    b=p.mul(p.mul(four, dx2), dy2), rtol=1e-8, atol=1e-8)
+            two = p.fill(2.0)
+            tx = s.bind(pr[0], pr[1], p.div(p.mul(two, dx2), dxy))
+            s.scale[nid] = p.div(p.mul(tx, tx), dx2)
+        elif isinstance(node, OutputNode):
+            t = s.resolve(pr[0])
+            if isinstance(t, _Pending):
+                s.pin_default(t.conv)
+                t = s.concrete(pr[0])
+            p.check(L.OP_CHECK_CLOSE, t, "output scale did not land on one",
+                    b=p.fill(1.0, t.n, t.alloc), rtol=1e-5, atol=1e-8)
+            s.scale[nid] = t
+        else:
+            raise TransformError(f"cannot scale node kind {node.kind!r}")
+    for nid in order:
+        if isinstance(g.nodes[nid], ConvNode) and nid in s.free and s.free[nid] is None:
+            s.pin_default(nid)
+
+    listed: List[Tuple[str, Optional[int]]] = []
+    for nid in order:
+        node = g.nodes[nid]
+        if isinstance(node, (InputNode, OutputNode, AddNode)):
+            continue
+        tv = s.concrete(nid)
+        tu = [s.concrete(q) for q in preds[nid]]
+        sl = lw.slots.get(nid, {})
+        if isinstance(node, (ConvNode, LinearNode)):
+            idx = p.nflags
+            p.flag_allone(tv, nid)
+            for q in tu:
+                p.flag_allone(q, nid)
+            listed.append((nid, idx))
+            w, b = sl["weight"], sl["bias"]
+            if isinstance(node, ConvNode):
+                m = w.meta
+                row = (m["kp"], m["npad"], 1, 1, 1)
+                col = (m["kh"] * m["kw"] * m["cb"], m["nblk"], m["cb"], 1, m["cb"])
+            else:
+                k, n = w.meta["k"], w.meta["n"]
+                row = (n, k, 1, 1, 1)
+                col = (1, n, 1, 1, 1)
+            p.factor(w.offset, w.n, tv, False, row)
+            p.factor(w.offset, w.n, tu[0], True, col)
+            p.factor(b.offset, b.n, tv, False, vec_spec(b.n))
+        elif isinstance(node, BatchNormNode):
+            st = sl["bn"]
+            cp, c = st.meta["cpad"], st.meta["c"]
+            b1 = _bn_b1(p, nid)
+            b0 = p.sub(p.load(st.offset + cp, c, cp), p.mul(b1, p.load(st.offset + 2 * cp, c, cp)))
+            p.set_from(st.offset + cp, cp, p.mul(tv, b0))
+            p.set_const(st.offset, cp, 1.0)
+            p.set_const(st.offset + 2 * cp, cp, 0.0)
+            p.set_const(st.offset + 3 * cp, cp, 1.0)
+            listed.append((nid, None))
+        elif isinstance(node, PolyActNode):
+            offs, cp, _ = _coeff_offsets(lw, nid)
+            for i, off in enumerate(offs[:-1]):
+                p.factor(off, cp, tv, False, vec_spec(cp))
+                if i:
+                    p.factor(off, cp, tu[0] if i == 1 else p.powi(tu[0], i), True, vec_spec(cp))
+            p.set_const(offs[-1], cp, 1.0)
+            listed.append((nid, None))
+        elif isinstance(node, PolySkipNode):
+            offs, cp, _ = _coeff_offsets(lw, nid)
+            ko = dict(zip(PS_KEYS, offs))
+            p.set_const(ko["x2"], cp, 1.0)
+            p.set_const(ko["y2"], cp, 1.0)
+            p.set_const(ko["xy"], cp, 2.0)
+            for k, t in (("x", tu[0]), ("y", tu[1])):
+                p.factor(ko[k], cp, tv, False, vec_spec(cp))
+                p.factor(ko[k], cp, t, True, vec_spec(cp))
+            p.factor(ko["c"], cp, tv, False, vec_spec(cp))
+            listed.append((nid, None))
+        elif isinstance(node, AvgPoolNode):
+            p.set_const(sl["divisor"].offset, 1, 1.0)
+            listed.append((nid, None))
+
+    n_in = {nid: len(preds[nid]) for nid in g.nodes}
+
+    def finish(flags: np.ndarray):
+        rewrites = []
+        for nid, idx in listed:
+            if idx is not None:
+                k = 1 + n_in[nid]
+                if all(flags[idx:idx + k]):
+                    continue
+            rewrites.append(("channel_scale", (nid,)))
+        return rewrites
+
+    return finish
+
+
+# ---------------------------------------------------------------------------
+# graph-level API (copy semantics, like the reference)
+# ---------------------------------------------------------------------------
+
+def _engine(g: ModelGraph):
+    from .runtime import Engine
+    return Engine(g, use_tc=False)
+
+
+def redistribute_forward(g: ModelGraph, donor: str, upsilon: Optional[float] = None) -> ModelGraph:
+    """transforms.py:423-449 on the GPU: donor / upsilon, receivers * upsilon."""
+    if donor not in g.nodes:
+        raise TransformError(f"no node {donor!r}")
+    g.validate()
+    targets = forward_targets(g, donor)
+    eng = _engine(g)
+    prog = Program(eng.lw)
+    compile_forward(prog, g, donor, upsilon, targets)
+    run_program(eng, prog)
+    return eng.to_graph()
+
+
+def redistribute_backward(g: ModelGraph, donor: str, upsilon: Optional[float] = None,
+                          allow_negative_leading: bool = False) -> ModelGraph:
+    """transforms.py:452-485 on the GPU: donor c_i u^-i, upstream receivers * u."""
+    if donor not in g.nodes:
+        raise TransformError(f"no node {donor!r}")
+    g.validate()
+    if upsilon is None and not isinstance(g.nodes[donor], DONORS):
+        raise TransformError(f"donor must be a polynomial or pool node, got {g.nodes[donor].kind!r}")
+    branch = 0 if isinstance(g.nodes[donor], PolySkipNode) else None
+    targets = backward_targets(g, donor, branch)
+    eng = _engine(g)
+    prog = Program(eng.lw)
+    compile_backward(prog, g, donor, upsilon, allow_negative_leading, targets)
+    run_program(eng, prog)
+    return eng.to_graph()
+
+
+def plan_sweep(engine, g: ModelGraph, direction: str, kinds=DONORS, allow_negative_leading=False):
+    """Decide which donors a sweep applies (topological order, reference
+    refusal rules).  Structural refusals come from the host walk; value
+    refusals from device probe launches (each probe only runs phase (a)
+    checks of the remaining candidates).  Returns (accepted, refused)."""
+    refused: List[Tuple[str, str]] = []
+    cand: List[Tuple[str, object]] = []
+    for nid in g.topo_order():
+        node = g.nodes[nid]
+        if not isinstance(node, kinds):
+            continue
+        if isinstance(node, BiPoolNode) and direction == "backward":
+            refused.append((nid, "bivariate pools only donate forward in sweeps"))
+            continue
+        try:
+            if direction == "forward":
+                t = forward_targets(g, nid)
+            else:
+                t = backward_targets(g, nid, 0 if isinstance(node, PolySkipNode) else None)
+            cand.append((nid, t))
+        except TransformError as e:
+            refused.append((nid, str(e)))
+    while True:
+        prog = Program(engine.lw)
+        bad = None
+        for i, (nid, t) in enumerate(cand):
+            n_err = len(prog.errors)
+            if direction == "forward":
+                compile_forward(prog, g, nid, None, t)
+            else:
+                compile_backward(prog, g, nid, None, allow_negative_leading, t)
+            prog.errors[n_err:] = [f"{i}\x00{m}" for m in prog.errors[n_err:]]
+        probe = Program(engine.lw)
+        probe.ops, probe.arena, probe.errors = prog.ops, prog.arena, prog.errors
+        try:
+            _probe(engine, probe)
+        except TransformError as e:
+            idx, msg = str(e).split("\x00", 1)
+            bad = (int(idx), msg)
+        if bad is None:
+            return cand, refused
+        nid, _ = cand.pop(bad[0])
+        refused.append((nid, bad[1]))
+
+
+def _probe(engine, prog: Program) -> None:
+    """Run only the scale program (no rewrites) to surface value refusals."""
+    import torch
+    from .runtime import _stream_handle
+    arena = torch.empty(max(prog.arena, 1), dtype=torch.float64, device=engine.device)
+    status = torch.zeros(4, dtype=torch.int64, device=engine.device)
+    ops = L.array(L.ScaleOp, prog.ops)
+    L.check(L.lib().pcnn_redistribute(ctypes.c_void_p(engine.master.data_ptr()), ctypes.c_void_p(arena.data_ptr()),
+                                      prog.arena, ops, len(prog.ops), L.array(L.RewriteDesc, []), 0,
+                                      ctypes.c_void_p(status.data_ptr()), None, _stream_handle(None)),
+            "pcnn_redistribute")
+    st = status.cpu().numpy()
+    if st[0] != 0:
+        raise TransformError(prog.errors[int(st[0]) - 1])
+
+
+def compile_sweep(engine, g: ModelGraph, direction: str, accepted, allow_negative_leading=False) -> Program:
+    prog = Program(engine.lw)
+    for nid, t in accepted:
+        if direction == "forward":
+            compile_forward(prog, g, nid, None, t)
+        else:
+            compile_backward(prog, g, nid, None, allow_negative_leading, t)
+    return prog
+
+
+def redistribute_sweep(g: ModelGraph, direction: str, kinds=DONORS, allow_negative_leading: bool = False):
+    """EXTENSION: per-donor updates for every donor in topological order,
+    skipping the ones the reference refuses, as ONE device
+    launch.  Returns (graph, applied, refused)."""
+    g.validate()
+    eng = _engine(g)
+    accepted, refused = plan_sweep(eng, g, direction, kinds, allow_negative_leading)
+    prog = compile_sweep(eng, g, direction, accepted, allow_negative_leading)
+    run_program(eng, prog)
+    return eng.to_graph(), [n for n, _ in accepted], refused
+
+
+def redistribute_pass(g: ModelGraph):
+    """transforms.py:575-705 on the GPU: every polynomial monic, BN slopes
+    and pool divisors one, via per-channel scales folded into kernels."""
+    g.validate()
+    eng = _engine(g)
+    prog = Program(eng.lw)
+    finish = compile_pass(prog, g)
+    flags = run_program(eng, prog)
+    vec = {(nid, k) for nid, n in g.nodes.items() if isinstance(n, PolyActNode)
+           for k in [f"c{i}" for i in range(n.degree)]}
+    vec |= {(nid, k) for nid, n in g.nodes.items() if isinstance(n, PolySkipNode) for k in ("x", "y", "c")}
+    lead = {(nid, f"c{n.degree}") for nid, n in g.nodes.items() if isinstance(n, PolyActNode)}
+    lead |= {(nid, k) for nid, n in g.nodes.items() if isinstance(n, PolySkipNode) for k in ("x2", "y2", "xy")}
+    out = graph_from_master(eng.lw, eng.master_numpy(), vector_keys=vec, scalar_keys=lead)
+    return out, finish(flags)
+
+
+# ---------------------------------------------------------------------------
+# node fusing (host algebra, transforms.py:62-277)
+# ---------------------------------------------------------------------------
+
+def fuse_bn_act(bn: BatchNormNode, act: PolyActNode) -> PolyActNode:
+    """Quadratic P(B(x)) (transforms.py:62-73)."""
+    if act.degree != 2:
+        raise TransformError(f"batchnorm folds into degree-2 activations only, got degree {act.degree}")
+    s, t = bn.b1, bn.b0
+    c0, c1, c2 = (np.asarray(c, dtype=np.float64) for c in act.coeffs)
+    return PolyActNode(act.id, [t * t * c2 + t * c1 + c0, s * (2.0 * t * c2 + c1), s * s * c2])
+
+
+def fuse_bn_conv(conv: ConvNode, bn: BatchNormNode) -> ConvNode:
+    """B(C(x)) (transforms.py:76-86)."""
+    if bn.gamma.shape[0] != conv.weight.shape[0]:
+        raise TransformError(f"batchnorm width {bn.gamma.shape[0]} does not match "
+                             f"{conv.weight.shape[0]} conv output channels")
+    s, t = bn.b1, bn.b0
+    return ConvNode(conv.id, conv.weight * s[:, None, None, None], s * conv.bias + t,
+                    conv.stride, conv.padding)
+
+
+def _join_coeffs(act: PolyActNode, ax, bx, ay, by) -> Dict[str, np.ndarray]:
+    """P(ax x + bx + ay y + by) as a bivariate quadratic (transforms.py:89-101)."""
+    c0, c1, c2 = (np.asarray(c, dtype=np.float64) for c in act.coeffs)
+    k = np.asarray(bx + by, dtype=np.float64)
+    lin = 2.0 * c2 * k + c1
+    one = np.ones_like(np.asarray(ax, dtype=np.float64))
+    return {"x2": c2 * ax * ax * one, "y2": c2 * ay * ay * one, "xy": 2.0 * c2 * ax * ay * one,
+            "x": ax * lin, "y": ay * lin, "c": c2 * k * k + c1 * k + c0}
+
+
+def fuse_skip_bn_bn(bnX: BatchNormNode, bnY: BatchNormNode, act: PolyActNode) -> PolySkipNode:
+    if act.degree != 2:
+        raise TransformError(f"skip fusion needs a degree-2 activation, got degree {act.degree}")
+    return PolySkipNode(act.id, _join_coeffs(act, bnX.b1, bnX.b0, bnY.b1, bnY.b0))
+
+
+def fuse_skip_identity(bnX: BatchNormNode, act: PolyActNode) -> PolySkipNode:
+    if act.degree != 2:
+        raise TransformError(f"skip fusion needs a degree-2 activation, got degree {act.degree}")
+    return PolySkipNode(act.id, _join_coeffs(act, bnX.b1, bnX.b0, 1.0, 0.0))
+
+
+def _fusion_sites(g: ModelGraph):
+    """Disjoint claims: joins first, then conv folds, then activation folds."""
+    sites, claimed = [], set()
+    order = g.topo_order()
+    for nid in order:
+        if not isinstance(g.nodes[nid], AddNode):
+            continue
+        cons = g.consumers_of(nid)
+        if len(cons) != 1 or not isinstance(g.nodes[cons[0]], PolyActNode) or g.nodes[cons[0]].degree != 2:
+            continue
+        ins = g.inputs_of(nid)
+        only = [isinstance(g.nodes[q], BatchNormNode) and [c for c, _ in g.consumer_edges(q)] == [nid]
+                for q in ins]
+        if only[0] and only[1]:
+            sites.append(("fuse_skip_bn_bn", (ins[0], ins[1], nid, cons[0])))
+            claimed.update(ins)
+        elif only[0]:
+            sites.append(("fuse_skip_identity", (ins[0], nid, cons[0])))
+            claimed.add(ins[0])
+        elif only[1]:
+            sites.append(("fuse_skip_identity_y", (ins[1], nid, cons[0])))
+            claimed.add(ins[1])
+    folded = set()
+    for nid in order:
+        if isinstance(g.nodes[nid], ConvNode):
+            cons = g.consumers_of(nid)
+            if len(cons) == 1 and isinstance(g.nodes[cons[0]], BatchNormNode) and cons[0] not in claimed:
+                sites.append(("fuse_bn_conv", (nid, cons[0])))
+                folded.add(cons[0])
+    for nid in order:
+        if isinstance(g.nodes[nid], BatchNormNode) and nid not in claimed and nid not in folded:
+            cons = g.consumers_of(nid)
+            if len(cons) == 1 and isinstance(g.nodes[cons[0]], PolyActNode) and g.nodes[cons[0]].degree == 2:
+                sites.append(("fuse_bn_act", (nid, cons[0])))
+    return sites
+
+
+def _remove_edges(g: ModelGraph, pairs) -> None:
+    todo = list(pairs)
+    keep = []
+    for e in g.edges:
+        if e in todo:
+            todo.remove(e)
+        else:
+            keep.append(e)
+    g.edges = keep
+
+
+def _apply_site(g: ModelGraph, rule: str, ids) -> None:
+    if rule == "fuse_bn_conv":
+        conv_id, bn_id = ids
+        g.nodes[conv_id] = fuse_bn_conv(g.nodes[conv_id], g.nodes[bn_id])
+        _remove_edges(g, [(conv_id, bn_id)])
+        g.edges = [(conv_id if s == bn_id else s, d) for s, d in g.edges]
+        del g.nodes[bn_id]
+        return
+    if rule == "fuse_bn_act":
+        bn_id, act_id = ids
+        src = g.inputs_of(bn_id)[0]
+        g.nodes[act_id] = fuse_bn_act(g.nodes[bn_id], g.nodes[act_id])
+        _remove_edges(g, [(src, bn_id), (bn_id, act_id)])
+        del g.nodes[bn_id]
+        g.connect(src, act_id)
+        return
+    if rule == "fuse_skip_bn_bn":
+        bx, by, add_id, act_id = ids
+        ps = fuse_skip_bn_bn(g.nodes[bx], g.nodes[by], g.nodes[act_id])
+        xs, ys, gone = g.inputs_of(bx)[0], g.inputs_of(by)[0], [bx, by]
+    elif rule == "fuse_skip_identity":
+        bx, add_id, act_id = ids
+        ps = fuse_skip_identity(g.nodes[bx], g.nodes[act_id])
+        xs, ys, gone = g.inputs_of(bx)[0], [q for q in g.inputs_of(add_id) if q != bx][0], [bx]
+    elif rule == "fuse_skip_identity_y":
+        by, add_id, act_id = ids
+        b = g.nodes[by]
+        ps = PolySkipNode(act_id, _join_coeffs(g.nodes[act_id], 1.0, 0.0, b.b1, b.b0))
+        xs, ys, gone = [q for q in g.inputs_of(add_id) if q != by][0], g.inputs_of(by)[0], [by]
+    else:
+        raise TransformError(f"unknown fusion rule {rule!r}")
+    g.nodes[act_id] = ps
+    drop = [(add_id, act_id)]
+    for b in gone:
+        drop += [(g.inputs_of(b)[0], b), (b, add_id)]
+    drop += [(q, add_id) for q in g.inputs_of(add_id) if q not in gone]
+    _remove_edges(g, drop)
+    for b in gone:
+        del g.nodes[b]
+    del g.nodes[add_id]
+    g.connect(xs, act_id)
+    g.connect(ys, act_id)
+
+
+def fuse_pass(g: ModelGraph, rng: Optional[np.random.Generator] = None):
+    g = g.copy()
+    applied = []
+    while True:
+        sites = _fusion_sites(g)
+        if not sites:
+            return g, applied
+        if rng is not None:
+            rng.shuffle(sites)
+        for rule, ids in sites:
+            _apply_site(g, rule, ids)
+            applied.append((rule, ids))
+
+
+# ---------------------------------------------------------------------------
+# depth bookkeeping, pipelines, equivalence
+# ---------------------------------------------------------------------------
+
+def _mult_depth(d: int, monic: bool) -> int:
+    return (d - 1).bit_length() if monic else (2 * d - 1).bit_length()
+
+
+def _level_cost(node: Node) -> int:
+    if isinstance(node, (InputNode, OutputNode, AddNode, FlattenNode)):
+        return 0
+    if isinstance(node, (ConvNode, LinearNode)):
+        return 1
+    if isinstance(node, BatchNormNode):
+        return 0 if np.all(node.b1 == 1.0) else 1
+    if isinstance(node, (AvgPoolNode, LocalPoolNode)):
+        return 0 if np.all(np.asarray(node.divisor) == 1.0) else 1
+    if isinstance(node, PolyActNode):
+        return _mult_depth(node.degree, node.is_monic())
+    if isinstance(node, PolySkipNode):
+        return _mult_depth(2, node.is_monic())
+    if isinstance(node, BiPoolNode):
+        return _mult_depth(node.degree, node.is_monic())
+    raise TransformError(f"no level cost for node kind {node.kind!r}")
+
+
+def critical_path_levels(g: ModelGraph) -> int:
+    """Longest input-to-output path by level cost (reference levels.py:76-84)."""
+    dist: Dict[str, int] = {}
+    preds = {nid: g.inputs_of(nid) for nid in g.nodes}
+    for nid in g.topo_order():
+        dist[nid] = max((dist[q] for q in preds[nid]), default=0) + _level_cost(g.nodes[nid])
+    return dist[g.output_id()]
+
+
+def apply_pipeline(g: ModelGraph, strategy: str) -> Tuple[ModelGraph, PassReport]:
+    """transforms.py:712-742: P2F fuses, P2R runs the channelwise pass (on the GPU)."""
+    name = strategy.upper()
+    if name not in PIPELINES:
+        raise TransformError(f"unknown strategy {strategy!r} (have {PIPELINES})")
+    g.validate()
+    want = 4 if name == "P4" else 2
+    for node in g.nodes.values():
+        if isinstance(node, PolyActNode) and node.degree != want:
+            raise TransformError(f"{name} expects degree-{want} activations, "
+                                 f"{node.id!r} has degree {node.degree}")
+    before = critical_path_levels(g)
+    out = g.copy()
+    rewrites: List[Tuple[str, Tuple[str, ...]]] = []
+    if name in ("P2F", "P2FR"):
+        out, rw = fuse_pass(out)
+        rewrites.extend(rw)
+    if name in ("P2R", "P2FR"):
+        out, rw = redistribute_pass(out)
+        rewrites.extend(rw)
+    out.validate()
+    return out, PassReport(rewrites, len(g.nodes) - len(out.nodes), before, critical_path_levels(out))
+
+
+def check_equivalence(ref: ModelGraph, candidate: ModelGraph, n_inputs: int = 100,
+                      rtol: float = 1e-8, seed: int = 0) -> EquivReport:
+    """transforms.py:753-778 with both forwards batched on the GPU (float32
+    compute, so use rtol around 1e-4 rather than the reference's float64 1e-8).
+    Inputs are the same U(-1, 1) draws from default_rng(seed)."""
+    from .runtime import Engine
+    import torch
+    shapes = ref.validate()
+    candidate.validate()
+    in_shape = shapes[ref.input_id()]
+    rng = np.random.default_rng(seed)
+    xs = np.stack([rng.uniform(-1.0, 1.0, in_shape) for _ in range(n_inputs)])
+    xt = torch.from_numpy(xs.astype(np.float32)).cuda()
+    a = Engine(ref).forward(xt).double().cpu().numpy().reshape(n_inputs, -1)
+    b = Engine(candidate).forward(xt).double().cpu().numpy().reshape(n_inputs, -1)
+    err = np.max(np.abs(a - b), axis=1) / np.maximum(np.max(np.abs(a), axis=1), 1e-12)
+    worst = float(err.max())
+    match = float(np.mean(np.argmax(a, axis=1) == np.argmax(b, axis=1)))
+    return EquivReport(n_inputs, worst, match, worst <= rtol)
