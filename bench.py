@@ -1,0 +1,483 @@
+"""Benchmark: images/s of the redistributed poly-CNN forward on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config resnet20] [--impl ours|reference]
+
+One step = one fused forward of the redistributed network over one batch of
+the configuration (input already resident in HBM), replayed as a CUDA graph
+by libpcnn.  L2 is flushed (256 MiB write) between timed steps; each step is
+bracketed by CUDA events on the launching stream and the per-step times are
+summed; under torchrun the max over ranks is reported ("replicas only": each
+rank runs its own batch, no collective on the data path).
+
+The JSON line also carries
+* e2e      -- the same metric through pcnn_forward_host with pinned host
+              buffers (H2D of the batch + forward + D2H of the logits timed);
+* roofline -- the conv kernel family (dominant kernels) against the
+              3xTF32-effective tensor rate and HBM bandwidth from
+              MEASURED_PEAKS.json, from per-unit CUDA-event timings;
+* cpu_baseline -- the float64 oracle (restatement of levnet's
+              reference_eval) on the host cores, bounded sample;
+* redistribution -- the device redistribution program (one launch), us/call.
+
+``--impl reference`` times the reference CPU path (the oracle port of
+reference_eval, multiprocess over host cores) on the same config and prints
+its own line; ranks > 0 exit without work.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import pathlib
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "images/sec of redistributed poly-CNN forward at 1 B200; % of roofline"
+UNIT = "images/s"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# model preparation
+# ---------------------------------------------------------------------------
+
+def build_model(name: str):
+    from paper_2509_22857_b200 import configs
+    return configs.build(name)
+
+
+def redistributed_engine(g, cfg):
+    """Apply the config's redistribution on the device; return (engine, info)."""
+    from paper_2509_22857_b200 import transforms as T
+    from paper_2509_22857_b200.runtime import Engine
+    eng = Engine(g)
+    info = []
+    cur = g
+    for direction in cfg.redistribution:
+        accepted, refused = T.plan_sweep(eng, cur, direction, allow_negative_leading=cfg.allow_negative_leading)
+        prog = T.compile_sweep(eng, cur, direction, accepted, cfg.allow_negative_leading)
+        T.run_program(eng, prog)
+        info.append({"direction": direction, "donors": len(accepted), "refused": len(refused)})
+        cur = eng.to_graph()
+    return eng, cur, info
+
+
+def time_redistribution(g, cfg, reps=20):
+    """us per launch of the (last) sweep program, run in place on a scratch engine."""
+    import torch
+    from paper_2509_22857_b200 import transforms as T
+    from paper_2509_22857_b200.runtime import Engine
+    eng = Engine(g)
+    direction = cfg.redistribution[0]
+    accepted, _ = T.plan_sweep(eng, g, direction, allow_negative_leading=cfg.allow_negative_leading)
+    prog = T.compile_sweep(eng, g, direction, accepted, cfg.allow_negative_leading)
+    saved = eng.master.clone()
+    times = []
+    for i in range(reps + 3):
+        eng.master.copy_(saved)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        T.run_program(eng, prog)  # includes the status read-back and the repack
+        torch.cuda.synchronize()
+        if i >= 3:
+            times.append(time.perf_counter() - t0)
+    return {"us_per_call": 1e6 * float(np.median(times)), "direction": direction, "donors": len(accepted),
+            "ops": len(prog.ops), "rewrites": len(prog.rewrite_descs()),
+            "note": "wall time of pcnn_redistribute (one cooperative launch) + status read + repack"}
+
+
+# ---------------------------------------------------------------------------
+# roofline bookkeeping
+# ---------------------------------------------------------------------------
+
+def unit_cost(lw, u, batch):
+    """(algorithmic FLOPs, algorithmic bytes) of one conv unit."""
+    t_in = lw.tensors[u["in_"]]
+    t_out = lw.tensors[u["out"]]
+    cin, cout, kh, kw, s, p = u["cin"], u["cout"], u["kh"], u["kw"], u["stride"], u["pad"]
+    ho = (t_in.h + 2 * p - kh) // s + 1
+    wo = (t_in.w + 2 * p - kw) // s + 1
+    m = batch * ho * wo
+    k = cin * kh * kw
+    flops = 2.0 * m * cout * k
+    byts = 4.0 * (batch * cin * t_in.h * t_in.w + batch * t_out.c * t_out.h * t_out.w + cout * k + cout)
+    if u.get("residual", 0):
+        byts += 4.0 * batch * cout * ho * wo
+    return flops, byts
+
+
+def per_unit_times(eng, x, out, reps, flush):
+    """Eager pass, CUDA events between units on the launching stream."""
+    import torch
+    from paper_2509_22857_b200 import _lib as L
+    plan = eng.plan(x.shape[0])
+    n = plan.n_units
+    stream = torch.cuda.current_stream()
+    acc = np.zeros(n)
+    for _ in range(reps):
+        flush()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(n + 1)]
+        ev[0].record(stream)
+        for i in range(n):
+            eng.forward_unit(x.shape[0], i, x, out)
+            ev[i + 1].record(stream)
+        torch.cuda.synchronize()
+        acc += np.array([ev[i].elapsed_time(ev[i + 1]) for i in range(n)])
+    return acc / reps  # ms per unit
+
+
+def roofline(eng, batch, unit_ms):
+    hbm, bf16, bf16s, basis = peaks()
+    p_tc = bf16 / 2.0 / 3.0  # 3xTF32-effective fp32 rate (TF32 = bf16/2, three passes)
+    lw = eng.lw
+    F = B = T = Troof = 0.0
+    rows = []
+    for i, u in enumerate(lw.units):
+        if u.get("kind") != 2:
+            continue
+        f, b = unit_cost(lw, u, batch)
+        t = unit_ms[i] * 1e-3
+        F, B, T = F + f, B + b, T + t
+        tr = max(f / (p_tc * 1e12), b / (hbm * 1e9))
+        Troof += tr
+        rows.append((f, b, t, tr))
+    total = float(np.sum(unit_ms)) * 1e-3
+    bound = "tensor" if F / (p_tc * 1e12) >= B / (hbm * 1e9) else "hbm"
+    if bound == "tensor":
+        achieved, peak, unit = F / T / 1e12, p_tc, "TFLOP/s"
+    else:
+        achieved, peak, unit = B / T / 1e9, hbm, "GB/s"
+    return {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": unit,
+            "frac": round(achieved / peak, 4), "traffic": None,
+            "kernel": "conv units (fused implicit-GEMM conv + epilogue), %d launches/step" % len(rows),
+            "peak_basis": f"{basis} bf16_tflops/2/3 = 3xTF32-effective fp32 tensor rate; hbm_gbs {hbm}",
+            "roofline_time_frac": round(Troof / T, 4) if T else None,
+            "conv_share_of_step": round(T / total, 4) if total else None,
+            "algorithmic_flops_per_step": F, "algorithmic_bytes_per_step": B}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port of levnet.graph.reference_eval
+# ---------------------------------------------------------------------------
+
+_POOL_G = None
+
+
+def _worker_init(path):
+    global _POOL_G
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from paper_2509_22857_b200.graph import load_model
+    _POOL_G = load_model(path)
+
+
+def _worker_eval(x):
+    from oracle import levnet_oracle as O
+    return O.reference_eval(_POOL_G, x)
+
+
+class CpuReference:
+    """The float64 oracle over host cores: one process per core, each running
+    reference_eval on whole images (OpenBLAS single-threaded per process)."""
+
+    def __init__(self, g, procs: int | None = None):
+        import multiprocessing as mp
+        import tempfile
+        from paper_2509_22857_b200.graph import save_model
+        self.procs = procs or os.cpu_count() or 1
+        self.tmp = tempfile.TemporaryDirectory()
+        path = os.path.join(self.tmp.name, "m.json")
+        save_model(g, path)
+        env_before = os.environ.get("OPENBLAS_NUM_THREADS")
+        os.environ["OPENBLAS_NUM_THREADS"] = "1"
+        self.pool = mp.get_context("spawn").Pool(self.procs, initializer=_worker_init, initargs=(path,))
+        if env_before is None:
+            os.environ.pop("OPENBLAS_NUM_THREADS", None)
+        else:
+            os.environ["OPENBLAS_NUM_THREADS"] = env_before
+        self.i = 0
+
+    def run(self, x, budget_s: float):
+        """Evaluate rounds of `procs` images until budget_s elapses; (img/s, images, seconds)."""
+        done, t0 = 0, time.perf_counter()
+        while True:
+            chunk = [x[(self.i + j) % len(x)] for j in range(self.procs)]
+            self.pool.map(_worker_eval, chunk)
+            self.i += len(chunk)
+            done += len(chunk)
+            el = time.perf_counter() - t0
+            if el >= budget_s:
+                return done / el, done, el
+
+    def close(self):
+        self.pool.terminate()
+        self.tmp.cleanup()
+
+
+def cpu_reference(g, x, budget_s: float):
+    ref = CpuReference(g)
+    try:
+        ref.run(x[:1], 0.0)  # warm-up: imports and first touch in every worker
+        ips, done, el = ref.run(x, budget_s)
+    finally:
+        ref.close()
+    return ips, done, el, ref.procs
+
+
+# ---------------------------------------------------------------------------
+# clocks
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([v.strip() for v in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# arms
+# ---------------------------------------------------------------------------
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2509_22857_b200 import configs
+    cfg = configs.CONFIGS[args.config]
+    g = build_model(args.config)
+    x = configs.make_input(cfg, batch=min(cfg.batch, 64))
+    ref = CpuReference(g)
+    procs = ref.procs
+    budget = max(0.5, min(6.0, 150.0 / max(args.steps + args.warmup, 1)))
+    total_imgs, t = 0, 0.0
+    try:
+        for i in range(args.warmup + args.steps):
+            _, done, el = ref.run(x, budget if i >= args.warmup else 0.0)
+            if i >= args.warmup:
+                total_imgs += done
+                t += el
+    finally:
+        ref.close()
+    value = total_imgs / t
+    line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(1e3 * t / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"{args.config}_b{cfg.batch}_forward", "global_batch": cfg.batch,
+                       "note": "each step = a bounded sample of the batch's images"},
+            "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": procs, "kind": "port",
+                             "sample": f"{total_imgs} images of {args.config} over {args.steps} steps, "
+                                       f"oracle reference_eval (float64, per image, levnet graph.py:413) "
+                                       f"in {procs} processes"},
+            "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    from paper_2509_22857_b200 import configs
+    from paper_2509_22857_b200._lib import require_device
+    require_device()
+    cfg = configs.CONFIGS[args.config]
+    batch = args.batch or cfg.batch
+    g = build_model(args.config)
+    eng, gr, redist_info = redistributed_engine(g, cfg)
+    x_host = configs.make_input(cfg, batch=batch, seed=2 + rank).astype(np.float32)
+    x = torch.from_numpy(x_host).cuda()
+    out = torch.empty(eng.out_shape(batch), dtype=torch.float32, device="cuda")
+    flush_buf = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+
+    def flush():
+        flush_buf.fill_(1.0)
+
+    stream = torch.cuda.current_stream()
+    for _ in range(max(args.warmup, 3)):
+        eng.forward(x, out)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local) as clocks:
+        # keep the GPU under the same load while the sampler spins up, so the
+        # clock samples bracket the timed steps (which can be only ~ms long)
+        t_end = time.perf_counter() + 0.6
+        while time.perf_counter() < t_end:
+            flush()
+            eng.forward(x, out)
+            torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush()
+            starts[i].record(stream)
+            eng.forward(x, out)
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+        t_end = time.perf_counter() + 0.3
+        while time.perf_counter() < t_end:
+            flush()
+            eng.forward(x, out)
+            torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * batch * args.steps / (ms * 1e-3)
+
+    # e2e through the C ABI with pinned host buffers
+    xh = torch.from_numpy(x_host).pin_memory()
+    oh = torch.empty(eng.out_shape(batch), dtype=torch.float32).pin_memory()
+    xd = torch.empty_like(x)
+    od = torch.empty_like(out)
+    from paper_2509_22857_b200 import _lib as L
+    import ctypes
+    from paper_2509_22857_b200.runtime import _stream_handle
+    plan = eng.plan(batch)
+
+    def e2e_step():
+        L.check(L.lib().pcnn_forward_host(plan.handle, ctypes.c_void_p(xh.data_ptr()), ctypes.c_void_p(oh.data_ptr()),
+                                          ctypes.c_void_p(xd.data_ptr()), ctypes.c_void_p(od.data_ptr()),
+                                          _stream_handle()), "pcnn_forward_host")
+
+    for _ in range(3):
+        e2e_step()
+    torch.cuda.synchronize()
+    e_ms = 0.0
+    for i in range(args.steps):
+        flush()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        e2e_step()
+        s1.record(stream)
+        torch.cuda.synchronize()
+        e_ms += s0.elapsed_time(s1)
+    if world > 1:
+        t = torch.tensor([e_ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e_ms = float(t.item())
+    e2e_value = world * batch * args.steps / (e_ms * 1e-3)
+    # fused global pools reduce with float atomics, so repeated runs agree to rounding only
+    np.testing.assert_allclose(oh.numpy(), out.cpu().numpy(), rtol=1e-5, atol=1e-6)
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+    unit_ms = per_unit_times(eng, x, out, reps=max(3, min(args.steps, 10)), flush=flush)
+    roof = roofline(eng, batch, unit_ms)
+    launches = plan.launches()
+    line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+            "config": {"workload": f"{args.config}_b{batch}_redistributed_forward", "model": args.config,
+                       "global_batch": batch * world, "input": "x".join(map(str, cfg.input_shape)),
+                       "parallelism": f"replicas{world}", "l2": "flushed (256 MiB write) between timed steps",
+                       "redistribution": redist_info,
+                       "conv_impl": sorted({plan.unit_impl(i) for i, u in enumerate(eng.lw.units)
+                                            if u.get("kind") == 2})},
+            "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": int(xh.numel() * 4),
+                    "d2h_bytes_per_step": int(oh.numel() * 4)},
+            "gpu_launches": launches * args.steps,
+            "roofline": roof,
+            "clocks": clocks.summary(),
+            "unit_ms": [round(float(v), 4) for v in unit_ms]}
+    if not args.no_cpu and world == 1:
+        ips, done, el, procs = cpu_reference(g, configs.make_input(cfg, batch=64), args.cpu_seconds)
+        line["cpu_baseline"] = {"value": round(ips, 3), "unit": UNIT, "cores": procs, "kind": "port",
+                                "sample": f"{done} images in {el:.1f} s, float64 oracle reference_eval "
+                                          f"(restates levnet graph.py:413) in {procs} processes"}
+    if not args.no_redist_timing:
+        line["redistribution"] = time_redistribution(g, cfg)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="resnet20")
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-redist-timing", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

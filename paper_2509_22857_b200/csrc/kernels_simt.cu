@@ -91,16 +91,25 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(ConvArgs a) {
       }
     }
     __syncthreads();
-    for (int e = tid; e < BK * BM; e += 256) {
-      int kk = e / BM, mm = e - kk * BM;
-      float v = 0.f;
-      int b = pb[mm];
-      if (b >= 0) {
-        int iy = piy[mm] + kky[kk], ix = pix_[mm] + kkx[kk];
-        if (iy >= 0 && iy < in.h && ix >= 0 && ix < in.w)
-          v = __ldg(in.base + (int64_t)b * in.nblk * plane + koff[kk] + ((int64_t)piy[mm] * in.w + pix_[mm]) * in.cb);
-      }
-      As[kk][mm] = v;
+    // gather: issue every predicated load of this thread first, then store,
+    // so the loads overlap instead of serialising on memory latency
+    constexpr int PER = BK * BM / 256;
+    float gv[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int e = tid + q * 256;
+      const int kk = e / BM, mm = e - kk * BM;
+      const int b = pb[mm];
+      const int iy = piy[mm] + kky[kk], ix = pix_[mm] + kkx[kk];
+      const bool ok = b >= 0 && iy >= 0 && iy < in.h && ix >= 0 && ix < in.w;
+      const float* src = in.base + (int64_t)max(b, 0) * in.nblk * plane + koff[kk] +
+                         ((int64_t)piy[mm] * in.w + pix_[mm]) * in.cb;
+      gv[q] = ok ? __ldg(src) : 0.f;
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int e = tid + q * 256;
+      As[e / BM][e % BM] = gv[q];
     }
     for (int e = tid; e < BK * BN; e += 256) {
       int nn = e / BK, kk = e - nn * BK;
