@@ -1,0 +1,130 @@
+"""tcgen05 conv kernel (3xTF32, A from TMEM) against the float64 oracle on
+single fused conv units of every supported shape class, and against the SIMT
+kernel.  impl=2 forces the tcgen05 path (plan creation fails loudly if the
+shape is not supported)."""
+
+import numpy as np
+import pytest
+
+from helpers import chain, rel_err
+from oracle import levnet_oracle as O
+from paper_2509_22857_b200.graph import (AddNode, AvgPoolNode, BiPoolNode, ConvNode, InputNode, LinearNode,
+                                         LocalPoolNode, ModelGraph, OutputNode, PolyActNode)
+from paper_2509_22857_b200.runtime import Engine
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [
+    # cin, cout, k, stride, pad, hw, batch
+    (3, 16, 3, 1, 1, 32, 4),
+    (16, 16, 3, 1, 1, 16, 8),
+    (16, 32, 3, 2, 1, 16, 8),
+    (32, 64, 3, 1, 1, 8, 16),
+    (64, 128, 3, 1, 1, 8, 4),
+    (128, 256, 3, 2, 1, 8, 4),
+    (256, 512, 3, 1, 1, 4, 4),
+    (16, 32, 1, 2, 0, 16, 8),
+    (3, 64, 7, 2, 3, 30, 2),
+    (6, 16, 5, 1, 0, 12, 8),
+]
+
+
+def conv_graph(rng, cin, cout, k, s, p, hw, tail=(), gain=1.0):
+    """Conv (+ fused tail); gain sets the conv output std (the configs keep
+    polynomial inputs near 0.3 by calibration, see configs.py)."""
+    nodes = [InputNode("in", cin, hw, hw),
+             ConvNode("conv", rng.normal(0, gain / np.sqrt(cin * k * k), (cout, cin, k, k)),
+                      rng.normal(0, 0.1, cout), s, p)]
+    nodes += list(tail)
+    nodes.append(OutputNode("out"))
+    return chain(nodes)
+
+
+def run(g, x, impl):
+    import torch
+    eng = Engine(g, impl=impl)
+    y = eng.forward(torch.from_numpy(x.astype(np.float32)).cuda())
+    impls = {eng.plan(x.shape[0]).unit_impl(i) for i, u in enumerate(eng.lw.units) if u["kind"] == 2}
+    return y.double().cpu().numpy(), impls
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=[f"{s[0]}x{s[1]}k{s[2]}s{s[3]}h{s[5]}" for s in SHAPES])
+def test_tc_plain_conv(cuda, shape):
+    cin, cout, k, s, p, hw, batch = shape
+    rng = np.random.default_rng(hash(shape) % 2**32)
+    g = conv_graph(rng, cin, cout, k, s, p, hw)
+    x = rng.normal(0, 1, (batch, cin, hw, hw))
+    want = O.eval_batch(g, x)
+    got, impls = run(g, x, 2)
+    assert impls == {2}
+    np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-5)
+    simt, _ = run(g, x, 1)
+    # fp32-class accuracy from 3xTF32: within a small factor of plain fp32 FMA
+    assert rel_err(got, want) <= max(4 * rel_err(simt, want), 2e-6)
+
+
+def _poly(rng, c, d):
+    cs = [rng.normal(0, 0.3, c) for _ in range(d)] + [rng.uniform(0.05, 0.3, c)]
+    return PolyActNode("act", cs)
+
+
+@pytest.mark.parametrize("deg", [2, 4, 8])
+def test_tc_conv_poly(cuda, deg):
+    rng = np.random.default_rng(deg)
+    g = conv_graph(rng, 16, 32, 3, 1, 1, 16, [_poly(rng, 32, deg)], gain=0.5)
+    x = rng.normal(0, 1, (8, 16, 16, 16))
+    want = O.eval_batch(g, x)
+    got, impls = run(g, x, 2)
+    assert impls == {2}
+    np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-5)
+
+
+def test_tc_conv_pools(cuda):
+    rng = np.random.default_rng(11)
+    d = 4
+    c = rng.normal(0, 0.2, (d + 1, d + 1, 64))
+    i, j = np.indices((d + 1, d + 1))
+    c[(i + j) > d] = 0
+    for tail in ([_poly(rng, 64, 2), LocalPoolNode("pool", 2, 2, 0, np.float64(0.25))],
+                 [_poly(rng, 64, 3), BiPoolNode("pw", "w", c), BiPoolNode("ph", "h", c.copy())],
+                 [_poly(rng, 64, 3), BiPoolNode("ph", "h", c), BiPoolNode("pw", "w", c.copy())],
+                 [_poly(rng, 64, 2), AvgPoolNode("gp", 64, np.float64(1 / 64))]):
+        g = conv_graph(rng, 32, 64, 3, 1, 1, 8, tail, gain=0.3)
+        x = rng.normal(0, 1, (16, 32, 8, 8))
+        want = O.eval_batch(g, x)
+        got, impls = run(g, x, 2)
+        assert impls == {2}
+        np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-5)
+
+
+def test_tc_conv_residual(cuda):
+    rng = np.random.default_rng(12)
+    g = ModelGraph()
+    g.add(InputNode("in", 32, 8, 8))
+    g.add(ConvNode("ca", rng.normal(0, 0.1, (32, 32, 3, 3)), rng.normal(0, 0.1, 32), 1, 1))
+    g.add(PolyActNode("aa", [np.float64(0.0), np.float64(0.5), np.float64(0.2)]))
+    g.add(ConvNode("cb", rng.normal(0, 0.1, (32, 32, 3, 3)), rng.normal(0, 0.1, 32), 1, 1))
+    g.add(AddNode("j"))
+    g.add(PolyActNode("aj", [rng.normal(0, 0.1, 32), rng.normal(0.5, 0.1, 32), rng.uniform(0.05, 0.3, 32)]))
+    g.add(OutputNode("out"))
+    for s_, d_ in (("in", "ca"), ("ca", "aa"), ("aa", "cb"), ("cb", "j"), ("in", "j"), ("j", "aj"), ("aj", "out")):
+        g.connect(s_, d_)
+    g.validate()
+    x = rng.normal(0, 1, (16, 32, 8, 8))
+    want = O.eval_batch(g, x)
+    got, impls = run(g, x, 2)
+    assert impls == {2}
+    np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-5)
+
+
+def test_tc_matches_simt_on_resnet20(cuda):
+    import torch
+    from paper_2509_22857_b200 import configs
+    g = configs.build("resnet20")
+    x = configs.make_input(configs.CONFIGS["resnet20"], batch=32)
+    tc, impls = run(g, x, 0)
+    assert 2 in impls
+    simt, _ = run(g, x, 1)
+    want = O.eval_batch(g, x[:4])
+    np.testing.assert_allclose(tc[:4], want, rtol=1e-4, atol=1e-5)
+    np.testing.assert_allclose(tc, simt, rtol=1e-4, atol=1e-5)
