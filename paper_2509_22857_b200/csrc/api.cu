@@ -69,6 +69,8 @@ TensorView make_view(const pcnn_tensor_desc& t, float* ws) {
   v.cb = (int)t.cb;
   v.nblk = (int)t.nblk;
   v.is_vector = (int)t.is_vector;
+  v.cbs = 0;
+  while ((1 << v.cbs) < v.cb) ++v.cbs;
   return v;
 }
 

@@ -15,15 +15,14 @@ constexpr int kMaxBiDeg = 4;
 struct TensorView {
   float* base;
   int c, h, w, cb, nblk, is_vector;
+  int cbs;  // log2(cb); cb is a power of two
   __host__ __device__ int cpad() const { return nblk * cb; }
   // address of element (b, channel, y, x) of a spatial tensor
   __device__ __forceinline__ float* at(int b, int ch, int y, int x) const {
-    return base + ((((int64_t)b * nblk + ch / cb) * h + y) * w + x) * cb + (ch % cb);
+    return base + ((((int64_t)b * nblk + (ch >> cbs)) * h + y) * w + x) * cb + (ch & (cb - 1));
   }
-  // address of channel group starting at ch (ch % 4 == 0, group stays in a block)
-  __device__ __forceinline__ float* pix(int b, int ch, int y, int x) const {
-    return base + ((((int64_t)b * nblk + ch / cb) * h + y) * w + x) * cb + (ch & (cb - 1));
-  }
+  // address of the channel group starting at ch (the group stays in a block)
+  __device__ __forceinline__ float* pix(int b, int ch, int y, int x) const { return at(b, ch, y, x); }
 };
 
 // Output-pixel enumeration of a conv unit.  PLAIN walks (b, oy, ox);
@@ -35,20 +34,21 @@ struct PixelMap {
   int order;
   int ho, wo;  // conv output dims
   int hp, wp;  // pooled dims (WINDOW)
-  __device__ __forceinline__ void decode(int64_t m, int& b, int& oy, int& ox) const {
+  // m < 2^31 for every supported batch (checked at plan creation)
+  __device__ __forceinline__ void decode(int64_t m64, int& b, int& oy, int& ox) const {
+    const int m = (int)m64;
     if (order == kPlain) {
-      int64_t hw = (int64_t)ho * wo;
-      b = (int)(m / hw);
-      int r = (int)(m - (int64_t)b * hw);
+      const int hw = ho * wo;
+      b = m / hw;
+      const int r = m - b * hw;
       oy = r / wo;
       ox = r - oy * wo;
     } else {
-      int64_t q = m >> 2;
-      int d = (int)(m & 3);
-      int64_t hw = (int64_t)hp * wp;
-      b = (int)(q / hw);
-      int r = (int)(q - (int64_t)b * hw);
-      int py = r / wp, px = r - (r / wp) * wp;
+      const int q = m >> 2, d = m & 3;
+      const int hw = hp * wp;
+      b = q / hw;
+      const int r = q - b * hw;
+      const int py = r / wp, px = r - py * wp;
       oy = 2 * py + (d >> 1);
       ox = 2 * px + (d & 1);
     }

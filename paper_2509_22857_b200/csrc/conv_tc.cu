@@ -27,9 +27,12 @@
 //     across the four lanes that hold one window (WINDOW pixel order), the
 //     global pool reduces a warp and issues one atomic per channel.
 //
-// Warp roles (384 threads, persistent, one CTA per SM):
+// Warp roles (512 threads, persistent, one CTA per SM):
 //   warp 0: bulk-copy producer for B;  warp 1: MMA issuer;  warp 2: TMEM
-//   allocator;  warps 4-7: A converters;  warps 8-11: epilogue.
+//   allocator;  warps 4-11: A converters (two warpgroups, alternate K-blocks);
+//   warps 12-15: epilogue.
+#include <cstdlib>
+
 #include "kernels.cuh"
 #include "tc_layout.cuh"
 #include "tc_ptx.cuh"
@@ -38,10 +41,9 @@ namespace pcnn {
 
 namespace {
 
-constexpr int kThreads = 384;
+constexpr int kThreads = 512;
 constexpr int kMaxAStages = 4;   // A hi/lo stages in TMEM (64 columns each)
 constexpr int kBStages = 4;      // streamed B stages in smem
-constexpr int kBResidentMax = 160 * 1024;
 constexpr int kTileM = 128;
 constexpr int kMaxPartials = 4;
 constexpr int kAddsPerPartial = 96;  // main-accumulator MMAs per partial before splitting
@@ -60,7 +62,23 @@ struct TcParams {
   int partials;    // main partial accumulators P
   uint32_t b_stage_bytes;
   uint32_t tmem_cols;
+  int ptab_rows;   // per-channel parameter table staged in smem: bias, [affine], [poly], [join]
+  int row_aff, row_poly, row_res;
+  int concat;      // N-concatenated hi|lo B operand (NT <= 64): 2 MMAs per K step
+  int dbg;         // PCNN_TC_DEBUG bits: 1 no converter loads, 2 no MMA, 4 no epilogue math
 };
+
+// PCNN_TC_DEBUG bit 32: CTA 0 records clock64 events here (see pcnn_tc_trace)
+constexpr int kTraceLen = 1 << 16;
+__device__ unsigned long long g_trace[kTraceLen];
+__device__ unsigned int g_trace_n;
+
+__device__ __forceinline__ void trace(const TcParams& P, uint32_t tag) {
+  if ((P.dbg & 32) && blockIdx.x == 0) {
+    unsigned int i = atomicAdd(&g_trace_n, 1u);
+    if (i < kTraceLen) g_trace[i] = ((unsigned long long)tag << 48) | (clock64() & 0xFFFFFFFFFFFFull);
+  }
+}
 
 struct Smem {
   uint64_t a_full[kMaxAStages], a_empty[kMaxAStages];
@@ -69,30 +87,54 @@ struct Smem {
   uint32_t tmem_base;
 };
 
+// x = hi + lo with hi, lo representable in tf32 (low 13 mantissa bits zero),
+// both rounded to nearest (ties away) by an integer add on the bit pattern --
+// 5 instructions; cvt.rna.tf32.f32 is emulated on sm_100 and cost ~8x more.
+// |x - hi - lo| <= 2^-22 |x| for finite x.
 __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
-  hi = f32_to_tf32(x);
-  lo = f32_to_tf32(x - __uint_as_float(hi));
+  hi = (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;
+  lo = (__float_as_uint(x - __uint_as_float(hi)) + 0x1000u) & 0xFFFFE000u;
 }
 
 // ---- converter: im2col row of one pixel -> tf32 hi/lo in TMEM -------------------
-__device__ __forceinline__ void convert_kblock(const TcParams& P, int kb, int b, int iy0, int ix0, bool valid,
-                                               uint32_t t_hi, uint32_t t_lo) {
+// seg[s] (shared): channel segment s of the K axis = cb consecutive channels
+// of one (channel block, ky, kx); .x = float offset relative to the pixel's
+// (iy0, ix0) origin, .y = ky | kx << 8 (ky = 31 marks K padding).
+struct PixelRow {
+  const float* base;  // &in[b][0][iy0][ix0][0] (may point outside; only read when valid)
+  uint32_t ymask, xmask;
+};
+
+__device__ __forceinline__ PixelRow pixel_row(const TcParams& P, int b, int oy, int ox, bool valid) {
   const ConvArgs& a = P.a;
   const TensorView& in = a.in;
-  const int cb = in.cb;
-  float4 f[8];
-  // issue all eight 16-byte loads of the K-block before using any of them
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int k = kb * kTcBK + q * 4;
-    const int seg = k / cb, ci = k - seg * cb;
-    const int blk = seg / P.taps, tap = seg - blk * P.taps;
-    const int ky = tap / a.kw, kx = tap - ky * a.kw;
-    const int iy = iy0 + ky, ix = ix0 + kx;
-    const bool ok = valid && seg < P.nseg && iy >= 0 && iy < in.h && ix >= 0 && ix < in.w;
-    const float* src = in.base + ((((int64_t)b * in.nblk + blk) * in.h + iy) * in.w + ix) * cb + ci;
-    f[q] = ok ? __ldg(reinterpret_cast<const float4*>(src)) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const int iy0 = oy * a.stride - a.pad, ix0 = ox * a.stride - a.pad;
+  PixelRow r;
+  r.base = in.base + (((int64_t)b * in.nblk * in.h + iy0) * in.w + ix0) * in.cb;
+  r.ymask = r.xmask = 0;
+  if (valid) {
+    for (int k = 0; k < a.kh; ++k) r.ymask |= (uint32_t)(iy0 + k >= 0 && iy0 + k < in.h) << k;
+    for (int k = 0; k < a.kw; ++k) r.xmask |= (uint32_t)(ix0 + k >= 0 && ix0 + k < in.w) << k;
   }
+  return r;
+}
+
+template <int CBS>
+__device__ __forceinline__ void load_kblock(const int2* __restrict__ seg, int kb, const PixelRow& px, float4* f) {
+  constexpr int CB = 1 << CBS, SEGS = 32 >> CBS, PER = 8 / SEGS;  // float4 per segment
+  // eight independent 16-byte loads, all issued before any use
+#pragma unroll
+  for (int g = 0; g < SEGS; ++g) {
+    const int2 e = seg[kb * SEGS + g];
+    const bool ok = (px.ymask >> (e.y & 0xFF)) & (px.xmask >> (e.y >> 8)) & 1u;
+    const float4* src = reinterpret_cast<const float4*>(px.base + e.x);
+#pragma unroll
+    for (int q = 0; q < PER; ++q) f[g * PER + q] = ok ? __ldg(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  (void)CB;
+}
+
+__device__ __forceinline__ void store_kblock(const TcParams& P, const float4* f, uint32_t t_hi, uint32_t t_lo) {
 #pragma unroll
   for (int g = 0; g < 4; ++g) {
     const float v[8] = {f[2 * g].x, f[2 * g].y, f[2 * g].z, f[2 * g].w,
@@ -100,6 +142,7 @@ __device__ __forceinline__ void convert_kblock(const TcParams& P, int kb, int b,
     uint32_t hi[8], lo[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) split_tf32(v[i], hi[i], lo[i]);
+    if (P.dbg & 8) continue;
     ptx::tmem_st8(t_hi + g * 8, hi);
     ptx::tmem_st8(t_lo + g * 8, lo);
   }
@@ -109,19 +152,24 @@ __device__ __forceinline__ void store4(const EpiParams& e, int b, int ch, int y,
   *reinterpret_cast<float4*>(e.out.pix(b, ch, y, x)) = make_float4(o[0], o[1], o[2], o[3]);
 }
 
+template <int CBS>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_constant__ TcParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const ConvArgs& a = P.a;
   const uint32_t b_region = P.resident ? P.b_stage_bytes * P.nkb : P.b_stage_bytes * kBStages;
   Smem* S = reinterpret_cast<Smem*>(smem + b_region);
+  int2* seg = reinterpret_cast<int2*>(smem + b_region + ((sizeof(Smem) + 15) & ~size_t(15)));
+  float* ptab = reinterpret_cast<float*>(seg + (P.nkb << (5 - a.in.cbs)));
   const uint32_t b_base = ptx::smem_u32(smem);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total_tiles = P.m_tiles * P.n_tiles;
   const int64_t M = a.pm.count(a.batch);
   const int SA = P.a_stages, NB = P.acc_bufs, NP = P.partials;
-  const uint32_t acc_set_cols = (uint32_t)(NP + 1) * P.nt;  // P main partials + correction
+  // accumulator set: concat -> NP blocks [main_p | corr_p] of 2*NT columns;
+  // otherwise NP main partials then one correction accumulator
+  const uint32_t acc_set_cols = P.concat ? (uint32_t)NP * 2 * P.nt : (uint32_t)(NP + 1) * P.nt;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kMaxAStages; ++i) {
@@ -139,6 +187,30 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     ptx::fence_mbar_init();
   }
   if (warp == 2) ptx::tmem_alloc(ptx::smem_u32(&S->tmem_base), P.tmem_cols);
+  {
+    const TensorView& in = a.in;
+    const int nsegs = P.nkb << (5 - in.cbs);
+    for (int s2 = threadIdx.x; s2 < nsegs; s2 += kThreads) {
+      int2 e = make_int2(0, 31);
+      if (s2 < P.nseg) {
+        const int blk = s2 / P.taps, tap = s2 - blk * P.taps;
+        const int ky = tap / a.kw, kx = tap - ky * a.kw;
+        e = make_int2(((blk * in.h + ky) * in.w + kx) * in.cb, ky | (kx << 8));
+      }
+      seg[s2] = e;
+    }
+    const EpiParams& ep = a.epi;
+    const int np = ep.npad;
+    for (int i = threadIdx.x; i < P.ptab_rows * np; i += kThreads) {
+      const int r = i / np, c = i - r * np;
+      float v;
+      if (r == 0) v = ep.bias[c];
+      else if (P.row_aff >= 0 && r < P.row_aff + 2 && r >= P.row_aff) v = ep.aff[(r - P.row_aff) * np + c];
+      else if (P.row_poly >= 0 && r >= P.row_poly && r <= P.row_poly + ep.poly_deg) v = ep.poly[(r - P.row_poly) * np + c];
+      else v = ep.res[(r - P.row_res) * np + c];
+      ptab[i] = v;
+    }
+  }
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -170,111 +242,219 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       }
     }
   } else if (warp == 1) {
-    // ===== MMA issuer =====
+    // ===== MMA issuer (one thread; every per-MMA quantity is an add) =====
     if (lane == 0) {
       const uint32_t idesc = ptx::idesc_tf32(kTileM, P.nt);
-      const uint32_t lo_off = P.nt * 128;  // lo image follows the hi image
-      uint32_t it = 0, bit = 0, acc_it = 0;
-      if (P.resident) ptx::mbar_wait(ptx::smem_u32(&S->b_full[0]), 0);
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++acc_it) {
-        const uint32_t acc = NB == 2 ? (acc_it & 1) : 0;
-        const uint32_t acc_ph = (NB == 2 ? (acc_it >> 1) : acc_it) & 1;
-        ptx::mbar_wait(ptx::smem_u32(&S->acc_empty[acc]), acc_ph ^ 1);
+      const uint32_t idesc2 = ptx::idesc_tf32(kTileM, 2 * P.nt);
+      const uint32_t lo_enc = (P.nt * 128) >> 4;  // lo image offset in descriptor units
+      const uint64_t desc0 = ptx::smem_desc_sw128(b_base);
+      const uint32_t a_empty0 = ptx::smem_u32(&S->a_empty[0]), a_full0 = ptx::smem_u32(&S->a_full[0]);
+      const uint32_t b_empty0 = ptx::smem_u32(&S->b_empty[0]), b_full0 = ptx::smem_u32(&S->b_full[0]);
+      const uint32_t acc_full0 = ptx::smem_u32(&S->acc_full[0]), acc_empty0 = ptx::smem_u32(&S->acc_empty[0]);
+      const uint32_t part_cols = P.nt;
+      const bool do_mma = !(P.dbg & 2);
+      int s = 0, bs = 0;
+      uint32_t ph = 0, bph = 0;
+      uint32_t acc = 0, acc_ph = 0;
+      if (P.resident) ptx::mbar_wait(b_full0, 0);
+      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        ptx::mbar_wait(acc_empty0 + 8 * acc, acc_ph ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_set = tmem + acc * acc_set_cols;
-        const uint32_t d_corr = d_set + NP * P.nt;
-        int step = 0;
-        for (int kb = 0; kb < P.nkb; ++kb, ++it) {
-          const int s = it % SA;
-          ptx::mbar_wait(ptx::smem_u32(&S->a_full[s]), (it / SA) & 1);
-          uint32_t bsm;
-          int bs = 0;
+        const uint32_t d_corr = d_set + NP * part_cols;
+        uint32_t d_main = d_set;
+        const uint32_t d_main_end = d_set + acc_set_cols - (P.concat ? 0 : part_cols);
+        uint32_t first_corr = 0;  // accumulate flags
+        int main_seen = 0;
+        for (int kb = 0; kb < P.nkb; ++kb) {
+          trace(P, 0x400 | kb);
+          ptx::mbar_wait(a_full0 + 8 * s, ph);
+          trace(P, 0x500 | kb);
+          uint64_t dkb;
           if (P.resident) {
-            bsm = b_base + kb * P.b_stage_bytes;
+            dkb = desc0 + ((kb * P.b_stage_bytes) >> 4);
           } else {
-            bs = bit % kBStages;
-            ptx::mbar_wait(ptx::smem_u32(&S->b_full[bs]), (bit / kBStages) & 1);
-            bsm = b_base + bs * P.b_stage_bytes;
+            ptx::mbar_wait(b_full0 + 8 * bs, bph);
+            dkb = desc0 + ((bs * P.b_stage_bytes) >> 4);
           }
           ptx::tc_fence_after();
           const uint32_t a_hi = tmem + a_col0 + s * 64, a_lo = a_hi + 32;
+          if (do_mma) {
 #pragma unroll
-          for (int k4 = 0; k4 < kTcBK / 8; ++k4, ++step) {
-            const uint64_t dh = ptx::smem_desc_sw128(bsm + k4 * 32);
-            const uint64_t dl = ptx::smem_desc_sw128(bsm + lo_off + k4 * 32);
-            const int part = step % NP;
-            ptx::mma_tf32_ts(d_corr, a_lo + k4 * 8, dh, idesc, step != 0);
-            ptx::mma_tf32_ts(d_corr, a_hi + k4 * 8, dl, idesc, 1);
-            ptx::mma_tf32_ts(d_set + part * P.nt, a_hi + k4 * 8, dh, idesc, step >= NP);
+            for (int k4 = 0; k4 < kTcBK / 8; ++k4) {
+              const uint64_t dh = dkb + 2 * k4, dl = dh + lo_enc;  // +32 B per 8-deep K step
+              if (P.concat) {
+                // B rows [hi; lo] as one N = 2*NT operand: [main | corr] += A_hi * [B_hi | B_lo],
+                // then corr += A_lo * B_hi -- two MMAs per K step instead of three
+                ptx::mma_tf32_ts(d_main, a_hi + k4 * 8, dh, idesc2, main_seen >= NP);
+                ptx::mma_tf32_ts(d_main + part_cols, a_lo + k4 * 8, dh, idesc, 1);
+                d_main += 2 * part_cols;
+              } else {
+                ptx::mma_tf32_ts(d_corr, a_lo + k4 * 8, dh, idesc, first_corr);
+                ptx::mma_tf32_ts(d_corr, a_hi + k4 * 8, dl, idesc, 1);
+                ptx::mma_tf32_ts(d_main, a_hi + k4 * 8, dh, idesc, main_seen >= NP);
+                d_main += part_cols;
+              }
+              first_corr = 1;
+              ++main_seen;
+              if (d_main == d_main_end) d_main = d_set;
+            }
           }
-          ptx::mma_commit(ptx::smem_u32(&S->a_empty[s]));
+          ptx::mma_commit(a_empty0 + 8 * s);
+          trace(P, 0x600 | kb);
+          if (++s == SA) { s = 0; ph ^= 1; }
           if (!P.resident) {
-            ptx::mma_commit(ptx::smem_u32(&S->b_empty[bs]));
-            ++bit;
+            ptx::mma_commit(b_empty0 + 8 * bs);
+            if (++bs == kBStages) { bs = 0; bph ^= 1; }
           }
         }
-        ptx::mma_commit(ptx::smem_u32(&S->acc_full[acc]));
+        ptx::mma_commit(acc_full0 + 8 * acc);
+        if (NB == 2) { acc ^= 1; if (acc == 0) acc_ph ^= 1; } else { acc_ph ^= 1; }
       }
     }
-  } else if (warp >= 4 && warp < 8) {
-    // ===== A converters: thread r of the warpgroup owns accumulator row r =====
-    const int row = threadIdx.x - 128;
+  } else if (warp >= 4 && warp < 12) {
+    // ===== A converters: two warpgroups take alternate K-blocks; thread r of
+    // a warpgroup owns accumulator row r.  The next K-block's loads are issued
+    // before the current one is split and stored (software pipelining).  All
+    // bookkeeping is incremental -- no divisions in the loop. =====
+    const int cw = (warp - 4) >> 2;
+    const int row = (threadIdx.x - 128) & 127;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    uint32_t it = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-      const int m_tile = tile % P.m_tiles;
-      const int64_t m = (int64_t)m_tile * kTileM + row;
+    const int nkb = P.nkb;
+    auto px_for = [&](int tile) {
+      const int64_t m = (int64_t)(tile % P.m_tiles) * kTileM + row;
       int b = 0, oy = 0, ox = 0;
-      const bool valid = m < M;
+      const bool valid = m < M && !(P.dbg & 1);
       if (valid) a.pm.decode(m, b, oy, ox);
-      const int iy0 = oy * a.stride - a.pad, ix0 = ox * a.stride - a.pad;
-      for (int kb = 0; kb < P.nkb; ++kb, ++it) {
-        const int s = it % SA;
-        ptx::mbar_wait(ptx::smem_u32(&S->a_empty[s]), ((it / SA) & 1) ^ 1);
-        ptx::tc_fence_after();
-        const uint32_t t_hi = tmem + lane_off + a_col0 + s * 64;
-        convert_kblock(P, kb, b, iy0, ix0, valid, t_hi, t_hi + 32);
-        ptx::tmem_st_wait();
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->a_full[s]));
+      return pixel_row(P, b, oy, ox, valid);
+    };
+    // position of this warpgroup's first K-block
+    int tile = blockIdx.x, kb = cw;
+    while (kb >= nkb) { kb -= nkb; tile += gridDim.x; }
+    int s = cw, par = 1;  // stage and the parity to wait for on a_empty
+    while (s >= SA) { s -= SA; par ^= 1; }
+    PixelRow px = px_for(tile);
+    float4 fa[8];
+    if (tile < total_tiles) load_kblock<CBS>(seg, kb, px, fa);
+    while (tile < total_tiles) {
+      int tile_n = tile, kb_n = kb + 2;
+      while (kb_n >= nkb) { kb_n -= nkb; tile_n += gridDim.x; }
+      float4 fb[8];
+      if (tile_n < total_tiles) {
+        const PixelRow pxn = tile_n == tile ? px : px_for(tile_n);
+        load_kblock<CBS>(seg, kb_n, pxn, fb);
+        px = pxn;
       }
+      if (lane == 0 && warp == 4) trace(P, 0x100 | kb);
+      ptx::mbar_wait_warp(ptx::smem_u32(&S->a_empty[s]), par);
+      if (lane == 0 && warp == 4) trace(P, 0x200 | kb);
+      ptx::tc_fence_after();
+      const uint32_t t_hi = tmem + lane_off + a_col0 + s * 64;
+      store_kblock(P, fa, t_hi, t_hi + 32);
+      if (!(P.dbg & 16)) ptx::tmem_st_wait();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->a_full[s]));
+      if (lane == 0 && warp == 4) trace(P, 0x300 | kb);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) fa[q] = fb[q];
+      tile = tile_n;
+      kb = kb_n;
+      s += 2;
+      if (s >= SA) { s -= SA; par ^= 1; }
     }
-  } else if (warp >= 8) {
+  } else if (warp >= 12) {
     // ===== epilogue =====
     const EpiParams& e = a.epi;
-    const int row = threadIdx.x - 256;
+    const int row = threadIdx.x - 384;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     uint32_t acc_it = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++acc_it) {
       const int m_tile = tile % P.m_tiles, n_tile = tile / P.m_tiles;
       const uint32_t acc = NB == 2 ? (acc_it & 1) : 0;
       const uint32_t acc_ph = (NB == 2 ? (acc_it >> 1) : acc_it) & 1;
-      ptx::mbar_wait(ptx::smem_u32(&S->acc_full[acc]), acc_ph);
+      if (lane == 0 && warp == 12) trace(P, 0x700);
+      ptx::mbar_wait_warp(ptx::smem_u32(&S->acc_full[acc]), acc_ph);
+      if (lane == 0 && warp == 12) trace(P, 0x800);
       ptx::tc_fence_after();
       const int64_t m = (int64_t)m_tile * kTileM + row;
       int b = -1, oy = 0, ox = 0;
       const bool valid = m < M;
       if (valid) a.pm.decode(m, b, oy, ox);
       const uint32_t d_set = tmem + lane_off + acc * acc_set_cols;
-      for (int c0 = 0; c0 < P.nt; c0 += 16) {
+      const int np = e.npad;
+      for (int c0 = 0; c0 < ((P.dbg & 4) ? 0 : P.nt); c0 += 16) {
         float v[16], t[16];
-        ptx::tmem_ld16(d_set + NP * P.nt + c0, v);  // correction terms
-        for (int p = 0; p < NP; ++p) {
-          ptx::tmem_ld16(d_set + p * P.nt + c0, t);
+        if (P.concat) {
+          ptx::tmem_ld16(d_set + P.nt + c0, v);  // corr_0
+          for (int p = 0; p < NP; ++p) {
+            if (p) {
+              ptx::tmem_ld16(d_set + 2 * p * P.nt + P.nt + c0, t);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] += t[i];
+              for (int i = 0; i < 16; ++i) v[i] += t[i];
+            }
+            ptx::tmem_ld16(d_set + 2 * p * P.nt + c0, t);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] += t[i];
+          }
+        } else {
+          ptx::tmem_ld16(d_set + NP * P.nt + c0, v);  // correction terms
+          for (int p = 0; p < NP; ++p) {
+            ptx::tmem_ld16(d_set + p * P.nt + c0, t);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] += t[i];
+          }
         }
         const int chb = n_tile * P.nt + c0;
+        const float* pt = ptab + chb;  // per-channel parameters, shared by all rows
+        float sk[16];
+        if (e.residual) {
+          // the 16 channels are contiguous: cb >= 16 whenever npad >= 16
+          const float4* sp = reinterpret_cast<const float4*>(e.skip.at(valid ? b : 0, chb, oy, ox));
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float4 f = valid ? __ldg(sp + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+            sk[4 * q] = f.x; sk[4 * q + 1] = f.y; sk[4 * q + 2] = f.z; sk[4 * q + 3] = f.w;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] += pt[j];
+        if (P.row_aff >= 0) {
+          const float* sc = pt + P.row_aff * np;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = fmaf(v[j], sc[j], sc[np + j]);
+        }
+        if (e.residual == 1) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] += sk[j];
+        } else if (e.residual >= 2) {
+          const float* rc = pt + P.row_res * np;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float xv = e.residual == 2 ? v[j] : sk[j], yv = e.residual == 2 ? sk[j] : v[j];
+            v[j] = fmaf(rc[j] * xv, xv, fmaf(rc[np + j] * yv, yv, fmaf(rc[2 * np + j] * xv, yv,
+                   fmaf(rc[3 * np + j], xv, fmaf(rc[4 * np + j], yv, rc[5 * np + j])))));
+          }
+        }
+        if (e.poly_deg) {
+          const float* pc = pt + P.row_poly * np;
+          float h[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) h[j] = pc[e.poly_deg * np + j];
+          for (int k = e.poly_deg - 1; k >= 0; --k) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) h[j] = fmaf(h[j], v[j], pc[k * np + j]);
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = h[j];
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (!valid || chb + j >= e.cout) v[j] = 0.f;
 #pragma unroll
         for (int grp = 0; grp < 4; ++grp) {
-          float o[4];
+          float* o = v + grp * 4;
           const int ch0 = chb + grp * 4;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int ch = ch0 + j;
-            o[j] = (valid && ch < e.cout) ? epi_point(e, v[grp * 4 + j], b, oy, ox, ch) : 0.f;
-          }
           if (e.pool == PCNN_POOL_NONE) {
             if (valid) store4(e, b, ch0, oy, ox, o);
           } else if (e.pool == PCNN_POOL_GLOBAL) {
@@ -283,13 +463,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             const bool uniform = __all_sync(0xffffffffu, valid && b == b0);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              float s = o[j] * div;
+              float sum = o[j] * div;
               if (uniform) {
 #pragma unroll
-                for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-                if (lane == 0 && ch0 + j < e.cout) atomicAdd(e.out.base + (int64_t)b0 * e.npad + ch0 + j, s);
+                for (int off = 16; off; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+                if (lane == 0 && ch0 + j < e.cout) atomicAdd(e.out.base + (int64_t)b0 * e.npad + ch0 + j, sum);
               } else if (valid && ch0 + j < e.cout) {
-                atomicAdd(e.out.base + (int64_t)b * e.npad + ch0 + j, s);
+                atomicAdd(e.out.base + (int64_t)b * e.npad + ch0 + j, sum);
               }
             }
           } else {
@@ -302,11 +482,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
               q3[j] = __shfl_down_sync(0xffffffffu, o[j], 3);
             }
             if (valid && (lane & 3) == 0) {
-              float p[4];
+              float pr[4];
 #pragma unroll
               for (int j = 0; j < 4; ++j)
-                p[j] = (ch0 + j < e.cout) ? epi_pool4(e, ch0 + j, o[j], q1[j], q2[j], q3[j]) : 0.f;
-              store4(e, b, ch0, oy >> 1, ox >> 1, p);
+                pr[j] = (ch0 + j < e.cout) ? epi_pool4(e, ch0 + j, o[j], q1[j], q2[j], q3[j]) : 0.f;
+              store4(e, b, ch0, oy >> 1, ox >> 1, pr);
             }
           }
         }
@@ -314,6 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->acc_empty[acc]));
+      if (lane == 0 && warp == 12) trace(P, 0x900);
     }
   }
   __syncthreads();
@@ -323,11 +504,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   }
 }
 
+size_t smem_aux_bytes(const TcParams& P);
+
 bool make_params(const ConvArgs& a, TcParams& P) {
   const int cb = a.in.cb;
   if (!(cb == 4 || cb == 8 || cb == 16 || cb == 32)) return false;
   if (a.npad < 16 || a.npad % 16) return false;
   if (!a.tcw) return false;
+  if (a.kh > 31 || a.kw > 31 || host_pixel_count(a.pm, a.batch) >= (1ll << 31)) return false;
   P.a = a;
   P.nt = a.npad <= 128 ? a.npad : 128;
   if (a.npad % P.nt) return false;
@@ -338,16 +522,31 @@ bool make_params(const ConvArgs& a, TcParams& P) {
   P.taps = a.kh * a.kw;
   P.nseg = a.in.nblk * P.taps;
   P.b_stage_bytes = (uint32_t)(2 * P.nt * kTcBK * 4);
-  P.resident = (P.n_tiles == 1 && (int64_t)P.b_stage_bytes * P.nkb <= kBResidentMax) ? 1 : 0;
+  const EpiParams& e = a.epi;
+  int rows = 1;
+  P.row_aff = e.aff ? rows : -1;
+  rows += e.aff ? 2 : 0;
+  P.row_poly = e.poly_deg ? rows : -1;
+  rows += e.poly_deg ? e.poly_deg + 1 : 0;
+  P.row_res = e.residual >= 2 ? rows : -1;
+  rows += e.residual >= 2 ? 6 : 0;
+  P.ptab_rows = rows;
+  const size_t aux = smem_aux_bytes(P);
+  if (1024 + (size_t)P.b_stage_bytes * kBStages + aux > 227 * 1024) return false;
+  P.resident = (P.n_tiles == 1 && 1024 + (size_t)P.b_stage_bytes * P.nkb + aux <= 220 * 1024) ? 1 : 0;
   // TMEM budget (512 columns): acc_bufs x (P + 1) x NT accumulators + a_stages x 64
+  const char* dbg = getenv("PCNN_TC_DEBUG");
+  P.dbg = dbg ? atoi(dbg) : 0;
   const int ksteps = P.nkb * (kTcBK / 8);
   int want = (ksteps + kAddsPerPartial - 1) / kAddsPerPartial;
   want = want < 1 ? 1 : (want > kMaxPartials ? kMaxPartials : want);
   const int cfg[4][2] = {{2, 4}, {2, 2}, {1, 4}, {1, 2}};  // (acc_bufs, a_stages), preferred first
+  P.concat = P.nt <= 64 && !(P.dbg & 64);
   P.partials = 0;
   for (int want_p = want; want_p >= 1 && !P.partials; --want_p) {
+    const int set_cols = P.concat ? want_p * 2 * P.nt : (want_p + 1) * P.nt;
     for (auto& c : cfg) {
-      if (c[0] * (want_p + 1) * P.nt + c[1] * 64 <= 512) {
+      if (c[0] * set_cols + c[1] * 64 <= 512) {
         P.acc_bufs = c[0];
         P.a_stages = c[1];
         P.partials = want_p;
@@ -356,17 +555,35 @@ bool make_params(const ConvArgs& a, TcParams& P) {
     }
   }
   if (!P.partials) return false;
-  const uint32_t need = P.acc_bufs * (P.partials + 1) * P.nt + P.a_stages * 64;
+  const uint32_t set_cols = P.concat ? P.partials * 2 * P.nt : (P.partials + 1) * P.nt;
+  const uint32_t need = P.acc_bufs * set_cols + P.a_stages * 64;
   P.tmem_cols = need <= 128 ? 128 : (need <= 256 ? 256 : 512);
   return true;
 }
 
+size_t smem_aux_bytes(const TcParams& P) {
+  const size_t segs = (size_t)P.nkb << (5 - P.a.in.cbs);
+  return ((sizeof(Smem) + 15) & ~size_t(15)) + segs * sizeof(int2) + (size_t)P.ptab_rows * P.a.epi.npad * 4;
+}
+
 size_t smem_bytes(const TcParams& P) {
   size_t b = P.resident ? (size_t)P.b_stage_bytes * P.nkb : (size_t)P.b_stage_bytes * kBStages;
-  return 1024 + b + sizeof(Smem);
+  return 1024 + b + smem_aux_bytes(P);
 }
 
 }  // namespace
+
+// debugging aid (not part of pcnn.h): drain the CTA-0 event trace
+extern "C" int pcnn_tc_trace(unsigned long long* host, int n) {
+  unsigned int cnt = 0;
+  cudaMemcpyFromSymbol(&cnt, g_trace_n, sizeof(cnt));
+  int m = (int)(cnt < (unsigned)n ? cnt : (unsigned)n);
+  if (m > kTraceLen) m = kTraceLen;
+  cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * m);
+  unsigned int z = 0;
+  cudaMemcpyToSymbol(g_trace_n, &z, sizeof(z));
+  return m;
+}
 
 bool conv_tc_supported(const ConvArgs& a) {
   TcParams P;
@@ -383,10 +600,21 @@ void launch_conv_tc(const ConvArgs& a, cudaStream_t s) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
   const size_t smem = smem_bytes(P);
-  cudaFuncSetAttribute(conv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int tiles = P.m_tiles * P.n_tiles;
   const int grid = tiles < nsm ? tiles : nsm;
-  conv_tc_kernel<<<grid, kThreads, smem, s>>>(P);
+  switch (a.in.cbs) {
+#define PCNN_TC_LAUNCH(C)                                                                            \
+  case C:                                                                                            \
+    cudaFuncSetAttribute(conv_tc_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    conv_tc_kernel<C><<<grid, kThreads, smem, s>>>(P);                                               \
+    break;
+    PCNN_TC_LAUNCH(2)
+    PCNN_TC_LAUNCH(3)
+    PCNN_TC_LAUNCH(4)
+    PCNN_TC_LAUNCH(5)
+#undef PCNN_TC_LAUNCH
+    default: break;
+  }
 }
 
 }  // namespace pcnn

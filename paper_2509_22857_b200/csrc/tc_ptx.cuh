@@ -35,13 +35,31 @@ __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 // Bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU.
+// Polls with the non-suspending test_wait: hand-offs completed by the async
+// proxy (tcgen05.commit, bulk-copy complete_tx) are seen immediately.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t spins = 0;
-  while (!mbar_try(bar, parity)) {
-    if (++spins > (1u << 26)) __trap();
-    if (spins > 64) __nanosleep(32);
+  while (!mbar_test(bar, parity)) {
+    if (++spins > (1u << 30)) __trap();
   }
+}
+
+// One lane polls, the warp follows (keeps 31 lanes off the barrier unit).
+__device__ __forceinline__ void mbar_wait_warp(uint32_t bar, uint32_t parity) {
+  if ((threadIdx.x & 31) == 0) mbar_wait(bar, parity);
+  __syncwarp();
 }
 
 // ---- bulk copy (TMA engine, non-tensor) ----------------------------------------

@@ -1,0 +1,27 @@
+"""Timeline of the tcgen05 conv pipeline in CTA 0 (PCNN_TC_DEBUG |= 32)."""
+import ctypes, os, sys, pathlib
+sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
+import numpy as np, torch
+from paper_2509_22857_b200 import configs, _lib as L
+from paper_2509_22857_b200.runtime import Engine
+unit = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+g = configs.build("resnet20")
+eng = Engine(g)
+x = torch.from_numpy(configs.make_input(configs.CONFIGS["resnet20"]).astype(np.float32)).cuda()
+out = eng.forward(x)
+lib = L.lib()
+fn = lib.pcnn_tc_trace
+fn.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
+buf = (ctypes.c_ulonglong * 65536)()
+fn(buf, 65536)  # reset
+for i in range(unit + 1):
+    eng.forward_unit(256, i, x, out)
+torch.cuda.synchronize()
+n = fn(buf, 65536)
+ev = [(int(v) >> 48, int(v) & 0xFFFFFFFFFFFF) for v in buf[:n]]
+t0 = min(t for _, t in ev)
+names = {1: "cv_wait", 2: "cv_go", 3: "cv_done", 4: "mma_wait", 5: "mma_go", 6: "mma_done", 7: "ep_wait", 8: "ep_go", 9: "ep_done"}
+ev.sort(key=lambda e: e[1])
+for tag, t in ev[:160]:
+    print(f"{t - t0:8d} {names.get(tag >> 8, tag >> 8):9s} kb={tag & 0xff}")
+print("events", n, "span", max(t for _, t in ev) - t0)

@@ -1,0 +1,229 @@
+// Microbenchmarks of the tcgen05 pipeline primitives on B200 (sm_100a):
+// mbarrier hand-off latency, tcgen05.commit latency, MMA latency/throughput
+// (kind::tf32, A from TMEM), TMEM store throughput.  Build:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2509_22857_b200/csrc \
+//        -I include tools/ubench_tc.cu -o build/ubench_tc
+#include <cstdio>
+#include <cstdint>
+
+#include "tc_ptx.cuh"
+
+using namespace pcnn;
+
+__device__ __forceinline__ uint64_t clk() { return clock64(); }
+
+__global__ void ubench(uint64_t* out, int iters, int n_mma) {
+  __shared__ __align__(1024) uint8_t bsm[16 * 1024];
+  __shared__ uint64_t bar[4];
+  __shared__ uint32_t tbase;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 4; ++i) ptx::mbar_init(ptx::smem_u32(&bar[i]), 1);
+    ptx::fence_mbar_init();
+  }
+  for (int i = threadIdx.x; i < 16 * 1024 / 4; i += blockDim.x) reinterpret_cast<float*>(bsm)[i] = 0.f;
+  if (warp == 0) ptx::tmem_alloc(ptx::smem_u32(&tbase), 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = tbase;
+  const uint32_t b0 = ptx::smem_u32(&bar[0]), b1 = ptx::smem_u32(&bar[1]), b2 = ptx::smem_u32(&bar[2]);
+
+  // 1. ping-pong between warp 0 lane 0 and warp 1 lane 0
+  uint64_t t0 = clk();
+  if (lane == 0 && warp < 2) {
+    for (int i = 0; i < iters; ++i) {
+      if (warp == 0) {
+        ptx::mbar_arrive(b0);
+        ptx::mbar_wait(b1, i & 1);
+      } else {
+        ptx::mbar_wait(b0, i & 1);
+        ptx::mbar_arrive(b1);
+      }
+    }
+  }
+  uint64_t t1 = clk();
+  if (threadIdx.x == 0) out[0] = (t1 - t0) / iters;
+  __syncthreads();
+
+  // 2. commit latency with nothing in flight
+  if (threadIdx.x == 0) {
+    t0 = clk();
+    for (int i = 0; i < iters; ++i) {
+      ptx::mma_commit(b2);
+      ptx::mbar_wait(b2, i & 1);
+    }
+    t1 = clk();
+    out[1] = (t1 - t0) / iters;
+  }
+  __syncthreads();
+
+  // 3. MMA latency: n_mma dependent MMAs (same accumulator) + commit + wait
+  const uint32_t idesc16 = ptx::idesc_tf32(128, 16), idesc128 = ptx::idesc_tf32(128, 128);
+  const uint64_t bd = ptx::smem_desc_sw128(ptx::smem_u32(bsm));
+  if (threadIdx.x == 0) {
+    for (int cfg = 0; cfg < 2; ++cfg) {
+      const uint32_t idesc = cfg ? idesc128 : idesc16;
+      t0 = clk();
+      for (int i = 0; i < iters; ++i) {
+        for (int k = 0; k < n_mma; ++k) ptx::mma_tf32_ts(tmem, tmem + 256 + (k & 7) * 8, bd, idesc, k > 0);
+        ptx::mma_commit(b2);
+        ptx::mbar_wait(b2, (iters * (1 + cfg) + i) & 1);  // b2 phases continue from step 2
+      }
+      t1 = clk();
+      out[2 + cfg] = (t1 - t0) / iters;
+    }
+  }
+  __syncthreads();
+
+  // 3b. MMA throughput vs number of independent accumulators and N (48 MMAs)
+  if (threadIdx.x == 0) {
+    int slot = 6;
+    const int ns[4] = {16, 32, 64, 128};
+    uint32_t ph = (iters * 3) & 1;  // b2 completed 3*iters phases so far
+    for (int ni = 0; ni < 4; ++ni) {
+      const uint32_t idesc = ptx::idesc_tf32(128, ns[ni]);
+      for (int R = 1; R <= 8; R *= 2) {
+        if (R * ns[ni] > 256) { out[slot++] = 0; continue; }
+        t0 = clk();
+        for (int i = 0; i < 20; ++i) {
+          for (int k = 0; k < 48; ++k)
+            ptx::mma_tf32_ts(tmem + (k % R) * ns[ni], tmem + 256 + (k & 7) * 8, bd, idesc, k >= R);
+          ptx::mma_commit(b2);
+          ptx::mbar_wait(b2, ph);
+          ph ^= 1;
+        }
+        t1 = clk();
+        out[slot++] = (t1 - t0) / 20 / 48;
+      }
+    }
+    // SS mode (A from smem, same zero image), N=16 and 128, R=1 and 4
+    for (int ni = 0; ni < 2; ++ni) {
+      const uint32_t idesc = ptx::idesc_tf32(128, ni ? 128 : 16);
+      for (int R = 1; R <= 4; R *= 4) {
+        t0 = clk();
+        for (int i = 0; i < 20; ++i) {
+          for (int k = 0; k < 48; ++k)
+            ptx::mma_tf32_ss(tmem + (k % R) * (ni ? 64 : 16), bd, bd, idesc, k >= R);
+          ptx::mma_commit(b2);
+          ptx::mbar_wait(b2, ph);
+          ph ^= 1;
+        }
+        t1 = clk();
+        out[slot++] = (t1 - t0) / 20 / 48;
+      }
+    }
+  }
+  __syncthreads();
+
+  // 3c. N=256 and MMA throughput under concurrent TMEM store/load traffic
+  {
+    __shared__ volatile int stop;
+    if (threadIdx.x == 0) stop = 0;
+    __syncthreads();
+    uint32_t ph2 = 0;
+    for (int mode = 1; mode < 3; ++mode) {   // 0: N=256 alone, 1: N=64 + STTM traffic, 2: N=64 + LDTM traffic
+      if (threadIdx.x == 0) stop = 0;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const uint32_t idesc = ptx::idesc_tf32(128, mode == 0 ? 256 : 64);
+        t0 = clk();
+        for (int i = 0; i < 20; ++i) {
+          for (int k = 0; k < 48; ++k) ptx::mma_tf32_ts(tmem, tmem + 256 + (k & 7) * 8, bd, idesc, k > 0);
+          ptx::mma_commit(b1);
+          ptx::mbar_wait(b1, ph2);
+          ph2 ^= 1;
+        }
+        t1 = clk();
+        out[30 + mode] = (t1 - t0) / 20 / 48;
+        stop = 1;
+      } else if (warp >= 4 && mode > 0) {
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        uint32_t r[8] = {1, 2, 3, 4, 5, 6, 7, 8};
+        float v[16];
+        while (!stop) {
+          if (mode == 1) {
+            for (int g = 0; g < 8; ++g) ptx::tmem_st8(tmem + lane_off + 320 + g * 8, r);
+            ptx::tmem_st_wait();
+          } else {
+            ptx::tmem_ld16(tmem + lane_off + 384, v);
+            r[0] += __float_as_uint(v[3]);
+          }
+        }
+        if (r[0] == 12345) out[40] = 1;
+      }
+      __syncthreads();
+    }
+  }
+
+  // 4. TMEM store throughput: warps 0-3, 16 x STTM.x8 + wait::st per iteration
+  if (warp < 4) {
+    uint32_t r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    t0 = clk();
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        ptx::tmem_st8(tmem + lane_off + 256 + g * 8, r);
+        ptx::tmem_st8(tmem + lane_off + 320 + g * 8, r);
+      }
+      ptx::tmem_st_wait();
+    }
+    t1 = clk();
+    if (threadIdx.x == 0) out[4] = (t1 - t0) / iters;
+  }
+  __syncthreads();
+  // 5. TMEM load: 4 warps, ld16 x 8 (128 columns)
+  if (warp < 4) {
+    float v[16];
+    float acc = 0.f;
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    t0 = clk();
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        ptx::tmem_ld16(tmem + lane_off + g * 16, v);
+        acc += v[0];
+      }
+    }
+    t1 = clk();
+    if (threadIdx.x == 0) out[5] = (t1 - t0) / iters + (acc == 12345.f);
+  }
+  __syncthreads();
+  if (warp == 0) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
+int main() {
+  uint64_t* d;
+  cudaMalloc(&d, 64 * sizeof(uint64_t));
+  cudaMemset(d, 0, 64 * sizeof(uint64_t));
+  for (int n_mma : {1, 12, 48}) {
+    ubench<<<1, 384>>>(d, 200, n_mma);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+      printf("error %s\n", cudaGetErrorString(e));
+      return 1;
+    }
+    uint64_t h[64];
+    cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+    if (n_mma == 1) {
+      const int ns[4] = {16, 32, 64, 128};
+      for (int ni = 0; ni < 4; ++ni)
+        printf("TS N=%3d cycles/MMA with R=1,2,4,8 accumulators: %llu %llu %llu %llu\n", ns[ni],
+               (unsigned long long)h[6 + ni * 4], (unsigned long long)h[7 + ni * 4],
+               (unsigned long long)h[8 + ni * 4], (unsigned long long)h[9 + ni * 4]);
+      printf("TS N=256 alone: %llu; N=64 with STTM traffic: %llu; with LDTM traffic: %llu\n",
+             (unsigned long long)h[30], (unsigned long long)h[31], (unsigned long long)h[32]);
+      printf("SS N=16 R=1,4: %llu %llu   SS N=128 R=1,4: %llu %llu\n", (unsigned long long)h[22],
+             (unsigned long long)h[23], (unsigned long long)h[24], (unsigned long long)h[25]);
+    }
+    printf("n_mma=%d: pingpong=%llu commit_empty=%llu mma_chain_N16=%llu mma_chain_N128=%llu "
+           "sttm(32KB)+wait=%llu ldtm(4w x 128col)=%llu cycles\n",
+           n_mma, (unsigned long long)h[0], (unsigned long long)h[1], (unsigned long long)h[2],
+           (unsigned long long)h[3], (unsigned long long)h[4], (unsigned long long)h[5]);
+  }
+  return 0;
+}
