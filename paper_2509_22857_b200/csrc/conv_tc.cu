@@ -28,9 +28,11 @@
 //     global pool reduces a warp and issues one atomic per channel.
 //
 // Warp roles (512 threads, persistent, one CTA per SM):
-//   warp 0: bulk-copy producer for B;  warp 1: MMA issuer;  warp 2: TMEM
-//   allocator;  warps 4-11: A converters (two warpgroups, alternate K-blocks);
-//   warps 12-15: epilogue.
+//   warps 0-3: epilogue;  warps 4-11: A converters (staged: 4-7 only; direct:
+//   two warpgroups taking alternate K-blocks);  warp 12: TMEM allocator;
+//   warp 14: TMA / bulk-copy producer;  warp 15: MMA issuer.
+#include <cuda.h>
+
 #include <cstdlib>
 
 #include "kernels.cuh"
@@ -42,13 +44,22 @@ namespace pcnn {
 namespace {
 
 constexpr int kThreads = 512;
+// warp roles: the warp scheduler favours higher warp ids, so the single MMA
+// issuing thread gets the highest id; epilogue warps 0-3 and converter
+// warpgroups 4-7 / 8-11 each cover TMEM lanes 0-127 (warp w owns 32*(w%4)..)
+constexpr int kWarpAlloc = 12, kWarpProducer = 14, kWarpMma = 15;
 constexpr int kMaxAStages = 4;   // A hi/lo stages in TMEM (64 columns each)
 constexpr int kBStages = 4;      // streamed B stages in smem
 constexpr int kTileM = 128;
 constexpr int kMaxPartials = 4;
 constexpr int kAddsPerPartial = 96;  // main-accumulator MMAs per partial before splitting
 
+struct alignas(64) TmaMap {
+  uint64_t v[16];  // CUtensorMap (opaque 128 bytes)
+};
+
 struct TcParams {
+  TmaMap tmap;     // first member: 64-byte aligned in the param space
   ConvArgs a;
   int nt;          // N tile (UMMA N), 16..128
   int n_tiles;
@@ -65,25 +76,37 @@ struct TcParams {
   int ptab_rows;   // per-channel parameter table staged in smem: bias, [affine], [poly], [join]
   int row_aff, row_poly, row_res;
   int concat;      // N-concatenated hi|lo B operand (NT <= 64): 2 MMAs per K step
+  // TMA-staged input (staged = 1): per (tile, channel block) the input rows a
+  // tile needs are loaded as <= `pieces` 4-D boxes (one per image), zero
+  // padded by the TMA unit, and the converter reads im2col rows from smem.
+  int staged;
+  int box_w, box_h, pieces, kpc, nblk_in;
+  uint32_t piece_bytes, st_bytes;
+  int nbs;         // streamed B stages
   int dbg;         // PCNN_TC_DEBUG bits: 1 no converter loads, 2 no MMA, 4 no epilogue math
 };
 
-// PCNN_TC_DEBUG bit 32: CTA 0 records clock64 events here (see pcnn_tc_trace)
+// PCNN_TC_DEBUG bit 32: CTA 0 records clock64 events here (see pcnn_tc_trace).
+// Each role writes its own region with a private counter: plain stores, no
+// atomics, so tracing barely perturbs the pipeline.
 constexpr int kTraceLen = 1 << 16;
+constexpr int kTraceRegion = kTraceLen / 4;
 __device__ unsigned long long g_trace[kTraceLen];
 __device__ unsigned int g_trace_n;
 
-__device__ __forceinline__ void trace(const TcParams& P, uint32_t tag) {
-  if ((P.dbg & 32) && blockIdx.x == 0) {
-    unsigned int i = atomicAdd(&g_trace_n, 1u);
-    if (i < kTraceLen) g_trace[i] = ((unsigned long long)tag << 48) | (clock64() & 0xFFFFFFFFFFFFull);
+struct Tracer {
+  uint32_t n = 0;
+  __device__ __forceinline__ void operator()(const TcParams& P, int region, uint32_t tag) {
+    if ((P.dbg & 32) && blockIdx.x == 0 && n < kTraceRegion)
+      g_trace[region * kTraceRegion + n++] = ((unsigned long long)tag << 48) | (clock64() & 0xFFFFFFFFFFFFull);
   }
-}
+};
 
 struct Smem {
   uint64_t a_full[kMaxAStages], a_empty[kMaxAStages];
   uint64_t b_full[kBStages], b_empty[kBStages];
   uint64_t acc_full[2], acc_empty[2];
+  uint64_t st_full[2], st_empty[2];
   uint32_t tmem_base;
 };
 
@@ -157,14 +180,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const ConvArgs& a = P.a;
-  const uint32_t b_region = P.resident ? P.b_stage_bytes * P.nkb : P.b_stage_bytes * kBStages;
-  Smem* S = reinterpret_cast<Smem*>(smem + b_region);
-  int2* seg = reinterpret_cast<int2*>(smem + b_region + ((sizeof(Smem) + 15) & ~size_t(15)));
+  const uint32_t b_region = P.resident ? P.b_stage_bytes * P.nkb : P.b_stage_bytes * P.nbs;
+  const uint32_t st_region = P.staged ? 2 * P.st_bytes : 0;
+  uint8_t* st_buf = smem + b_region;
+  Smem* S = reinterpret_cast<Smem*>(smem + b_region + st_region);
+  int2* seg = reinterpret_cast<int2*>(smem + b_region + st_region + ((sizeof(Smem) + 15) & ~size_t(15)));
   float* ptab = reinterpret_cast<float*>(seg + (P.nkb << (5 - a.in.cbs)));
   const uint32_t b_base = ptx::smem_u32(smem);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total_tiles = P.m_tiles * P.n_tiles;
+  Tracer tr;
   const int64_t M = a.pm.count(a.batch);
   const int SA = P.a_stages, NB = P.acc_bufs, NP = P.partials;
   // accumulator set: concat -> NP blocks [main_p | corr_p] of 2*NT columns;
@@ -183,10 +209,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(ptx::smem_u32(&S->acc_full[i]), 1);
       ptx::mbar_init(ptx::smem_u32(&S->acc_empty[i]), 4);
+      ptx::mbar_init(ptx::smem_u32(&S->st_full[i]), 1);
+      ptx::mbar_init(ptx::smem_u32(&S->st_empty[i]), 4);
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 2) ptx::tmem_alloc(ptx::smem_u32(&S->tmem_base), P.tmem_cols);
+  if (warp == kWarpAlloc) ptx::tmem_alloc(ptx::smem_u32(&S->tmem_base), P.tmem_cols);
   {
     const TensorView& in = a.in;
     const int nsegs = P.nkb << (5 - in.cbs);
@@ -195,7 +223,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       if (s2 < P.nseg) {
         const int blk = s2 / P.taps, tap = s2 - blk * P.taps;
         const int ky = tap / a.kw, kx = tap - ky * a.kw;
-        e = make_int2(((blk * in.h + ky) * in.w + kx) * in.cb, ky | (kx << 8));
+        // staged: float offset inside the staged box; direct: inside the tensor
+        e = P.staged ? make_int2((ky * P.box_w + kx) * in.cb, ky | (kx << 8))
+                     : make_int2(((blk * in.h + ky) * in.w + kx) * in.cb, ky | (kx << 8));
       }
       seg[s2] = e;
     }
@@ -217,33 +247,57 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   const uint32_t tmem = S->tmem_base;
   const uint32_t a_col0 = (uint32_t)NB * acc_set_cols;
 
-  if (warp == 0) {
-    // ===== B producer =====
+  if (warp == kWarpProducer) {
+    // ===== producer: TMA input staging + B (weights) bulk copies =====
     if (lane == 0) {
+      if (P.staged) ptx::prefetch_tmap(&P.tmap);
       if (P.resident) {
         const uint32_t bar = ptx::smem_u32(&S->b_full[0]);
         ptx::mbar_arrive_tx(bar, P.b_stage_bytes * P.nkb);
         for (int kb = 0; kb < P.nkb; ++kb)
           ptx::bulk_g2s(b_base + kb * P.b_stage_bytes, a.tcw + (size_t)kb * (P.b_stage_bytes / 4),
                         P.b_stage_bytes, bar);
-      } else {
-        uint32_t it = 0;
-        for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-          const int n_tile = tile / P.m_tiles;
-          for (int kb = 0; kb < P.nkb; ++kb, ++it) {
-            const int s = it % kBStages;
-            ptx::mbar_wait(ptx::smem_u32(&S->b_empty[s]), ((it / kBStages) & 1) ^ 1);
-            const uint32_t bar = ptx::smem_u32(&S->b_full[s]);
+      }
+      int bs = 0, sb = 0;
+      uint32_t bph = 0, sph = 0;
+      const uint32_t box_bytes = (uint32_t)P.box_w * P.box_h * a.in.cb * 4;
+      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        const int n_tile = tile / P.m_tiles, m_tile = tile - n_tile * P.m_tiles;
+        int b0 = 0, oy0 = 0, ox0 = 0, b1 = 0, oy1 = 0, ox1 = 0;
+        if (P.staged) {
+          const int64_t m0 = (int64_t)m_tile * kTileM;
+          const int64_t m1 = (m0 + kTileM < M ? m0 + kTileM : M) - 1;
+          a.pm.decode(m0, b0, oy0, ox0);
+          a.pm.decode(m1, b1, oy1, ox1);
+        }
+        for (int kb = 0; kb < P.nkb; ++kb) {
+          if (P.staged && kb % P.kpc == 0) {
+            const int blk = kb / P.kpc;
+            ptx::mbar_wait_sleep(ptx::smem_u32(&S->st_empty[sb]), sph ^ 1);
+            const uint32_t bar = ptx::smem_u32(&S->st_full[sb]);
+            ptx::mbar_arrive_tx(bar, box_bytes * (uint32_t)(b1 - b0 + 1));
+            for (int bi = b0; bi <= b1; ++bi) {
+              const int lo = bi == b0 ? oy0 : 0;
+              ptx::tma_load_4d(ptx::smem_u32(st_buf + sb * P.st_bytes + (bi - b0) * P.piece_bytes), &P.tmap, 0,
+                               -a.pad, lo * a.stride - a.pad, bi * P.nblk_in + blk, bar);
+            }
+            if (++sb == 2) { sb = 0; sph ^= 1; }
+          }
+          if (!P.resident) {
+            ptx::mbar_wait_sleep(ptx::smem_u32(&S->b_empty[bs]), bph ^ 1);
+            const uint32_t bar = ptx::smem_u32(&S->b_full[bs]);
             ptx::mbar_arrive_tx(bar, P.b_stage_bytes);
             const float* src = a.tcw + ((size_t)n_tile * P.nkb + kb) * (P.b_stage_bytes / 4);
-            ptx::bulk_g2s(b_base + s * P.b_stage_bytes, src, P.b_stage_bytes, bar);
+            ptx::bulk_g2s(b_base + bs * P.b_stage_bytes, src, P.b_stage_bytes, bar);
+            if (++bs == P.nbs) { bs = 0; bph ^= 1; }
           }
         }
       }
     }
-  } else if (warp == 1) {
-    // ===== MMA issuer (one thread; every per-MMA quantity is an add) =====
-    if (lane == 0) {
+  } else if (warp == kWarpMma) {
+    // ===== MMA issuer: the whole warp runs the loop with warp-uniform state,
+    // one elected lane issues each tcgen05 instruction =====
+    {
       const uint32_t idesc = ptx::idesc_tf32(kTileM, P.nt);
       const uint32_t idesc2 = ptx::idesc_tf32(kTileM, 2 * P.nt);
       const uint32_t lo_enc = (P.nt * 128) >> 4;  // lo image offset in descriptor units
@@ -258,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       uint32_t acc = 0, acc_ph = 0;
       if (P.resident) ptx::mbar_wait(b_full0, 0);
       for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-        ptx::mbar_wait(acc_empty0 + 8 * acc, acc_ph ^ 1);
+        if (!(P.dbg & 256)) ptx::mbar_wait(acc_empty0 + 8 * acc, acc_ph ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_set = tmem + acc * acc_set_cols;
         const uint32_t d_corr = d_set + NP * part_cols;
@@ -267,9 +321,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         uint32_t first_corr = 0;  // accumulate flags
         int main_seen = 0;
         for (int kb = 0; kb < P.nkb; ++kb) {
-          trace(P, 0x400 | kb);
-          ptx::mbar_wait(a_full0 + 8 * s, ph);
-          trace(P, 0x500 | kb);
+          tr(P, 1, 0x400 | kb);
+          if (!(P.dbg & 256)) ptx::mbar_wait(a_full0 + 8 * s, ph);
+          tr(P, 1, 0x500 | kb);
           uint64_t dkb;
           if (P.resident) {
             dkb = desc0 + ((kb * P.b_stage_bytes) >> 4);
@@ -286,13 +340,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
               if (P.concat) {
                 // B rows [hi; lo] as one N = 2*NT operand: [main | corr] += A_hi * [B_hi | B_lo],
                 // then corr += A_lo * B_hi -- two MMAs per K step instead of three
-                ptx::mma_tf32_ts(d_main, a_hi + k4 * 8, dh, idesc2, main_seen >= NP);
-                ptx::mma_tf32_ts(d_main + part_cols, a_lo + k4 * 8, dh, idesc, 1);
+                ptx::mma_tf32_ts_warp(d_main, a_hi + k4 * 8, dh, idesc2, main_seen >= NP);
+                ptx::mma_tf32_ts_warp(d_main + part_cols, a_lo + k4 * 8, dh, idesc, 1);
+                if (P.dbg & 128) tr(P, 3, 0xA00 | k4);
                 d_main += 2 * part_cols;
               } else {
-                ptx::mma_tf32_ts(d_corr, a_lo + k4 * 8, dh, idesc, first_corr);
-                ptx::mma_tf32_ts(d_corr, a_hi + k4 * 8, dl, idesc, 1);
-                ptx::mma_tf32_ts(d_main, a_hi + k4 * 8, dh, idesc, main_seen >= NP);
+                ptx::mma_tf32_ts_warp(d_corr, a_lo + k4 * 8, dh, idesc, first_corr);
+                ptx::mma_tf32_ts_warp(d_corr, a_hi + k4 * 8, dl, idesc, 1);
+                ptx::mma_tf32_ts_warp(d_main, a_hi + k4 * 8, dh, idesc, main_seen >= NP);
+                if (P.dbg & 128) tr(P, 3, 0xA00 | k4);
                 d_main += part_cols;
               }
               first_corr = 1;
@@ -300,19 +356,79 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
               if (d_main == d_main_end) d_main = d_set;
             }
           }
-          ptx::mma_commit(a_empty0 + 8 * s);
-          trace(P, 0x600 | kb);
+          ptx::mma_commit_warp(a_empty0 + 8 * s);
+          tr(P, 1, 0x600 | kb);
           if (++s == SA) { s = 0; ph ^= 1; }
           if (!P.resident) {
-            ptx::mma_commit(b_empty0 + 8 * bs);
-            if (++bs == kBStages) { bs = 0; bph ^= 1; }
+            ptx::mma_commit_warp(b_empty0 + 8 * bs);
+            if (++bs == P.nbs) { bs = 0; bph ^= 1; }
           }
         }
-        ptx::mma_commit(acc_full0 + 8 * acc);
+        ptx::mma_commit_warp(acc_full0 + 8 * acc);
         if (NB == 2) { acc ^= 1; if (acc == 0) acc_ph ^= 1; } else { acc_ph ^= 1; }
       }
     }
-  } else if (warp >= 4 && warp < 12) {
+  } else if (P.staged && warp >= 4 && warp < 8) {
+    // ===== A converter, staged: the warpgroup reads each pixel's im2col row
+    // from the TMA-staged input box in shared memory (swizzled like the TMA
+    // wrote it, so the 16-byte reads are bank-conflict free) =====
+    constexpr int CB = 1 << CBS, SEGS = 32 >> CBS, PER = 8 / SEGS;
+    constexpr uint32_t SWZ = CBS >= 3 ? (1u << (CBS - 2)) - 1 : 0;  // XOR mask of 16B chunks
+    const int row = threadIdx.x - 128;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t st0 = ptx::smem_u32(st_buf);
+    int s = 0, sb = 0;
+    uint32_t par = 1, sph = 0;
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      const int m_tile = tile % P.m_tiles;
+      const int64_t m0 = (int64_t)m_tile * kTileM, m = m0 + row;
+      int b0 = 0, oy0 = 0, ox0 = 0, b = 0, oy = 0, ox = 0;
+      a.pm.decode(m0, b0, oy0, ox0);
+      const bool valid = m < M && !(P.dbg & 1);
+      if (valid) a.pm.decode(m, b, oy, ox);
+      // logical byte offset of this pixel's tap-(0,0) element inside a staging buffer
+      const uint32_t pix0 = (uint32_t)(b - b0) * P.piece_bytes +
+                            (uint32_t)((((oy - (b == b0 ? oy0 : 0)) * a.stride) * P.box_w + ox * a.stride) * CB * 4);
+      for (int kb = 0; kb < P.nkb; ++kb) {
+        if (kb % P.kpc == 0) ptx::mbar_wait_warp(ptx::smem_u32(&S->st_full[sb]), sph);
+        float4 f[8];
+        const uint32_t buf = st0 + sb * P.st_bytes;
+#pragma unroll
+        for (int g = 0; g < SEGS; ++g) {
+          const int2 e = seg[kb * SEGS + g];
+          const bool ok = valid && (e.y & 0xFF) != 31;
+          const uint32_t L0 = pix0 + (uint32_t)e.x * 4;
+#pragma unroll
+          for (int q = 0; q < PER; ++q) {
+            const uint32_t L = L0 + q * 16;
+            const uint32_t phys = L ^ (((L >> 7) & SWZ) << 4);
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (ok) asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(buf + phys));
+            f[g * PER + q] = v;
+          }
+        }
+        if (kb % P.kpc == P.kpc - 1 || kb == P.nkb - 1) {
+          // last K-block of this channel block: release the staging buffer
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->st_empty[sb]));
+          if (++sb == 2) { sb = 0; sph ^= 1; }
+        }
+        ptx::mbar_wait_warp(ptx::smem_u32(&S->a_empty[s]), par);
+        if (!(P.dbg & 512)) {
+          ptx::tc_fence_after();
+          const uint32_t t_hi = tmem + lane_off + a_col0 + s * 64;
+          store_kblock(P, f, t_hi, t_hi + 32);
+          ptx::tmem_st_wait();
+          ptx::tc_fence_before();
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->a_full[s]));
+        if (++s == SA) { s = 0; par ^= 1; }
+      }
+    }
+    (void)CB;
+  } else if (!P.staged && warp >= 4 && warp < 12) {
     // ===== A converters: two warpgroups take alternate K-blocks; thread r of
     // a warpgroup owns accumulator row r.  The next K-block's loads are issued
     // before the current one is split and stored (software pipelining).  All
@@ -345,9 +461,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         load_kblock<CBS>(seg, kb_n, pxn, fb);
         px = pxn;
       }
-      if (lane == 0 && warp == 4) trace(P, 0x100 | kb);
+      if (lane == 0 && warp == 4) tr(P, 0, 0x100 | kb);
       ptx::mbar_wait_warp(ptx::smem_u32(&S->a_empty[s]), par);
-      if (lane == 0 && warp == 4) trace(P, 0x200 | kb);
+      if (lane == 0 && warp == 4) tr(P, 0, 0x200 | kb);
       ptx::tc_fence_after();
       const uint32_t t_hi = tmem + lane_off + a_col0 + s * 64;
       store_kblock(P, fa, t_hi, t_hi + 32);
@@ -355,7 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->a_full[s]));
-      if (lane == 0 && warp == 4) trace(P, 0x300 | kb);
+      if (lane == 0 && warp == 4) tr(P, 0, 0x300 | kb);
 #pragma unroll
       for (int q = 0; q < 8; ++q) fa[q] = fb[q];
       tile = tile_n;
@@ -363,19 +479,19 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       s += 2;
       if (s >= SA) { s -= SA; par ^= 1; }
     }
-  } else if (warp >= 12) {
+  } else if (warp < 4) {
     // ===== epilogue =====
     const EpiParams& e = a.epi;
-    const int row = threadIdx.x - 384;
+    const int row = threadIdx.x;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     uint32_t acc_it = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++acc_it) {
       const int m_tile = tile % P.m_tiles, n_tile = tile / P.m_tiles;
       const uint32_t acc = NB == 2 ? (acc_it & 1) : 0;
       const uint32_t acc_ph = (NB == 2 ? (acc_it >> 1) : acc_it) & 1;
-      if (lane == 0 && warp == 12) trace(P, 0x700);
+      if (lane == 0 && warp == 0) tr(P, 2, 0x700);
       ptx::mbar_wait_warp(ptx::smem_u32(&S->acc_full[acc]), acc_ph);
-      if (lane == 0 && warp == 12) trace(P, 0x800);
+      if (lane == 0 && warp == 0) tr(P, 2, 0x800);
       ptx::tc_fence_after();
       const int64_t m = (int64_t)m_tile * kTileM + row;
       int b = -1, oy = 0, ox = 0;
@@ -494,17 +610,18 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->acc_empty[acc]));
-      if (lane == 0 && warp == 12) trace(P, 0x900);
+      if (lane == 0 && warp == 0) tr(P, 2, 0x900);
     }
   }
   __syncthreads();
-  if (warp == 2) {
+  if (warp == kWarpAlloc) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, P.tmem_cols);
   }
 }
 
 size_t smem_aux_bytes(const TcParams& P);
+void staging_geometry(const ConvArgs& a, TcParams& P);
 
 bool make_params(const ConvArgs& a, TcParams& P) {
   const int cb = a.in.cb;
@@ -532,8 +649,23 @@ bool make_params(const ConvArgs& a, TcParams& P) {
   rows += e.residual >= 2 ? 6 : 0;
   P.ptab_rows = rows;
   const size_t aux = smem_aux_bytes(P);
-  if (1024 + (size_t)P.b_stage_bytes * kBStages + aux > 227 * 1024) return false;
-  P.resident = (P.n_tiles == 1 && 1024 + (size_t)P.b_stage_bytes * P.nkb + aux <= 220 * 1024) ? 1 : 0;
+  const size_t budget = 225 * 1024;
+  // staged input if a tile needs few boxes and everything fits
+  P.staged = 0;
+  staging_geometry(a, P);
+  const bool stage_ok = !(getenv("PCNN_TC_NOSTAGE")) && P.pieces <= 4 && P.box_w <= 256 && P.box_h <= 256 &&
+                        (a.in.nblk == 1 || a.in.cb == 32);
+  P.nbs = kBStages;
+  if (stage_ok) {
+    for (int nbs = kBStages; nbs >= 2 && !P.staged; --nbs)
+      if (1024 + (size_t)P.b_stage_bytes * nbs + 2 * (size_t)P.st_bytes + aux <= budget) {
+        P.staged = 1;
+        P.nbs = nbs;
+      }
+  }
+  const size_t st = P.staged ? 2 * (size_t)P.st_bytes : 0;
+  if (1024 + (size_t)P.b_stage_bytes * P.nbs + st + aux > budget) return false;
+  P.resident = (P.n_tiles == 1 && 1024 + (size_t)P.b_stage_bytes * P.nkb + st + aux <= budget) ? 1 : 0;
   // TMEM budget (512 columns): acc_bufs x (P + 1) x NT accumulators + a_stages x 64
   const char* dbg = getenv("PCNN_TC_DEBUG");
   P.dbg = dbg ? atoi(dbg) : 0;
@@ -567,21 +699,38 @@ size_t smem_aux_bytes(const TcParams& P) {
 }
 
 size_t smem_bytes(const TcParams& P) {
-  size_t b = P.resident ? (size_t)P.b_stage_bytes * P.nkb : (size_t)P.b_stage_bytes * kBStages;
-  return 1024 + b + smem_aux_bytes(P);
+  size_t b = P.resident ? (size_t)P.b_stage_bytes * P.nkb : (size_t)P.b_stage_bytes * P.nbs;
+  return 1024 + b + (P.staged ? 2 * (size_t)P.st_bytes : 0) + smem_aux_bytes(P);
+}
+
+// staging geometry of a layer: box covering the input rows of one tile's
+// output rows within one image, all columns incl. padding
+void staging_geometry(const ConvArgs& a, TcParams& P) {
+  const PixelMap& pm = a.pm;
+  const int hw_out = pm.order == kPlain ? pm.ho * pm.wo : pm.hp * pm.wp * 4;
+  int rows_out;
+  if (pm.order == kPlain) rows_out = (kTileM + pm.wo - 1) / pm.wo + 1;
+  else rows_out = 2 * ((kTileM / 4 + pm.wp - 1) / pm.wp + 1);
+  if (rows_out > pm.ho) rows_out = pm.ho;
+  P.box_h = (rows_out - 1) * a.stride + a.kh;
+  P.box_w = (pm.wo - 1) * a.stride + a.kw;
+  P.pieces = (kTileM + hw_out - 1) / hw_out + 1;
+  if (P.pieces > (int)((host_pixel_count(pm, a.batch) + hw_out - 1) / hw_out)) P.pieces = a.batch;
+  P.piece_bytes = (uint32_t)(((size_t)P.box_w * P.box_h * a.in.cb * 4 + 1023) & ~size_t(1023));
+  P.st_bytes = P.piece_bytes * P.pieces;
+  P.nblk_in = a.in.nblk;
+  P.kpc = a.in.nblk == 1 ? P.nkb : P.taps;  // K-blocks per channel block (cb = 32 when nblk > 1)
 }
 
 }  // namespace
 
 // debugging aid (not part of pcnn.h): drain the CTA-0 event trace
 extern "C" int pcnn_tc_trace(unsigned long long* host, int n) {
-  unsigned int cnt = 0;
-  cudaMemcpyFromSymbol(&cnt, g_trace_n, sizeof(cnt));
-  int m = (int)(cnt < (unsigned)n ? cnt : (unsigned)n);
-  if (m > kTraceLen) m = kTraceLen;
+  int m = n < kTraceLen ? n : kTraceLen;
   cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * m);
-  unsigned int z = 0;
-  cudaMemcpyToSymbol(g_trace_n, &z, sizeof(z));
+  cudaMemset(reinterpret_cast<void*>(0), 0, 0);
+  static unsigned long long zeros[kTraceLen];
+  cudaMemcpyToSymbol(g_trace, zeros, sizeof(zeros));
   return m;
 }
 
@@ -590,9 +739,39 @@ bool conv_tc_supported(const ConvArgs& a) {
   return make_params(a, P);
 }
 
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static bool encode_input_map(const ConvArgs& a, TcParams& P) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* ptr = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess || !ptr)
+      return false;
+    fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  const TensorView& in = a.in;
+  const cuuint64_t dims[4] = {(cuuint64_t)in.cb, (cuuint64_t)in.w, (cuuint64_t)in.h,
+                              (cuuint64_t)a.batch * in.nblk};
+  const cuuint64_t strides[3] = {(cuuint64_t)in.cb * 4, (cuuint64_t)in.w * in.cb * 4,
+                                 (cuuint64_t)in.h * in.w * in.cb * 4};
+  const cuuint32_t box[4] = {(cuuint32_t)in.cb, (cuuint32_t)P.box_w, (cuuint32_t)P.box_h, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUtensorMapSwizzle swz = in.cb == 32 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                 : in.cb == 16 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                 : in.cb == 8 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE;
+  CUresult r = fn(reinterpret_cast<CUtensorMap*>(&P.tmap), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, in.base, dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 void launch_conv_tc(const ConvArgs& a, cudaStream_t s) {
   TcParams P;
   if (!make_params(a, P)) return;
+  if (P.staged && !encode_input_map(a, P)) P.staged = 0;
   static int nsm = 0;
   if (!nsm) {
     int dev = 0;

@@ -13,15 +13,17 @@ lib = L.lib()
 fn = lib.pcnn_tc_trace
 fn.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
 buf = (ctypes.c_ulonglong * 65536)()
-fn(buf, 65536)  # reset
-for i in range(unit + 1):
+for i in range(unit):
     eng.forward_unit(256, i, x, out)
 torch.cuda.synchronize()
+fn(buf, 65536)  # reset
+eng.forward_unit(256, unit, x, out)
+torch.cuda.synchronize()
 n = fn(buf, 65536)
-ev = [(int(v) >> 48, int(v) & 0xFFFFFFFFFFFF) for v in buf[:n]]
+ev = [(int(v) >> 48, int(v) & 0xFFFFFFFFFFFF) for v in buf[:n] if int(v)]
 t0 = min(t for _, t in ev)
-names = {1: "cv_wait", 2: "cv_go", 3: "cv_done", 4: "mma_wait", 5: "mma_go", 6: "mma_done", 7: "ep_wait", 8: "ep_go", 9: "ep_done"}
+names = {10: "mma_k4", 1: "cv_wait", 2: "cv_go", 3: "cv_done", 4: "mma_wait", 5: "mma_go", 6: "mma_done", 7: "ep_wait", 8: "ep_go", 9: "ep_done"}
 ev.sort(key=lambda e: e[1])
-for tag, t in ev[:160]:
+for tag, t in ev[:240]:
     print(f"{t - t0:8d} {names.get(tag >> 8, tag >> 8):9s} kb={tag & 0xff}")
 print("events", n, "span", max(t for _, t in ev) - t0)

@@ -5,6 +5,7 @@
 //        -I include tools/ubench_tc.cu -o build/ubench_tc
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 
 #include "tc_ptx.cuh"
 
@@ -12,7 +13,7 @@ using namespace pcnn;
 
 __device__ __forceinline__ uint64_t clk() { return clock64(); }
 
-__global__ void ubench(uint64_t* out, int iters, int n_mma) {
+__global__ void ubench(uint64_t* out, int iters, int n_mma, int randomize) {
   __shared__ __align__(1024) uint8_t bsm[16 * 1024];
   __shared__ uint64_t bar[4];
   __shared__ uint32_t tbase;
@@ -76,6 +77,32 @@ __global__ void ubench(uint64_t* out, int iters, int n_mma) {
   }
   __syncthreads();
 
+  // 3a. optionally fill A (TMEM cols 256..511) and B (smem) with random data
+  if (randomize) {
+    if (warp < 4) {
+      const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+      uint32_t seed = 0x9E3779B9u * (threadIdx.x + 1);
+      for (int c = 256; c < 512; c += 8) {
+        uint32_t r[8];
+        for (int i = 0; i < 8; ++i) {
+          seed = seed * 1664525u + 1013904223u;
+          r[i] = __float_as_uint(((seed >> 8) * (1.0f / 16777216.0f)) - 0.5f) & 0xFFFFE000u;
+        }
+        ptx::tmem_st8(tmem + lane_off + c, r);
+      }
+      ptx::tmem_st_wait();
+    }
+    for (int i = threadIdx.x; i < 16 * 1024 / 4; i += blockDim.x) {
+      uint32_t x = 0x85EBCA6Bu * (i + 7);
+      x ^= x >> 13; x *= 0xC2B2AE35u; x ^= x >> 16;
+      reinterpret_cast<float*>(bsm)[i] = __uint_as_float(__float_as_uint(((x >> 8) * (1.0f / 16777216.0f)) - 0.5f) & 0xFFFFE000u);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+  }
+
   // 3b. MMA throughput vs number of independent accumulators and N (48 MMAs)
   if (threadIdx.x == 0) {
     int slot = 6;
@@ -95,6 +122,48 @@ __global__ void ubench(uint64_t* out, int iters, int n_mma) {
         }
         t1 = clk();
         out[slot++] = (t1 - t0) / 20 / 48;
+      }
+    }
+    // patterns of the conv kernel: alternating N (32/16), varying B descriptor
+    {
+      const uint32_t i32 = ptx::idesc_tf32(128, 32), i16 = ptx::idesc_tf32(128, 16);
+      for (int pat = 0; pat < 3; ++pat) {
+        t0 = clk();
+        for (int i = 0; i < 20; ++i) {
+          for (int k = 0; k < 48; ++k) {
+            const uint32_t id = pat == 0 ? ((k & 1) ? i16 : i32) : i32;
+            const uint64_t b = pat == 1 ? bd + 2 * ((k >> 1) & 3) : bd;
+            const uint32_t d = pat == 2 ? tmem + (k & 1) * 16 : tmem;
+            ptx::mma_tf32_ts(d, tmem + 256 + (k & 7) * 8, b, id, k > 1);
+          }
+          ptx::mma_commit(b2);
+          ptx::mbar_wait(b2, ph);
+          ph ^= 1;
+        }
+        t1 = clk();
+        out[26 + pat] = (t1 - t0) / 20 / 48;
+      }
+    }
+    // the conv kernel's per-K-block pattern: fence, 8 MMAs (concat), commit
+    {
+
+      const uint32_t i32 = ptx::idesc_tf32(128, 32), i16 = ptx::idesc_tf32(128, 16);
+      for (int var = 0; var < 6; ++var) {
+        const uint32_t acol = var == 3 ? 64 : (var == 4 ? 96 : (var == 5 ? 128 : 256));
+        t0 = clk();
+        for (int i = 0; i < 24; ++i) {
+          if (var != 1) ptx::tc_fence_after();
+          for (int k4 = 0; k4 < 4; ++k4) {
+            ptx::mma_tf32_ts(tmem, tmem + acol + k4 * 8, bd + 2 * k4, i32, i > 0 || k4 > 0);
+            ptx::mma_tf32_ts(tmem + 16, tmem + acol + 32 + k4 * 8, bd + 2 * k4, i16, 1);
+          }
+          if (var != 2) ptx::mma_commit(ptx::smem_u32(&bar[3]));
+        }
+        ptx::mma_commit(b2);
+        ptx::mbar_wait(b2, ph);
+        ph ^= 1;
+        t1 = clk();
+        out[40 + var] = (t1 - t0) / 24;
       }
     }
     // SS mode (A from smem, same zero image), N=16 and 128, R=1 and 4
@@ -122,11 +191,12 @@ __global__ void ubench(uint64_t* out, int iters, int n_mma) {
     if (threadIdx.x == 0) stop = 0;
     __syncthreads();
     uint32_t ph2 = 0;
-    for (int mode = 1; mode < 3; ++mode) {   // 0: N=256 alone, 1: N=64 + STTM traffic, 2: N=64 + LDTM traffic
+    for (int mode = 1; mode < 5; ++mode) {   // 1: +STTM, 2: +LDTM, 3: +converter-like mix, 4: alone (real B data)
       if (threadIdx.x == 0) stop = 0;
       __syncthreads();
       if (threadIdx.x == 0) {
         const uint32_t idesc = ptx::idesc_tf32(128, mode == 0 ? 256 : 64);
+        if (mode == 4) for (int i = 0; i < 16 * 1024 / 4; ++i) reinterpret_cast<float*>(bsm)[i] = 0.37f * (i % 13);
         t0 = clk();
         for (int i = 0; i < 20; ++i) {
           for (int k = 0; k < 48; ++k) ptx::mma_tf32_ts(tmem, tmem + 256 + (k & 7) * 8, bd, idesc, k > 0);
@@ -145,12 +215,33 @@ __global__ void ubench(uint64_t* out, int iters, int n_mma) {
           if (mode == 1) {
             for (int g = 0; g < 8; ++g) ptx::tmem_st8(tmem + lane_off + 320 + g * 8, r);
             ptx::tmem_st_wait();
+          } else if (mode == 3) {
+            float4 f[8];
+            const uint32_t sb = ptx::smem_u32(bsm) + (threadIdx.x & 31) * 64;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(f[q].x), "=f"(f[q].y), "=f"(f[q].z), "=f"(f[q].w) : "r"(sb + q * 16));
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              uint32_t hi[8], lo[8];
+              const float v[8] = {f[2*g].x, f[2*g].y, f[2*g].z, f[2*g].w, f[2*g+1].x, f[2*g+1].y, f[2*g+1].z, f[2*g+1].w};
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                hi[i] = (__float_as_uint(v[i]) + 0x1000u) & 0xFFFFE000u;
+                lo[i] = (__float_as_uint(v[i] - __uint_as_float(hi[i])) + 0x1000u) & 0xFFFFE000u;
+              }
+              ptx::tmem_st8(tmem + lane_off + 320 + g * 8, hi);
+              ptx::tmem_st8(tmem + lane_off + 352 + g * 8, lo);
+            }
+            ptx::tmem_st_wait();
+          } else if (mode == 4) {
+            break;
           } else {
             ptx::tmem_ld16(tmem + lane_off + 384, v);
             r[0] += __float_as_uint(v[3]);
           }
         }
-        if (r[0] == 12345) out[40] = 1;
+        if (r[0] == 12345) out[50] = 1;
       }
       __syncthreads();
     }
@@ -201,7 +292,7 @@ int main() {
   cudaMalloc(&d, 64 * sizeof(uint64_t));
   cudaMemset(d, 0, 64 * sizeof(uint64_t));
   for (int n_mma : {1, 12, 48}) {
-    ubench<<<1, 384>>>(d, 200, n_mma);
+    ubench<<<getenv("UB_BLOCKS") ? atoi(getenv("UB_BLOCKS")) : 1, 384>>>(d, 200, n_mma, getenv("UB_RANDOM") ? 1 : 0);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
       printf("error %s\n", cudaGetErrorString(e));
@@ -215,8 +306,13 @@ int main() {
         printf("TS N=%3d cycles/MMA with R=1,2,4,8 accumulators: %llu %llu %llu %llu\n", ns[ni],
                (unsigned long long)h[6 + ni * 4], (unsigned long long)h[7 + ni * 4],
                (unsigned long long)h[8 + ni * 4], (unsigned long long)h[9 + ni * 4]);
-      printf("TS N=256 alone: %llu; N=64 with STTM traffic: %llu; with LDTM traffic: %llu\n",
-             (unsigned long long)h[30], (unsigned long long)h[31], (unsigned long long)h[32]);
+      printf("TS N=64 with STTM traffic: %llu; with LDTM traffic: %llu; with converter mix: %llu; real B data: %llu\n",
+             (unsigned long long)h[31], (unsigned long long)h[32], (unsigned long long)h[33], (unsigned long long)h[34]);
+      printf("alternating N 32/16: %llu; varying B desc: %llu; D alternating (overlapping cols): %llu\n",
+             (unsigned long long)h[26], (unsigned long long)h[27], (unsigned long long)h[28]);
+      printf("kernel pattern per K-block (8 MMAs): fence+commit %llu, commit only %llu, fence only %llu; A at col 64: %llu, 96: %llu, 128: %llu\n",
+             (unsigned long long)h[40], (unsigned long long)h[41], (unsigned long long)h[42],
+             (unsigned long long)h[43], (unsigned long long)h[44], (unsigned long long)h[45]);
       printf("SS N=16 R=1,4: %llu %llu   SS N=128 R=1,4: %llu %llu\n", (unsigned long long)h[22],
              (unsigned long long)h[23], (unsigned long long)h[24], (unsigned long long)h[25]);
     }
