@@ -43,11 +43,12 @@ namespace pcnn {
 
 namespace {
 
-constexpr int kThreads = 512;
+constexpr int kThreads = 640;
 // warp roles: the warp scheduler favours higher warp ids, so the single MMA
-// issuing thread gets the highest id; epilogue warps 0-3 and converter
-// warpgroups 4-7 / 8-11 each cover TMEM lanes 0-127 (warp w owns 32*(w%4)..)
-constexpr int kWarpAlloc = 12, kWarpProducer = 14, kWarpMma = 15;
+// issuing warp gets the highest id.  Epilogue warpgroups 0-3 / 12-15 (one per
+// accumulator buffer) and converter warpgroups 4-7 / 8-11 (alternate A
+// stages) each cover TMEM lanes 0-127 (warp w owns lanes 32*(w%4)..+31).
+constexpr int kWarpAlloc = 16, kWarpProducer = 18, kWarpMma = 19;
 constexpr int kMaxAStages = 4;   // A hi/lo stages in TMEM (64 columns each)
 constexpr int kBStages = 4;      // streamed B stages in smem
 constexpr int kTileM = 128;
@@ -69,6 +70,7 @@ struct TcParams {
   int taps;        // kh * kw
   int nseg;        // nblk_in * taps (valid channel segments)
   int a_stages;    // A stages in TMEM
+  int ks;          // K-blocks (of 32) per A stage: 1 or 2
   int acc_bufs;    // accumulator sets (1 or 2)
   int partials;    // main partial accumulators P
   uint32_t b_stage_bytes;
@@ -92,7 +94,6 @@ struct TcParams {
 constexpr int kTraceLen = 1 << 16;
 constexpr int kTraceRegion = kTraceLen / 4;
 __device__ unsigned long long g_trace[kTraceLen];
-__device__ unsigned int g_trace_n;
 
 struct Tracer {
   uint32_t n = 0;
@@ -192,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   const int total_tiles = P.m_tiles * P.n_tiles;
   Tracer tr;
   const int64_t M = a.pm.count(a.batch);
-  const int SA = P.a_stages, NB = P.acc_bufs, NP = P.partials;
+  const int SA = P.a_stages, NB = P.acc_bufs, NP = P.partials, KS = P.ks;
   // accumulator set: concat -> NP blocks [main_p | corr_p] of 2*NT columns;
   // otherwise NP main partials then one correction accumulator
   const uint32_t acc_set_cols = P.concat ? (uint32_t)NP * 2 * P.nt : (uint32_t)(NP + 1) * P.nt;
@@ -210,7 +211,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       ptx::mbar_init(ptx::smem_u32(&S->acc_full[i]), 1);
       ptx::mbar_init(ptx::smem_u32(&S->acc_empty[i]), 4);
       ptx::mbar_init(ptx::smem_u32(&S->st_full[i]), 1);
-      ptx::mbar_init(ptx::smem_u32(&S->st_empty[i]), 4);
+      ptx::mbar_init(ptx::smem_u32(&S->st_empty[i]), 8);
     }
     ptx::fence_mbar_init();
   }
@@ -320,61 +321,83 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         const uint32_t d_main_end = d_set + acc_set_cols - (P.concat ? 0 : part_cols);
         uint32_t first_corr = 0;  // accumulate flags
         int main_seen = 0;
-        for (int kb = 0; kb < P.nkb; ++kb) {
-          tr(P, 1, 0x400 | kb);
+        for (int kb0 = 0; kb0 < P.nkb; kb0 += KS) {
+          tr(P, 1, 0x400 | kb0);
           if (!(P.dbg & 256)) ptx::mbar_wait(a_full0 + 8 * s, ph);
-          tr(P, 1, 0x500 | kb);
-          uint64_t dkb;
-          if (P.resident) {
-            dkb = desc0 + ((kb * P.b_stage_bytes) >> 4);
-          } else {
-            ptx::mbar_wait(b_full0 + 8 * bs, bph);
-            dkb = desc0 + ((bs * P.b_stage_bytes) >> 4);
-          }
+          tr(P, 1, 0x500 | kb0);
           ptx::tc_fence_after();
-          const uint32_t a_hi = tmem + a_col0 + s * 64, a_lo = a_hi + 32;
-          if (do_mma) {
+          const int kbn = P.nkb - kb0 < KS ? P.nkb - kb0 : KS;
+          for (int j = 0; j < kbn; ++j) {
+            const int kb = kb0 + j;
+            uint64_t dkb;
+            if (P.resident) {
+              dkb = desc0 + ((kb * P.b_stage_bytes) >> 4);
+            } else {
+              ptx::mbar_wait(b_full0 + 8 * bs, bph);
+              ptx::tc_fence_after();
+              dkb = desc0 + ((bs * P.b_stage_bytes) >> 4);
+            }
+            const uint32_t a_hi = tmem + a_col0 + s * 64 * KS + j * 32, a_lo = a_hi + 32 * KS;
+            if (do_mma && P.concat && !(P.dbg & 128)) {
+              // the whole K-block in one asm statement (operands go uniform once)
+              uint32_t dk[4], accm = 0;
 #pragma unroll
-            for (int k4 = 0; k4 < kTcBK / 8; ++k4) {
-              const uint64_t dh = dkb + 2 * k4, dl = dh + lo_enc;  // +32 B per 8-deep K step
-              if (P.concat) {
-                // B rows [hi; lo] as one N = 2*NT operand: [main | corr] += A_hi * [B_hi | B_lo],
-                // then corr += A_lo * B_hi -- two MMAs per K step instead of three
-                ptx::mma_tf32_ts_warp(d_main, a_hi + k4 * 8, dh, idesc2, main_seen >= NP);
-                ptx::mma_tf32_ts_warp(d_main + part_cols, a_lo + k4 * 8, dh, idesc, 1);
-                if (P.dbg & 128) tr(P, 3, 0xA00 | k4);
+              for (int k4 = 0; k4 < 4; ++k4) {
+                dk[k4] = d_main;
+                accm |= (main_seen >= NP ? 1u : 0u) << k4;
+                ++main_seen;
                 d_main += 2 * part_cols;
-              } else {
-                ptx::mma_tf32_ts_warp(d_corr, a_lo + k4 * 8, dh, idesc, first_corr);
-                ptx::mma_tf32_ts_warp(d_corr, a_hi + k4 * 8, dl, idesc, 1);
-                ptx::mma_tf32_ts_warp(d_main, a_hi + k4 * 8, dh, idesc, main_seen >= NP);
-                if (P.dbg & 128) tr(P, 3, 0xA00 | k4);
-                d_main += part_cols;
+                if (d_main == d_main_end) d_main = d_set;
               }
+              ptx::mma_kblock_concat(dk[0], dk[1], dk[2], dk[3], part_cols, a_hi, a_lo, dkb, idesc2, idesc, accm);
               first_corr = 1;
-              ++main_seen;
-              if (d_main == d_main_end) d_main = d_set;
+            } else if (do_mma) {
+#pragma unroll
+              for (int k4 = 0; k4 < kTcBK / 8; ++k4) {
+                const uint64_t dh = dkb + 2 * k4, dl = dh + lo_enc;  // +32 B per 8-deep K step
+                if (P.concat) {
+                  // B rows [hi; lo] as one N = 2*NT operand: [main | corr] += A_hi * [B_hi | B_lo],
+                  // then corr += A_lo * B_hi -- two MMAs per K step instead of three
+                  ptx::mma_tf32_ts_warp(d_main, a_hi + k4 * 8, dh, idesc2, main_seen >= NP);
+                  ptx::mma_tf32_ts_warp(d_main + part_cols, a_lo + k4 * 8, dh, idesc, 1);
+                  if (P.dbg & 128) tr(P, 3, 0xA00 | k4);
+                  d_main += 2 * part_cols;
+                } else {
+                  ptx::mma_tf32_ts_warp(d_corr, a_lo + k4 * 8, dh, idesc, first_corr);
+                  ptx::mma_tf32_ts_warp(d_corr, a_hi + k4 * 8, dl, idesc, 1);
+                  ptx::mma_tf32_ts_warp(d_main, a_hi + k4 * 8, dh, idesc, main_seen >= NP);
+                  if (P.dbg & 128) tr(P, 3, 0xA00 | k4);
+                  d_main += part_cols;
+                }
+                first_corr = 1;
+                ++main_seen;
+                if (d_main == d_main_end) d_main = d_set;
+              }
+            }
+            if (!P.resident) {
+              ptx::mma_commit_warp(b_empty0 + 8 * bs);
+              if (++bs == P.nbs) { bs = 0; bph ^= 1; }
             }
           }
           ptx::mma_commit_warp(a_empty0 + 8 * s);
-          tr(P, 1, 0x600 | kb);
+          tr(P, 1, 0x600 | kb0);
           if (++s == SA) { s = 0; ph ^= 1; }
-          if (!P.resident) {
-            ptx::mma_commit_warp(b_empty0 + 8 * bs);
-            if (++bs == P.nbs) { bs = 0; bph ^= 1; }
-          }
         }
         ptx::mma_commit_warp(acc_full0 + 8 * acc);
         if (NB == 2) { acc ^= 1; if (acc == 0) acc_ph ^= 1; } else { acc_ph ^= 1; }
       }
     }
-  } else if (P.staged && warp >= 4 && warp < 8) {
-    // ===== A converter, staged: the warpgroup reads each pixel's im2col row
-    // from the TMA-staged input box in shared memory (swizzled like the TMA
-    // wrote it, so the 16-byte reads are bank-conflict free) =====
+  } else if (P.staged && warp >= 4 && warp < 12) {
+    // ===== A converters, staged: two warpgroups take alternate A stages and
+    // read each pixel's im2col row from the TMA-staged input box in shared
+    // memory (swizzled like the TMA wrote it: conflict-free 16-byte reads).
+    // Every converter warp waits st_full and arrives st_empty once per
+    // channel block, whether or not it converted any of its K-blocks. =====
     constexpr int CB = 1 << CBS, SEGS = 32 >> CBS, PER = 8 / SEGS;
     constexpr uint32_t SWZ = CBS >= 3 ? (1u << (CBS - 2)) - 1 : 0;  // XOR mask of 16B chunks
-    const int row = threadIdx.x - 128;
+    const int cw = (warp - 4) >> 2;
+    const int row = (threadIdx.x - 128) & 127;
+    int gstage = 0;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const uint32_t st0 = ptx::smem_u32(st_buf);
     int s = 0, sb = 0;
@@ -389,54 +412,74 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       // logical byte offset of this pixel's tap-(0,0) element inside a staging buffer
       const uint32_t pix0 = (uint32_t)(b - b0) * P.piece_bytes +
                             (uint32_t)((((oy - (b == b0 ? oy0 : 0)) * a.stride) * P.box_w + ox * a.stride) * CB * 4);
-      for (int kb = 0; kb < P.nkb; ++kb) {
-        if (kb % P.kpc == 0) ptx::mbar_wait_warp(ptx::smem_u32(&S->st_full[sb]), sph);
-        float4 f[8];
-        const uint32_t buf = st0 + sb * P.st_bytes;
-#pragma unroll
-        for (int g = 0; g < SEGS; ++g) {
-          const int2 e = seg[kb * SEGS + g];
-          const bool ok = valid && (e.y & 0xFF) != 31;
-          const uint32_t L0 = pix0 + (uint32_t)e.x * 4;
-#pragma unroll
-          for (int q = 0; q < PER; ++q) {
-            const uint32_t L = L0 + q * 16;
-            const uint32_t phys = L ^ (((L >> 7) & SWZ) << 4);
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (ok) asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(buf + phys));
-            f[g * PER + q] = v;
+      for (int kb0 = 0; kb0 < P.nkb; kb0 += KS, ++gstage) {
+        const int kbn = P.nkb - kb0 < KS ? P.nkb - kb0 : KS;
+        const bool mine = (gstage & 1) == cw;
+        if (!mine) {
+          // not this warpgroup's stage: only keep the staging-buffer protocol
+          for (int j = 0; j < kbn; ++j) {
+            const int kb = kb0 + j;
+            if (kb % P.kpc == 0) ptx::mbar_wait_warp(ptx::smem_u32(&S->st_full[sb]), sph);
+            if (kb % P.kpc == P.kpc - 1 || kb == P.nkb - 1) {
+              __syncwarp();
+              if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->st_empty[sb]));
+              if (++sb == 2) { sb = 0; sph ^= 1; }
+            }
           }
+          if (++s == SA) { s = 0; par ^= 1; }
+          continue;
         }
-        if (kb % P.kpc == P.kpc - 1 || kb == P.nkb - 1) {
-          // last K-block of this channel block: release the staging buffer
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->st_empty[sb]));
-          if (++sb == 2) { sb = 0; sph ^= 1; }
-        }
+        if (lane == 0 && warp == 4) tr(P, 0, 0x200 | kb0);
         ptx::mbar_wait_warp(ptx::smem_u32(&S->a_empty[s]), par);
-        if (!(P.dbg & 512)) {
-          ptx::tc_fence_after();
-          const uint32_t t_hi = tmem + lane_off + a_col0 + s * 64;
-          store_kblock(P, f, t_hi, t_hi + 32);
-          ptx::tmem_st_wait();
-          ptx::tc_fence_before();
+        ptx::tc_fence_after();
+        const uint32_t t_stage = tmem + lane_off + a_col0 + s * 64 * KS;
+        for (int j = 0; j < kbn; ++j) {
+          const int kb = kb0 + j;
+          if (kb % P.kpc == 0) ptx::mbar_wait_warp(ptx::smem_u32(&S->st_full[sb]), sph);
+          float4 f[8];
+          const uint32_t buf = st0 + sb * P.st_bytes;
+#pragma unroll
+          for (int g = 0; g < SEGS; ++g) {
+            const int2 e = seg[kb * SEGS + g];
+            const bool ok = valid && (e.y & 0xFF) != 31;
+            const uint32_t L0 = pix0 + (uint32_t)e.x * 4;
+#pragma unroll
+            for (int q = 0; q < PER; ++q) {
+              const uint32_t L = L0 + q * 16;
+              const uint32_t phys = L ^ (((L >> 7) & SWZ) << 4);
+              float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (ok) asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                                   : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(buf + phys));
+              f[g * PER + q] = v;
+            }
+          }
+          if (kb % P.kpc == P.kpc - 1 || kb == P.nkb - 1) {
+            // last K-block of this channel block: release the staging buffer
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->st_empty[sb]));
+            if (++sb == 2) { sb = 0; sph ^= 1; }
+          }
+          if (!(P.dbg & 512)) store_kblock(P, f, t_stage + j * 32, t_stage + 32 * KS + j * 32);
         }
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->a_full[s]));
+        if (lane == 0 && warp == 4) tr(P, 0, 0x300 | kb0);
         if (++s == SA) { s = 0; par ^= 1; }
       }
     }
     (void)CB;
   } else if (!P.staged && warp >= 4 && warp < 12) {
-    // ===== A converters: two warpgroups take alternate K-blocks; thread r of
-    // a warpgroup owns accumulator row r.  The next K-block's loads are issued
-    // before the current one is split and stored (software pipelining).  All
-    // bookkeeping is incremental -- no divisions in the loop. =====
+    // ===== A converters, direct loads: two warpgroups take alternate A stages
+    // (KS K-blocks each); thread r of a warpgroup owns accumulator row r.  All
+    // loads of a stage are issued before the stage's wait.  Bookkeeping is
+    // incremental -- no divisions in the loop. =====
     const int cw = (warp - 4) >> 2;
     const int row = (threadIdx.x - 128) & 127;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const int nkb = P.nkb;
+    const int spt = (nkb + KS - 1) / KS;  // stages per tile
     auto px_for = [&](int tile) {
       const int64_t m = (int64_t)(tile % P.m_tiles) * kTileM + row;
       int b = 0, oy = 0, ox = 0;
@@ -444,51 +487,51 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       if (valid) a.pm.decode(m, b, oy, ox);
       return pixel_row(P, b, oy, ox, valid);
     };
-    // position of this warpgroup's first K-block
-    int tile = blockIdx.x, kb = cw;
-    while (kb >= nkb) { kb -= nkb; tile += gridDim.x; }
-    int s = cw, par = 1;  // stage and the parity to wait for on a_empty
+    int tile = blockIdx.x, r = cw;  // r: stage index within the tile
+    while (r >= spt) { r -= spt; tile += gridDim.x; }
+    int s = cw, par = 1;  // A stage and the parity to wait for on a_empty
     while (s >= SA) { s -= SA; par ^= 1; }
-    PixelRow px = px_for(tile);
-    float4 fa[8];
-    if (tile < total_tiles) load_kblock<CBS>(seg, kb, px, fa);
+    int px_tile = -1;
+    PixelRow px;
     while (tile < total_tiles) {
-      int tile_n = tile, kb_n = kb + 2;
-      while (kb_n >= nkb) { kb_n -= nkb; tile_n += gridDim.x; }
-      float4 fb[8];
-      if (tile_n < total_tiles) {
-        const PixelRow pxn = tile_n == tile ? px : px_for(tile_n);
-        load_kblock<CBS>(seg, kb_n, pxn, fb);
-        px = pxn;
+      if (px_tile != tile) {
+        px = px_for(tile);
+        px_tile = tile;
       }
-      if (lane == 0 && warp == 4) tr(P, 0, 0x100 | kb);
+      const int kb0 = r * KS;
+      const int kbn = nkb - kb0 < KS ? nkb - kb0 : KS;
+      float4 f[2][8];
+      load_kblock<CBS>(seg, kb0, px, f[0]);
+      if (kbn > 1) load_kblock<CBS>(seg, kb0 + 1, px, f[1]);
+      if (lane == 0 && warp == 4) tr(P, 0, 0x200 | kb0);
       ptx::mbar_wait_warp(ptx::smem_u32(&S->a_empty[s]), par);
-      if (lane == 0 && warp == 4) tr(P, 0, 0x200 | kb);
       ptx::tc_fence_after();
-      const uint32_t t_hi = tmem + lane_off + a_col0 + s * 64;
-      store_kblock(P, fa, t_hi, t_hi + 32);
+      const uint32_t t_stage = tmem + lane_off + a_col0 + s * 64 * KS;
+      store_kblock(P, f[0], t_stage, t_stage + 32 * KS);
+      if (kbn > 1) store_kblock(P, f[1], t_stage + 32, t_stage + 32 * KS + 32);
       if (!(P.dbg & 16)) ptx::tmem_st_wait();
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->a_full[s]));
-      if (lane == 0 && warp == 4) tr(P, 0, 0x300 | kb);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) fa[q] = fb[q];
-      tile = tile_n;
-      kb = kb_n;
+      if (lane == 0 && warp == 4) tr(P, 0, 0x300 | kb0);
+      r += 2;
+      while (r >= spt) { r -= spt; tile += gridDim.x; }
       s += 2;
-      if (s >= SA) { s -= SA; par ^= 1; }
+      while (s >= SA) { s -= SA; par ^= 1; }
     }
-  } else if (warp < 4) {
-    // ===== epilogue =====
+  } else if (warp < 4 || (warp >= 12 && warp < 16)) {
+    // ===== epilogue: warpgroup ew drains accumulator buffer ew (with one
+    // buffer, warpgroup 0 takes every tile) =====
+    const int ew = warp < 4 ? 0 : 1;
     const EpiParams& e = a.epi;
-    const int row = threadIdx.x;
+    const int row = threadIdx.x & 127;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     uint32_t acc_it = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++acc_it) {
       const int m_tile = tile % P.m_tiles, n_tile = tile / P.m_tiles;
       const uint32_t acc = NB == 2 ? (acc_it & 1) : 0;
       const uint32_t acc_ph = (NB == 2 ? (acc_it >> 1) : acc_it) & 1;
+      if ((int)acc != ew || (NB == 1 && ew == 1)) continue;
       if (lane == 0 && warp == 0) tr(P, 2, 0x700);
       ptx::mbar_wait_warp(ptx::smem_u32(&S->acc_full[acc]), acc_ph);
       if (lane == 0 && warp == 0) tr(P, 2, 0x800);
@@ -688,7 +731,14 @@ bool make_params(const ConvArgs& a, TcParams& P) {
   }
   if (!P.partials) return false;
   const uint32_t set_cols = P.concat ? P.partials * 2 * P.nt : (P.partials + 1) * P.nt;
-  const uint32_t need = P.acc_bufs * set_cols + P.a_stages * 64;
+  // two K-blocks per A stage halves the hand-offs (waits, fences, commits)
+  // per MMA when TMEM has room for at least two such stages
+  const int free_cols = 512 - P.acc_bufs * (int)set_cols;
+  P.ks = (!(P.dbg & 1024) && free_cols >= 2 * 128 && P.nkb > 1) ? 2 : 1;
+  P.a_stages = free_cols / (64 * P.ks);
+  if (P.a_stages > kMaxAStages) P.a_stages = kMaxAStages;
+  if (P.a_stages < 2) return false;
+  const uint32_t need = P.acc_bufs * set_cols + P.a_stages * 64 * P.ks;
   P.tmem_cols = need <= 128 ? 128 : (need <= 256 ? 256 : 512);
   return true;
 }

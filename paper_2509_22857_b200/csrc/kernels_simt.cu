@@ -10,26 +10,31 @@ namespace pcnn {
 // ingest: user NCHW float32 -> channel-blocked [B][nblk][H][W][cb], pad = 0
 // ---------------------------------------------------------------------------
 __global__ void ingest_kernel(const float* __restrict__ x, TensorView t, int batch) {
-  int64_t total = (int64_t)batch * t.nblk * t.h * t.w * t.cb;
+  // one thread per (image, 4-channel group, pixel); pixels fastest so the
+  // NCHW reads of each channel plane are coalesced, one float4 store each
+  const int64_t hw = (int64_t)t.h * t.w;
+  const int groups = t.cpad() / 4;
+  const int64_t total = (int64_t)batch * groups * hw;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    int ci = (int)(i % t.cb);
-    int64_t r = i / t.cb;
-    int xw = (int)(r % t.w); r /= t.w;
-    int yh = (int)(r % t.h); r /= t.h;
-    int blk = (int)(r % t.nblk);
-    int b = (int)(r / t.nblk);
-    int ch = blk * t.cb + ci;
-    float v = 0.f;
-    if (ch < t.c) v = __ldg(x + (((int64_t)b * t.c + ch) * t.h + yh) * t.w + xw);
-    t.base[i] = v;
+    const int64_t p = i % hw;
+    const int64_t r = i / hw;
+    const int g = (int)(r % groups), b = (int)(r / groups);
+    const int y = (int)(p / t.w), xw = (int)(p - (int64_t)y * t.w);
+    float v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int ch = g * 4 + j;
+      v[j] = ch < t.c ? __ldg(x + ((int64_t)b * t.c + ch) * hw + p) : 0.f;
+    }
+    *reinterpret_cast<float4*>(t.pix(b, g * 4, y, xw)) = make_float4(v[0], v[1], v[2], v[3]);
   }
 }
 
 void launch_ingest(const float* x, const TensorView& t, int batch, cudaStream_t s) {
-  int64_t total = (int64_t)batch * t.nblk * t.h * t.w * t.cb;
+  int64_t total = (int64_t)batch * (t.cpad() / 4) * t.h * t.w;
   int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-  ingest_kernel<<<blocks, 256, 0, s>>>(x, t, batch);
+  ingest_kernel<<<std::max(blocks, 1), 256, 0, s>>>(x, t, batch);
 }
 
 // ---------------------------------------------------------------------------
@@ -280,6 +285,23 @@ __global__ void eltwise_kernel(EltArgs a) {
     int g = (int)(r % groups);
     int b = (int)(r / groups);
     int ch0 = g * 4;
+    if (a.kind == PCNN_UNIT_LOCALPOOL) {
+      // window sum on 4-channel float4 groups (channels >= c are zero in the input)
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int dy = 0; dy < a.k; ++dy) {
+        const int iy = y * a.st - a.pad + dy;
+        if (iy < 0 || iy >= a.in.h) continue;
+        for (int dx = 0; dx < a.k; ++dx) {
+          const int ix = xw * a.st - a.pad + dx;
+          if (ix < 0 || ix >= a.in.w) continue;
+          const float4 v = __ldg(reinterpret_cast<const float4*>(a.in.pix(b, ch0, iy, ix)));
+          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+      }
+      const float dv = __ldg(a.p);
+      *reinterpret_cast<float4*>(o.pix(b, ch0, y, xw)) = make_float4(acc.x * dv, acc.y * dv, acc.z * dv, acc.w * dv);
+      continue;
+    }
     float res[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {

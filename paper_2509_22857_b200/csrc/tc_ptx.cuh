@@ -134,6 +134,52 @@ __device__ __forceinline__ void mma_tf32_ts_warp(uint32_t d_tmem, uint32_t a_tme
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// One K-block (four 8-deep K steps) of the N-concatenated 3xTF32 scheme in a
+// single asm statement, so every operand is moved to the uniform datapath
+// once per K-block instead of once per MMA:
+//   [main_k | corr_k] (+)= A_hi[k] * [B_hi | B_lo][k]   (N = 2*NT, idesc2)
+//   corr_k            +=  A_lo[k] * B_hi[k]             (N = NT,   idesc1)
+// d[k] = main accumulator of step k (corr at d[k] + corr_off); acc bit k of
+// `accm` says whether main_k accumulates; desc = hi image descriptor of the
+// K-block (+2 per step = +32 bytes).
+__device__ __forceinline__ void mma_kblock_concat(uint32_t d0, uint32_t d1, uint32_t d2, uint32_t d3,
+                                                  uint32_t corr_off, uint32_t a_hi, uint32_t a_lo,
+                                                  uint64_t desc, uint32_t idesc2, uint32_t idesc1,
+                                                  uint32_t accm) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred e, p, t;\n\t.reg .b32 r, dc, ah, al;\n\t.reg .b64 bd;\n\t"
+      "elect.sync r|e, 0xffffffff;\n\t"
+      "setp.eq.u32 t, 0, 0;\n\t"
+      // step 0
+      "and.b32 r, %11, 1;\n\tsetp.ne.u32 p, r, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%5], %7, %8, p;\n\t"
+      "add.u32 dc, %0, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [dc], [%6], %7, %9, t;\n\t"
+      // step 1
+      "and.b32 r, %11, 2;\n\tsetp.ne.u32 p, r, 0;\n\t"
+      "add.u32 ah, %5, 8;\n\tadd.u32 al, %6, 8;\n\tadd.s64 bd, %7, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [ah], bd, %8, p;\n\t"
+      "add.u32 dc, %1, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [dc], [al], bd, %9, t;\n\t"
+      // step 2
+      "and.b32 r, %11, 4;\n\tsetp.ne.u32 p, r, 0;\n\t"
+      "add.u32 ah, %5, 16;\n\tadd.u32 al, %6, 16;\n\tadd.s64 bd, %7, 4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%2], [ah], bd, %8, p;\n\t"
+      "add.u32 dc, %2, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [dc], [al], bd, %9, t;\n\t"
+      // step 3
+      "and.b32 r, %11, 8;\n\tsetp.ne.u32 p, r, 0;\n\t"
+      "add.u32 ah, %5, 24;\n\tadd.u32 al, %6, 24;\n\tadd.s64 bd, %7, 6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%3], [ah], bd, %8, p;\n\t"
+      "add.u32 dc, %3, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [dc], [al], bd, %9, t;\n\t"
+      "}\n" ::"r"(d0),
+      "r"(d1), "r"(d2), "r"(d3), "r"(corr_off), "r"(a_hi), "r"(a_lo), "l"(desc), "r"(idesc2), "r"(idesc1),
+      "r"(0), "r"(accm)
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_commit_warp(uint32_t bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\t"

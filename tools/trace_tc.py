@@ -5,24 +5,25 @@ import numpy as np, torch
 from paper_2509_22857_b200 import configs, _lib as L
 from paper_2509_22857_b200.runtime import Engine
 unit = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-g = configs.build("resnet20")
+g = configs.build(sys.argv[2] if len(sys.argv) > 2 else "resnet20")
 eng = Engine(g)
-x = torch.from_numpy(configs.make_input(configs.CONFIGS["resnet20"]).astype(np.float32)).cuda()
+cfgname = sys.argv[2] if len(sys.argv) > 2 else "resnet20"
+x = torch.from_numpy(configs.make_input(configs.CONFIGS[cfgname]).astype(np.float32)).cuda()
 out = eng.forward(x)
 lib = L.lib()
 fn = lib.pcnn_tc_trace
 fn.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
 buf = (ctypes.c_ulonglong * 65536)()
 for i in range(unit):
-    eng.forward_unit(256, i, x, out)
+    eng.forward_unit(x.shape[0], i, x, out)
 torch.cuda.synchronize()
 fn(buf, 65536)  # reset
-eng.forward_unit(256, unit, x, out)
+eng.forward_unit(x.shape[0], unit, x, out)
 torch.cuda.synchronize()
 n = fn(buf, 65536)
 ev = [(int(v) >> 48, int(v) & 0xFFFFFFFFFFFF) for v in buf[:n] if int(v)]
 t0 = min(t for _, t in ev)
-names = {10: "mma_k4", 1: "cv_wait", 2: "cv_go", 3: "cv_done", 4: "mma_wait", 5: "mma_go", 6: "mma_done", 7: "ep_wait", 8: "ep_go", 9: "ep_done"}
+names = {11: "cv_stwait", 10: "mma_k4", 1: "cv_lds", 2: "cv_go", 3: "cv_done", 4: "mma_wait", 5: "mma_go", 6: "mma_done", 7: "ep_wait", 8: "ep_go", 9: "ep_done"}
 ev.sort(key=lambda e: e[1])
 for tag, t in ev[:240]:
     print(f"{t - t0:8d} {names.get(tag >> 8, tag >> 8):9s} kb={tag & 0xff}")
