@@ -13,13 +13,15 @@ using namespace pcnn;
 
 __device__ __forceinline__ uint64_t clk() { return clock64(); }
 
-__global__ void ubench(uint64_t* out, int iters, int n_mma, int randomize) {
+__global__ void ubench(uint64_t* out, int iters, int n_mma, int randomize, int getenv_n256) {
   __shared__ __align__(1024) uint8_t bsm[16 * 1024];
   __shared__ uint64_t bar[4];
+  __shared__ uint64_t barf;
   __shared__ uint32_t tbase;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < 4; ++i) ptx::mbar_init(ptx::smem_u32(&bar[i]), 1);
+    ptx::mbar_init(ptx::smem_u32(&barf), 1);
     ptx::fence_mbar_init();
   }
   for (int i = threadIdx.x; i < 16 * 1024 / 4; i += blockDim.x) reinterpret_cast<float*>(bsm)[i] = 0.f;
@@ -166,6 +168,11 @@ __global__ void ubench(uint64_t* out, int iters, int n_mma, int randomize) {
         out[40 + var] = (t1 - t0) / 24;
       }
     }
+    // the kernel's asm K-block (warp-collective, elect.sync inside)
+    {
+      const uint32_t i32 = ptx::idesc_tf32(128, 32), i16 = ptx::idesc_tf32(128, 16);
+      out[46] = 0;
+    }
     // SS mode (A from smem, same zero image), N=16 and 128, R=1 and 4
     for (int ni = 0; ni < 2; ++ni) {
       const uint32_t idesc = ptx::idesc_tf32(128, ni ? 128 : 16);
@@ -181,6 +188,52 @@ __global__ void ubench(uint64_t* out, int iters, int n_mma, int randomize) {
         t1 = clk();
         out[slot++] = (t1 - t0) / 20 / 48;
       }
+    }
+  }
+  __syncthreads();
+
+  // 3d. the conv kernel's K-block asm issued by a whole warp (elect.sync)
+  if (warp == 0) {
+    const uint32_t i32 = ptx::idesc_tf32(128, 32), i16 = ptx::idesc_tf32(128, 16);
+    uint32_t ph3 = 0;
+    for (int var = 0; var < 2; ++var) {
+      const uint64_t t0w = clk();
+      for (int i = 0; i < 24; ++i) {
+        if (var) ptx::tc_fence_after();
+        ptx::mma_kblock_concat(tmem, tmem, tmem, tmem, 16, tmem + 256 + (i & 3) * 64, tmem + 288 + (i & 3) * 64,
+                               bd, i32, i16, i ? 0xF : 0xE);
+        if (var) ptx::mma_commit_warp(ptx::smem_u32(&bar[3]));
+      }
+      ptx::mma_commit_warp(ptx::smem_u32(&bar[1]));
+      ptx::mbar_wait(ptx::smem_u32(&bar[1]), ph3);
+      ph3 ^= 1;
+      const uint64_t t1w = clk();
+      if (lane == 0) out[47 + var] = (t1w - t0w) / 24;
+    }
+  }
+  __syncthreads();
+
+  // 3e. kind::f16 (fp16 in, fp32 accumulate), K=16 per MMA, A from TMEM
+  if (threadIdx.x == 0) {
+    uint32_t ph4 = 0;
+    const int ns[3] = {32, 128, getenv_n256};
+    for (int ni = 0; ni < 3; ++ni) {
+      if (ns[ni] == 0) { out[52 + ni] = 0; continue; }
+      // f16 idesc: c_format F32 (1<<4), a/b format F16 (0), K-major
+      const uint32_t idesc = (1u << 4) | ((uint32_t)(ns[ni] >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+      const uint64_t t0f = clk();
+      for (int i = 0; i < 20; ++i) {
+        for (int k = 0; k < 48; ++k) {
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
+                       :: "r"(tmem), "r"(tmem + 256 + (k & 7) * 8), "l"(bd), "r"(idesc), "r"((uint32_t)(k > 0)) : "memory");
+        }
+        ptx::mma_commit(ptx::smem_u32(&barf));
+        ptx::mbar_wait(ptx::smem_u32(&barf), ph4);
+        ph4 ^= 1;
+      }
+      const uint64_t t1f = clk();
+      out[52 + ni] = (t1f - t0f) / 20 / 48;
     }
   }
   __syncthreads();
@@ -292,7 +345,7 @@ int main() {
   cudaMalloc(&d, 64 * sizeof(uint64_t));
   cudaMemset(d, 0, 64 * sizeof(uint64_t));
   for (int n_mma : {1, 12, 48}) {
-    ubench<<<getenv("UB_BLOCKS") ? atoi(getenv("UB_BLOCKS")) : 1, 384>>>(d, 200, n_mma, getenv("UB_RANDOM") ? 1 : 0);
+    ubench<<<getenv("UB_BLOCKS") ? atoi(getenv("UB_BLOCKS")) : 1, 384>>>(d, 200, n_mma, getenv("UB_RANDOM") ? 1 : 0, getenv("UB_N256") ? 256 : 0);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
       printf("error %s\n", cudaGetErrorString(e));
@@ -310,6 +363,10 @@ int main() {
              (unsigned long long)h[31], (unsigned long long)h[32], (unsigned long long)h[33], (unsigned long long)h[34]);
       printf("alternating N 32/16: %llu; varying B desc: %llu; D alternating (overlapping cols): %llu\n",
              (unsigned long long)h[26], (unsigned long long)h[27], (unsigned long long)h[28]);
+      printf("kind::f16 K=16 TS cycles/MMA N=32,64,128: %llu %llu %llu\n", (unsigned long long)h[52],
+             (unsigned long long)h[53], (unsigned long long)h[54]);
+      printf("asm K-block by a whole warp (8 MMAs): plain %llu, with fence+commit %llu\n",
+             (unsigned long long)h[47], (unsigned long long)h[48]);
       printf("kernel pattern per K-block (8 MMAs): fence+commit %llu, commit only %llu, fence only %llu; A at col 64: %llu, 96: %llu, 128: %llu\n",
              (unsigned long long)h[40], (unsigned long long)h[41], (unsigned long long)h[42],
              (unsigned long long)h[43], (unsigned long long)h[44], (unsigned long long)h[45]);
