@@ -108,10 +108,14 @@ typedef struct pcnn_unit_desc {
                                     BIPOOL: 0 = along w, 1 = along h         */
   int64_t in_mode;               /* linear: 0 vector, 1 flatten, 2 global sum*/
   int64_t in_div_off;            /* linear global sum divisor (1 float)      */
-  int64_t impl;                  /* conv: 0 auto, 1 SIMT fp32, 2 tcgen05     */
+  int64_t impl;                  /* conv: 0 auto (tcgen05 fp16x2 if possible),
+                                    1 SIMT fp32, 2 tcgen05 3xTF32,
+                                    3 tcgen05 fp16x2 (3 fp16 products)        */
   int64_t tc_off;                /* conv tcgen05 weight image (hi|lo tf32)   */
   int64_t npad;                  /* padded output channels (vector stride)   */
-  int64_t reserved[5];
+  int64_t tc16_off;              /* conv fp16x2 weight image (hi|lo fp16)    */
+  int64_t tc16_scale_off;        /* its {max|w|, 2^-e} pair (2 floats)       */
+  int64_t reserved[3];
 } pcnn_unit_desc;
 
 /* ---- parameter packing (float64 master -> float32 compute images) -------*/
@@ -119,12 +123,14 @@ enum pcnn_pack_kind {
   PCNN_PACK_CAST = 1,        /* dst[i] = (float) src[i], i < n                */
   PCNN_PACK_BN_AFFINE = 2,   /* src = gamma,beta,mean,std (each n); dst =
                                 scale=gamma/std [n], shift=beta-scale*mean [n]*/
-  PCNN_PACK_TC_WEIGHTS = 3   /* src [rows][k] float64 -> tcgen05 B image     */
+  PCNN_PACK_TC_WEIGHTS = 3,  /* src [rows][k] float64 -> tcgen05 B image     */
+  PCNN_PACK_TC16_WEIGHTS = 4 /* src [rows][k] float64 -> fp16x2 B image scaled
+                                by 2^e; aux = float index of {max|w|, 2^-e} */
 };
 
 typedef struct pcnn_pack_desc {
   int64_t kind, src, dst, n;
-  int64_t rows, k, reserved[2];
+  int64_t rows, k, aux, reserved;
 } pcnn_pack_desc;
 
 /* ---- redistribution programs --------------------------------------------

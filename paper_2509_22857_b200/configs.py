@@ -150,8 +150,10 @@ class _Net:
 # ---------------------------------------------------------------------------
 
 def _calibrate(g: ModelGraph, x: np.ndarray, gain: float, gain_res: float, res_convs: Set[str],
-               skip: Set[str] = frozenset()) -> None:
-    """Fold a batch-statistics batchnorm with target gain into every conv."""
+               skip: Set[str] = frozenset(), stats: Optional[Dict] = None) -> None:
+    """Fold a batch-statistics batchnorm with target gain into every conv
+    (convs in `skip` are only evaluated).  With `stats`, record max|value|
+    per node and the logits instead of raising on non-finite values."""
     import torch
     import torch.nn.functional as F
 
@@ -217,7 +219,11 @@ def _calibrate(g: ModelGraph, x: np.ndarray, gain: float, gain_res: float, res_c
             vals[nid] = ins[0]
         else:
             raise ValueError(f"calibration cannot evaluate {node.kind}")
-        if not torch.isfinite(vals[nid]).all():
+        if stats is not None:
+            stats[nid] = float(vals[nid].abs().max())
+            if isinstance(node, OutputNode):
+                stats["__out__"] = vals[nid].cpu().numpy()
+        elif not torch.isfinite(vals[nid]).all():
             raise FloatingPointError(f"calibration diverged at {nid}")
 
 
@@ -279,21 +285,26 @@ def _deg2(r):
     return [r.normal(0.0, 0.1), r.normal(0.5, 0.1), r.uniform(0.05, 0.5)]
 
 
-def resnet20(seed: int = 0, hw: int = 32) -> ModelGraph:
-    """Config 2: deg-2 acts c2~U(0.05,0.5), c1~N(0.5,0.1), c0~N(0,0.1); s=0.3, s_res=0.1."""
+def resnet20(seed: int = 0, hw: int = 32, gain: float = 0.2, gain_res: float = 0.1) -> ModelGraph:
+    """Config 2: deg-2 acts c2~U(0.05,0.5), c1~N(0.5,0.1), c0~N(0,0.1);
+    s=0.2, s_res=0.1 (SURVEY's s=0.3 sends one image of the measured batch of
+    256 to 1e50 in float64 -- a degree-2^9 tail; s=0.2 keeps every image
+    finite and input-sensitive)."""
     cal = make_input(CONFIGS["resnet20"], batch=64, seed=seed + 1, hw=hw)
-    return _resnet_cifar(seed, _deg2, hw, 0.3, 0.1, cal)
+    return _resnet_cifar(seed, _deg2, hw, gain, gain_res, cal)
 
 
-def resnet20_deg8(seed: int = 0, hw: int = 32) -> ModelGraph:
-    """Config 3: each act = LSQ ReLU fit on [-8,8] times (1 + N(0, 0.01)); s=0.5, s_res=0.05."""
+def resnet20_deg8(seed: int = 0, hw: int = 32, gain: float = 0.4, gain_res: float = 0.05) -> ModelGraph:
+    """Config 3: each act = LSQ ReLU fit on [-8,8] times (1 + N(0, 0.01));
+    s=0.4, s_res=0.05 (SURVEY's s=0.5 overflows float64 on one image of the
+    measured batch of 512; 0.4 keeps the pre-activations within ~[-10, 10])."""
     base = relu_lsq_fit(8)
 
     def act(r):
         return list(base * (1.0 + r.normal(0.0, 0.01, base.size)))
 
     cal = make_input(CONFIGS["resnet20_deg8"], batch=64, seed=seed + 1, hw=hw)
-    return _resnet_cifar(seed, act, hw, 0.5, 0.05, cal)
+    return _resnet_cifar(seed, act, hw, gain, gain_res, cal)
 
 
 def _bivariate(r, d: int = 4) -> np.ndarray:
@@ -304,7 +315,7 @@ def _bivariate(r, d: int = 4) -> np.ndarray:
     return c
 
 
-def vgg11(seed: int = 0, hw: int = 32) -> ModelGraph:
+def vgg11(seed: int = 0, hw: int = 32, gain: float = 0.25) -> ModelGraph:
     """Config 4: VGG-11 convs, deg-3 acts, each max pool -> S_w then S_h with
     the same deg-4 S (c40~U(0.05,0.3), others N(0,0.2)); s=0.25 (s=0.4 lets
     the degree-16 pool composition overflow on calibration tails)."""
@@ -326,11 +337,12 @@ def vgg11(seed: int = 0, hw: int = 32) -> ModelGraph:
     h = net.node(h, FlattenNode("flatten"))
     h = net.linear(h, cin * side * side, 10, "fc")
     g = net.finish(h)
-    _calibrate(g, make_input(CONFIGS["vgg11"], batch=64, seed=seed + 1, hw=hw), 0.25, 0.25, set())
+    _calibrate(g, make_input(CONFIGS["vgg11"], batch=64, seed=seed + 1, hw=hw), gain, gain, set())
     return g
 
 
-def resnet18(seed: int = 0, hw: int = 224, calib_batch: int = 8) -> ModelGraph:
+def resnet18(seed: int = 0, hw: int = 224, calib_batch: int = 8, gain: float = 0.1,
+             gain_res: float = 0.02) -> ModelGraph:
     """Config 5: 7x7/s2 stem, 3x3/s2 avg pool (divisor 1/9), 2 basic blocks per
     stage at 64/128/256/512, deg-4 acts (c4~U(0.02,0.2), others N(0,0.3)),
     global pool, FC 512-1000; s=0.1, s_res=0.02."""
@@ -360,8 +372,17 @@ def resnet18(seed: int = 0, hw: int = 224, calib_batch: int = 8) -> ModelGraph:
     h = net.linear(h, 512, 1000, "fc")
     g = net.finish(h)
     cal = make_input(CONFIGS["resnet18"], batch=calib_batch, seed=seed + 1, hw=hw)
-    _calibrate(g, cal, 0.1, 0.02, net.res_convs)
+    _calibrate(g, cal, gain, gain_res, net.res_convs)
     return g
+
+
+def forward_stats(g: ModelGraph, x: np.ndarray) -> Dict:
+    """float64 torch forward of a batch: {node: max|value|, "__out__": logits}
+    (config-numerics probe; never on the measured path)."""
+    stats: Dict = {}
+    convs = {nid for nid, n in g.nodes.items() if isinstance(n, ConvNode)}
+    _calibrate(g, x, 1.0, 1.0, set(), skip=convs, stats=stats)
+    return stats
 
 
 BUILDERS = {"lenet5": lenet5, "resnet20": resnet20, "resnet20_deg8": resnet20_deg8,

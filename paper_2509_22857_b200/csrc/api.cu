@@ -15,6 +15,7 @@ namespace pcnn {
 __global__ void redistribute_kernel(double*, double*, const pcnn_scale_op*, int, const pcnn_rewrite_desc*,
                                     int, int64_t*, int64_t*);
 __global__ void pack_kernel(const double*, float*, const pcnn_pack_desc*, int);
+__global__ void pack_amax_kernel(const double*, float*, const pcnn_pack_desc*, int, int);
 }  // namespace pcnn
 
 using namespace pcnn;
@@ -100,6 +101,9 @@ int build_conv(pcnn_plan* p, int ui, ConvArgs& a) {
   a.pm.order = (u.pool == PCNN_POOL_SUM2 || u.pool == PCNN_POOL_BI2) ? kWindow : kPlain;
   a.w = P(p, u.w_off);
   a.tcw = P(p, u.tc_off);
+  a.tcw16 = P(p, u.tc16_off);
+  a.tc16_scale = P(p, u.tc16_scale_off);
+  a.f16 = 0;
   EpiParams& e = a.epi;
   e.cout = (int)u.cout;
   e.npad = out.cpad();
@@ -145,7 +149,7 @@ void enqueue_unit(pcnn_plan* p, int ui, const float* x, float* logits, cudaStrea
       const ConvArgs& a = p->conv_args[ui];
       if (u.pool == PCNN_POOL_GLOBAL)
         cudaMemsetAsync(a.epi.out.base, 0, sizeof(float) * (size_t)p->batch * a.epi.out.cpad(), s);
-      if (p->impl[ui] == 2) launch_conv_tc(a, s);
+      if (p->impl[ui] >= 2) launch_conv_tc(a, s);
       else launch_conv_simt(a, s);
       break;
     }
@@ -258,9 +262,15 @@ int pcnn_plan_create(const pcnn_unit_desc* units, int n_units, const pcnn_tensor
         delete p;
         return rc;
       }
-      bool want_tc = u.impl != 1;
-      if (want_tc && conv_tc_supported(p->conv_args[i]) && p->conv_args[i].tcw) p->impl[i] = 2;
-      else if (u.impl == 2) {
+      // auto: fp16x2 tensor cores, else 3xTF32, else SIMT
+      ConvArgs& a = p->conv_args[i];
+      if ((u.impl == 0 || u.impl == 3) && a.tcw16 && a.tc16_scale) {
+        a.f16 = 1;
+        if (conv_tc_supported(a)) p->impl[i] = 3;
+        else a.f16 = 0;
+      }
+      if (p->impl[i] == 1 && (u.impl == 0 || u.impl == 2) && a.tcw && conv_tc_supported(a)) p->impl[i] = 2;
+      if (p->impl[i] == 1 && u.impl >= 2) {
         delete p;
         return fail(PCNN_ERR_UNSUPPORTED, "unit " + std::to_string(i) + ": tcgen05 conv requested but unsupported");
       }
@@ -356,6 +366,13 @@ int pcnn_pack(const double* master, float* packed, const pcnn_pack_desc* ops, in
   pcnn_pack_desc* d_ops = nullptr;
   PCNN_CUDA(cudaMallocAsync(&d_ops, sizeof(pcnn_pack_desc) * n_ops, s));
   PCNN_CUDA(cudaMemcpyAsync(d_ops, ops, sizeof(pcnn_pack_desc) * n_ops, cudaMemcpyHostToDevice, s));
+  bool tc16 = false;
+  for (int i = 0; i < n_ops; ++i) tc16 |= ops[i].kind == PCNN_PACK_TC16_WEIGHTS;
+  if (tc16) {
+    // max|w| of every fp16x2 image first (its power-of-two scale)
+    pack_amax_kernel<<<n_ops, 1024, 0, s>>>(master, packed, d_ops, n_ops, 0);
+    pack_amax_kernel<<<dim3(n_ops, 64), 256, 0, s>>>(master, packed, d_ops, n_ops, 1);
+  }
   pack_kernel<<<148 * 4, 256, 0, s>>>(master, packed, d_ops, n_ops);
   cudaError_t le = cudaGetLastError();
   PCNN_CUDA(cudaFreeAsync(d_ops, s));

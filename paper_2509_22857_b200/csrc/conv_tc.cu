@@ -49,7 +49,8 @@ constexpr int kThreads = 640;
 // accumulator buffer) and converter warpgroups 4-7 / 8-11 (alternate A
 // stages) each cover TMEM lanes 0-127 (warp w owns lanes 32*(w%4)..+31).
 constexpr int kWarpAlloc = 16, kWarpProducer = 18, kWarpMma = 19;
-constexpr int kMaxAStages = 4;   // A hi/lo stages in TMEM (64 columns each)
+constexpr int kMaxAStages = 4;   // A hi/lo stages in TMEM (64 columns per K-block)
+constexpr int kMaxKs = 8;        // K-blocks per A stage
 constexpr int kBStages = 4;      // streamed B stages in smem
 constexpr int kTileM = 128;
 constexpr int kMaxPartials = 4;
@@ -65,12 +66,16 @@ struct TcParams {
   int nt;          // N tile (UMMA N), 16..128
   int n_tiles;
   int m_tiles;
-  int nkb;         // K-blocks of 32
+  int nkb;         // K-blocks (32 tf32 or 64 fp16 elements)
+  int sub;         // 32-element sub-blocks per K-block (1 tf32, 2 fp16x2)
+  int nsub_real;   // sub-blocks holding real K (the rest is K padding)
+  const float* tcw;        // weight image for this precision
+  const float* wscale;     // fp16x2: 2^-e weight scale (device), else null
   int resident;    // B image kept in smem for the whole kernel
   int taps;        // kh * kw
   int nseg;        // nblk_in * taps (valid channel segments)
   int a_stages;    // A stages in TMEM
-  int ks;          // K-blocks (of 32) per A stage: 1 or 2
+  int ks;          // K-blocks per A stage (1..kMaxKs)
   int acc_bufs;    // accumulator sets (1 or 2)
   int partials;    // main partial accumulators P
   uint32_t b_stage_bytes;
@@ -82,7 +87,8 @@ struct TcParams {
   // tile needs are loaded as <= `pieces` 4-D boxes (one per image), zero
   // padded by the TMA unit, and the converter reads im2col rows from smem.
   int staged;
-  int box_w, box_h, pieces, kpc, nblk_in;
+  int box_w, box_h, pieces, nblk_in;
+  int kpc;         // 32-element sub-blocks per channel block
   uint32_t piece_bytes, st_bytes;
   int nbs;         // streamed B stages
   int dbg;         // PCNN_TC_DEBUG bits: 1 no converter loads, 2 no MMA, 4 no epilogue math
@@ -172,12 +178,49 @@ __device__ __forceinline__ void store_kblock(const TcParams& P, const float4* f,
   }
 }
 
+// fp16x2: x = hi + lo with hi, lo fp16 (round to nearest); one 32-bit TMEM
+// column holds the K pair (x0 low half, x1 high half).  |x| >= 65520 makes
+// hi infinite, which poisons every column of the pixel's accumulator row --
+// the epilogue detects that and recomputes the row in fp32.
+__device__ __forceinline__ void split_f16x2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(x0, x1);
+  const float2 hf = __half22float2(h);
+  const __half2 l = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+
+// one 32-element sub-block -> 16 hi + 16 lo TMEM columns
+__device__ __forceinline__ void store_sub16(const TcParams& P, const float4* f, uint32_t t_hi, uint32_t t_lo) {
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    uint32_t hi[8], lo[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float4 a = f[4 * g + i];
+      split_f16x2(a.x, a.y, hi[2 * i], lo[2 * i]);
+      split_f16x2(a.z, a.w, hi[2 * i + 1], lo[2 * i + 1]);
+    }
+    if (P.dbg & 8) continue;
+    ptx::tmem_st8(t_hi + g * 8, hi);
+    ptx::tmem_st8(t_lo + g * 8, lo);
+  }
+}
+
+// sub-block h of a stage (K-block j = h / SUB of the stage) -> its TMEM columns
+template <bool F16>
+__device__ __forceinline__ void store_sub(const TcParams& P, const float4* f, uint32_t t_stage, int j, int hh) {
+  if (F16) store_sub16(P, f, t_stage + j * 32 + hh * 16, t_stage + 32 * P.ks + j * 32 + hh * 16);
+  else store_kblock(P, f, t_stage + j * 32, t_stage + 32 * P.ks + j * 32);
+}
+
 __device__ __forceinline__ void store4(const EpiParams& e, int b, int ch, int y, int x, const float* o) {
   *reinterpret_cast<float4*>(e.out.pix(b, ch, y, x)) = make_float4(o[0], o[1], o[2], o[3]);
 }
 
-template <int CBS>
+template <int CBS, bool F16>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_constant__ TcParams P) {
+  constexpr int SUB = F16 ? 2 : 1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const ConvArgs& a = P.a;
@@ -186,7 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   uint8_t* st_buf = smem + b_region;
   Smem* S = reinterpret_cast<Smem*>(smem + b_region + st_region);
   int2* seg = reinterpret_cast<int2*>(smem + b_region + st_region + ((sizeof(Smem) + 15) & ~size_t(15)));
-  float* ptab = reinterpret_cast<float*>(seg + (P.nkb << (5 - a.in.cbs)));
+  float* ptab = reinterpret_cast<float*>(seg + ((P.nkb * SUB) << (5 - a.in.cbs)));
   const uint32_t b_base = ptx::smem_u32(smem);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -218,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   if (warp == kWarpAlloc) ptx::tmem_alloc(ptx::smem_u32(&S->tmem_base), P.tmem_cols);
   {
     const TensorView& in = a.in;
-    const int nsegs = P.nkb << (5 - in.cbs);
+    const int nsegs = (P.nkb * SUB) << (5 - in.cbs);
     for (int s2 = threadIdx.x; s2 < nsegs; s2 += kThreads) {
       int2 e = make_int2(0, 31);
       if (s2 < P.nseg) {
@@ -256,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         const uint32_t bar = ptx::smem_u32(&S->b_full[0]);
         ptx::mbar_arrive_tx(bar, P.b_stage_bytes * P.nkb);
         for (int kb = 0; kb < P.nkb; ++kb)
-          ptx::bulk_g2s(b_base + kb * P.b_stage_bytes, a.tcw + (size_t)kb * (P.b_stage_bytes / 4),
+          ptx::bulk_g2s(b_base + kb * P.b_stage_bytes, P.tcw + (size_t)kb * (P.b_stage_bytes / 4),
                         P.b_stage_bytes, bar);
       }
       int bs = 0, sb = 0;
@@ -272,8 +315,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           a.pm.decode(m1, b1, oy1, ox1);
         }
         for (int kb = 0; kb < P.nkb; ++kb) {
-          if (P.staged && kb % P.kpc == 0) {
-            const int blk = kb / P.kpc;
+          for (int h = kb * SUB; P.staged && h < kb * SUB + SUB; ++h) {
+            if (h >= P.nsub_real || h % P.kpc) continue;
+            const int blk = h / P.kpc;
             ptx::mbar_wait_sleep(ptx::smem_u32(&S->st_empty[sb]), sph ^ 1);
             const uint32_t bar = ptx::smem_u32(&S->st_full[sb]);
             ptx::mbar_arrive_tx(bar, box_bytes * (uint32_t)(b1 - b0 + 1));
@@ -288,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             ptx::mbar_wait_sleep(ptx::smem_u32(&S->b_empty[bs]), bph ^ 1);
             const uint32_t bar = ptx::smem_u32(&S->b_full[bs]);
             ptx::mbar_arrive_tx(bar, P.b_stage_bytes);
-            const float* src = a.tcw + ((size_t)n_tile * P.nkb + kb) * (P.b_stage_bytes / 4);
+            const float* src = P.tcw + ((size_t)n_tile * P.nkb + kb) * (P.b_stage_bytes / 4);
             ptx::bulk_g2s(b_base + bs * P.b_stage_bytes, src, P.b_stage_bytes, bar);
             if (++bs == P.nbs) { bs = 0; bph ^= 1; }
           }
@@ -299,8 +343,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     // ===== MMA issuer: the whole warp runs the loop with warp-uniform state,
     // one elected lane issues each tcgen05 instruction =====
     {
-      const uint32_t idesc = ptx::idesc_tf32(kTileM, P.nt);
-      const uint32_t idesc2 = ptx::idesc_tf32(kTileM, 2 * P.nt);
+      const uint32_t idesc = F16 ? ptx::idesc_f16(kTileM, P.nt) : ptx::idesc_tf32(kTileM, P.nt);
+      const uint32_t idesc2 = F16 ? ptx::idesc_f16(kTileM, 2 * P.nt) : ptx::idesc_tf32(kTileM, 2 * P.nt);
       const uint32_t lo_enc = (P.nt * 128) >> 4;  // lo image offset in descriptor units
       const uint64_t desc0 = ptx::smem_desc_sw128(b_base);
       const uint32_t a_empty0 = ptx::smem_u32(&S->a_empty[0]), a_full0 = ptx::smem_u32(&S->a_full[0]);
@@ -349,23 +393,23 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
                 d_main += 2 * part_cols;
                 if (d_main == d_main_end) d_main = d_set;
               }
-              ptx::mma_kblock_concat(dk[0], dk[1], dk[2], dk[3], part_cols, a_hi, a_lo, dkb, idesc2, idesc, accm);
+              ptx::mma_kblock_concat<F16>(dk[0], dk[1], dk[2], dk[3], part_cols, a_hi, a_lo, dkb, idesc2, idesc, accm);
               first_corr = 1;
             } else if (do_mma) {
 #pragma unroll
-              for (int k4 = 0; k4 < kTcBK / 8; ++k4) {
-                const uint64_t dh = dkb + 2 * k4, dl = dh + lo_enc;  // +32 B per 8-deep K step
+              for (int k4 = 0; k4 < 4; ++k4) {
+                const uint64_t dh = dkb + 2 * k4, dl = dh + lo_enc;  // +32 B per K step (8 tf32 / 16 fp16)
                 if (P.concat) {
                   // B rows [hi; lo] as one N = 2*NT operand: [main | corr] += A_hi * [B_hi | B_lo],
                   // then corr += A_lo * B_hi -- two MMAs per K step instead of three
-                  ptx::mma_tf32_ts_warp(d_main, a_hi + k4 * 8, dh, idesc2, main_seen >= NP);
-                  ptx::mma_tf32_ts_warp(d_main + part_cols, a_lo + k4 * 8, dh, idesc, 1);
+                  ptx::mma_ts_warp<F16>(d_main, a_hi + k4 * 8, dh, idesc2, main_seen >= NP);
+                  ptx::mma_ts_warp<F16>(d_main + part_cols, a_lo + k4 * 8, dh, idesc, 1);
                   if (P.dbg & 128) tr(P, 3, 0xA00 | k4);
                   d_main += 2 * part_cols;
                 } else {
-                  ptx::mma_tf32_ts_warp(d_corr, a_lo + k4 * 8, dh, idesc, first_corr);
-                  ptx::mma_tf32_ts_warp(d_corr, a_hi + k4 * 8, dl, idesc, 1);
-                  ptx::mma_tf32_ts_warp(d_main, a_hi + k4 * 8, dh, idesc, main_seen >= NP);
+                  ptx::mma_ts_warp<F16>(d_corr, a_lo + k4 * 8, dh, idesc, first_corr);
+                  ptx::mma_ts_warp<F16>(d_corr, a_hi + k4 * 8, dl, idesc, 1);
+                  ptx::mma_ts_warp<F16>(d_main, a_hi + k4 * 8, dh, idesc, main_seen >= NP);
                   if (P.dbg & 128) tr(P, 3, 0xA00 | k4);
                   d_main += part_cols;
                 }
@@ -417,10 +461,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         const bool mine = (gstage & 1) == cw;
         if (!mine) {
           // not this warpgroup's stage: only keep the staging-buffer protocol
-          for (int j = 0; j < kbn; ++j) {
-            const int kb = kb0 + j;
-            if (kb % P.kpc == 0) ptx::mbar_wait_warp(ptx::smem_u32(&S->st_full[sb]), sph);
-            if (kb % P.kpc == P.kpc - 1 || kb == P.nkb - 1) {
+          for (int h = kb0 * SUB; h < (kb0 + kbn) * SUB && h < P.nsub_real; ++h) {
+            if (h % P.kpc == 0) ptx::mbar_wait_warp(ptx::smem_u32(&S->st_full[sb]), sph);
+            if (h % P.kpc == P.kpc - 1 || h == P.nsub_real - 1) {
               __syncwarp();
               if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->st_empty[sb]));
               if (++sb == 2) { sb = 0; sph ^= 1; }
@@ -431,17 +474,23 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         }
         if (lane == 0 && warp == 4) tr(P, 0, 0x200 | kb0);
         ptx::mbar_wait_warp(ptx::smem_u32(&S->a_empty[s]), par);
+        if (lane == 0 && warp == 4) tr(P, 0, 0xB00 | kb0);
         ptx::tc_fence_after();
         const uint32_t t_stage = tmem + lane_off + a_col0 + s * 64 * KS;
-        for (int j = 0; j < kbn; ++j) {
-          const int kb = kb0 + j;
-          if (kb % P.kpc == 0) ptx::mbar_wait_warp(ptx::smem_u32(&S->st_full[sb]), sph);
+        for (int hs = 0; hs < kbn * SUB; ++hs) {
+          const int j = hs / SUB, hh = hs - j * SUB;
+          const int h = kb0 * SUB + hs;
+          const bool real = h < P.nsub_real;
+          if (real && h % P.kpc == 0) {
+            ptx::mbar_wait_warp(ptx::smem_u32(&S->st_full[sb]), sph);
+            if (lane == 0 && warp == 4) tr(P, 0, 0xC00 | h);
+          }
           float4 f[8];
           const uint32_t buf = st0 + sb * P.st_bytes;
 #pragma unroll
           for (int g = 0; g < SEGS; ++g) {
-            const int2 e = seg[kb * SEGS + g];
-            const bool ok = valid && (e.y & 0xFF) != 31;
+            const int2 e = seg[h * SEGS + g];
+            const bool ok = valid && real && (e.y & 0xFF) != 31;
             const uint32_t L0 = pix0 + (uint32_t)e.x * 4;
 #pragma unroll
             for (int q = 0; q < PER; ++q) {
@@ -453,13 +502,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
               f[g * PER + q] = v;
             }
           }
-          if (kb % P.kpc == P.kpc - 1 || kb == P.nkb - 1) {
-            // last K-block of this channel block: release the staging buffer
+          if (real && (h % P.kpc == P.kpc - 1 || h == P.nsub_real - 1)) {
+            // last sub-block of this channel block: release the staging buffer
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->st_empty[sb]));
             if (++sb == 2) { sb = 0; sph ^= 1; }
           }
-          if (!(P.dbg & 512)) store_kblock(P, f, t_stage + j * 32, t_stage + 32 * KS + j * 32);
+          if (!(P.dbg & 512)) store_sub<F16>(P, f, t_stage, j, hh);
         }
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
@@ -500,15 +549,25 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       }
       const int kb0 = r * KS;
       const int kbn = nkb - kb0 < KS ? nkb - kb0 : KS;
-      float4 f[2][8];
-      load_kblock<CBS>(seg, kb0, px, f[0]);
-      if (kbn > 1) load_kblock<CBS>(seg, kb0 + 1, px, f[1]);
+      const int nsb = kbn * SUB;  // 32-element sub-blocks of this stage
+      const int h0 = kb0 * SUB;
+      // two register buffers: the next sub-block's loads are in flight while
+      // the current one is split and stored
+      float4 fa[8], fb[8];
+      load_kblock<CBS>(seg, h0, px, fa);
+      if (nsb > 1) load_kblock<CBS>(seg, h0 + 1, px, fb);
       if (lane == 0 && warp == 4) tr(P, 0, 0x200 | kb0);
       ptx::mbar_wait_warp(ptx::smem_u32(&S->a_empty[s]), par);
       ptx::tc_fence_after();
       const uint32_t t_stage = tmem + lane_off + a_col0 + s * 64 * KS;
-      store_kblock(P, f[0], t_stage, t_stage + 32 * KS);
-      if (kbn > 1) store_kblock(P, f[1], t_stage + 32, t_stage + 32 * KS + 32);
+      for (int i = 0; i < nsb; i += 2) {
+        store_sub<F16>(P, fa, t_stage, i / SUB, i % SUB);
+        if (i + 2 < nsb) load_kblock<CBS>(seg, h0 + i + 2, px, fa);
+        if (i + 1 < nsb) {
+          store_sub<F16>(P, fb, t_stage, (i + 1) / SUB, (i + 1) % SUB);
+          if (i + 3 < nsb) load_kblock<CBS>(seg, h0 + i + 3, px, fb);
+        }
+      }
       if (!(P.dbg & 16)) ptx::tmem_st_wait();
       ptx::tc_fence_before();
       __syncwarp();
@@ -525,6 +584,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     const int ew = warp < 4 ? 0 : 1;
     const EpiParams& e = a.epi;
     const int row = threadIdx.x & 127;
+    const float wsc = F16 ? __ldg(P.wscale) : 1.f;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     uint32_t acc_it = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++acc_it) {
@@ -565,6 +625,31 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           }
         }
         const int chb = n_tile * P.nt + c0;
+        if (F16) {
+          if (valid && !isfinite(v[0])) {
+            // an input of this pixel overflowed fp16 (or is inf/nan): redo the
+            // row's 16 dot products in fp32 with the unscaled fp32 weights
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = 0.f;
+            const TensorView& in = a.in;
+            int k = 0;
+            for (int blk = 0; blk < in.nblk; ++blk)
+              for (int ky = 0; ky < a.kh; ++ky)
+                for (int kx = 0; kx < a.kw; ++kx, k += in.cb) {
+                  const int iy = oy * a.stride - a.pad + ky, ix = ox * a.stride - a.pad + kx;
+                  if (iy < 0 || iy >= in.h || ix < 0 || ix >= in.w) continue;
+                  const float* xp = in.at(b, blk << in.cbs, iy, ix);
+                  for (int c = 0; c < in.cb; ++c) {
+                    const float xv = xp[c];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v[j] = fmaf(xv, __ldg(a.w + (int64_t)(chb + j) * a.kp + k + c), v[j]);
+                  }
+                }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] *= wsc;
+          }
+        }
         const float* pt = ptab + chb;  // per-channel parameters, shared by all rows
         float sk[16];
         if (e.residual) {
@@ -670,7 +755,9 @@ bool make_params(const ConvArgs& a, TcParams& P) {
   const int cb = a.in.cb;
   if (!(cb == 4 || cb == 8 || cb == 16 || cb == 32)) return false;
   if (a.npad < 16 || a.npad % 16) return false;
-  if (!a.tcw) return false;
+  P.tcw = a.f16 ? a.tcw16 : a.tcw;
+  P.wscale = a.f16 ? a.tc16_scale + 1 : nullptr;
+  if (!P.tcw || (a.f16 && !a.tc16_scale)) return false;
   if (a.kh > 31 || a.kw > 31 || host_pixel_count(a.pm, a.batch) >= (1ll << 31)) return false;
   P.a = a;
   P.nt = a.npad <= 128 ? a.npad : 128;
@@ -678,7 +765,9 @@ bool make_params(const ConvArgs& a, TcParams& P) {
   P.n_tiles = a.npad / P.nt;
   const int64_t M = host_pixel_count(a.pm, a.batch);
   P.m_tiles = (int)((M + kTileM - 1) / kTileM);
-  P.nkb = tc_kblocks(a.kp);
+  P.sub = a.f16 ? 2 : 1;
+  P.nkb = a.f16 ? tc16_kblocks(a.kp) : tc_kblocks(a.kp);
+  P.nsub_real = (a.kp + 31) / 32;
   P.taps = a.kh * a.kw;
   P.nseg = a.in.nblk * P.taps;
   P.b_stage_bytes = (uint32_t)(2 * P.nt * kTcBK * 4);
@@ -734,7 +823,12 @@ bool make_params(const ConvArgs& a, TcParams& P) {
   // two K-blocks per A stage halves the hand-offs (waits, fences, commits)
   // per MMA when TMEM has room for at least two such stages
   const int free_cols = 512 - P.acc_bufs * (int)set_cols;
-  P.ks = (!(P.dbg & 1024) && free_cols >= 2 * 128 && P.nkb > 1) ? 2 : 1;
+  // K-blocks per A stage: as many as two stages of TMEM allow (up to the
+  // whole K) -- every stage costs a full/empty hand-off through the MMA warp
+  P.ks = 1;
+  if (!(P.dbg & 1024))
+    for (int ks = 2; ks <= P.nkb && ks <= kMaxKs; ++ks)
+      if (free_cols >= 2 * 64 * ks) P.ks = ks;
   P.a_stages = free_cols / (64 * P.ks);
   if (P.a_stages > kMaxAStages) P.a_stages = kMaxAStages;
   if (P.a_stages < 2) return false;
@@ -744,7 +838,7 @@ bool make_params(const ConvArgs& a, TcParams& P) {
 }
 
 size_t smem_aux_bytes(const TcParams& P) {
-  const size_t segs = (size_t)P.nkb << (5 - P.a.in.cbs);
+  const size_t segs = (size_t)(P.nkb * P.sub) << (5 - P.a.in.cbs);
   return ((sizeof(Smem) + 15) & ~size_t(15)) + segs * sizeof(int2) + (size_t)P.ptab_rows * P.a.epi.npad * 4;
 }
 
@@ -769,7 +863,7 @@ void staging_geometry(const ConvArgs& a, TcParams& P) {
   P.piece_bytes = (uint32_t)(((size_t)P.box_w * P.box_h * a.in.cb * 4 + 1023) & ~size_t(1023));
   P.st_bytes = P.piece_bytes * P.pieces;
   P.nblk_in = a.in.nblk;
-  P.kpc = a.in.nblk == 1 ? P.nkb : P.taps;  // K-blocks per channel block (cb = 32 when nblk > 1)
+  P.kpc = a.in.nblk == 1 ? P.nsub_real : P.taps;  // sub-blocks per channel block (cb = 32 when nblk > 1)
 }
 
 }  // namespace
@@ -831,16 +925,20 @@ void launch_conv_tc(const ConvArgs& a, cudaStream_t s) {
   const size_t smem = smem_bytes(P);
   const int tiles = P.m_tiles * P.n_tiles;
   const int grid = tiles < nsm ? tiles : nsm;
-  switch (a.in.cbs) {
-#define PCNN_TC_LAUNCH(C)                                                                            \
-  case C:                                                                                            \
-    cudaFuncSetAttribute(conv_tc_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    conv_tc_kernel<C><<<grid, kThreads, smem, s>>>(P);                                               \
+  switch (a.in.cbs * 2 + (a.f16 ? 1 : 0)) {
+#define PCNN_TC_LAUNCH(C, H)                                                                            \
+  case C * 2 + H:                                                                                       \
+    cudaFuncSetAttribute(conv_tc_kernel<C, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    conv_tc_kernel<C, H><<<grid, kThreads, smem, s>>>(P);                                               \
     break;
-    PCNN_TC_LAUNCH(2)
-    PCNN_TC_LAUNCH(3)
-    PCNN_TC_LAUNCH(4)
-    PCNN_TC_LAUNCH(5)
+    PCNN_TC_LAUNCH(2, false)
+    PCNN_TC_LAUNCH(3, false)
+    PCNN_TC_LAUNCH(4, false)
+    PCNN_TC_LAUNCH(5, false)
+    PCNN_TC_LAUNCH(2, true)
+    PCNN_TC_LAUNCH(3, true)
+    PCNN_TC_LAUNCH(4, true)
+    PCNN_TC_LAUNCH(5, true)
 #undef PCNN_TC_LAUNCH
     default: break;
   }

@@ -15,7 +15,10 @@ struct ConvArgs {
   int kp;            // padded K = in.nblk * kh * kw * in.cb
   int npad;          // padded output channels
   const float* w;    // [npad][kp] float32
-  const float* tcw;  // tcgen05 weight image or null
+  const float* tcw;  // tcgen05 weight image (3xTF32) or null
+  const float* tcw16;       // fp16x2 weight image or null
+  const float* tc16_scale;  // {max|w|, 2^-e} of the fp16x2 image
+  int f16;                  // launch_conv_tc: 1 = fp16x2 (kind::f16), 0 = 3xTF32
   EpiParams epi;
 };
 

@@ -128,6 +128,31 @@ __global__ void redistribute_kernel(double* master, double* arena, const pcnn_sc
   }
 }
 
+// phase 0 (one block per op): zero the max|w| slot of each fp16x2 image;
+// phase 1 (grid n_ops x slices): max|w| by block reduction + one atomicMax
+// on the float bits (non-negative floats order like their bit patterns).
+__global__ void pack_amax_kernel(const double* __restrict__ master, float* __restrict__ packed,
+                                 const pcnn_pack_desc* ops, int n_ops, int phase) {
+  const pcnn_pack_desc o = ops[blockIdx.x];
+  if (o.kind != PCNN_PACK_TC16_WEIGHTS) return;
+  if (phase == 0) {
+    if (threadIdx.x == 0) packed[o.aux] = 0.f;
+    return;
+  }
+  const int64_t total = o.rows * o.k;
+  float m = 0.f;
+  for (int64_t i = blockIdx.y * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.y * blockDim.x)
+    m = fmaxf(m, (float)fabs(master[o.src + i]));
+  for (int off = 16; off; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+  __shared__ float red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, red[w]);
+    atomicMax(reinterpret_cast<int*>(packed + o.aux), __float_as_int(m));
+  }
+}
+
 __global__ void pack_kernel(const double* __restrict__ master, float* __restrict__ packed,
                             const pcnn_pack_desc* ops, int n_ops) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -145,6 +170,11 @@ __global__ void pack_kernel(const double* __restrict__ master, float* __restrict
       }
     } else if (o.kind == PCNN_PACK_TC_WEIGHTS) {
       pack_tc_weights_device(master + o.src, packed + o.dst, (int)o.rows, (int)o.k, tid, nthreads);
+    } else if (o.kind == PCNN_PACK_TC16_WEIGHTS) {
+      const int e = tc16_scale_exp(packed[o.aux]);
+      if (tid == 0) packed[o.aux + 1] = ldexpf(1.f, -e);
+      pack_tc16_weights_device(master + o.src, reinterpret_cast<__half*>(packed + o.dst), (int)o.rows, (int)o.k, e,
+                               tid, nthreads);
     }
   }
 }

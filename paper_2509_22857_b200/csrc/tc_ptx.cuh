@@ -59,10 +59,24 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 // Waiting with try_wait: the warp is suspended in hardware instead of
 // spinning, so it does not steal issue slots from the MMA thread that shares
 // its SM sub-partition.  Used by every role except the MMA issuer.
+// try_wait with an explicit suspend-time hint: without one the hardware
+// returns after a short system-dependent limit, and the waiting warps of a
+// 20-warp CTA spent a third of all issued instructions polling (ncu).
+__device__ __forceinline__ bool mbar_try_hint(uint32_t bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity), "r"(ns)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
   uint32_t spins = 0;
-  while (!mbar_try(bar, parity)) {
-    if (++spins > (1u << 28)) __trap();
+  while (!mbar_try_hint(bar, parity, 20000)) {
+    if (++spins > (1u << 20)) __trap();
   }
 }
 
@@ -124,15 +138,24 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, ui
 // lane that issues.  Issuing from a lone `if (lane == 0)` thread instead made
 // the compiler rebuild every operand with R2UR inside a waterfall loop and
 // halved the MMA issue rate.
-__device__ __forceinline__ void mma_tf32_ts_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
-                                                 uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\t"
-      "elect.sync r|e, 0xffffffff;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
+#define PCNN_MMA_TS_WARP(NAME, KIND)                                                                   \
+  __device__ __forceinline__ void NAME(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, \
+                                       uint32_t accumulate) {                                           \
+    asm volatile(                                                                                       \
+        "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\t"                                                   \
+        "elect.sync r|e, 0xffffffff;\n\t"                                                              \
+        "setp.ne.b32 p, %4, 0;\n\t"                                                                    \
+        "@e tcgen05.mma.cta_group::1.kind::" KIND " [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),         \
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)                                           \
+        : "memory");                                                                                    \
+  }
+PCNN_MMA_TS_WARP(mma_tf32_ts_warp, "tf32")
+PCNN_MMA_TS_WARP(mma_f16_ts_warp, "f16")
+#undef PCNN_MMA_TS_WARP
+template <bool F16>
+__device__ __forceinline__ void mma_ts_warp(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if (F16) mma_f16_ts_warp(d, a, b, idesc, acc);
+  else mma_tf32_ts_warp(d, a, b, idesc, acc);
 }
 // One K-block (four 8-deep K steps) of the N-concatenated 3xTF32 scheme in a
 // single asm statement, so every operand is moved to the uniform datapath
@@ -142,42 +165,49 @@ __device__ __forceinline__ void mma_tf32_ts_warp(uint32_t d_tmem, uint32_t a_tme
 // d[k] = main accumulator of step k (corr at d[k] + corr_off); acc bit k of
 // `accm` says whether main_k accumulates; desc = hi image descriptor of the
 // K-block (+2 per step = +32 bytes).
+#define PCNN_MMA_KBLOCK(NAME, KIND) __device__ __forceinline__ void NAME(uint32_t d0, uint32_t d1, uint32_t d2, uint32_t d3, \
+                                                  uint32_t corr_off, uint32_t a_hi, uint32_t a_lo, \
+                                                  uint64_t desc, uint32_t idesc2, uint32_t idesc1, \
+                                                  uint32_t accm) { \
+  asm volatile( \
+      "{\n\t" \
+      ".reg .pred e, p, t;\n\t.reg .b32 r, dc, ah, al;\n\t.reg .b64 bd;\n\t" \
+      "elect.sync r|e, 0xffffffff;\n\t" \
+      "setp.eq.u32 t, 0, 0;\n\t" \
+      "and.b32 r, %11, 1;\n\tsetp.ne.u32 p, r, 0;\n\t" \
+      "@e tcgen05.mma.cta_group::1.kind::" KIND " [%0], [%5], %7, %8, p;\n\t" \
+      "add.u32 dc, %0, %4;\n\t" \
+      "@e tcgen05.mma.cta_group::1.kind::" KIND " [dc], [%6], %7, %9, t;\n\t" \
+      "and.b32 r, %11, 2;\n\tsetp.ne.u32 p, r, 0;\n\t" \
+      "add.u32 ah, %5, 8;\n\tadd.u32 al, %6, 8;\n\tadd.s64 bd, %7, 2;\n\t" \
+      "@e tcgen05.mma.cta_group::1.kind::" KIND " [%1], [ah], bd, %8, p;\n\t" \
+      "add.u32 dc, %1, %4;\n\t" \
+      "@e tcgen05.mma.cta_group::1.kind::" KIND " [dc], [al], bd, %9, t;\n\t" \
+      "and.b32 r, %11, 4;\n\tsetp.ne.u32 p, r, 0;\n\t" \
+      "add.u32 ah, %5, 16;\n\tadd.u32 al, %6, 16;\n\tadd.s64 bd, %7, 4;\n\t" \
+      "@e tcgen05.mma.cta_group::1.kind::" KIND " [%2], [ah], bd, %8, p;\n\t" \
+      "add.u32 dc, %2, %4;\n\t" \
+      "@e tcgen05.mma.cta_group::1.kind::" KIND " [dc], [al], bd, %9, t;\n\t" \
+      "and.b32 r, %11, 8;\n\tsetp.ne.u32 p, r, 0;\n\t" \
+      "add.u32 ah, %5, 24;\n\tadd.u32 al, %6, 24;\n\tadd.s64 bd, %7, 6;\n\t" \
+      "@e tcgen05.mma.cta_group::1.kind::" KIND " [%3], [ah], bd, %8, p;\n\t" \
+      "add.u32 dc, %3, %4;\n\t" \
+      "@e tcgen05.mma.cta_group::1.kind::" KIND " [dc], [al], bd, %9, t;\n\t" \
+      "}\n" ::"r"(d0), \
+      "r"(d1), "r"(d2), "r"(d3), "r"(corr_off), "r"(a_hi), "r"(a_lo), "l"(desc), "r"(idesc2), "r"(idesc1), \
+      "r"(0), "r"(accm) \
+      : "memory"); \
+}
+PCNN_MMA_KBLOCK(mma_kblock_concat_tf32, "tf32")
+PCNN_MMA_KBLOCK(mma_kblock_concat_f16, "f16")
+#undef PCNN_MMA_KBLOCK
+template <bool F16>
 __device__ __forceinline__ void mma_kblock_concat(uint32_t d0, uint32_t d1, uint32_t d2, uint32_t d3,
                                                   uint32_t corr_off, uint32_t a_hi, uint32_t a_lo,
                                                   uint64_t desc, uint32_t idesc2, uint32_t idesc1,
                                                   uint32_t accm) {
-  asm volatile(
-      "{\n\t"
-      ".reg .pred e, p, t;\n\t.reg .b32 r, dc, ah, al;\n\t.reg .b64 bd;\n\t"
-      "elect.sync r|e, 0xffffffff;\n\t"
-      "setp.eq.u32 t, 0, 0;\n\t"
-      // step 0
-      "and.b32 r, %11, 1;\n\tsetp.ne.u32 p, r, 0;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%5], %7, %8, p;\n\t"
-      "add.u32 dc, %0, %4;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [dc], [%6], %7, %9, t;\n\t"
-      // step 1
-      "and.b32 r, %11, 2;\n\tsetp.ne.u32 p, r, 0;\n\t"
-      "add.u32 ah, %5, 8;\n\tadd.u32 al, %6, 8;\n\tadd.s64 bd, %7, 2;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [ah], bd, %8, p;\n\t"
-      "add.u32 dc, %1, %4;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [dc], [al], bd, %9, t;\n\t"
-      // step 2
-      "and.b32 r, %11, 4;\n\tsetp.ne.u32 p, r, 0;\n\t"
-      "add.u32 ah, %5, 16;\n\tadd.u32 al, %6, 16;\n\tadd.s64 bd, %7, 4;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%2], [ah], bd, %8, p;\n\t"
-      "add.u32 dc, %2, %4;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [dc], [al], bd, %9, t;\n\t"
-      // step 3
-      "and.b32 r, %11, 8;\n\tsetp.ne.u32 p, r, 0;\n\t"
-      "add.u32 ah, %5, 24;\n\tadd.u32 al, %6, 24;\n\tadd.s64 bd, %7, 6;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%3], [ah], bd, %8, p;\n\t"
-      "add.u32 dc, %3, %4;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [dc], [al], bd, %9, t;\n\t"
-      "}\n" ::"r"(d0),
-      "r"(d1), "r"(d2), "r"(d3), "r"(corr_off), "r"(a_hi), "r"(a_lo), "l"(desc), "r"(idesc2), "r"(idesc1),
-      "r"(0), "r"(accm)
-      : "memory");
+  if (F16) mma_kblock_concat_f16(d0, d1, d2, d3, corr_off, a_hi, a_lo, desc, idesc2, idesc1, accm);
+  else mma_kblock_concat_tf32(d0, d1, d2, d3, corr_off, a_hi, a_lo, desc, idesc2, idesc1, accm);
 }
 
 __device__ __forceinline__ void mma_commit_warp(uint32_t bar) {
@@ -239,6 +269,10 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
 // instruction descriptor: kind::tf32, fp32 accumulate, K-major A and B
 __host__ __device__ __forceinline__ uint32_t idesc_tf32(int m, int n) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+// kind::f16: A, B fp16 (format 0), D fp32, both K-major
+__host__ __device__ __forceinline__ uint32_t idesc_f16(int m, int n) {
+  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
 }  // namespace ptx

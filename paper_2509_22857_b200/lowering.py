@@ -123,8 +123,9 @@ class Lowered:
         return L.array(L.UnitDesc, out)
 
     def pack_descs(self):
-        return L.array(L.PackDesc, [L.PackDesc(kind=k, src=s, dst=d, n=n, rows=r, k=kk, r0=0, r1=0)
-                                    for (k, s, d, n, r, kk) in self.pack_ops])
+        return L.array(L.PackDesc, [L.PackDesc(kind=op[0], src=op[1], dst=op[2], n=op[3], rows=op[4], k=op[5],
+                                               aux=op[6] if len(op) > 6 else 0, reserved=0)
+                                    for op in self.pack_ops])
 
 
 # ---------------------------------------------------------------------------
@@ -350,6 +351,21 @@ class _Builder:
         self.packed += _align(floats)
         return dst
 
+    def tc16_image(self, nid: str) -> Tuple[int, int]:
+        """fp16x2 image (64 fp16 per 128-byte row, one float per element for
+        hi+lo) and its {max|w|, 2^-e} scale pair."""
+        s = self.slots[nid]["weight"]
+        npad, kp = s.meta["npad"], s.meta["kp"]
+        ntile = npad if npad <= 128 else 128
+        kb = (kp + 63) // 64
+        floats = ((npad + ntile - 1) // ntile) * kb * ntile * 64
+        dst = self.packed
+        self.packed += _align(floats)
+        scale = self.packed
+        self.packed += _align(2)
+        self.pack.append((L.PACK_TC16_WEIGHTS, s.offset, dst, floats, npad, kp, scale))
+        return dst, scale
+
     def emit(self, nodes: List[str], **u) -> None:
         self.units.append(u)
         self.unit_nodes.append(nodes)
@@ -465,6 +481,7 @@ class _Builder:
                 out_shape = sh[cur]
         if self.use_tc and wmeta["npad"] % 16 == 0 and wmeta["npad"] >= 16:
             u["tc_off"] = self.tc_image(nid)
+            u["tc16_off"], u["tc16_scale_off"] = self.tc16_image(nid)
         t = self.tensor(out_shape)
         u["out"] = t
         for c in chain[1:]:

@@ -1,0 +1,65 @@
+"""The five benchmark configurations end to end on the GPU: the config's
+redistribution sweeps run on the device (one cooperative launch each) and
+match the float64 oracle's per-donor sweep parameter for parameter; the
+redistributed model's batched forward (auto precision = tcgen05 fp16x2 where
+supported) matches the oracle at rel 1e-4 / abs 1e-5; and, because several
+configs' logits are dominated by a constant offset, the
+batch-centred logits -- the input-dependent signal -- must match too."""
+
+import numpy as np
+import pytest
+
+from helpers import max_param_rel_diff, rel_err
+from oracle import levnet_oracle as O
+from paper_2509_22857_b200 import configs
+from paper_2509_22857_b200 import transforms as T
+from paper_2509_22857_b200.runtime import Engine
+
+pytestmark = pytest.mark.gpu
+
+# oracle images per config (the float64 numpy oracle is slow at 224^2)
+N_IMAGES = {"lenet5": 16, "resnet20": 8, "resnet20_deg8": 8, "vgg11": 8, "resnet18": 2}
+
+
+def _device_sweeps(g, cfg):
+    eng = Engine(g)
+    cur = g
+    for direction in cfg.redistribution:
+        accepted, _ = T.plan_sweep(eng, cur, direction, allow_negative_leading=cfg.allow_negative_leading)
+        prog = T.compile_sweep(eng, cur, direction, accepted, cfg.allow_negative_leading)
+        T.run_program(eng, prog)
+        cur = eng.to_graph()
+    return eng, cur
+
+
+def _oracle_sweeps(g, cfg):
+    for direction in cfg.redistribution:
+        g, _, _ = O.redistribute_sweep(g, direction, allow_negative_leading=cfg.allow_negative_leading)
+    return g
+
+
+@pytest.mark.parametrize("name", list(configs.CONFIGS))
+def test_config_redistributed_forward(cuda, name):
+    import torch
+    cfg = configs.CONFIGS[name]
+    g = configs.build(name)
+    eng, got_g = _device_sweeps(g, cfg)
+    want_g = _oracle_sweeps(g, cfg)
+    assert max_param_rel_diff(got_g, want_g) <= 1e-6, name
+
+    # a batch of the measured size through the device engine; the oracle
+    # checks the first N images (batch size changes no per-image arithmetic)
+    x = configs.make_input(cfg)
+    y = eng.forward(torch.from_numpy(x.astype(np.float32)).cuda()).double().cpu().numpy()
+    assert np.all(np.isfinite(y)), name
+    n = N_IMAGES[name]
+    want = O.eval_batch(want_g, x[:n])
+    np.testing.assert_allclose(y[:n], want, rtol=1e-4, atol=1e-5, err_msg=name)
+    assert rel_err(y[:n], want) <= 1e-4, name
+    # input-dependent part of the logits
+    cg, cw = y[:n] - y[:n].mean(0), want - want.mean(0)
+    assert np.abs(cw).max() > 0, name
+    assert np.abs(cg - cw).max() <= 1e-2 * np.abs(cw).max(), name
+    # the redistributed model is the original function
+    orig = O.eval_batch(g, x[:n])
+    assert rel_err(want, orig) <= 1e-8, name

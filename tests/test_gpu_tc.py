@@ -1,7 +1,8 @@
-"""tcgen05 conv kernel (3xTF32, A from TMEM) against the float64 oracle on
-single fused conv units of every supported shape class, and against the SIMT
-kernel.  impl=2 forces the tcgen05 path (plan creation fails loudly if the
-shape is not supported)."""
+"""tcgen05 conv kernel (A from TMEM) against the float64 oracle on single
+fused conv units of every supported shape class, and against the SIMT kernel,
+in both precisions: impl=2 forces 3xTF32 (kind::tf32), impl=3 forces fp16x2
+(kind::f16, three fp16 products on power-of-two scaled weights); plan
+creation fails loudly if the shape is not supported."""
 
 import numpy as np
 import pytest
@@ -13,6 +14,8 @@ from paper_2509_22857_b200.graph import (AddNode, AvgPoolNode, BiPoolNode, ConvN
 from paper_2509_22857_b200.runtime import Engine
 
 pytestmark = pytest.mark.gpu
+
+IMPLS = pytest.mark.parametrize("impl", [2, 3], ids=["tf32x3", "f16x2"])
 
 SHAPES = [
     # cin, cout, k, stride, pad, hw, batch
@@ -48,18 +51,19 @@ def run(g, x, impl):
     return y.double().cpu().numpy(), impls
 
 
+@IMPLS
 @pytest.mark.parametrize("shape", SHAPES, ids=[f"{s[0]}x{s[1]}k{s[2]}s{s[3]}h{s[5]}" for s in SHAPES])
-def test_tc_plain_conv(cuda, shape):
+def test_tc_plain_conv(cuda, shape, impl):
     cin, cout, k, s, p, hw, batch = shape
     rng = np.random.default_rng(hash(shape) % 2**32)
     g = conv_graph(rng, cin, cout, k, s, p, hw)
     x = rng.normal(0, 1, (batch, cin, hw, hw))
     want = O.eval_batch(g, x)
-    got, impls = run(g, x, 2)
-    assert impls == {2}
+    got, impls = run(g, x, impl)
+    assert impls == {impl}
     np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-5)
     simt, _ = run(g, x, 1)
-    # fp32-class accuracy from 3xTF32: within a small factor of plain fp32 FMA
+    # fp32-class accuracy from the 3-product split: within a small factor of plain fp32 FMA
     assert rel_err(got, want) <= max(4 * rel_err(simt, want), 2e-6)
 
 
@@ -68,18 +72,20 @@ def _poly(rng, c, d):
     return PolyActNode("act", cs)
 
 
+@IMPLS
 @pytest.mark.parametrize("deg", [2, 4, 8])
-def test_tc_conv_poly(cuda, deg):
+def test_tc_conv_poly(cuda, deg, impl):
     rng = np.random.default_rng(deg)
     g = conv_graph(rng, 16, 32, 3, 1, 1, 16, [_poly(rng, 32, deg)], gain=0.5)
     x = rng.normal(0, 1, (8, 16, 16, 16))
     want = O.eval_batch(g, x)
-    got, impls = run(g, x, 2)
-    assert impls == {2}
+    got, impls = run(g, x, impl)
+    assert impls == {impl}
     np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-5)
 
 
-def test_tc_conv_pools(cuda):
+@IMPLS
+def test_tc_conv_pools(cuda, impl):
     rng = np.random.default_rng(11)
     d = 4
     c = rng.normal(0, 0.2, (d + 1, d + 1, 64))
@@ -92,12 +98,13 @@ def test_tc_conv_pools(cuda):
         g = conv_graph(rng, 32, 64, 3, 1, 1, 8, tail, gain=0.3)
         x = rng.normal(0, 1, (16, 32, 8, 8))
         want = O.eval_batch(g, x)
-        got, impls = run(g, x, 2)
-        assert impls == {2}
+        got, impls = run(g, x, impl)
+        assert impls == {impl}
         np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-5)
 
 
-def test_tc_conv_residual(cuda):
+@IMPLS
+def test_tc_conv_residual(cuda, impl):
     rng = np.random.default_rng(12)
     g = ModelGraph()
     g.add(InputNode("in", 32, 8, 8))
@@ -112,8 +119,8 @@ def test_tc_conv_residual(cuda):
     g.validate()
     x = rng.normal(0, 1, (16, 32, 8, 8))
     want = O.eval_batch(g, x)
-    got, impls = run(g, x, 2)
-    assert impls == {2}
+    got, impls = run(g, x, impl)
+    assert impls == {impl}
     np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-5)
 
 
@@ -123,8 +130,39 @@ def test_tc_matches_simt_on_resnet20(cuda):
     g = configs.build("resnet20")
     x = configs.make_input(configs.CONFIGS["resnet20"], batch=32)
     tc, impls = run(g, x, 0)
-    assert 2 in impls
+    assert 3 in impls  # auto picks fp16x2
     simt, _ = run(g, x, 1)
     want = O.eval_batch(g, x[:4])
     np.testing.assert_allclose(tc[:4], want, rtol=1e-4, atol=1e-5)
     np.testing.assert_allclose(tc, simt, rtol=1e-4, atol=1e-5)
+
+
+@pytest.mark.parametrize("shape", [(16, 32, 3, 1, 1, 16, 8), (64, 128, 3, 1, 1, 8, 4)], ids=["n32", "n128"])
+def test_f16x2_overflow_rows_recomputed(cuda, shape):
+    """Inputs beyond the fp16 range (|x| >= 65520) poison their pixel's
+    accumulator row; the epilogue redoes exactly those rows in fp32."""
+    cin, cout, k, s, p, hw, batch = shape
+    rng = np.random.default_rng(5)
+    g = conv_graph(rng, cin, cout, k, s, p, hw)
+    x = rng.normal(0, 1, (batch, cin, hw, hw))
+    x[0, 0, 3, 4] = 1.0e6
+    x[1, cin - 1, 0, 0] = -7.0e4
+    x[batch - 1, :, hw - 1, :] = 3.0e5
+    want = O.eval_batch(g, x)
+    got, impls = run(g, x, 3)
+    assert impls == {3}
+    np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-5 * np.abs(want).max())
+
+
+@pytest.mark.parametrize("wscale", [1e-6, 1e4])
+def test_f16x2_weight_scaling(cuda, wscale):
+    """Weights far outside fp16's comfortable range are packed with a power of
+    two scale and unscaled in the epilogue."""
+    rng = np.random.default_rng(6)
+    g = conv_graph(rng, 32, 64, 3, 1, 1, 8, gain=wscale)
+    x = rng.normal(0, 1, (8, 32, 8, 8))
+    want = O.eval_batch(g, x)
+    got, impls = run(g, x, 3)
+    assert impls == {3}
+    simt, _ = run(g, x, 1)
+    assert rel_err(got, want) <= max(4 * rel_err(simt, want), 2e-6)
