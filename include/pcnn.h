@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define PCNN_ABI_VERSION 1
+#define PCNN_ABI_VERSION 2
 
 enum pcnn_status {
   PCNN_OK = 0,
@@ -110,7 +110,8 @@ typedef struct pcnn_unit_desc {
   int64_t in_div_off;            /* linear global sum divisor (1 float)      */
   int64_t impl;                  /* conv: 0 auto (tcgen05 fp16x2 if possible),
                                     1 SIMT fp32, 2 tcgen05 3xTF32,
-                                    3 tcgen05 fp16x2 (3 fp16 products)        */
+                                    3 tcgen05 fp16x2 (3 fp16 products),
+                                    4 auto without fp16x2 (all tensors fp32) */
   int64_t tc_off;                /* conv tcgen05 weight image (hi|lo tf32)   */
   int64_t npad;                  /* padded output channels (vector stride)   */
   int64_t tc16_off;              /* conv fp16x2 weight image (hi|lo fp16)    */
@@ -206,8 +207,18 @@ int pcnn_plan_create(const pcnn_unit_desc* units, int n_units,
 int pcnn_plan_destroy(pcnn_plan* plan);
 /* number of kernel launches one forward issues (for gpu_launches) */
 int pcnn_plan_num_launches(const pcnn_plan* plan);
-/* 1 if unit i runs on the tcgen05 kernel */
+/* conv implementation of unit i: 1 SIMT, 2 tcgen05 3xTF32, 3 tcgen05 fp16x2 */
 int pcnn_plan_unit_impl(const pcnn_plan* plan, int unit);
+/* 1 if tensor t is stored split (two fp16 planes x = hi + lo, written by
+ * its producer for fp16x2 convs), 0 if float32 */
+int pcnn_plan_tensor_split(const pcnn_plan* plan, int tensor);
+/* Status of the last forward on `stream` (synchronises it): bit 0 = a value
+ * of a split tensor left the fp16 range (|x| >= 2^15 or non-finite), so the
+ * result is not fp32-accurate and must be recomputed with float32 tensors
+ * (impl 2).  pcnn_forward_host copies the status with the logits;
+ * pcnn_plan_last_status returns that copy once the stream is synchronised. */
+int pcnn_plan_status(pcnn_plan* plan, void* stream);
+int pcnn_plan_last_status(const pcnn_plan* plan);
 
 /* x: device [batch][C][H][W] float32; logits: device [batch][K] float32.
  * use_graph: replay a captured CUDA graph of the whole network.          */

@@ -31,13 +31,14 @@ POOL_NONE, POOL_SUM2, POOL_BI2, POOL_GLOBAL = 0, 1, 2, 3
 # pack kinds
 PACK_CAST, PACK_BN_AFFINE, PACK_TC_WEIGHTS, PACK_TC16_WEIGHTS = 1, 2, 3, 4
 # conv implementations (pcnn_unit_desc.impl)
-IMPL_AUTO, IMPL_SIMT, IMPL_TF32, IMPL_F16X2 = 0, 1, 2, 3
+IMPL_AUTO, IMPL_SIMT, IMPL_TF32, IMPL_F16X2, IMPL_FP32_TENSORS = 0, 1, 2, 3, 4
 # scale opcodes
 (OP_FILL, OP_LOAD, OP_MUL, OP_DIV, OP_SUB, OP_POWI, OP_SROOT, OP_AROOT, OP_RECIP, OP_SOLVE,
  OP_CHECK_UNIFORM, OP_CHECK_NONZERO, OP_CHECK_NONNEG, OP_CHECK_CLOSE, OP_CHECK_ALLONE,
  OP_SQRT, OP_STORE) = range(1, 18)
 
 MAX_FACTORS = 6
+ABI_VERSION = 2
 
 
 class PcnnError(RuntimeError):
@@ -96,6 +97,9 @@ SYMBOLS = {
     "pcnn_plan_destroy": ([ctypes.c_void_p], ctypes.c_int),
     "pcnn_plan_num_launches": ([ctypes.c_void_p], ctypes.c_int),
     "pcnn_plan_unit_impl": ([ctypes.c_void_p, ctypes.c_int], ctypes.c_int),
+    "pcnn_plan_tensor_split": ([ctypes.c_void_p, ctypes.c_int], ctypes.c_int),
+    "pcnn_plan_status": ([ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "pcnn_plan_last_status": ([ctypes.c_void_p], ctypes.c_int),
     "pcnn_forward": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int],
                      ctypes.c_int),
     "pcnn_forward_host": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
@@ -121,7 +125,7 @@ def lib() -> ctypes.CDLL:
             fn = getattr(handle, name)
             fn.argtypes = args
             fn.restype = res
-        if handle.pcnn_abi_version() != 1:
+        if handle.pcnn_abi_version() != ABI_VERSION:
             raise PcnnError("libpcnn ABI version mismatch")
         _lib = handle
     return _lib

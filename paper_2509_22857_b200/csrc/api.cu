@@ -57,6 +57,9 @@ struct pcnn_plan {
   cudaStream_t capture_stream = nullptr;
   std::vector<GraphEntry> graphs;
   int launches = 0;
+  bool any_split = false;
+  int* status_dev = nullptr;   // bit 0: a split-format value left the fp16 range
+  int* status_host = nullptr;  // pinned copy written by pcnn_forward_host
 };
 
 namespace {
@@ -72,11 +75,50 @@ TensorView make_view(const pcnn_tensor_desc& t, float* ws) {
   v.is_vector = (int)t.is_vector;
   v.cbs = 0;
   while ((1 << v.cbs) < v.cb) ++v.cbs;
+  v.split = 0;
+  v.plane = 0;
+  v.flag = nullptr;
   return v;
 }
 
 int64_t tensor_floats(const pcnn_tensor_desc& t, int batch) {
   return (int64_t)batch * t.nblk * t.cb * t.h * t.w;
+}
+
+// Storage formats: a tensor is kept split (two fp16 planes, common.cuh) when
+// its producer is the ingest or an fp16x2 tcgen05 conv writing a spatial
+// tensor, and every reader is an fp16x2 tcgen05 conv (input or residual
+// skip).  Everything else stays fp32.
+void choose_formats(pcnn_plan* p) {
+  const int nt = (int)p->tensors.size();
+  std::vector<int> ok(nt, 1), produced(nt, 0);
+  for (int i = 0; i < (int)p->units.size(); ++i) {
+    const pcnn_unit_desc& u = p->units[i];
+    const bool tc16 = u.kind == PCNN_UNIT_CONV && p->impl[i] == 3;
+    if (u.out >= 0) {
+      produced[u.out] = 1;
+      if (!(u.kind == PCNN_UNIT_INGEST || (tc16 && u.pool != PCNN_POOL_GLOBAL))) ok[u.out] = 0;
+    }
+    if (u.in >= 0 && !tc16) ok[u.in] = 0;
+    if (u.in2 >= 0 && !(tc16 && u.residual)) ok[u.in2] = 0;
+  }
+  if (getenv("PCNN_NO_SPLIT")) ok.assign(nt, 0);
+  for (int t = 0; t < nt; ++t) {
+    TensorView& v = p->views[t];
+    if (!ok[t] || !produced[t] || v.is_vector || t == p->output) continue;
+    v.split = 1;
+    v.plane = tensor_floats(p->tensors[t], p->batch);
+    v.flag = p->status_dev;
+    p->any_split = true;
+  }
+  for (int i = 0; i < (int)p->units.size(); ++i) {
+    const pcnn_unit_desc& u = p->units[i];
+    if (u.kind != PCNN_UNIT_CONV) continue;
+    ConvArgs& a = p->conv_args[i];
+    a.in = p->views[u.in];
+    a.epi.out = p->views[u.out];
+    if (u.residual) a.epi.skip = p->views[u.in2];
+  }
 }
 
 const float* P(const pcnn_plan* p, int64_t off) { return off < 0 ? nullptr : p->params + off; }
@@ -196,6 +238,7 @@ void enqueue_unit(pcnn_plan* p, int ui, const float* x, float* logits, cudaStrea
 }
 
 void enqueue_all(pcnn_plan* p, const float* x, float* logits, cudaStream_t s) {
+  if (p->any_split) cudaMemsetAsync(p->status_dev, 0, sizeof(int), s);
   for (int i = 0; i < (int)p->units.size(); ++i) enqueue_unit(p, i, x, logits, s);
 }
 
@@ -262,21 +305,30 @@ int pcnn_plan_create(const pcnn_unit_desc* units, int n_units, const pcnn_tensor
         delete p;
         return rc;
       }
-      // auto: fp16x2 tensor cores, else 3xTF32, else SIMT
+      // auto: fp16x2 tensor cores, else 3xTF32, else SIMT; 4: auto without fp16x2
       ConvArgs& a = p->conv_args[i];
       if ((u.impl == 0 || u.impl == 3) && a.tcw16 && a.tc16_scale) {
         a.f16 = 1;
         if (conv_tc_supported(a)) p->impl[i] = 3;
         else a.f16 = 0;
       }
-      if (p->impl[i] == 1 && (u.impl == 0 || u.impl == 2) && a.tcw && conv_tc_supported(a)) p->impl[i] = 2;
-      if (p->impl[i] == 1 && u.impl >= 2) {
+      if (p->impl[i] == 1 && (u.impl == 0 || u.impl == 2 || u.impl == 4) && a.tcw && conv_tc_supported(a))
+        p->impl[i] = 2;
+      if (p->impl[i] == 1 && (u.impl == 2 || u.impl == 3)) {
         delete p;
         return fail(PCNN_ERR_UNSUPPORTED, "unit " + std::to_string(i) + ": tcgen05 conv requested but unsupported");
       }
     }
     p->launches += 1;
   }
+  if (cudaMalloc(&p->status_dev, sizeof(int)) != cudaSuccess ||
+      cudaMallocHost(&p->status_host, sizeof(int)) != cudaSuccess) {
+    pcnn_plan_destroy(p);
+    return fail(PCNN_ERR_CUDA, "status allocation failed");
+  }
+  cudaMemset(p->status_dev, 0, sizeof(int));
+  *p->status_host = 0;
+  choose_formats(p);
   if (cudaStreamCreateWithFlags(&p->capture_stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete p;
     return fail(PCNN_ERR_CUDA, "cudaStreamCreate failed");
@@ -289,6 +341,8 @@ int pcnn_plan_destroy(pcnn_plan* p) {
   if (!p) return PCNN_OK;
   for (auto& g : p->graphs) cudaGraphExecDestroy(g.exec);
   if (p->capture_stream) cudaStreamDestroy(p->capture_stream);
+  if (p->status_dev) cudaFree(p->status_dev);
+  if (p->status_host) cudaFreeHost(p->status_host);
   delete p;
   return PCNN_OK;
 }
@@ -299,6 +353,21 @@ int pcnn_plan_unit_impl(const pcnn_plan* p, int unit) {
   if (!p || unit < 0 || unit >= (int)p->units.size()) return -1;
   return p->impl[unit];
 }
+
+int pcnn_plan_tensor_split(const pcnn_plan* p, int tensor) {
+  if (!p || tensor < 0 || tensor >= (int)p->views.size()) return -1;
+  return p->views[tensor].split;
+}
+
+int pcnn_plan_status(pcnn_plan* p, void* stream) {
+  if (!p) return fail(PCNN_ERR_INVALID, "pcnn_plan_status: null plan");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  PCNN_CUDA(cudaMemcpyAsync(p->status_host, p->status_dev, sizeof(int), cudaMemcpyDeviceToHost, s));
+  PCNN_CUDA(cudaStreamSynchronize(s));
+  return *p->status_host;
+}
+
+int pcnn_plan_last_status(const pcnn_plan* p) { return p ? *p->status_host : -1; }
 
 int pcnn_forward(pcnn_plan* p, const float* x, float* logits, void* stream, int use_graph) {
   if (!p || !x || !logits) return fail(PCNN_ERR_INVALID, "pcnn_forward: null argument");
@@ -349,6 +418,7 @@ int pcnn_forward_host(pcnn_plan* p, const float* x_host, float* logits_host, flo
   int rc = pcnn_forward(p, x_dev, logits_dev, stream, 1);
   if (rc != PCNN_OK) return rc;
   PCNN_CUDA(cudaMemcpyAsync(logits_host, logits_dev, out_bytes, cudaMemcpyDeviceToHost, s));
+  if (p->any_split) PCNN_CUDA(cudaMemcpyAsync(p->status_host, p->status_dev, sizeof(int), cudaMemcpyDeviceToHost, s));
   return PCNN_OK;
 }
 

@@ -1,6 +1,7 @@
 // Shared device helpers for libpcnn (sm_100a).
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -12,18 +13,99 @@ constexpr int kMaxPolyDeg = 8;
 constexpr int kMaxBiDeg = 4;
 
 // Resolved view of one activation tensor for a given batch.
+//
+// Storage formats (same bytes, same blocked index e(b, ch, y, x)):
+//   fp32  (split = 0): float at base[e];
+//   split (split = 1): x = hi + lo as two fp16 planes, hi at half index e,
+//         lo at plane + e (|x - hi - lo| <= 2^-22 |x| + 2^-25).  Written by
+//         the producers of tensors that only tcgen05 fp16x2 convs read, so
+//         the consumer feeds tensor memory without converting anything; a
+//         value outside the fp16 range (|x| >= 2^15, or not finite) sets
+//         *flag and the host reruns the batch on fp32 tensors.
 struct TensorView {
   float* base;
   int c, h, w, cb, nblk, is_vector;
   int cbs;  // log2(cb); cb is a power of two
+  int split;
+  int64_t plane;  // split: halves per plane
+  int* flag;      // split: overflow flag (device)
   __host__ __device__ int cpad() const { return nblk * cb; }
-  // address of element (b, channel, y, x) of a spatial tensor
-  __device__ __forceinline__ float* at(int b, int ch, int y, int x) const {
-    return base + ((((int64_t)b * nblk + (ch >> cbs)) * h + y) * w + x) * cb + (ch & (cb - 1));
+  __host__ __device__ __forceinline__ int64_t index(int b, int ch, int y, int x) const {
+    return ((((int64_t)b * nblk + (ch >> cbs)) * h + y) * w + x) * cb + (ch & (cb - 1));
   }
+  // address of element (b, channel, y, x) of a spatial tensor (fp32 format)
+  __device__ __forceinline__ float* at(int b, int ch, int y, int x) const { return base + index(b, ch, y, x); }
+  __device__ __forceinline__ const __half* hi() const { return reinterpret_cast<const __half*>(base); }
+  __device__ __forceinline__ const __half* lo() const { return reinterpret_cast<const __half*>(base) + plane; }
   // address of the channel group starting at ch (the group stays in a block)
   __device__ __forceinline__ float* pix(int b, int ch, int y, int x) const { return at(b, ch, y, x); }
 };
+
+// ---- split-format element access ------------------------------------------------
+__device__ __forceinline__ uint32_t pack_half2(float a, float b) {
+  const __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+__device__ __forceinline__ float2 unpack_half2(uint32_t u) {
+  return __half22float2(*reinterpret_cast<const __half2*>(&u));
+}
+// hi/lo fp16 pairs of (a, b); returns false if either is outside |x| < 2^15
+__device__ __forceinline__ bool split_pair(float a, float b, uint32_t& hi, uint32_t& lo) {
+  hi = pack_half2(a, b);
+  const float2 h = unpack_half2(hi);
+  lo = pack_half2(a - h.x, b - h.y);
+  return fabsf(a) < 32768.f && fabsf(b) < 32768.f;
+}
+
+// store 4 consecutive channels (one channel block) in the tensor's format
+__device__ __forceinline__ void store4_any(const TensorView& t, int b, int ch, int y, int x, float v0, float v1,
+                                           float v2, float v3) {
+  const int64_t e = t.index(b, ch, y, x);
+  if (!t.split) {
+    *reinterpret_cast<float4*>(t.base + e) = make_float4(v0, v1, v2, v3);
+    return;
+  }
+  uint2 hi, lo;
+  const bool ok = split_pair(v0, v1, hi.x, lo.x) & split_pair(v2, v3, hi.y, lo.y);
+  __half* h = reinterpret_cast<__half*>(t.base);
+  *reinterpret_cast<uint2*>(h + e) = hi;
+  *reinterpret_cast<uint2*>(h + t.plane + e) = lo;
+  if (!ok) atomicExch(t.flag, 1);
+}
+
+// store 16 consecutive channels of one block (cb >= 16, ch % 16 == 0):
+// full 32-byte sectors per thread in both formats
+__device__ __forceinline__ void store16_any(const TensorView& t, int b, int ch, int y, int x, const float* v) {
+  const int64_t e = t.index(b, ch, y, x);
+  if (!t.split) {
+    float4* o = reinterpret_cast<float4*>(t.base + e);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    return;
+  }
+  uint32_t hi[8], lo[8];
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) ok &= split_pair(v[2 * i], v[2 * i + 1], hi[i], lo[i]);
+  __half* h = reinterpret_cast<__half*>(t.base);
+  uint4* ho = reinterpret_cast<uint4*>(h + e);
+  uint4* lp = reinterpret_cast<uint4*>(h + t.plane + e);
+  ho[0] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+  ho[1] = make_uint4(hi[4], hi[5], hi[6], hi[7]);
+  lp[0] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  lp[1] = make_uint4(lo[4], lo[5], lo[6], lo[7]);
+  if (!ok) atomicExch(t.flag, 1);
+}
+
+// load 4 consecutive channels as fp32
+__device__ __forceinline__ float4 load4_any(const TensorView& t, int b, int ch, int y, int x) {
+  const int64_t e = t.index(b, ch, y, x);
+  if (!t.split) return __ldg(reinterpret_cast<const float4*>(t.base + e));
+  const uint2 hi = __ldg(reinterpret_cast<const uint2*>(t.hi() + e));
+  const uint2 lo = __ldg(reinterpret_cast<const uint2*>(t.lo() + e));
+  const float2 h0 = unpack_half2(hi.x), h1 = unpack_half2(hi.y), l0 = unpack_half2(lo.x), l1 = unpack_half2(lo.y);
+  return make_float4(h0.x + l0.x, h0.y + l0.y, h1.x + l1.x, h1.y + l1.y);
+}
 
 // Output-pixel enumeration of a conv unit.  PLAIN walks (b, oy, ox);
 // WINDOW walks 2x2 pool windows (b, py, px) with the four window pixels at

@@ -131,7 +131,8 @@ __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) 
 // of one (channel block, ky, kx); .x = float offset relative to the pixel's
 // (iy0, ix0) origin, .y = ky | kx << 8 (ky = 31 marks K padding).
 struct PixelRow {
-  const float* base;  // &in[b][0][iy0][ix0][0] (may point outside; only read when valid)
+  const float* base;    // &in[b][0][iy0][ix0][0] (may point outside; only read when valid)
+  const __half* hbase;  // the same element in the hi plane of a split tensor
   uint32_t ymask, xmask;
 };
 
@@ -140,7 +141,9 @@ __device__ __forceinline__ PixelRow pixel_row(const TcParams& P, int b, int oy, 
   const TensorView& in = a.in;
   const int iy0 = oy * a.stride - a.pad, ix0 = ox * a.stride - a.pad;
   PixelRow r;
-  r.base = in.base + (((int64_t)b * in.nblk * in.h + iy0) * in.w + ix0) * in.cb;
+  const int64_t idx = (((int64_t)b * in.nblk * in.h + iy0) * in.w + ix0) * in.cb;
+  r.base = in.base + idx;
+  r.hbase = reinterpret_cast<const __half*>(in.base) + idx;
   r.ymask = r.xmask = 0;
   if (valid) {
     for (int k = 0; k < a.kh; ++k) r.ymask |= (uint32_t)(iy0 + k >= 0 && iy0 + k < in.h) << k;
@@ -207,7 +210,63 @@ __device__ __forceinline__ void store_sub16(const TcParams& P, const float4* f, 
   }
 }
 
+// Converter register buffer for one 32-element sub-block: fp32 values to
+// split, or (split input) the hi/lo fp16 words ready for tensor memory.
+template <int CBS, bool SPL>
+struct SubBuf {
+  float4 f[8];
+  __device__ __forceinline__ void load(const int2* seg, int h, const PixelRow& px, int64_t) {
+    load_kblock<CBS>(seg, h, px, f);
+  }
+};
+template <int CBS>
+struct SubBuf<CBS, true> {
+  uint32_t hw[16], lw[16];
+  __device__ __forceinline__ void load(const int2* __restrict__ seg, int h, const PixelRow& px, int64_t plane) {
+    constexpr int SEGS = 32 >> CBS, WPS = (1 << CBS) / 2;  // segments, words per segment
+#pragma unroll
+    for (int g = 0; g < SEGS; ++g) {
+      const int2 e = seg[h * SEGS + g];
+      const bool ok = (px.ymask >> (e.y & 0xFF)) & (px.xmask >> (e.y >> 8)) & 1u;
+      const __half* src = px.hbase + e.x;
+      if (WPS >= 4) {
+#pragma unroll
+        for (int q = 0; q < WPS / 4; ++q) {
+          const uint4 a = ok ? __ldg(reinterpret_cast<const uint4*>(src) + q) : make_uint4(0, 0, 0, 0);
+          const uint4 b = ok ? __ldg(reinterpret_cast<const uint4*>(src + plane) + q) : make_uint4(0, 0, 0, 0);
+          uint32_t* H = hw + g * WPS + 4 * q;
+          uint32_t* L = lw + g * WPS + 4 * q;
+          H[0] = a.x; H[1] = a.y; H[2] = a.z; H[3] = a.w;
+          L[0] = b.x; L[1] = b.y; L[2] = b.z; L[3] = b.w;
+        }
+      } else {
+        const uint2 a = ok ? __ldg(reinterpret_cast<const uint2*>(src)) : make_uint2(0, 0);
+        const uint2 b = ok ? __ldg(reinterpret_cast<const uint2*>(src + plane)) : make_uint2(0, 0);
+        hw[g * 2] = a.x; hw[g * 2 + 1] = a.y;
+        lw[g * 2] = b.x; lw[g * 2 + 1] = b.y;
+      }
+    }
+  }
+};
+
 // sub-block h of a stage (K-block j = h / SUB of the stage) -> its TMEM columns
+template <bool F16, int CBS>
+__device__ __forceinline__ void store_buf(const TcParams& P, const SubBuf<CBS, false>& b, uint32_t t_stage, int j,
+                                          int hh) {
+  if (F16) store_sub16(P, b.f, t_stage + j * 32 + hh * 16, t_stage + 32 * P.ks + j * 32 + hh * 16);
+  else store_kblock(P, b.f, t_stage + j * 32, t_stage + 32 * P.ks + j * 32);
+}
+template <bool F16, int CBS>
+__device__ __forceinline__ void store_buf(const TcParams& P, const SubBuf<CBS, true>& b, uint32_t t_stage, int j,
+                                          int hh) {
+  if (P.dbg & 8) return;
+  const uint32_t th = t_stage + j * 32 + hh * 16, tl = t_stage + 32 * P.ks + j * 32 + hh * 16;
+  ptx::tmem_st8(th, b.hw);
+  ptx::tmem_st8(th + 8, b.hw + 8);
+  ptx::tmem_st8(tl, b.lw);
+  ptx::tmem_st8(tl + 8, b.lw + 8);
+}
+
 template <bool F16>
 __device__ __forceinline__ void store_sub(const TcParams& P, const float4* f, uint32_t t_stage, int j, int hh) {
   if (F16) store_sub16(P, f, t_stage + j * 32 + hh * 16, t_stage + 32 * P.ks + j * 32 + hh * 16);
@@ -215,11 +274,12 @@ __device__ __forceinline__ void store_sub(const TcParams& P, const float4* f, ui
 }
 
 __device__ __forceinline__ void store4(const EpiParams& e, int b, int ch, int y, int x, const float* o) {
-  *reinterpret_cast<float4*>(e.out.pix(b, ch, y, x)) = make_float4(o[0], o[1], o[2], o[3]);
+  store4_any(e.out, b, ch, y, x, o[0], o[1], o[2], o[3]);
 }
 
-template <int CBS, bool F16>
+template <int CBS, bool F16, bool SPL>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_constant__ TcParams P) {
+  static_assert(F16 || !SPL, "split-format input feeds the fp16x2 kernel only");
   constexpr int SUB = F16 ? 2 : 1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -553,19 +613,20 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       const int h0 = kb0 * SUB;
       // two register buffers: the next sub-block's loads are in flight while
       // the current one is split and stored
-      float4 fa[8], fb[8];
-      load_kblock<CBS>(seg, h0, px, fa);
-      if (nsb > 1) load_kblock<CBS>(seg, h0 + 1, px, fb);
+      SubBuf<CBS, SPL> fa, fb;
+      const int64_t plane = a.in.plane;
+      fa.load(seg, h0, px, plane);
+      if (nsb > 1) fb.load(seg, h0 + 1, px, plane);
       if (lane == 0 && warp == 4) tr(P, 0, 0x200 | kb0);
       ptx::mbar_wait_warp(ptx::smem_u32(&S->a_empty[s]), par);
       ptx::tc_fence_after();
       const uint32_t t_stage = tmem + lane_off + a_col0 + s * 64 * KS;
       for (int i = 0; i < nsb; i += 2) {
-        store_sub<F16>(P, fa, t_stage, i / SUB, i % SUB);
-        if (i + 2 < nsb) load_kblock<CBS>(seg, h0 + i + 2, px, fa);
+        store_buf<F16>(P, fa, t_stage, i / SUB, i % SUB);
+        if (i + 2 < nsb) fa.load(seg, h0 + i + 2, px, plane);
         if (i + 1 < nsb) {
-          store_sub<F16>(P, fb, t_stage, (i + 1) / SUB, (i + 1) % SUB);
-          if (i + 3 < nsb) load_kblock<CBS>(seg, h0 + i + 3, px, fb);
+          store_buf<F16>(P, fb, t_stage, (i + 1) / SUB, (i + 1) % SUB);
+          if (i + 3 < nsb) fb.load(seg, h0 + i + 3, px, plane);
         }
       }
       if (!(P.dbg & 16)) ptx::tmem_st_wait();
@@ -605,16 +666,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       for (int c0 = 0; c0 < ((P.dbg & 4) ? 0 : P.nt); c0 += 16) {
         float v[16], t[16];
         if (P.concat) {
-          ptx::tmem_ld16(d_set + P.nt + c0, v);  // corr_0
-          for (int p = 0; p < NP; ++p) {
-            if (p) {
-              ptx::tmem_ld16(d_set + 2 * p * P.nt + P.nt + c0, t);
+          // [main_p | corr_p] blocks: corr_0 + main_0 + sum_p (corr_p + main_p)
+          ptx::tmem_ld16x2(d_set + P.nt + c0, d_set + c0, v, t);
 #pragma unroll
-              for (int i = 0; i < 16; ++i) v[i] += t[i];
-            }
-            ptx::tmem_ld16(d_set + 2 * p * P.nt + c0, t);
+          for (int i = 0; i < 16; ++i) v[i] += t[i];
+          for (int p = 1; p < NP; ++p) {
+            float u[16];
+            ptx::tmem_ld16x2(d_set + 2 * p * P.nt + P.nt + c0, d_set + 2 * p * P.nt + c0, u, t);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] += t[i];
+            for (int i = 0; i < 16; ++i) v[i] += u[i] + t[i];
           }
         } else {
           ptx::tmem_ld16(d_set + NP * P.nt + c0, v);  // correction terms
@@ -625,10 +685,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           }
         }
         const int chb = n_tile * P.nt + c0;
+        if (lane == 0 && warp == 0) tr(P, 2, 0xD00 | c0);
         if (F16) {
-          if (valid && !isfinite(v[0])) {
+          if (valid && !isfinite(v[0]) && !SPL) {
             // an input of this pixel overflowed fp16 (or is inf/nan): redo the
             // row's 16 dot products in fp32 with the unscaled fp32 weights
+            // (split inputs cannot overflow here: their producer flagged it)
 #pragma unroll
             for (int j = 0; j < 16; ++j) v[j] = 0.f;
             const TensorView& in = a.in;
@@ -654,11 +716,29 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         float sk[16];
         if (e.residual) {
           // the 16 channels are contiguous: cb >= 16 whenever npad >= 16
-          const float4* sp = reinterpret_cast<const float4*>(e.skip.at(valid ? b : 0, chb, oy, ox));
+          const int64_t ei = e.skip.index(valid ? b : 0, chb, oy, ox);
+          if (e.skip.split) {
+            const uint4* hp = reinterpret_cast<const uint4*>(e.skip.hi() + ei);
+            const uint4* lp = reinterpret_cast<const uint4*>(e.skip.lo() + ei);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float4 f = valid ? __ldg(sp + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-            sk[4 * q] = f.x; sk[4 * q + 1] = f.y; sk[4 * q + 2] = f.z; sk[4 * q + 3] = f.w;
+            for (int q = 0; q < 2; ++q) {
+              const uint4 h = valid ? __ldg(hp + q) : make_uint4(0, 0, 0, 0);
+              const uint4 l = valid ? __ldg(lp + q) : make_uint4(0, 0, 0, 0);
+              const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+              for (int w = 0; w < 4; ++w) {
+                const float2 a2 = unpack_half2(hw[w]), b2 = unpack_half2(lw[w]);
+                sk[8 * q + 2 * w] = a2.x + b2.x;
+                sk[8 * q + 2 * w + 1] = a2.y + b2.y;
+              }
+            }
+          } else {
+            const float4* sp = reinterpret_cast<const float4*>(e.skip.base + ei);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float4 f = valid ? __ldg(sp + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+              sk[4 * q] = f.x; sk[4 * q + 1] = f.y; sk[4 * q + 2] = f.z; sk[4 * q + 3] = f.w;
+            }
           }
         }
 #pragma unroll
@@ -695,6 +775,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
 #pragma unroll
         for (int j = 0; j < 16; ++j)
           if (!valid || chb + j >= e.cout) v[j] = 0.f;
+        if (e.pool == PCNN_POOL_NONE) {
+          // the 16 channels are contiguous (cb >= 16)
+          if (lane == 0 && warp == 0) tr(P, 2, 0xE00 | c0);
+          if (valid) store16_any(e.out, b, chb, oy, ox, v);
+          continue;
+        }
 #pragma unroll
         for (int grp = 0; grp < 4; ++grp) {
           float* o = v + grp * 4;
@@ -785,7 +871,8 @@ bool make_params(const ConvArgs& a, TcParams& P) {
   // staged input if a tile needs few boxes and everything fits
   P.staged = 0;
   staging_geometry(a, P);
-  const bool stage_ok = !(getenv("PCNN_TC_NOSTAGE")) && P.pieces <= 4 && P.box_w <= 256 && P.box_h <= 256 &&
+  const bool stage_ok = !(getenv("PCNN_TC_NOSTAGE")) && !a.in.split && P.pieces <= 4 && P.box_w <= 256 &&
+                        P.box_h <= 256 &&
                         (a.in.nblk == 1 || a.in.cb == 32);
   P.nbs = kBStages;
   if (stage_ok) {
@@ -925,20 +1012,25 @@ void launch_conv_tc(const ConvArgs& a, cudaStream_t s) {
   const size_t smem = smem_bytes(P);
   const int tiles = P.m_tiles * P.n_tiles;
   const int grid = tiles < nsm ? tiles : nsm;
-  switch (a.in.cbs * 2 + (a.f16 ? 1 : 0)) {
-#define PCNN_TC_LAUNCH(C, H)                                                                            \
-  case C * 2 + H:                                                                                       \
-    cudaFuncSetAttribute(conv_tc_kernel<C, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    conv_tc_kernel<C, H><<<grid, kThreads, smem, s>>>(P);                                               \
+  const int mode = a.f16 ? (a.in.split ? 2 : 1) : 0;
+  switch (a.in.cbs * 4 + mode) {
+#define PCNN_TC_LAUNCH(C, H, SP)                                                                              \
+  case C * 4 + (H ? (SP ? 2 : 1) : 0):                                                                        \
+    cudaFuncSetAttribute(conv_tc_kernel<C, H, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
+    conv_tc_kernel<C, H, SP><<<grid, kThreads, smem, s>>>(P);                                                 \
     break;
-    PCNN_TC_LAUNCH(2, false)
-    PCNN_TC_LAUNCH(3, false)
-    PCNN_TC_LAUNCH(4, false)
-    PCNN_TC_LAUNCH(5, false)
-    PCNN_TC_LAUNCH(2, true)
-    PCNN_TC_LAUNCH(3, true)
-    PCNN_TC_LAUNCH(4, true)
-    PCNN_TC_LAUNCH(5, true)
+    PCNN_TC_LAUNCH(2, false, false)
+    PCNN_TC_LAUNCH(3, false, false)
+    PCNN_TC_LAUNCH(4, false, false)
+    PCNN_TC_LAUNCH(5, false, false)
+    PCNN_TC_LAUNCH(2, true, false)
+    PCNN_TC_LAUNCH(3, true, false)
+    PCNN_TC_LAUNCH(4, true, false)
+    PCNN_TC_LAUNCH(5, true, false)
+    PCNN_TC_LAUNCH(2, true, true)
+    PCNN_TC_LAUNCH(3, true, true)
+    PCNN_TC_LAUNCH(4, true, true)
+    PCNN_TC_LAUNCH(5, true, true)
 #undef PCNN_TC_LAUNCH
     default: break;
   }

@@ -27,7 +27,7 @@ __global__ void ingest_kernel(const float* __restrict__ x, TensorView t, int bat
       const int ch = g * 4 + j;
       v[j] = ch < t.c ? __ldg(x + ((int64_t)b * t.c + ch) * hw + p) : 0.f;
     }
-    *reinterpret_cast<float4*>(t.pix(b, g * 4, y, xw)) = make_float4(v[0], v[1], v[2], v[3]);
+    store4_any(t, b, g * 4, y, xw, v[0], v[1], v[2], v[3]);
   }
 }
 

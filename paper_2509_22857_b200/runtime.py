@@ -62,6 +62,19 @@ class Plan:
     def unit_impl(self, i: int) -> int:
         return L.lib().pcnn_plan_unit_impl(self.handle, i)
 
+    def tensor_split(self, t: int) -> bool:
+        return L.lib().pcnn_plan_tensor_split(self.handle, t) == 1
+
+    def status(self, stream=None) -> int:
+        """Status word of the last forward on `stream` (synchronises it)."""
+        rc = L.lib().pcnn_plan_status(self.handle, _stream_handle(stream))
+        if rc < 0:
+            L.check(rc, "pcnn_plan_status")
+        return rc
+
+    def last_status(self) -> int:
+        return L.lib().pcnn_plan_last_status(self.handle)
+
     def __del__(self):
         h = getattr(self, "handle", None)
         if h is not None and L._lib is not None:
@@ -85,6 +98,8 @@ class Engine:
         self._packs = self.lw.pack_descs()
         self.repack()
         self.plans: Dict[int, Plan] = {}
+        self.fallback_plans: Dict[int, Plan] = {}
+        self.fallbacks = 0  # forwards recomputed on float32 tensors
 
     # -- parameters -----------------------------------------------------------
     def repack(self, stream=None) -> None:
@@ -105,11 +120,25 @@ class Engine:
             p = self.plans[batch] = Plan(self, batch, self.impl)
         return p
 
+    def fallback_plan(self, batch: int) -> Plan:
+        """Same network with every tensor in float32 (no fp16x2 convs): the
+        recompute path when a split-format activation left the fp16 range."""
+        p = self.fallback_plans.get(batch)
+        if p is None:
+            p = self.fallback_plans[batch] = Plan(self, batch, L.IMPL_FP32_TENSORS)
+        return p
+
     def out_shape(self, batch: int) -> Tuple[int, ...]:
         return (batch,) + tuple(self.lw.out_shape)
 
-    def forward(self, x, out=None, use_graph: bool = True, stream=None):
-        """x: (B, C, H, W) float32 CUDA tensor -> (B, K) float32 CUDA tensor."""
+    def forward(self, x, out=None, use_graph: bool = True, stream=None, check: bool = True):
+        """x: (B, C, H, W) float32 CUDA tensor -> (B, K) float32 CUDA tensor.
+
+        check=True reads the plan's status word after the forward (one
+        4-byte read, synchronises the stream) and, if an activation stored
+        in split fp16 format left the fp16 range, recomputes the batch with
+        float32 tensors.  check=False leaves the forward asynchronous; call
+        plan(B).status() before trusting the result."""
         torch = _torch()
         if x.dtype != torch.float32 or not x.is_cuda:
             raise GraphError("forward expects a float32 CUDA tensor; use forward_host for host data")
@@ -123,6 +152,11 @@ class Engine:
         p = self.plan(b)
         L.check(L.lib().pcnn_forward(p.handle, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()),
                                      _stream_handle(stream), int(use_graph)), "pcnn_forward")
+        if check and p.status(stream):
+            self.fallbacks += 1
+            f = self.fallback_plan(b)
+            L.check(L.lib().pcnn_forward(f.handle, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                         _stream_handle(stream), int(use_graph)), "pcnn_forward")
         return out
 
     def forward_host(self, x_host: np.ndarray, x_dev=None, out_dev=None, out_host=None, stream=None):
@@ -142,6 +176,14 @@ class Engine:
                                           ctypes.c_void_p(x_dev.data_ptr()), ctypes.c_void_p(out_dev.data_ptr()),
                                           _stream_handle(stream)), "pcnn_forward_host")
         (stream or torch.cuda.current_stream()).synchronize()
+        if p.last_status():
+            self.fallbacks += 1
+            f = self.fallback_plan(b)
+            L.check(L.lib().pcnn_forward_host(f.handle, xh.ctypes.data_as(ctypes.c_void_p),
+                                              out_host.ctypes.data_as(ctypes.c_void_p),
+                                              ctypes.c_void_p(x_dev.data_ptr()), ctypes.c_void_p(out_dev.data_ptr()),
+                                              _stream_handle(stream)), "pcnn_forward_host")
+            (stream or torch.cuda.current_stream()).synchronize()
         return out_host
 
     def forward_unit(self, batch: int, i: int, x, out, stream=None) -> None:

@@ -22,7 +22,7 @@ def declared_functions():
 
 def test_library_loads_without_gpu():
     lib = L.lib()
-    assert lib.pcnn_abi_version() == 1
+    assert lib.pcnn_abi_version() == L.ABI_VERSION == 2
 
 
 def test_every_declared_symbol_is_exported():

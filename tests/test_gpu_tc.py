@@ -166,3 +166,42 @@ def test_f16x2_weight_scaling(cuda, wscale):
     assert impls == {3}
     simt, _ = run(g, x, 1)
     assert rel_err(got, want) <= max(4 * rel_err(simt, want), 2e-6)
+
+
+def test_split_tensors_and_overflow_fallback(cuda):
+    """fp16x2 convs chained through split-format (hi/lo fp16) activations; an
+    activation outside the fp16 range sets the plan status and the engine
+    recomputes the batch on float32 tensors (device and host entry points)."""
+    import torch
+    rng = np.random.default_rng(21)
+    g = ModelGraph()
+    g.add(InputNode("in", 16, 8, 8))
+    g.add(ConvNode("ca", rng.normal(0, 0.1, (32, 16, 3, 3)), rng.normal(0, 0.1, 32), 1, 1))
+    g.add(PolyActNode("aa", [np.float64(0.0), np.float64(0.5), np.float64(0.2)]))
+    g.add(ConvNode("cb", rng.normal(0, 0.1, (32, 32, 3, 3)), rng.normal(0, 0.1, 32), 1, 1))
+    g.add(ConvNode("cd", rng.normal(0, 0.1, (32, 16, 1, 1)), rng.normal(0, 0.1, 32), 1, 0))
+    g.add(AddNode("j"))
+    g.add(PolyActNode("aj", [rng.normal(0, 0.1, 32), rng.normal(0.5, 0.1, 32), rng.uniform(0.05, 0.3, 32)]))
+    g.add(AvgPoolNode("gp", 64, np.float64(1 / 64)))
+    g.add(LinearNode("fc", rng.normal(0, 0.2, (10, 32)), rng.normal(0, 0.1, 10)))
+    g.add(OutputNode("out"))
+    for s_, d_ in (("in", "ca"), ("ca", "aa"), ("aa", "cb"), ("cb", "j"), ("in", "cd"), ("cd", "j"),
+                   ("j", "aj"), ("aj", "gp"), ("gp", "fc"), ("fc", "out")):
+        g.connect(s_, d_)
+    g.validate()
+    eng = Engine(g)
+    x = rng.normal(0, 1, (16, 16, 8, 8))
+    plan = eng.plan(16)
+    assert any(plan.tensor_split(t) for t in range(len(eng.lw.tensors)))
+    got = eng.forward(torch.from_numpy(x.astype(np.float32)).cuda()).double().cpu().numpy()
+    assert eng.fallbacks == 0
+    np.testing.assert_allclose(got, O.eval_batch(g, x), rtol=1e-4, atol=1e-5)
+    # an input value beyond fp16 range: the ingest flags it, the rerun is exact
+    x[3, 2, 4, 4] = 1.0e5
+    want = O.eval_batch(g, x)
+    got = eng.forward(torch.from_numpy(x.astype(np.float32)).cuda()).double().cpu().numpy()
+    assert eng.fallbacks == 1
+    np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-5 * np.abs(want).max())
+    got_h = eng.forward_host(x.astype(np.float32)).astype(np.float64)
+    assert eng.fallbacks == 2
+    np.testing.assert_allclose(got_h, want, rtol=1e-4, atol=1e-5 * np.abs(want).max())
