@@ -76,13 +76,15 @@ TensorView make_view(const pcnn_tensor_desc& t, float* ws) {
   v.cbs = 0;
   while ((1 << v.cbs) < v.cb) ++v.cbs;
   v.split = 0;
+  v.hp = v.wp = 0;
+  v.kstride = 0;
   v.plane = 0;
   v.flag = nullptr;
   return v;
 }
 
 int64_t tensor_floats(const pcnn_tensor_desc& t, int batch) {
-  return (int64_t)batch * t.nblk * t.cb * t.h * t.w;
+  return tensor_storage_floats(batch, t.c, t.nblk * t.cb, t.h, t.w, t.is_vector != 0);
 }
 
 // Storage formats: a tensor is kept split (two fp16 planes, common.cuh) when
@@ -106,8 +108,16 @@ void choose_formats(pcnn_plan* p) {
   for (int t = 0; t < nt; ++t) {
     TensorView& v = p->views[t];
     if (!ok[t] || !produced[t] || v.is_vector || t == p->output) continue;
+    if (v.cb < 8 && v.nblk > 1) continue;
     v.split = 1;
-    v.plane = tensor_floats(p->tensors[t], p->batch);
+    v.hp = v.h + 2;
+    v.wp = v.w + 2;
+    v.kstride = (int64_t)p->batch * v.hp * v.wp * 8;
+    v.plane = (int64_t)((v.cpad() + 7) / 8) * v.kstride;
+    if (v.plane >= (1ll << 31)) {  // 32-bit segment offsets in the conv kernel
+      v.split = 0;
+      continue;
+    }
     v.flag = p->status_dev;
     p->any_split = true;
   }

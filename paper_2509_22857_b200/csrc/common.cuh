@@ -14,32 +14,49 @@ constexpr int kMaxBiDeg = 4;
 
 // Resolved view of one activation tensor for a given batch.
 //
-// Storage formats (same bytes, same blocked index e(b, ch, y, x)):
-//   fp32  (split = 0): float at base[e];
-//   split (split = 1): x = hi + lo as two fp16 planes, hi at half index e,
-//         lo at plane + e (|x - hi - lo| <= 2^-22 |x| + 2^-25).  Written by
-//         the producers of tensors that only tcgen05 fp16x2 convs read, so
-//         the consumer feeds tensor memory without converting anything; a
-//         value outside the fp16 range (|x| >= 2^15, or not finite) sets
-//         *flag and the host reruns the batch on fp32 tensors.
+// Storage formats:
+//   fp32  (split = 0): channel-blocked [B][C/cb][H][W][cb] floats.
+//   split (split = 1): x = hi + lo as two fp16 planes (|x - hi - lo| <=
+//         2^-22 |x| + 2^-25), each laid out [C/8][B][H+2][W+2][8] with a
+//         one-pixel zero border: 8 channels = 16 bytes per position, and a
+//         3x3 conv's taps are fixed offsets in the flattened padded grid.
+//         Written by producers of tensors that only tcgen05 fp16x2 convs
+//         read; a value outside |x| < 2^15 (or not finite) sets *flag and the
+//         host reruns the batch on fp32 tensors.
 struct TensorView {
   float* base;
   int c, h, w, cb, nblk, is_vector;
   int cbs;  // log2(cb); cb is a power of two
   int split;
-  int64_t plane;  // split: halves per plane
-  int* flag;      // split: overflow flag (device)
+  int hp, wp;       // split: padded grid h + 2, w + 2
+  int64_t kstride;  // split: halves per 8-channel group (batch * hp * wp * 8)
+  int64_t plane;    // split: halves per plane
+  int* flag;        // split: overflow flag (device)
   __host__ __device__ int cpad() const { return nblk * cb; }
   __host__ __device__ __forceinline__ int64_t index(int b, int ch, int y, int x) const {
     return ((((int64_t)b * nblk + (ch >> cbs)) * h + y) * w + x) * cb + (ch & (cb - 1));
   }
+  // split: half index of (b, ch, y, x) inside a plane
+  __host__ __device__ __forceinline__ int64_t sindex(int b, int ch, int y, int x) const {
+    return (ch >> 3) * kstride + (((int64_t)b * hp + y + 1) * wp + x + 1) * 8 + (ch & 7);
+  }
   // address of element (b, channel, y, x) of a spatial tensor (fp32 format)
   __device__ __forceinline__ float* at(int b, int ch, int y, int x) const { return base + index(b, ch, y, x); }
-  __device__ __forceinline__ const __half* hi() const { return reinterpret_cast<const __half*>(base); }
-  __device__ __forceinline__ const __half* lo() const { return reinterpret_cast<const __half*>(base) + plane; }
-  // address of the channel group starting at ch (the group stays in a block)
+  __device__ __forceinline__ __half* hi() const { return reinterpret_cast<__half*>(base); }
+  __device__ __forceinline__ __half* lo() const { return reinterpret_cast<__half*>(base) + plane; }
+  // address of element (b, channel, y, x) of a spatial tensor (fp32 format)
   __device__ __forceinline__ float* pix(int b, int ch, int y, int x) const { return at(b, ch, y, x); }
 };
+
+// floats a tensor occupies in either format (the workspace holds the larger)
+__host__ __device__ inline int64_t tensor_storage_floats(int64_t batch, int64_t c, int64_t cpad, int64_t h, int64_t w,
+                                                         bool is_vector) {
+  const int64_t fp32 = batch * cpad * h * w;
+  if (is_vector) return fp32;
+  const int64_t split = ((cpad + 7) / 8) * 8 * batch * (h + 2) * (w + 2);  // 2 planes of halves
+  (void)c;
+  return fp32 > split ? fp32 : split;
+}
 
 // ---- split-format element access ------------------------------------------------
 __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
@@ -57,28 +74,26 @@ __device__ __forceinline__ bool split_pair(float a, float b, uint32_t& hi, uint3
   return fabsf(a) < 32768.f && fabsf(b) < 32768.f;
 }
 
-// store 4 consecutive channels (one channel block) in the tensor's format
+// store 4 consecutive channels (ch % 4 == 0) in the tensor's format
 __device__ __forceinline__ void store4_any(const TensorView& t, int b, int ch, int y, int x, float v0, float v1,
                                            float v2, float v3) {
-  const int64_t e = t.index(b, ch, y, x);
   if (!t.split) {
-    *reinterpret_cast<float4*>(t.base + e) = make_float4(v0, v1, v2, v3);
+    *reinterpret_cast<float4*>(t.base + t.index(b, ch, y, x)) = make_float4(v0, v1, v2, v3);
     return;
   }
+  const int64_t e = t.sindex(b, ch, y, x);
   uint2 hi, lo;
   const bool ok = split_pair(v0, v1, hi.x, lo.x) & split_pair(v2, v3, hi.y, lo.y);
-  __half* h = reinterpret_cast<__half*>(t.base);
-  *reinterpret_cast<uint2*>(h + e) = hi;
-  *reinterpret_cast<uint2*>(h + t.plane + e) = lo;
+  *reinterpret_cast<uint2*>(t.hi() + e) = hi;
+  *reinterpret_cast<uint2*>(t.lo() + e) = lo;
   if (!ok) atomicExch(t.flag, 1);
 }
 
-// store 16 consecutive channels of one block (cb >= 16, ch % 16 == 0):
-// full 32-byte sectors per thread in both formats
+// store 16 consecutive channels (ch % 16 == 0; one block when fp32, cb >= 16):
+// whole 32-byte sectors per thread in both formats
 __device__ __forceinline__ void store16_any(const TensorView& t, int b, int ch, int y, int x, const float* v) {
-  const int64_t e = t.index(b, ch, y, x);
   if (!t.split) {
-    float4* o = reinterpret_cast<float4*>(t.base + e);
+    float4* o = reinterpret_cast<float4*>(t.base + t.index(b, ch, y, x));
 #pragma unroll
     for (int q = 0; q < 4; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     return;
@@ -87,24 +102,42 @@ __device__ __forceinline__ void store16_any(const TensorView& t, int b, int ch, 
   bool ok = true;
 #pragma unroll
   for (int i = 0; i < 8; ++i) ok &= split_pair(v[2 * i], v[2 * i + 1], hi[i], lo[i]);
-  __half* h = reinterpret_cast<__half*>(t.base);
-  uint4* ho = reinterpret_cast<uint4*>(h + e);
-  uint4* lp = reinterpret_cast<uint4*>(h + t.plane + e);
-  ho[0] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-  ho[1] = make_uint4(hi[4], hi[5], hi[6], hi[7]);
-  lp[0] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-  lp[1] = make_uint4(lo[4], lo[5], lo[6], lo[7]);
+  const int64_t e = t.sindex(b, ch, y, x);
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    *reinterpret_cast<uint4*>(t.hi() + e + g * t.kstride) = make_uint4(hi[4 * g], hi[4 * g + 1], hi[4 * g + 2], hi[4 * g + 3]);
+    *reinterpret_cast<uint4*>(t.lo() + e + g * t.kstride) = make_uint4(lo[4 * g], lo[4 * g + 1], lo[4 * g + 2], lo[4 * g + 3]);
+  }
   if (!ok) atomicExch(t.flag, 1);
 }
 
-// load 4 consecutive channels as fp32
-__device__ __forceinline__ float4 load4_any(const TensorView& t, int b, int ch, int y, int x) {
-  const int64_t e = t.index(b, ch, y, x);
-  if (!t.split) return __ldg(reinterpret_cast<const float4*>(t.base + e));
-  const uint2 hi = __ldg(reinterpret_cast<const uint2*>(t.hi() + e));
-  const uint2 lo = __ldg(reinterpret_cast<const uint2*>(t.lo() + e));
-  const float2 h0 = unpack_half2(hi.x), h1 = unpack_half2(hi.y), l0 = unpack_half2(lo.x), l1 = unpack_half2(lo.y);
-  return make_float4(h0.x + l0.x, h0.y + l0.y, h1.x + l1.x, h1.y + l1.y);
+// 8 channels (one 16-byte group) of a split tensor as fp32
+__device__ __forceinline__ void load8_split(const TensorView& t, int64_t e, float* v) {
+  const uint4 h = __ldg(reinterpret_cast<const uint4*>(t.hi() + e));
+  const uint4 l = __ldg(reinterpret_cast<const uint4*>(t.lo() + e));
+  const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 a = unpack_half2(hw[i]), c = unpack_half2(lw[i]);
+    v[2 * i] = a.x + c.x;
+    v[2 * i + 1] = a.y + c.y;
+  }
+}
+
+// load 16 consecutive channels (ch % 16 == 0; one block when fp32) as fp32
+__device__ __forceinline__ void load16_any(const TensorView& t, int b, int ch, int y, int x, float* v) {
+  if (!t.split) {
+    const float4* s = reinterpret_cast<const float4*>(t.base + t.index(b, ch, y, x));
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 f = __ldg(s + q);
+      v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
+    }
+    return;
+  }
+  const int64_t e = t.sindex(b, ch, y, x);
+  load8_split(t, e, v);
+  load8_split(t, e + t.kstride, v + 8);
 }
 
 // Output-pixel enumeration of a conv unit.  PLAIN walks (b, oy, ox);

@@ -143,7 +143,7 @@ __device__ __forceinline__ PixelRow pixel_row(const TcParams& P, int b, int oy, 
   PixelRow r;
   const int64_t idx = (((int64_t)b * in.nblk * in.h + iy0) * in.w + ix0) * in.cb;
   r.base = in.base + idx;
-  r.hbase = reinterpret_cast<const __half*>(in.base) + idx;
+  r.hbase = in.split ? in.hi() + (((int64_t)b * in.hp + iy0 + 1) * in.wp + ix0 + 1) * 8 : nullptr;
   r.ymask = r.xmask = 0;
   if (valid) {
     for (int k = 0; k < a.kh; ++k) r.ymask |= (uint32_t)(iy0 + k >= 0 && iy0 + k < in.h) << k;
@@ -215,15 +215,18 @@ __device__ __forceinline__ void store_sub16(const TcParams& P, const float4* f, 
 template <int CBS, bool SPL>
 struct SubBuf {
   float4 f[8];
-  __device__ __forceinline__ void load(const int2* seg, int h, const PixelRow& px, int64_t) {
+  __device__ __forceinline__ void load(const int2* seg, int h, const PixelRow& px, const TensorView&) {
     load_kblock<CBS>(seg, h, px, f);
   }
 };
 template <int CBS>
 struct SubBuf<CBS, true> {
   uint32_t hw[16], lw[16];
-  __device__ __forceinline__ void load(const int2* __restrict__ seg, int h, const PixelRow& px, int64_t plane) {
+  // split layout: a segment's cb channels are cb/8 groups of 16 bytes, one per
+  // 8-channel plane (kstride apart); cb = 4 is the first half of a group
+  __device__ __forceinline__ void load(const int2* __restrict__ seg, int h, const PixelRow& px, const TensorView& in) {
     constexpr int SEGS = 32 >> CBS, WPS = (1 << CBS) / 2;  // segments, words per segment
+    const int64_t plane = in.plane;
 #pragma unroll
     for (int g = 0; g < SEGS; ++g) {
       const int2 e = seg[h * SEGS + g];
@@ -232,8 +235,9 @@ struct SubBuf<CBS, true> {
       if (WPS >= 4) {
 #pragma unroll
         for (int q = 0; q < WPS / 4; ++q) {
-          const uint4 a = ok ? __ldg(reinterpret_cast<const uint4*>(src) + q) : make_uint4(0, 0, 0, 0);
-          const uint4 b = ok ? __ldg(reinterpret_cast<const uint4*>(src + plane) + q) : make_uint4(0, 0, 0, 0);
+          const __half* sq = src + q * in.kstride;
+          const uint4 a = ok ? __ldg(reinterpret_cast<const uint4*>(sq)) : make_uint4(0, 0, 0, 0);
+          const uint4 b = ok ? __ldg(reinterpret_cast<const uint4*>(sq + plane)) : make_uint4(0, 0, 0, 0);
           uint32_t* H = hw + g * WPS + 4 * q;
           uint32_t* L = lw + g * WPS + 4 * q;
           H[0] = a.x; H[1] = a.y; H[2] = a.z; H[3] = a.w;
@@ -327,9 +331,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       if (s2 < P.nseg) {
         const int blk = s2 / P.taps, tap = s2 - blk * P.taps;
         const int ky = tap / a.kw, kx = tap - ky * a.kw;
-        // staged: float offset inside the staged box; direct: inside the tensor
-        e = P.staged ? make_int2((ky * P.box_w + kx) * in.cb, ky | (kx << 8))
-                     : make_int2(((blk * in.h + ky) * in.w + kx) * in.cb, ky | (kx << 8));
+        // staged: float offset inside the staged box; direct: inside the
+        // tensor (split: halves from the pixel's first 8-channel group)
+        e = P.staged  ? make_int2((ky * P.box_w + kx) * in.cb, ky | (kx << 8))
+            : in.split ? make_int2((int)(blk * (in.cb >> 3) * in.kstride + (ky * in.wp + kx) * 8), ky | (kx << 8))
+                       : make_int2(((blk * in.h + ky) * in.w + kx) * in.cb, ky | (kx << 8));
       }
       seg[s2] = e;
     }
@@ -614,19 +620,18 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       // two register buffers: the next sub-block's loads are in flight while
       // the current one is split and stored
       SubBuf<CBS, SPL> fa, fb;
-      const int64_t plane = a.in.plane;
-      fa.load(seg, h0, px, plane);
-      if (nsb > 1) fb.load(seg, h0 + 1, px, plane);
+      fa.load(seg, h0, px, a.in);
+      if (nsb > 1) fb.load(seg, h0 + 1, px, a.in);
       if (lane == 0 && warp == 4) tr(P, 0, 0x200 | kb0);
       ptx::mbar_wait_warp(ptx::smem_u32(&S->a_empty[s]), par);
       ptx::tc_fence_after();
       const uint32_t t_stage = tmem + lane_off + a_col0 + s * 64 * KS;
       for (int i = 0; i < nsb; i += 2) {
         store_buf<F16>(P, fa, t_stage, i / SUB, i % SUB);
-        if (i + 2 < nsb) fa.load(seg, h0 + i + 2, px, plane);
+        if (i + 2 < nsb) fa.load(seg, h0 + i + 2, px, a.in);
         if (i + 1 < nsb) {
           store_buf<F16>(P, fb, t_stage, (i + 1) / SUB, (i + 1) % SUB);
-          if (i + 3 < nsb) fb.load(seg, h0 + i + 3, px, plane);
+          if (i + 3 < nsb) fb.load(seg, h0 + i + 3, px, a.in);
         }
       }
       if (!(P.dbg & 16)) ptx::tmem_st_wait();
@@ -716,30 +721,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         float sk[16];
         if (e.residual) {
           // the 16 channels are contiguous: cb >= 16 whenever npad >= 16
-          const int64_t ei = e.skip.index(valid ? b : 0, chb, oy, ox);
-          if (e.skip.split) {
-            const uint4* hp = reinterpret_cast<const uint4*>(e.skip.hi() + ei);
-            const uint4* lp = reinterpret_cast<const uint4*>(e.skip.lo() + ei);
+          if (valid) load16_any(e.skip, b, chb, oy, ox, sk);
+          else
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
-              const uint4 h = valid ? __ldg(hp + q) : make_uint4(0, 0, 0, 0);
-              const uint4 l = valid ? __ldg(lp + q) : make_uint4(0, 0, 0, 0);
-              const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {l.x, l.y, l.z, l.w};
-#pragma unroll
-              for (int w = 0; w < 4; ++w) {
-                const float2 a2 = unpack_half2(hw[w]), b2 = unpack_half2(lw[w]);
-                sk[8 * q + 2 * w] = a2.x + b2.x;
-                sk[8 * q + 2 * w + 1] = a2.y + b2.y;
-              }
-            }
-          } else {
-            const float4* sp = reinterpret_cast<const float4*>(e.skip.base + ei);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const float4 f = valid ? __ldg(sp + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-              sk[4 * q] = f.x; sk[4 * q + 1] = f.y; sk[4 * q + 2] = f.z; sk[4 * q + 3] = f.w;
-            }
-          }
+            for (int j = 0; j < 16; ++j) sk[j] = 0.f;
         }
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] += pt[j];

@@ -76,7 +76,13 @@ class Tensor:
         return cpad_for(self.c)
 
     def floats(self, batch: int) -> int:
-        return batch * self.cpad * self.h * self.w
+        """Workspace floats: the larger of the float32 blocked layout and the
+        split fp16 hi/lo layout (two planes [C/8][B][H+2][W+2][8] halves) --
+        libpcnn picks the format per tensor (csrc/common.cuh)."""
+        fp32 = batch * self.cpad * self.h * self.w
+        if self.is_vector:
+            return fp32
+        return max(fp32, -(-self.cpad // 8) * 8 * batch * (self.h + 2) * (self.w + 2))
 
 
 @dataclass

@@ -59,6 +59,10 @@ def test_device_entry_points_fail_loudly_without_gpu():
 
 
 def test_workspace_bytes_is_host_only():
+    # a spatial tensor reserves the larger of its float32 blocked layout and
+    # the split fp16 hi/lo layout (two planes [C/8][B][H+2][W+2][8] halves)
+    split = 8 * 8 * 34 * 34
+    assert split > 8 * 4 * 32 * 32
     descs = L.array(L.TensorDesc, [L.TensorDesc(c=3, h=32, w=32, cb=4, nblk=1, is_vector=0, offset=0),
-                                   L.TensorDesc(c=10, h=1, w=1, cb=16, nblk=1, is_vector=1, offset=4096 * 8)])
-    assert L.lib().pcnn_workspace_bytes(descs, 2, 8) == 4 * (4096 * 8 + 8 * 16)
+                                   L.TensorDesc(c=10, h=1, w=1, cb=16, nblk=1, is_vector=1, offset=split)])
+    assert L.lib().pcnn_workspace_bytes(descs, 2, 8) == 4 * (split + 8 * 16)
