@@ -111,12 +111,16 @@ typedef struct pcnn_unit_desc {
   int64_t impl;                  /* conv: 0 auto (tcgen05 fp16x2 if possible),
                                     1 SIMT fp32, 2 tcgen05 3xTF32,
                                     3 tcgen05 fp16x2 (3 fp16 products),
-                                    4 auto without fp16x2 (all tensors fp32) */
+                                    4 auto without fp16x2 (all tensors fp32),
+                                    5 tcgen05 fp16x2 with A from shared memory
+                                      (halo tiles of split activations)      */
   int64_t tc_off;                /* conv tcgen05 weight image (hi|lo tf32)   */
   int64_t npad;                  /* padded output channels (vector stride)   */
   int64_t tc16_off;              /* conv fp16x2 weight image (hi|lo fp16)    */
   int64_t tc16_scale_off;        /* its {max|w|, 2^-e} pair (2 floats)       */
-  int64_t reserved[3];
+  int64_t tcss_off;              /* conv fp16x2 image of the shared-memory
+                                    (halo tile) kernel, or -1                */
+  int64_t reserved[2];
 } pcnn_unit_desc;
 
 /* ---- parameter packing (float64 master -> float32 compute images) -------*/
@@ -125,8 +129,12 @@ enum pcnn_pack_kind {
   PCNN_PACK_BN_AFFINE = 2,   /* src = gamma,beta,mean,std (each n); dst =
                                 scale=gamma/std [n], shift=beta-scale*mean [n]*/
   PCNN_PACK_TC_WEIGHTS = 3,  /* src [rows][k] float64 -> tcgen05 B image     */
-  PCNN_PACK_TC16_WEIGHTS = 4 /* src [rows][k] float64 -> fp16x2 B image scaled
+  PCNN_PACK_TC16_WEIGHTS = 4,/* src [rows][k] float64 -> fp16x2 B image scaled
                                 by 2^e; aux = float index of {max|w|, 2^-e} */
+  PCNN_PACK_TCSS_WEIGHTS = 5 /* same weights -> image of the shared-memory
+                                conv kernel ([n][16-ch chunk][tap] blocks);
+                                aux = the fp16x2 image's scale pair;
+                                reserved = taps | cb << 16                  */
 };
 
 typedef struct pcnn_pack_desc {

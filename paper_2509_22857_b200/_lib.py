@@ -29,9 +29,9 @@ UNIT_AFFINE, UNIT_LOCALPOOL, UNIT_BIPOOL, UNIT_GLOBALPOOL, UNIT_FLATTEN, UNIT_CO
 # fused pool kinds
 POOL_NONE, POOL_SUM2, POOL_BI2, POOL_GLOBAL = 0, 1, 2, 3
 # pack kinds
-PACK_CAST, PACK_BN_AFFINE, PACK_TC_WEIGHTS, PACK_TC16_WEIGHTS = 1, 2, 3, 4
+PACK_CAST, PACK_BN_AFFINE, PACK_TC_WEIGHTS, PACK_TC16_WEIGHTS, PACK_TCSS_WEIGHTS = 1, 2, 3, 4, 5
 # conv implementations (pcnn_unit_desc.impl)
-IMPL_AUTO, IMPL_SIMT, IMPL_TF32, IMPL_F16X2, IMPL_FP32_TENSORS = 0, 1, 2, 3, 4
+IMPL_AUTO, IMPL_SIMT, IMPL_TF32, IMPL_F16X2, IMPL_FP32_TENSORS, IMPL_F16X2_SS = 0, 1, 2, 3, 4, 5
 # scale opcodes
 (OP_FILL, OP_LOAD, OP_MUL, OP_DIV, OP_SUB, OP_POWI, OP_SROOT, OP_AROOT, OP_RECIP, OP_SOLVE,
  OP_CHECK_UNIFORM, OP_CHECK_NONZERO, OP_CHECK_NONNEG, OP_CHECK_CLOSE, OP_CHECK_ALLONE,
@@ -52,16 +52,16 @@ class TensorDesc(ctypes.Structure):
 _UNIT_FIELDS = ("kind", "in_", "in2", "out", "cin", "cout", "kh", "kw", "stride", "pad",
                 "w_off", "b_off", "affine_off", "residual", "res_off", "poly_deg", "poly_off",
                 "pool", "pool_off", "pool_deg", "pool_order", "in_mode", "in_div_off", "impl",
-                "tc_off", "npad", "tc16_off", "tc16_scale_off")
+                "tc_off", "npad", "tc16_off", "tc16_scale_off", "tcss_off")
 
 
 class UnitDesc(ctypes.Structure):
-    _fields_ = [(n, c_i64) for n in _UNIT_FIELDS] + [("reserved", c_i64 * 3)]
+    _fields_ = [(n, c_i64) for n in _UNIT_FIELDS] + [("reserved", c_i64 * 2)]
 
     def __init__(self, **kw):
         defaults = {"in_": -1, "in2": -1, "out": -1, "w_off": -1, "b_off": -1, "affine_off": -1,
                     "res_off": -1, "poly_off": -1, "pool_off": -1, "in_div_off": -1, "tc_off": -1,
-                    "tc16_off": -1, "tc16_scale_off": -1}
+                    "tc16_off": -1, "tc16_scale_off": -1, "tcss_off": -1}
         defaults.update(kw)
         super().__init__(**defaults)
 

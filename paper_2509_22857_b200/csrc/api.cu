@@ -128,6 +128,11 @@ void choose_formats(pcnn_plan* p) {
     a.in = p->views[u.in];
     a.epi.out = p->views[u.out];
     if (u.residual) a.epi.skip = p->views[u.in2];
+    // fp16x2 convs reading a split tensor: the shared-memory kernel when the
+    // shape allows (unit impl 0, 3 or 5)
+    if (p->impl[i] == 3 && (u.impl == 0 || u.impl == 3 || u.impl == 5) && !getenv("PCNN_NO_SS") &&
+        conv_ss_supported(a))
+      p->impl[i] = 5;
   }
 }
 
@@ -155,6 +160,7 @@ int build_conv(pcnn_plan* p, int ui, ConvArgs& a) {
   a.tcw = P(p, u.tc_off);
   a.tcw16 = P(p, u.tc16_off);
   a.tc16_scale = P(p, u.tc16_scale_off);
+  a.tcwss = P(p, u.tcss_off);
   a.f16 = 0;
   EpiParams& e = a.epi;
   e.cout = (int)u.cout;
@@ -201,7 +207,8 @@ void enqueue_unit(pcnn_plan* p, int ui, const float* x, float* logits, cudaStrea
       const ConvArgs& a = p->conv_args[ui];
       if (u.pool == PCNN_POOL_GLOBAL)
         cudaMemsetAsync(a.epi.out.base, 0, sizeof(float) * (size_t)p->batch * a.epi.out.cpad(), s);
-      if (p->impl[ui] >= 2) launch_conv_tc(a, s);
+      if (p->impl[ui] == 5) launch_conv_ss(a, s);
+      else if (p->impl[ui] >= 2) launch_conv_tc(a, s);
       else launch_conv_simt(a, s);
       break;
     }
@@ -317,14 +324,14 @@ int pcnn_plan_create(const pcnn_unit_desc* units, int n_units, const pcnn_tensor
       }
       // auto: fp16x2 tensor cores, else 3xTF32, else SIMT; 4: auto without fp16x2
       ConvArgs& a = p->conv_args[i];
-      if ((u.impl == 0 || u.impl == 3) && a.tcw16 && a.tc16_scale) {
+      if ((u.impl == 0 || u.impl == 3 || u.impl == 5) && a.tcw16 && a.tc16_scale) {
         a.f16 = 1;
         if (conv_tc_supported(a)) p->impl[i] = 3;
         else a.f16 = 0;
       }
       if (p->impl[i] == 1 && (u.impl == 0 || u.impl == 2 || u.impl == 4) && a.tcw && conv_tc_supported(a))
         p->impl[i] = 2;
-      if (p->impl[i] == 1 && (u.impl == 2 || u.impl == 3)) {
+      if (p->impl[i] == 1 && (u.impl == 2 || u.impl == 3 || u.impl == 5)) {
         delete p;
         return fail(PCNN_ERR_UNSUPPORTED, "unit " + std::to_string(i) + ": tcgen05 conv requested but unsupported");
       }

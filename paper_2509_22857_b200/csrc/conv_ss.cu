@@ -1,0 +1,434 @@
+// tcgen05 fp16x2 convolution with both operands in shared memory ("halo
+// tiles"), for stride-1 3x3 / 1x1 convs whose input is a split tensor.
+//
+// The split layout (common.cuh) stores every 8-channel group as a plane
+// [B][H+2][W+2][8] fp16 with a zero border.  Flatten the padded grid: position
+// g = (b*(H+2) + y')*(W+2) + x'.  Computing the conv on that grid, output g
+// needs input g + (ky-1)*(W+2) + (kx-1) for tap (ky, kx) -- a FIXED offset.
+// So a tile of 128 consecutive grid positions needs one contiguous range of
+// 128 + 2R input positions (R = (W+2) + 1), and for every tap the A operand
+// (M = 128 positions x K = 16 channels) is just that range shifted: a
+// shared-memory descriptor at +offset*16 bytes in a K-major, no-swizzle
+// layout (core matrices = 8 positions x 16 bytes).  No im2col, no converter
+// warps, no A in tensor memory: per 16-channel chunk the producer issues four
+// bulk copies (hi/lo plane x two 8-channel groups) plus one for the weights,
+// and the MMA warp issues taps x {2 | 3} MMAs.  Positions on the border are
+// computed and discarded (waste (H+2)(W+2)/HW - 1).
+//
+// Precision: x = x_hi + x_lo, w = w_hi + w_lo (fp16, weights scaled by 2^e);
+// x*w ~ x_hi w_hi + x_hi w_lo + x_lo w_hi with fp32 accumulation, the main
+// products spread over P partial accumulators (the tensor core truncates when
+// accumulating) and summed in the epilogue -- the same scheme as conv_tc.cu.
+//
+// Warp roles (320 threads, persistent, one CTA per SM): warps 0-3 / 4-7
+// epilogue warpgroups (one per accumulator buffer), warp 8 TMEM allocator +
+// bulk-copy producer, warp 9 MMA issuer.
+#include <cstdlib>
+
+#include "epi_tc.cuh"
+#include "kernels.cuh"
+#include "tc_layout.cuh"
+#include "tc_ptx.cuh"
+
+namespace pcnn {
+
+namespace {
+
+constexpr int kThreads = 320;
+constexpr int kWarpProducer = 8, kWarpMma = 9;
+constexpr int kTileM = 128;
+constexpr int kMaxStages = 8;
+constexpr int kMaxPartials = 4;
+constexpr int kAddsPerPartial = 96;
+
+struct SsParams {
+  ConvArgs a;
+  EpiTab etab;
+  const __half* w;       // weight image
+  const float* wscale;   // 2^-e
+  int nt, n_tiles, m_tiles;
+  int nq;                // 16-channel chunks
+  int taps, kw, wp, hp;  // conv taps; padded grid
+  int halo;              // R: positions before/after a tile
+  int span;              // 128 + 2R
+  int64_t gtotal;        // grid positions (batch * hp * wp)
+  uint32_t a_bytes;      // one 8-channel group of one plane: span * 16
+  uint32_t b_bytes;      // taps * 64 * NT
+  uint32_t stage_bytes;  // 4 * a_bytes + b_bytes
+  int stages, partials, acc_bufs, concat;
+  uint32_t tmem_cols;
+  FastDiv div_hw, div_wp, div_mt;  // grid position decode, tile -> n_tile
+  int dbg;
+};
+
+// PCNN_TC_DEBUG bit 32: CTA 0 records clock64 events (see pcnn_ss_trace)
+constexpr int kTraceLen = 1 << 16;
+constexpr int kTraceRegion = kTraceLen / 4;
+__device__ unsigned long long g_ss_trace[kTraceLen];
+
+struct Tracer {
+  uint32_t n = 0;
+  __device__ __forceinline__ void operator()(const SsParams& P, int region, uint32_t tag) {
+    if ((P.dbg & 32) && blockIdx.x == 0 && n < kTraceRegion)
+      g_ss_trace[region * kTraceRegion + n++] = ((unsigned long long)tag << 48) | (clock64() & 0xFFFFFFFFFFFFull);
+  }
+};
+
+struct Smem {
+  uint64_t full[kMaxStages], empty[kMaxStages];
+  uint64_t acc_full[2], acc_empty[2];
+  uint32_t tmem_base;
+};
+
+
+// ---- one stage (all taps of one 16-channel chunk) in one asm statement ----
+// Every operand is a warp-uniform descriptor and one elected lane issues, so
+// the loop costs no per-MMA address arithmetic in the (single) MMA warp.  A
+// descriptors advance by the tap's grid offset (in the 16-byte units of the
+// start-address field), B by one (chunk, tap) block per tap.
+#define SS_HEAD                                                   \
+  "{\n\t.reg .pred e, p, q, t;\n\t.reg .b32 r;\n\t"                \
+  ".reg .b64 ah, al, bd, bl;\n\t"                                  \
+  "elect.sync r|e, 0xffffffff;\n\tsetp.eq.u32 t, 0, 0;\n\t"
+// concat (NT <= 64): [main | corr] (+)= A_hi [B_hi | B_lo] (N = 2NT);
+// corr += A_lo B_hi.  %0 main, %1 corr, %2 a_hi, %3 a_lo, %4 b, %5 b step,
+// %6 idesc N=2NT, %7 idesc N=NT, %8 main accumulates, %9.. tap offsets
+#define SS_TAP_C(OFF, PRED)                                              \
+  "add.s64 ah, %2, " OFF ";\n\tadd.s64 al, %3, " OFF ";\n\t"            \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ah, bd, %6, " PRED ";\n\t" \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%1], al, bd, %7, t;\n\t"        \
+  "add.s64 bd, bd, %5;\n\t"
+// split (NT = 128): corr (+)= A_lo B_hi; corr += A_hi B_lo; main (+)= A_hi B_hi.
+// %0 main, %1 corr, %2 a_hi, %3 a_lo, %4 b, %5 b step, %6 B_lo offset,
+// %7 idesc, %8 main accumulates, %9 corr accumulates, %10.. tap offsets
+#define SS_TAP_S(OFF, PM, PC)                                            \
+  "add.s64 ah, %2, " OFF ";\n\tadd.s64 al, %3, " OFF ";\n\t"            \
+  "add.s64 bl, bd, %6;\n\t"                                              \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%1], al, bd, %7, " PC ";\n\t"   \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ah, bl, %7, t;\n\t"        \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ah, bd, %7, " PM ";\n\t"   \
+  "add.s64 bd, bd, %5;\n\t"
+
+__device__ __forceinline__ void ss_stage_concat9(uint32_t dm, uint32_t dc, uint64_t ah, uint64_t al, uint64_t b,
+                                                 uint64_t bstep, uint32_t id2, uint32_t id1, uint32_t acc,
+                                                 const uint64_t* o) {
+  asm volatile(SS_HEAD "setp.ne.b32 p, %8, 0;\n\tmov.b64 bd, %4;\n\t"
+               SS_TAP_C("%9", "p") SS_TAP_C("%10", "t") SS_TAP_C("%11", "t") SS_TAP_C("%12", "t")
+               SS_TAP_C("%13", "t") SS_TAP_C("%14", "t") SS_TAP_C("%15", "t") SS_TAP_C("%16", "t")
+               SS_TAP_C("%17", "t") "}\n"
+               ::"r"(dm), "r"(dc), "l"(ah), "l"(al), "l"(b), "l"(bstep), "r"(id2), "r"(id1), "r"(acc),
+               "l"(o[0]), "l"(o[1]), "l"(o[2]), "l"(o[3]), "l"(o[4]), "l"(o[5]), "l"(o[6]), "l"(o[7]), "l"(o[8])
+               : "memory");
+}
+__device__ __forceinline__ void ss_stage_concat1(uint32_t dm, uint32_t dc, uint64_t ah, uint64_t al, uint64_t b,
+                                                 uint64_t bstep, uint32_t id2, uint32_t id1, uint32_t acc,
+                                                 const uint64_t* o) {
+  asm volatile(SS_HEAD "setp.ne.b32 p, %8, 0;\n\tmov.b64 bd, %4;\n\t" SS_TAP_C("%9", "p") "}\n"
+               ::"r"(dm), "r"(dc), "l"(ah), "l"(al), "l"(b), "l"(bstep), "r"(id2), "r"(id1), "r"(acc), "l"(o[0])
+               : "memory");
+}
+__device__ __forceinline__ void ss_stage_split9(uint32_t dm, uint32_t dc, uint64_t ah, uint64_t al, uint64_t b,
+                                                uint64_t bstep, uint64_t blo, uint32_t id, uint32_t accm,
+                                                uint32_t accc, const uint64_t* o) {
+  asm volatile(SS_HEAD "setp.ne.b32 p, %8, 0;\n\tsetp.ne.b32 q, %9, 0;\n\tmov.b64 bd, %4;\n\t"
+               SS_TAP_S("%10", "p", "q") SS_TAP_S("%11", "t", "t") SS_TAP_S("%12", "t", "t")
+               SS_TAP_S("%13", "t", "t") SS_TAP_S("%14", "t", "t") SS_TAP_S("%15", "t", "t")
+               SS_TAP_S("%16", "t", "t") SS_TAP_S("%17", "t", "t") SS_TAP_S("%18", "t", "t") "}\n"
+               ::"r"(dm), "r"(dc), "l"(ah), "l"(al), "l"(b), "l"(bstep), "l"(blo), "r"(id), "r"(accm), "r"(accc),
+               "l"(o[0]), "l"(o[1]), "l"(o[2]), "l"(o[3]), "l"(o[4]), "l"(o[5]), "l"(o[6]), "l"(o[7]), "l"(o[8])
+               : "memory");
+}
+__device__ __forceinline__ void ss_stage_split1(uint32_t dm, uint32_t dc, uint64_t ah, uint64_t al, uint64_t b,
+                                                uint64_t bstep, uint64_t blo, uint32_t id, uint32_t accm,
+                                                uint32_t accc, const uint64_t* o) {
+  asm volatile(SS_HEAD "setp.ne.b32 p, %8, 0;\n\tsetp.ne.b32 q, %9, 0;\n\tmov.b64 bd, %4;\n\t"
+               SS_TAP_S("%10", "p", "q") "}\n"
+               ::"r"(dm), "r"(dc), "l"(ah), "l"(al), "l"(b), "l"(bstep), "l"(blo), "r"(id), "r"(accm), "r"(accc),
+               "l"(o[0])
+               : "memory");
+}
+#undef SS_HEAD
+#undef SS_TAP_C
+#undef SS_TAP_S
+
+template <int TAPS>
+__global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_constant__ SsParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  const ConvArgs& a = P.a;
+  Smem* S = reinterpret_cast<Smem*>(smem + (size_t)P.stages * P.stage_bytes);
+  float* ptab = reinterpret_cast<float*>(smem + (size_t)P.stages * P.stage_bytes + ((sizeof(Smem) + 15) & ~size_t(15)));
+  const uint32_t base = ptx::smem_u32(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int total_tiles = P.m_tiles * P.n_tiles;
+  const int NP = P.partials, NB = P.acc_bufs;
+  const uint32_t set_cols = P.concat ? (uint32_t)NP * 2 * P.nt : (uint32_t)(NP + 1) * P.nt;
+  Tracer tr;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < P.stages; ++i) {
+      ptx::mbar_init(ptx::smem_u32(&S->full[i]), 1);
+      ptx::mbar_init(ptx::smem_u32(&S->empty[i]), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(ptx::smem_u32(&S->acc_full[i]), 1);
+      ptx::mbar_init(ptx::smem_u32(&S->acc_empty[i]), 4);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == kWarpProducer) ptx::tmem_alloc(ptx::smem_u32(&S->tmem_base), P.tmem_cols);
+  epi_fill_tab(a.epi, P.etab, ptab, threadIdx.x, kThreads);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = S->tmem_base;
+
+  if (warp == kWarpProducer) {
+    // ===== producer: per (tile, 16-channel chunk) one stage = the tile's
+    // input range for both planes and both 8-channel groups + the weights =====
+    if (lane == 0) {
+      const __half* hi = a.in.hi();
+      const __half* lo = a.in.lo();
+      int st = 0;
+      uint32_t ph = 0;
+      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        const int n_tile = tile / P.m_tiles, m_tile = tile - n_tile * P.m_tiles;
+        const int64_t gs = (int64_t)m_tile * kTileM - P.halo;
+        const int64_t cs = gs < 0 ? 0 : gs;
+        const int64_t ge = gs + P.span;
+        const int64_t ce = ge > P.gtotal ? P.gtotal : ge;
+        const uint32_t slot0 = (uint32_t)(cs - gs) * 16, bytes = (uint32_t)(ce - cs) * 16;
+        for (int q = 0; q < P.nq; ++q) {
+          if (P.dbg & 2048) ptx::mbar_wait_nohint(ptx::smem_u32(&S->empty[st]), ph ^ 1);
+          else ptx::mbar_wait_sleep(ptx::smem_u32(&S->empty[st]), ph ^ 1);
+          tr(P, 0, 0x100 | q);
+          const uint32_t bar = ptx::smem_u32(&S->full[st]);
+          const uint32_t sb = base + st * P.stage_bytes;
+          ptx::mbar_arrive_tx(bar, 4 * bytes + P.b_bytes);
+#pragma unroll
+          for (int g = 0; g < 2; ++g) {
+            const int64_t off = (2 * q + g) * a.in.kstride + cs * 8;
+            ptx::bulk_g2s(sb + g * P.a_bytes + slot0, hi + off, bytes, bar);
+            ptx::bulk_g2s(sb + (2 + g) * P.a_bytes + slot0, lo + off, bytes, bar);
+          }
+          ptx::bulk_g2s(sb + 4 * P.a_bytes, P.w + ((int64_t)n_tile * P.nq + q) * P.taps * 32 * P.nt, P.b_bytes, bar);
+          if (++st == P.stages) { st = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == kWarpMma) {
+    // ===== MMA issuer: whole warp, one elected lane issues; main products
+    // rotate over the NP partial accumulators per stage =====
+    const uint32_t idesc = ptx::idesc_f16(kTileM, P.nt);
+    const uint32_t idesc2 = ptx::idesc_f16(kTileM, 2 * P.nt);
+    const uint32_t a_lbo = P.a_bytes, b_lbo = 2 * P.nt * 16;
+    const bool do_mma = !(P.dbg & 2);
+    // tap offsets in the descriptors' 16-byte address units
+    uint64_t offs[TAPS];
+#pragma unroll
+    for (int t = 0; t < TAPS; ++t) offs[t] = (uint64_t)((t / P.kw) * P.wp + t % P.kw);
+    const uint64_t bstep = (uint64_t)(64 * P.nt) >> 4, blo = (uint64_t)(P.nt * 16) >> 4;
+    int st = 0;
+    uint32_t ph = 0, acc = 0, acc_ph = 0;
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      ptx::mbar_wait(ptx::smem_u32(&S->acc_empty[acc]), acc_ph ^ 1);
+      ptx::tc_fence_after();
+      const uint32_t d_set = tmem + acc * set_cols;
+      int p = 0;
+      for (int q = 0; q < P.nq; ++q) {
+        tr(P, 1, 0x400 | q);
+        ptx::mbar_wait(ptx::smem_u32(&S->full[st]), ph);
+        tr(P, 1, 0x500 | q);
+        ptx::tc_fence_after();
+        const uint32_t sb = base + st * P.stage_bytes;
+        const uint64_t a_hi = ptx::smem_desc_noswz(sb, a_lbo, 128);
+        const uint64_t a_lo = ptx::smem_desc_noswz(sb + 2 * P.a_bytes, a_lbo, 128);
+        const uint64_t b0 = ptx::smem_desc_noswz(sb + 4 * P.a_bytes, b_lbo, 128);
+        const uint32_t main_acc = q >= NP ? 1u : 0u;
+        if (do_mma) {
+          if (P.concat) {
+            const uint32_t dm = d_set + p * 2 * P.nt;
+            if (TAPS == 9) ss_stage_concat9(dm, dm + P.nt, a_hi, a_lo, b0, bstep, idesc2, idesc, main_acc, offs);
+            else ss_stage_concat1(dm, dm + P.nt, a_hi, a_lo, b0, bstep, idesc2, idesc, main_acc, offs);
+          } else {
+            const uint32_t dm = d_set + p * P.nt, dc = d_set + NP * P.nt;
+            if (TAPS == 9) ss_stage_split9(dm, dc, a_hi, a_lo, b0, bstep, blo, idesc, main_acc, q > 0, offs);
+            else ss_stage_split1(dm, dc, a_hi, a_lo, b0, bstep, blo, idesc, main_acc, q > 0, offs);
+          }
+        }
+        if (++p == NP) p = 0;
+        ptx::mma_commit_warp(ptx::smem_u32(&S->empty[st]));
+        tr(P, 1, 0x600 | q);
+        if (++st == P.stages) { st = 0; ph ^= 1; }
+      }
+      ptx::mma_commit_warp(ptx::smem_u32(&S->acc_full[acc]));
+      if (NB == 2) { acc ^= 1; if (acc == 0) acc_ph ^= 1; } else { acc_ph ^= 1; }
+    }
+  } else if (warp < 8) {
+    // ===== epilogue: warpgroup ew drains accumulator buffer ew =====
+    const int ew = warp >> 2;
+    const EpiParams& e = a.epi;
+    const int row = threadIdx.x & 127;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const float wsc = __ldg(P.wscale);
+    EpiTab etab = P.etab;
+    etab.ptab = ptab;
+    const int hw = P.hp * P.wp;
+    uint32_t acc_it = 0;
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++acc_it) {
+      const uint32_t acc = NB == 2 ? (acc_it & 1) : 0;
+      const uint32_t acc_ph = (NB == 2 ? (acc_it >> 1) : acc_it) & 1;
+      if ((int)acc != ew || (NB == 1 && ew == 1)) continue;
+      const int n_tile = (int)P.div_mt.div(tile), m_tile = tile - n_tile * P.m_tiles;
+      // grid position of this row (g < 2^31) -> image, padded row / column
+      const int g = m_tile * kTileM + row;
+      const int b = (int)P.div_hw.div(g);
+      const int r = g - b * hw;
+      const int yp = (int)P.div_wp.div(r), xp = r - yp * P.wp;
+      const bool valid = g < P.gtotal && yp >= 1 && yp <= a.in.h && xp >= 1 && xp <= a.in.w;
+      // the residual input does not depend on the accumulators: load it first
+      float sk[16];
+      epi_load_skip(e, n_tile * P.nt, valid, b, yp - 1, xp - 1, sk);
+      if (lane == 0 && warp == 0) tr(P, 2, 0x700);
+      ptx::mbar_wait_warp(ptx::smem_u32(&S->acc_full[acc]), acc_ph);
+      if (lane == 0 && warp == 0) tr(P, 2, 0x800);
+      ptx::tc_fence_after();
+      const uint32_t d_set = tmem + lane_off + acc * set_cols;
+      for (int c0 = 0; c0 < ((P.dbg & 4) ? 0 : P.nt); c0 += 16) {
+        float v[16], t[16];
+        if (P.concat) {
+          ptx::tmem_ld16x2(d_set + P.nt + c0, d_set + c0, v, t);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] += t[i];
+          for (int p = 1; p < NP; ++p) {
+            float u[16];
+            ptx::tmem_ld16x2(d_set + 2 * p * P.nt + P.nt + c0, d_set + 2 * p * P.nt + c0, u, t);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] += u[i] + t[i];
+          }
+        } else {
+          ptx::tmem_ld16x2(d_set + NP * P.nt + c0, d_set + c0, v, t);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] += t[i];
+          for (int p = 1; p < NP; ++p) {
+            ptx::tmem_ld16(d_set + p * P.nt + c0, t);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] += t[i];
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] *= wsc;
+        if (lane == 0 && warp == 0) tr(P, 2, 0xD00 | c0);
+        epi_chunk16(e, etab, v, sk, n_tile * P.nt + c0, valid, valid ? b : 0, yp - 1, xp - 1, lane);
+        if (lane == 0 && warp == 0) tr(P, 2, 0xE00 | c0);
+        if (c0 + 16 < P.nt) epi_load_skip(e, n_tile * P.nt + c0 + 16, valid, b, yp - 1, xp - 1, sk);
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->acc_empty[acc]));
+      if (lane == 0 && warp == 0) tr(P, 2, 0x900);
+    }
+  }
+  __syncthreads();
+  if (warp == kWarpProducer) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, P.tmem_cols);
+  }
+}
+
+size_t ss_aux_bytes(const SsParams& P) {
+  return ((sizeof(Smem) + 15) & ~size_t(15)) + (size_t)P.etab.rows * P.a.epi.npad * 4;
+}
+
+bool make_ss_params(const ConvArgs& a, SsParams& P) {
+  const TensorView& in = a.in;
+  if (!a.f16 || !in.split || !a.tcwss || !a.tc16_scale) return false;
+  if (a.stride != 1 || a.kh != a.kw || !((a.kh == 3 && a.pad == 1) || (a.kh == 1 && a.pad == 0))) return false;
+  if (a.epi.pool != PCNN_POOL_NONE && a.epi.pool != PCNN_POOL_GLOBAL) return false;
+  if (in.cpad() % 16 || a.npad < 16 || a.npad % 16) return false;
+  P.a = a;
+  P.nt = a.npad <= 128 ? a.npad : 128;
+  if (a.npad % P.nt) return false;
+  P.n_tiles = a.npad / P.nt;
+  P.hp = in.hp;
+  P.wp = in.wp;
+  P.gtotal = (int64_t)a.batch * in.hp * in.wp;
+  if (P.gtotal >= (1ll << 31)) return false;
+  P.m_tiles = (int)((P.gtotal + kTileM - 1) / kTileM);
+  P.nq = in.cpad() / 16;
+  P.taps = a.kh * a.kw;
+  P.kw = a.kw;
+  P.halo = a.kh == 3 ? in.wp + 1 : 0;
+  P.span = kTileM + 2 * P.halo;
+  P.w = reinterpret_cast<const __half*>(a.tcwss);
+  P.wscale = a.tc16_scale + 1;
+  P.etab = epi_tab_layout(a.epi);
+  P.a_bytes = (uint32_t)P.span * 16;
+  P.b_bytes = (uint32_t)P.taps * 64 * P.nt;
+  P.stage_bytes = 4 * P.a_bytes + P.b_bytes;
+  const size_t budget = 225 * 1024 - 128 - ss_aux_bytes(P);
+  P.stages = (int)(budget / P.stage_bytes);
+  if (P.stages > kMaxStages) P.stages = kMaxStages;
+  if (P.stages < 2) return false;
+  const char* dbg = getenv("PCNN_TC_DEBUG");
+  P.dbg = dbg ? atoi(dbg) : 0;
+  // accumulators: as many partials as accuracy asks for, then two buffers
+  // main products rotate over the partials per stage (taps MMAs each)
+  const int stages_per_partial = kAddsPerPartial / P.taps > 0 ? kAddsPerPartial / P.taps : 1;
+  int want = (P.nq + stages_per_partial - 1) / stages_per_partial;
+  want = want < 1 ? 1 : (want > kMaxPartials ? kMaxPartials : want);
+  P.concat = P.nt <= 64;
+  P.partials = 0;
+  for (int wp = want; wp >= 1 && !P.partials; --wp) {
+    const int set = P.concat ? wp * 2 * P.nt : (wp + 1) * P.nt;
+    if (2 * set <= 512) { P.partials = wp; P.acc_bufs = 2; }
+    else if (set <= 512) { P.partials = wp; P.acc_bufs = 1; }
+  }
+  if (!P.partials) return false;
+  const uint32_t set = P.concat ? P.partials * 2 * P.nt : (P.partials + 1) * P.nt;
+  const uint32_t need = P.acc_bufs * set;
+  P.tmem_cols = need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
+  P.div_hw = make_fastdiv((uint32_t)(P.hp * P.wp));
+  P.div_wp = make_fastdiv((uint32_t)P.wp);
+  P.div_mt = make_fastdiv((uint32_t)P.m_tiles);
+  return true;
+}
+
+}  // namespace
+
+// debugging aid (not part of pcnn.h): drain the CTA-0 event trace
+extern "C" int pcnn_ss_trace(unsigned long long* host, int n) {
+  int m = n < kTraceLen ? n : kTraceLen;
+  cudaMemcpyFromSymbol(host, g_ss_trace, sizeof(unsigned long long) * m);
+  static unsigned long long zeros[kTraceLen];
+  cudaMemcpyToSymbol(g_ss_trace, zeros, sizeof(zeros));
+  return m;
+}
+
+bool conv_ss_supported(const ConvArgs& a) {
+  SsParams P;
+  return make_ss_params(a, P);
+}
+
+void launch_conv_ss(const ConvArgs& a, cudaStream_t s) {
+  SsParams P;
+  if (!make_ss_params(a, P)) return;
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const size_t smem = 128 + (size_t)P.stages * P.stage_bytes + ss_aux_bytes(P);
+  const int tiles = P.m_tiles * P.n_tiles;
+  const int grid = tiles < nsm ? tiles : nsm;
+  if (P.taps == 9) {
+    cudaFuncSetAttribute(conv_ss_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    conv_ss_kernel<9><<<grid, kThreads, smem, s>>>(P);
+  } else {
+    cudaFuncSetAttribute(conv_ss_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    conv_ss_kernel<1><<<grid, kThreads, smem, s>>>(P);
+  }
+}
+
+}  // namespace pcnn

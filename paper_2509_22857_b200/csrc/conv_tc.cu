@@ -35,6 +35,7 @@
 
 #include <cstdlib>
 
+#include "epi_tc.cuh"
 #include "kernels.cuh"
 #include "tc_layout.cuh"
 #include "tc_ptx.cuh"
@@ -80,8 +81,7 @@ struct TcParams {
   int partials;    // main partial accumulators P
   uint32_t b_stage_bytes;
   uint32_t tmem_cols;
-  int ptab_rows;   // per-channel parameter table staged in smem: bias, [affine], [poly], [join]
-  int row_aff, row_poly, row_res;
+  EpiTab etab;     // per-channel parameter table staged in smem (epi_tc.cuh)
   int concat;      // N-concatenated hi|lo B operand (NT <= 64): 2 MMAs per K step
   // TMA-staged input (staged = 1): per (tile, channel block) the input rows a
   // tile needs are loaded as <= `pieces` 4-D boxes (one per image), zero
@@ -277,10 +277,6 @@ __device__ __forceinline__ void store_sub(const TcParams& P, const float4* f, ui
   else store_kblock(P, f, t_stage + j * 32, t_stage + 32 * P.ks + j * 32);
 }
 
-__device__ __forceinline__ void store4(const EpiParams& e, int b, int ch, int y, int x, const float* o) {
-  store4_any(e.out, b, ch, y, x, o[0], o[1], o[2], o[3]);
-}
-
 template <int CBS, bool F16, bool SPL>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_constant__ TcParams P) {
   static_assert(F16 || !SPL, "split-format input feeds the fp16x2 kernel only");
@@ -293,7 +289,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   uint8_t* st_buf = smem + b_region;
   Smem* S = reinterpret_cast<Smem*>(smem + b_region + st_region);
   int2* seg = reinterpret_cast<int2*>(smem + b_region + st_region + ((sizeof(Smem) + 15) & ~size_t(15)));
-  float* ptab = reinterpret_cast<float*>(seg + ((P.nkb * SUB) << (5 - a.in.cbs)));
+  // parameter table: 16-byte aligned (read with ld.shared.v4)
+  float* ptab = reinterpret_cast<float*>(
+      (reinterpret_cast<uintptr_t>(seg + ((P.nkb * SUB) << (5 - a.in.cbs))) + 15) & ~uintptr_t(15));
   const uint32_t b_base = ptx::smem_u32(smem);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -339,17 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       }
       seg[s2] = e;
     }
-    const EpiParams& ep = a.epi;
-    const int np = ep.npad;
-    for (int i = threadIdx.x; i < P.ptab_rows * np; i += kThreads) {
-      const int r = i / np, c = i - r * np;
-      float v;
-      if (r == 0) v = ep.bias[c];
-      else if (P.row_aff >= 0 && r < P.row_aff + 2 && r >= P.row_aff) v = ep.aff[(r - P.row_aff) * np + c];
-      else if (P.row_poly >= 0 && r >= P.row_poly && r <= P.row_poly + ep.poly_deg) v = ep.poly[(r - P.row_poly) * np + c];
-      else v = ep.res[(r - P.row_res) * np + c];
-      ptab[i] = v;
-    }
+    epi_fill_tab(a.epi, P.etab, ptab, threadIdx.x, kThreads);
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -651,6 +639,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     const EpiParams& e = a.epi;
     const int row = threadIdx.x & 127;
     const float wsc = F16 ? __ldg(P.wscale) : 1.f;
+    EpiTab etab = P.etab;
+    etab.ptab = ptab;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     uint32_t acc_it = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++acc_it) {
@@ -667,7 +657,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       const bool valid = m < M;
       if (valid) a.pm.decode(m, b, oy, ox);
       const uint32_t d_set = tmem + lane_off + acc * acc_set_cols;
-      const int np = e.npad;
       for (int c0 = 0; c0 < ((P.dbg & 4) ? 0 : P.nt); c0 += 16) {
         float v[16], t[16];
         if (P.concat) {
@@ -717,94 +706,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             for (int j = 0; j < 16; ++j) v[j] *= wsc;
           }
         }
-        const float* pt = ptab + chb;  // per-channel parameters, shared by all rows
         float sk[16];
-        if (e.residual) {
-          // the 16 channels are contiguous: cb >= 16 whenever npad >= 16
-          if (valid) load16_any(e.skip, b, chb, oy, ox, sk);
-          else
-#pragma unroll
-            for (int j = 0; j < 16; ++j) sk[j] = 0.f;
-        }
-#pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] += pt[j];
-        if (P.row_aff >= 0) {
-          const float* sc = pt + P.row_aff * np;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = fmaf(v[j], sc[j], sc[np + j]);
-        }
-        if (e.residual == 1) {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] += sk[j];
-        } else if (e.residual >= 2) {
-          const float* rc = pt + P.row_res * np;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const float xv = e.residual == 2 ? v[j] : sk[j], yv = e.residual == 2 ? sk[j] : v[j];
-            v[j] = fmaf(rc[j] * xv, xv, fmaf(rc[np + j] * yv, yv, fmaf(rc[2 * np + j] * xv, yv,
-                   fmaf(rc[3 * np + j], xv, fmaf(rc[4 * np + j], yv, rc[5 * np + j])))));
-          }
-        }
-        if (e.poly_deg) {
-          const float* pc = pt + P.row_poly * np;
-          float h[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) h[j] = pc[e.poly_deg * np + j];
-          for (int k = e.poly_deg - 1; k >= 0; --k) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) h[j] = fmaf(h[j], v[j], pc[k * np + j]);
-          }
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = h[j];
-        }
-#pragma unroll
-        for (int j = 0; j < 16; ++j)
-          if (!valid || chb + j >= e.cout) v[j] = 0.f;
-        if (e.pool == PCNN_POOL_NONE) {
-          // the 16 channels are contiguous (cb >= 16)
-          if (lane == 0 && warp == 0) tr(P, 2, 0xE00 | c0);
-          if (valid) store16_any(e.out, b, chb, oy, ox, v);
-          continue;
-        }
-#pragma unroll
-        for (int grp = 0; grp < 4; ++grp) {
-          float* o = v + grp * 4;
-          const int ch0 = chb + grp * 4;
-          if (e.pool == PCNN_POOL_NONE) {
-            if (valid) store4(e, b, ch0, oy, ox, o);
-          } else if (e.pool == PCNN_POOL_GLOBAL) {
-            const float div = __ldg(e.pool_p);
-            const int b0 = __shfl_sync(0xffffffffu, b, 0);
-            const bool uniform = __all_sync(0xffffffffu, valid && b == b0);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              float sum = o[j] * div;
-              if (uniform) {
-#pragma unroll
-                for (int off = 16; off; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
-                if (lane == 0 && ch0 + j < e.cout) atomicAdd(e.out.base + (int64_t)b0 * e.npad + ch0 + j, sum);
-              } else if (valid && ch0 + j < e.cout) {
-                atomicAdd(e.out.base + (int64_t)b * e.npad + ch0 + j, sum);
-              }
-            }
-          } else {
-            // WINDOW order: lanes 4q..4q+3 hold the (dy, dx) = 00, 01, 10, 11 window pixels
-            float q1[4], q2[4], q3[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              q1[j] = __shfl_down_sync(0xffffffffu, o[j], 1);
-              q2[j] = __shfl_down_sync(0xffffffffu, o[j], 2);
-              q3[j] = __shfl_down_sync(0xffffffffu, o[j], 3);
-            }
-            if (valid && (lane & 3) == 0) {
-              float pr[4];
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-                pr[j] = (ch0 + j < e.cout) ? epi_pool4(e, ch0 + j, o[j], q1[j], q2[j], q3[j]) : 0.f;
-              store4(e, b, ch0, oy >> 1, ox >> 1, pr);
-            }
-          }
-        }
+        epi_load_skip(e, chb, valid, b, oy, ox, sk);
+        epi_chunk16(e, etab, v, sk, chb, valid, b, oy, ox, lane);
       }
       ptx::tc_fence_before();
       __syncwarp();
@@ -842,15 +746,7 @@ bool make_params(const ConvArgs& a, TcParams& P) {
   P.taps = a.kh * a.kw;
   P.nseg = a.in.nblk * P.taps;
   P.b_stage_bytes = (uint32_t)(2 * P.nt * kTcBK * 4);
-  const EpiParams& e = a.epi;
-  int rows = 1;
-  P.row_aff = e.aff ? rows : -1;
-  rows += e.aff ? 2 : 0;
-  P.row_poly = e.poly_deg ? rows : -1;
-  rows += e.poly_deg ? e.poly_deg + 1 : 0;
-  P.row_res = e.residual >= 2 ? rows : -1;
-  rows += e.residual >= 2 ? 6 : 0;
-  P.ptab_rows = rows;
+  P.etab = epi_tab_layout(a.epi);
   const size_t aux = smem_aux_bytes(P);
   const size_t budget = 225 * 1024;
   // staged input if a tile needs few boxes and everything fits
@@ -911,7 +807,7 @@ bool make_params(const ConvArgs& a, TcParams& P) {
 
 size_t smem_aux_bytes(const TcParams& P) {
   const size_t segs = (size_t)(P.nkb * P.sub) << (5 - P.a.in.cbs);
-  return ((sizeof(Smem) + 15) & ~size_t(15)) + segs * sizeof(int2) + (size_t)P.ptab_rows * P.a.epi.npad * 4;
+  return ((sizeof(Smem) + 15) & ~size_t(15)) + segs * sizeof(int2) + 16 + (size_t)P.etab.rows * P.a.epi.npad * 4;
 }
 
 size_t smem_bytes(const TcParams& P) {

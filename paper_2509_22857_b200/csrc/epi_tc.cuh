@@ -1,0 +1,162 @@
+// Fused conv epilogue of the tcgen05 kernels for one pixel row and 16
+// consecutive output channels: bias -> [affine] -> [residual: + skip |
+// S(v, skip)] -> [polynomial] -> [pool] -> store in the output's format.
+// Per-channel parameters come from a table staged in shared memory (rows of
+// npad floats: bias, [affine scale, shift], [poly c_0..c_d], [join x2 y2 xy x
+// y c]).  Restates epilogue.cuh's epi_point / epi_pool4 16 channels at a time.
+#pragma once
+
+#include "epilogue.cuh"
+
+namespace pcnn {
+
+struct EpiTab {
+  const float* ptab;  // shared memory
+  int rows;
+  int row_aff, row_poly, row_res;  // -1 if absent
+};
+
+inline EpiTab epi_tab_layout(const EpiParams& e) {
+  EpiTab t;
+  t.ptab = nullptr;
+  int rows = 1;
+  t.row_aff = e.aff ? rows : -1;
+  rows += e.aff ? 2 : 0;
+  t.row_poly = e.poly_deg ? rows : -1;
+  rows += e.poly_deg ? e.poly_deg + 1 : 0;
+  t.row_res = e.residual >= 2 ? rows : -1;
+  rows += e.residual >= 2 ? 6 : 0;
+  t.rows = rows;
+  return t;
+}
+
+__device__ __forceinline__ void epi_fill_tab(const EpiParams& ep, const EpiTab& T, float* ptab, int tid, int nthreads) {
+  const int np = ep.npad;
+  for (int i = tid; i < T.rows * np; i += nthreads) {
+    const int r = i / np, c = i - r * np;
+    float v;
+    if (r == 0) v = ep.bias[c];
+    else if (T.row_aff >= 0 && r < T.row_aff + 2 && r >= T.row_aff) v = ep.aff[(r - T.row_aff) * np + c];
+    else if (T.row_poly >= 0 && r >= T.row_poly && r <= T.row_poly + ep.poly_deg) v = ep.poly[(r - T.row_poly) * np + c];
+    else v = ep.res[(r - T.row_res) * np + c];
+    ptab[i] = v;
+  }
+}
+
+__device__ __forceinline__ void epi_store4(const EpiParams& e, int b, int ch, int y, int x, const float* o) {
+  store4_any(e.out, b, ch, y, x, o[0], o[1], o[2], o[3]);
+}
+
+// skip values of channels [chb, chb + 16) for a residual epilogue (zeros
+// for an invalid row); issued ahead of the accumulator wait by the callers
+__device__ __forceinline__ void epi_load_skip(const EpiParams& e, int chb, bool valid, int b, int oy, int ox,
+                                              float* sk) {
+  if (e.residual && valid) {
+    load16_any(e.skip, b, chb, oy, ox, sk);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) sk[j] = 0.f;
+  }
+}
+
+// v: accumulator values of channels [chb, chb + 16) (scaled to true units);
+// sk: their skip values (epi_load_skip); lanes of a warp hold consecutive
+// pixel rows (WINDOW order for 2x2 pools)
+__device__ __forceinline__ void epi_chunk16(const EpiParams& e, const EpiTab& T, float* v, const float* sk, int chb,
+                                            bool valid, int b, int oy, int ox, int lane) {
+  const float* pt = T.ptab + chb;  // per-channel parameters, shared by all rows
+  const int np = e.npad;
+  float c[16];
+  lds16(pt, c);
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] += c[j];
+  if (T.row_aff >= 0) {
+    float sc[16], sh[16];
+    lds16(pt + T.row_aff * np, sc);
+    lds16(pt + (T.row_aff + 1) * np, sh);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = fmaf(v[j], sc[j], sh[j]);
+  }
+  if (e.residual == 1) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] += sk[j];
+  } else if (e.residual >= 2) {
+    // S(x, y) = x2 x^2 + y2 y^2 + xy x y + cx x + cy y + c, 4 channels at a time
+    const float* rc = pt + T.row_res * np;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      float k[6][4];
+#pragma unroll
+      for (int r = 0; r < 6; ++r) {
+        const float4 f = lds4(rc + r * np + 4 * g);
+        k[r][0] = f.x; k[r][1] = f.y; k[r][2] = f.z; k[r][3] = f.w;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int j = 4 * g + i;
+        const float xv = e.residual == 2 ? v[j] : sk[j], yv = e.residual == 2 ? sk[j] : v[j];
+        v[j] = fmaf(k[0][i] * xv, xv, fmaf(k[1][i] * yv, yv, fmaf(k[2][i] * xv, yv,
+               fmaf(k[3][i], xv, fmaf(k[4][i], yv, k[5][i])))));
+      }
+    }
+  }
+  if (e.poly_deg) {
+    const float* pc = pt + T.row_poly * np;
+    float h[16], ck[16];
+    lds16(pc + e.poly_deg * np, h);
+    for (int k = e.poly_deg - 1; k >= 0; --k) {
+      lds16(pc + k * np, ck);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) h[j] = fmaf(h[j], v[j], ck[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = h[j];
+  }
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (!valid || chb + j >= e.cout) v[j] = 0.f;
+  if (e.pool == PCNN_POOL_NONE) {
+    // the 16 channels are contiguous (cb >= 16)
+    if (valid) store16_any(e.out, b, chb, oy, ox, v);
+    return;
+  }
+#pragma unroll
+  for (int grp = 0; grp < 4; ++grp) {
+    float* o = v + grp * 4;
+    const int ch0 = chb + grp * 4;
+    if (e.pool == PCNN_POOL_GLOBAL) {
+      const float div = __ldg(e.pool_p);
+      const int b0 = __shfl_sync(0xffffffffu, b, 0);
+      const bool uniform = __all_sync(0xffffffffu, valid && b == b0);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float sum = o[j] * div;
+        if (uniform) {
+#pragma unroll
+          for (int off = 16; off; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+          if (lane == 0 && ch0 + j < e.cout) atomicAdd(e.out.base + (int64_t)b0 * e.npad + ch0 + j, sum);
+        } else if (valid && ch0 + j < e.cout) {
+          atomicAdd(e.out.base + (int64_t)b * e.npad + ch0 + j, sum);
+        }
+      }
+    } else {
+      // WINDOW order: lanes 4q..4q+3 hold the (dy, dx) = 00, 01, 10, 11 window pixels
+      float q1[4], q2[4], q3[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        q1[j] = __shfl_down_sync(0xffffffffu, o[j], 1);
+        q2[j] = __shfl_down_sync(0xffffffffu, o[j], 2);
+        q3[j] = __shfl_down_sync(0xffffffffu, o[j], 3);
+      }
+      if (valid && (lane & 3) == 0) {
+        float pr[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          pr[j] = (ch0 + j < e.cout) ? epi_pool4(e, ch0 + j, o[j], q1[j], q2[j], q3[j]) : 0.f;
+        epi_store4(e, b, ch0, oy >> 1, ox >> 1, pr);
+      }
+    }
+  }
+}
+
+}  // namespace pcnn

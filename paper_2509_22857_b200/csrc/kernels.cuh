@@ -18,6 +18,7 @@ struct ConvArgs {
   const float* tcw;  // tcgen05 weight image (3xTF32) or null
   const float* tcw16;       // fp16x2 weight image or null
   const float* tc16_scale;  // {max|w|, 2^-e} of the fp16x2 image
+  const float* tcwss;       // fp16x2 image of the shared-memory kernel or null
   int f16;                  // launch_conv_tc: 1 = fp16x2 (kind::f16), 0 = 3xTF32
   EpiParams epi;
 };
@@ -57,5 +58,10 @@ void launch_copyout(const TensorView& t, float* dst, int batch, cudaStream_t s);
 bool conv_tc_supported(const ConvArgs& a);
 void launch_conv_tc(const ConvArgs& a, cudaStream_t s);
 void tc_weight_image_dims(int npad, int kp, int64_t* floats);
+
+// fp16x2 conv with A from shared memory (conv_ss.cu): stride-1 3x3/1x1 convs
+// reading a split tensor
+bool conv_ss_supported(const ConvArgs& a);
+void launch_conv_ss(const ConvArgs& a, cudaStream_t s);
 
 }  // namespace pcnn

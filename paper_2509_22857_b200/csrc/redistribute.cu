@@ -170,6 +170,11 @@ __global__ void pack_kernel(const double* __restrict__ master, float* __restrict
       }
     } else if (o.kind == PCNN_PACK_TC_WEIGHTS) {
       pack_tc_weights_device(master + o.src, packed + o.dst, (int)o.rows, (int)o.k, tid, nthreads);
+    } else if (o.kind == PCNN_PACK_TCSS_WEIGHTS) {
+      // shares the fp16x2 image's scale pair (computed by pack_amax_kernel)
+      const int e = tc16_scale_exp(packed[o.aux]);
+      pack_tcss_weights_device(master + o.src, reinterpret_cast<__half*>(packed + o.dst), (int)o.rows, (int)o.k,
+                               (int)(o.reserved & 0xFFFF), (int)(o.reserved >> 16), e, tid, nthreads);
     } else if (o.kind == PCNN_PACK_TC16_WEIGHTS) {
       const int e = tc16_scale_exp(packed[o.aux]);
       if (tid == 0) packed[o.aux + 1] = ldexpf(1.f, -e);

@@ -109,4 +109,35 @@ __device__ inline void pack_tc16_weights_device(const double* src, __half* dst, 
   }
 }
 
+// ---- fp16x2 image of the shared-memory (halo tile) conv kernel ---------------------
+// K-block = one (16-channel chunk q, tap t); per block the B operand is
+// [kc8 = 2][2 NT rows: hi then lo][8 fp16], K-major without swizzle (core
+// matrices of 8 rows x 16 bytes), so [B_hi | B_lo] is one N = 2 NT operand.
+// Global order [n_tile][q][tap][block]: a stage streams taps consecutive blocks.
+__host__ __device__ inline int64_t tcss_image_floats(int npad, int cpad, int taps) {
+  const int nt_rows = tc_ntile(npad);
+  const int ntiles = (npad + nt_rows - 1) / nt_rows;
+  return (int64_t)ntiles * (cpad / 16) * taps * 16 * nt_rows;
+}
+
+__device__ inline void pack_tcss_weights_device(const double* src, __half* dst, int rows, int k, int taps, int cb,
+                                                int e, int64_t tid, int64_t nthreads) {
+  const int NT = tc_ntile(rows);
+  const int cpad = k / taps, nq = cpad / 16;
+  const int64_t total = (int64_t)rows * cpad * taps;
+  for (int64_t i = tid; i < total; i += nthreads) {
+    const int n = (int)(i / ((int64_t)cpad * taps));
+    const int rem = (int)(i - (int64_t)n * cpad * taps);
+    const int t = rem / cpad, ch = rem - t * cpad;
+    const double w = ldexp(src[(int64_t)n * k + ((ch / cb) * taps + t) * cb + ch % cb], e);
+    const __half hi = __double2half(w);
+    const __half lo = __double2half(w - (double)__half2float(hi));
+    const int q = ch >> 4, g = (ch >> 3) & 1, j = ch & 7;
+    const int nt = n / NT, r = n - nt * NT;
+    const int64_t base = (((int64_t)nt * nq + q) * taps + t) * 32 * NT + g * 16 * NT;
+    dst[base + r * 8 + j] = hi;
+    dst[base + (NT + r) * 8 + j] = lo;
+  }
+}
+
 }  // namespace pcnn

@@ -79,6 +79,12 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
     if (++spins > (1u << 20)) __trap();
   }
 }
+__device__ __forceinline__ void mbar_wait_nohint(uint32_t bar, uint32_t parity) {
+  uint32_t spins = 0;
+  while (!mbar_try(bar, parity)) {
+    if (++spins > (1u << 28)) __trap();
+  }
+}
 
 // One lane waits, the warp follows (keeps 31 lanes off the barrier unit).
 __device__ __forceinline__ void mbar_wait_warp(uint32_t bar, uint32_t parity) {
@@ -288,6 +294,29 @@ __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.
 
 // ---- descriptors -------------------------------------------------------------
 // K-major operand, 128-byte swizzle, 8-row atoms 1024 B apart (SBO), version 1.
+// K-major, no swizzle: core matrices of 8 rows x 16 bytes (rows 16 B apart);
+// lbo = bytes between core matrices adjacent in K, sbo = adjacent in M/N.
+__device__ __forceinline__ uint64_t smem_desc_noswz(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version (sm_100); layout 0 = SWIZZLE_NONE
+  return d;
+}
+
+// D[tmem] (+)= A[smem desc] * B[smem desc], kind::f16, issued by one elected lane
+__device__ __forceinline__ void mma_f16_ss_warp(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\t"
+      "elect.sync r|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);       // start address

@@ -130,7 +130,8 @@ class Lowered:
 
     def pack_descs(self):
         return L.array(L.PackDesc, [L.PackDesc(kind=op[0], src=op[1], dst=op[2], n=op[3], rows=op[4], k=op[5],
-                                               aux=op[6] if len(op) > 6 else 0, reserved=0)
+                                               aux=op[6] if len(op) > 6 else 0,
+                                               reserved=op[7] if len(op) > 7 else 0)
                                     for op in self.pack_ops])
 
 
@@ -372,6 +373,21 @@ class _Builder:
         self.pack.append((L.PACK_TC16_WEIGHTS, s.offset, dst, floats, npad, kp, scale))
         return dst, scale
 
+    def tcss_image(self, nid: str, scale: int) -> int:
+        """fp16x2 image of the shared-memory (halo tile) kernel: blocks of
+        [2 x 8-channel groups][hi NT rows | lo NT rows][8] per (16-channel
+        chunk, tap); shares the fp16x2 image's scale pair."""
+        s = self.slots[nid]["weight"]
+        m = s.meta
+        npad, kp, taps, cb = m["npad"], m["kp"], m["kh"] * m["kw"], m["cb"]
+        ntile = npad if npad <= 128 else 128
+        cpad = kp // taps
+        floats = ((npad + ntile - 1) // ntile) * (cpad // 16) * taps * 16 * ntile
+        dst = self.packed
+        self.packed += _align(floats)
+        self.pack.append((L.PACK_TCSS_WEIGHTS, s.offset, dst, floats, npad, kp, scale, taps | (cb << 16)))
+        return dst
+
     def emit(self, nodes: List[str], **u) -> None:
         self.units.append(u)
         self.unit_nodes.append(nodes)
@@ -488,6 +504,10 @@ class _Builder:
         if self.use_tc and wmeta["npad"] % 16 == 0 and wmeta["npad"] >= 16:
             u["tc_off"] = self.tc_image(nid)
             u["tc16_off"], u["tc16_scale_off"] = self.tc16_image(nid)
+            k, st, pd = wmeta["kh"], u["stride"], u["pad"]
+            if (wmeta["kh"] == wmeta["kw"] and st == 1 and ((k == 3 and pd == 1) or (k == 1 and pd == 0))
+                    and (wmeta["kp"] // (k * k)) % 16 == 0 and u.get("pool", 0) in (L.POOL_NONE, L.POOL_GLOBAL)):
+                u["tcss_off"] = self.tcss_image(nid, u["tc16_scale_off"])
         t = self.tensor(out_shape)
         u["out"] = t
         for c in chain[1:]:

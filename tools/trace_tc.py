@@ -11,7 +11,7 @@ cfgname = sys.argv[2] if len(sys.argv) > 2 else "resnet20"
 x = torch.from_numpy(configs.make_input(configs.CONFIGS[cfgname]).astype(np.float32)).cuda()
 out = eng.forward(x)
 lib = L.lib()
-fn = lib.pcnn_tc_trace
+fn = lib.pcnn_ss_trace if os.environ.get("SS") else lib.pcnn_tc_trace
 fn.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
 buf = (ctypes.c_ulonglong * 65536)()
 for i in range(unit):
