@@ -143,11 +143,17 @@ def per_unit_times(eng, x, out, reps, flush):
     return acc / reps  # ms per unit
 
 
-def roofline(eng, batch, unit_ms):
+def roofline(eng, batch, unit_ms, plan):
+    """Per conv unit: time at the roofline = max(flops / P, bytes / BW) with P
+    the unit's fp32-accurate tensor rate -- three fp16 products at the dense
+    fp16 (= bf16) rate for the fp16x2 kernels (impl 3, 5), three TF32 passes
+    (TF32 = bf16 / 2) for the 3xTF32 kernel."""
     hbm, bf16, bf16s, basis = peaks()
-    p_tc = bf16 / 2.0 / 3.0  # 3xTF32-effective fp32 rate (TF32 = bf16/2, three passes)
+    p_f16 = bf16 / 3.0
+    p_tf32 = bf16 / 2.0 / 3.0
     lw = eng.lw
     F = B = T = Troof = 0.0
+    p_tc = p_f16
     rows = []
     for i, u in enumerate(lw.units):
         if u.get("kind") != 2:
@@ -155,7 +161,9 @@ def roofline(eng, batch, unit_ms):
         f, b = unit_cost(lw, u, batch)
         t = unit_ms[i] * 1e-3
         F, B, T = F + f, B + b, T + t
-        tr = max(f / (p_tc * 1e12), b / (hbm * 1e9))
+        p_unit = p_f16 if plan.unit_impl(i) in (3, 5) else p_tf32
+        p_tc = min(p_tc, p_unit)
+        tr = max(f / (p_unit * 1e12), b / (hbm * 1e9))
         Troof += tr
         rows.append((f, b, t, tr))
     total = float(np.sum(unit_ms)) * 1e-3
@@ -167,7 +175,8 @@ def roofline(eng, batch, unit_ms):
     return {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": unit,
             "frac": round(achieved / peak, 4), "traffic": None,
             "kernel": "conv units (fused implicit-GEMM conv + epilogue), %d launches/step" % len(rows),
-            "peak_basis": f"{basis} bf16_tflops/2/3 = 3xTF32-effective fp32 tensor rate; hbm_gbs {hbm}",
+            "peak_basis": f"{basis}: fp16x2 units bf16_tflops/3 (three fp16 products), 3xTF32 units "
+                          f"bf16_tflops/6; peak = the lower rate in use; hbm_gbs {hbm}",
             "roofline_time_frac": round(Troof / T, 4) if T else None,
             "conv_share_of_step": round(T / total, 4) if total else None,
             "algorithmic_flops_per_step": F, "algorithmic_bytes_per_step": B}
@@ -437,7 +446,7 @@ def run_ours(args):
             torch.distributed.destroy_process_group()
         return
     unit_ms = per_unit_times(eng, x, out, reps=max(3, min(args.steps, 10)), flush=flush)
-    roof = roofline(eng, batch, unit_ms)
+    roof = roofline(eng, batch, unit_ms, plan)
     launches = plan.launches()
     line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,

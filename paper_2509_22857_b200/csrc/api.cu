@@ -99,7 +99,8 @@ void choose_formats(pcnn_plan* p) {
     const bool tc16 = u.kind == PCNN_UNIT_CONV && p->impl[i] == 3;
     if (u.out >= 0) {
       produced[u.out] = 1;
-      if (!(u.kind == PCNN_UNIT_INGEST || (tc16 && u.pool != PCNN_POOL_GLOBAL))) ok[u.out] = 0;
+      const bool pool_split = u.kind == PCNN_UNIT_LOCALPOOL && p->tensors[u.in].cb == p->tensors[u.out].cb;
+      if (!(u.kind == PCNN_UNIT_INGEST || pool_split || (tc16 && u.pool != PCNN_POOL_GLOBAL))) ok[u.out] = 0;
     }
     if (u.in >= 0 && !tc16) ok[u.in] = 0;
     if (u.in2 >= 0 && !(tc16 && u.residual)) ok[u.in2] = 0;

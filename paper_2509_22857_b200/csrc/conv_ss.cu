@@ -48,6 +48,7 @@ struct SsParams {
   const float* wscale;   // 2^-e
   int nt, n_tiles, m_tiles;
   int nq;                // 16-channel chunks
+  int last_groups;       // 8-channel groups in the last chunk (1 when cpad is 4 or 8)
   int taps, kw, wp, hp;  // conv taps; padded grid
   int halo;              // R: positions before/after a tile
   int span;              // 128 + 2R
@@ -74,9 +75,11 @@ struct Tracer {
   }
 };
 
+constexpr int kMaxAcc = 4;  // accumulator buffers in TMEM
+
 struct Smem {
   uint64_t full[kMaxStages], empty[kMaxStages];
-  uint64_t acc_full[2], acc_empty[2];
+  uint64_t acc_full[kMaxAcc], acc_empty[kMaxAcc];
   uint32_t tmem_base;
 };
 
@@ -170,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       ptx::mbar_init(ptx::smem_u32(&S->full[i]), 1);
       ptx::mbar_init(ptx::smem_u32(&S->empty[i]), 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kMaxAcc; ++i) {
       ptx::mbar_init(ptx::smem_u32(&S->acc_full[i]), 1);
       ptx::mbar_init(ptx::smem_u32(&S->acc_empty[i]), 4);
     }
@@ -178,10 +181,23 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
   }
   if (warp == kWarpProducer) ptx::tmem_alloc(ptx::smem_u32(&S->tmem_base), P.tmem_cols);
   epi_fill_tab(a.epi, P.etab, ptab, threadIdx.x, kThreads);
+  if (P.last_groups == 1) {
+    // cpad 4 / 8: the second 8-channel group of every stage stays zero
+    for (int st = 0; st < P.stages; ++st)
+      for (int pl = 0; pl < 2; ++pl) {
+        uint4* z = reinterpret_cast<uint4*>(smem + (size_t)st * P.stage_bytes + (2 * pl + 1) * P.a_bytes);
+        for (uint32_t i = threadIdx.x; i < P.a_bytes / 16; i += kThreads) z[i] = make_uint4(0, 0, 0, 0);
+      }
+    ptx::fence_proxy_async();
+  }
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = S->tmem_base;
+  // everything above reads only parameters; activations come from the
+  // previous kernel
+  ptx::griddep_wait();
+  ptx::griddep_launch();
 
   if (warp == kWarpProducer) {
     // ===== producer: per (tile, 16-channel chunk) one stage = the tile's
@@ -204,9 +220,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
           tr(P, 0, 0x100 | q);
           const uint32_t bar = ptx::smem_u32(&S->full[st]);
           const uint32_t sb = base + st * P.stage_bytes;
-          ptx::mbar_arrive_tx(bar, 4 * bytes + P.b_bytes);
-#pragma unroll
-          for (int g = 0; g < 2; ++g) {
+          const int ng = q == P.nq - 1 ? P.last_groups : 2;
+          ptx::mbar_arrive_tx(bar, 2 * ng * bytes + P.b_bytes);
+          for (int g = 0; g < ng; ++g) {
             const int64_t off = (2 * q + g) * a.in.kstride + cs * 8;
             ptx::bulk_g2s(sb + g * P.a_bytes + slot0, hi + off, bytes, bar);
             ptx::bulk_g2s(sb + (2 + g) * P.a_bytes + slot0, lo + off, bytes, bar);
@@ -262,7 +278,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
         if (++st == P.stages) { st = 0; ph ^= 1; }
       }
       ptx::mma_commit_warp(ptx::smem_u32(&S->acc_full[acc]));
-      if (NB == 2) { acc ^= 1; if (acc == 0) acc_ph ^= 1; } else { acc_ph ^= 1; }
+      if (++acc == (uint32_t)NB) { acc = 0; acc_ph ^= 1; }
     }
   } else if (warp < 8) {
     // ===== epilogue: warpgroup ew drains accumulator buffer ew =====
@@ -276,9 +292,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
     const int hw = P.hp * P.wp;
     uint32_t acc_it = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++acc_it) {
-      const uint32_t acc = NB == 2 ? (acc_it & 1) : 0;
-      const uint32_t acc_ph = (NB == 2 ? (acc_it >> 1) : acc_it) & 1;
-      if ((int)acc != ew || (NB == 1 && ew == 1)) continue;
+      // buffer acc_it % NB, drained by warpgroup (buffer % 2); one buffer: warpgroup 0
+      const uint32_t acc = acc_it % NB;
+      const uint32_t acc_ph = (acc_it / NB) & 1;
+      if ((int)(acc & 1) != ew || (NB == 1 && ew == 1)) continue;
       const int n_tile = (int)P.div_mt.div(tile), m_tile = tile - n_tile * P.m_tiles;
       // grid position of this row (g < 2^31) -> image, padded row / column
       const int g = m_tile * kTileM + row;
@@ -345,7 +362,8 @@ bool make_ss_params(const ConvArgs& a, SsParams& P) {
   if (!a.f16 || !in.split || !a.tcwss || !a.tc16_scale) return false;
   if (a.stride != 1 || a.kh != a.kw || !((a.kh == 3 && a.pad == 1) || (a.kh == 1 && a.pad == 0))) return false;
   if (a.epi.pool != PCNN_POOL_NONE && a.epi.pool != PCNN_POOL_GLOBAL) return false;
-  if (in.cpad() % 16 || a.npad < 16 || a.npad % 16) return false;
+  const int cpad = in.cpad();
+  if (!(cpad == 4 || cpad == 8 || cpad % 16 == 0) || a.npad < 16 || a.npad % 16) return false;
   P.a = a;
   P.nt = a.npad <= 128 ? a.npad : 128;
   if (a.npad % P.nt) return false;
@@ -355,7 +373,8 @@ bool make_ss_params(const ConvArgs& a, SsParams& P) {
   P.gtotal = (int64_t)a.batch * in.hp * in.wp;
   if (P.gtotal >= (1ll << 31)) return false;
   P.m_tiles = (int)((P.gtotal + kTileM - 1) / kTileM);
-  P.nq = in.cpad() / 16;
+  P.nq = (cpad + 15) / 16;
+  P.last_groups = cpad % 16 == 0 ? 2 : 1;
   P.taps = a.kh * a.kw;
   P.kw = a.kw;
   P.halo = a.kh == 3 ? in.wp + 1 : 0;
@@ -381,8 +400,9 @@ bool make_ss_params(const ConvArgs& a, SsParams& P) {
   P.partials = 0;
   for (int wp = want; wp >= 1 && !P.partials; --wp) {
     const int set = P.concat ? wp * 2 * P.nt : (wp + 1) * P.nt;
-    if (2 * set <= 512) { P.partials = wp; P.acc_bufs = 2; }
-    else if (set <= 512) { P.partials = wp; P.acc_bufs = 1; }
+    // up to four buffers: the MMA warp runs ahead of two epilogue warpgroups
+    for (int nb = kMaxAcc; nb >= 1 && !P.partials; --nb)
+      if (nb * set <= 512 && nb != 3) { P.partials = wp; P.acc_bufs = nb; }
   }
   if (!P.partials) return false;
   const uint32_t set = P.concat ? P.partials * 2 * P.nt : (P.partials + 1) * P.nt;
@@ -422,13 +442,9 @@ void launch_conv_ss(const ConvArgs& a, cudaStream_t s) {
   const size_t smem = 128 + (size_t)P.stages * P.stage_bytes + ss_aux_bytes(P);
   const int tiles = P.m_tiles * P.n_tiles;
   const int grid = tiles < nsm ? tiles : nsm;
-  if (P.taps == 9) {
-    cudaFuncSetAttribute(conv_ss_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    conv_ss_kernel<9><<<grid, kThreads, smem, s>>>(P);
-  } else {
-    cudaFuncSetAttribute(conv_ss_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    conv_ss_kernel<1><<<grid, kThreads, smem, s>>>(P);
-  }
+  void (*k)(SsParams) = P.taps == 9 ? conv_ss_kernel<9> : conv_ss_kernel<1>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  launch_pdl(k, grid, kThreads, smem, s, P);
 }
 
 }  // namespace pcnn

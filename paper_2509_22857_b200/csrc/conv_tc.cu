@@ -342,6 +342,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
+  ptx::griddep_wait();  // activations come from the previous kernel
+  ptx::griddep_launch();
   const uint32_t tmem = S->tmem_base;
   const uint32_t a_col0 = (uint32_t)NB * acc_set_cols;
 
@@ -898,7 +900,7 @@ void launch_conv_tc(const ConvArgs& a, cudaStream_t s) {
 #define PCNN_TC_LAUNCH(C, H, SP)                                                                              \
   case C * 4 + (H ? (SP ? 2 : 1) : 0):                                                                        \
     cudaFuncSetAttribute(conv_tc_kernel<C, H, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
-    conv_tc_kernel<C, H, SP><<<grid, kThreads, smem, s>>>(P);                                                 \
+    launch_pdl(conv_tc_kernel<C, H, SP>, grid, kThreads, smem, s, P);                                         \
     break;
     PCNN_TC_LAUNCH(2, false, false)
     PCNN_TC_LAUNCH(3, false, false)

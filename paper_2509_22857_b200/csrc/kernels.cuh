@@ -2,6 +2,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "epilogue.cuh"
 
@@ -53,6 +54,26 @@ void launch_conv_simt(const ConvArgs& a, cudaStream_t s);
 void launch_linear(const LinearArgs& a, cudaStream_t s);
 void launch_eltwise(const EltArgs& a, cudaStream_t s);
 void launch_copyout(const TensorView& t, float* dst, int batch, cudaStream_t s);
+
+// Launch a persistent tcgen05 kernel with programmatic stream serialization:
+// its prologue (barriers, TMEM allocation, parameter table) overlaps the tail
+// of the previous kernel, and griddep_wait() in the kernel orders the data.
+// PCNN_NO_PDL=1 launches it plainly.
+template <typename Params>
+inline void launch_pdl(void (*kernel)(Params), int grid, int threads, size_t smem, cudaStream_t s, const Params& P) {
+  static const bool off = getenv("PCNN_NO_PDL") != nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, P);
+}
 
 // tcgen05 path (conv_tc.cu); returns false if the shape is not supported
 bool conv_tc_supported(const ConvArgs& a);

@@ -387,9 +387,50 @@ __global__ void to_vector_kernel(EltArgs a) {
   }
 }
 
+// k x k / stride local sum pool * divisor.  One thread per (4-channel group,
+// output pixel) with the channel group fastest, so a warp's loads cover whole
+// 128-byte pixel rows of the channel-blocked input; the output may be split.
+__global__ void localpool_kernel(EltArgs a) {
+  const TensorView& in = a.in;
+  const TensorView& o = a.out;
+  const int gpb = in.cb / 4;  // 4-channel groups per channel block
+  const int64_t total = (int64_t)a.batch * o.nblk * o.h * o.w * gpb;
+  const float dv = __ldg(a.p);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int gi = (int)(i % gpb);
+    int64_t r = i / gpb;
+    const int xw = (int)(r % o.w);
+    r /= o.w;
+    const int y = (int)(r % o.h);
+    r /= o.h;
+    const int blk = (int)(r % o.nblk);
+    const int b = (int)(r / o.nblk);
+    const int ch0 = blk * in.cb + gi * 4;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int dy = 0; dy < a.k; ++dy) {
+      const int iy = y * a.st - a.pad + dy;
+      if (iy < 0 || iy >= in.h) continue;
+      for (int dx = 0; dx < a.k; ++dx) {
+        const int ix = xw * a.st - a.pad + dx;
+        if (ix < 0 || ix >= in.w) continue;
+        const float4 v = __ldg(reinterpret_cast<const float4*>(in.at(b, ch0, iy, ix)));
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
+    }
+    store4_any(o, b, ch0, y, xw, acc.x * dv, acc.y * dv, acc.z * dv, acc.w * dv);
+  }
+}
+
 void launch_eltwise(const EltArgs& a, cudaStream_t s) {
   if (a.kind == PCNN_UNIT_GLOBALPOOL || a.kind == PCNN_UNIT_FLATTEN) {
     to_vector_kernel<<<148 * 8, 256, 0, s>>>(a);
+    return;
+  }
+  if (a.kind == PCNN_UNIT_LOCALPOOL && !a.in.split && a.in.cb == a.out.cb) {
+    const int64_t total = (int64_t)a.batch * a.out.nblk * a.out.h * a.out.w * (a.in.cb / 4);
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 32);
+    localpool_kernel<<<std::max(blocks, 1), 256, 0, s>>>(a);
     return;
   }
   int64_t total = (int64_t)a.batch * (a.out.cpad() / 4) * a.out.h * a.out.w;

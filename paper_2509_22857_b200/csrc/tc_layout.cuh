@@ -117,13 +117,13 @@ __device__ inline void pack_tc16_weights_device(const double* src, __half* dst, 
 __host__ __device__ inline int64_t tcss_image_floats(int npad, int cpad, int taps) {
   const int nt_rows = tc_ntile(npad);
   const int ntiles = (npad + nt_rows - 1) / nt_rows;
-  return (int64_t)ntiles * (cpad / 16) * taps * 16 * nt_rows;
+  return (int64_t)ntiles * ((cpad + 15) / 16) * taps * 16 * nt_rows;
 }
 
 __device__ inline void pack_tcss_weights_device(const double* src, __half* dst, int rows, int k, int taps, int cb,
                                                 int e, int64_t tid, int64_t nthreads) {
   const int NT = tc_ntile(rows);
-  const int cpad = k / taps, nq = cpad / 16;
+  const int cpad = k / taps, nq = (cpad + 15) / 16;  // channels >= cpad stay zero
   const int64_t total = (int64_t)rows * cpad * taps;
   for (int64_t i = tid; i < total; i += nthreads) {
     const int n = (int)(i / ((int64_t)cpad * taps));

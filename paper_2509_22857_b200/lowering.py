@@ -382,7 +382,7 @@ class _Builder:
         npad, kp, taps, cb = m["npad"], m["kp"], m["kh"] * m["kw"], m["cb"]
         ntile = npad if npad <= 128 else 128
         cpad = kp // taps
-        floats = ((npad + ntile - 1) // ntile) * (cpad // 16) * taps * 16 * ntile
+        floats = ((npad + ntile - 1) // ntile) * (-(-cpad // 16)) * taps * 16 * ntile
         dst = self.packed
         self.packed += _align(floats)
         self.pack.append((L.PACK_TCSS_WEIGHTS, s.offset, dst, floats, npad, kp, scale, taps | (cb << 16)))
@@ -506,7 +506,8 @@ class _Builder:
             u["tc16_off"], u["tc16_scale_off"] = self.tc16_image(nid)
             k, st, pd = wmeta["kh"], u["stride"], u["pad"]
             if (wmeta["kh"] == wmeta["kw"] and st == 1 and ((k == 3 and pd == 1) or (k == 1 and pd == 0))
-                    and (wmeta["kp"] // (k * k)) % 16 == 0 and u.get("pool", 0) in (L.POOL_NONE, L.POOL_GLOBAL)):
+                    and ((cp := wmeta["kp"] // (k * k)) in (4, 8) or cp % 16 == 0)
+                    and u.get("pool", 0) in (L.POOL_NONE, L.POOL_GLOBAL)):
                 u["tcss_off"] = self.tcss_image(nid, u["tc16_scale_off"])
         t = self.tensor(out_shape)
         u["out"] = t
