@@ -143,43 +143,62 @@ def per_unit_times(eng, x, out, reps, flush):
     return acc / reps  # ms per unit
 
 
-def roofline(eng, batch, unit_ms, plan):
-    """Per conv unit: time at the roofline = max(flops / P, bytes / BW) with P
-    the unit's fp32-accurate tensor rate -- three fp16 products at the dense
-    fp16 (= bf16) rate for the fp16x2 kernels (impl 3, 5), three TF32 passes
-    (TF32 = bf16 / 2) for the 3xTF32 kernel."""
+KERNEL_NAMES = {1: "conv_simt_kernel", 2: "conv_tc_kernel (3xTF32, A in TMEM)",
+                3: "conv_tc_kernel (fp16x2, A in TMEM)", 5: "conv_ss_kernel (fp16x2, halo tiles in smem)"}
+
+
+def measured_traffic(config, kernel):
+    """dram read+write bytes per launch of `kernel` from the committed ncu
+    capture summary (profiles/traffic.json, written by tools/profile_round.py)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            t = json.load(f)
+        return t.get(config, {}).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
+def roofline(eng, batch, unit_ms, plan, config):
+    """Roofline of the dominant kernel (the conv kernel with the largest share
+    of the step), over all its launches in one step: achieved = algorithmic
+    FLOPs (or bytes) / its CUDA-event time.  P is the fp32-accurate tensor
+    rate of that kernel: three fp16 products at the dense fp16 (= bf16) rate
+    for the fp16x2 kernels (impl 3, 5), three TF32 passes (TF32 = bf16 / 2)
+    for the 3xTF32 kernel.  Per unit: time at the roofline = max(flops / P,
+    bytes / BW)."""
     hbm, bf16, bf16s, basis = peaks()
-    p_f16 = bf16 / 3.0
-    p_tf32 = bf16 / 2.0 / 3.0
+    rate = {3: bf16 / 3.0, 5: bf16 / 3.0, 2: bf16 / 6.0, 1: bf16 / 6.0}
     lw = eng.lw
-    F = B = T = Troof = 0.0
-    p_tc = p_f16
-    rows = []
+    groups = {}
+    T = Troof = 0.0
     for i, u in enumerate(lw.units):
         if u.get("kind") != 2:
             continue
         f, b = unit_cost(lw, u, batch)
         t = unit_ms[i] * 1e-3
-        F, B, T = F + f, B + b, T + t
-        p_unit = p_f16 if plan.unit_impl(i) in (3, 5) else p_tf32
-        p_tc = min(p_tc, p_unit)
-        tr = max(f / (p_unit * 1e12), b / (hbm * 1e9))
-        Troof += tr
-        rows.append((f, b, t, tr))
+        impl = plan.unit_impl(i)
+        g = groups.setdefault(impl, [0.0, 0.0, 0.0, 0])
+        g[0] += f; g[1] += b; g[2] += t; g[3] += 1
+        T += t
+        Troof += max(f / (rate[impl] * 1e12), b / (hbm * 1e9))
     total = float(np.sum(unit_ms)) * 1e-3
-    bound = "tensor" if F / (p_tc * 1e12) >= B / (hbm * 1e9) else "hbm"
+    impl = max(groups, key=lambda k: groups[k][2])
+    F, B, Tk, n = groups[impl]
+    P = rate[impl]
+    bound = "tensor" if F / (P * 1e12) >= B / (hbm * 1e9) else "hbm"
     if bound == "tensor":
-        achieved, peak, unit = F / T / 1e12, p_tc, "TFLOP/s"
+        achieved, peak, unit = F / Tk / 1e12, P, "TFLOP/s"
     else:
-        achieved, peak, unit = B / T / 1e9, hbm, "GB/s"
+        achieved, peak, unit = B / Tk / 1e9, hbm, "GB/s"
+    name = KERNEL_NAMES[impl]
     return {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": unit,
-            "frac": round(achieved / peak, 4), "traffic": None,
-            "kernel": "conv units (fused implicit-GEMM conv + epilogue), %d launches/step" % len(rows),
-            "peak_basis": f"{basis}: fp16x2 units bf16_tflops/3 (three fp16 products), 3xTF32 units "
-                          f"bf16_tflops/6; peak = the lower rate in use; hbm_gbs {hbm}",
-            "roofline_time_frac": round(Troof / T, 4) if T else None,
-            "conv_share_of_step": round(T / total, 4) if total else None,
-            "algorithmic_flops_per_step": F, "algorithmic_bytes_per_step": B}
+            "frac": round(achieved / peak, 4), "traffic": measured_traffic(config, name),
+            "kernel": f"{name}: {n} launches/step, {100 * Tk / total:.1f}% of the step",
+            "algorithmic_per_launch": {"flops": F / n, "bytes": B / n},
+            "peak_basis": f"{basis} bf16_tflops {bf16} (tensor: /3 for fp16x2, /6 for 3xTF32); hbm_gbs {hbm}",
+            "all_conv_roofline_time_frac": round(Troof / T, 4) if T else None,
+            "conv_share_of_step": round(T / total, 4) if total else None}
 
 
 # ---------------------------------------------------------------------------
@@ -446,7 +465,7 @@ def run_ours(args):
             torch.distributed.destroy_process_group()
         return
     unit_ms = per_unit_times(eng, x, out, reps=max(3, min(args.steps, 10)), flush=flush)
-    roof = roofline(eng, batch, unit_ms, plan)
+    roof = roofline(eng, batch, unit_ms, plan, args.config)
     launches = plan.launches()
     line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
@@ -457,7 +476,7 @@ def run_ours(args):
                        "redistribution": redist_info,
                        "conv_impl": sorted({plan.unit_impl(i) for i, u in enumerate(eng.lw.units)
                                             if u.get("kind") == 2}),
-                       "split_tensors": sum(plan.tensor_split(t) for t in range(len(eng.lw.tensors)))},
+                       "split_tensors": sum(plan.tensor_split(t) > 0 for t in range(len(eng.lw.tensors)))},
             "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": int(xh.numel() * 4),
                     "d2h_bytes_per_step": int(oh.numel() * 4) + (4 if any_split else 0)},
             "gpu_launches": launches * args.steps,

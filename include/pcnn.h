@@ -217,8 +217,9 @@ int pcnn_plan_destroy(pcnn_plan* plan);
 int pcnn_plan_num_launches(const pcnn_plan* plan);
 /* conv implementation of unit i: 1 SIMT, 2 tcgen05 3xTF32, 3 tcgen05 fp16x2 */
 int pcnn_plan_unit_impl(const pcnn_plan* plan, int unit);
-/* 1 if tensor t is stored split (two fp16 planes x = hi + lo, written by
- * its producer for fp16x2 convs), 0 if float32 */
+/* storage format of tensor t: 0 float32; 1 split (two fp16 planes x = hi +
+ * lo on the zero-bordered grid, written by its producer for fp16x2 convs);
+ * 2 split in the four (row, column) parity planes (stride-2 readers) */
 int pcnn_plan_tensor_split(const pcnn_plan* plan, int tensor);
 /* Status of the last forward on `stream` (synchronises it): bit 0 = a value
  * of a split tensor left the fp16 range (|x| >= 2^15 or non-finite), so the

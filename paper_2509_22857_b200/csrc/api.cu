@@ -77,7 +77,7 @@ TensorView make_view(const pcnn_tensor_desc& t, float* ws) {
   while ((1 << v.cbs) < v.cb) ++v.cbs;
   v.split = 0;
   v.hp = v.wp = 0;
-  v.kstride = 0;
+  v.kstride = v.pstride = 0;
   v.plane = 0;
   v.flag = nullptr;
   return v;
@@ -88,12 +88,14 @@ int64_t tensor_floats(const pcnn_tensor_desc& t, int batch) {
 }
 
 // Storage formats: a tensor is kept split (two fp16 planes, common.cuh) when
-// its producer is the ingest or an fp16x2 tcgen05 conv writing a spatial
-// tensor, and every reader is an fp16x2 tcgen05 conv (input or residual
-// skip).  Everything else stays fp32.
+// its producer is the ingest, a local pool or an fp16x2 tcgen05 conv writing
+// a spatial tensor, and every reader is an fp16x2 tcgen05 conv (input or
+// residual skip).  It takes the parity layout when every conv that reads it
+// as input has stride 2 and a shape the halo-tile kernel runs.  Everything
+// else stays fp32.
 void choose_formats(pcnn_plan* p) {
   const int nt = (int)p->tensors.size();
-  std::vector<int> ok(nt, 1), produced(nt, 0);
+  std::vector<int> ok(nt, 1), produced(nt, 0), s2_only(nt, 1), inputs(nt, 0);
   for (int i = 0; i < (int)p->units.size(); ++i) {
     const pcnn_unit_desc& u = p->units[i];
     const bool tc16 = u.kind == PCNN_UNIT_CONV && p->impl[i] == 3;
@@ -102,7 +104,13 @@ void choose_formats(pcnn_plan* p) {
       const bool pool_split = u.kind == PCNN_UNIT_LOCALPOOL && p->tensors[u.in].cb == p->tensors[u.out].cb;
       if (!(u.kind == PCNN_UNIT_INGEST || pool_split || (tc16 && u.pool != PCNN_POOL_GLOBAL))) ok[u.out] = 0;
     }
-    if (u.in >= 0 && !tc16) ok[u.in] = 0;
+    if (u.in >= 0) {
+      ++inputs[u.in];
+      if (!tc16) ok[u.in] = 0;
+      const bool ss2 = tc16 && u.stride == 2 && (u.impl == 0 || u.impl == 3 || u.impl == 5) &&
+                       !getenv("PCNN_NO_SS") && conv_ss_shape_ok(p->conv_args[i]);
+      if (!ss2) s2_only[u.in] = 0;
+    }
     if (u.in2 >= 0 && !(tc16 && u.residual)) ok[u.in2] = 0;
   }
   if (getenv("PCNN_NO_SPLIT")) ok.assign(nt, 0);
@@ -110,12 +118,20 @@ void choose_formats(pcnn_plan* p) {
     TensorView& v = p->views[t];
     if (!ok[t] || !produced[t] || v.is_vector || t == p->output) continue;
     if (v.cb < 8 && v.nblk > 1) continue;
-    v.split = 1;
-    v.hp = v.h + 2;
-    v.wp = v.w + 2;
-    v.kstride = (int64_t)p->batch * v.hp * v.wp * 8;
+    if (s2_only[t] && inputs[t] > 0) {
+      v.split = 2;
+      v.hp = (v.h + 3) / 2;
+      v.wp = (v.w + 3) / 2;
+      v.pstride = (int64_t)p->batch * v.hp * v.wp * 8;
+      v.kstride = 4 * v.pstride;
+    } else {
+      v.split = 1;
+      v.hp = v.h + 2;
+      v.wp = v.w + 2;
+      v.kstride = v.pstride = (int64_t)p->batch * v.hp * v.wp * 8;
+    }
     v.plane = (int64_t)((v.cpad() + 7) / 8) * v.kstride;
-    if (v.plane >= (1ll << 31)) {  // 32-bit segment offsets in the conv kernel
+    if (v.plane >= (1ll << 31)) {  // 32-bit segment offsets in the conv kernels
       v.split = 0;
       continue;
     }
@@ -129,7 +145,7 @@ void choose_formats(pcnn_plan* p) {
     a.in = p->views[u.in];
     a.epi.out = p->views[u.out];
     if (u.residual) a.epi.skip = p->views[u.in2];
-    // fp16x2 convs reading a split tensor: the shared-memory kernel when the
+    // fp16x2 convs reading a split tensor: the halo-tile kernel when the
     // shape allows (unit impl 0, 3 or 5)
     if (p->impl[i] == 3 && (u.impl == 0 || u.impl == 3 || u.impl == 5) && !getenv("PCNN_NO_SS") &&
         conv_ss_supported(a))

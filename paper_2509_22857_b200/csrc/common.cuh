@@ -23,14 +23,20 @@ constexpr int kMaxBiDeg = 4;
 //         Written by producers of tensors that only tcgen05 fp16x2 convs
 //         read; a value outside |x| < 2^15 (or not finite) sets *flag and the
 //         host reruns the batch on fp32 tensors.
+//   parity split (split = 2): the same padded grid cut into its four
+//         (row, column) parity planes, [C/8][4][B][Hq][Wq][8] with Hq =
+//         ceil((H+2)/2): a stride-2 conv's taps become fixed offsets inside
+//         one parity plane.  Used when every conv reading the tensor has
+//         stride 2.
 struct TensorView {
   float* base;
   int c, h, w, cb, nblk, is_vector;
   int cbs;  // log2(cb); cb is a power of two
   int split;
-  int hp, wp;       // split: padded grid h + 2, w + 2
-  int64_t kstride;  // split: halves per 8-channel group (batch * hp * wp * 8)
-  int64_t plane;    // split: halves per plane
+  int hp, wp;       // split 1: padded grid h + 2, w + 2; split 2: parity grid ceil(hp / 2), ceil(wp / 2)
+  int64_t pstride;  // split 2: halves per parity plane (batch * hp * wp * 8)
+  int64_t kstride;  // halves per 8-channel group (batch * hp * wp * 8, x4 planes for split 2)
+  int64_t plane;    // split: halves per hi / lo plane
   int* flag;        // split: overflow flag (device)
   __host__ __device__ int cpad() const { return nblk * cb; }
   __host__ __device__ __forceinline__ int64_t index(int b, int ch, int y, int x) const {
@@ -38,6 +44,11 @@ struct TensorView {
   }
   // split: half index of (b, ch, y, x) inside a plane
   __host__ __device__ __forceinline__ int64_t sindex(int b, int ch, int y, int x) const {
+    if (split == 2) {
+      const int yp = y + 1, xp = x + 1;
+      return (ch >> 3) * kstride + (((yp & 1) << 1) | (xp & 1)) * pstride +
+             (((int64_t)b * hp + (yp >> 1)) * wp + (xp >> 1)) * 8 + (ch & 7);
+    }
     return (ch >> 3) * kstride + (((int64_t)b * hp + y + 1) * wp + x + 1) * 8 + (ch & 7);
   }
   // address of element (b, channel, y, x) of a spatial tensor (fp32 format)
@@ -53,7 +64,8 @@ __host__ __device__ inline int64_t tensor_storage_floats(int64_t batch, int64_t 
                                                          bool is_vector) {
   const int64_t fp32 = batch * cpad * h * w;
   if (is_vector) return fp32;
-  const int64_t split = ((cpad + 7) / 8) * 8 * batch * (h + 2) * (w + 2);  // 2 planes of halves
+  // 2 planes (hi, lo) of halves; the parity layout rounds the padded grid up to even
+  const int64_t split = ((cpad + 7) / 8) * 8 * batch * ((h + 3) / 2 * 2) * ((w + 3) / 2 * 2);
   (void)c;
   return fp32 > split ? fp32 : split;
 }

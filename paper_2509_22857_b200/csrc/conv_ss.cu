@@ -1,5 +1,7 @@
 // tcgen05 fp16x2 convolution with both operands in shared memory ("halo
-// tiles"), for stride-1 3x3 / 1x1 convs whose input is a split tensor.
+// tiles"), for 3x3 / 1x1 convs of stride 1 or 2 whose input is a split tensor
+// (stride 2 reads the parity layout: every tap is again a fixed offset, now
+// inside one of the four parity planes).
 //
 // The split layout (common.cuh) stores every 8-channel group as a plane
 // [B][H+2][W+2][8] fp16 with a zero border.  Flatten the padded grid: position
@@ -49,9 +51,13 @@ struct SsParams {
   int nt, n_tiles, m_tiles;
   int nq;                // 16-channel chunks
   int last_groups;       // 8-channel groups in the last chunk (1 when cpad is 4 or 8)
-  int taps, kw, wp, hp;  // conv taps; padded grid
-  int halo;              // R: positions before/after a tile
-  int span;              // 128 + 2R
+  int taps, wp, hp;      // conv taps; output grid = input grid (padded, or one parity grid)
+  int halo;              // positions loaded before a tile's first (stride 1, 3x3: wp + 1)
+  int span;              // positions per loaded plane: 128 + halo + reach
+  int nplanes;           // input planes loaded per stage (4 parity planes for 3x3 / stride 2)
+  int plane_id[4];       // which parity plane goes to loaded slot i
+  int toff[9];           // tap -> A start in 16-byte units: slot * 4 * span + position offset
+  int vy0, vy1, vx0, vx1;  // grid rows / columns holding outputs (output = grid - v*0)
   int64_t gtotal;        // grid positions (batch * hp * wp)
   uint32_t a_bytes;      // one 8-channel group of one plane: span * 16
   uint32_t b_bytes;      // taps * 64 * NT
@@ -184,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
   if (P.last_groups == 1) {
     // cpad 4 / 8: the second 8-channel group of every stage stays zero
     for (int st = 0; st < P.stages; ++st)
-      for (int pl = 0; pl < 2; ++pl) {
+      for (int pl = 0; pl < 2 * P.nplanes; ++pl) {  // (plane, hi/lo): its second 8-channel group
         uint4* z = reinterpret_cast<uint4*>(smem + (size_t)st * P.stage_bytes + (2 * pl + 1) * P.a_bytes);
         for (uint32_t i = threadIdx.x; i < P.a_bytes / 16; i += kThreads) z[i] = make_uint4(0, 0, 0, 0);
       }
@@ -209,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       uint32_t ph = 0;
       for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
         const int n_tile = tile / P.m_tiles, m_tile = tile - n_tile * P.m_tiles;
-        const int64_t gs = (int64_t)m_tile * kTileM - P.halo;
+        const int64_t gs = (int64_t)m_tile * kTileM - P.halo;  // grid position of buffer slot 0
         const int64_t cs = gs < 0 ? 0 : gs;
         const int64_t ge = gs + P.span;
         const int64_t ce = ge > P.gtotal ? P.gtotal : ge;
@@ -221,13 +227,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
           const uint32_t bar = ptx::smem_u32(&S->full[st]);
           const uint32_t sb = base + st * P.stage_bytes;
           const int ng = q == P.nq - 1 ? P.last_groups : 2;
-          ptx::mbar_arrive_tx(bar, 2 * ng * bytes + P.b_bytes);
-          for (int g = 0; g < ng; ++g) {
-            const int64_t off = (2 * q + g) * a.in.kstride + cs * 8;
-            ptx::bulk_g2s(sb + g * P.a_bytes + slot0, hi + off, bytes, bar);
-            ptx::bulk_g2s(sb + (2 + g) * P.a_bytes + slot0, lo + off, bytes, bar);
+          ptx::mbar_arrive_tx(bar, 2 * ng * P.nplanes * bytes + P.b_bytes);
+          for (int pl = 0; pl < P.nplanes; ++pl) {
+            const uint32_t ps = sb + pl * 4 * P.a_bytes;
+            for (int g = 0; g < ng; ++g) {
+              const int64_t off = (2 * q + g) * a.in.kstride + P.plane_id[pl] * a.in.pstride + cs * 8;
+              ptx::bulk_g2s(ps + g * P.a_bytes + slot0, hi + off, bytes, bar);
+              ptx::bulk_g2s(ps + (2 + g) * P.a_bytes + slot0, lo + off, bytes, bar);
+            }
           }
-          ptx::bulk_g2s(sb + 4 * P.a_bytes, P.w + ((int64_t)n_tile * P.nq + q) * P.taps * 32 * P.nt, P.b_bytes, bar);
+          ptx::bulk_g2s(sb + P.nplanes * 4 * P.a_bytes, P.w + ((int64_t)n_tile * P.nq + q) * P.taps * 32 * P.nt,
+                        P.b_bytes, bar);
           if (++st == P.stages) { st = 0; ph ^= 1; }
         }
       }
@@ -242,7 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
     // tap offsets in the descriptors' 16-byte address units
     uint64_t offs[TAPS];
 #pragma unroll
-    for (int t = 0; t < TAPS; ++t) offs[t] = (uint64_t)((t / P.kw) * P.wp + t % P.kw);
+    for (int t = 0; t < TAPS; ++t) offs[t] = (uint64_t)P.toff[t];
     const uint64_t bstep = (uint64_t)(64 * P.nt) >> 4, blo = (uint64_t)(P.nt * 16) >> 4;
     int st = 0;
     uint32_t ph = 0, acc = 0, acc_ph = 0;
@@ -259,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
         const uint32_t sb = base + st * P.stage_bytes;
         const uint64_t a_hi = ptx::smem_desc_noswz(sb, a_lbo, 128);
         const uint64_t a_lo = ptx::smem_desc_noswz(sb + 2 * P.a_bytes, a_lbo, 128);
-        const uint64_t b0 = ptx::smem_desc_noswz(sb + 4 * P.a_bytes, b_lbo, 128);
+        const uint64_t b0 = ptx::smem_desc_noswz(sb + P.nplanes * 4 * P.a_bytes, b_lbo, 128);
         const uint32_t main_acc = q >= NP ? 1u : 0u;
         if (do_mma) {
           if (P.concat) {
@@ -301,8 +311,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       const int g = m_tile * kTileM + row;
       const int b = (int)P.div_hw.div(g);
       const int r = g - b * hw;
-      const int yp = (int)P.div_wp.div(r), xp = r - yp * P.wp;
-      const bool valid = g < P.gtotal && yp >= 1 && yp <= a.in.h && xp >= 1 && xp <= a.in.w;
+      const int gy = (int)P.div_wp.div(r), gx = r - gy * P.wp;
+      const bool valid = g < P.gtotal && gy >= P.vy0 && gy < P.vy1 && gx >= P.vx0 && gx < P.vx1;
+      const int yp = gy - P.vy0 + 1, xp = gx - P.vx0 + 1;  // output pixel + 1
       // the residual input does not depend on the accumulators: load it first
       float sk[16];
       epi_load_skip(e, n_tile * P.nt, valid, b, yp - 1, xp - 1, sk);
@@ -359,11 +370,14 @@ size_t ss_aux_bytes(const SsParams& P) {
 
 bool make_ss_params(const ConvArgs& a, SsParams& P) {
   const TensorView& in = a.in;
-  if (!a.f16 || !in.split || !a.tcwss || !a.tc16_scale) return false;
-  if (a.stride != 1 || a.kh != a.kw || !((a.kh == 3 && a.pad == 1) || (a.kh == 1 && a.pad == 0))) return false;
+  if (!a.f16 || !a.tcwss || !a.tc16_scale) return false;
+  if ((a.stride != 1 && a.stride != 2) || a.kh != a.kw || !((a.kh == 3 && a.pad == 1) || (a.kh == 1 && a.pad == 0)))
+    return false;
   if (a.epi.pool != PCNN_POOL_NONE && a.epi.pool != PCNN_POOL_GLOBAL) return false;
+  if (!(in.cpad() == 4 || in.cpad() == 8 || in.cpad() % 16 == 0) || a.npad < 16 || a.npad % 16) return false;
+  // stride 1 reads the padded grid, stride 2 the parity planes
+  if (in.split != (a.stride == 2 ? 2 : 1)) return false;
   const int cpad = in.cpad();
-  if (!(cpad == 4 || cpad == 8 || cpad % 16 == 0) || a.npad < 16 || a.npad % 16) return false;
   P.a = a;
   P.nt = a.npad <= 128 ? a.npad : 128;
   if (a.npad % P.nt) return false;
@@ -376,15 +390,46 @@ bool make_ss_params(const ConvArgs& a, SsParams& P) {
   P.nq = (cpad + 15) / 16;
   P.last_groups = cpad % 16 == 0 ? 2 : 1;
   P.taps = a.kh * a.kw;
-  P.kw = a.kw;
-  P.halo = a.kh == 3 ? in.wp + 1 : 0;
-  P.span = kTileM + 2 * P.halo;
+  if (a.stride == 1) {
+    // padded grid; tap (ky, kx) of output g reads g + (ky - 1) wp + kx - 1
+    P.nplanes = 1;
+    P.plane_id[0] = 0;
+    P.halo = a.kh == 3 ? in.wp + 1 : 0;
+    P.span = kTileM + 2 * P.halo;
+    P.vy0 = P.vx0 = 1;
+    P.vy1 = in.h + 1;
+    P.vx1 = in.w + 1;
+    for (int t = 0; t < P.taps; ++t) P.toff[t] = (t / a.kw) * in.wp + t % a.kw;
+  } else {
+    // parity planes: padded input (2y + ky, 2x + kx) = plane (ky & 1, kx & 1)
+    // at (y + ky / 2, x + kx / 2); a 1x1 conv reads plane (1, 1) at (y, x)
+    const int ho = (in.h + 2 * a.pad - a.kh) / 2 + 1, wo = (in.w + 2 * a.pad - a.kw) / 2 + 1;
+    P.halo = 0;
+    P.vy0 = P.vx0 = 0;
+    P.vy1 = ho;
+    P.vx1 = wo;
+    if (a.kh == 1) {
+      P.nplanes = 1;
+      P.plane_id[0] = 3;
+      P.span = kTileM;
+      P.toff[0] = 0;
+    } else {
+      P.nplanes = 4;
+      for (int i = 0; i < 4; ++i) P.plane_id[i] = i;
+      P.span = kTileM + in.wp + 1;
+    }
+  }
+  if (a.stride == 2 && a.kh == 3)
+    for (int t = 0; t < 9; ++t) {
+      const int ky = t / 3, kx = t % 3;
+      P.toff[t] = (((ky & 1) << 1) | (kx & 1)) * 4 * P.span + (ky >> 1) * in.wp + (kx >> 1);
+    }
   P.w = reinterpret_cast<const __half*>(a.tcwss);
   P.wscale = a.tc16_scale + 1;
   P.etab = epi_tab_layout(a.epi);
   P.a_bytes = (uint32_t)P.span * 16;
   P.b_bytes = (uint32_t)P.taps * 64 * P.nt;
-  P.stage_bytes = 4 * P.a_bytes + P.b_bytes;
+  P.stage_bytes = P.nplanes * 4 * P.a_bytes + P.b_bytes;
   const size_t budget = 225 * 1024 - 128 - ss_aux_bytes(P);
   P.stages = (int)(budget / P.stage_bytes);
   if (P.stages > kMaxStages) P.stages = kMaxStages;
@@ -423,6 +468,25 @@ extern "C" int pcnn_ss_trace(unsigned long long* host, int n) {
   static unsigned long long zeros[kTraceLen];
   cudaMemcpyToSymbol(g_ss_trace, zeros, sizeof(zeros));
   return m;
+}
+
+bool conv_ss_shape_ok(const ConvArgs& a) {
+  if (!a.f16 || !a.tcwss || !a.tc16_scale) return false;
+  if ((a.stride != 1 && a.stride != 2) || a.kh != a.kw || !((a.kh == 3 && a.pad == 1) || (a.kh == 1 && a.pad == 0)))
+    return false;
+  if (a.epi.pool != PCNN_POOL_NONE && a.epi.pool != PCNN_POOL_GLOBAL) return false;
+  const int cpad = a.in.cpad();
+  if (!(cpad == 4 || cpad == 8 || cpad % 16 == 0) || a.npad < 16 || a.npad % 16) return false;
+  // and the tiles fit shared memory, given the input in the layout it would get
+  ConvArgs b = a;
+  TensorView& in = b.in;
+  in.split = a.stride == 2 ? 2 : 1;
+  in.hp = a.stride == 2 ? (in.h + 3) / 2 : in.h + 2;
+  in.wp = a.stride == 2 ? (in.w + 3) / 2 : in.w + 2;
+  in.pstride = (int64_t)b.batch * in.hp * in.wp * 8;
+  in.kstride = a.stride == 2 ? 4 * in.pstride : in.pstride;
+  SsParams P;
+  return make_ss_params(b, P);
 }
 
 bool conv_ss_supported(const ConvArgs& a) {

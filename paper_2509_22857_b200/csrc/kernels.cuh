@@ -83,6 +83,8 @@ void tc_weight_image_dims(int npad, int kp, int64_t* floats);
 // fp16x2 conv with A from shared memory (conv_ss.cu): stride-1 3x3/1x1 convs
 // reading a split tensor
 bool conv_ss_supported(const ConvArgs& a);
+// the shape/precision part of conv_ss_supported (input format not checked)
+bool conv_ss_shape_ok(const ConvArgs& a);
 void launch_conv_ss(const ConvArgs& a, cudaStream_t s);
 
 }  // namespace pcnn

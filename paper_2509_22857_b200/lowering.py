@@ -82,7 +82,8 @@ class Tensor:
         fp32 = batch * self.cpad * self.h * self.w
         if self.is_vector:
             return fp32
-        return max(fp32, -(-self.cpad // 8) * 8 * batch * (self.h + 2) * (self.w + 2))
+        # (the parity layout of stride-2 inputs rounds the padded grid up to even)
+        return max(fp32, -(-self.cpad // 8) * 8 * batch * ((self.h + 3) // 2 * 2) * ((self.w + 3) // 2 * 2))
 
 
 @dataclass
@@ -505,7 +506,7 @@ class _Builder:
             u["tc_off"] = self.tc_image(nid)
             u["tc16_off"], u["tc16_scale_off"] = self.tc16_image(nid)
             k, st, pd = wmeta["kh"], u["stride"], u["pad"]
-            if (wmeta["kh"] == wmeta["kw"] and st == 1 and ((k == 3 and pd == 1) or (k == 1 and pd == 0))
+            if (wmeta["kh"] == wmeta["kw"] and st in (1, 2) and ((k == 3 and pd == 1) or (k == 1 and pd == 0))
                     and ((cp := wmeta["kp"] // (k * k)) in (4, 8) or cp % 16 == 0)
                     and u.get("pool", 0) in (L.POOL_NONE, L.POOL_GLOBAL)):
                 u["tcss_off"] = self.tcss_image(nid, u["tc16_scale_off"])

@@ -62,8 +62,9 @@ class Plan:
     def unit_impl(self, i: int) -> int:
         return L.lib().pcnn_plan_unit_impl(self.handle, i)
 
-    def tensor_split(self, t: int) -> bool:
-        return L.lib().pcnn_plan_tensor_split(self.handle, t) == 1
+    def tensor_split(self, t: int) -> int:
+        """0 float32, 1 split fp16 hi/lo (padded grid), 2 split in parity planes."""
+        return L.lib().pcnn_plan_tensor_split(self.handle, t)
 
     def status(self, stream=None) -> int:
         """Status word of the last forward on `stream` (synchronises it)."""
@@ -74,6 +75,37 @@ class Plan:
 
     def last_status(self) -> int:
         return L.lib().pcnn_plan_last_status(self.handle)
+
+    def read_tensor(self, t: int) -> np.ndarray:
+        """Copy tensor t out of the workspace, decoded from its storage format
+        (csrc/common.cuh) to float32 (B, C, H, W), or (B, C) for vectors.
+        Debug / test aid; synchronises the device."""
+        desc = self.tdescs[t]
+        c, h, w, cb, nblk = int(desc.c), int(desc.h), int(desc.w), int(desc.cb), int(desc.nblk)
+        b, cpad = self.batch, nblk * cb
+        base = int(desc.offset)
+        fmt = self.tensor_split(t)
+        if desc.is_vector:
+            return self.ws[base:base + b * cpad].view(b, cpad)[:, :c].cpu().numpy()
+        if fmt == 0:
+            x = self.ws[base:base + b * cpad * h * w].view(b, nblk, h, w, cb)
+            return x.permute(0, 1, 4, 2, 3).reshape(b, cpad, h, w)[:, :c].cpu().numpy()
+        halves = self.ws.view(_torch().float16)[2 * base:]
+        ng = -(-cpad // 8)
+        if fmt == 1:
+            hp, wp = h + 2, w + 2
+            n = ng * b * hp * wp * 8
+            planes = [halves[k * n:(k + 1) * n].float().view(ng, b, hp, wp, 8) for k in (0, 1)]
+            x = (planes[0] + planes[1])[:, :, 1:h + 1, 1:w + 1, :]
+        else:
+            hq, wq = (h + 3) // 2, (w + 3) // 2
+            n = ng * 4 * b * hq * wq * 8
+            planes = [halves[k * n:(k + 1) * n].float().view(ng, 2, 2, b, hq, wq, 8) for k in (0, 1)]
+            q = planes[0] + planes[1]                    # [g][ry][rx][b][i][j][8]
+            full = q.permute(0, 3, 4, 1, 5, 2, 6).reshape(ng, b, 2 * hq, 2 * wq, 8)
+            x = full[:, :, 1:h + 1, 1:w + 1, :]
+        x = x.permute(1, 0, 4, 2, 3).reshape(b, ng * 8, h, w)
+        return x[:, :c].cpu().numpy()
 
     def __del__(self):
         h = getattr(self, "handle", None)

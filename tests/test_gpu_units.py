@@ -1,0 +1,69 @@
+"""Every unit of every configuration against the float64 oracle, tensor by
+tensor: after one batched forward, each unit's output is read back from the
+workspace (decoded from its storage format: float32 blocked, split fp16
+hi/lo, or split parity planes) and compared with the oracle value of the last
+graph node fused into that unit.  The logits alone are a weak check on the
+input-insensitive configs (RN18's vary by ~0.5% across images), so this is
+where a wrong intermediate shows."""
+
+from collections import defaultdict
+
+import numpy as np
+import pytest
+
+from oracle import levnet_oracle as O
+from paper_2509_22857_b200 import configs
+from paper_2509_22857_b200.runtime import Engine
+
+pytestmark = pytest.mark.gpu
+
+N_IMAGES = {"lenet5": 4, "resnet20": 4, "resnet20_deg8": 4, "vgg11": 2, "resnet18": 1}
+
+
+def oracle_values(g, x):
+    """float64 value of every node for a batch (reference_eval's loop)."""
+    preds = defaultdict(list)
+    for s, d in g.edges:
+        preds[d].append(s)
+    vals = {g.input_id(): np.asarray(x, dtype=np.float64)}
+    for nid in g.topo_order():
+        if nid == g.input_id():
+            continue
+        vals[nid] = np.stack([O.eval_node(g.nodes[nid], [vals[p][b] for p in preds[nid]])
+                              for b in range(x.shape[0])])
+    return vals
+
+
+@pytest.mark.parametrize("name", list(configs.CONFIGS))
+@pytest.mark.parametrize("impl", [0, 4], ids=["auto", "fp32_tensors"])
+def test_every_unit_matches_oracle(cuda, name, impl):
+    import torch
+    g = configs.build(name)
+    n = N_IMAGES[name]
+    x = configs.make_input(configs.CONFIGS[name], batch=n)
+    eng = Engine(g, impl=impl)
+    y = eng.forward(torch.from_numpy(x.astype(np.float32)).cuda())
+    torch.cuda.synchronize()
+    plan = eng.plan(n)
+    want = oracle_values(g, x)
+    # plain float32 FMA (SIMT kernels, float32 tensors) as the fp32-class yardstick
+    simt = Engine(g, impl=1)
+    simt.forward(torch.from_numpy(x.astype(np.float32)).cuda())
+    torch.cuda.synchronize()
+    splan = simt.plan(n)
+    checked = 0
+    for i, (u, chain) in enumerate(zip(eng.lw.units, eng.lw.unit_nodes)):
+        if u["kind"] in (1, 12) or u.get("out", -1) < 0:  # ingest / copyout
+            continue
+        got = plan.read_tensor(u["out"]).astype(np.float64)
+        ref = want[chain[-1]].reshape(got.shape)
+        scale = max(float(np.abs(ref).max()), 1e-30)
+        err = float(np.abs(got - ref).max()) / scale
+        err_simt = float(np.abs(splan.read_tensor(u["out"]).astype(np.float64) - ref).max()) / scale
+        # errors accumulate through the network in both; the tensor-core path
+        # must stay within the tolerance or within a small factor of fp32 FMA
+        assert err <= max(1e-4, 4 * err_simt), (name, i, chain, plan.unit_impl(i), plan.tensor_split(u["out"]),
+                                                 err, err_simt)
+        checked += 1
+    assert checked >= 3
+    np.testing.assert_allclose(y.double().cpu().numpy(), want[g.output_id()].reshape(n, -1), rtol=1e-4, atol=1e-5)
