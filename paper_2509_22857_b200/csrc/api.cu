@@ -126,9 +126,10 @@ void choose_formats(pcnn_plan* p) {
       v.kstride = 4 * v.pstride;
     } else {
       v.split = 1;
-      v.hp = v.h + 2;
-      v.wp = v.w + 2;
-      v.kstride = v.pstride = (int64_t)p->batch * v.hp * v.wp * 8;
+      v.hp = v.h + 1;
+      v.wp = v.w + 1;
+      // positions: leading zero, B (H+1) + 1 rows of pitch W+1, one spare
+      v.kstride = v.pstride = (2 + ((int64_t)p->batch * v.hp + 1) * v.wp) * 8;
     }
     v.plane = (int64_t)((v.cpad() + 7) / 8) * v.kstride;
     if (v.plane >= (1ll << 31)) {  // 32-bit segment offsets in the conv kernels

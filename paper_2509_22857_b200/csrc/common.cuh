@@ -17,9 +17,14 @@ constexpr int kMaxBiDeg = 4;
 // Storage formats:
 //   fp32  (split = 0): channel-blocked [B][C/cb][H][W][cb] floats.
 //   split (split = 1): x = hi + lo as two fp16 planes (|x - hi - lo| <=
-//         2^-22 |x| + 2^-25), each laid out [C/8][B][H+2][W+2][8] with a
-//         one-pixel zero border: 8 channels = 16 bytes per position, and a
-//         3x3 conv's taps are fixed offsets in the flattened padded grid.
+//         2^-22 |x| + 2^-25), each [C/8][grid][8]: 8 channels = 16 bytes per
+//         position of a zero-bordered grid whose border rows and columns are
+//         SHARED by neighbours -- row pitch W+1 (column W is zero and is also
+//         the left neighbour of the next row), H+1 rows per image (row 0 of
+//         each image is zero and is also the previous image's bottom
+//         neighbour), one leading zero position: element (b, y, x) at
+//         position 1 + (b (H+1) + y + 1)(W+1) + x.  A 3x3 conv's taps are
+//         fixed offsets (ky-1)(W+1) + kx-1 in this flattened grid.
 //         Written by producers of tensors that only tcgen05 fp16x2 convs
 //         read; a value outside |x| < 2^15 (or not finite) sets *flag and the
 //         host reruns the batch on fp32 tensors.
@@ -33,7 +38,7 @@ struct TensorView {
   int c, h, w, cb, nblk, is_vector;
   int cbs;  // log2(cb); cb is a power of two
   int split;
-  int hp, wp;       // split 1: padded grid h + 2, w + 2; split 2: parity grid ceil(hp / 2), ceil(wp / 2)
+  int hp, wp;       // split 1: rows per image h + 1, pitch w + 1; split 2: parity grid ceil((h+2)/2), ceil((w+2)/2)
   int64_t pstride;  // split 2: halves per parity plane (batch * hp * wp * 8)
   int64_t kstride;  // halves per 8-channel group (batch * hp * wp * 8, x4 planes for split 2)
   int64_t plane;    // split: halves per hi / lo plane
@@ -49,7 +54,7 @@ struct TensorView {
       return (ch >> 3) * kstride + (((yp & 1) << 1) | (xp & 1)) * pstride +
              (((int64_t)b * hp + (yp >> 1)) * wp + (xp >> 1)) * 8 + (ch & 7);
     }
-    return (ch >> 3) * kstride + (((int64_t)b * hp + y + 1) * wp + x + 1) * 8 + (ch & 7);
+    return (ch >> 3) * kstride + (1 + ((int64_t)b * hp + y + 1) * wp + x) * 8 + (ch & 7);
   }
   // address of element (b, channel, y, x) of a spatial tensor (fp32 format)
   __device__ __forceinline__ float* at(int b, int ch, int y, int x) const { return base + index(b, ch, y, x); }

@@ -58,6 +58,8 @@ struct SsParams {
   int plane_id[4];       // which parity plane goes to loaded slot i
   int toff[9];           // tap -> A start in 16-byte units: slot * 4 * span + position offset
   int vy0, vy1, vx0, vx1;  // grid rows / columns holding outputs (output = grid - v*0)
+  int shared_grid;         // stride 1: split layout with shared borders (common.cuh)
+  FastDiv div_h1;          // shared grid: rows per image (H + 1)
   int64_t gtotal;        // grid positions (batch * hp * wp)
   uint32_t a_bytes;      // one 8-channel group of one plane: span * 16
   uint32_t b_bytes;      // taps * 64 * NT
@@ -309,10 +311,24 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       const int n_tile = (int)P.div_mt.div(tile), m_tile = tile - n_tile * P.m_tiles;
       // grid position of this row (g < 2^31) -> image, padded row / column
       const int g = m_tile * kTileM + row;
-      const int b = (int)P.div_hw.div(g);
-      const int r = g - b * hw;
-      const int gy = (int)P.div_wp.div(r), gx = r - gy * P.wp;
-      const bool valid = g < P.gtotal && gy >= P.vy0 && gy < P.vy1 && gx >= P.vx0 && gx < P.vx1;
+      int b, gy, gx;
+      bool valid;
+      if (P.shared_grid) {
+        // position 1 + R (W+1) + x, global row R = b (H+1) + y + 1
+        const int g1 = g > 0 ? g - 1 : 0;
+        const int R = (int)P.div_wp.div(g1);
+        gx = g1 - R * P.wp;
+        const int R1 = R > 0 ? R - 1 : 0;
+        b = (int)P.div_h1.div(R1);
+        gy = R1 - b * P.hp;
+        valid = g >= 1 && R >= 1 && g < P.gtotal && gx < P.vx1 && gy < P.vy1 && b < a.batch;
+      } else {
+        b = (int)P.div_hw.div(g);
+        const int r = g - b * hw;
+        gy = (int)P.div_wp.div(r);
+        gx = r - gy * P.wp;
+        valid = g < P.gtotal && gy >= P.vy0 && gy < P.vy1 && gx >= P.vx0 && gx < P.vx1;
+      }
       const int yp = gy - P.vy0 + 1, xp = gx - P.vx0 + 1;  // output pixel + 1
       // the residual input does not depend on the accumulators: load it first
       float sk[16];
@@ -384,21 +400,22 @@ bool make_ss_params(const ConvArgs& a, SsParams& P) {
   P.n_tiles = a.npad / P.nt;
   P.hp = in.hp;
   P.wp = in.wp;
-  P.gtotal = (int64_t)a.batch * in.hp * in.wp;
+  P.shared_grid = a.stride == 1;
+  P.gtotal = a.stride == 1 ? in.kstride / 8 : (int64_t)a.batch * in.hp * in.wp;
   if (P.gtotal >= (1ll << 31)) return false;
   P.m_tiles = (int)((P.gtotal + kTileM - 1) / kTileM);
   P.nq = (cpad + 15) / 16;
   P.last_groups = cpad % 16 == 0 ? 2 : 1;
   P.taps = a.kh * a.kw;
   if (a.stride == 1) {
-    // padded grid; tap (ky, kx) of output g reads g + (ky - 1) wp + kx - 1
+    // shared-border grid; tap (ky, kx) of output g reads g + (ky - 1) wp + kx - 1
     P.nplanes = 1;
     P.plane_id[0] = 0;
     P.halo = a.kh == 3 ? in.wp + 1 : 0;
     P.span = kTileM + 2 * P.halo;
-    P.vy0 = P.vx0 = 1;
-    P.vy1 = in.h + 1;
-    P.vx1 = in.w + 1;
+    P.vy0 = P.vx0 = 0;
+    P.vy1 = in.h;
+    P.vx1 = in.w;
     for (int t = 0; t < P.taps; ++t) P.toff[t] = (t / a.kw) * in.wp + t % a.kw;
   } else {
     // parity planes: padded input (2y + ky, 2x + kx) = plane (ky & 1, kx & 1)
@@ -454,6 +471,7 @@ bool make_ss_params(const ConvArgs& a, SsParams& P) {
   const uint32_t need = P.acc_bufs * set;
   P.tmem_cols = need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
   P.div_hw = make_fastdiv((uint32_t)(P.hp * P.wp));
+  P.div_h1 = make_fastdiv((uint32_t)P.hp);
   P.div_wp = make_fastdiv((uint32_t)P.wp);
   P.div_mt = make_fastdiv((uint32_t)P.m_tiles);
   return true;
@@ -481,9 +499,9 @@ bool conv_ss_shape_ok(const ConvArgs& a) {
   ConvArgs b = a;
   TensorView& in = b.in;
   in.split = a.stride == 2 ? 2 : 1;
-  in.hp = a.stride == 2 ? (in.h + 3) / 2 : in.h + 2;
-  in.wp = a.stride == 2 ? (in.w + 3) / 2 : in.w + 2;
-  in.pstride = (int64_t)b.batch * in.hp * in.wp * 8;
+  in.hp = a.stride == 2 ? (in.h + 3) / 2 : in.h + 1;
+  in.wp = a.stride == 2 ? (in.w + 3) / 2 : in.w + 1;
+  in.pstride = a.stride == 2 ? (int64_t)b.batch * in.hp * in.wp * 8 : (2 + ((int64_t)b.batch * in.hp + 1) * in.wp) * 8;
   in.kstride = a.stride == 2 ? 4 * in.pstride : in.pstride;
   SsParams P;
   return make_ss_params(b, P);

@@ -143,7 +143,7 @@ __device__ __forceinline__ PixelRow pixel_row(const TcParams& P, int b, int oy, 
   PixelRow r;
   const int64_t idx = (((int64_t)b * in.nblk * in.h + iy0) * in.w + ix0) * in.cb;
   r.base = in.base + idx;
-  r.hbase = in.split ? in.hi() + (((int64_t)b * in.hp + iy0 + 1) * in.wp + ix0 + 1) * 8 : nullptr;
+  r.hbase = in.split ? in.hi() + (1 + ((int64_t)b * in.hp + iy0 + 1) * in.wp + ix0) * 8 : nullptr;
   r.ymask = r.xmask = 0;
   if (valid) {
     for (int k = 0; k < a.kh; ++k) r.ymask |= (uint32_t)(iy0 + k >= 0 && iy0 + k < in.h) << k;

@@ -93,10 +93,12 @@ class Plan:
         halves = self.ws.view(_torch().float16)[2 * base:]
         ng = -(-cpad // 8)
         if fmt == 1:
-            hp, wp = h + 2, w + 2
-            n = ng * b * hp * wp * 8
-            planes = [halves[k * n:(k + 1) * n].float().view(ng, b, hp, wp, 8) for k in (0, 1)]
-            x = (planes[0] + planes[1])[:, :, 1:h + 1, 1:w + 1, :]
+            # shared borders: position 1 + (b (H+1) + y + 1)(W+1) + x
+            npos = 2 + (b * (h + 1) + 1) * (w + 1)
+            n = ng * npos * 8
+            planes = [halves[k * n:(k + 1) * n].float().view(ng, npos, 8) for k in (0, 1)]
+            q = (planes[0] + planes[1])[:, 1:1 + b * (h + 1) * (w + 1)].reshape(ng, b, h + 1, w + 1, 8)
+            x = q[:, :, 1:, :w, :]
         else:
             hq, wq = (h + 3) // 2, (w + 3) // 2
             n = ng * 4 * b * hq * wq * 8

@@ -64,7 +64,9 @@ def test_forward_host_e2e_matches_device(cuda, golden):
     eng = Engine(g)
     a = eng.forward(torch.from_numpy(x).cuda()).cpu().numpy()
     b = eng.forward_host(x)
-    np.testing.assert_array_equal(a, b)
+    # a global pool fused into a conv epilogue sums with float atomics: runs
+    # agree to rounding, not bit for bit
+    np.testing.assert_allclose(a, b, rtol=1e-6, atol=1e-7)
 
 
 def test_graph_replay_equals_eager(cuda, golden):
@@ -76,8 +78,9 @@ def test_graph_replay_equals_eager(cuda, golden):
     a = eng.forward(x, use_graph=False).cpu().numpy()
     b = eng.forward(x, use_graph=True).cpu().numpy()
     c = eng.forward(x, use_graph=True).cpu().numpy()
-    np.testing.assert_array_equal(a, b)
-    np.testing.assert_array_equal(b, c)
+    # (fused global pools sum with float atomics: equal to rounding)
+    np.testing.assert_allclose(a, b, rtol=1e-6, atol=1e-7)
+    np.testing.assert_allclose(b, c, rtol=1e-6, atol=1e-7)
 
 
 def _ext_graph(rng, kind):
