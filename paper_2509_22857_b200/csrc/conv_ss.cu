@@ -45,6 +45,7 @@ constexpr int kAddsPerPartial = 96;
 
 struct SsParams {
   ConvArgs a;
+  int mt;                // 128-row sub-tiles per tile (two for small N: halves the per-tile hand-offs)
   EpiTab etab;
   const __half* w;       // weight image
   const float* wscale;   // 2^-e
@@ -92,75 +93,47 @@ struct Smem {
 };
 
 
-// ---- one stage (all taps of one 16-channel chunk) in one asm statement ----
-// Every operand is a warp-uniform descriptor and one elected lane issues, so
-// the loop costs no per-MMA address arithmetic in the (single) MMA warp.  A
-// descriptors advance by the tap's grid offset (in the 16-byte units of the
-// start-address field), B by one (chunk, tap) block per tap.
-#define SS_HEAD                                                   \
-  "{\n\t.reg .pred e, p, q, t;\n\t.reg .b32 r;\n\t"                \
-  ".reg .b64 ah, al, bd, bl;\n\t"                                  \
-  "elect.sync r|e, 0xffffffff;\n\tsetp.eq.u32 t, 0, 0;\n\t"
+// ---- one stage (all taps of one 16-channel chunk) ----
+// Descriptor adds in C++ on warp-uniform values (A advances by the tap's grid
+// offset in the 16-byte units of the start-address field, B by one (chunk,
+// tap) block), one minimal asm per MMA predicated on a lane elected once per
+// stage: ~64 cycles per MMA issued, vs ~75 for one asm block per stage.
 // concat (NT <= 64): [main | corr] (+)= A_hi [B_hi | B_lo] (N = 2NT);
-// corr += A_lo B_hi.  %0 main, %1 corr, %2 a_hi, %3 a_lo, %4 b, %5 b step,
-// %6 idesc N=2NT, %7 idesc N=NT, %8 main accumulates, %9.. tap offsets
-#define SS_TAP_C(OFF, PRED)                                              \
-  "add.s64 ah, %2, " OFF ";\n\tadd.s64 al, %3, " OFF ";\n\t"            \
-  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ah, bd, %6, " PRED ";\n\t" \
-  "@e tcgen05.mma.cta_group::1.kind::f16 [%1], al, bd, %7, t;\n\t"        \
-  "add.s64 bd, bd, %5;\n\t"
+//   corr += A_lo B_hi.
 // split (NT = 128): corr (+)= A_lo B_hi; corr += A_hi B_lo; main (+)= A_hi B_hi.
-// %0 main, %1 corr, %2 a_hi, %3 a_lo, %4 b, %5 b step, %6 B_lo offset,
-// %7 idesc, %8 main accumulates, %9 corr accumulates, %10.. tap offsets
-#define SS_TAP_S(OFF, PM, PC)                                            \
-  "add.s64 ah, %2, " OFF ";\n\tadd.s64 al, %3, " OFF ";\n\t"            \
-  "add.s64 bl, bd, %6;\n\t"                                              \
-  "@e tcgen05.mma.cta_group::1.kind::f16 [%1], al, bd, %7, " PC ";\n\t"   \
-  "@e tcgen05.mma.cta_group::1.kind::f16 [%1], ah, bl, %7, t;\n\t"        \
-  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ah, bd, %7, " PM ";\n\t"   \
-  "add.s64 bd, bd, %5;\n\t"
-
-__device__ __forceinline__ void ss_stage_concat9(uint32_t dm, uint32_t dc, uint64_t ah, uint64_t al, uint64_t b,
-                                                 uint64_t bstep, uint32_t id2, uint32_t id1, uint32_t acc,
-                                                 const uint64_t* o) {
-  asm volatile(SS_HEAD "setp.ne.b32 p, %8, 0;\n\tmov.b64 bd, %4;\n\t"
-               SS_TAP_C("%9", "p") SS_TAP_C("%10", "t") SS_TAP_C("%11", "t") SS_TAP_C("%12", "t")
-               SS_TAP_C("%13", "t") SS_TAP_C("%14", "t") SS_TAP_C("%15", "t") SS_TAP_C("%16", "t")
-               SS_TAP_C("%17", "t") "}\n"
-               ::"r"(dm), "r"(dc), "l"(ah), "l"(al), "l"(b), "l"(bstep), "r"(id2), "r"(id1), "r"(acc),
-               "l"(o[0]), "l"(o[1]), "l"(o[2]), "l"(o[3]), "l"(o[4]), "l"(o[5]), "l"(o[6]), "l"(o[7]), "l"(o[8])
+__device__ __forceinline__ uint32_t elect_one_sync() {
+  uint32_t e;
+  asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 r;\n\telect.sync r|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+               : "=r"(e));
+  return e;
+}
+__device__ __forceinline__ void mma_f16_ss_if(uint32_t e, uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                              uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p, q;\n\tsetp.ne.b32 q, %0, 0;\n\tsetp.ne.b32 p, %5, 0;\n\t"
+               "@q tcgen05.mma.cta_group::1.kind::f16 [%1], %2, %3, %4, p;\n\t}"
+               ::"r"(e), "r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc)
                : "memory");
 }
-__device__ __forceinline__ void ss_stage_concat1(uint32_t dm, uint32_t dc, uint64_t ah, uint64_t al, uint64_t b,
-                                                 uint64_t bstep, uint32_t id2, uint32_t id1, uint32_t acc,
-                                                 const uint64_t* o) {
-  asm volatile(SS_HEAD "setp.ne.b32 p, %8, 0;\n\tmov.b64 bd, %4;\n\t" SS_TAP_C("%9", "p") "}\n"
-               ::"r"(dm), "r"(dc), "l"(ah), "l"(al), "l"(b), "l"(bstep), "r"(id2), "r"(id1), "r"(acc), "l"(o[0])
-               : "memory");
+template <int TAPS>
+__device__ __forceinline__ void ss_stage(bool concat, uint32_t dm, uint32_t dc, uint64_t ah, uint64_t al,
+                                             uint64_t b, uint64_t bstep, uint64_t blo, uint32_t id2, uint32_t id1,
+                                             uint32_t accm, uint32_t accc, const uint64_t* o) {
+  const uint32_t e = elect_one_sync();
+  if (concat) {
+#pragma unroll
+    for (int t = 0; t < TAPS; ++t) {
+      mma_f16_ss_if(e, dm, ah + o[t], b + t * bstep, id2, t ? 1u : accm);
+      mma_f16_ss_if(e, dc, al + o[t], b + t * bstep, id1, 1u);
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < TAPS; ++t) {
+      mma_f16_ss_if(e, dc, al + o[t], b + t * bstep, id1, t ? 1u : accc);
+      mma_f16_ss_if(e, dc, ah + o[t], b + t * bstep + blo, id1, 1u);
+      mma_f16_ss_if(e, dm, ah + o[t], b + t * bstep, id1, t ? 1u : accm);
+    }
+  }
 }
-__device__ __forceinline__ void ss_stage_split9(uint32_t dm, uint32_t dc, uint64_t ah, uint64_t al, uint64_t b,
-                                                uint64_t bstep, uint64_t blo, uint32_t id, uint32_t accm,
-                                                uint32_t accc, const uint64_t* o) {
-  asm volatile(SS_HEAD "setp.ne.b32 p, %8, 0;\n\tsetp.ne.b32 q, %9, 0;\n\tmov.b64 bd, %4;\n\t"
-               SS_TAP_S("%10", "p", "q") SS_TAP_S("%11", "t", "t") SS_TAP_S("%12", "t", "t")
-               SS_TAP_S("%13", "t", "t") SS_TAP_S("%14", "t", "t") SS_TAP_S("%15", "t", "t")
-               SS_TAP_S("%16", "t", "t") SS_TAP_S("%17", "t", "t") SS_TAP_S("%18", "t", "t") "}\n"
-               ::"r"(dm), "r"(dc), "l"(ah), "l"(al), "l"(b), "l"(bstep), "l"(blo), "r"(id), "r"(accm), "r"(accc),
-               "l"(o[0]), "l"(o[1]), "l"(o[2]), "l"(o[3]), "l"(o[4]), "l"(o[5]), "l"(o[6]), "l"(o[7]), "l"(o[8])
-               : "memory");
-}
-__device__ __forceinline__ void ss_stage_split1(uint32_t dm, uint32_t dc, uint64_t ah, uint64_t al, uint64_t b,
-                                                uint64_t bstep, uint64_t blo, uint32_t id, uint32_t accm,
-                                                uint32_t accc, const uint64_t* o) {
-  asm volatile(SS_HEAD "setp.ne.b32 p, %8, 0;\n\tsetp.ne.b32 q, %9, 0;\n\tmov.b64 bd, %4;\n\t"
-               SS_TAP_S("%10", "p", "q") "}\n"
-               ::"r"(dm), "r"(dc), "l"(ah), "l"(al), "l"(b), "l"(bstep), "l"(blo), "r"(id), "r"(accm), "r"(accc),
-               "l"(o[0])
-               : "memory");
-}
-#undef SS_HEAD
-#undef SS_TAP_C
-#undef SS_TAP_S
 
 template <int TAPS>
 __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_constant__ SsParams P) {
@@ -217,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       uint32_t ph = 0;
       for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
         const int n_tile = tile / P.m_tiles, m_tile = tile - n_tile * P.m_tiles;
-        const int64_t gs = (int64_t)m_tile * kTileM - P.halo;  // grid position of buffer slot 0
+        const int64_t gs = (int64_t)m_tile * kTileM * P.mt - P.halo;  // grid position of buffer slot 0
         const int64_t cs = gs < 0 ? 0 : gs;
         const int64_t ge = gs + P.span;
         const int64_t ce = ge > P.gtotal ? P.gtotal : ge;
@@ -261,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
       ptx::mbar_wait(ptx::smem_u32(&S->acc_empty[acc]), acc_ph ^ 1);
       ptx::tc_fence_after();
-      const uint32_t d_set = tmem + acc * set_cols;
+      const uint32_t d_tile = tmem + acc * P.mt * set_cols;
       int p = 0;
       for (int q = 0; q < P.nq; ++q) {
         tr(P, 1, 0x400 | q);
@@ -274,14 +247,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
         const uint64_t b0 = ptx::smem_desc_noswz(sb + P.nplanes * 4 * P.a_bytes, b_lbo, 128);
         const uint32_t main_acc = q >= NP ? 1u : 0u;
         if (do_mma) {
-          if (P.concat) {
-            const uint32_t dm = d_set + p * 2 * P.nt;
-            if (TAPS == 9) ss_stage_concat9(dm, dm + P.nt, a_hi, a_lo, b0, bstep, idesc2, idesc, main_acc, offs);
-            else ss_stage_concat1(dm, dm + P.nt, a_hi, a_lo, b0, bstep, idesc2, idesc, main_acc, offs);
-          } else {
-            const uint32_t dm = d_set + p * P.nt, dc = d_set + NP * P.nt;
-            if (TAPS == 9) ss_stage_split9(dm, dc, a_hi, a_lo, b0, bstep, blo, idesc, main_acc, q > 0, offs);
-            else ss_stage_split1(dm, dc, a_hi, a_lo, b0, bstep, blo, idesc, main_acc, q > 0, offs);
+          for (int sub = 0; sub < P.mt; ++sub) {
+            // sub-tile rows start 128 positions further in the same buffer
+            const uint32_t d_set = d_tile + sub * set_cols;
+            const uint32_t dm = P.concat ? d_set + p * 2 * P.nt : d_set + p * P.nt;
+            const uint32_t dc = P.concat ? dm + P.nt : d_set + NP * P.nt;
+            const uint64_t shift = (uint64_t)(sub * kTileM);
+            ss_stage<TAPS>(P.concat, dm, dc, a_hi + shift, a_lo + shift, b0, bstep, blo, idesc2, idesc, main_acc,
+                           q > 0, offs);
           }
         }
         if (++p == NP) p = 0;
@@ -309,8 +282,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       const uint32_t acc_ph = (acc_it / NB) & 1;
       if ((int)(acc & 1) != ew || (NB == 1 && ew == 1)) continue;
       const int n_tile = (int)P.div_mt.div(tile), m_tile = tile - n_tile * P.m_tiles;
+     for (int sub = 0; sub < P.mt; ++sub) {
       // grid position of this row (g < 2^31) -> image, padded row / column
-      const int g = m_tile * kTileM + row;
+      const int g = (m_tile * P.mt + sub) * kTileM + row;
       int b, gy, gx;
       bool valid;
       if (P.shared_grid) {
@@ -333,11 +307,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       // the residual input does not depend on the accumulators: load it first
       float sk[16];
       epi_load_skip(e, n_tile * P.nt, valid, b, yp - 1, xp - 1, sk);
-      if (lane == 0 && warp == 0) tr(P, 2, 0x700);
-      ptx::mbar_wait_warp(ptx::smem_u32(&S->acc_full[acc]), acc_ph);
-      if (lane == 0 && warp == 0) tr(P, 2, 0x800);
-      ptx::tc_fence_after();
-      const uint32_t d_set = tmem + lane_off + acc * set_cols;
+      if (sub == 0) {
+        if (lane == 0 && warp == 0) tr(P, 2, 0x700);
+        ptx::mbar_wait_warp(ptx::smem_u32(&S->acc_full[acc]), acc_ph);
+        if (lane == 0 && warp == 0) tr(P, 2, 0x800);
+        ptx::tc_fence_after();
+      }
+      const uint32_t d_set = tmem + lane_off + (acc * P.mt + sub) * set_cols;
       for (int c0 = 0; c0 < ((P.dbg & 4) ? 0 : P.nt); c0 += 16) {
         float v[16], t[16];
         if (P.concat) {
@@ -367,6 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
         if (lane == 0 && warp == 0) tr(P, 2, 0xE00 | c0);
         if (c0 + 16 < P.nt) epi_load_skip(e, n_tile * P.nt + c0 + 16, valid, b, yp - 1, xp - 1, sk);
       }
+     }
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->acc_empty[acc]));
@@ -403,7 +380,13 @@ bool make_ss_params(const ConvArgs& a, SsParams& P) {
   P.shared_grid = a.stride == 1;
   P.gtotal = a.stride == 1 ? in.kstride / 8 : (int64_t)a.batch * in.hp * in.wp;
   if (P.gtotal >= (1ll << 31)) return false;
-  P.m_tiles = (int)((P.gtotal + kTileM - 1) / kTileM);
+  // two 128-row sub-tiles per tile for small N: one stage, one weight copy
+  // and one set of hand-offs serve 256 positions
+  const char* mt_env = getenv("PCNN_SS_MT");
+  P.mt = mt_env ? atoi(mt_env) : (P.nt <= 32 ? 2 : 1);
+  if (P.mt < 1 || P.mt > 2) P.mt = 1;
+  const int tm = kTileM * P.mt;
+  P.m_tiles = (int)((P.gtotal + tm - 1) / tm);
   P.nq = (cpad + 15) / 16;
   P.last_groups = cpad % 16 == 0 ? 2 : 1;
   P.taps = a.kh * a.kw;
@@ -412,7 +395,7 @@ bool make_ss_params(const ConvArgs& a, SsParams& P) {
     P.nplanes = 1;
     P.plane_id[0] = 0;
     P.halo = a.kh == 3 ? in.wp + 1 : 0;
-    P.span = kTileM + 2 * P.halo;
+    P.span = tm + 2 * P.halo;
     P.vy0 = P.vx0 = 0;
     P.vy1 = in.h;
     P.vx1 = in.w;
@@ -428,12 +411,12 @@ bool make_ss_params(const ConvArgs& a, SsParams& P) {
     if (a.kh == 1) {
       P.nplanes = 1;
       P.plane_id[0] = 3;
-      P.span = kTileM;
+      P.span = tm;
       P.toff[0] = 0;
     } else {
       P.nplanes = 4;
       for (int i = 0; i < 4; ++i) P.plane_id[i] = i;
-      P.span = kTileM + in.wp + 1;
+      P.span = tm + in.wp + 1;
     }
   }
   if (a.stride == 2 && a.kh == 3)
@@ -464,11 +447,11 @@ bool make_ss_params(const ConvArgs& a, SsParams& P) {
     const int set = P.concat ? wp * 2 * P.nt : (wp + 1) * P.nt;
     // up to four buffers: the MMA warp runs ahead of two epilogue warpgroups
     for (int nb = kMaxAcc; nb >= 1 && !P.partials; --nb)
-      if (nb * set <= 512 && nb != 3) { P.partials = wp; P.acc_bufs = nb; }
+      if (nb * P.mt * set <= 512 && nb != 3) { P.partials = wp; P.acc_bufs = nb; }
   }
   if (!P.partials) return false;
   const uint32_t set = P.concat ? P.partials * 2 * P.nt : (P.partials + 1) * P.nt;
-  const uint32_t need = P.acc_bufs * set;
+  const uint32_t need = P.acc_bufs * P.mt * set;
   P.tmem_cols = need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
   P.div_hw = make_fastdiv((uint32_t)(P.hp * P.wp));
   P.div_h1 = make_fastdiv((uint32_t)P.hp);

@@ -125,19 +125,31 @@ __device__ __forceinline__ void epi_chunk16(const EpiParams& e, const EpiTab& T,
     float* o = v + grp * 4;
     const int ch0 = chb + grp * 4;
     if (e.pool == PCNN_POOL_GLOBAL) {
+      // a warp's 32 rows belong to at most two images unless the images are
+      // tiny: two segmented warp sums, one atomic per (image, channel)
       const float div = __ldg(e.pool_p);
-      const int b0 = __shfl_sync(0xffffffffu, b, 0);
-      const bool uniform = __all_sync(0xffffffffu, valid && b == b0);
+      const int lo_b = (int)__reduce_min_sync(0xffffffffu, valid ? (unsigned)b : 0x7fffffffu);
+      const int hi_b = (int)__reduce_max_sync(0xffffffffu, valid ? (unsigned)b : 0u);
+      if (lo_b == 0x7fffffff) continue;  // no valid row in this warp
+      if (hi_b - lo_b <= 1) {
+        const bool first = !valid || b == lo_b;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float sum = o[j] * div;
-        if (uniform) {
+        for (int j = 0; j < 4; ++j) {
+          float s0 = first ? o[j] * div : 0.f, s1 = first ? 0.f : o[j] * div;
 #pragma unroll
-          for (int off = 16; off; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
-          if (lane == 0 && ch0 + j < e.cout) atomicAdd(e.out.base + (int64_t)b0 * e.npad + ch0 + j, sum);
-        } else if (valid && ch0 + j < e.cout) {
-          atomicAdd(e.out.base + (int64_t)b * e.npad + ch0 + j, sum);
+          for (int off = 16; off; off >>= 1) {
+            s0 += __shfl_xor_sync(0xffffffffu, s0, off);
+            s1 += __shfl_xor_sync(0xffffffffu, s1, off);
+          }
+          if (lane == 0 && ch0 + j < e.cout) {
+            atomicAdd(e.out.base + (int64_t)lo_b * e.npad + ch0 + j, s0);
+            if (hi_b != lo_b) atomicAdd(e.out.base + (int64_t)hi_b * e.npad + ch0 + j, s1);
+          }
         }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (valid && ch0 + j < e.cout) atomicAdd(e.out.base + (int64_t)b * e.npad + ch0 + j, o[j] * div);
       }
     } else {
       // WINDOW order: lanes 4q..4q+3 hold the (dy, dx) = 00, 01, 10, 11 window pixels

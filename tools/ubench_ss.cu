@@ -71,6 +71,30 @@ __global__ void ubench_ss(unsigned long long* out, float* probe) {
       ++slot;
     }
   }
+  // A start shifted by s x 16 B (s = 0..7), M=128 N=32 and N=16; then taps
+  // cycling through shifts 0..8 like a 3x3 conv over a pitch-33 grid
+  for (int sh = 0; sh < 10; ++sh) {
+    for (int nn = 0; nn < 2; ++nn) {
+      const int N = nn ? 16 : 32;
+      const uint32_t idesc = ptx::idesc_f16(128, N);
+      __syncthreads();
+      if (warp == 1) {
+        const long long t0 = clock64();
+        for (int i = 0; i < 64; ++i) {
+          int s16 = sh < 8 ? sh : (sh == 8 ? (i % 9) / 3 * 33 + (i % 3) : (i % 9) / 3 * 32 + (i % 3));
+          s16 &= 63;  // stay inside the 4 KB A buffer region (the values do not matter)
+          const uint64_t ad = ptx::smem_desc_noswz(a0 + s16 * 16, 128 * 16, 128);
+          const uint64_t bd = ptx::smem_desc_noswz(b0, 256 * 16, 128);
+          ptx::mma_f16_ss_warp(tmem, ad, bd, idesc, i > 0);
+        }
+        ptx::mma_commit_warp(ptx::smem_u32(&bar));
+        ptx::mbar_wait(ptx::smem_u32(&bar), phase);
+        const long long t1 = clock64();
+        if (lane == 0) out[20 + sh * 2 + nn] = (unsigned long long)(t1 - t0) / 64;
+      }
+      phase ^= 1;
+    }
+  }
   __syncthreads();
   if (warp == 0) ptx::tmem_dealloc(tmem, 512);
 }
@@ -79,6 +103,7 @@ int main() {
   unsigned long long* d;
   float* p;
   cudaMalloc(&d, 64 * 8);
+  cudaMemset(d, 0, 64 * 8);
   cudaMalloc(&p, 128 * 4);
   cudaMemset(p, 0, 128 * 4);
   cudaFuncSetAttribute(ubench_ss, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384);
@@ -99,6 +124,9 @@ int main() {
     printf("\n");
     (void)Ns;
   }
+  printf("A start shifted by s*16 B, cycles/MMA (N=32, N=16):");
+  for (int sh = 0; sh < 8; ++sh) printf("  s=%d: %llu %llu", sh, h[20 + 2 * sh], h[21 + 2 * sh]);
+  printf("\n3x3 tap shifts, pitch 33: %llu %llu   pitch 32: %llu %llu\n", h[36], h[37], h[38], h[39]);
   printf("M=64 accumulator, column 0 per TMEM lane (value/64 = row+1):\n");
   for (int l = 0; l < 128; ++l) printf("%g%c", hp[l] / 64.f, (l % 32 == 31) ? '\n' : ' ');
   return 0;
