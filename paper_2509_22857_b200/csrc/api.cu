@@ -407,7 +407,10 @@ int pcnn_plan_last_status(const pcnn_plan* p) { return p ? *p->status_host : -1;
 int pcnn_forward(pcnn_plan* p, const float* x, float* logits, void* stream, int use_graph) {
   if (!p || !x || !logits) return fail(PCNN_ERR_INVALID, "pcnn_forward: null argument");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (!use_graph) {
+  // PCNN_NO_GRAPH=1: eager launches (ncu cannot replay the extended-launch
+  // kernels inside a CUDA graph)
+  static const bool no_graph = getenv("PCNN_NO_GRAPH") != nullptr;
+  if (!use_graph || no_graph) {
     enqueue_all(p, x, logits, s);
     PCNN_CUDA(cudaGetLastError());
     return PCNN_OK;

@@ -71,7 +71,7 @@ inline void launch_pdl(void (*kernel)(Params), int grid, int threads, size_t sme
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = off ? 0 : 1;
   cudaLaunchKernelEx(&cfg, kernel, P);
 }
 

@@ -6,6 +6,9 @@
 #   3. one --set full capture of the largest conv launch (source-level stalls)
 # Usage: tools/profile_round.sh <config> <round-tag> <full-capture kernel regex> <launch-skip>
 set -e
+# ncu's kernel replay fails on extended launches inside CUDA graphs: profile
+# eager, plain launches (identical kernels; the launch list compares shares)
+export PCNN_NO_PDL=1 PCNN_NO_GRAPH=1
 cfg=${1:-resnet20}; tag=${2:-r01}; kre=${3:-conv_ss_kernel}; skip=${4:-0}
 mkdir -p gpurun_out
 python bench.py --config $cfg --steps 5 --warmup 3 --no-cpu --no-redist-timing > gpurun_out/${tag}_${cfg}_plain.json 2> gpurun_out/${tag}_${cfg}_plain.err

@@ -27,8 +27,11 @@ def display(name):
     if "conv_ss_kernel" in name:
         return "conv_ss_kernel (fp16x2, halo tiles in smem)"
     if "conv_tc_kernel" in name:
-        return ("conv_tc_kernel (fp16x2, A in TMEM)" if "(bool)1" in name or ", true" in name
-                else "conv_tc_kernel (3xTF32, A in TMEM)")
+        # template <CBS, F16, SPL>: the second argument says fp16x2
+        import re
+        m = re.search(r"conv_tc_kernel<[^,]*,\s*([^,>]*)", name)
+        f16 = m is not None and m.group(1).strip() in ("1", "true", "(bool)1")
+        return "conv_tc_kernel (fp16x2, A in TMEM)" if f16 else "conv_tc_kernel (3xTF32, A in TMEM)"
     if "conv_simt" in name:
         return "conv_simt_kernel"
     return name.split("(")[0]
