@@ -384,6 +384,9 @@ def run_ours(args):
         flush_buf.fill_(1.0)
 
     stream = torch.cuda.current_stream()
+    # one checked forward: if an activation overflows the fp16 split format the
+    # engine reruns it in float32 and rescales those tensors (Engine.recalibrate)
+    eng.forward(x, out)
     for _ in range(max(args.warmup, 3)):
         eng.forward(x, out, check=False)
     torch.cuda.synchronize()

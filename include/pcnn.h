@@ -59,7 +59,9 @@ enum pcnn_status {
  * the 1x1 case, i.e. [B][nblk*cb].  offset is in floats from the workspace
  * base, for the plan's batch size. */
 typedef struct pcnn_tensor_desc {
-  int64_t c, h, w, cb, nblk, is_vector, offset, reserved;
+  int64_t c, h, w, cb, nblk, is_vector, offset;
+  int64_t scale_log2;  /* split storage keeps x * 2^scale_log2 (large activations
+                          are scaled into fp16 range; readers undo it)   */
 } pcnn_tensor_desc;
 
 /* ---- fused units ---------------------------------------------------------*/

@@ -46,7 +46,7 @@ class PcnnError(RuntimeError):
 
 
 class TensorDesc(ctypes.Structure):
-    _fields_ = [(n, c_i64) for n in ("c", "h", "w", "cb", "nblk", "is_vector", "offset", "reserved")]
+    _fields_ = [(n, c_i64) for n in ("c", "h", "w", "cb", "nblk", "is_vector", "offset", "scale_log2")]
 
 
 _UNIT_FIELDS = ("kind", "in_", "in2", "out", "cin", "cout", "kh", "kw", "stride", "pad",

@@ -76,6 +76,8 @@ TensorView make_view(const pcnn_tensor_desc& t, float* ws) {
   v.cbs = 0;
   while ((1 << v.cbs) < v.cb) ++v.cbs;
   v.split = 0;
+  v.sstore = ldexpf(1.f, (int)t.scale_log2);
+  v.sload = ldexpf(1.f, -(int)t.scale_log2);
   v.hp = v.wp = 0;
   v.kstride = v.pstride = 0;
   v.plane = 0;

@@ -43,6 +43,7 @@ struct TensorView {
   int64_t kstride;  // halves per 8-channel group (batch * hp * wp * 8, x4 planes for split 2)
   int64_t plane;    // split: halves per hi / lo plane
   int* flag;        // split: overflow flag (device)
+  float sstore, sload;  // split: stored value = x * sstore; x = stored * sload (powers of two)
   __host__ __device__ int cpad() const { return nblk * cb; }
   __host__ __device__ __forceinline__ int64_t index(int b, int ch, int y, int x) const {
     return ((((int64_t)b * nblk + (ch >> cbs)) * h + y) * w + x) * cb + (ch & (cb - 1));
@@ -131,7 +132,8 @@ __device__ __forceinline__ void store4_any(const TensorView& t, int b, int ch, i
   }
   const int64_t e = t.sindex(b, ch, y, x);
   uint2 hi, lo;
-  const bool ok = split_pair(v0, v1, hi.x, lo.x) & split_pair(v2, v3, hi.y, lo.y);
+  const float s = t.sstore;
+  const bool ok = split_pair(v0 * s, v1 * s, hi.x, lo.x) & split_pair(v2 * s, v3 * s, hi.y, lo.y);
   *reinterpret_cast<uint2*>(t.hi() + e) = hi;
   *reinterpret_cast<uint2*>(t.lo() + e) = lo;
   if (!ok) atomicExch(t.flag, 1);
@@ -148,8 +150,9 @@ __device__ __forceinline__ void store16_any(const TensorView& t, int b, int ch, 
   }
   uint32_t hi[8], lo[8];
   bool ok = true;
+  const float s = t.sstore;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) ok &= split_pair(v[2 * i], v[2 * i + 1], hi[i], lo[i]);
+  for (int i = 0; i < 8; ++i) ok &= split_pair(v[2 * i] * s, v[2 * i + 1] * s, hi[i], lo[i]);
   const int64_t e = t.sindex(b, ch, y, x);
 #pragma unroll
   for (int g = 0; g < 2; ++g) {
@@ -161,8 +164,10 @@ __device__ __forceinline__ void store16_any(const TensorView& t, int b, int ch, 
 
 // 8 channels (one 16-byte group) of a split tensor as fp32
 __device__ __forceinline__ void load8_split(const TensorView& t, int64_t e, float* v) {
-  const uint4 h = __ldg(reinterpret_cast<const uint4*>(t.hi() + e));
-  const uint4 l = __ldg(reinterpret_cast<const uint4*>(t.lo() + e));
+  // .cg (L2 only): inside a chained kernel the tensor is written by other
+  // SMs during the same launch, so L1 must not hold stale lines
+  const uint4 h = __ldcg(reinterpret_cast<const uint4*>(t.hi() + e));
+  const uint4 l = __ldcg(reinterpret_cast<const uint4*>(t.lo() + e));
   const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {l.x, l.y, l.z, l.w};
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -178,7 +183,7 @@ __device__ __forceinline__ void load16_any(const TensorView& t, int b, int ch, i
     const float4* s = reinterpret_cast<const float4*>(t.base + t.index(b, ch, y, x));
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const float4 f = __ldg(s + q);
+      const float4 f = __ldcg(s + q);
       v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
     }
     return;
@@ -186,6 +191,8 @@ __device__ __forceinline__ void load16_any(const TensorView& t, int b, int ch, i
   const int64_t e = t.sindex(b, ch, y, x);
   load8_split(t, e, v);
   load8_split(t, e + t.kstride, v + 8);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] *= t.sload;
 }
 
 // Output-pixel enumeration of a conv unit.  PLAIN walks (b, oy, ox);

@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
     const EpiParams& e = a.epi;
     const int row = threadIdx.x & 127;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const float wsc = __ldg(P.wscale);
+    const float wsc = __ldg(P.wscale) * a.in.sload;  // weight scale, input storage scale
     EpiTab etab = P.etab;
     etab.ptab = ptab;
     const int hw = P.hp * P.wp;

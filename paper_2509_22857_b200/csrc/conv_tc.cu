@@ -640,7 +640,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     const int ew = warp < 4 ? 0 : 1;
     const EpiParams& e = a.epi;
     const int row = threadIdx.x & 127;
-    const float wsc = F16 ? __ldg(P.wscale) : 1.f;
+    // fp16 weight scale, and the input's storage scale when it is split
+    const float wsc = (F16 ? __ldg(P.wscale) : 1.f) * (a.in.split ? a.in.sload : 1.f);
     EpiTab etab = P.etab;
     etab.ptab = ptab;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;

@@ -111,12 +111,13 @@ class Lowered:
     scalar: Dict[Tuple[str, str], bool]
 
     # -- descriptor tables for the C ABI --------------------------------------
-    def tensor_descs(self, batch: int):
+    def tensor_descs(self, batch: int, scale_log2=None):
         descs = []
         off = 0
-        for t in self.tensors:
+        for i, t in enumerate(self.tensors):
             descs.append(L.TensorDesc(c=t.c, h=t.h, w=t.w, cb=t.cb, nblk=t.nblk,
-                                      is_vector=int(t.is_vector), offset=off, reserved=0))
+                                      is_vector=int(t.is_vector), offset=off,
+                                      scale_log2=int(scale_log2[i]) if scale_log2 is not None else 0))
             off += _align(t.floats(batch))
         return L.array(L.TensorDesc, descs), off
 

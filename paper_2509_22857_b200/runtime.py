@@ -42,7 +42,7 @@ class Plan:
         torch = _torch()
         lw = engine.lw
         self.batch = batch
-        tdescs, floats = lw.tensor_descs(batch)
+        tdescs, floats = lw.tensor_descs(batch, engine.scale_log2)
         self.ws = torch.zeros(max(floats, 1), dtype=torch.float32, device=engine.device)
         self.units = lw.unit_descs(impl)
         self.tdescs = tdescs
@@ -134,6 +134,9 @@ class Engine:
         self.plans: Dict[int, Plan] = {}
         self.fallback_plans: Dict[int, Plan] = {}
         self.fallbacks = 0  # forwards recomputed on float32 tensors
+        # per tensor: split storage keeps x * 2^scale_log2 (set from the float32
+        # rerun's magnitudes when an activation left the fp16 range)
+        self.scale_log2 = np.zeros(len(self.lw.tensors), dtype=np.int64)
 
     # -- parameters -----------------------------------------------------------
     def repack(self, stream=None) -> None:
@@ -161,6 +164,28 @@ class Engine:
         if p is None:
             p = self.fallback_plans[batch] = Plan(self, batch, L.IMPL_FP32_TENSORS)
         return p
+
+    def recalibrate(self, f: "Plan") -> bool:
+        """After a float32 rerun on plan f: give every tensor whose magnitude
+        exceeds 2^13 a power-of-two storage scale that brings it back under
+        2^13 (2^2 of headroom below the split format's 2^15 limit) and drop the
+        cached fast plans.  Returns True if any scale changed."""
+        torch = _torch()
+        changed = False
+        for t, d in enumerate(f.tdescs):
+            if d.is_vector:
+                continue
+            n = int(f.batch * d.nblk * d.cb * d.h * d.w)
+            m = float(f.ws[int(d.offset):int(d.offset) + n].abs().max().item()) if n else 0.0
+            if not np.isfinite(m) or m <= 2.0 ** 13:
+                continue
+            k = 13 - int(np.ceil(np.log2(m)))
+            if k < self.scale_log2[t]:
+                self.scale_log2[t] = k
+                changed = True
+        if changed:
+            self.plans.clear()
+        return changed
 
     def out_shape(self, batch: int) -> Tuple[int, ...]:
         return (batch,) + tuple(self.lw.out_shape)
@@ -191,6 +216,7 @@ class Engine:
             f = self.fallback_plan(b)
             L.check(L.lib().pcnn_forward(f.handle, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()),
                                          _stream_handle(stream), int(use_graph)), "pcnn_forward")
+            self.recalibrate(f)
         return out
 
     def forward_host(self, x_host: np.ndarray, x_dev=None, out_dev=None, out_host=None, stream=None):
@@ -218,6 +244,7 @@ class Engine:
                                               ctypes.c_void_p(x_dev.data_ptr()), ctypes.c_void_p(out_dev.data_ptr()),
                                               _stream_handle(stream)), "pcnn_forward_host")
             (stream or torch.cuda.current_stream()).synchronize()
+            self.recalibrate(f)
         return out_host
 
     def forward_unit(self, batch: int, i: int, x, out, stream=None) -> None:
