@@ -120,6 +120,54 @@ __device__ __forceinline__ void epi_chunk16(const EpiParams& e, const EpiTab& T,
     if (valid) store16_any(e.out, b, chb, oy, ox, v);
     return;
   }
+  if (e.pool != PCNN_POOL_GLOBAL) {
+    // WINDOW order: lanes 4q..4q+3 hold the (dy, dx) = 00, 01, 10, 11 pixels
+    // of window q.  Lane 4q+j pools channels [4j, 4j+4) of window q, so all
+    // 32 lanes work: gather those 4 channels of the 4 pixels by shuffles.
+    const int j4 = lane & 3, src = lane & ~3;
+    float4 px[4];
+#pragma unroll
+    for (int pix = 0; pix < 4; ++pix) {
+      float4 mine = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const float a0 = __shfl_sync(0xffffffffu, v[4 * g], src + pix);
+        const float a1 = __shfl_sync(0xffffffffu, v[4 * g + 1], src + pix);
+        const float a2 = __shfl_sync(0xffffffffu, v[4 * g + 2], src + pix);
+        const float a3 = __shfl_sync(0xffffffffu, v[4 * g + 3], src + pix);
+        if (g == j4) mine = make_float4(a0, a1, a2, a3);
+      }
+      px[pix] = mine;
+    }
+    const int ch0 = chb + 4 * j4;
+    float4 r;
+    if (e.pool == PCNN_POOL_SUM2) {
+      const float dv = __ldg(e.pool_p);
+      r = make_float4((px[0].x + px[1].x + px[2].x + px[3].x) * dv, (px[0].y + px[1].y + px[2].y + px[3].y) * dv,
+                      (px[0].z + px[1].z + px[2].z + px[3].z) * dv, (px[0].w + px[1].w + px[2].w + px[3].w) * dv);
+    } else {
+      // bivariate tree: stage 1 pairs along the first axis, stage 2 across
+      const int64_t nc = (int64_t)(e.pool_deg + 1) * (e.pool_deg + 1) * e.npad;
+      const float* s1 = e.pool_p;
+      const float* s2 = e.pool_p + nc;
+      float4 u, w;
+      if (e.pool_order == 0) {  // w first: S1(q0,q1), S1(q2,q3) then S2 along h
+        u = bivariate4(s1, e.npad, e.pool_deg, ch0, px[0], px[1]);
+        w = bivariate4(s1, e.npad, e.pool_deg, ch0, px[2], px[3]);
+      } else {                  // h first: S1(q0,q2), S1(q1,q3) then S2 along w
+        u = bivariate4(s1, e.npad, e.pool_deg, ch0, px[0], px[2]);
+        w = bivariate4(s1, e.npad, e.pool_deg, ch0, px[1], px[3]);
+      }
+      r = bivariate4(s2, e.npad, e.pool_deg, ch0, u, w);
+    }
+    // padded channels (>= cout) stay zero; rows past M are not stored
+    if (ch0 + 0 >= e.cout) r.x = 0.f;
+    if (ch0 + 1 >= e.cout) r.y = 0.f;
+    if (ch0 + 2 >= e.cout) r.z = 0.f;
+    if (ch0 + 3 >= e.cout) r.w = 0.f;
+    if (valid) store4_any(e.out, b, ch0, oy >> 1, ox >> 1, r.x, r.y, r.z, r.w);
+    return;
+  }
 #pragma unroll
   for (int grp = 0; grp < 4; ++grp) {
     float* o = v + grp * 4;
