@@ -122,7 +122,8 @@ typedef struct pcnn_unit_desc {
   int64_t tc16_scale_off;        /* its {max|w|, 2^-e} pair (2 floats)       */
   int64_t tcss_off;              /* conv fp16x2 image of the shared-memory
                                     (halo tile) kernel, or -1                */
-  int64_t reserved[2];
+  int64_t flags;                 /* PCNN_FLAG_*                              */
+  int64_t reserved;
 } pcnn_unit_desc;
 
 /* ---- parameter packing (float64 master -> float32 compute images) -------*/
@@ -137,6 +138,13 @@ enum pcnn_pack_kind {
                                 conv kernel ([n][16-ch chunk][tap] blocks);
                                 aux = the fp16x2 image's scale pair;
                                 reserved = taps | cb << 16                  */
+};
+
+/* unit flags */
+enum pcnn_unit_flag {
+  PCNN_FLAG_S2D = 1    /* ingest: write the NCHW image as 2x2 space-to-depth
+                          blocks, channel (dy*2 + dx)*C + c at (y/2 + 1,
+                          x/2 + 1) -- row 0 and column 0 stay zero         */
 };
 
 typedef struct pcnn_pack_desc {

@@ -31,6 +31,8 @@ POOL_NONE, POOL_SUM2, POOL_BI2, POOL_GLOBAL = 0, 1, 2, 3
 # pack kinds
 PACK_CAST, PACK_BN_AFFINE, PACK_TC_WEIGHTS, PACK_TC16_WEIGHTS, PACK_TCSS_WEIGHTS = 1, 2, 3, 4, 5
 # conv implementations (pcnn_unit_desc.impl)
+# unit flags
+FLAG_S2D = 1
 IMPL_AUTO, IMPL_SIMT, IMPL_TF32, IMPL_F16X2, IMPL_FP32_TENSORS, IMPL_F16X2_SS = 0, 1, 2, 3, 4, 5
 # scale opcodes
 (OP_FILL, OP_LOAD, OP_MUL, OP_DIV, OP_SUB, OP_POWI, OP_SROOT, OP_AROOT, OP_RECIP, OP_SOLVE,
@@ -52,11 +54,11 @@ class TensorDesc(ctypes.Structure):
 _UNIT_FIELDS = ("kind", "in_", "in2", "out", "cin", "cout", "kh", "kw", "stride", "pad",
                 "w_off", "b_off", "affine_off", "residual", "res_off", "poly_deg", "poly_off",
                 "pool", "pool_off", "pool_deg", "pool_order", "in_mode", "in_div_off", "impl",
-                "tc_off", "npad", "tc16_off", "tc16_scale_off", "tcss_off")
+                "tc_off", "npad", "tc16_off", "tc16_scale_off", "tcss_off", "flags")
 
 
 class UnitDesc(ctypes.Structure):
-    _fields_ = [(n, c_i64) for n in _UNIT_FIELDS] + [("reserved", c_i64 * 2)]
+    _fields_ = [(n, c_i64) for n in _UNIT_FIELDS] + [("reserved", c_i64)]
 
     def __init__(self, **kw):
         defaults = {"in_": -1, "in2": -1, "out": -1, "w_off": -1, "b_off": -1, "affine_off": -1,

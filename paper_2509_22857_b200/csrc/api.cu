@@ -221,7 +221,7 @@ void enqueue_unit(pcnn_plan* p, int ui, const float* x, float* logits, cudaStrea
   const pcnn_unit_desc& u = p->units[ui];
   switch (u.kind) {
     case PCNN_UNIT_INGEST:
-      launch_ingest(x, p->views[u.out], p->batch, s);
+      launch_ingest(x, p->views[u.out], p->batch, (u.flags & PCNN_FLAG_S2D) != 0, s);
       break;
     case PCNN_UNIT_CONV: {
       const ConvArgs& a = p->conv_args[ui];

@@ -57,7 +57,7 @@ struct SsParams {
   int span;              // positions per loaded plane: 128 + halo + reach
   int nplanes;           // input planes loaded per stage (4 parity planes for 3x3 / stride 2)
   int plane_id[4];       // which parity plane goes to loaded slot i
-  int toff[9];           // tap -> A start in 16-byte units: slot * 4 * span + position offset
+  int toff[16];          // tap -> A start in 16-byte units: slot * 4 * span + position offset
   int vy0, vy1, vx0, vx1;  // grid rows / columns holding outputs (output = grid - v*0)
   int shared_grid;         // stride 1: split layout with shared borders (common.cuh)
   FastDiv div_h1;          // shared grid: rows per image (H + 1)
@@ -364,7 +364,8 @@ size_t ss_aux_bytes(const SsParams& P) {
 bool make_ss_params(const ConvArgs& a, SsParams& P) {
   const TensorView& in = a.in;
   if (!a.f16 || !a.tcwss || !a.tc16_scale) return false;
-  if ((a.stride != 1 && a.stride != 2) || a.kh != a.kw || !((a.kh == 3 && a.pad == 1) || (a.kh == 1 && a.pad == 0)))
+  if ((a.stride != 1 && a.stride != 2) || a.kh != a.kw ||
+      !((a.kh == 3 && a.pad == 1) || (a.kh == 1 && a.pad == 0) || (a.kh == 4 && a.pad == 1 && a.stride == 1)))
     return false;
   if (a.epi.pool != PCNN_POOL_NONE && a.epi.pool != PCNN_POOL_GLOBAL) return false;
   if (!(in.cpad() == 4 || in.cpad() == 8 || in.cpad() % 16 == 0) || a.npad < 16 || a.npad % 16) return false;
@@ -391,14 +392,15 @@ bool make_ss_params(const ConvArgs& a, SsParams& P) {
   P.last_groups = cpad % 16 == 0 ? 2 : 1;
   P.taps = a.kh * a.kw;
   if (a.stride == 1) {
-    // shared-border grid; tap (ky, kx) of output g reads g + (ky - 1) wp + kx - 1
+    // shared-border grid; tap (ky, kx) of output g reads g + (ky - pad) wp + kx - pad
+    // (the 4x4 space-to-depth stem reaches one position back, two forward)
     P.nplanes = 1;
     P.plane_id[0] = 0;
-    P.halo = a.kh == 3 ? in.wp + 1 : 0;
-    P.span = tm + 2 * P.halo;
+    P.halo = a.pad * in.wp + a.pad;
+    P.span = tm + P.halo + (a.kh - 1 - a.pad) * in.wp + (a.kw - 1 - a.pad);
     P.vy0 = P.vx0 = 0;
-    P.vy1 = in.h;
-    P.vx1 = in.w;
+    P.vy1 = a.pm.ho;  // = in.h for "same" convs; one less for the 4x4 stem
+    P.vx1 = a.pm.wo;
     for (int t = 0; t < P.taps; ++t) P.toff[t] = (t / a.kw) * in.wp + t % a.kw;
   } else {
     // parity planes: padded input (2y + ky, 2x + kx) = plane (ky & 1, kx & 1)
@@ -473,7 +475,8 @@ extern "C" int pcnn_ss_trace(unsigned long long* host, int n) {
 
 bool conv_ss_shape_ok(const ConvArgs& a) {
   if (!a.f16 || !a.tcwss || !a.tc16_scale) return false;
-  if ((a.stride != 1 && a.stride != 2) || a.kh != a.kw || !((a.kh == 3 && a.pad == 1) || (a.kh == 1 && a.pad == 0)))
+  if ((a.stride != 1 && a.stride != 2) || a.kh != a.kw ||
+      !((a.kh == 3 && a.pad == 1) || (a.kh == 1 && a.pad == 0) || (a.kh == 4 && a.pad == 1 && a.stride == 1)))
     return false;
   if (a.epi.pool != PCNN_POOL_NONE && a.epi.pool != PCNN_POOL_GLOBAL) return false;
   const int cpad = a.in.cpad();
@@ -507,7 +510,7 @@ void launch_conv_ss(const ConvArgs& a, cudaStream_t s) {
   const size_t smem = 128 + (size_t)P.stages * P.stage_bytes + ss_aux_bytes(P);
   const int tiles = P.m_tiles * P.n_tiles;
   const int grid = tiles < nsm ? tiles : nsm;
-  void (*k)(SsParams) = P.taps == 9 ? conv_ss_kernel<9> : conv_ss_kernel<1>;
+  void (*k)(SsParams) = P.taps == 16 ? conv_ss_kernel<16> : P.taps == 9 ? conv_ss_kernel<9> : conv_ss_kernel<1>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   launch_pdl(k, grid, kThreads, smem, s, P);
 }

@@ -49,7 +49,8 @@ inline int64_t host_pixel_count(const PixelMap& pm, int batch) {
   return pm.order == kPlain ? (int64_t)batch * pm.ho * pm.wo : (int64_t)batch * pm.hp * pm.wp * 4;
 }
 
-void launch_ingest(const float* x, const TensorView& t, int batch, cudaStream_t s);
+// s2d: x is [B][C/4][2H][2W] and t holds it as 2x2 blocks, channel (dy*2+dx)*(C/4)+c
+void launch_ingest(const float* x, const TensorView& t, int batch, bool s2d, cudaStream_t s);
 void launch_conv_simt(const ConvArgs& a, cudaStream_t s);
 void launch_linear(const LinearArgs& a, cudaStream_t s);
 void launch_eltwise(const EltArgs& a, cudaStream_t s);

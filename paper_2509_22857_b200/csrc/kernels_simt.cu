@@ -9,7 +9,7 @@ namespace pcnn {
 // ---------------------------------------------------------------------------
 // ingest: user NCHW float32 -> channel-blocked [B][nblk][H][W][cb], pad = 0
 // ---------------------------------------------------------------------------
-__global__ void ingest_kernel(const float* __restrict__ x, TensorView t, int batch) {
+__global__ void ingest_kernel(const float* __restrict__ x, TensorView t, int batch, int s2d) {
   // one thread per (image, 4-channel group, pixel); pixels fastest so the
   // NCHW reads of each channel plane are coalesced, one float4 store each
   const int64_t hw = (int64_t)t.h * t.w;
@@ -22,19 +22,33 @@ __global__ void ingest_kernel(const float* __restrict__ x, TensorView t, int bat
     const int g = (int)(r % groups), b = (int)(r / groups);
     const int y = (int)(p / t.w), xw = (int)(p - (int64_t)y * t.w);
     float v[4];
+    if (s2d) {
+      // channel ch = (dy*2 + dx)*cin + c of block (y, xw) = pixel (2(y-1)+dy,
+      // 2(xw-1)+dx); block row 0 and column 0 are zero
+      const int cin = t.c / 4, H = 2 * (t.h - 1), W = 2 * (t.w - 1);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int ch = g * 4 + j;
-      v[j] = ch < t.c ? __ldg(x + ((int64_t)b * t.c + ch) * hw + p) : 0.f;
+      for (int j = 0; j < 4; ++j) {
+        const int ch = g * 4 + j;
+        const int q = ch / cin, c = ch - q * cin;
+        v[j] = (ch < t.c && y > 0 && xw > 0)
+                   ? __ldg(x + (((int64_t)b * cin + c) * H + 2 * (y - 1) + (q >> 1)) * W + 2 * (xw - 1) + (q & 1))
+                   : 0.f;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int ch = g * 4 + j;
+        v[j] = ch < t.c ? __ldg(x + ((int64_t)b * t.c + ch) * hw + p) : 0.f;
+      }
     }
     store4_any(t, b, g * 4, y, xw, v[0], v[1], v[2], v[3]);
   }
 }
 
-void launch_ingest(const float* x, const TensorView& t, int batch, cudaStream_t s) {
+void launch_ingest(const float* x, const TensorView& t, int batch, bool s2d, cudaStream_t s) {
   int64_t total = (int64_t)batch * (t.cpad() / 4) * t.h * t.w;
   int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-  ingest_kernel<<<std::max(blocks, 1), 256, 0, s>>>(x, t, batch);
+  ingest_kernel<<<std::max(blocks, 1), 256, 0, s>>>(x, t, batch, s2d ? 1 : 0);
 }
 
 // ---------------------------------------------------------------------------

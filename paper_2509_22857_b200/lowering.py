@@ -166,7 +166,72 @@ def conv_weight_to_master(w: np.ndarray, npad: int, cin: int) -> Tuple[np.ndarra
 def conv_weight_from_master(m: np.ndarray, meta: Dict) -> np.ndarray:
     npad, nblk, cb, kh, kw = meta["npad"], meta["nblk"], meta["cb"], meta["kh"], meta["kw"]
     full = m.reshape(npad, nblk, kh, kw, cb).transpose(0, 1, 4, 2, 3).reshape(npad, nblk * cb, kh, kw)
+    if "s2d" in meta:
+        return s2d_weight_back(full[:meta["o"]], meta["s2d"])
     return np.array(full[:meta["o"], :meta["i"]])
+
+
+# ---------------------------------------------------------------------------
+# space-to-depth stem: a k x k / stride-2 conv (pad p, odd k) on a cin <= 4
+# image is the same function as a k' x k' / stride-1 conv on the image cut
+# into 2 x 2 blocks, X'[(dy,dx,c)][i][j] = X[c][2i+dy][2j+dx]:
+# W'[o][(dy,dx,c)][ti][tj] = W[o][c][2(ti-P)+p+dy][2(tj-P)+p+dx] (0 outside the
+# kernel), taps reaching P blocks back.  For 7x7/s2/p3: k' = 4, P = 2.  The
+# ingest stores X' shifted by one block (a zero first row and column, H/2+1 x
+# W/2+1), which turns the (-2..+1) reach into an ordinary pad-1 conv that
+# yields exactly H/2 x W/2 outputs: 4 cin <= 16 channels feed the halo-tile
+# kernel (one 16-channel chunk, 16 taps) instead of a 49-tap gather.
+# ---------------------------------------------------------------------------
+
+S2D_K, S2D_P = 4, 2  # the 7x7 / s2 / p3 stem
+
+
+def s2d_eligible(g: ModelGraph, shapes, nid: str) -> bool:
+    node = g.nodes[nid]
+    if not isinstance(node, ConvNode) or node.stride != 2 or node.padding != 3:
+        return False
+    o, i, kh, kw = node.weight.shape
+    if kh != 7 or kw != 7 or i > 4:
+        return False
+    preds = [s for s, d in g.edges if d == nid]
+    if len(preds) != 1 or not isinstance(g.nodes[preds[0]], InputNode):
+        return False
+    if len(g.consumer_edges(preds[0])) != 1:
+        return False
+    c, h, w = shapes[preds[0]]
+    return h % 2 == 0 and w % 2 == 0
+
+
+def s2d_weight(w: np.ndarray) -> np.ndarray:
+    o, cin, k, _ = w.shape
+    p = (k - 1) // 2
+    out = np.zeros((o, 4 * cin, S2D_K, S2D_K))
+    for ti in range(S2D_K):
+        for dy in range(2):
+            ky = 2 * (ti - S2D_P) + p + dy
+            if not 0 <= ky < k:
+                continue
+            for tj in range(S2D_K):
+                for dx in range(2):
+                    kx = 2 * (tj - S2D_P) + p + dx
+                    if not 0 <= kx < k:
+                        continue
+                    c0 = (dy * 2 + dx) * cin
+                    out[:, c0:c0 + cin, ti, tj] = w[:, :, ky, kx]
+    return out
+
+
+def s2d_weight_back(w2: np.ndarray, info: Dict) -> np.ndarray:
+    o, cin, k = w2.shape[0], info["cin"], info["k"]
+    p = (k - 1) // 2
+    w = np.zeros((o, cin, k, k))
+    for ky in range(k):
+        dy, ti = (ky - p) % 2, (ky - p - (ky - p) % 2) // 2 + S2D_P
+        for kx in range(k):
+            dx, tj = (kx - p) % 2, (kx - p - (kx - p) % 2) // 2 + S2D_P
+            c0 = (dy * 2 + dx) * cin
+            w[:, :, ky, kx] = w2[:, c0:c0 + cin, ti, tj]
+    return w
 
 
 def build_master(g: ModelGraph, shapes) -> Tuple[Dict[str, Dict[str, Slot]], List[np.ndarray], int, Dict]:
@@ -192,7 +257,12 @@ def build_master(g: ModelGraph, shapes) -> Tuple[Dict[str, Dict[str, Slot]], Lis
         cp = cpad_for(c_out)
         if isinstance(node, ConvNode):
             cin = shapes[preds[nid][0]][0]
-            m, meta = conv_weight_to_master(node.weight, cp, cin)
+            if s2d_eligible(g, shapes, nid):
+                m, meta = conv_weight_to_master(s2d_weight(node.weight), cp, 4 * cin)
+                meta["s2d"] = {"cin": cin, "k": node.weight.shape[2]}
+                meta["i"] = cin
+            else:
+                m, meta = conv_weight_to_master(node.weight, cp, cin)
             put(nid, "weight", m, **meta)
             put(nid, "bias", _vec(node.bias, cp))
         elif isinstance(node, LinearNode):
@@ -404,10 +474,15 @@ class _Builder:
                 continue
             node = g.nodes[nid]
             if isinstance(node, InputNode):
-                t = self.tensor(self.shapes[nid])
+                c, h, w = self.shapes[nid]
+                nxt = self.single(nid)
+                s2d = nxt is not None and "s2d" in self.slots.get(nxt[0], {}).get("weight", Slot(0, 0, {})).meta
+                # space-to-depth stem: the ingest writes the image as 2x2 blocks
+                # behind a zero first row and column
+                t = self.tensor((4 * c, h // 2 + 1, w // 2 + 1) if s2d else (c, h, w))
                 self.value[nid] = t
                 self.input_tensor = t
-                self.emit([nid], kind=L.UNIT_INGEST, out=t)
+                self.emit([nid], kind=L.UNIT_INGEST, out=t, flags=L.FLAG_S2D if s2d else 0)
             elif isinstance(node, ConvNode):
                 self.lower_conv(nid)
             elif isinstance(node, LinearNode):
@@ -445,6 +520,9 @@ class _Builder:
         wmeta = self.slots[nid]["weight"].meta
         u = dict(kind=L.UNIT_CONV, in_=src, cin=wmeta["i"], cout=wmeta["o"], kh=wmeta["kh"], kw=wmeta["kw"],
                  stride=node.stride, pad=node.padding, npad=wmeta["npad"])
+        if "s2d" in wmeta:
+            # 4x4 / stride-1 / pad-1 conv over the shifted blocked image
+            u.update(cin=4 * wmeta["i"], stride=1, pad=1)
         u["w_off"] = self.cast(nid, "weight")
         u["b_off"] = self.cast(nid, "bias")
         chain = [nid]
@@ -507,7 +585,8 @@ class _Builder:
             u["tc_off"] = self.tc_image(nid)
             u["tc16_off"], u["tc16_scale_off"] = self.tc16_image(nid)
             k, st, pd = wmeta["kh"], u["stride"], u["pad"]
-            if (wmeta["kh"] == wmeta["kw"] and st in (1, 2) and ((k == 3 and pd == 1) or (k == 1 and pd == 0))
+            if (wmeta["kh"] == wmeta["kw"] and st in (1, 2)
+                    and ((k == 3 and pd == 1) or (k == 1 and pd == 0) or (k == S2D_K and pd == 1 and st == 1))
                     and ((cp := wmeta["kp"] // (k * k)) in (4, 8) or cp % 16 == 0)
                     and u.get("pool", 0) in (L.POOL_NONE, L.POOL_GLOBAL)):
                 u["tcss_off"] = self.tcss_image(nid, u["tc16_scale_off"])

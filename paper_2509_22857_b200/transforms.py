@@ -661,7 +661,10 @@ def compile_pass(prog: Program, g: ModelGraph):
                 row = (n, k, 1, 1, 1)
                 col = (1, n, 1, 1, 1)
             p.factor(w.offset, w.n, tv, False, row)
-            p.factor(w.offset, w.n, tu[0], True, col)
+            # a space-to-depth stem reads the graph input, whose scale is
+            # pinned to one (its blocked channel order has no per-channel map)
+            if not ("s2d" in w.meta and isinstance(g.nodes[preds[nid][0]], InputNode)):
+                p.factor(w.offset, w.n, tu[0], True, col)
             p.factor(b.offset, b.n, tv, False, vec_spec(b.n))
         elif isinstance(node, BatchNormNode):
             st = sl["bn"]
