@@ -45,7 +45,47 @@ __global__ void ingest_kernel(const float* __restrict__ x, TensorView t, int bat
   }
 }
 
+// space-to-depth ingest, one thread per block position and all 16 channels:
+// per input channel two float2 row reads (coalesced across the warp), one
+// 16-channel store (whole 32-byte sectors in the split layout)
+__global__ void ingest_s2d_kernel(const float* __restrict__ x, TensorView t, int batch) {
+  const int cin = t.c / 4, H = 2 * (t.h - 1), W = 2 * (t.w - 1);
+  const int64_t hw = (int64_t)t.h * t.w;
+  const int64_t total = (int64_t)batch * hw;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(i / hw);
+    const int64_t p = i - (int64_t)b * hw;
+    const int y = (int)(p / t.w), xw = (int)(p - (int64_t)y * t.w);
+    float v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = 0.f;
+    if (y > 0 && xw > 0) {
+      for (int c = 0; c < cin; ++c) {
+#pragma unroll
+        for (int dy = 0; dy < 2; ++dy) {
+          const float2 f = __ldg(reinterpret_cast<const float2*>(
+              x + (((int64_t)b * cin + c) * H + 2 * (y - 1) + dy) * W + 2 * (xw - 1)));
+          v[(dy * 2) * cin + c] = f.x;       // (dy, dx = 0)
+          v[(dy * 2 + 1) * cin + c] = f.y;   // (dy, dx = 1)
+        }
+      }
+    }
+    if (t.cpad() >= 16 && (t.cb >= 16 || t.split)) {
+      store16_any(t, b, 0, y, xw, v);
+    } else {
+      for (int g = 0; g < t.cpad() / 4; ++g) store4_any(t, b, 4 * g, y, xw, v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+    }
+  }
+}
+
 void launch_ingest(const float* x, const TensorView& t, int batch, bool s2d, cudaStream_t s) {
+  if (s2d && t.c <= 16 && (2 * (t.w - 1)) % 2 == 0) {
+    const int64_t total = (int64_t)batch * t.h * t.w;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    ingest_s2d_kernel<<<std::max(blocks, 1), 256, 0, s>>>(x, t, batch);
+    return;
+  }
   int64_t total = (int64_t)batch * (t.cpad() / 4) * t.h * t.w;
   int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
   ingest_kernel<<<std::max(blocks, 1), 256, 0, s>>>(x, t, batch, s2d ? 1 : 0);
@@ -219,14 +259,29 @@ __global__ void __launch_bounds__(256) linear_kernel(LinearArgs a) {
   const TensorView& in = a.in;
   const int hw = in.h * in.w;
   const float div = a.in_div ? __ldg(a.in_div) : 1.f;
-  for (int e = threadIdx.x; e < BB * n; e += blockDim.x) {
+  if (a.in_mode == 0) {
+    // vector input: eight loads per thread in flight, then the stores
+    for (int e0 = threadIdx.x; e0 < BB * n; e0 += 8 * blockDim.x) {
+      float v8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * blockDim.x;
+        const int bb = e / n, j = e - bb * n;
+        v8[u] = (e < BB * n && b0 + bb < a.batch) ? __ldg(in.base + (int64_t)(b0 + bb) * in.cpad() + j) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * blockDim.x;
+        if (e < BB * n) xs[e] = v8[u];
+      }
+    }
+  }
+  for (int e = threadIdx.x; e < BB * n && a.in_mode != 0; e += blockDim.x) {
     int bb = e / n, j = e - bb * n;
     int b = b0 + bb;
     float v = 0.f;
     if (b < a.batch) {
-      if (a.in_mode == 0) {
-        v = __ldg(in.base + (int64_t)b * in.cpad() + j);
-      } else if (a.in_mode == 1) {
+      if (a.in_mode == 1) {
         int c = j / hw, r = j - c * hw;
         int y = r / in.w, xw = r - y * in.w;
         v = *in.at(b, c, y, xw);
@@ -252,10 +307,23 @@ __global__ void __launch_bounds__(256) linear_kernel(LinearArgs a) {
     float acc[BB];
 #pragma unroll
     for (int i = 0; i < BB; ++i) acc[i] = 0.f;
-    for (int j = lane; j < n; j += 32) {
-      float wv = __ldg(wr + j);
+    // eight weights per lane in flight before the FMAs (the loop was bound by
+    // one dependent global load per 16 FMAs)
+    for (int j0 = 0; j0 < n; j0 += 32 * 8) {
+      float wv[8];
 #pragma unroll
-      for (int i = 0; i < BB; ++i) acc[i] = fmaf(wv, xs[i * n + j], acc[i]);
+      for (int u = 0; u < 8; ++u) {
+        const int j = j0 + u * 32 + lane;
+        wv[u] = j < n ? __ldg(wr + j) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = j0 + u * 32 + lane;
+        if (j < n) {
+#pragma unroll
+          for (int i = 0; i < BB; ++i) acc[i] = fmaf(wv[u], xs[i * n + j], acc[i]);
+        }
+      }
     }
 #pragma unroll
     for (int i = 0; i < BB; ++i) {
@@ -422,6 +490,25 @@ __global__ void localpool_kernel(EltArgs a) {
     const int b = (int)(r / o.nblk);
     const int ch0 = blk * in.cb + gi * 4;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (a.k == 3) {
+      // all nine loads in flight at once
+      float4 t9[9];
+#pragma unroll
+      for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) {
+          const int iy = y * a.st - a.pad + dy, ix = xw * a.st - a.pad + dx;
+          const bool ok = iy >= 0 && iy < in.h && ix >= 0 && ix < in.w;
+          t9[dy * 3 + dx] = ok ? __ldg(reinterpret_cast<const float4*>(in.at(b, ch0, ok ? iy : 0, ok ? ix : 0)))
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+      for (int q = 0; q < 9; ++q) {
+        acc.x += t9[q].x; acc.y += t9[q].y; acc.z += t9[q].z; acc.w += t9[q].w;
+      }
+      store4_any(o, b, ch0, y, xw, acc.x * dv, acc.y * dv, acc.z * dv, acc.w * dv);
+      continue;
+    }
     for (int dy = 0; dy < a.k; ++dy) {
       const int iy = y * a.st - a.pad + dy;
       if (iy < 0 || iy >= in.h) continue;
