@@ -159,6 +159,25 @@ def measured_traffic(config, kernel):
         return None
 
 
+def step_roofline(eng, batch, step_ms):
+    """SURVEY 8(d)'s whole-step figure: Σ over conv layers of max(FLOP / P,
+    BYTES / BW) against the measured (graph-replay) step time, with P the
+    3xTF32-effective rate the SURVEY defines (bf16/2/3) and, stricter, the
+    rate of the three-fp16-product scheme this build uses (bf16/3)."""
+    hbm, bf16, _, basis = peaks()
+    out = {}
+    for key, P in (("p_tc_3xtf32", bf16 / 6.0), ("p_tc_fp16x2", bf16 / 3.0)):
+        t = 0.0
+        for u in eng.lw.units:
+            if u.get("kind") == 2:
+                f, b = unit_cost(eng.lw, u, batch)
+                t += max(f / (P * 1e12), b / (hbm * 1e9))
+        out[key] = {"p_tflops": round(P, 2), "roofline_time_us": round(t * 1e6, 1),
+                    "frac": round(t * 1e3 / step_ms, 4)}
+    out["basis"] = f"{basis}; measured step {step_ms:.4f} ms (graph replay, L2 flushed)"
+    return out
+
+
 def roofline(eng, batch, unit_ms, plan, config):
     """Roofline of the dominant kernel (the conv kernel with the largest share
     of the step), over all its launches in one step: achieved = algorithmic
@@ -469,6 +488,7 @@ def run_ours(args):
         return
     unit_ms = per_unit_times(eng, x, out, reps=max(3, min(args.steps, 10)), flush=flush)
     roof = roofline(eng, batch, unit_ms, plan, args.config)
+    roof["step"] = step_roofline(eng, batch, ms / args.steps)
     launches = plan.launches()
     line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
