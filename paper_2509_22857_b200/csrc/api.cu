@@ -60,6 +60,10 @@ struct pcnn_plan {
   bool any_split = false;
   int* status_dev = nullptr;   // bit 0: a split-format value left the fp16 range
   int* status_host = nullptr;  // pinned copy written by pcnn_forward_host
+  // halo-tile conv units run as chains (one persistent launch per run of
+  // consecutive units): chain_of[u] = chain index or -1
+  std::vector<SsChain*> chains;
+  std::vector<int> chain_of, chain_first, chain_len;
 };
 
 namespace {
@@ -156,6 +160,66 @@ void choose_formats(pcnn_plan* p) {
   }
 }
 
+// Experimental, opt-in (PCNN_CHAIN=1): runs of consecutive halo-tile units
+// become one persistent launch each.  Measured slower than separate PDL
+// launches on RN20/RN18, so plans default to one
+// launch per unit.  A layer depends on the chain layers
+// that write its input and residual: on the tiles covering its position range
+// when both are stride-1 convs over the same shared-border grid, else on all
+// their tiles.  Runs that cannot share a launch are shortened.
+void build_chains(pcnn_plan* p) {
+  const int n = (int)p->units.size();
+  p->chain_of.assign(n, -1);
+  if (!getenv("PCNN_CHAIN")) return;
+  std::vector<int> producer(p->tensors.size(), -1);
+  for (int i = 0; i < n; ++i)
+    if (p->units[i].out >= 0) producer[p->units[i].out] = i;
+  int i = 0;
+  while (i < n) {
+    if (p->impl[i] != 5) { ++i; continue; }
+    int j = i + 1;
+    static const int cap = getenv("PCNN_CHAIN_MAX") ? atoi(getenv("PCNN_CHAIN_MAX")) : 22;
+    while (j < n && p->impl[j] == 5 && j - i < cap) ++j;
+    int end = j;
+    static const int lo = getenv("PCNN_CHAIN_SINGLE") ? 0 : 1;  // debugging: one-layer chains
+    for (; end > i + lo; --end) {
+      const int m = end - i;
+      std::vector<ConvArgs> args(m);
+      std::vector<int> din(m), dinm(m), dsk(m), dskm(m);
+      for (int k = 0; k < m; ++k) {
+        const pcnn_unit_desc& u = p->units[i + k];
+        args[k] = p->conv_args[i + k];
+        auto dep = [&](int64_t t, int& d, int& mode) {
+          d = -1;
+          mode = 0;
+          if (t < 0) return;
+          const int q = producer[t];
+          if (q < i || q >= i + k) return;  // written before the launch
+          d = q - i;
+          mode = (u.stride == 1 && p->units[q].stride == 1 && p->views[t].split == 1) ? 1 : 2;
+        };
+        dep(u.in, din[k], dinm[k]);
+        if (u.residual) {
+          dep(u.in2, dsk[k], dskm[k]);
+        } else {
+          dsk[k] = -1;
+          dskm[k] = 0;
+        }
+      }
+      SsChain* c = ss_chain_create(args.data(), m, din.data(), dinm.data(), dsk.data(), dskm.data());
+      if (c) {
+        const int id = (int)p->chains.size();
+        p->chains.push_back(c);
+        p->chain_first.push_back(i);
+        p->chain_len.push_back(m);
+        for (int k = i; k < end; ++k) p->chain_of[k] = id;
+        break;
+      }
+    }
+    i = end > i ? end : i + 1;  // a single unit keeps the one-layer kernel
+  }
+}
+
 const float* P(const pcnn_plan* p, int64_t off) { return off < 0 ? nullptr : p->params + off; }
 
 int build_conv(pcnn_plan* p, int ui, ConvArgs& a) {
@@ -225,10 +289,26 @@ void enqueue_unit(pcnn_plan* p, int ui, const float* x, float* logits, cudaStrea
       break;
     case PCNN_UNIT_CONV: {
       const ConvArgs& a = p->conv_args[ui];
+      const bool chained = p->impl[ui] == 5 && p->chain_of[ui] >= 0;
+      if (chained && p->chain_first[p->chain_of[ui]] != ui) break;  // launched with its chain's first unit
       if (u.pool == PCNN_POOL_GLOBAL)
         cudaMemsetAsync(a.epi.out.base, 0, sizeof(float) * (size_t)p->batch * a.epi.out.cpad(), s);
-      if (p->impl[ui] == 5) launch_conv_ss(a, s);
-      else if (p->impl[ui] >= 2) launch_conv_tc(a, s);
+      if (chained) {
+        const int c = p->chain_of[ui];
+        // every global-pool output of the chain is zeroed before its launch
+        for (int j = ui + 1; j < ui + p->chain_len[c]; ++j) {
+          const pcnn_unit_desc& uj = p->units[j];
+          if (uj.pool == PCNN_POOL_GLOBAL) {
+            const ConvArgs& aj = p->conv_args[j];
+            cudaMemsetAsync(aj.epi.out.base, 0, sizeof(float) * (size_t)p->batch * aj.epi.out.cpad(), s);
+          }
+        }
+        ss_chain_launch(p->chains[c], s);
+      } else if (p->impl[ui] == 5) {
+        launch_conv_ss(a, s);
+      } else if (p->impl[ui] >= 2) {
+        launch_conv_tc(a, s);
+      }
       else launch_conv_simt(a, s);
       break;
     }
@@ -366,6 +446,8 @@ int pcnn_plan_create(const pcnn_unit_desc* units, int n_units, const pcnn_tensor
   cudaMemset(p->status_dev, 0, sizeof(int));
   *p->status_host = 0;
   choose_formats(p);
+  build_chains(p);
+  for (int len : p->chain_len) p->launches -= len - 1;  // one kernel per chain
   if (cudaStreamCreateWithFlags(&p->capture_stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete p;
     return fail(PCNN_ERR_CUDA, "cudaStreamCreate failed");
@@ -378,6 +460,7 @@ int pcnn_plan_destroy(pcnn_plan* p) {
   if (!p) return PCNN_OK;
   for (auto& g : p->graphs) cudaGraphExecDestroy(g.exec);
   if (p->capture_stream) cudaStreamDestroy(p->capture_stream);
+  for (SsChain* c : p->chains) ss_chain_destroy(c);
   if (p->status_dev) cudaFree(p->status_dev);
   if (p->status_host) cudaFreeHost(p->status_host);
   delete p;

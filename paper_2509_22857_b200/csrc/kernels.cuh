@@ -60,8 +60,8 @@ void launch_copyout(const TensorView& t, float* dst, int batch, cudaStream_t s);
 // its prologue (barriers, TMEM allocation, parameter table) overlaps the tail
 // of the previous kernel, and griddep_wait() in the kernel orders the data.
 // PCNN_NO_PDL=1 launches it plainly.
-template <typename Params>
-inline void launch_pdl(void (*kernel)(Params), int grid, int threads, size_t smem, cudaStream_t s, const Params& P) {
+template <typename... Params, typename... Args>
+inline void launch_pdl(void (*kernel)(Params...), int grid, int threads, size_t smem, cudaStream_t s, Args... args) {
   static const bool off = getenv("PCNN_NO_PDL") != nullptr;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -73,7 +73,7 @@ inline void launch_pdl(void (*kernel)(Params), int grid, int threads, size_t sme
   at[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
   cfg.attrs = at;
   cfg.numAttrs = off ? 0 : 1;
-  cudaLaunchKernelEx(&cfg, kernel, P);
+  cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
 // tcgen05 path (conv_tc.cu); returns false if the shape is not supported
@@ -84,6 +84,16 @@ void tc_weight_image_dims(int npad, int kp, int64_t* floats);
 // fp16x2 conv with A from shared memory (conv_ss.cu): stride-1 3x3/1x1 convs
 // reading a split tensor
 bool conv_ss_supported(const ConvArgs& a);
+// A run of consecutive halo-tile conv layers in ONE persistent launch; each
+// layer's producer waits (per-tile counters) for the earlier chain layers
+// that write its input / residual: dep_* = chain index or -1, mode 1 = the
+// tiles covering the position range (stride-1 layers on the same grid), 2 =
+// all tiles.  nullptr if the layers cannot share one launch.
+struct SsChain;
+SsChain* ss_chain_create(const ConvArgs* args, int n, const int* dep_in, const int* dep_in_mode, const int* dep_sk,
+                         const int* dep_sk_mode);
+void ss_chain_launch(const SsChain* c, cudaStream_t s);
+void ss_chain_destroy(SsChain* c);
 // the shape/precision part of conv_ss_supported (input format not checked)
 bool conv_ss_shape_ok(const ConvArgs& a);
 void launch_conv_ss(const ConvArgs& a, cudaStream_t s);
