@@ -69,7 +69,9 @@ struct SsParams {
   int stages, partials, acc_bufs, concat;
   uint32_t tmem_cols;
   FastDiv div_hw, div_wp, div_mt;  // grid position decode, tile -> n_tile
+  int share_epi;         // both epilogue warpgroups drain every tile (alternate chunks)
   int dbg;
+  int time_slot;         // PCNN_TC_DEBUG bit 64: per-CTA globaltimer stamps slot, else -1
   // ---- chained launches (conv_chain_kernel) ----
   uint32_t buf_cols;        // TMEM columns between accumulator buffers
   int dep_in, dep_in_mode;  // chain index of the layer writing the input (-1: before the launch); 1 range, 2 all
@@ -92,6 +94,21 @@ struct ChainCommon {
 constexpr int kTraceLen = 1 << 16;
 constexpr int kTraceRegion = kTraceLen / 4;
 __device__ unsigned long long g_ss_trace[kTraceLen];
+
+// PCNN_TC_DEBUG bit 64: every CTA's thread 0 stamps %globaltimer at entry,
+// after griddepcontrol.wait, after its role loop and at exit (launch slot
+// assigned on the host; see pcnn_ss_cta_times)
+constexpr int kTimeSlots = 64, kTimeCtas = 160;
+__device__ unsigned long long g_cta_time[kTimeSlots][kTimeCtas][4];
+static int g_time_next = 0;
+
+__device__ __forceinline__ void cta_stamp(const SsParams& P, int k) {
+  if (P.time_slot >= 0 && threadIdx.x == 0 && blockIdx.x < kTimeCtas) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_cta_time[P.time_slot][blockIdx.x][k] = t;
+  }
+}
 
 struct Tracer {
   uint32_t n = 0;
@@ -165,6 +182,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
   const int NP = P.partials, NB = P.acc_bufs;
   const uint32_t set_cols = P.concat ? (uint32_t)NP * 2 * P.nt : (uint32_t)(NP + 1) * P.nt;
   Tracer tr;
+  cta_stamp(P, 0);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < P.stages; ++i) {
@@ -173,7 +191,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
     }
     for (int i = 0; i < kMaxAcc; ++i) {
       ptx::mbar_init(ptx::smem_u32(&S->acc_full[i]), 1);
-      ptx::mbar_init(ptx::smem_u32(&S->acc_empty[i]), 4);
+      ptx::mbar_init(ptx::smem_u32(&S->acc_empty[i]), P.share_epi ? 8 : 4);  // one arrive per draining warp
     }
     ptx::fence_mbar_init();
   }
@@ -196,6 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
   // previous kernel
   ptx::griddep_wait();
   ptx::griddep_launch();
+  cta_stamp(P, 1);
 
   if (warp == kWarpProducer) {
     // ===== producer: per (tile, 16-channel chunk) one stage = the tile's
@@ -283,7 +302,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       if (++acc == (uint32_t)NB) { acc = 0; acc_ph ^= 1; }
     }
   } else if (warp < 8) {
-    // ===== epilogue: warpgroup ew drains accumulator buffer ew =====
+    // ===== epilogue: a tile's 16-column chunks (sub-tile, channel chunk)
+    // k = 0 .. mt * nt / 16 - 1.  Unshared: warpgroup (buffer % 2) drains
+    // the whole buffer; shared: both warpgroups drain every buffer, warpgroup
+    // ew taking the chunks k = ew (mod 2), halving a tile's epilogue latency.
+    // The warpgroup walks its (tile, chunk) items in order and issues the
+    // next item's residual loads (across tiles too) before this item's math. =====
     const int ew = warp >> 2;
     const EpiParams& e = a.epi;
     const int row = threadIdx.x & 127;
@@ -292,46 +316,81 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
     EpiTab etab = P.etab;
     etab.ptab = ptab;
     const int hw = P.hp * P.wp;
-    uint32_t acc_it = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++acc_it) {
-      // buffer acc_it % NB, drained by warpgroup (buffer % 2); one buffer: warpgroup 0
-      const uint32_t acc = acc_it % NB;
-      const uint32_t acc_ph = (acc_it / NB) & 1;
-      if ((int)(acc & 1) != ew || (NB == 1 && ew == 1)) continue;
-      const int n_tile = (int)P.div_mt.div(tile), m_tile = tile - n_tile * P.m_tiles;
-     for (int sub = 0; sub < P.mt; ++sub) {
-      // grid position of this row (g < 2^31) -> image, padded row / column
-      const int g = (m_tile * P.mt + sub) * kTileM + row;
-      int b, gy, gx;
+    const int nch = P.nt >> 4, lg_nch = __ffs(nch) - 1, nk = P.mt * nch;  // nt / 16 is a power of two
+    const int k0 = P.share_epi ? ew : 0, kstep = P.share_epi ? 2 : 1;
+    struct Item {
+      int tile, k, n_tile, b, oy, ox;
+      uint32_t it;
       bool valid;
+    };
+    // this thread's row of sub-tile (k >> lg_nch) of the item's tile -> image, output row / column
+    auto locate = [&](Item& x) {
+      const int n_tile = (int)P.div_mt.div(x.tile), m_tile = x.tile - n_tile * P.m_tiles;
+      x.n_tile = n_tile;
+      const int g = (m_tile * P.mt + (x.k >> lg_nch)) * kTileM + row;
+      int gy, gx;
       if (P.shared_grid) {
         // position 1 + R (W+1) + x, global row R = b (H+1) + y + 1
         const int g1 = g > 0 ? g - 1 : 0;
         const int R = (int)P.div_wp.div(g1);
         gx = g1 - R * P.wp;
         const int R1 = R > 0 ? R - 1 : 0;
-        b = (int)P.div_h1.div(R1);
-        gy = R1 - b * P.hp;
-        valid = g >= 1 && R >= 1 && g < P.gtotal && gx < P.vx1 && gy < P.vy1 && b < a.batch;
+        x.b = (int)P.div_h1.div(R1);
+        gy = R1 - x.b * P.hp;
+        x.valid = g >= 1 && R >= 1 && g < P.gtotal && gx < P.vx1 && gy < P.vy1 && x.b < a.batch;
       } else {
-        b = (int)P.div_hw.div(g);
-        const int r = g - b * hw;
+        x.b = (int)P.div_hw.div(g);
+        const int r = g - x.b * hw;
         gy = (int)P.div_wp.div(r);
         gx = r - gy * P.wp;
-        valid = g < P.gtotal && gy >= P.vy0 && gy < P.vy1 && gx >= P.vx0 && gx < P.vx1;
+        x.valid = g < P.gtotal && gy >= P.vy0 && gy < P.vy1 && gx >= P.vx0 && gx < P.vx1;
       }
-      const int yp = gy - P.vy0 + 1, xp = gx - P.vx0 + 1;  // output pixel + 1
-      // the residual input does not depend on the accumulators: load it first
-      float sk[16];
-      epi_load_skip(e, n_tile * P.nt, valid, b, yp - 1, xp - 1, sk);
-      if (sub == 0) {
+      x.oy = gy - P.vy0;
+      x.ox = gx - P.vx0;
+    };
+    // next item of this warpgroup; false past the last
+    auto advance = [&](Item& x) -> bool {
+      x.k += kstep;
+      if (x.k < nk) return true;
+      for (;;) {
+        x.tile += gridDim.x;
+        ++x.it;
+        if (x.tile >= total_tiles) return false;
+        if (P.share_epi || ((int)((x.it % NB) & 1) == ew && !(NB == 1 && ew == 1))) break;
+      }
+      x.k = k0;
+      return true;
+    };
+    auto chan = [&](const Item& x) { return x.n_tile * P.nt + (x.k & (nch - 1)) * 16; };
+    Item cur;
+    cur.tile = (int)blockIdx.x - (int)gridDim.x;
+    cur.it = ~0u;
+    cur.k = nk;
+    bool have = advance(cur);
+    float sk[16];
+    if (have) {
+      locate(cur);
+      epi_load_skip(e, chan(cur), cur.valid, cur.b, cur.oy, cur.ox, sk);
+    }
+    while (have) {
+      Item nxt = cur;
+      const bool have_next = advance(nxt);
+      const bool last_of_tile = !have_next || nxt.tile != cur.tile;
+      float skn[16];
+      if (have_next) {
+        if (nxt.tile != cur.tile || (nxt.k >> lg_nch) != (cur.k >> lg_nch)) locate(nxt);
+        epi_load_skip(e, chan(nxt), nxt.valid, nxt.b, nxt.oy, nxt.ox, skn);
+      }
+      const uint32_t acc = cur.it % NB;
+      if (cur.k == k0) {
         if (lane == 0 && warp == 0) tr(P, 2, 0x700);
-        ptx::mbar_wait_warp(ptx::smem_u32(&S->acc_full[acc]), acc_ph);
+        ptx::mbar_wait_warp(ptx::smem_u32(&S->acc_full[acc]), (cur.it / NB) & 1);
         if (lane == 0 && warp == 0) tr(P, 2, 0x800);
         ptx::tc_fence_after();
       }
+      const int sub = cur.k >> lg_nch, c0 = (cur.k & (nch - 1)) * 16;
       const uint32_t d_set = tmem + lane_off + (acc * P.mt + sub) * set_cols;
-      for (int c0 = 0; c0 < ((P.dbg & 4) ? 0 : P.nt); c0 += 16) {
+      if (!(P.dbg & 4)) {
         float v[16], t[16];
         if (P.concat) {
           ptx::tmem_ld16x2(d_set + P.nt + c0, d_set + c0, v, t);
@@ -353,25 +412,39 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
             for (int i = 0; i < 16; ++i) v[i] += t[i];
           }
         }
+        if (last_of_tile) {
+          // the accumulators are in registers: release the buffer to the MMA warp
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->acc_empty[acc]));
+        }
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] *= wsc;
         if (lane == 0 && warp == 0) tr(P, 2, 0xD00 | c0);
-        epi_chunk16(e, etab, v, sk, n_tile * P.nt + c0, valid, valid ? b : 0, yp - 1, xp - 1, lane);
+        epi_chunk16(e, etab, v, sk, chan(cur), cur.valid, cur.valid ? cur.b : 0, cur.oy, cur.ox, lane);
         if (lane == 0 && warp == 0) tr(P, 2, 0xE00 | c0);
-        if (c0 + 16 < P.nt) epi_load_skip(e, n_tile * P.nt + c0 + 16, valid, b, yp - 1, xp - 1, sk);
+      } else if (last_of_tile) {
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->acc_empty[acc]));
       }
-     }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->acc_empty[acc]));
-      if (lane == 0 && warp == 0) tr(P, 2, 0x900);
+      if (last_of_tile && lane == 0 && warp == 0) tr(P, 2, 0x900);
+      if (!have_next) break;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) sk[i] = skn[i];
+      if (nxt.tile == cur.tile && (nxt.k >> lg_nch) == (cur.k >> lg_nch)) {
+        nxt.b = cur.b; nxt.oy = cur.oy; nxt.ox = cur.ox; nxt.valid = cur.valid; nxt.n_tile = cur.n_tile;
+      }
+      cur = nxt;
     }
   }
+  cta_stamp(P, 2);
   __syncthreads();
   if (warp == kWarpProducer) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, P.tmem_cols);
   }
+  cta_stamp(P, 3);
 }
 
 // ---- chained layers: one persistent launch runs a run of consecutive layers.
@@ -742,6 +815,7 @@ bool make_ss_params(const ConvArgs& a, SsParams& P) {
   if (P.stages < 2) return false;
   const char* dbg = getenv("PCNN_TC_DEBUG");
   P.dbg = dbg ? atoi(dbg) : 0;
+  P.time_slot = -1;
   // accumulators: as many partials as accuracy asks for, then two buffers
   // main products rotate over the partials per stage (taps MMAs each)
   const int stages_per_partial = kAddsPerPartial / P.taps > 0 ? kAddsPerPartial / P.taps : 1;
@@ -760,6 +834,9 @@ bool make_ss_params(const ConvArgs& a, SsParams& P) {
   const uint32_t need = P.acc_bufs * P.mt * set;
   P.tmem_cols = need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
   P.buf_cols = P.mt * set;
+  // shared epilogue when a tile has an even number of 16-column chunks
+  const char* sh = getenv("PCNN_SS_SHARE");
+  P.share_epi = sh ? atoi(sh) : ((P.mt * P.nt / 16) % 2 == 0);
   P.dep_in = P.dep_sk = -1;
   P.dep_in_mode = P.dep_sk_mode = 0;
   P.done = nullptr;
@@ -780,6 +857,19 @@ extern "C" int pcnn_ss_trace(unsigned long long* host, int n) {
   static unsigned long long zeros[kTraceLen];
   cudaMemcpyToSymbol(g_ss_trace, zeros, sizeof(zeros));
   return m;
+}
+
+// debugging aid (not part of pcnn.h): per-CTA stamps [slot][cta][4] in ns;
+// reset = 1 zeroes them, reset = 2 also restarts the host slot counter
+extern "C" int pcnn_ss_cta_times(unsigned long long* host, int reset) {
+  static unsigned long long buf[kTimeSlots][kTimeCtas][4];
+  if (host) cudaMemcpyFromSymbol(host, g_cta_time, sizeof(buf));
+  if (reset) {
+    static unsigned long long zeros[kTimeSlots][kTimeCtas][4];
+    cudaMemcpyToSymbol(g_cta_time, zeros, sizeof(zeros));
+  }
+  if (reset == 2) g_time_next = 0;
+  return g_time_next;
 }
 
 bool conv_ss_shape_ok(const ConvArgs& a) {
@@ -821,6 +911,7 @@ void launch_conv_ss(const ConvArgs& a, cudaStream_t s) {
   const int grid = tiles < nsm ? tiles : nsm;
   void (*k)(SsParams) = P.taps == 16 ? conv_ss_kernel<16> : P.taps == 9 ? conv_ss_kernel<9> : conv_ss_kernel<1>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (P.dbg & 64) P.time_slot = g_time_next++ % kTimeSlots;
   launch_pdl(k, grid, kThreads, smem, s, P);
 }
 
