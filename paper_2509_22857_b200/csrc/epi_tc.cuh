@@ -59,6 +59,19 @@ __device__ __forceinline__ void epi_load_skip(const EpiParams& e, int chb, bool 
   }
 }
 
+// one transposing butterfly step over 2 * O values: lanes with bit O set keep
+// the upper half, the others the lower half, each adding its partner's copy
+template <int O>
+__device__ __forceinline__ void butterfly_step(float* x, int lane) {
+  const bool up = (lane & O) != 0;
+#pragma unroll
+  for (int i = 0; i < O; ++i) {
+    const float send = up ? x[i] : x[i + O];
+    const float keep = up ? x[i + O] : x[i];
+    x[i] = keep + __shfl_xor_sync(0xffffffffu, send, O);
+  }
+}
+
 // v: accumulator values of channels [chb, chb + 16) (scaled to true units);
 // sk: their skip values (epi_load_skip); lanes of a warp hold consecutive
 // pixel rows (WINDOW order for 2x2 pools)
@@ -168,55 +181,35 @@ __device__ __forceinline__ void epi_chunk16(const EpiParams& e, const EpiTab& T,
     if (valid) store4_any(e.out, b, ch0, oy >> 1, ox >> 1, r.x, r.y, r.z, r.w);
     return;
   }
+  // GLOBAL: a warp's 32 rows belong to at most two images unless the images
+  // are tiny.  The 16 channels x 2 images are reduced over the 32 lanes by a
+  // transposing butterfly (31 shuffles): afterwards lane L holds the sum of
+  // image lo_b + L / 16, channel chb + L % 16, and all lanes add at once.
+  const float div = __ldg(e.pool_p);
+  const int lo_b = (int)__reduce_min_sync(0xffffffffu, valid ? (unsigned)b : 0x7fffffffu);
+  const int hi_b = (int)__reduce_max_sync(0xffffffffu, valid ? (unsigned)b : 0u);
+  if (lo_b == 0x7fffffff) return;  // no valid row in this warp
+  if (hi_b - lo_b <= 1) {
+    float x[32];
+    const bool first = !valid || b == lo_b;
 #pragma unroll
-  for (int grp = 0; grp < 4; ++grp) {
-    float* o = v + grp * 4;
-    const int ch0 = chb + grp * 4;
-    if (e.pool == PCNN_POOL_GLOBAL) {
-      // a warp's 32 rows belong to at most two images unless the images are
-      // tiny: two segmented warp sums, one atomic per (image, channel)
-      const float div = __ldg(e.pool_p);
-      const int lo_b = (int)__reduce_min_sync(0xffffffffu, valid ? (unsigned)b : 0x7fffffffu);
-      const int hi_b = (int)__reduce_max_sync(0xffffffffu, valid ? (unsigned)b : 0u);
-      if (lo_b == 0x7fffffff) continue;  // no valid row in this warp
-      if (hi_b - lo_b <= 1) {
-        const bool first = !valid || b == lo_b;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          float s0 = first ? o[j] * div : 0.f, s1 = first ? 0.f : o[j] * div;
-#pragma unroll
-          for (int off = 16; off; off >>= 1) {
-            s0 += __shfl_xor_sync(0xffffffffu, s0, off);
-            s1 += __shfl_xor_sync(0xffffffffu, s1, off);
-          }
-          if (lane == 0 && ch0 + j < e.cout) {
-            atomicAdd(e.out.base + (int64_t)lo_b * e.npad + ch0 + j, s0);
-            if (hi_b != lo_b) atomicAdd(e.out.base + (int64_t)hi_b * e.npad + ch0 + j, s1);
-          }
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (valid && ch0 + j < e.cout) atomicAdd(e.out.base + (int64_t)b * e.npad + ch0 + j, o[j] * div);
-      }
-    } else {
-      // WINDOW order: lanes 4q..4q+3 hold the (dy, dx) = 00, 01, 10, 11 window pixels
-      float q1[4], q2[4], q3[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        q1[j] = __shfl_down_sync(0xffffffffu, o[j], 1);
-        q2[j] = __shfl_down_sync(0xffffffffu, o[j], 2);
-        q3[j] = __shfl_down_sync(0xffffffffu, o[j], 3);
-      }
-      if (valid && (lane & 3) == 0) {
-        float pr[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          pr[j] = (ch0 + j < e.cout) ? epi_pool4(e, ch0 + j, o[j], q1[j], q2[j], q3[j]) : 0.f;
-        epi_store4(e, b, ch0, oy >> 1, ox >> 1, pr);
-      }
+    for (int j = 0; j < 16; ++j) {
+      const float t = v[j] * div;
+      x[j] = first ? t : 0.f;
+      x[16 + j] = first ? 0.f : t;
     }
+    butterfly_step<16>(x, lane);
+    butterfly_step<8>(x, lane);
+    butterfly_step<4>(x, lane);
+    butterfly_step<2>(x, lane);
+    butterfly_step<1>(x, lane);
+    const int ch = chb + (lane & 15);
+    if (ch < e.cout && (lane < 16 || hi_b != lo_b)) atomicAdd(e.out.base + (int64_t)(lo_b + (lane >> 4)) * e.npad + ch, x[0]);
+    return;
   }
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (valid && chb + j < e.cout) atomicAdd(e.out.base + (int64_t)b * e.npad + chb + j, v[j] * div);
 }
 
 }  // namespace pcnn
