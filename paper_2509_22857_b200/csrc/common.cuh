@@ -139,6 +139,27 @@ __device__ __forceinline__ void store4_any(const TensorView& t, int b, int ch, i
   if (!ok) atomicExch(t.flag, 1);
 }
 
+// 16 consecutive channels of a split tensor at half index e (channel group
+// 2j of the row; the second group is kstride further)
+__device__ __forceinline__ void store16_split_at(const TensorView& t, int64_t e, const float* v) {
+  uint32_t hi[8], lo[8];
+  const float s = t.sstore;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) split_pair(v[2 * i] * s, v[2 * i + 1] * s, hi[i], lo[i]);
+  // range check on the packed hi halves: max |hi| (NaN-propagating) < 2^15
+  __half2 m = __habs2(*reinterpret_cast<const __half2*>(&hi[0]));
+#pragma unroll
+  for (int i = 1; i < 8; ++i) m = __hmax2_nan(m, __habs2(*reinterpret_cast<const __half2*>(&hi[i])));
+  const float2 mf = __half22float2(m);
+  const bool ok = mf.x < 32768.f && mf.y < 32768.f;
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    *reinterpret_cast<uint4*>(t.hi() + e + g * t.kstride) = make_uint4(hi[4 * g], hi[4 * g + 1], hi[4 * g + 2], hi[4 * g + 3]);
+    *reinterpret_cast<uint4*>(t.lo() + e + g * t.kstride) = make_uint4(lo[4 * g], lo[4 * g + 1], lo[4 * g + 2], lo[4 * g + 3]);
+  }
+  if (!ok) atomicExch(t.flag, 1);
+}
+
 // store 16 consecutive channels (ch % 16 == 0; one block when fp32, cb >= 16):
 // whole 32-byte sectors per thread in both formats
 __device__ __forceinline__ void store16_any(const TensorView& t, int b, int ch, int y, int x, const float* v) {
@@ -148,18 +169,7 @@ __device__ __forceinline__ void store16_any(const TensorView& t, int b, int ch, 
     for (int q = 0; q < 4; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     return;
   }
-  uint32_t hi[8], lo[8];
-  bool ok = true;
-  const float s = t.sstore;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) ok &= split_pair(v[2 * i] * s, v[2 * i + 1] * s, hi[i], lo[i]);
-  const int64_t e = t.sindex(b, ch, y, x);
-#pragma unroll
-  for (int g = 0; g < 2; ++g) {
-    *reinterpret_cast<uint4*>(t.hi() + e + g * t.kstride) = make_uint4(hi[4 * g], hi[4 * g + 1], hi[4 * g + 2], hi[4 * g + 3]);
-    *reinterpret_cast<uint4*>(t.lo() + e + g * t.kstride) = make_uint4(lo[4 * g], lo[4 * g + 1], lo[4 * g + 2], lo[4 * g + 3]);
-  }
-  if (!ok) atomicExch(t.flag, 1);
+  store16_split_at(t, t.sindex(b, ch, y, x), v);
 }
 
 // 8 channels (one 16-byte group) of a split tensor as fp32
@@ -193,6 +203,92 @@ __device__ __forceinline__ void load16_any(const TensorView& t, int b, int ch, i
   load8_split(t, e + t.kstride, v + 8);
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] *= t.sload;
+}
+
+// The same 16 channels as raw 16-byte words (fp32: 4 x float4; split: hi/lo
+// of group 0, hi/lo of group 1): issue the loads early, decode at use, so the
+// load latency overlaps other work instead of stalling on the conversion.
+struct Raw16 {
+  uint4 q[4];
+};
+__device__ __forceinline__ void load16_raw(const TensorView& t, int b, int ch, int y, int x, Raw16& r) {
+  if (!t.split) {
+    const uint4* s = reinterpret_cast<const uint4*>(t.base + t.index(b, ch, y, x));
+#pragma unroll
+    for (int q = 0; q < 4; ++q) r.q[q] = __ldcg(s + q);
+    return;
+  }
+  const int64_t e = t.sindex(b, ch, y, x);
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    r.q[2 * g] = __ldcg(reinterpret_cast<const uint4*>(t.hi() + e + g * t.kstride));
+    r.q[2 * g + 1] = __ldcg(reinterpret_cast<const uint4*>(t.lo() + e + g * t.kstride));
+  }
+}
+__device__ __forceinline__ void decode16_raw(const TensorView& t, const Raw16& r, float* v) {
+  if (!t.split) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      v[4 * q] = __uint_as_float(r.q[q].x);
+      v[4 * q + 1] = __uint_as_float(r.q[q].y);
+      v[4 * q + 2] = __uint_as_float(r.q[q].z);
+      v[4 * q + 3] = __uint_as_float(r.q[q].w);
+    }
+    return;
+  }
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    const uint32_t hw[4] = {r.q[2 * g].x, r.q[2 * g].y, r.q[2 * g].z, r.q[2 * g].w};
+    const uint32_t lw[4] = {r.q[2 * g + 1].x, r.q[2 * g + 1].y, r.q[2 * g + 1].z, r.q[2 * g + 1].w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 a = unpack_half2(hw[i]), c = unpack_half2(lw[i]);
+      v[8 * g + 2 * i] = (a.x + c.x) * t.sload;
+      v[8 * g + 2 * i + 1] = (a.y + c.y) * t.sload;
+    }
+  }
+}
+
+// cp.async (L2 -> shared, no register dependency) of the 16 channels of one
+// row into four 16-byte slots dst + q * qstride, zero-filled when !ok; read
+// back with lds_raw16 + decode16_raw after cp.async.wait_group
+__device__ __forceinline__ void load16_async_src(const char* const* src, bool ok, uint32_t dst, uint32_t qstride) {
+  const uint32_t n = ok ? 16u : 0u;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst + q * qstride), "l"(src[q]), "r"(n)
+                 : "memory");
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+// split tensor, 16 channels at half index e (as store16_split_at)
+__device__ __forceinline__ void load16_async_at(const TensorView& t, int64_t e, bool ok, uint32_t dst,
+                                                uint32_t qstride) {
+  const char* src[4];
+  src[0] = reinterpret_cast<const char*>(t.hi() + e);
+  src[1] = reinterpret_cast<const char*>(t.lo() + e);
+  src[2] = reinterpret_cast<const char*>(t.hi() + e + t.kstride);
+  src[3] = reinterpret_cast<const char*>(t.lo() + e + t.kstride);
+  load16_async_src(src, ok, dst, qstride);
+}
+__device__ __forceinline__ void load16_async(const TensorView& t, int b, int ch, int y, int x, bool ok, uint32_t dst,
+                                             uint32_t qstride) {
+  if (!t.split) {
+    const char* src[4];
+    const float* p = t.base + (ok ? t.index(b, ch, y, x) : 0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) src[q] = reinterpret_cast<const char*>(p + 4 * q);
+    load16_async_src(src, ok, dst, qstride);
+    return;
+  }
+  load16_async_at(t, ok ? t.sindex(b, ch, y, x) : 0, ok, dst, qstride);
+}
+__device__ __forceinline__ void lds_raw16(uint32_t src, uint32_t qstride, Raw16& r) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.q[q].x), "=r"(r.q[q].y), "=r"(r.q[q].z), "=r"(r.q[q].w)
+                 : "r"(src + q * qstride)
+                 : "memory");
 }
 
 // Output-pixel enumeration of a conv unit.  PLAIN walks (b, oy, ox);

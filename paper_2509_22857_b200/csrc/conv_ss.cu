@@ -70,6 +70,8 @@ struct SsParams {
   uint32_t tmem_cols;
   FastDiv div_hw, div_wp, div_mt;  // grid position decode, tile -> n_tile
   int share_epi;         // both epilogue warpgroups drain every tile (alternate chunks)
+  int out_pos, skip_pos; // output / residual row of grid position g starts at half index 8 g (split,
+                         // same shared-border geometry as the input grid)
   int dbg;
   int time_slot;         // PCNN_TC_DEBUG bit 64: per-CTA globaltimer stamps slot, else -1
   // ---- chained launches (conv_chain_kernel) ----
@@ -110,11 +112,16 @@ __device__ __forceinline__ void cta_stamp(const SsParams& P, int k) {
   }
 }
 
+// compiled in only with -DPCNN_SS_TRACE (make NVEXTRA=-DPCNN_SS_TRACE)
 struct Tracer {
   uint32_t n = 0;
   __device__ __forceinline__ void operator()(const SsParams& P, int region, uint32_t tag) {
+#ifdef PCNN_SS_TRACE
     if ((P.dbg & 32) && blockIdx.x == 0 && n < kTraceRegion)
       g_ss_trace[region * kTraceRegion + n++] = ((unsigned long long)tag << 48) | (clock64() & 0xFFFFFFFFFFFFull);
+#else
+    (void)P; (void)region; (void)tag;
+#endif
   }
 };
 
@@ -318,8 +325,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
     const int hw = P.hp * P.wp;
     const int nch = P.nt >> 4, lg_nch = __ffs(nch) - 1, nk = P.mt * nch;  // nt / 16 is a power of two
     const int k0 = P.share_epi ? ew : 0, kstep = P.share_epi ? 2 : 1;
+    const int lg_nb = __ffs(NB) - 1;
+    // residual rows are staged in shared memory by cp.async one item ahead
+    // ([buffer][word][thread] x 16 bytes: conflict-free 16-byte reads)
+    const uint32_t skq = 256 * 16;
+    const uint32_t sk_slot = ptx::smem_u32(ptab + P.etab.rows * e.npad) + threadIdx.x * 16;
     struct Item {
-      int tile, k, n_tile, b, oy, ox;
+      int tile, k, n_tile, b, oy, ox, g;
       uint32_t it;
       bool valid;
     };
@@ -328,6 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       const int n_tile = (int)P.div_mt.div(x.tile), m_tile = x.tile - n_tile * P.m_tiles;
       x.n_tile = n_tile;
       const int g = (m_tile * P.mt + (x.k >> lg_nch)) * kTileM + row;
+      x.g = g;
       int gy, gx;
       if (P.shared_grid) {
         // position 1 + R (W+1) + x, global row R = b (H+1) + y + 1
@@ -356,35 +369,40 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
         x.tile += gridDim.x;
         ++x.it;
         if (x.tile >= total_tiles) return false;
-        if (P.share_epi || ((int)((x.it % NB) & 1) == ew && !(NB == 1 && ew == 1))) break;
+        if (P.share_epi || ((int)((x.it & (NB - 1)) & 1) == ew && !(NB == 1 && ew == 1))) break;
       }
       x.k = k0;
       return true;
     };
     auto chan = [&](const Item& x) { return x.n_tile * P.nt + (x.k & (nch - 1)) * 16; };
+    auto skip_async = [&](const Item& x, uint32_t dst) {
+      if (P.skip_pos)
+        load16_async_at(e.skip, (int64_t)(chan(x) >> 3) * e.skip.kstride + (int64_t)x.g * 8, x.valid, dst, skq);
+      else
+        load16_async(e.skip, x.b, chan(x), x.oy, x.ox, x.valid, dst, skq);
+    };
     Item cur;
     cur.tile = (int)blockIdx.x - (int)gridDim.x;
     cur.it = ~0u;
     cur.k = nk;
     bool have = advance(cur);
-    float sk[16];
+    uint32_t par = 0;  // staging buffer of the current item
     if (have) {
       locate(cur);
-      epi_load_skip(e, chan(cur), cur.valid, cur.b, cur.oy, cur.ox, sk);
+      if (e.residual) skip_async(cur, sk_slot);
     }
     while (have) {
       Item nxt = cur;
       const bool have_next = advance(nxt);
       const bool last_of_tile = !have_next || nxt.tile != cur.tile;
-      float skn[16];
       if (have_next) {
         if (nxt.tile != cur.tile || (nxt.k >> lg_nch) != (cur.k >> lg_nch)) locate(nxt);
-        epi_load_skip(e, chan(nxt), nxt.valid, nxt.b, nxt.oy, nxt.ox, skn);
+        if (e.residual) skip_async(nxt, sk_slot + (par ^ 1) * 4 * skq);
       }
-      const uint32_t acc = cur.it % NB;
+      const uint32_t acc = cur.it & (NB - 1);  // NB is 1, 2 or 4
       if (cur.k == k0) {
         if (lane == 0 && warp == 0) tr(P, 2, 0x700);
-        ptx::mbar_wait_warp(ptx::smem_u32(&S->acc_full[acc]), (cur.it / NB) & 1);
+        ptx::mbar_wait_warp(ptx::smem_u32(&S->acc_full[acc]), (cur.it >> lg_nb) & 1);
         if (lane == 0 && warp == 0) tr(P, 2, 0x800);
         ptx::tc_fence_after();
       }
@@ -418,10 +436,21 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->acc_empty[acc]));
         }
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] *= wsc;
         if (lane == 0 && warp == 0) tr(P, 2, 0xD00 | c0);
-        epi_chunk16(e, etab, v, sk, chan(cur), cur.valid, cur.valid ? cur.b : 0, cur.oy, cur.ox, lane);
+        float sk[16];
+        if (e.residual) {
+          // this item's group is complete once at most the next one is pending
+          if (have_next) asm volatile("cp.async.wait_group 1;" ::: "memory");
+          else asm volatile("cp.async.wait_group 0;" ::: "memory");
+          Raw16 r;
+          lds_raw16(sk_slot + par * 4 * skq, skq, r);
+          decode16_raw(e.skip, r, sk);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) sk[i] = 0.f;
+        }
+        epi_chunk16(e, etab, v, wsc, sk, chan(cur), cur.valid, cur.valid ? cur.b : 0, cur.oy, cur.ox, lane,
+                    P.out_pos ? (int64_t)cur.g * 8 : -1);
         if (lane == 0 && warp == 0) tr(P, 2, 0xE00 | c0);
       } else if (last_of_tile) {
         ptx::tc_fence_before();
@@ -430,8 +459,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       }
       if (last_of_tile && lane == 0 && warp == 0) tr(P, 2, 0x900);
       if (!have_next) break;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) sk[i] = skn[i];
+      par ^= 1;
       if (nxt.tile == cur.tile && (nxt.k >> lg_nch) == (cur.k >> lg_nch)) {
         nxt.b = cur.b; nxt.oy = cur.oy; nxt.ox = cur.ox; nxt.valid = cur.valid; nxt.n_tile = cur.n_tile;
       }
@@ -707,8 +735,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_chain_kernel(const SsParams*
               }
             }
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] *= wsc;
-            epi_chunk16(e, etab, v, sk, n_tile * P.nt + c0, valid, valid ? b : 0, yp - 1, xp - 1, lane);
+            epi_chunk16(e, etab, v, wsc, sk, n_tile * P.nt + c0, valid, valid ? b : 0, yp - 1, xp - 1, lane);
             if (c0 + 16 < P.nt) epi_load_skip(e, n_tile * P.nt + c0 + 16, valid, b, yp - 1, xp - 1, sk);
           }
         }
@@ -734,8 +761,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_chain_kernel(const SsParams*
   }
 }
 
+// residual staging: [2 buffers][4 words][256 epilogue threads] x 16 bytes
+constexpr uint32_t kSkipStage = 2 * 4 * 256 * 16;
+
 size_t ss_aux_bytes(const SsParams& P) {
-  return ((sizeof(Smem) + 15) & ~size_t(15)) + (size_t)P.etab.rows * P.a.epi.npad * 4;
+  return ((sizeof(Smem) + 15) & ~size_t(15)) + (size_t)P.etab.rows * P.a.epi.npad * 4 +
+         (P.a.epi.residual ? kSkipStage : 0);
 }
 
 bool make_ss_params(const ConvArgs& a, SsParams& P) {
@@ -806,6 +837,12 @@ bool make_ss_params(const ConvArgs& a, SsParams& P) {
   P.w = reinterpret_cast<const __half*>(a.tcwss);
   P.wscale = a.tc16_scale + 1;
   P.etab = epi_tab_layout(a.epi);
+  auto same_grid = [&](const TensorView& t) {
+    return P.shared_grid && t.split == 1 && !t.is_vector && t.hp == in.hp && t.wp == in.wp && P.vy0 == 0 &&
+           P.vx0 == 0;
+  };
+  P.out_pos = a.epi.pool == PCNN_POOL_NONE && same_grid(a.epi.out);
+  P.skip_pos = a.epi.residual && same_grid(a.epi.skip);
   P.a_bytes = (uint32_t)P.span * 16;
   P.b_bytes = (uint32_t)P.taps * 64 * P.nt;
   P.stage_bytes = P.nplanes * 4 * P.a_bytes + P.b_bytes;

@@ -711,7 +711,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         }
         float sk[16];
         epi_load_skip(e, chb, valid, b, oy, ox, sk);
-        epi_chunk16(e, etab, v, sk, chb, valid, b, oy, ox, lane);
+        epi_chunk16(e, etab, v, 1.f, sk, chb, valid, b, oy, ox, lane);
       }
       ptx::tc_fence_before();
       __syncwarp();

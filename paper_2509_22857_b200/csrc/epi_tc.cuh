@@ -72,17 +72,39 @@ __device__ __forceinline__ void butterfly_step(float* x, int lane) {
   }
 }
 
-// v: accumulator values of channels [chb, chb + 16) (scaled to true units);
+// raw form: issue now, decode (epi_skip_decode) right before the math
+__device__ __forceinline__ void epi_load_skip_raw(const EpiParams& e, int chb, bool valid, int b, int oy, int ox,
+                                                  Raw16& r) {
+  if (e.residual && valid) {
+    load16_raw(e.skip, b, chb, oy, ox, r);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) r.q[q] = make_uint4(0, 0, 0, 0);
+  }
+}
+__device__ __forceinline__ void epi_skip_decode(const EpiParams& e, const Raw16& r, float* sk) {
+  if (e.residual) {
+    decode16_raw(e.skip, r, sk);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) sk[j] = 0.f;
+  }
+}
+
+// v: accumulator values of channels [chb, chb + 16), times vscale in true units;
 // sk: their skip values (epi_load_skip); lanes of a warp hold consecutive
 // pixel rows (WINDOW order for 2x2 pools)
-__device__ __forceinline__ void epi_chunk16(const EpiParams& e, const EpiTab& T, float* v, const float* sk, int chb,
-                                            bool valid, int b, int oy, int ox, int lane) {
+// opos >= 0: the output is a split tensor whose row starts at half index
+// opos (+ channel-group terms), so no (b, y, x) addressing is needed
+__device__ __forceinline__ void epi_chunk16(const EpiParams& e, const EpiTab& T, float* v, float vscale,
+                                            const float* sk, int chb, bool valid, int b, int oy, int ox, int lane,
+                                            int64_t opos = -1) {
   const float* pt = T.ptab + chb;  // per-channel parameters, shared by all rows
   const int np = e.npad;
   float c[16];
   lds16(pt, c);
 #pragma unroll
-  for (int j = 0; j < 16; ++j) v[j] += c[j];
+  for (int j = 0; j < 16; ++j) v[j] = fmaf(v[j], vscale, c[j]);
   if (T.row_aff >= 0) {
     float sc[16], sh[16];
     lds16(pt + T.row_aff * np, sc);
@@ -125,18 +147,27 @@ __device__ __forceinline__ void epi_chunk16(const EpiParams& e, const EpiTab& T,
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] = h[j];
   }
+  if (chb + 16 > e.cout) {  // padded channels stay zero
 #pragma unroll
-  for (int j = 0; j < 16; ++j)
-    if (!valid || chb + j >= e.cout) v[j] = 0.f;
+    for (int j = 0; j < 16; ++j)
+      if (chb + j >= e.cout) v[j] = 0.f;
+  }
   if (e.pool == PCNN_POOL_NONE) {
     // the 16 channels are contiguous (cb >= 16)
-    if (valid) store16_any(e.out, b, chb, oy, ox, v);
+    if (valid) {
+      if (opos >= 0) store16_split_at(e.out, (int64_t)(chb >> 3) * e.out.kstride + opos, v);
+      else store16_any(e.out, b, chb, oy, ox, v);
+    }
     return;
   }
   if (e.pool != PCNN_POOL_GLOBAL) {
     // WINDOW order: lanes 4q..4q+3 hold the (dy, dx) = 00, 01, 10, 11 pixels
     // of window q.  Lane 4q+j pools channels [4j, 4j+4) of window q, so all
     // 32 lanes work: gather those 4 channels of the 4 pixels by shuffles.
+    if (!valid) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = 0.f;
+    }
     const int j4 = lane & 3, src = lane & ~3;
     float4 px[4];
 #pragma unroll
@@ -194,7 +225,7 @@ __device__ __forceinline__ void epi_chunk16(const EpiParams& e, const EpiTab& T,
     const bool first = !valid || b == lo_b;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      const float t = v[j] * div;
+      const float t = valid ? v[j] * div : 0.f;
       x[j] = first ? t : 0.f;
       x[16 + j] = first ? 0.f : t;
     }
