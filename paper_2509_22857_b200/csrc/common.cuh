@@ -141,9 +141,9 @@ __device__ __forceinline__ void store4_any(const TensorView& t, int b, int ch, i
 
 // 16 consecutive channels of a split tensor at half index e (channel group
 // 2j of the row; the second group is kstride further)
-__device__ __forceinline__ void store16_split_at(const TensorView& t, int64_t e, const float* v) {
+// (s: storage scale applied here, 1 when the caller folded it into its math)
+__device__ __forceinline__ void store16_split_at(const TensorView& t, int64_t e, const float* v, float s) {
   uint32_t hi[8], lo[8];
-  const float s = t.sstore;
 #pragma unroll
   for (int i = 0; i < 8; ++i) split_pair(v[2 * i] * s, v[2 * i + 1] * s, hi[i], lo[i]);
   // range check on the packed hi halves: max |hi| (NaN-propagating) < 2^15
@@ -169,7 +169,7 @@ __device__ __forceinline__ void store16_any(const TensorView& t, int b, int ch, 
     for (int q = 0; q < 4; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     return;
   }
-  store16_split_at(t, t.sindex(b, ch, y, x), v);
+  store16_split_at(t, t.sindex(b, ch, y, x), v, t.sstore);
 }
 
 // 8 channels (one 16-byte group) of a split tensor as fp32
@@ -225,7 +225,8 @@ __device__ __forceinline__ void load16_raw(const TensorView& t, int b, int ch, i
     r.q[2 * g + 1] = __ldcg(reinterpret_cast<const uint4*>(t.lo() + e + g * t.kstride));
   }
 }
-__device__ __forceinline__ void decode16_raw(const TensorView& t, const Raw16& r, float* v) {
+// (s: load scale for split words, 1 when the caller folded it into its math)
+__device__ __forceinline__ void decode16_raw(const TensorView& t, const Raw16& r, float* v, float s) {
   if (!t.split) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -243,8 +244,8 @@ __device__ __forceinline__ void decode16_raw(const TensorView& t, const Raw16& r
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const float2 a = unpack_half2(hw[i]), c = unpack_half2(lw[i]);
-      v[8 * g + 2 * i] = (a.x + c.x) * t.sload;
-      v[8 * g + 2 * i + 1] = (a.y + c.y) * t.sload;
+      v[8 * g + 2 * i] = (a.x + c.x) * s;
+      v[8 * g + 2 * i + 1] = (a.y + c.y) * s;
     }
   }
 }

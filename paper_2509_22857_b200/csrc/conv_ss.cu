@@ -72,6 +72,7 @@ struct SsParams {
   int share_epi;         // both epilogue warpgroups drain every tile (alternate chunks)
   int out_pos, skip_pos; // output / residual row of grid position g starts at half index 8 g (split,
                          // same shared-border geometry as the input grid)
+  int fold_skip, fold_out;  // storage scales folded into the epilogue table (epi_fill_tab)
   int dbg;
   int time_slot;         // PCNN_TC_DEBUG bit 64: per-CTA globaltimer stamps slot, else -1
   // ---- chained launches (conv_chain_kernel) ----
@@ -203,7 +204,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
     ptx::fence_mbar_init();
   }
   if (warp == kWarpProducer) ptx::tmem_alloc(ptx::smem_u32(&S->tmem_base), P.tmem_cols);
-  epi_fill_tab(a.epi, P.etab, ptab, threadIdx.x, kThreads);
+  epi_fill_tab(a.epi, P.etab, ptab, threadIdx.x, kThreads, P.fold_skip ? a.epi.skip.sload : 1.f,
+               P.fold_out ? a.epi.out.sstore : 1.f);
   if (P.last_groups == 1) {
     // cpad 4 / 8: the second 8-channel group of every stage stays zero
     for (int st = 0; st < P.stages; ++st)
@@ -444,13 +446,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
           else asm volatile("cp.async.wait_group 0;" ::: "memory");
           Raw16 r;
           lds_raw16(sk_slot + par * 4 * skq, skq, r);
-          decode16_raw(e.skip, r, sk);
+          decode16_raw(e.skip, r, sk, P.fold_skip ? 1.f : e.skip.sload);
         } else {
 #pragma unroll
           for (int i = 0; i < 16; ++i) sk[i] = 0.f;
         }
         epi_chunk16(e, etab, v, wsc, sk, chan(cur), cur.valid, cur.valid ? cur.b : 0, cur.oy, cur.ox, lane,
-                    P.out_pos ? (int64_t)cur.g * 8 : -1);
+                    P.out_pos ? (int64_t)cur.g * 8 : -1, P.fold_out ? 1.f : e.out.sstore);
         if (lane == 0 && warp == 0) tr(P, 2, 0xE00 | c0);
       } else if (last_of_tile) {
         ptx::tc_fence_before();
@@ -843,6 +845,10 @@ bool make_ss_params(const ConvArgs& a, SsParams& P) {
   };
   P.out_pos = a.epi.pool == PCNN_POOL_NONE && same_grid(a.epi.out);
   P.skip_pos = a.epi.residual && same_grid(a.epi.skip);
+  // split residual read by S: its load scale goes into S's rows; split output
+  // at a position (no pool) after a poly or S: its storage scale goes into them
+  P.fold_skip = a.epi.residual >= 2 && a.epi.skip.split;
+  P.fold_out = P.out_pos && (a.epi.poly_deg > 0 || a.epi.residual >= 2);
   P.a_bytes = (uint32_t)P.span * 16;
   P.b_bytes = (uint32_t)P.taps * 64 * P.nt;
   P.stage_bytes = P.nplanes * 4 * P.a_bytes + P.b_bytes;

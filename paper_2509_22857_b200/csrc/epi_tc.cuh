@@ -30,15 +30,30 @@ inline EpiTab epi_tab_layout(const EpiParams& e) {
   return t;
 }
 
-__device__ __forceinline__ void epi_fill_tab(const EpiParams& ep, const EpiTab& T, float* ptab, int tid, int nthreads) {
+// Scale folding (halo-tile kernel): yscale multiplies the rows of S's
+// skip variable (its powers), so split skip words enter without their load
+// scale; oscale multiplies the rows of the last stage (poly, else S), so the
+// result comes out already in storage units.  Both are powers of two: the
+// folded arithmetic is exact.
+__device__ __forceinline__ void epi_fill_tab(const EpiParams& ep, const EpiTab& T, float* ptab, int tid, int nthreads,
+                                             float yscale = 1.f, float oscale = 1.f) {
   const int np = ep.npad;
   for (int i = tid; i < T.rows * np; i += nthreads) {
     const int r = i / np, c = i - r * np;
     float v;
     if (r == 0) v = ep.bias[c];
     else if (T.row_aff >= 0 && r < T.row_aff + 2 && r >= T.row_aff) v = ep.aff[(r - T.row_aff) * np + c];
-    else if (T.row_poly >= 0 && r >= T.row_poly && r <= T.row_poly + ep.poly_deg) v = ep.poly[(r - T.row_poly) * np + c];
-    else v = ep.res[(r - T.row_res) * np + c];
+    else if (T.row_poly >= 0 && r >= T.row_poly && r <= T.row_poly + ep.poly_deg) {
+      v = ep.poly[(r - T.row_poly) * np + c] * oscale;
+    } else {
+      // S rows: x2 y2 xy x y c; the skip is y for residual 2, x for residual 3
+      const int k = r - T.row_res;
+      v = ep.res[k * np + c];
+      const int sq = ep.residual == 2 ? 1 : 0, lin = ep.residual == 2 ? 4 : 3;
+      if (k == sq) v *= yscale * yscale;
+      else if (k == 2 || k == lin) v *= yscale;
+      if (!ep.poly_deg) v *= oscale;
+    }
     ptab[i] = v;
   }
 }
@@ -84,7 +99,7 @@ __device__ __forceinline__ void epi_load_skip_raw(const EpiParams& e, int chb, b
 }
 __device__ __forceinline__ void epi_skip_decode(const EpiParams& e, const Raw16& r, float* sk) {
   if (e.residual) {
-    decode16_raw(e.skip, r, sk);
+    decode16_raw(e.skip, r, sk, e.skip.sload);
   } else {
 #pragma unroll
     for (int j = 0; j < 16; ++j) sk[j] = 0.f;
@@ -95,10 +110,11 @@ __device__ __forceinline__ void epi_skip_decode(const EpiParams& e, const Raw16&
 // sk: their skip values (epi_load_skip); lanes of a warp hold consecutive
 // pixel rows (WINDOW order for 2x2 pools)
 // opos >= 0: the output is a split tensor whose row starts at half index
-// opos (+ channel-group terms), so no (b, y, x) addressing is needed
+// opos (+ channel-group terms), so no (b, y, x) addressing is needed; then
+// ostore is its storage scale (1 when folded into the table, epi_fill_tab)
 __device__ __forceinline__ void epi_chunk16(const EpiParams& e, const EpiTab& T, float* v, float vscale,
                                             const float* sk, int chb, bool valid, int b, int oy, int ox, int lane,
-                                            int64_t opos = -1) {
+                                            int64_t opos = -1, float ostore = 1.f) {
   const float* pt = T.ptab + chb;  // per-channel parameters, shared by all rows
   const int np = e.npad;
   float c[16];
@@ -155,7 +171,7 @@ __device__ __forceinline__ void epi_chunk16(const EpiParams& e, const EpiTab& T,
   if (e.pool == PCNN_POOL_NONE) {
     // the 16 channels are contiguous (cb >= 16)
     if (valid) {
-      if (opos >= 0) store16_split_at(e.out, (int64_t)(chb >> 3) * e.out.kstride + opos, v);
+      if (opos >= 0) store16_split_at(e.out, (int64_t)(chb >> 3) * e.out.kstride + opos, v, ostore);
       else store16_any(e.out, b, chb, oy, ox, v);
     }
     return;

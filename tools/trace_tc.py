@@ -1,4 +1,5 @@
-"""Timeline of the tcgen05 conv pipeline in CTA 0 (PCNN_TC_DEBUG |= 32)."""
+"""Timeline of the tcgen05 conv pipeline in CTA 0 (PCNN_TC_DEBUG |= 32; for the
+halo-tile kernel (SS=1) build with `make -B NVEXTRA=-DPCNN_SS_TRACE` first)."""
 import ctypes, os, sys, pathlib
 sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
 import numpy as np, torch
