@@ -70,6 +70,12 @@ struct SsParams {
   uint32_t tmem_cols;
   FastDiv div_hw, div_wp, div_mt;  // grid position decode, tile -> n_tile
   int share_epi;         // both epilogue warpgroups drain every tile (alternate chunks)
+  int b_img_nt;          // rows per tile of the packed weight image (nt, or 128 when nt = 64)
+  // psub: 3x3 stride-2 conv staged one parity plane at a time (4 sub-stages
+  // per 16-channel chunk, each with that plane's taps): smaller stages, more
+  // of them in flight
+  int psub;
+  int pl_ntaps[4], pl_tap[4][4], pl_toff[4][4];
   int out_pos, skip_pos; // output / residual row of grid position g starts at half index 8 g (split,
                          // same shared-border geometry as the input grid)
   int fold_skip, fold_out;  // storage scales folded into the epilogue table (epi_fill_tab)
@@ -240,6 +246,41 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
         const int64_t ge = gs + P.span;
         const int64_t ce = ge > P.gtotal ? P.gtotal : ge;
         const uint32_t slot0 = (uint32_t)(cs - gs) * 16, bytes = (uint32_t)(ce - cs) * 16;
+        if (P.psub) {
+          // one parity plane and its taps' weights per stage
+          for (int q = 0; q < P.nq; ++q)
+            for (int ps = 0; ps < 4; ++ps) {
+              ptx::mbar_wait_sleep(ptx::smem_u32(&S->empty[st]), ph ^ 1);
+              const uint32_t bar = ptx::smem_u32(&S->full[st]);
+              const uint32_t sb = base + st * P.stage_bytes;
+              const int ng = q == P.nq - 1 ? P.last_groups : 2;
+              const int ntp = P.pl_ntaps[ps];
+              ptx::mbar_arrive_tx(bar, 2 * ng * bytes + (uint32_t)ntp * 64 * P.nt);
+              for (int g = 0; g < ng; ++g) {
+                const int64_t off = (2 * q + g) * a.in.kstride + P.plane_id[ps] * a.in.pstride + cs * 8;
+                ptx::bulk_g2s(sb + g * P.a_bytes + slot0, hi + off, bytes, bar);
+                ptx::bulk_g2s(sb + (2 + g) * P.a_bytes + slot0, lo + off, bytes, bar);
+              }
+              const int INT = P.b_img_nt, row0 = n_tile * P.nt, it = row0 / INT, r0 = row0 - it * INT;
+              for (int j = 0; j < ntp; ++j) {
+                const int t = P.pl_tap[ps][j];
+                const __half* blk = P.w + (((int64_t)it * P.nq + q) * P.taps + t) * 32 * INT;
+                const uint32_t dst = sb + 4 * P.a_bytes + (uint32_t)j * 64 * P.nt;
+                if (INT == P.nt) {
+                  ptx::bulk_g2s(dst, blk, 64 * P.nt, bar);
+                } else {
+                  const uint32_t rows_bytes = (uint32_t)P.nt * 16;
+                  for (int g = 0; g < 2; ++g) {
+                    ptx::bulk_g2s(dst + g * 32 * P.nt, blk + g * 16 * INT + r0 * 8, rows_bytes, bar);
+                    ptx::bulk_g2s(dst + g * 32 * P.nt + rows_bytes, blk + g * 16 * INT + (INT + r0) * 8, rows_bytes,
+                                  bar);
+                  }
+                }
+              }
+              if (++st == P.stages) { st = 0; ph ^= 1; }
+            }
+          continue;
+        }
         for (int q = 0; q < P.nq; ++q) {
           if (P.dbg & 2048) ptx::mbar_wait_nohint(ptx::smem_u32(&S->empty[st]), ph ^ 1);
           else ptx::mbar_wait_sleep(ptx::smem_u32(&S->empty[st]), ph ^ 1);
@@ -256,8 +297,22 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
               ptx::bulk_g2s(ps + (2 + g) * P.a_bytes + slot0, lo + off, bytes, bar);
             }
           }
-          ptx::bulk_g2s(sb + P.nplanes * 4 * P.a_bytes, P.w + ((int64_t)n_tile * P.nq + q) * P.taps * 32 * P.nt,
-                        P.b_bytes, bar);
+          if (P.b_img_nt == P.nt) {
+            ptx::bulk_g2s(sb + P.nplanes * 4 * P.a_bytes, P.w + ((int64_t)n_tile * P.nq + q) * P.taps * 32 * P.nt,
+                          P.b_bytes, bar);
+          } else {
+            // nt of the image's b_img_nt rows: per (tap, group) the hi and lo row ranges
+            const int INT = P.b_img_nt, row0 = n_tile * P.nt, it = row0 / INT, r0 = row0 - it * INT;
+            const uint32_t rows_bytes = (uint32_t)P.nt * 16;
+            for (int t = 0; t < P.taps; ++t) {
+              const __half* blk = P.w + (((int64_t)it * P.nq + q) * P.taps + t) * 32 * INT;
+              for (int g = 0; g < 2; ++g) {
+                const uint32_t dst = sb + P.nplanes * 4 * P.a_bytes + (uint32_t)(t * 32 * P.nt + g * 16 * P.nt) * 2;
+                ptx::bulk_g2s(dst, blk + g * 16 * INT + r0 * 8, rows_bytes, bar);
+                ptx::bulk_g2s(dst + rows_bytes, blk + g * 16 * INT + (INT + r0) * 8, rows_bytes, bar);
+              }
+            }
+          }
           if (++st == P.stages) { st = 0; ph ^= 1; }
         }
       }
@@ -281,7 +336,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       ptx::tc_fence_after();
       const uint32_t d_tile = tmem + acc * P.mt * set_cols;
       int p = 0;
+      const int nsub = P.psub ? 4 : 1;
       for (int q = 0; q < P.nq; ++q) {
+       for (int ps = 0; ps < nsub; ++ps) {
         tr(P, 1, 0x400 | q);
         ptx::mbar_wait(ptx::smem_u32(&S->full[st]), ph);
         tr(P, 1, 0x500 | q);
@@ -290,7 +347,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
         const uint64_t a_hi = ptx::smem_desc_noswz(sb, a_lbo, 128);
         const uint64_t a_lo = ptx::smem_desc_noswz(sb + 2 * P.a_bytes, a_lbo, 128);
         const uint64_t b0 = ptx::smem_desc_noswz(sb + P.nplanes * 4 * P.a_bytes, b_lbo, 128);
-        const uint32_t main_acc = q >= NP ? 1u : 0u;
+        // first writes: main partial at its first chunk's first sub-stage,
+        // correction at the tile's first sub-stage
+        const uint32_t main_acc = (q >= NP || ps > 0) ? 1u : 0u;
+        const uint32_t corr_acc = (q > 0 || ps > 0) ? 1u : 0u;
         if (do_mma) {
           for (int sub = 0; sub < P.mt; ++sub) {
             // sub-tile rows start 128 positions further in the same buffer
@@ -298,14 +358,33 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
             const uint32_t dm = P.concat ? d_set + p * 2 * P.nt : d_set + p * P.nt;
             const uint32_t dc = P.concat ? dm + P.nt : d_set + NP * P.nt;
             const uint64_t shift = (uint64_t)(sub * kTileM);
+            if constexpr (TAPS == 9) {
+              if (P.psub) {
+                uint64_t o4[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) o4[t] = (uint64_t)P.pl_toff[ps][t];
+                const int ntp = P.pl_ntaps[ps];
+                if (ntp == 4)
+                  ss_stage<4>(P.concat, dm, dc, a_hi + shift, a_lo + shift, b0, bstep, blo, idesc2, idesc, main_acc,
+                              corr_acc, o4);
+                else if (ntp == 2)
+                  ss_stage<2>(P.concat, dm, dc, a_hi + shift, a_lo + shift, b0, bstep, blo, idesc2, idesc, main_acc,
+                              corr_acc, o4);
+                else
+                  ss_stage<1>(P.concat, dm, dc, a_hi + shift, a_lo + shift, b0, bstep, blo, idesc2, idesc, main_acc,
+                              corr_acc, o4);
+                continue;
+              }
+            }
             ss_stage<TAPS>(P.concat, dm, dc, a_hi + shift, a_lo + shift, b0, bstep, blo, idesc2, idesc, main_acc,
-                           q > 0, offs);
+                           corr_acc, offs);
           }
         }
-        if (++p == NP) p = 0;
         ptx::mma_commit_warp(ptx::smem_u32(&S->empty[st]));
         tr(P, 1, 0x600 | q);
         if (++st == P.stages) { st = 0; ph ^= 1; }
+       }
+        if (++p == NP) p = 0;
       }
       ptx::mma_commit_warp(ptx::smem_u32(&S->acc_full[acc]));
       if (++acc == (uint32_t)NB) { acc = 0; acc_ph ^= 1; }
@@ -771,7 +850,9 @@ size_t ss_aux_bytes(const SsParams& P) {
          (P.a.epi.residual ? kSkipStage : 0);
 }
 
-bool make_ss_params(const ConvArgs& a, SsParams& P) {
+// nt: output channels per tile (the weight image is packed in tiles of
+// min(npad, 128) rows; a smaller nt copies its rows out of that image)
+static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub) {
   const TensorView& in = a.in;
   if (!a.f16 || !a.tcwss || !a.tc16_scale) return false;
   if ((a.stride != 1 && a.stride != 2) || a.kh != a.kw ||
@@ -783,8 +864,9 @@ bool make_ss_params(const ConvArgs& a, SsParams& P) {
   if (in.split != (a.stride == 2 ? 2 : 1)) return false;
   const int cpad = in.cpad();
   P.a = a;
-  P.nt = a.npad <= 128 ? a.npad : 128;
-  if (a.npad % P.nt) return false;
+  P.b_img_nt = a.npad <= 128 ? a.npad : 128;
+  P.nt = nt;
+  if (a.npad % P.nt || P.b_img_nt % P.nt) return false;
   P.n_tiles = a.npad / P.nt;
   P.hp = in.hp;
   P.wp = in.wp;
@@ -794,8 +876,10 @@ bool make_ss_params(const ConvArgs& a, SsParams& P) {
   // two 128-row sub-tiles per tile for small N: one stage, one weight copy
   // and one set of hand-offs serve 256 positions
   const char* mt_env = getenv("PCNN_SS_MT");
+  const char* mt16_env = getenv("PCNN_SS_MT16");  // experiment: sub-tiles for NT = 16 layers only
   P.mt = mt_env ? atoi(mt_env) : (P.nt <= 32 ? 2 : 1);
-  if (P.mt < 1 || P.mt > 2) P.mt = 1;
+  if (mt16_env && P.nt == 16) P.mt = atoi(mt16_env);
+  if (P.mt < 1 || P.mt > 4) P.mt = 1;
   const int tm = kTileM * P.mt;
   P.m_tiles = (int)((P.gtotal + tm - 1) / tm);
   P.nq = (cpad + 15) / 16;
@@ -836,6 +920,21 @@ bool make_ss_params(const ConvArgs& a, SsParams& P) {
       const int ky = t / 3, kx = t % 3;
       P.toff[t] = (((ky & 1) << 1) | (kx & 1)) * 4 * P.span + (ky >> 1) * in.wp + (kx >> 1);
     }
+  P.psub = 0;
+  if (psub) {
+    if (!(a.stride == 2 && a.kh == 3)) return false;
+    P.psub = 1;
+    P.nplanes = 1;  // stage layout: one plane
+    for (int pl = 0; pl < 4; ++pl) P.pl_ntaps[pl] = 0;
+    for (int t = 0; t < 9; ++t) {
+      const int ky = t / 3, kx = t % 3, pl = ((ky & 1) << 1) | (kx & 1);
+      const int j = P.pl_ntaps[pl]++;
+      P.pl_tap[pl][j] = t;
+      P.pl_toff[pl][j] = (ky >> 1) * in.wp + (kx >> 1);
+    }
+    for (int pl = 0; pl < 4; ++pl)
+      for (int j = P.pl_ntaps[pl]; j < 4; ++j) P.pl_tap[pl][j] = P.pl_toff[pl][j] = 0;
+  }
   P.w = reinterpret_cast<const __half*>(a.tcwss);
   P.wscale = a.tc16_scale + 1;
   P.etab = epi_tab_layout(a.epi);
@@ -850,7 +949,7 @@ bool make_ss_params(const ConvArgs& a, SsParams& P) {
   P.fold_skip = a.epi.residual >= 2 && a.epi.skip.split;
   P.fold_out = P.out_pos && (a.epi.poly_deg > 0 || a.epi.residual >= 2);
   P.a_bytes = (uint32_t)P.span * 16;
-  P.b_bytes = (uint32_t)P.taps * 64 * P.nt;
+  P.b_bytes = (uint32_t)(P.psub ? 4 : P.taps) * 64 * P.nt;  // psub: at most 4 taps per plane
   P.stage_bytes = P.nplanes * 4 * P.a_bytes + P.b_bytes;
   const size_t budget = 225 * 1024 - 128 - ss_aux_bytes(P);
   P.stages = (int)(budget / P.stage_bytes);
@@ -889,6 +988,20 @@ bool make_ss_params(const ConvArgs& a, SsParams& P) {
   P.div_wp = make_fastdiv((uint32_t)P.wp);
   P.div_mt = make_fastdiv((uint32_t)P.m_tiles);
   return true;
+}
+
+// Staging choice: whole-chunk stages (a 16-channel chunk of every plane and
+// all taps' weights) when two fit; else, for 3x3 stride 2, one parity plane
+// per stage (measured: faster than 64-channel tiles, slower than whole-chunk
+// stages when those fit); else two 64-channel tiles.  PCNN_SS_PSUB=0/1 forces.
+bool make_ss_params(const ConvArgs& a, SsParams& P) {
+  const int nt = a.npad <= 128 ? a.npad : 128;
+  const char* env = getenv("PCNN_SS_PSUB");
+  const int force = env ? atoi(env) : -1;
+  if (force == 1 && make_ss_params_nt(a, P, nt, true)) return true;
+  if (make_ss_params_nt(a, P, nt, false)) return true;
+  if (force != 0 && make_ss_params_nt(a, P, nt, true)) return true;
+  return nt == 128 && make_ss_params_nt(a, P, 64, false);
 }
 
 }  // namespace
@@ -983,7 +1096,7 @@ SsChain* ss_chain_create(const ConvArgs* args, int n, const int* dep_in, const i
   int ptab_max = 0, tiles_max = 0, taps_max = 1;
   std::vector<int> needed(n, 0);
   for (int i = 0; i < n; ++i) {
-    if (!make_ss_params(args[i], L[i])) return nullptr;
+    if (!make_ss_params(args[i], L[i]) || L[i].b_img_nt != L[i].nt || L[i].psub) return nullptr;
     if ((size_t)L[i].span * 16 > (1u << 17)) return nullptr;
     stage_max = stage_max > L[i].stage_bytes ? stage_max : L[i].stage_bytes;
     buf = buf > L[i].buf_cols ? buf : L[i].buf_cols;
