@@ -48,6 +48,7 @@ struct pcnn_plan {
   std::vector<pcnn_unit_desc> units;
   std::vector<pcnn_tensor_desc> tensors;
   std::vector<TensorView> views;
+  std::vector<char> prezeroed;  // unit's global-pool output zeroed by the previous kernel
   std::vector<int> impl;  // per unit: 1 SIMT, 2 tcgen05
   std::vector<ConvArgs> conv_args;
   int batch = 0, input = 0, output = 0;
@@ -291,7 +292,7 @@ void enqueue_unit(pcnn_plan* p, int ui, const float* x, float* logits, cudaStrea
       const ConvArgs& a = p->conv_args[ui];
       const bool chained = p->impl[ui] == 5 && p->chain_of[ui] >= 0;
       if (chained && p->chain_first[p->chain_of[ui]] != ui) break;  // launched with its chain's first unit
-      if (u.pool == PCNN_POOL_GLOBAL)
+      if (u.pool == PCNN_POOL_GLOBAL && !p->prezeroed[ui])
         cudaMemsetAsync(a.epi.out.base, 0, sizeof(float) * (size_t)p->batch * a.epi.out.cpad(), s);
       if (chained) {
         const int c = p->chain_of[ui];
@@ -447,6 +448,19 @@ int pcnn_plan_create(const pcnn_unit_desc* units, int n_units, const pcnn_tensor
   *p->status_host = 0;
   choose_formats(p);
   build_chains(p);
+  // a global-pool conv right after an unchained halo-tile conv: that kernel
+  // zeroes the sums in its prologue (keeps the launch chain free of memset
+  // nodes, which would break programmatic dependent launch)
+  p->prezeroed.assign(n_units, 0);
+  for (int i = 1; i < n_units; ++i) {
+    const pcnn_unit_desc& u = p->units[i];
+    if (u.kind != PCNN_UNIT_CONV || u.pool != PCNN_POOL_GLOBAL || p->chain_of[i] >= 0) continue;
+    if (p->impl[i - 1] != 5 || p->chain_of[i - 1] >= 0 || getenv("PCNN_NO_PREZERO")) continue;
+    ConvArgs& prev = p->conv_args[i - 1];
+    prev.prezero = p->conv_args[i].epi.out.base;
+    prev.prezero_n = (int64_t)p->batch * p->conv_args[i].epi.out.cpad();
+    p->prezeroed[i] = 1;
+  }
   for (int len : p->chain_len) p->launches -= len - 1;  // one kernel per chain
   if (cudaStreamCreateWithFlags(&p->capture_stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete p;
@@ -547,6 +561,11 @@ int pcnn_forward_host(pcnn_plan* p, const float* x_host, float* logits_host, flo
 
 int pcnn_forward_unit(pcnn_plan* p, int unit, const float* x, float* logits, void* stream) {
   if (!p || unit < 0 || unit >= (int)p->units.size()) return fail(PCNN_ERR_INVALID, "bad unit");
+  if (p->prezeroed[unit]) {  // run alone: its global-pool sums need their own zeroing
+    const ConvArgs& a = p->conv_args[unit];
+    cudaMemsetAsync(a.epi.out.base, 0, sizeof(float) * (size_t)p->batch * a.epi.out.cpad(),
+                    static_cast<cudaStream_t>(stream));
+  }
   enqueue_unit(p, unit, x, logits, static_cast<cudaStream_t>(stream));
   PCNN_CUDA(cudaGetLastError());
   return PCNN_OK;

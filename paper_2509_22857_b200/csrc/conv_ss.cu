@@ -225,6 +225,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = S->tmem_base;
+  // the next unit's global-pool sums (not touched by any kernel of this
+  // forward before this one)
+  if (a.prezero) {
+    float4* z = reinterpret_cast<float4*>(a.prezero);
+    const int64_t n4 = a.prezero_n / 4;
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n4; i += (int64_t)gridDim.x * kThreads)
+      z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   // everything above reads only parameters; activations come from the
   // previous kernel
   ptx::griddep_wait();

@@ -22,6 +22,10 @@ struct ConvArgs {
   const float* tcwss;       // fp16x2 image of the shared-memory kernel or null
   int f16;                  // launch_conv_tc: 1 = fp16x2 (kind::f16), 0 = 3xTF32
   EpiParams epi;
+  // halo-tile kernel: zero this buffer (the next unit's global-pool sums)
+  // in the prologue, instead of a memset node between the two launches
+  float* prezero = nullptr;
+  int64_t prezero_n = 0;  // floats, a multiple of 4
 };
 
 struct LinearArgs {
