@@ -506,13 +506,15 @@ def run_ours(args):
             "roofline": roof,
             "clocks": clocks.summary(),
             "unit_ms": [round(float(v), 4) for v in unit_ms]}
+    # (before the CPU baseline: its worker processes would load the host
+    # thread that drives the wall-clock timing)
+    if not args.no_redist_timing:
+        line["redistribution"] = time_redistribution(g, cfg)
     if not args.no_cpu and world == 1:
         ips, done, el, procs = cpu_reference(g, configs.make_input(cfg, batch=64), args.cpu_seconds)
         line["cpu_baseline"] = {"value": round(ips, 3), "unit": UNIT, "cores": procs, "kind": "port",
                                 "sample": f"{done} images in {el:.1f} s, float64 oracle reference_eval "
                                           f"(restates levnet graph.py:413) in {procs} processes"}
-    if not args.no_redist_timing:
-        line["redistribution"] = time_redistribution(g, cfg)
     print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
