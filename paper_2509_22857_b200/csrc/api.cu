@@ -349,6 +349,7 @@ void enqueue_unit(pcnn_plan* p, int ui, const float* x, float* logits, cudaStrea
       a.st = (int)u.stride;
       a.pad = (int)u.pad;
       a.axis = (int)u.pool_order;
+      a.pool = (int)u.pool;
       launch_eltwise(a, s);
       break;
     }

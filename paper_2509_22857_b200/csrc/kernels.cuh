@@ -47,6 +47,7 @@ struct EltArgs {
   const float* p;
   int64_t stride;
   int deg, k, st, pad, axis;
+  int pool = 0;  // LOCALPOOL: PCNN_POOL_BI2 = 2x2 window through two bivariate stages
 };
 
 inline int64_t host_pixel_count(const PixelMap& pm, int batch) {

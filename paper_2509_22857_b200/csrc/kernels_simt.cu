@@ -523,7 +523,53 @@ __global__ void localpool_kernel(EltArgs a) {
   }
 }
 
+// 2x2 / stride-2 window through two bivariate polynomials (axis 0: along w,
+// then across rows; 1: along h, then across columns), 4 channels per thread,
+// consecutive threads on consecutive memory (channel sub-group, then x);
+// fp32 blocked input, output in its storage format.  Restates the BI2 pool
+// of the conv epilogue (epi_tc.cuh) as a pass of its own.
+__global__ void bipool2_kernel(EltArgs a) {
+  const TensorView& in = a.in;
+  const TensorView& o = a.out;
+  const int sub_n = o.cb / 4;
+  const int64_t total = (int64_t)a.batch * o.nblk * o.h * o.w * sub_n;
+  const int64_t nc = (int64_t)(a.deg + 1) * (a.deg + 1) * a.stride;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i;
+    const int sub = (int)(r % sub_n); r /= sub_n;
+    const int x = (int)(r % o.w); r /= o.w;
+    const int y = (int)(r % o.h); r /= o.h;
+    const int blk = (int)(r % o.nblk);
+    const int b = (int)(r / o.nblk);
+    const int ch0 = blk * o.cb + 4 * sub;
+    const float4 q00 = __ldg(reinterpret_cast<const float4*>(in.pix(b, ch0, 2 * y, 2 * x)));
+    const float4 q01 = __ldg(reinterpret_cast<const float4*>(in.pix(b, ch0, 2 * y, 2 * x + 1)));
+    const float4 q10 = __ldg(reinterpret_cast<const float4*>(in.pix(b, ch0, 2 * y + 1, 2 * x)));
+    const float4 q11 = __ldg(reinterpret_cast<const float4*>(in.pix(b, ch0, 2 * y + 1, 2 * x + 1)));
+    float4 u, w;
+    if (a.axis == 0) {
+      u = bivariate4(a.p, a.stride, a.deg, ch0, q00, q01);
+      w = bivariate4(a.p, a.stride, a.deg, ch0, q10, q11);
+    } else {
+      u = bivariate4(a.p, a.stride, a.deg, ch0, q00, q10);
+      w = bivariate4(a.p, a.stride, a.deg, ch0, q01, q11);
+    }
+    float4 v = bivariate4(a.p + nc, a.stride, a.deg, ch0, u, w);
+    if (ch0 + 0 >= o.c) v.x = 0.f;
+    if (ch0 + 1 >= o.c) v.y = 0.f;
+    if (ch0 + 2 >= o.c) v.z = 0.f;
+    if (ch0 + 3 >= o.c) v.w = 0.f;
+    store4_any(o, b, ch0, y, x, v.x, v.y, v.z, v.w);
+  }
+}
+
 void launch_eltwise(const EltArgs& a, cudaStream_t s) {
+  if (a.kind == PCNN_UNIT_LOCALPOOL && a.pool == PCNN_POOL_BI2) {
+    const int64_t total = (int64_t)a.batch * a.out.nblk * a.out.h * a.out.w * (a.out.cb / 4);
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 32);
+    bipool2_kernel<<<std::max(blocks, 1), 256, 0, s>>>(a);
+    return;
+  }
   if (a.kind == PCNN_UNIT_GLOBALPOOL || a.kind == PCNN_UNIT_FLATTEN) {
     to_vector_kernel<<<148 * 8, 256, 0, s>>>(a);
     return;

@@ -26,6 +26,8 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Tuple
 
+import os
+
 import numpy as np
 
 from . import _lib as L
@@ -556,9 +558,25 @@ class _Builder:
             u["poly_off"] = self.cast(cur, "coeffs")
             nxt = self.single(cur)
         out_shape = sh[cur]
+        k, st, pd = wmeta["kh"], u["stride"], u["pad"]
+        # shapes the halo-tile kernel (conv_ss) runs; it has no 2x2-window
+        # epilogue, so for these a following 2x2 pool stays a separate unit
+        # (measured: conv_ss + pool pass beats the TMEM-A kernel with the
+        # pool fused, VGG-11; PCNN_FUSE_WINDOW_POOL=1 restores the fusion)
+        ss_shape = (self.use_tc and wmeta["npad"] % 16 == 0 and wmeta["npad"] >= 16
+                    and wmeta["kh"] == wmeta["kw"] and st in (1, 2)
+                    and ((k == 3 and pd == 1) or (k == 1 and pd == 0) or (k == S2D_K and pd == 1 and st == 1))
+                    and ((cp := wmeta["kp"] // (k * k)) in (4, 8) or cp % 16 == 0))
+        window_ok = not ss_shape or os.environ.get("PCNN_FUSE_WINDOW_POOL") == "1"
+        post_pool = None  # (first, second) BiPool nodes lowered as one 2x2 pool unit after the conv
         if nxt:
             pn = g.nodes[nxt[0]]
-            if isinstance(pn, LocalPoolNode) and pn.k == 2 and pn.stride == 2 and pn.padding == 0:
+            if not window_ok and isinstance(pn, (LocalPoolNode, BiPoolNode)):
+                nn = self.single(nxt[0]) if isinstance(pn, BiPoolNode) else None
+                if nn and isinstance(g.nodes[nn[0]], BiPoolNode) and g.nodes[nn[0]].axis != pn.axis \
+                        and g.nodes[nn[0]].degree == pn.degree and pn.degree <= 4:
+                    post_pool = (nxt[0], nn[0])
+            elif isinstance(pn, LocalPoolNode) and pn.k == 2 and pn.stride == 2 and pn.padding == 0:
                 cur = nxt[0]
                 chain.append(cur)
                 u["pool"] = L.POOL_SUM2
@@ -584,11 +602,7 @@ class _Builder:
         if self.use_tc and wmeta["npad"] % 16 == 0 and wmeta["npad"] >= 16:
             u["tc_off"] = self.tc_image(nid)
             u["tc16_off"], u["tc16_scale_off"] = self.tc16_image(nid)
-            k, st, pd = wmeta["kh"], u["stride"], u["pad"]
-            if (wmeta["kh"] == wmeta["kw"] and st in (1, 2)
-                    and ((k == 3 and pd == 1) or (k == 1 and pd == 0) or (k == S2D_K and pd == 1 and st == 1))
-                    and ((cp := wmeta["kp"] // (k * k)) in (4, 8) or cp % 16 == 0)
-                    and u.get("pool", 0) in (L.POOL_NONE, L.POOL_GLOBAL)):
+            if ss_shape and u.get("pool", 0) in (L.POOL_NONE, L.POOL_GLOBAL):
                 u["tcss_off"] = self.tcss_image(nid, u["tc16_scale_off"])
         t = self.tensor(out_shape)
         u["out"] = t
@@ -596,6 +610,16 @@ class _Builder:
             self.fused.add(c)
         self.value[cur] = t
         self.emit(chain, **u)
+        if post_pool:
+            # both bivariate stages of the 2x2 window in one pass (kernels_simt.cu bipool2_kernel)
+            a, b = post_pool
+            pn = g.nodes[a]
+            tp = self.tensor(sh[b])
+            self.fused.update(post_pool)
+            self.value[b] = tp
+            self.emit([a, b], kind=L.UNIT_LOCALPOOL, in_=t, out=tp, npad=cpad_for(sh[b][0]), kh=2, kw=2,
+                      stride=2, pad=0, pool=L.POOL_BI2, pool_deg=pn.degree,
+                      pool_order=0 if pn.axis == "w" else 1, pool_off=self.cast_pair(a, b))
 
     def lower_linear(self, nid: str):
         g = self.g
