@@ -37,8 +37,10 @@ namespace pcnn {
 
 namespace {
 
-constexpr int kThreads = 320;
+constexpr int kThreads = 352;
 constexpr int kWarpProducer = 8, kWarpMma = 9;
+constexpr int kWarpSignal = 10;  // flag mode: publishes finished tiles (idle otherwise)
+constexpr int kSigRing = 8;      // tile-stored barriers: 2 x the accumulator buffers
 constexpr int kTileM = 128;
 constexpr int kMaxStages = 8;
 constexpr int kMaxPartials = 4;
@@ -87,6 +89,11 @@ struct SsParams {
   int dep_sk, dep_sk_mode;  // same for the residual skip
   int* done;                // [m_tiles] finished n-tiles per m-tile, [m_tiles] all finished tiles; or null
   const __half* zeros;      // zero source for the missing second 8-channel group (cpad 4 / 8)
+  // wres: the whole weight image (one n-tile, every chunk) stays resident in
+  // shared memory after the stage ring, copied once before
+  // griddepcontrol.wait; the ring stages then hold activations only
+  int wres;
+  uint32_t res_bytes;       // resident weight bytes (nq * b_bytes), 0 without wres
 };
 
 // launch-wide configuration of a chain
@@ -137,7 +144,10 @@ constexpr int kMaxAcc = 4;  // accumulator buffers in TMEM
 struct Smem {
   uint64_t full[kMaxStages], empty[kMaxStages];
   uint64_t acc_full[kMaxAcc], acc_empty[kMaxAcc];
+  uint64_t wfull;  // resident weights landed
+  uint64_t tstored[kSigRing];  // flag mode: a tile's rows are stored (one arrival per draining warp)
   uint32_t tmem_base;
+  int dep_seq;     // flag mode: this CTA's tiles whose producer tiles were acquired
 };
 
 
@@ -183,14 +193,55 @@ __device__ __forceinline__ void ss_stage(bool concat, uint32_t dm, uint32_t dc, 
   }
 }
 
+// Flag-synchronised launches: wait until the producer tiles covering grid
+// positions [lo, hi) (mode 1) or all its tiles (mode 2) have bumped their
+// counters (release-ordered after their stores).  Bounded: a missing signal
+// traps instead of hanging the GPU.
+__device__ __forceinline__ void flag_wait(const FlagDep& d, int64_t lo, int64_t hi, bool& all_done) {
+  if (all_done) return;
+  {
+    // once the whole producer is done, no more per-tile polls
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(d.done + d.m_tiles) : "memory");
+    if (v >= d.all) {
+      all_done = true;
+      return;
+    }
+  }
+  auto wait_ge = [](const int* c, int target) {
+    uint32_t spins = 0;
+    for (;;) {
+      int v;
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+      if (v >= target) break;
+      __nanosleep(64);
+      if (++spins > (1u << 25)) __trap();
+    }
+  };
+  if (d.mode == 1) {
+    lo = lo < 0 ? 0 : lo;
+    hi = hi > d.gtotal ? d.gtotal : hi;
+    if (hi <= lo) return;
+    const int first = (int)(lo / d.tm);
+    int last = (int)((hi - 1) / d.tm);
+    if (last >= d.m_tiles) last = d.m_tiles - 1;
+    for (int t = first; t <= last; ++t) wait_ge(d.done + t, d.per_tile);
+  } else if (d.mode == 2) {
+    wait_ge(d.done + d.m_tiles, d.all);
+    all_done = true;
+  }
+}
+
 template <int TAPS>
 __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_constant__ SsParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   const ConvArgs& a = P.a;
-  Smem* S = reinterpret_cast<Smem*>(smem + (size_t)P.stages * P.stage_bytes);
-  float* ptab = reinterpret_cast<float*>(smem + (size_t)P.stages * P.stage_bytes + ((sizeof(Smem) + 15) & ~size_t(15)));
+  const size_t ring = (size_t)P.stages * P.stage_bytes;  // resident weights (wres) follow the ring
+  Smem* S = reinterpret_cast<Smem*>(smem + ring + P.res_bytes);
+  float* ptab = reinterpret_cast<float*>(smem + ring + P.res_bytes + ((sizeof(Smem) + 15) & ~size_t(15)));
   const uint32_t base = ptx::smem_u32(smem);
+  const uint32_t wres_base = base + (uint32_t)ring;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total_tiles = P.m_tiles * P.n_tiles;
   const int NP = P.partials, NB = P.acc_bufs;
@@ -207,6 +258,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       ptx::mbar_init(ptx::smem_u32(&S->acc_full[i]), 1);
       ptx::mbar_init(ptx::smem_u32(&S->acc_empty[i]), P.share_epi ? 8 : 4);  // one arrive per draining warp
     }
+    ptx::mbar_init(ptx::smem_u32(&S->wfull), 1);
+    for (int i = 0; i < kSigRing; ++i) ptx::mbar_init(ptx::smem_u32(&S->tstored[i]), P.share_epi ? 8 : 4);
+    S->dep_seq = 0;
     ptx::fence_mbar_init();
   }
   if (warp == kWarpProducer) ptx::tmem_alloc(ptx::smem_u32(&S->tmem_base), P.tmem_cols);
@@ -221,21 +275,30 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       }
     ptx::fence_proxy_async();
   }
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = S->tmem_base;
   // the next unit's global-pool sums (not touched by any kernel of this
-  // forward before this one)
+  // forward before this one); before the CTA barrier, so the epilogue's
+  // completion signals (flag mode) are ordered after these stores
   if (a.prezero) {
     float4* z = reinterpret_cast<float4*>(a.prezero);
     const int64_t n4 = a.prezero_n / 4;
     for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n4; i += (int64_t)gridDim.x * kThreads)
       z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = S->tmem_base;
+  // resident weights: parameters, not written by the previous kernel, so the
+  // copy overlaps its tail
+  if (P.wres && warp == kWarpProducer && lane == 0) {
+    const uint32_t wb = ptx::smem_u32(&S->wfull);
+    ptx::mbar_arrive_tx(wb, P.res_bytes);
+    ptx::bulk_g2s(wres_base, P.w, P.res_bytes, wb);
+  }
   // everything above reads only parameters; activations come from the
-  // previous kernel
-  ptx::griddep_wait();
+  // previous kernel (or, flag mode, from producers whose tiles are awaited
+  // one by one below)
+  if (!a.skip_gridwait) ptx::griddep_wait();
   ptx::griddep_launch();
   cta_stamp(P, 1);
 
@@ -247,6 +310,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       const __half* lo = a.in.lo();
       int st = 0;
       uint32_t ph = 0;
+      bool fin_all = false, fsk_all = false;
+      int dep_seq = 0;
       for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
         const int n_tile = tile / P.m_tiles, m_tile = tile - n_tile * P.m_tiles;
         const int64_t gs = (int64_t)m_tile * kTileM * P.mt - P.halo;  // grid position of buffer slot 0
@@ -254,6 +319,18 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
         const int64_t ge = gs + P.span;
         const int64_t ce = ge > P.gtotal ? P.gtotal : ge;
         const uint32_t slot0 = (uint32_t)(cs - gs) * 16, bytes = (uint32_t)(ce - cs) * 16;
+        if (a.fin.mode || a.fsk.mode) {
+          // the producer tiles of this tile's input range and residual rows;
+          // dep_seq hands the acquired state to the epilogue (CTA scope)
+          if (a.fin.mode) flag_wait(a.fin, cs, ce, fin_all);
+          if (a.fsk.mode) {
+            const int64_t r0 = (int64_t)m_tile * kTileM * P.mt;
+            flag_wait(a.fsk, r0, r0 + kTileM * P.mt, fsk_all);
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> bulk-copy reads
+          asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(ptx::smem_u32(&S->dep_seq)), "r"(++dep_seq)
+                       : "memory");
+        }
         if (P.psub) {
           // one parity plane and its taps' weights per stage
           for (int q = 0; q < P.nq; ++q)
@@ -296,7 +373,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
           const uint32_t bar = ptx::smem_u32(&S->full[st]);
           const uint32_t sb = base + st * P.stage_bytes;
           const int ng = q == P.nq - 1 ? P.last_groups : 2;
-          ptx::mbar_arrive_tx(bar, 2 * ng * P.nplanes * bytes + P.b_bytes);
+          ptx::mbar_arrive_tx(bar, 2 * ng * P.nplanes * bytes + (P.wres ? 0u : P.b_bytes));
           for (int pl = 0; pl < P.nplanes; ++pl) {
             const uint32_t ps = sb + pl * 4 * P.a_bytes;
             for (int g = 0; g < ng; ++g) {
@@ -305,7 +382,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
               ptx::bulk_g2s(ps + (2 + g) * P.a_bytes + slot0, lo + off, bytes, bar);
             }
           }
-          if (P.b_img_nt == P.nt) {
+          if (P.wres) {
+          } else if (P.b_img_nt == P.nt) {
             ptx::bulk_g2s(sb + P.nplanes * 4 * P.a_bytes, P.w + ((int64_t)n_tile * P.nq + q) * P.taps * 32 * P.nt,
                           P.b_bytes, bar);
           } else {
@@ -339,6 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
     const uint64_t bstep = (uint64_t)(64 * P.nt) >> 4, blo = (uint64_t)(P.nt * 16) >> 4;
     int st = 0;
     uint32_t ph = 0, acc = 0, acc_ph = 0;
+    if (P.wres) ptx::mbar_wait(ptx::smem_u32(&S->wfull), 0);
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
       ptx::mbar_wait(ptx::smem_u32(&S->acc_empty[acc]), acc_ph ^ 1);
       ptx::tc_fence_after();
@@ -354,7 +433,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
         const uint32_t sb = base + st * P.stage_bytes;
         const uint64_t a_hi = ptx::smem_desc_noswz(sb, a_lbo, 128);
         const uint64_t a_lo = ptx::smem_desc_noswz(sb + 2 * P.a_bytes, a_lbo, 128);
-        const uint64_t b0 = ptx::smem_desc_noswz(sb + P.nplanes * 4 * P.a_bytes, b_lbo, 128);
+        const uint64_t b0 = ptx::smem_desc_noswz(P.wres ? wres_base + (uint32_t)q * P.b_bytes : sb + P.nplanes * 4 * P.a_bytes,
+                                                 b_lbo, 128);
         // first writes: main partial at its first chunk's first sub-stage,
         // correction at the tile's first sub-stage
         const uint32_t main_acc = (q >= NP || ps > 0) ? 1u : 0u;
@@ -396,6 +476,24 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       }
       ptx::mma_commit_warp(ptx::smem_u32(&S->acc_full[acc]));
       if (++acc == (uint32_t)NB) { acc = 0; acc_ph ^= 1; }
+    }
+  } else if (warp == kWarpSignal) {
+    // ===== flag mode: after all draining warps stored a tile, bump its
+    // producer counters with GPU-scope release (cumulative over the stores
+    // the CTA-scope barrier ordered before it) =====
+    if (a.sig_done && lane == 0) {
+      uint32_t it = 0;
+      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
+        ptx::mbar_wait_sleep(ptx::smem_u32(&S->tstored[it & (kSigRing - 1)]), (it / kSigRing) & 1);
+        const int m_tile = tile - (tile / P.m_tiles) * P.m_tiles;
+        if (P.dbg & 8192) {  // timing diagnostic only: no release ordering
+          asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(a.sig_done + m_tile) : "memory");
+          asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(a.sig_done + P.m_tiles) : "memory");
+        } else {
+          asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.sig_done + m_tile) : "memory");
+          asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.sig_done + P.m_tiles) : "memory");
+        }
+      }
     }
   } else if (warp < 8) {
     // ===== epilogue: a tile's 16-column chunks (sub-tile, channel chunk)
@@ -464,7 +562,25 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       return true;
     };
     auto chan = [&](const Item& x) { return x.n_tile * P.nt + (x.k & (nch - 1)) * 16; };
+    int sk_checked = -1;  // flag mode: tile whose residual rows were acquired
     auto skip_async = [&](const Item& x, uint32_t dst) {
+      if (a.fsk.mode && x.tile != sk_checked) {
+        // the producer warp acquired this tile's residual rows (x.it + 1
+        // tiles so far): CTA-scope acquire of its hand-off
+        if (lane == 0) {
+          uint32_t spins = 0;
+          for (;;) {
+            int v;
+            asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(ptx::smem_u32(&S->dep_seq))
+                         : "memory");
+            if (v > (int)x.it) break;
+            __nanosleep(32);
+            if (++spins > (1u << 26)) __trap();
+          }
+        }
+        __syncwarp();
+        sk_checked = x.tile;
+      }
       if (P.skip_pos)
         load16_async_at(e.skip, (int64_t)(chan(x) >> 3) * e.skip.kstride + (int64_t)x.g * 8, x.valid, dst, skq);
       else
@@ -541,6 +657,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
         epi_chunk16(e, etab, v, wsc, sk, chan(cur), cur.valid, cur.valid ? cur.b : 0, cur.oy, cur.ox, lane,
                     P.out_pos ? (int64_t)cur.g * 8 : -1, P.fold_out ? 1.f : e.out.sstore);
         if (lane == 0 && warp == 0) tr(P, 2, 0xE00 | c0);
+        if (last_of_tile && a.sig_done) {
+          // this warp's rows of the tile are stored: __syncwarp orders the
+          // lanes' stores before lane 0's CTA-scope release; the signal warp
+          // publishes the tile at GPU scope (its fence stays off this path)
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->tstored[cur.it & (kSigRing - 1)]));
+        }
       } else if (last_of_tile) {
         ptx::tc_fence_before();
         __syncwarp();
@@ -860,7 +983,7 @@ size_t ss_aux_bytes(const SsParams& P) {
 
 // nt: output channels per tile (the weight image is packed in tiles of
 // min(npad, 128) rows; a smaller nt copies its rows out of that image)
-static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub) {
+static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub, bool allow_wres) {
   const TensorView& in = a.in;
   if (!a.f16 || !a.tcwss || !a.tc16_scale) return false;
   if ((a.stride != 1 && a.stride != 2) || a.kh != a.kw ||
@@ -963,6 +1086,25 @@ static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub)
   P.stages = (int)(budget / P.stage_bytes);
   if (P.stages > kMaxStages) P.stages = kMaxStages;
   if (P.stages < 2) return false;
+  // resident weights when one n-tile covers every output channel and the
+  // image leaves room for at least min(4, streamed stages) activation stages
+  P.wres = 0;
+  P.res_bytes = 0;
+  {
+    static const char* wenv = getenv("PCNN_SS_WRES");
+    const bool want = wenv ? atoi(wenv) != 0 : true;
+    const uint32_t res = (uint32_t)P.nq * P.b_bytes, sa = P.nplanes * 4 * P.a_bytes;
+    if (want && allow_wres && !P.psub && P.b_img_nt == P.nt && P.n_tiles == 1 && res < budget) {
+      int st = (int)((budget - res) / sa);
+      if (st > kMaxStages) st = kMaxStages;
+      if (st >= 2 && st >= (P.stages < 4 ? P.stages : 4)) {
+        P.wres = 1;
+        P.res_bytes = res;
+        P.stage_bytes = sa;
+        P.stages = st;
+      }
+    }
+  }
   const char* dbg = getenv("PCNN_TC_DEBUG");
   P.dbg = dbg ? atoi(dbg) : 0;
   P.time_slot = -1;
@@ -1002,14 +1144,14 @@ static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub)
 // all taps' weights) when two fit; else, for 3x3 stride 2, one parity plane
 // per stage (measured: faster than 64-channel tiles, slower than whole-chunk
 // stages when those fit); else two 64-channel tiles.  PCNN_SS_PSUB=0/1 forces.
-bool make_ss_params(const ConvArgs& a, SsParams& P) {
+bool make_ss_params(const ConvArgs& a, SsParams& P, bool allow_wres = true) {
   const int nt = a.npad <= 128 ? a.npad : 128;
   const char* env = getenv("PCNN_SS_PSUB");
   const int force = env ? atoi(env) : -1;
-  if (force == 1 && make_ss_params_nt(a, P, nt, true)) return true;
-  if (make_ss_params_nt(a, P, nt, false)) return true;
-  if (force != 0 && make_ss_params_nt(a, P, nt, true)) return true;
-  return nt == 128 && make_ss_params_nt(a, P, 64, false);
+  if (force == 1 && make_ss_params_nt(a, P, nt, true, allow_wres)) return true;
+  if (make_ss_params_nt(a, P, nt, false, allow_wres)) return true;
+  if (force != 0 && make_ss_params_nt(a, P, nt, true, allow_wres)) return true;
+  return nt == 128 && make_ss_params_nt(a, P, 64, false, allow_wres);
 }
 
 }  // namespace
@@ -1056,6 +1198,17 @@ bool conv_ss_shape_ok(const ConvArgs& a) {
   return make_ss_params(b, P);
 }
 
+bool conv_ss_flag_geometry(const ConvArgs& a, FlagDep& d) {
+  SsParams P;
+  if (!make_ss_params(a, P)) return false;
+  d.tm = kTileM * P.mt;
+  d.m_tiles = P.m_tiles;
+  d.gtotal = P.gtotal;
+  d.per_tile = P.n_tiles;  // one signal per (m-tile, n-tile)
+  d.all = P.m_tiles * P.n_tiles;
+  return true;
+}
+
 bool conv_ss_supported(const ConvArgs& a) {
   SsParams P;
   return make_ss_params(a, P);
@@ -1070,7 +1223,7 @@ void launch_conv_ss(const ConvArgs& a, cudaStream_t s) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
-  const size_t smem = 128 + (size_t)P.stages * P.stage_bytes + ss_aux_bytes(P);
+  const size_t smem = 128 + (size_t)P.stages * P.stage_bytes + P.res_bytes + ss_aux_bytes(P);
   const int tiles = P.m_tiles * P.n_tiles;
   const int grid = tiles < nsm ? tiles : nsm;
   void (*k)(SsParams) = P.taps == 16 ? conv_ss_kernel<16> : P.taps == 9 ? conv_ss_kernel<9> : conv_ss_kernel<1>;
@@ -1104,7 +1257,7 @@ SsChain* ss_chain_create(const ConvArgs* args, int n, const int* dep_in, const i
   int ptab_max = 0, tiles_max = 0, taps_max = 1;
   std::vector<int> needed(n, 0);
   for (int i = 0; i < n; ++i) {
-    if (!make_ss_params(args[i], L[i]) || L[i].b_img_nt != L[i].nt || L[i].psub) return nullptr;
+    if (!make_ss_params(args[i], L[i], false) || L[i].b_img_nt != L[i].nt || L[i].psub) return nullptr;
     if ((size_t)L[i].span * 16 > (1u << 17)) return nullptr;
     stage_max = stage_max > L[i].stage_bytes ? stage_max : L[i].stage_bytes;
     buf = buf > L[i].buf_cols ? buf : L[i].buf_cols;

@@ -8,6 +8,18 @@
 
 namespace pcnn {
 
+// Flag-synchronised halo-tile launches: a consumer waits for the per-tile
+// completion counters of the unit that wrote its input / residual instead of
+// griddepcontrol.wait on the whole previous grid.  mode 1: the producer tiles
+// covering a position range (same grid), 2: every tile.
+struct FlagDep {
+  const int* done = nullptr;  // producer counters [m_tiles] per tile, [m_tiles] all
+  int mode = 0;               // 0 none
+  int tm = 0, m_tiles = 0;    // producer tile rows, tiles
+  int64_t gtotal = 0;         // producer grid positions
+  int per_tile = 0, all = 0;  // counter values meaning "done"
+};
+
 struct ConvArgs {
   TensorView in;
   PixelMap pm;
@@ -26,6 +38,10 @@ struct ConvArgs {
   // in the prologue, instead of a memset node between the two launches
   float* prezero = nullptr;
   int64_t prezero_n = 0;  // floats, a multiple of 4
+  // flag-synchronised launches (api.cu build_flags; halo-tile kernel only)
+  int* sig_done = nullptr;  // this unit's counters [m_tiles + 1], bumped after its stores
+  int skip_gridwait = 0;    // every producer signals: no griddepcontrol.wait
+  FlagDep fin, fsk;         // waits before reading the input / the residual
 };
 
 struct LinearArgs {
@@ -102,5 +118,8 @@ void ss_chain_destroy(SsChain* c);
 // the shape/precision part of conv_ss_supported (input format not checked)
 bool conv_ss_shape_ok(const ConvArgs& a);
 void launch_conv_ss(const ConvArgs& a, cudaStream_t s);
+// tile geometry of a halo-tile launch for its consumers' FlagDep (false if
+// the unit does not run on the halo-tile kernel)
+bool conv_ss_flag_geometry(const ConvArgs& a, FlagDep& d);
 
 }  // namespace pcnn
