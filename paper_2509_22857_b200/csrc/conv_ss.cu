@@ -140,11 +140,12 @@ struct Tracer {
 };
 
 constexpr int kMaxAcc = 4;  // accumulator buffers in TMEM
+constexpr int kMaxWChunks = 8;  // resident weights: one barrier per 16-channel chunk
 
 struct Smem {
   uint64_t full[kMaxStages], empty[kMaxStages];
   uint64_t acc_full[kMaxAcc], acc_empty[kMaxAcc];
-  uint64_t wfull;  // resident weights landed
+  uint64_t wfull[kMaxWChunks];  // resident weights: chunk q landed
   uint64_t tstored[kSigRing];  // flag mode: a tile's rows are stored (one arrival per draining warp)
   uint32_t tmem_base;
   int dep_seq;     // flag mode: this CTA's tiles whose producer tiles were acquired
@@ -258,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       ptx::mbar_init(ptx::smem_u32(&S->acc_full[i]), 1);
       ptx::mbar_init(ptx::smem_u32(&S->acc_empty[i]), P.share_epi ? 8 : 4);  // one arrive per draining warp
     }
-    ptx::mbar_init(ptx::smem_u32(&S->wfull), 1);
+    for (int i = 0; i < kMaxWChunks; ++i) ptx::mbar_init(ptx::smem_u32(&S->wfull[i]), 1);
     for (int i = 0; i < kSigRing; ++i) ptx::mbar_init(ptx::smem_u32(&S->tstored[i]), P.share_epi ? 8 : 4);
     S->dep_seq = 0;
     ptx::fence_mbar_init();
@@ -290,10 +291,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
   const uint32_t tmem = S->tmem_base;
   // resident weights: parameters, not written by the previous kernel, so the
   // copy overlaps its tail
+  // copy overlaps its tail; one barrier per chunk, so the first tile's MMAs
+  // start after the first chunk
   if (P.wres && warp == kWarpProducer && lane == 0) {
-    const uint32_t wb = ptx::smem_u32(&S->wfull);
-    ptx::mbar_arrive_tx(wb, P.res_bytes);
-    ptx::bulk_g2s(wres_base, P.w, P.res_bytes, wb);
+    for (int q = 0; q < P.nq; ++q) {
+      const uint32_t wb = ptx::smem_u32(&S->wfull[q]);
+      ptx::mbar_arrive_tx(wb, P.b_bytes);
+      ptx::bulk_g2s(wres_base + (uint32_t)q * P.b_bytes, reinterpret_cast<const uint8_t*>(P.w) + (size_t)q * P.b_bytes,
+                    P.b_bytes, wb);
+    }
   }
   // everything above reads only parameters; activations come from the
   // previous kernel (or, flag mode, from producers whose tiles are awaited
@@ -417,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
     const uint64_t bstep = (uint64_t)(64 * P.nt) >> 4, blo = (uint64_t)(P.nt * 16) >> 4;
     int st = 0;
     uint32_t ph = 0, acc = 0, acc_ph = 0;
-    if (P.wres) ptx::mbar_wait(ptx::smem_u32(&S->wfull), 0);
+    bool w_ready = !P.wres;  // every resident chunk seen (after the first tile)
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
       ptx::mbar_wait(ptx::smem_u32(&S->acc_empty[acc]), acc_ph ^ 1);
       ptx::tc_fence_after();
@@ -429,6 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
         tr(P, 1, 0x400 | q);
         ptx::mbar_wait(ptx::smem_u32(&S->full[st]), ph);
         tr(P, 1, 0x500 | q);
+        if (!w_ready) ptx::mbar_wait(ptx::smem_u32(&S->wfull[q]), 0);
         ptx::tc_fence_after();
         const uint32_t sb = base + st * P.stage_bytes;
         const uint64_t a_hi = ptx::smem_desc_noswz(sb, a_lbo, 128);
@@ -474,6 +481,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
        }
         if (++p == NP) p = 0;
       }
+      w_ready = true;
       ptx::mma_commit_warp(ptx::smem_u32(&S->acc_full[acc]));
       if (++acc == (uint32_t)NB) { acc = 0; acc_ph ^= 1; }
     }
@@ -1094,7 +1102,8 @@ static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub,
     static const char* wenv = getenv("PCNN_SS_WRES");
     const bool want = wenv ? atoi(wenv) != 0 : true;
     const uint32_t res = (uint32_t)P.nq * P.b_bytes, sa = P.nplanes * 4 * P.a_bytes;
-    if (want && allow_wres && !P.psub && P.b_img_nt == P.nt && P.n_tiles == 1 && res < budget) {
+    if (want && allow_wres && !P.psub && P.b_img_nt == P.nt && P.n_tiles == 1 && P.nq <= kMaxWChunks &&
+        res < budget) {
       int st = (int)((budget - res) / sa);
       if (st > kMaxStages) st = kMaxStages;
       if (st >= 2 && st >= (P.stages < 4 ? P.stages : 4)) {
