@@ -70,6 +70,8 @@ struct pcnn_plan {
   bool flags_on = false;
   int* flags_dev = nullptr;
   size_t flags_n = 0;
+  // fused[u]: unit u (a 1x1 projection) runs inside unit u - 1's halo-tile launch
+  std::vector<char> fused;
 };
 
 namespace {
@@ -297,6 +299,7 @@ void enqueue_unit(pcnn_plan* p, int ui, const float* x, float* logits, cudaStrea
       const ConvArgs& a = p->conv_args[ui];
       const bool chained = p->impl[ui] == 5 && p->chain_of[ui] >= 0;
       if (chained && p->chain_first[p->chain_of[ui]] != ui) break;  // launched with its chain's first unit
+      if (p->fused[ui]) break;  // computed by the previous unit's launch
       if (u.pool == PCNN_POOL_GLOBAL && !p->prezeroed[ui])
         cudaMemsetAsync(a.epi.out.base, 0, sizeof(float) * (size_t)p->batch * a.epi.out.cpad(), s);
       if (chained) {
@@ -377,6 +380,29 @@ void enqueue_all(pcnn_plan* p, const float* x, float* logits, cudaStream_t s) {
   for (int i = 0; i < (int)p->units.size(); ++i) enqueue_unit(p, i, x, logits, s, true);
 }
 
+// A residual block's 1x1 projection (unit i + 1) reads the same input with
+// the same stride as the block's first 3x3 conv (unit i): on the halo-tile
+// kernel its A operand is the 3x3 conv's centre tap, so the 3x3 launch
+// computes it too (two more MMAs per chunk, its own epilogue items and
+// output) and the projection's launch -- mostly fill / drain latency at
+// these sizes -- disappears.  PCNN_NO_PROJ_FUSE=1 keeps separate launches.
+void fuse_projections(pcnn_plan* p) {
+  const int n = (int)p->units.size();
+  p->fused.assign(n, 0);
+  for (int i = 0; i + 1 < n; ++i) {
+    const pcnn_unit_desc &u = p->units[i], &v = p->units[i + 1];
+    if (u.kind != PCNN_UNIT_CONV || v.kind != PCNN_UNIT_CONV || p->impl[i] != 5 || p->impl[i + 1] != 5) continue;
+    if (p->chain_of[i] >= 0 || p->chain_of[i + 1] >= 0 || p->fused[i]) continue;
+    if (v.in != u.in || v.kh != 1 || v.stride != u.stride || u.kh != 3) continue;
+    if (p->prezeroed[i] || p->prezeroed[i + 1] || (i + 2 < n && p->prezeroed[i + 2])) continue;
+    if (p->conv_args[i].prezero || p->conv_args[i + 1].prezero) continue;
+    if (!conv_ss_proj_ok(p->conv_args[i], p->conv_args[i + 1])) continue;
+    p->conv_args[i].proj = &p->conv_args[i + 1];
+    p->fused[i + 1] = 1;
+    p->launches -= 1;
+  }
+}
+
 // Flag-synchronised launches.  A halo-tile conv whose input and residual are
 // both written by halo-tile convs skips griddepcontrol.wait: its producer
 // warp waits, tile by tile, for the producer tiles covering the input range
@@ -403,13 +429,13 @@ void build_flags(pcnn_plan* p) {
   const int n = (int)p->units.size();
   std::vector<int> producer(p->tensors.size(), -1);
   for (int i = 0; i < n; ++i)
-    if (p->units[i].out >= 0) producer[p->units[i].out] = i;
+    if (p->units[i].out >= 0) producer[p->units[i].out] = p->fused[i] ? i - 1 : i;
   std::vector<char> sig(n, 0), skip(n, 0);
   std::vector<FlagDep> geo(n);
   size_t total = 0;
   std::vector<size_t> off(n, 0);
   for (int i = 0; i < n; ++i) {
-    if (p->units[i].kind != PCNN_UNIT_CONV || p->impl[i] != 5 || p->chain_of[i] >= 0) continue;
+    if (p->units[i].kind != PCNN_UNIT_CONV || p->impl[i] != 5 || p->chain_of[i] >= 0 || p->fused[i]) continue;
     if (!conv_ss_flag_geometry(p->conv_args[i], geo[i])) continue;
     sig[i] = 1;
     off[i] = total;
@@ -427,7 +453,7 @@ void build_flags(pcnn_plan* p) {
   // every griddepcontrol.wait unit reading a signalling conv's output must
   // read it from its immediate predecessor
   for (int i = 0; i < n; ++i) {
-    if (skip[i]) continue;
+    if (skip[i] || p->fused[i]) continue;
     const pcnn_unit_desc& u = p->units[i];
     for (int64_t t : {(int64_t)u.in, (int64_t)u.in2}) {
       if (t < 0 || t >= (int64_t)producer.size()) continue;
@@ -568,6 +594,7 @@ int pcnn_plan_create(const pcnn_unit_desc* units, int n_units, const pcnn_tensor
     prev.prezero_n = (int64_t)p->batch * p->conv_args[i].epi.out.cpad();
     p->prezeroed[i] = 1;
   }
+  fuse_projections(p);
   build_flags(p);
   for (int len : p->chain_len) p->launches -= len - 1;  // one kernel per chain
   if (cudaStreamCreateWithFlags(&p->capture_stream, cudaStreamNonBlocking) != cudaSuccess) {
@@ -591,6 +618,9 @@ int pcnn_plan_destroy(pcnn_plan* p) {
 }
 
 int pcnn_plan_num_launches(const pcnn_plan* p) { return p ? p->launches : -1; }
+
+// debugging aid (not part of pcnn.h): 1 if the plan runs flag-synchronised launches
+int pcnn_plan_flags(const pcnn_plan* p) { return p && p->flags_on ? 1 : 0; }
 
 int pcnn_plan_unit_impl(const pcnn_plan* p, int unit) {
   if (!p || unit < 0 || unit >= (int)p->units.size()) return -1;

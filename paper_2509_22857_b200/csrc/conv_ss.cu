@@ -37,10 +37,9 @@ namespace pcnn {
 
 namespace {
 
-constexpr int kThreads = 352;
+constexpr int kThreads = 320;
 constexpr int kWarpProducer = 8, kWarpMma = 9;
-constexpr int kWarpSignal = 10;  // flag mode: publishes finished tiles (idle otherwise)
-constexpr int kSigRing = 8;      // tile-stored barriers: 2 x the accumulator buffers
+constexpr int kSigRing = 8;  // flag mode: tile-stored counters, 2 x the accumulator buffers
 constexpr int kTileM = 128;
 constexpr int kMaxStages = 8;
 constexpr int kMaxPartials = 4;
@@ -94,6 +93,17 @@ struct SsParams {
   // griddepcontrol.wait; the ring stages then hold activations only
   int wres;
   uint32_t res_bytes;       // resident weight bytes (nq * b_bytes), 0 without wres
+  // fused projection (ConvArgs::proj): per chunk two more MMAs on the centre
+  // tap's A into 2 nt more TMEM columns, weights appended to the stage's B
+  // region, and nt / 16 more epilogue items per sub-tile with its own
+  // parameter table, weight scale and output
+  int proj;
+  EpiParams pe;
+  EpiTab petab;
+  const __half* pw;         // projection weight image (taps = 1)
+  const float* pwscale;
+  uint32_t pb_bytes;        // 64 * nt per chunk
+  int ptoff;                // centre tap offset (toff of the projection's input position)
 };
 
 // launch-wide configuration of a chain
@@ -146,7 +156,7 @@ struct Smem {
   uint64_t full[kMaxStages], empty[kMaxStages];
   uint64_t acc_full[kMaxAcc], acc_empty[kMaxAcc];
   uint64_t wfull[kMaxWChunks];  // resident weights: chunk q landed
-  uint64_t tstored[kSigRing];  // flag mode: a tile's rows are stored (one arrival per draining warp)
+  uint32_t tstored[kSigRing];  // flag mode: draining warps done with a tile (monotonic per slot)
   uint32_t tmem_base;
   int dep_seq;     // flag mode: this CTA's tiles whose producer tiles were acquired
 };
@@ -246,7 +256,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total_tiles = P.m_tiles * P.n_tiles;
   const int NP = P.partials, NB = P.acc_bufs;
-  const uint32_t set_cols = P.concat ? (uint32_t)NP * 2 * P.nt : (uint32_t)(NP + 1) * P.nt;
+  const uint32_t set_a = P.concat ? (uint32_t)NP * 2 * P.nt : (uint32_t)(NP + 1) * P.nt;
+  constexpr bool kProj = TAPS == 9;  // projection fusion: 3x3 convs only (keeps the stem's registers)
+  const bool proj = kProj && P.proj;
+  const uint32_t set_cols = set_a + (proj ? 2u * P.nt : 0u);  // + projection [main | corr]
   Tracer tr;
   cta_stamp(P, 0);
 
@@ -260,13 +273,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       ptx::mbar_init(ptx::smem_u32(&S->acc_empty[i]), P.share_epi ? 8 : 4);  // one arrive per draining warp
     }
     for (int i = 0; i < kMaxWChunks; ++i) ptx::mbar_init(ptx::smem_u32(&S->wfull[i]), 1);
-    for (int i = 0; i < kSigRing; ++i) ptx::mbar_init(ptx::smem_u32(&S->tstored[i]), P.share_epi ? 8 : 4);
+    for (int i = 0; i < kSigRing; ++i) S->tstored[i] = 0;
     S->dep_seq = 0;
     ptx::fence_mbar_init();
   }
   if (warp == kWarpProducer) ptx::tmem_alloc(ptx::smem_u32(&S->tmem_base), P.tmem_cols);
   epi_fill_tab(a.epi, P.etab, ptab, threadIdx.x, kThreads, P.fold_skip ? a.epi.skip.sload : 1.f,
                P.fold_out ? a.epi.out.sstore : 1.f);
+  float* ptab_p = ptab + P.etab.rows * a.epi.npad;  // projection table (P.proj)
+  if (proj) epi_fill_tab(P.pe, P.petab, ptab_p, threadIdx.x, kThreads);
   if (P.last_groups == 1) {
     // cpad 4 / 8: the second 8-channel group of every stage stays zero
     for (int st = 0; st < P.stages; ++st)
@@ -379,7 +394,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
           const uint32_t bar = ptx::smem_u32(&S->full[st]);
           const uint32_t sb = base + st * P.stage_bytes;
           const int ng = q == P.nq - 1 ? P.last_groups : 2;
-          ptx::mbar_arrive_tx(bar, 2 * ng * P.nplanes * bytes + (P.wres ? 0u : P.b_bytes));
+          ptx::mbar_arrive_tx(bar, 2 * ng * P.nplanes * bytes + (P.wres ? 0u : P.b_bytes) + P.pb_bytes);
+          if (P.proj)
+            ptx::bulk_g2s(sb + P.nplanes * 4 * P.a_bytes + P.b_bytes, P.pw + ((int64_t)n_tile * P.nq + q) * 32 * P.nt,
+                          P.pb_bytes, bar);
           for (int pl = 0; pl < P.nplanes; ++pl) {
             const uint32_t ps = sb + pl * 4 * P.a_bytes;
             for (int g = 0; g < ng; ++g) {
@@ -473,6 +491,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
             }
             ss_stage<TAPS>(P.concat, dm, dc, a_hi + shift, a_lo + shift, b0, bstep, blo, idesc2, idesc, main_acc,
                            corr_acc, offs);
+            if (proj) {
+              // projection: the centre tap's A, its weights after the taps'
+              const uint64_t po[1] = {(uint64_t)P.ptoff};
+              const uint32_t pm = d_set + set_a;
+              const uint64_t bp = b0 + ((uint64_t)P.b_bytes >> 4);
+              ss_stage<1>(P.concat, pm, pm + P.nt, a_hi + shift, a_lo + shift, bp, bstep, blo, idesc2, idesc,
+                          q > 0 ? 1u : 0u, q > 0 ? 1u : 0u, po);
+            }
           }
         }
         ptx::mma_commit_warp(ptx::smem_u32(&S->empty[st]));
@@ -484,24 +510,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       w_ready = true;
       ptx::mma_commit_warp(ptx::smem_u32(&S->acc_full[acc]));
       if (++acc == (uint32_t)NB) { acc = 0; acc_ph ^= 1; }
-    }
-  } else if (warp == kWarpSignal) {
-    // ===== flag mode: after all draining warps stored a tile, bump its
-    // producer counters with GPU-scope release (cumulative over the stores
-    // the CTA-scope barrier ordered before it) =====
-    if (a.sig_done && lane == 0) {
-      uint32_t it = 0;
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
-        ptx::mbar_wait_sleep(ptx::smem_u32(&S->tstored[it & (kSigRing - 1)]), (it / kSigRing) & 1);
-        const int m_tile = tile - (tile / P.m_tiles) * P.m_tiles;
-        if (P.dbg & 8192) {  // timing diagnostic only: no release ordering
-          asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(a.sig_done + m_tile) : "memory");
-          asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(a.sig_done + P.m_tiles) : "memory");
-        } else {
-          asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.sig_done + m_tile) : "memory");
-          asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.sig_done + P.m_tiles) : "memory");
-        }
-      }
     }
   } else if (warp < 8) {
     // ===== epilogue: a tile's 16-column chunks (sub-tile, channel chunk)
@@ -518,7 +526,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
     EpiTab etab = P.etab;
     etab.ptab = ptab;
     const int hw = P.hp * P.wp;
-    const int nch = P.nt >> 4, lg_nch = __ffs(nch) - 1, nk = P.mt * nch;  // nt / 16 is a power of two
+    // items per sub-tile: nt / 16 chunks (a power of two), twice that with
+    // a fused projection (chunk j >= nch: the projection's channel j - nch)
+    const int nch = P.nt >> 4, nchx = proj ? 2 * nch : nch, lg_nch = __ffs(nchx) - 1, nk = P.mt * nchx;
     const int k0 = P.share_epi ? ew : 0, kstep = P.share_epi ? 2 : 1;
     const int lg_nb = __ffs(NB) - 1;
     // residual rows are staged in shared memory by cp.async one item ahead
@@ -570,6 +580,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       return true;
     };
     auto chan = [&](const Item& x) { return x.n_tile * P.nt + (x.k & (nch - 1)) * 16; };
+    const float pwsc = proj ? __ldg(P.pwscale) * a.in.sload : 0.f;
+    EpiTab petab = P.petab;
+    petab.ptab = ptab_p;
     int sk_checked = -1;  // flag mode: tile whose residual rows were acquired
     auto skip_async = [&](const Item& x, uint32_t dst) {
       if (a.fsk.mode && x.tile != sk_checked) {
@@ -620,24 +633,26 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
         ptx::tc_fence_after();
       }
       const int sub = cur.k >> lg_nch, c0 = (cur.k & (nch - 1)) * 16;
-      const uint32_t d_set = tmem + lane_off + (acc * P.mt + sub) * set_cols;
+      const bool pj = proj && (cur.k & nch);  // a projection item
+      const uint32_t d_set = tmem + lane_off + (acc * P.mt + sub) * set_cols + (pj ? set_a : 0u);
       if (!(P.dbg & 4)) {
         float v[16], t[16];
+        const int npi = pj ? 1 : NP;  // the projection has one main partial and its correction
         if (P.concat) {
           ptx::tmem_ld16x2(d_set + P.nt + c0, d_set + c0, v, t);
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] += t[i];
-          for (int p = 1; p < NP; ++p) {
+          for (int p = 1; p < npi; ++p) {
             float u[16];
             ptx::tmem_ld16x2(d_set + 2 * p * P.nt + P.nt + c0, d_set + 2 * p * P.nt + c0, u, t);
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[i] += u[i] + t[i];
           }
         } else {
-          ptx::tmem_ld16x2(d_set + NP * P.nt + c0, d_set + c0, v, t);
+          ptx::tmem_ld16x2(d_set + npi * P.nt + c0, d_set + c0, v, t);
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] += t[i];
-          for (int p = 1; p < NP; ++p) {
+          for (int p = 1; p < npi; ++p) {
             ptx::tmem_ld16(d_set + p * P.nt + c0, t);
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[i] += t[i];
@@ -662,15 +677,30 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
 #pragma unroll
           for (int i = 0; i < 16; ++i) sk[i] = 0.f;
         }
-        epi_chunk16(e, etab, v, wsc, sk, chan(cur), cur.valid, cur.valid ? cur.b : 0, cur.oy, cur.ox, lane,
-                    P.out_pos ? (int64_t)cur.g * 8 : -1, P.fold_out ? 1.f : e.out.sstore);
+        if (kProj && pj)
+          epi_chunk16(P.pe, petab, v, pwsc, sk, chan(cur), cur.valid, cur.valid ? cur.b : 0, cur.oy, cur.ox, lane, -1,
+                      P.pe.out.sstore);
+        else
+          epi_chunk16(e, etab, v, wsc, sk, chan(cur), cur.valid, cur.valid ? cur.b : 0, cur.oy, cur.ox, lane,
+                      P.out_pos ? (int64_t)cur.g * 8 : -1, P.fold_out ? 1.f : e.out.sstore);
         if (lane == 0 && warp == 0) tr(P, 2, 0xE00 | c0);
         if (last_of_tile && a.sig_done) {
           // this warp's rows of the tile are stored: __syncwarp orders the
-          // lanes' stores before lane 0's CTA-scope release; the signal warp
-          // publishes the tile at GPU scope (its fence stays off this path)
+          // lanes' stores before lane 0's CTA-scope acq_rel count; the last
+          // draining warp of the tile publishes it with a GPU-scope release
+          // (cumulative over the stores the counter ordered before it)
           __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->tstored[cur.it & (kSigRing - 1)]));
+          if (lane == 0) {
+            const uint32_t nsig = P.share_epi ? 8u : 4u;
+            uint32_t old;
+            asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                         : "=r"(old) : "r"(ptx::smem_u32(&S->tstored[cur.it & (kSigRing - 1)])) : "memory");
+            if (old % nsig == nsig - 1) {
+              const int m_tile = cur.tile - cur.n_tile * P.m_tiles;
+              asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.sig_done + m_tile) : "memory");
+              asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.sig_done + P.m_tiles) : "memory");
+            }
+          }
         }
       } else if (last_of_tile) {
         ptx::tc_fence_before();
@@ -986,7 +1016,7 @@ constexpr uint32_t kSkipStage = 2 * 4 * 256 * 16;
 
 size_t ss_aux_bytes(const SsParams& P) {
   return ((sizeof(Smem) + 15) & ~size_t(15)) + (size_t)P.etab.rows * P.a.epi.npad * 4 +
-         (P.a.epi.residual ? kSkipStage : 0);
+         (P.proj ? (size_t)P.petab.rows * P.pe.npad * 4 : 0) + (P.a.epi.residual ? kSkipStage : 0);
 }
 
 // nt: output channels per tile (the weight image is packed in tiles of
@@ -1089,7 +1119,25 @@ static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub,
   P.fold_out = P.out_pos && (a.epi.poly_deg > 0 || a.epi.residual >= 2);
   P.a_bytes = (uint32_t)P.span * 16;
   P.b_bytes = (uint32_t)(P.psub ? 4 : P.taps) * 64 * P.nt;  // psub: at most 4 taps per plane
-  P.stage_bytes = P.nplanes * 4 * P.a_bytes + P.b_bytes;
+  P.proj = 0;
+  P.pb_bytes = 0;
+  if (a.proj) {
+    // the projection reads the 3x3 conv's centre tap: same input tensor,
+    // stride, output channels and tiles; no residual / pool on either side
+    const ConvArgs& q = *a.proj;
+    if (P.psub || P.b_img_nt != P.nt || a.kh != 3 || a.pad != 1 || q.kh != 1 || q.kw != 1 || q.pad != 0 ||
+        q.stride != a.stride || q.npad != a.npad || q.in.base != a.in.base || !q.f16 || !q.tcwss || !q.tc16_scale ||
+        a.epi.residual || q.epi.residual || q.epi.pool != PCNN_POOL_NONE || a.epi.pool != PCNN_POOL_NONE)
+      return false;
+    P.proj = 1;
+    P.pe = q.epi;
+    P.petab = epi_tab_layout(q.epi);
+    P.pw = reinterpret_cast<const __half*>(q.tcwss);
+    P.pwscale = q.tc16_scale + 1;
+    P.pb_bytes = 64u * P.nt;
+    P.ptoff = P.toff[4];
+  }
+  P.stage_bytes = P.nplanes * 4 * P.a_bytes + P.b_bytes + P.pb_bytes;
   const size_t budget = 225 * 1024 - 128 - ss_aux_bytes(P);
   P.stages = (int)(budget / P.stage_bytes);
   if (P.stages > kMaxStages) P.stages = kMaxStages;
@@ -1102,7 +1150,7 @@ static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub,
     static const char* wenv = getenv("PCNN_SS_WRES");
     const bool want = wenv ? atoi(wenv) != 0 : true;
     const uint32_t res = (uint32_t)P.nq * P.b_bytes, sa = P.nplanes * 4 * P.a_bytes;
-    if (want && allow_wres && !P.psub && P.b_img_nt == P.nt && P.n_tiles == 1 && P.nq <= kMaxWChunks &&
+    if (want && allow_wres && !P.psub && !P.proj && P.b_img_nt == P.nt && P.n_tiles == 1 && P.nq <= kMaxWChunks &&
         res < budget) {
       int st = (int)((budget - res) / sa);
       if (st > kMaxStages) st = kMaxStages;
@@ -1125,19 +1173,20 @@ static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub,
   P.concat = P.nt <= 64;
   P.partials = 0;
   for (int wp = want; wp >= 1 && !P.partials; --wp) {
-    const int set = P.concat ? wp * 2 * P.nt : (wp + 1) * P.nt;
+    const int set = (P.concat ? wp * 2 * P.nt : (wp + 1) * P.nt) + (P.proj ? 2 * P.nt : 0);
     // up to four buffers: the MMA warp runs ahead of two epilogue warpgroups
     for (int nb = kMaxAcc; nb >= 1 && !P.partials; --nb)
       if (nb * P.mt * set <= 512 && nb != 3) { P.partials = wp; P.acc_bufs = nb; }
   }
   if (!P.partials) return false;
-  const uint32_t set = P.concat ? P.partials * 2 * P.nt : (P.partials + 1) * P.nt;
+  const uint32_t set =
+      (P.concat ? P.partials * 2 * P.nt : (P.partials + 1) * P.nt) + (P.proj ? 2u * P.nt : 0u);
   const uint32_t need = P.acc_bufs * P.mt * set;
   P.tmem_cols = need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
   P.buf_cols = P.mt * set;
   // shared epilogue when a tile has an even number of 16-column chunks
   const char* sh = getenv("PCNN_SS_SHARE");
-  P.share_epi = sh ? atoi(sh) : ((P.mt * P.nt / 16) % 2 == 0);
+  P.share_epi = sh ? atoi(sh) : ((P.mt * (P.proj ? 2 : 1) * P.nt / 16) % 2 == 0);
   P.dep_in = P.dep_sk = -1;
   P.dep_in_mode = P.dep_sk_mode = 0;
   P.done = nullptr;
@@ -1216,6 +1265,14 @@ bool conv_ss_flag_geometry(const ConvArgs& a, FlagDep& d) {
   d.per_tile = P.n_tiles;  // one signal per (m-tile, n-tile)
   d.all = P.m_tiles * P.n_tiles;
   return true;
+}
+
+bool conv_ss_proj_ok(const ConvArgs& a, const ConvArgs& proj) {
+  if (getenv("PCNN_NO_PROJ_FUSE")) return false;
+  ConvArgs b = a;
+  b.proj = &proj;
+  SsParams P;
+  return make_ss_params(b, P) && P.proj;
 }
 
 bool conv_ss_supported(const ConvArgs& a) {

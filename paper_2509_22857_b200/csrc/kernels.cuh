@@ -42,6 +42,10 @@ struct ConvArgs {
   int* sig_done = nullptr;  // this unit's counters [m_tiles + 1], bumped after its stores
   int skip_gridwait = 0;    // every producer signals: no griddepcontrol.wait
   FlagDep fin, fsk;         // waits before reading the input / the residual
+  // halo-tile kernel: a 1x1 conv with the same input and stride (a residual
+  // block's projection) computed in the same launch from the centre tap's
+  // A operand, into its own output (api.cu fuse_projections); or null
+  const ConvArgs* proj = nullptr;
 };
 
 struct LinearArgs {
@@ -121,5 +125,7 @@ void launch_conv_ss(const ConvArgs& a, cudaStream_t s);
 // tile geometry of a halo-tile launch for its consumers' FlagDep (false if
 // the unit does not run on the halo-tile kernel)
 bool conv_ss_flag_geometry(const ConvArgs& a, FlagDep& d);
+// can `proj` (1x1, same input and stride) run inside `a`'s halo-tile launch?
+bool conv_ss_proj_ok(const ConvArgs& a, const ConvArgs& proj);
 
 }  // namespace pcnn

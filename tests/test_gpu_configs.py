@@ -63,3 +63,27 @@ def test_config_redistributed_forward(cuda, name):
     # the redistributed model is the original function
     orig = O.eval_batch(g, x[:n])
     assert rel_err(want, orig) <= 1e-8, name
+
+
+@pytest.mark.parametrize("name", ["resnet20", "resnet18", "resnet20_deg8"])
+def test_flag_synchronised_launches_match(cuda, name, monkeypatch):
+    """PCNN_FLAGS=1 (per-tile completion counters instead of whole-grid
+    griddepcontrol ordering, api.cu build_flags) computes the same logits:
+    every tile does the same arithmetic, only the global-pool atomics may
+    add in another order."""
+    import ctypes
+    import torch
+    from paper_2509_22857_b200 import _lib as L
+    cfg = configs.CONFIGS[name]
+    g, _, _ = T.redistribute_sweep(configs.build(name), cfg.redistribution[0],
+                                   allow_negative_leading=cfg.allow_negative_leading)
+    x = torch.from_numpy(configs.make_input(cfg).astype(np.float32)).cuda()
+    base = Engine(g).forward(x).double().cpu().numpy()
+    monkeypatch.setenv("PCNN_FLAGS", "1")
+    eng = Engine(g)
+    fn = L.lib().pcnn_plan_flags
+    fn.argtypes = [ctypes.c_void_p]
+    assert fn(eng.plan(cfg.batch).handle) == 1, name
+    for _ in range(3):  # graph replays reuse the zeroed counters
+        got = eng.forward(x).double().cpu().numpy()
+        assert rel_err(got, base) <= 1e-6, name
