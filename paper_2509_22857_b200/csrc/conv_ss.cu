@@ -1021,7 +1021,8 @@ size_t ss_aux_bytes(const SsParams& P) {
 
 // nt: output channels per tile (the weight image is packed in tiles of
 // min(npad, 128) rows; a smaller nt copies its rows out of that image)
-static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub, bool allow_wres) {
+static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub, bool allow_wres, int force_mt = 0,
+                              int max_np = 0) {
   const TensorView& in = a.in;
   if (!a.f16 || !a.tcwss || !a.tc16_scale) return false;
   if ((a.stride != 1 && a.stride != 2) || a.kh != a.kw ||
@@ -1048,6 +1049,7 @@ static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub,
   const char* mt16_env = getenv("PCNN_SS_MT16");  // experiment: sub-tiles for NT = 16 layers only
   P.mt = mt_env ? atoi(mt_env) : (P.nt <= 32 ? 2 : 1);
   if (mt16_env && P.nt == 16) P.mt = atoi(mt16_env);
+  if (force_mt) P.mt = force_mt;
   if (P.mt < 1 || P.mt > 4) P.mt = 1;
   const int tm = kTileM * P.mt;
   P.m_tiles = (int)((P.gtotal + tm - 1) / tm);
@@ -1170,6 +1172,7 @@ static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub,
   const int stages_per_partial = kAddsPerPartial / P.taps > 0 ? kAddsPerPartial / P.taps : 1;
   int want = (P.nq + stages_per_partial - 1) / stages_per_partial;
   want = want < 1 ? 1 : (want > kMaxPartials ? kMaxPartials : want);
+  if (max_np && want > max_np) want = max_np;
   P.concat = P.nt <= 64;
   P.partials = 0;
   for (int wp = want; wp >= 1 && !P.partials; --wp) {
