@@ -245,6 +245,17 @@ int pcnn_forward(pcnn_plan* plan, const float* x, float* logits, void* stream, i
 /* same with host buffers (pinned for overlap): H2D, forward, D2H inside  */
 int pcnn_forward_host(pcnn_plan* plan, const float* x_host, float* logits_host,
                       float* x_dev_staging, float* logits_dev_staging, void* stream);
+/* n host batches in a copy/compute pipeline: batch i+1's H2D (on an
+ * internal copy stream, into the other of the two x_dev_staging buffers)
+ * overlaps batch i's forward on `stream`; each batch's logits and status
+ * word come back with a D2H on `stream`.  Every batch is still copied in
+ * and out; only the copies overlap the network.  statuses (host, n ints,
+ * may be null) receives each batch's status once `stream` is synchronised.
+ * Replaces a loop over check_equivalence / reference_eval batches
+ * (reference transforms.py:768-769, graph.py:413). */
+int pcnn_forward_host_many(pcnn_plan* plan, const float* const* x_hosts, float* const* logits_hosts, int n,
+                           float* x_dev_staging0, float* x_dev_staging1, float* logits_dev_staging,
+                           int* statuses, void* stream);
 /* launch unit i alone (per-kernel timing / debugging) */
 int pcnn_forward_unit(pcnn_plan* plan, int unit, const float* x, float* logits, void* stream);
 

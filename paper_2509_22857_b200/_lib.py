@@ -106,6 +106,8 @@ SYMBOLS = {
                      ctypes.c_int),
     "pcnn_forward_host": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                            ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "pcnn_forward_host_many": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
+                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "pcnn_forward_unit": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p],
                           ctypes.c_int),
     "pcnn_pack": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(PackDesc), ctypes.c_int, ctypes.c_void_p],

@@ -72,6 +72,14 @@ struct pcnn_plan {
   size_t flags_n = 0;
   // fused[u]: unit u (a 1x1 projection) runs inside unit u - 1's halo-tile launch
   std::vector<char> fused;
+  // pcnn_forward_host_many: copy stream, per-buffer events, pinned statuses
+  cudaStream_t copy_stream = nullptr, out_stream = nullptr;
+  cudaEvent_t h2d_done[2] = {nullptr, nullptr}, x_free[2] = {nullptr, nullptr};
+  cudaEvent_t fwd_done[2] = {nullptr, nullptr}, out_free[2] = {nullptr, nullptr};
+  float* logits2 = nullptr;    // second logits staging buffer (plan-owned)
+  int* status_slots = nullptr; // device: one status word per batch
+  int* status_pinned = nullptr;
+  int status_pinned_n = 0;
 };
 
 namespace {
@@ -612,6 +620,14 @@ int pcnn_plan_destroy(pcnn_plan* p) {
   for (SsChain* c : p->chains) ss_chain_destroy(c);
   if (p->status_dev) cudaFree(p->status_dev);
   if (p->flags_dev) cudaFree(p->flags_dev);
+  if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
+  if (p->out_stream) cudaStreamDestroy(p->out_stream);
+  for (int i = 0; i < 2; ++i)
+    for (cudaEvent_t e : {p->h2d_done[i], p->x_free[i], p->fwd_done[i], p->out_free[i]})
+      if (e) cudaEventDestroy(e);
+  if (p->logits2) cudaFree(p->logits2);
+  if (p->status_slots) cudaFree(p->status_slots);
+  if (p->status_pinned) cudaFreeHost(p->status_pinned);
   if (p->status_host) cudaFreeHost(p->status_host);
   delete p;
   return PCNN_OK;
@@ -695,6 +711,75 @@ int pcnn_forward_host(pcnn_plan* p, const float* x_host, float* logits_host, flo
   if (rc != PCNN_OK) return rc;
   PCNN_CUDA(cudaMemcpyAsync(logits_host, logits_dev, out_bytes, cudaMemcpyDeviceToHost, s));
   if (p->any_split) PCNN_CUDA(cudaMemcpyAsync(p->status_host, p->status_dev, sizeof(int), cudaMemcpyDeviceToHost, s));
+  return PCNN_OK;
+}
+
+int pcnn_forward_host_many(pcnn_plan* p, const float* const* x_hosts, float* const* logits_hosts, int n,
+                           float* x_dev0, float* x_dev1, float* logits_dev, int* statuses, void* stream) {
+  if (!p || (n > 0 && (!x_hosts || !logits_hosts)) || !x_dev0 || !x_dev1 || !logits_dev || n < 0)
+    return fail(PCNN_ERR_INVALID, "pcnn_forward_host_many: null argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const pcnn_tensor_desc& ti = p->tensors[p->input];
+  const size_t in_bytes = sizeof(float) * (size_t)p->batch * ti.c * ti.h * ti.w;
+  const pcnn_tensor_desc& to = p->tensors[p->output];
+  const size_t out_bytes = sizeof(float) * (size_t)p->batch * to.c * to.h * to.w;
+  if (!p->copy_stream) {
+    PCNN_CUDA(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
+    PCNN_CUDA(cudaStreamCreateWithFlags(&p->out_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i)
+      for (cudaEvent_t* e : {&p->h2d_done[i], &p->x_free[i], &p->fwd_done[i], &p->out_free[i]})
+        PCNN_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    PCNN_CUDA(cudaMalloc(&p->logits2, out_bytes));
+  }
+  if (p->status_pinned_n < n) {
+    if (p->status_pinned) cudaFreeHost(p->status_pinned);
+    if (p->status_slots) cudaFree(p->status_slots);
+    p->status_pinned = nullptr;
+    p->status_slots = nullptr;
+    p->status_pinned_n = 0;
+    PCNN_CUDA(cudaMallocHost(&p->status_pinned, sizeof(int) * (size_t)n));
+    PCNN_CUDA(cudaMalloc(&p->status_slots, sizeof(int) * (size_t)n));
+    p->status_pinned_n = n;
+  }
+  float* xd[2] = {x_dev0, x_dev1};
+  float* ld[2] = {logits_dev, p->logits2};
+  // Three streams: H2D (copy_stream) -> forward (stream) -> D2H (out_stream).
+  // Buffers alternate; x_free / out_free say when a buffer may be reused.
+  // Both side streams start after everything already queued on `stream`.
+  for (int b = 0; b < 2; ++b) {
+    PCNN_CUDA(cudaEventRecord(p->x_free[b], s));
+    PCNN_CUDA(cudaEventRecord(p->out_free[b], s));
+  }
+  PCNN_CUDA(cudaStreamWaitEvent(p->out_stream, p->out_free[0], 0));
+  for (int i = 0; i < n; ++i) {
+    const int b = i & 1;
+    PCNN_CUDA(cudaStreamWaitEvent(p->copy_stream, p->x_free[b], 0));
+    PCNN_CUDA(cudaMemcpyAsync(xd[b], x_hosts[i], in_bytes, cudaMemcpyHostToDevice, p->copy_stream));
+    PCNN_CUDA(cudaEventRecord(p->h2d_done[b], p->copy_stream));
+    PCNN_CUDA(cudaStreamWaitEvent(s, p->h2d_done[b], 0));
+    PCNN_CUDA(cudaStreamWaitEvent(s, p->out_free[b], 0));  // batch i - 2's logits are on the host
+    const int rc = pcnn_forward(p, xd[b], ld[b], stream, 1);
+    if (rc != PCNN_OK) return rc;
+    if (p->any_split)
+      PCNN_CUDA(cudaMemcpyAsync(p->status_slots + i, p->status_dev, sizeof(int), cudaMemcpyDeviceToDevice, s));
+    PCNN_CUDA(cudaEventRecord(p->x_free[b], s));
+    PCNN_CUDA(cudaEventRecord(p->fwd_done[b], s));
+    PCNN_CUDA(cudaStreamWaitEvent(p->out_stream, p->fwd_done[b], 0));
+    PCNN_CUDA(cudaMemcpyAsync(logits_hosts[i], ld[b], out_bytes, cudaMemcpyDeviceToHost, p->out_stream));
+    PCNN_CUDA(cudaEventRecord(p->out_free[b], p->out_stream));
+  }
+  if (p->any_split && n)
+    PCNN_CUDA(cudaMemcpyAsync(p->status_pinned, p->status_slots, sizeof(int) * (size_t)n, cudaMemcpyDeviceToHost,
+                              p->out_stream));
+  else
+    for (int i = 0; i < n; ++i) p->status_pinned[i] = 0;
+  // `stream` completes after the last D2H (callers time and synchronise it)
+  PCNN_CUDA(cudaEventRecord(p->out_free[0], p->out_stream));
+  PCNN_CUDA(cudaStreamWaitEvent(s, p->out_free[0], 0));
+  if (statuses) {
+    PCNN_CUDA(cudaStreamSynchronize(s));
+    for (int i = 0; i < n; ++i) statuses[i] = p->status_pinned[i];
+  }
   return PCNN_OK;
 }
 

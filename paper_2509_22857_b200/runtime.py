@@ -247,6 +247,43 @@ class Engine:
             self.recalibrate(f)
         return out_host
 
+    def forward_host_many(self, xs_host, outs_host=None, staging=None, stream=None, sync: bool = True):
+        """Many host batches of one size through a copy/compute pipeline
+        (pcnn_forward_host_many): batch i+1's H2D overlaps batch i's forward;
+        every batch is copied in and its logits copied out.  xs_host: pinned
+        float32 host tensors (or numpy arrays, pinned here).  Batches whose
+        split activations left the fp16 range are recomputed in float32.
+        staging: optional (x_dev0, x_dev1, out_dev) device buffers."""
+        torch = _torch()
+        xs = [x if torch.is_tensor(x) else torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).pin_memory()
+              for x in xs_host]
+        if not xs:
+            return []
+        b = xs[0].shape[0]
+        if any(tuple(x.shape) != tuple(xs[0].shape) for x in xs):
+            raise GraphError("forward_host_many: all batches must have the same shape")
+        if outs_host is None:
+            outs_host = [torch.empty(self.out_shape(b), dtype=torch.float32).pin_memory() for _ in xs]
+        if staging is None:
+            staging = (torch.empty(xs[0].shape, dtype=torch.float32, device=self.device),
+                       torch.empty(xs[0].shape, dtype=torch.float32, device=self.device),
+                       torch.empty(self.out_shape(b), dtype=torch.float32, device=self.device))
+        n = len(xs)
+        xp = (ctypes.c_void_p * n)(*[x.data_ptr() for x in xs])
+        op = (ctypes.c_void_p * n)(*[o.data_ptr() for o in outs_host])
+        st = (ctypes.c_int * n)() if sync else None
+        p = self.plan(b)
+        L.check(L.lib().pcnn_forward_host_many(p.handle, xp, op, n, ctypes.c_void_p(staging[0].data_ptr()),
+                                               ctypes.c_void_p(staging[1].data_ptr()),
+                                               ctypes.c_void_p(staging[2].data_ptr()), st,
+                                               _stream_handle(stream)), "pcnn_forward_host_many")
+        if sync:
+            for i in range(n):
+                if st[i]:
+                    self.fallbacks += 1
+                    outs_host[i].copy_(torch.from_numpy(self.forward_host(xs[i].numpy(), stream=stream)))
+        return outs_host
+
     def forward_unit(self, batch: int, i: int, x, out, stream=None) -> None:
         p = self.plan(batch)
         L.check(L.lib().pcnn_forward_unit(p.handle, i, ctypes.c_void_p(x.data_ptr()),

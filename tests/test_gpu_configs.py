@@ -87,3 +87,21 @@ def test_flag_synchronised_launches_match(cuda, name, monkeypatch):
     for _ in range(3):  # graph replays reuse the zeroed counters
         got = eng.forward(x).double().cpu().numpy()
         assert rel_err(got, base) <= 1e-6, name
+
+
+def test_forward_host_many_pipeline(cuda):
+    """pcnn_forward_host_many (H2D of batch i+1 overlapping batch i's
+    forward, two staging buffers) returns, for every batch, the logits the
+    plain device forward computes for it."""
+    import torch
+    cfg = configs.CONFIGS["resnet20"]
+    g, _, _ = T.redistribute_sweep(configs.build("resnet20"), "forward")
+    eng = Engine(g)
+    xs = [configs.make_input(cfg, batch=64, seed=s).astype(np.float32) for s in (2, 5, 7, 9, 11)]
+    outs = eng.forward_host_many(xs)
+    for x, o in zip(xs, outs):
+        want = eng.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+        assert rel_err(o.numpy(), want) <= 1e-6
+    # odd counts and a single batch take the same path
+    one = eng.forward_host_many(xs[:1])
+    assert rel_err(one[0].numpy(), outs[0].numpy()) <= 1e-6
