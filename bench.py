@@ -337,10 +337,8 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    from paper_2509_22857_b200.replicas import dist_env as env
+    return env()
 
 
 def run_reference(args):
@@ -380,11 +378,10 @@ def run_reference(args):
 
 def run_ours(args):
     import torch
+    from paper_2509_22857_b200 import replicas
     rank, world, local = dist_env()
     if world > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        replicas.init_replicas("nccl")  # replicas only: the group carries the barrier and max-over-ranks
     else:
         torch.cuda.set_device(0)
     from paper_2509_22857_b200 import configs
@@ -436,10 +433,7 @@ def run_ours(args):
     if world > 1:
         torch.distributed.barrier()
     ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = replicas.max_over_ranks(ms)
     value = world * batch * args.steps / (ms * 1e-3)
 
     # e2e through the C ABI with pinned host buffers
@@ -469,10 +463,7 @@ def run_ours(args):
         s1.record(stream)
         torch.cuda.synchronize()
         e_ms += s0.elapsed_time(s1)
-    if world > 1:
-        t = torch.tensor([e_ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e_ms = float(t.item())
+    e_ms = replicas.max_over_ranks(e_ms)
     e2e_serial = world * batch * args.steps / (e_ms * 1e-3)
 
     # e2e, pipelined: the same K steps through Engine.forward_host_many
@@ -490,10 +481,7 @@ def run_ours(args):
     p1.record(stream)
     torch.cuda.synchronize()
     p_ms = p0.elapsed_time(p1)
-    if world > 1:
-        t = torch.tensor([p_ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        p_ms = float(t.item())
+    p_ms = replicas.max_over_ranks(p_ms)
     e2e_value = world * batch * args.steps / (p_ms * 1e-3)
     for o in outs_h:
         np.testing.assert_allclose(o.numpy(), out.cpu().numpy(), rtol=1e-5, atol=1e-6)

@@ -1063,6 +1063,29 @@ def apply_pipeline(g: ModelGraph, strategy: str) -> Tuple[ModelGraph, PassReport
     return out, PassReport(rewrites, len(g.nodes) - len(out.nodes), before, critical_path_levels(out))
 
 
+def check_equivalence_replicas(ref: ModelGraph, candidate: ModelGraph, n_inputs: int = 100,
+                               rtol: float = 1e-4, seed: int = 0) -> EquivReport:
+    """check_equivalence with the inputs spread over the ranks of the
+    process group (one GPU each, replicas.init_replicas): each rank runs both
+    models on its shard, the per-input verdicts are gathered, every rank gets
+    the same report.  Same inputs as check_equivalence for a given seed."""
+    from . import replicas
+    from .runtime import Engine
+    import torch
+    shapes = ref.validate()
+    candidate.validate()
+    in_shape = shapes[ref.input_id()]
+    rng = np.random.default_rng(seed)
+    xs = np.stack([rng.uniform(-1.0, 1.0, in_shape) for _ in range(n_inputs)])
+    ea, eb = Engine(ref), Engine(candidate)
+
+    def run(eng):
+        return lambda x: eng.forward(torch.from_numpy(x.astype(np.float32)).cuda()).double().cpu().numpy()
+
+    worst, match, ok = replicas.equivalence_over_ranks(run(ea), run(eb), xs, rtol)
+    return EquivReport(n_inputs, worst, match, ok)
+
+
 def check_equivalence(ref: ModelGraph, candidate: ModelGraph, n_inputs: int = 100,
                       rtol: float = 1e-8, seed: int = 0) -> EquivReport:
     """transforms.py:753-778 with both forwards batched on the GPU (float32

@@ -105,3 +105,14 @@ def test_forward_host_many_pipeline(cuda):
     # odd counts and a single batch take the same path
     one = eng.forward_host_many(xs[:1])
     assert rel_err(one[0].numpy(), outs[0].numpy()) <= 1e-6
+
+
+def test_check_equivalence_replicas_single_rank(cuda):
+    """Without a process group check_equivalence_replicas is
+    check_equivalence (same inputs, same report)."""
+    g = configs.build("lenet5")
+    rg, _, _ = T.redistribute_sweep(g, "forward")
+    a = T.check_equivalence(g, rg, n_inputs=32, rtol=1e-4)
+    b = T.check_equivalence_replicas(g, rg, n_inputs=32, rtol=1e-4)
+    assert a.passed and b.passed
+    assert abs(a.max_rel_err - b.max_rel_err) <= 1e-7 and a.argmax_match_rate == b.argmax_match_rate
