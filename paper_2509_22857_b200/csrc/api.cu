@@ -72,6 +72,10 @@ struct pcnn_plan {
   size_t flags_n = 0;
   // fused[u]: unit u (a 1x1 projection) runs inside unit u - 1's halo-tile launch
   std::vector<char> fused;
+  // stream-K halo-tile launches (plan_streamk): per-unit CTA flags, shared partial slots
+  int* sk_flags = nullptr;
+  size_t sk_flags_n = 0;
+  float* sk_slots = nullptr;
   // pcnn_forward_host_many: copy stream, per-buffer events, pinned statuses
   cudaStream_t copy_stream = nullptr, out_stream = nullptr;
   cudaEvent_t h2d_done[2] = {nullptr, nullptr}, x_free[2] = {nullptr, nullptr};
@@ -385,6 +389,7 @@ void enqueue_unit(pcnn_plan* p, int ui, const float* x, float* logits, cudaStrea
 void enqueue_all(pcnn_plan* p, const float* x, float* logits, cudaStream_t s) {
   if (p->any_split) cudaMemsetAsync(p->status_dev, 0, sizeof(int), s);
   if (p->flags_on) cudaMemsetAsync(p->flags_dev, 0, sizeof(int) * p->flags_n, s);
+  if (p->sk_flags) cudaMemsetAsync(p->sk_flags, 0, sizeof(int) * p->sk_flags_n, s);
   for (int i = 0; i < (int)p->units.size(); ++i) enqueue_unit(p, i, x, logits, s, true);
 }
 
@@ -409,6 +414,47 @@ void fuse_projections(pcnn_plan* p) {
     p->fused[i + 1] = 1;
     p->launches -= 1;
   }
+}
+
+// Stream-K for halo-tile convs whose tiles fill the grid's last round badly
+// (RN20 stage 3: 163 tiles on 148 SMs; RN18 stages 3-4; VGG's 8x8 .. 2x2
+// layers): the (tile, chunk) units are spread evenly over all SMs, partial
+// tiles meet in per-CTA slots (conv_ss.cu seg_at).  One slot buffer serves
+// every such unit (launches are ordered by griddepcontrol.wait); each unit
+// has its own CTA flags, zeroed at the start of the forward.
+// PCNN_NO_STREAMK=1 keeps whole tiles.
+void plan_streamk(pcnn_plan* p) {
+  if (p->flags_on) return;  // flag-synchronised launches keep whole tiles
+  int dev = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int n = (int)p->units.size();
+  std::vector<int> want(n, 0);
+  size_t slot_max = 0, nflags = 0;
+  for (int i = 0; i < n; ++i) {
+    if (p->units[i].kind != PCNN_UNIT_CONV || p->impl[i] != 5 || p->chain_of[i] >= 0 || p->fused[i]) continue;
+    size_t slot = 0;
+    if (!conv_ss_streamk_wanted(p->conv_args[i], nsm, &slot)) continue;
+    want[i] = 1;
+    slot_max = std::max(slot_max, slot);
+    nflags += (size_t)nsm;
+  }
+  if (!nflags) return;
+  if (cudaMalloc(&p->sk_flags, sizeof(int) * nflags) != cudaSuccess ||
+      cudaMalloc(&p->sk_slots, sizeof(float) * slot_max * (size_t)nsm) != cudaSuccess) {
+    if (p->sk_flags) cudaFree(p->sk_flags);
+    p->sk_flags = nullptr;
+    return;
+  }
+  cudaMemset(p->sk_flags, 0, sizeof(int) * nflags);
+  p->sk_flags_n = nflags;
+  size_t off = 0;
+  for (int i = 0; i < n; ++i)
+    if (want[i]) {
+      p->conv_args[i].sk_flags = p->sk_flags + off;
+      p->conv_args[i].sk_slots = p->sk_slots;
+      off += (size_t)nsm;
+    }
 }
 
 // Flag-synchronised launches.  A halo-tile conv whose input and residual are
@@ -604,6 +650,7 @@ int pcnn_plan_create(const pcnn_unit_desc* units, int n_units, const pcnn_tensor
   }
   fuse_projections(p);
   build_flags(p);
+  plan_streamk(p);
   for (int len : p->chain_len) p->launches -= len - 1;  // one kernel per chain
   if (cudaStreamCreateWithFlags(&p->capture_stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete p;
@@ -620,6 +667,8 @@ int pcnn_plan_destroy(pcnn_plan* p) {
   for (SsChain* c : p->chains) ss_chain_destroy(c);
   if (p->status_dev) cudaFree(p->status_dev);
   if (p->flags_dev) cudaFree(p->flags_dev);
+  if (p->sk_flags) cudaFree(p->sk_flags);
+  if (p->sk_slots) cudaFree(p->sk_slots);
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
   if (p->out_stream) cudaStreamDestroy(p->out_stream);
   for (int i = 0; i < 2; ++i)
@@ -785,6 +834,12 @@ int pcnn_forward_host_many(pcnn_plan* p, const float* const* x_hosts, float* con
 
 int pcnn_forward_unit(pcnn_plan* p, int unit, const float* x, float* logits, void* stream) {
   if (!p || unit < 0 || unit >= (int)p->units.size()) return fail(PCNN_ERR_INVALID, "bad unit");
+  if (p->conv_args.size() > (size_t)unit && p->conv_args[unit].sk_flags) {  // run alone: fresh stream-K flags
+    int dev = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaMemsetAsync(p->conv_args[unit].sk_flags, 0, sizeof(int) * nsm, static_cast<cudaStream_t>(stream));
+  }
   if (p->prezeroed[unit]) {  // run alone: its global-pool sums need their own zeroing
     const ConvArgs& a = p->conv_args[unit];
     cudaMemsetAsync(a.epi.out.base, 0, sizeof(float) * (size_t)p->batch * a.epi.out.cpad(),

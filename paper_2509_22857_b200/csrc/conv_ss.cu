@@ -204,6 +204,41 @@ __device__ __forceinline__ void ss_stage(bool concat, uint32_t dm, uint32_t dc, 
   }
 }
 
+// ---- work segments: what a CTA computes, in order ----
+// Whole tiles: tile = blockIdx.x + i * gridDim.x, all chunks, owner.
+// Stream-K: units u = tile * nq + chunk, CTA c owns [c U / G, (c + 1) U / G);
+// its segments are visited in descending tile order, so its only partial
+// (non-owner) segment -- the prefix of its last tile -- comes first and is
+// published early, and the tile it finishes (the suffix of its first tile,
+// whose earlier chunks belong to lower CTAs) comes last.
+struct Seg {
+  int tile, q0, q1;
+  int owner;  // holds the tile's last chunk: runs the epilogue
+  int c_lo;   // owner: first CTA holding earlier chunks of the tile (-1: none)
+};
+__device__ __forceinline__ bool seg_at(int i, int total_tiles, int nq, bool streamk, Seg& s) {
+  if (!streamk) {
+    s.tile = (int)blockIdx.x + i * (int)gridDim.x;
+    s.q0 = 0;
+    s.q1 = nq;
+    s.owner = 1;
+    s.c_lo = -1;
+    return s.tile < total_tiles;
+  }
+  const int64_t U = (int64_t)total_tiles * nq, G = gridDim.x, c = blockIdx.x;
+  const int64_t u0 = c * U / G, u1 = (c + 1) * U / G;
+  if (u1 <= u0) return false;
+  const int64_t t0 = u0 / nq, t1 = (u1 - 1) / nq, t = t1 - i;
+  if (t < t0) return false;
+  s.tile = (int)t;
+  s.q0 = (int)((u0 > t * nq ? u0 : t * nq) - t * nq);
+  s.q1 = (int)((u1 < (t + 1) * nq ? u1 : (t + 1) * nq) - t * nq);
+  s.owner = s.q1 == nq;
+  // first contributor: the CTA whose range holds unit t * nq
+  s.c_lo = (s.owner && s.q0 > 0) ? (int)(((t * nq + 1) * G - 1) / U) : -1;
+  return true;
+}
+
 // Flag-synchronised launches: wait until the producer tiles covering grid
 // positions [lo, hi) (mode 1) or all its tiles (mode 2) have bumped their
 // counters (release-ordered after their stores).  Bounded: a missing signal
@@ -243,7 +278,9 @@ __device__ __forceinline__ void flag_wait(const FlagDep& d, int64_t lo, int64_t 
   }
 }
 
-template <int TAPS>
+// SK: stream-K segments (a separate instantiation: the whole-tile kernel
+// keeps its registers and its simpler item walk)
+template <int TAPS, bool SK>
 __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_constant__ SsParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
@@ -255,6 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
   const uint32_t wres_base = base + (uint32_t)ring;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total_tiles = P.m_tiles * P.n_tiles;
+  constexpr bool streamk = SK;
   const int NP = P.partials, NB = P.acc_bufs;
   const uint32_t set_a = P.concat ? (uint32_t)NP * 2 * P.nt : (uint32_t)(NP + 1) * P.nt;
   constexpr bool kProj = TAPS == 9;  // projection fusion: 3x3 convs only (keeps the stem's registers)
@@ -333,7 +371,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       uint32_t ph = 0;
       bool fin_all = false, fsk_all = false;
       int dep_seq = 0;
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      Seg sg;
+      for (int si = 0; seg_at(si, total_tiles, P.nq, streamk, sg); ++si) {
+        const int tile = sg.tile;
         const int n_tile = tile / P.m_tiles, m_tile = tile - n_tile * P.m_tiles;
         const int64_t gs = (int64_t)m_tile * kTileM * P.mt - P.halo;  // grid position of buffer slot 0
         const int64_t cs = gs < 0 ? 0 : gs;
@@ -354,7 +394,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
         }
         if (P.psub) {
           // one parity plane and its taps' weights per stage
-          for (int q = 0; q < P.nq; ++q)
+          for (int q = sg.q0; q < sg.q1; ++q)
             for (int ps = 0; ps < 4; ++ps) {
               ptx::mbar_wait_sleep(ptx::smem_u32(&S->empty[st]), ph ^ 1);
               const uint32_t bar = ptx::smem_u32(&S->full[st]);
@@ -387,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
             }
           continue;
         }
-        for (int q = 0; q < P.nq; ++q) {
+        for (int q = sg.q0; q < sg.q1; ++q) {
           if (P.dbg & 2048) ptx::mbar_wait_nohint(ptx::smem_u32(&S->empty[st]), ph ^ 1);
           else ptx::mbar_wait_sleep(ptx::smem_u32(&S->empty[st]), ph ^ 1);
           tr(P, 0, 0x100 | q);
@@ -441,19 +481,24 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
     const uint64_t bstep = (uint64_t)(64 * P.nt) >> 4, blo = (uint64_t)(P.nt * 16) >> 4;
     int st = 0;
     uint32_t ph = 0, acc = 0, acc_ph = 0;
-    bool w_ready = !P.wres;  // every resident chunk seen (after the first tile)
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    uint32_t w_seen = P.wres ? 0u : ~0u;  // resident chunks already waited for
+    Seg sg;
+    for (int si = 0; seg_at(si, total_tiles, P.nq, streamk, sg); ++si) {
       ptx::mbar_wait(ptx::smem_u32(&S->acc_empty[acc]), acc_ph ^ 1);
       ptx::tc_fence_after();
       const uint32_t d_tile = tmem + acc * P.mt * set_cols;
       int p = 0;
       const int nsub = P.psub ? 4 : 1;
-      for (int q = 0; q < P.nq; ++q) {
+      const int q0 = sg.q0;
+      for (int q = q0; q < sg.q1; ++q) {
        for (int ps = 0; ps < nsub; ++ps) {
         tr(P, 1, 0x400 | q);
         ptx::mbar_wait(ptx::smem_u32(&S->full[st]), ph);
         tr(P, 1, 0x500 | q);
-        if (!w_ready) ptx::mbar_wait(ptx::smem_u32(&S->wfull[q]), 0);
+        if (!((w_seen >> q) & 1u)) {
+          ptx::mbar_wait(ptx::smem_u32(&S->wfull[q]), 0);
+          w_seen |= 1u << q;
+        }
         ptx::tc_fence_after();
         const uint32_t sb = base + st * P.stage_bytes;
         const uint64_t a_hi = ptx::smem_desc_noswz(sb, a_lbo, 128);
@@ -462,8 +507,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
                                                  b_lbo, 128);
         // first writes: main partial at its first chunk's first sub-stage,
         // correction at the tile's first sub-stage
-        const uint32_t main_acc = (q >= NP || ps > 0) ? 1u : 0u;
-        const uint32_t corr_acc = (q > 0 || ps > 0) ? 1u : 0u;
+        const uint32_t main_acc = (q - q0 >= NP || ps > 0) ? 1u : 0u;
+        const uint32_t corr_acc = (q > q0 || ps > 0) ? 1u : 0u;
         if (do_mma) {
           for (int sub = 0; sub < P.mt; ++sub) {
             // sub-tile rows start 128 positions further in the same buffer
@@ -497,7 +542,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
               const uint32_t pm = d_set + set_a;
               const uint64_t bp = b0 + ((uint64_t)P.b_bytes >> 4);
               ss_stage<1>(P.concat, pm, pm + P.nt, a_hi + shift, a_lo + shift, bp, bstep, blo, idesc2, idesc,
-                          q > 0 ? 1u : 0u, q > 0 ? 1u : 0u, po);
+                          q > q0 ? 1u : 0u, q > q0 ? 1u : 0u, po);
             }
           }
         }
@@ -507,7 +552,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
        }
         if (++p == NP) p = 0;
       }
-      w_ready = true;
       ptx::mma_commit_warp(ptx::smem_u32(&S->acc_full[acc]));
       if (++acc == (uint32_t)NB) { acc = 0; acc_ph ^= 1; }
     }
@@ -537,8 +581,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
     const uint32_t sk_slot = ptx::smem_u32(ptab + P.etab.rows * e.npad) + threadIdx.x * 16;
     struct Item {
       int tile, k, n_tile, b, oy, ox, g;
-      uint32_t it;
+      uint32_t it;  // segment index
       bool valid;
+      int owner, c_lo;  // segment: runs the epilogue; first contributing CTA
+      int nqs;          // segment chunks (partial accumulators beyond them were not written)
     };
     // this thread's row of sub-tile (k >> lg_nch) of the item's tile -> image, output row / column
     auto locate = [&](Item& x) {
@@ -571,9 +617,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       x.k += kstep;
       if (x.k < nk) return true;
       for (;;) {
-        x.tile += gridDim.x;
         ++x.it;
-        if (x.tile >= total_tiles) return false;
+        Seg sx;
+        if (!seg_at((int)x.it, total_tiles, P.nq, streamk, sx)) return false;
+        x.tile = sx.tile;
+        if constexpr (SK) {
+          x.owner = sx.owner;
+          x.c_lo = sx.c_lo;
+          x.nqs = sx.q1 - sx.q0;
+        }
         if (P.share_epi || ((int)((x.it & (NB - 1)) & 1) == ew && !(NB == 1 && ew == 1))) break;
       }
       x.k = k0;
@@ -608,9 +660,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
         load16_async(e.skip, x.b, chan(x), x.oy, x.ox, x.valid, dst, skq);
     };
     Item cur;
-    cur.tile = (int)blockIdx.x - (int)gridDim.x;
+    cur.tile = -1;
     cur.it = ~0u;
     cur.k = nk;
+    cur.owner = 1;
+    cur.c_lo = -1;
+    cur.nqs = P.nq;
     bool have = advance(cur);
     uint32_t par = 0;  // staging buffer of the current item
     if (have) {
@@ -620,9 +675,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
     while (have) {
       Item nxt = cur;
       const bool have_next = advance(nxt);
-      const bool last_of_tile = !have_next || nxt.tile != cur.tile;
+      const bool last_of_tile = !have_next || nxt.it != cur.it;
       if (have_next) {
-        if (nxt.tile != cur.tile || (nxt.k >> lg_nch) != (cur.k >> lg_nch)) locate(nxt);
+        if (nxt.it != cur.it || (nxt.k >> lg_nch) != (cur.k >> lg_nch)) locate(nxt);
         if (e.residual) skip_async(nxt, sk_slot + (par ^ 1) * 4 * skq);
       }
       const uint32_t acc = cur.it & (NB - 1);  // NB is 1, 2 or 4
@@ -637,7 +692,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       const uint32_t d_set = tmem + lane_off + (acc * P.mt + sub) * set_cols + (pj ? set_a : 0u);
       if (!(P.dbg & 4)) {
         float v[16], t[16];
-        const int npi = pj ? 1 : NP;  // the projection has one main partial and its correction
+        // the projection has one main partial and its correction; a stream-K
+        // segment shorter than NP chunks wrote only its first partials
+        const int npi = pj ? 1 : (SK && cur.nqs < NP ? cur.nqs : NP);
         if (P.concat) {
           ptx::tmem_ld16x2(d_set + P.nt + c0, d_set + c0, v, t);
 #pragma unroll
@@ -649,7 +706,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
             for (int i = 0; i < 16; ++i) v[i] += u[i] + t[i];
           }
         } else {
-          ptx::tmem_ld16x2(d_set + npi * P.nt + c0, d_set + c0, v, t);
+          // correction after all NP main partials (projection: after its one)
+          ptx::tmem_ld16x2(d_set + (pj ? 1 : NP) * P.nt + c0, d_set + c0, v, t);
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] += t[i];
           for (int p = 1; p < npi; ++p) {
@@ -677,12 +735,62 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
 #pragma unroll
           for (int i = 0; i < 16; ++i) sk[i] = 0.f;
         }
-        if (kProj && pj)
-          epi_chunk16(P.pe, petab, v, pwsc, sk, chan(cur), cur.valid, cur.valid ? cur.b : 0, cur.oy, cur.ox, lane, -1,
-                      P.pe.out.sstore);
-        else
-          epi_chunk16(e, etab, v, wsc, sk, chan(cur), cur.valid, cur.valid ? cur.b : 0, cur.oy, cur.ox, lane,
-                      P.out_pos ? (int64_t)cur.g * 8 : -1, P.fold_out ? 1.f : e.out.sstore);
+        if (streamk && !cur.owner) {
+          // stream-K partial: this CTA's chunks of the tile, raw, to its slot;
+          // the last draining warp publishes the slot (GPU-scope release,
+          // cumulative over the stores the CTA-scope counter ordered before it)
+          float4* dst = reinterpret_cast<float4*>(a.sk_slots + (((size_t)blockIdx.x * nk + cur.k) * 128 + row) * 16);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) __stcg(dst + i, make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
+          if (last_of_tile) {
+            // every lane fences its own slot stores at GPU scope (the CTA
+            // counter alone left partials invisible to the owner now and then)
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) {
+              const uint32_t nsig = P.share_epi ? 8u : 4u;
+              uint32_t old;
+              asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                           : "=r"(old) : "r"(ptx::smem_u32(&S->tstored[cur.it & (kSigRing - 1)])) : "memory");
+              if (old % nsig == nsig - 1)
+                asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.sk_flags + blockIdx.x) : "memory");
+            }
+          }
+        } else {
+          if (streamk && cur.c_lo >= 0) {
+            // owner of a tile whose earlier chunks lower CTAs computed: add
+            // their published partials (each published its one partial
+            // segment first, so these waits are short)
+            if (cur.k == k0) {
+              if (lane == 0)
+                for (int c = cur.c_lo; c < (int)blockIdx.x; ++c) {
+                  uint32_t spins = 0;
+                  for (;;) {
+                    int f;
+                    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(a.sk_flags + c) : "memory");
+                    if (f >= 1) break;
+                    __nanosleep(64);
+                    if (++spins > (1u << 25)) __trap();
+                  }
+                }
+              __syncwarp();
+            }
+            for (int c = cur.c_lo; c < (int)blockIdx.x; ++c) {
+              const float4* src = reinterpret_cast<const float4*>(a.sk_slots + (((size_t)c * nk + cur.k) * 128 + row) * 16);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float4 f = __ldcg(src + i);
+                v[4 * i] += f.x; v[4 * i + 1] += f.y; v[4 * i + 2] += f.z; v[4 * i + 3] += f.w;
+              }
+            }
+          }
+          if (kProj && pj)
+            epi_chunk16(P.pe, petab, v, pwsc, sk, chan(cur), cur.valid, cur.valid ? cur.b : 0, cur.oy, cur.ox, lane,
+                        -1, P.pe.out.sstore);
+          else
+            epi_chunk16(e, etab, v, wsc, sk, chan(cur), cur.valid, cur.valid ? cur.b : 0, cur.oy, cur.ox, lane,
+                        P.out_pos ? (int64_t)cur.g * 8 : -1, P.fold_out ? 1.f : e.out.sstore);
+        }
         if (lane == 0 && warp == 0) tr(P, 2, 0xE00 | c0);
         if (last_of_tile && a.sig_done) {
           // this warp's rows of the tile are stored: __syncwarp orders the
@@ -710,7 +818,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       if (last_of_tile && lane == 0 && warp == 0) tr(P, 2, 0x900);
       if (!have_next) break;
       par ^= 1;
-      if (nxt.tile == cur.tile && (nxt.k >> lg_nch) == (cur.k >> lg_nch)) {
+      if (nxt.it == cur.it && (nxt.k >> lg_nch) == (cur.k >> lg_nch)) {
         nxt.b = cur.b; nxt.oy = cur.oy; nxt.ox = cur.ox; nxt.valid = cur.valid; nxt.n_tile = cur.n_tile;
       }
       cur = nxt;
@@ -1278,6 +1386,24 @@ bool conv_ss_proj_ok(const ConvArgs& a, const ConvArgs& proj) {
   return make_ss_params(b, P) && P.proj;
 }
 
+bool conv_ss_streamk_wanted(const ConvArgs& a, int nsm, size_t* slot_floats) {
+  if (getenv("PCNN_NO_STREAMK")) return false;
+  SsParams P;
+  if (!make_ss_params(a, P) || P.nq < 2) return false;
+  const int tiles = P.m_tiles * P.n_tiles;
+  // Measured on B200 (PCNN_NO_STREAMK A/B): splitting pays only when whole
+  // tiles leave most SMs idle (VGG 2x2 layers: 36 tiles for 148 SMs);
+  // for 1.1-1.5 rounds of tiles (RN20 stage 3, RN18 stages 3-4) the partial
+  // round trips and shorter pipelines cost more than the balance gains
+  // (RN20 0.362 vs 0.322 ms).  PCNN_STREAMK_FILL overrides the threshold.
+  static const char* fill_env = getenv("PCNN_STREAMK_FILL");
+  const double fill = fill_env ? atof(fill_env) : 0.3;
+  if (tiles > fill * nsm) return false;
+  const int items = P.mt * (P.nt / 16) * (P.proj ? 2 : 1);
+  *slot_floats = (size_t)items * 128 * 16;
+  return true;
+}
+
 bool conv_ss_supported(const ConvArgs& a) {
   SsParams P;
   return make_ss_params(a, P);
@@ -1294,8 +1420,17 @@ void launch_conv_ss(const ConvArgs& a, cudaStream_t s) {
   }
   const size_t smem = 128 + (size_t)P.stages * P.stage_bytes + P.res_bytes + ss_aux_bytes(P);
   const int tiles = P.m_tiles * P.n_tiles;
-  const int grid = tiles < nsm ? tiles : nsm;
-  void (*k)(SsParams) = P.taps == 16 ? conv_ss_kernel<16> : P.taps == 9 ? conv_ss_kernel<9> : conv_ss_kernel<1>;
+  int grid = tiles < nsm ? tiles : nsm;
+  if (a.sk_flags) {
+    // stream-K: every SM, at least two chunks each (plan_streamk sized the slots for nsm CTAs)
+    const int64_t units = (int64_t)tiles * P.nq;
+    grid = units / 2 < nsm ? (int)(units / 2) : nsm;
+    if (grid < 1) grid = 1;
+  }
+  const bool sk = a.sk_flags != nullptr;
+  void (*k)(SsParams) = P.taps == 16 ? (sk ? conv_ss_kernel<16, true> : conv_ss_kernel<16, false>)
+                        : P.taps == 9 ? (sk ? conv_ss_kernel<9, true> : conv_ss_kernel<9, false>)
+                                      : (sk ? conv_ss_kernel<1, true> : conv_ss_kernel<1, false>);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (P.dbg & 64) P.time_slot = g_time_next++ % kTimeSlots;
   launch_pdl(k, grid, kThreads, smem, s, P);

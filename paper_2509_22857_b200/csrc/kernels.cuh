@@ -46,6 +46,13 @@ struct ConvArgs {
   // block's projection) computed in the same launch from the centre tap's
   // A operand, into its own output (api.cu fuse_projections); or null
   const ConvArgs* proj = nullptr;
+  // halo-tile kernel, stream-K (api.cu plan_streamk): the (tile, 16-channel
+  // chunk) units are split evenly over the grid; a CTA whose range ends
+  // inside a tile writes that tile's partial sums to its slot and sets its
+  // flag, the CTA holding the tile's last chunk adds them before the
+  // epilogue.  null: one whole tile per CTA turn.
+  int* sk_flags = nullptr;    // [grid], zeroed at the start of every forward
+  float* sk_slots = nullptr;  // [grid][items][128][16]
 };
 
 struct LinearArgs {
@@ -127,5 +134,8 @@ void launch_conv_ss(const ConvArgs& a, cudaStream_t s);
 bool conv_ss_flag_geometry(const ConvArgs& a, FlagDep& d);
 // can `proj` (1x1, same input and stride) run inside `a`'s halo-tile launch?
 bool conv_ss_proj_ok(const ConvArgs& a, const ConvArgs& proj);
+// stream-K for this halo-tile launch pays (whole tiles leave the grid's
+// last round mostly idle); slot_floats: the slot size it needs per CTA
+bool conv_ss_streamk_wanted(const ConvArgs& a, int nsm, size_t* slot_floats);
 
 }  // namespace pcnn

@@ -86,7 +86,9 @@ def test_flag_synchronised_launches_match(cuda, name, monkeypatch):
     assert fn(eng.plan(cfg.batch).handle) == 1, name
     for _ in range(3):  # graph replays reuse the zeroed counters
         got = eng.forward(x).double().cpu().numpy()
-        assert rel_err(got, base) <= 1e-6, name
+        # (flag mode keeps whole tiles; the default plan may split tiles
+        # stream-K, which sums the same products in another order)
+        assert rel_err(got, base) <= 1e-5, name
 
 
 def test_forward_host_many_pipeline(cuda):
