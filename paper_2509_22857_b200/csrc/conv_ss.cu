@@ -1396,7 +1396,7 @@ bool conv_ss_streamk_wanted(const ConvArgs& a, int nsm, size_t* slot_floats) {
   // for 1.1-1.5 rounds of tiles (RN20 stage 3, RN18 stages 3-4) the partial
   // round trips and shorter pipelines cost more than the balance gains
   // (RN20 0.362 vs 0.322 ms).  PCNN_STREAMK_FILL overrides the threshold.
-  static const char* fill_env = getenv("PCNN_STREAMK_FILL");
+  const char* fill_env = getenv("PCNN_STREAMK_FILL");
   const double fill = fill_env ? atof(fill_env) : 0.3;
   if (tiles > fill * nsm) return false;
   const int items = P.mt * (P.nt / 16) * (P.proj ? 2 : 1);

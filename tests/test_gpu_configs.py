@@ -118,3 +118,25 @@ def test_check_equivalence_replicas_single_rank(cuda):
     b = T.check_equivalence_replicas(g, rg, n_inputs=32, rtol=1e-4)
     assert a.passed and b.passed
     assert abs(a.max_rel_err - b.max_rel_err) <= 1e-7 and a.argmax_match_rate == b.argmax_match_rate
+
+
+@pytest.mark.parametrize("name", ["resnet20", "resnet18", "vgg11"])
+def test_streamk_matches_whole_tiles(cuda, name, monkeypatch):
+    """Stream-K forced onto every layer with <= 2 rounds of tiles
+    (PCNN_STREAMK_FILL=2: RN20 stage 3, RN18 stages 3-4, VGG's 8x8..2x2
+    layers, fused projections included) computes what whole tiles compute,
+    up to the summation order of the split chunks."""
+    import torch
+    cfg = configs.CONFIGS[name]
+    g = configs.build(name)
+    for d in cfg.redistribution:
+        g, _, _ = T.redistribute_sweep(g, d, allow_negative_leading=cfg.allow_negative_leading)
+    x = torch.from_numpy(configs.make_input(cfg).astype(np.float32)).cuda()
+    monkeypatch.setenv("PCNN_NO_STREAMK", "1")
+    base = Engine(g).forward(x).double().cpu().numpy()
+    monkeypatch.delenv("PCNN_NO_STREAMK")
+    monkeypatch.setenv("PCNN_STREAMK_FILL", "2")
+    eng = Engine(g)
+    for _ in range(2):
+        got = eng.forward(x).double().cpu().numpy()
+        assert rel_err(got, base) <= 1e-5, name
