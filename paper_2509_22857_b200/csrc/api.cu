@@ -70,7 +70,8 @@ struct pcnn_plan {
   bool flags_on = false;
   int* flags_dev = nullptr;
   size_t flags_n = 0;
-  // fused[u]: unit u (a 1x1 projection) runs inside unit u - 1's halo-tile launch
+  // fused[u]: unit u (a 1x1 projection) runs inside unit u - 1's halo-tile launch;
+  // for a copyout: the linear unit before it writes the user's logits itself
   std::vector<char> fused;
   // stream-K halo-tile launches (plan_streamk): per-unit CTA flags, shared partial slots
   int* sk_flags = nullptr;
@@ -358,10 +359,12 @@ void enqueue_unit(pcnn_plan* p, int ui, const float* x, float* logits, cudaStrea
       a.poly_stride = p->views[u.out].cpad();
       a.out = p->views[u.out].base;
       a.out_stride = p->views[u.out].cpad();
+      if (ui + 1 < (int)p->fused.size() && p->fused[ui + 1]) a.out2 = logits;
       launch_linear(a, s);
       break;
     }
     case PCNN_UNIT_COPYOUT: {
+      if (p->fused[ui]) break;  // the linear unit before it wrote the logits
       launch_copyout(p->views[u.in], logits, p->batch, s);
       break;
     }
@@ -411,6 +414,16 @@ void fuse_projections(pcnn_plan* p) {
     if (p->conv_args[i].prezero || p->conv_args[i + 1].prezero) continue;
     if (!conv_ss_proj_ok(p->conv_args[i], p->conv_args[i + 1])) continue;
     p->conv_args[i].proj = &p->conv_args[i + 1];
+    p->fused[i + 1] = 1;
+    p->launches -= 1;
+  }
+  // a linear unit whose vector output only the final copyout reads writes
+  // the logits directly (one launch less)
+  for (int i = 0; i + 1 < n; ++i) {
+    const pcnn_unit_desc &u = p->units[i], &v = p->units[i + 1];
+    if (u.kind != PCNN_UNIT_LINEAR || v.kind != PCNN_UNIT_COPYOUT || v.in != u.out) continue;
+    const TensorView& t = p->views[u.out];
+    if (!t.is_vector || t.c != (int)u.cout || getenv("PCNN_NO_LINEAR_OUT")) continue;
     p->fused[i + 1] = 1;
     p->launches -= 1;
   }

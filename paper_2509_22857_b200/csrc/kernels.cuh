@@ -66,6 +66,8 @@ struct LinearArgs {
   int64_t poly_stride;
   float* out;
   int64_t out_stride;
+  // also the user's [batch][n_out] logits (the copyout unit folded in), or null
+  float* out2 = nullptr;
 };
 
 struct EltArgs {

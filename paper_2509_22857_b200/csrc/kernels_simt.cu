@@ -340,6 +340,7 @@ __global__ void __launch_bounds__(256) linear_kernel(LinearArgs a) {
         v += __ldg(a.bias + k);
         if (a.poly_deg) v = horner(a.poly, a.poly_stride, a.poly_deg, k, v);
         a.out[(int64_t)b * a.out_stride + k] = v;
+        if (a.out2) a.out2[(int64_t)b * a.n_out + k] = v;
       }
     }
   }
