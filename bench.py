@@ -10,14 +10,22 @@ summed; under torchrun the max over ranks is reported ("replicas only": each
 rank runs its own batch, no collective on the data path).
 
 The JSON line also carries
-* e2e      -- the same metric through pcnn_forward_host with pinned host
-              buffers (H2D of the batch + forward + D2H of the logits timed);
-* roofline -- the conv kernel family (dominant kernels) against the
-              3xTF32-effective tensor rate and HBM bandwidth from
-              MEASURED_PEAKS.json, from per-unit CUDA-event timings;
+* e2e      -- the same metric through the C ABI with pinned host buffers
+              (pcnn_forward_host_many: every step's input H2D and logits
+              D2H inside the timed region, copies overlapping forwards);
+* roofline -- the dominant kernel family against the fp32-accurate tensor
+              rate of that kernel (fp16x2: bf16/3) or HBM bandwidth
+              (MEASURED_PEAKS.json); its time per step is the union of its
+              launches' intervals on the device timeline of every timed
+              graph replay (pcnn_plan_timeline), so it cannot exceed the step;
+* parity   -- the timed batch's logits against the float64 oracle, every
+              image (oracle/pool.py over the host cores; the checker);
+* secondary -- the same record for ResNet-18 (the second >= 60 % target
+              config), measured in the same run;
 * cpu_baseline -- the float64 oracle (restatement of levnet's
               reference_eval) on the host cores, bounded sample;
-* redistribution -- the device redistribution program (one launch), us/call.
+* redistribution -- the device redistribution program (one launch), us/call,
+              next to the oracle port of the reference's sweep on one core.
 
 ``--impl reference`` times the reference CPU path (the oracle port of
 reference_eval, multiprocess over host cores) on the same config and prints
@@ -63,11 +71,11 @@ def build_model(name: str):
     return configs.build(name)
 
 
-def redistributed_engine(g, cfg):
+def redistributed_engine(g, cfg, options=None):
     """Apply the config's redistribution on the device; return (engine, info)."""
     from paper_2509_22857_b200 import transforms as T
     from paper_2509_22857_b200.runtime import Engine
-    eng = Engine(g)
+    eng = Engine(g, options=options)
     info = []
     cur = g
     for direction in cfg.redistribution:
@@ -104,120 +112,168 @@ def time_redistribution(g, cfg, reps=20):
 
 
 # ---------------------------------------------------------------------------
-# roofline bookkeeping
+# roofline bookkeeping, from the device timeline of graph replays
 # ---------------------------------------------------------------------------
 
-def unit_cost(lw, u, batch):
-    """(algorithmic FLOPs, algorithmic bytes) of one conv unit."""
-    t_in = lw.tensors[u["in_"]]
-    t_out = lw.tensors[u["out"]]
-    cin, cout, kh, kw, s, p = u["cin"], u["cout"], u["kh"], u["kw"], u["stride"], u["pad"]
-    ho = (t_in.h + 2 * p - kh) // s + 1
-    wo = (t_in.w + 2 * p - kw) // s + 1
+KERNEL_NAMES = {1: "conv_simt_kernel", 2: "conv_tc_kernel (3xTF32, A in TMEM)",
+                3: "conv_tc_kernel (fp16x2, A in TMEM)", 5: "conv_ss_kernel (fp16x2, halo tiles in smem)"}
+OTHER_NAMES = {1: "ingest_kernel", 3: "linear_kernel", 12: "copyout_kernel"}
+
+
+def unit_cost(eng, i, batch):
+    """(algorithmic FLOPs, algorithmic bytes) of conv unit i, from the graph's
+    conv node (the reference's layer, not its lowered form -- e.g. RN18's
+    7x7/s2 stem counts K = 3*7*7 = 147, not the space-to-depth K = 192):
+    FLOP = 2 M N K, M = B Ho Wo, N = C_out, K = C_in kh kw; bytes = 4 (input
+    once + output after the fused pool + residual + weights + bias)."""
+    from paper_2509_22857_b200.graph import ConvNode
+    lw = eng.lw
+    g = lw.graph
+    shapes = lw.shapes
+    u = lw.units[i]
+    conv = next(nid for nid in lw.unit_nodes[i] if isinstance(g.nodes[nid], ConvNode))
+    node = g.nodes[conv]
+    src = g.inputs_of(conv)[0]
+    cin, h, w = shapes[src]
+    cout, _, kh, kw = node.weight.shape
+    ho, wo = shapes[conv][1], shapes[conv][2]
     m = batch * ho * wo
-    k = cin * kh * kw
-    flops = 2.0 * m * cout * k
-    byts = 4.0 * (batch * cin * t_in.h * t_in.w + batch * t_out.c * t_out.h * t_out.w + cout * k + cout)
+    flops = 2.0 * m * cout * cin * kh * kw
+    out = 1
+    for d in shapes[lw.unit_nodes[i][-1]]:
+        out *= d
+    byts = 4.0 * (batch * cin * h * w + batch * out + cout * cin * kh * kw + cout)
     if u.get("residual", 0):
         byts += 4.0 * batch * cout * ho * wo
     return flops, byts
 
 
-def per_unit_times(eng, x, out, reps, flush):
-    """Eager pass, CUDA events between units on the launching stream."""
-    import torch
-    from paper_2509_22857_b200 import _lib as L
-    plan = eng.plan(x.shape[0])
-    n = plan.n_units
-    stream = torch.cuda.current_stream()
-    acc = np.zeros(n)
-    for _ in range(reps):
-        flush()
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(n + 1)]
-        ev[0].record(stream)
-        for i in range(n):
-            eng.forward_unit(x.shape[0], i, x, out)
-            ev[i + 1].record(stream)
-        torch.cuda.synchronize()
-        acc += np.array([ev[i].elapsed_time(ev[i + 1]) for i in range(n)])
-    return acc / reps  # ms per unit
+def unit_family(eng, plan, i):
+    u = eng.lw.units[i]
+    if u["kind"] == 2:
+        return KERNEL_NAMES[plan.unit_impl(i)]
+    return OTHER_NAMES.get(u["kind"], "eltwise / pool kernels")
 
 
-KERNEL_NAMES = {1: "conv_simt_kernel", 2: "conv_tc_kernel (3xTF32, A in TMEM)",
-                3: "conv_tc_kernel (fp16x2, A in TMEM)", 5: "conv_ss_kernel (fp16x2, halo tiles in smem)"}
+def union_ns(iv):
+    """Total length of the union of [s, e) intervals."""
+    tot, cur_s, cur_e = 0, None, None
+    for s, e in sorted(iv):
+        if cur_e is None or s > cur_e:
+            if cur_e is not None:
+                tot += cur_e - cur_s
+            cur_s, cur_e = s, e
+        else:
+            cur_e = max(cur_e, e)
+    if cur_e is not None:
+        tot += cur_e - cur_s
+    return tot
 
 
-def measured_traffic(config, kernel):
-    """dram read+write bytes per launch of `kernel` from the committed ncu
-    capture summary (profiles/traffic.json, written by tools/profile_round.py)."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")
-    try:
-        with open(path) as f:
-            t = json.load(f)
-        return t.get(config, {}).get(kernel)
-    except (OSError, ValueError):
-        return None
+class TimelineStats:
+    """Per-step device timelines (pcnn_plan_timeline: %globaltimer at each
+    launch's first CTA start past its dependency wait and last CTA exit),
+    read after every timed step.  For each kernel family: the union of its
+    launches' intervals per step, so a family's time can never exceed the
+    step."""
+
+    def __init__(self, eng, plan):
+        self.eng, self.plan = eng, plan
+        n = plan.n_units
+        self.launch_of = [plan.unit_launch(i) for i in range(n)]
+        self.family = [unit_family(eng, plan, self.launch_of[i]) for i in range(n)]
+        self.fam_ns = {}
+        self.unit_ns = np.zeros(n)
+        self.span_ns = []
+        self.steps = 0
+
+    def add(self, tl):
+        live = [(i, int(s), int(e)) for i, (s, e) in enumerate(tl) if e > 0 and s > 0]
+        if not live:
+            return
+        self.steps += 1
+        self.span_ns.append(max(e for _, _, e in live) - min(s for _, s, _ in live))
+        fams = {}
+        for i, s, e in live:
+            fams.setdefault(self.family[i], []).append((s, e))
+            self.unit_ns[i] += e - s
+        for f, iv in fams.items():
+            self.fam_ns[f] = self.fam_ns.get(f, 0) + union_ns(iv)
+
+    def family_ms(self):
+        return {f: t / self.steps * 1e-6 for f, t in self.fam_ns.items()}
+
+    def unit_ms(self):
+        return self.unit_ns / max(self.steps, 1) * 1e-6
+
+    def launches(self, fam):
+        return sum(1 for i in range(len(self.family)) if self.family[i] == fam and self.launch_of[i] == i
+                   and self.eng.lw.units[i]["kind"] == 2)
 
 
-def step_roofline(eng, batch, step_ms):
-    """SURVEY 8(d)'s whole-step figure: Σ over conv layers of max(FLOP / P,
-    BYTES / BW) against the measured (graph-replay) step time, with P the
-    3xTF32-effective rate the SURVEY defines (bf16/2/3) and, stricter, the
-    rate of the three-fp16-product scheme this build uses (bf16/3)."""
+def roofline(eng, plan, batch, ts: TimelineStats, ms_per_step, config):
+    """The dominant kernel family (largest share of the device-timed step):
+    achieved = its algorithmic FLOPs (or bytes) per step / its graph-replay
+    time per step (timeline union), against the fp32-accurate tensor rate of
+    that kernel (three fp16 products at the dense fp16 = bf16 rate for the
+    fp16x2 kernels: bf16/3; 3xTF32: bf16/6) or HBM bandwidth, whichever the
+    per-layer roofline max(F/P, B/BW) says binds.  Also the SURVEY 8(d) step
+    figure sum_l max(F_l/P, B_l/BW) / ms_per_step."""
     hbm, bf16, _, basis = peaks()
-    out = {}
-    for key, P in (("p_tc_3xtf32", bf16 / 6.0), ("p_tc_fp16x2", bf16 / 3.0)):
-        t = 0.0
-        for u in eng.lw.units:
-            if u.get("kind") == 2:
-                f, b = unit_cost(eng.lw, u, batch)
-                t += max(f / (P * 1e12), b / (hbm * 1e9))
-        out[key] = {"p_tflops": round(P, 2), "roofline_time_us": round(t * 1e6, 1),
-                    "frac": round(t * 1e3 / step_ms, 4)}
-    out["basis"] = f"{basis}; measured step {step_ms:.4f} ms (graph replay, L2 flushed)"
-    return out
-
-
-def roofline(eng, batch, unit_ms, plan, config):
-    """Roofline of the dominant kernel (the conv kernel with the largest share
-    of the step), over all its launches in one step: achieved = algorithmic
-    FLOPs (or bytes) / its CUDA-event time.  P is the fp32-accurate tensor
-    rate of that kernel: three fp16 products at the dense fp16 (= bf16) rate
-    for the fp16x2 kernels (impl 3, 5), three TF32 passes (TF32 = bf16 / 2)
-    for the 3xTF32 kernel.  Per unit: time at the roofline = max(flops / P,
-    bytes / BW)."""
-    hbm, bf16, bf16s, basis = peaks()
     rate = {3: bf16 / 3.0, 5: bf16 / 3.0, 2: bf16 / 6.0, 1: bf16 / 6.0}
     lw = eng.lw
-    groups = {}
-    T = Troof = 0.0
+    fam_ms = ts.family_ms()
+    dom = max(fam_ms, key=fam_ms.get)
+    F = B = t_tensor = t_hbm = 0.0
+    step_roof = 0.0
+    per_layer = []
     for i, u in enumerate(lw.units):
         if u.get("kind") != 2:
             continue
-        f, b = unit_cost(lw, u, batch)
-        t = unit_ms[i] * 1e-3
         impl = plan.unit_impl(i)
-        g = groups.setdefault(impl, [0.0, 0.0, 0.0, 0])
-        g[0] += f; g[1] += b; g[2] += t; g[3] += 1
-        T += t
-        Troof += max(f / (rate[impl] * 1e12), b / (hbm * 1e9))
-    total = float(np.sum(unit_ms)) * 1e-3
-    impl = max(groups, key=lambda k: groups[k][2])
-    F, B, Tk, n = groups[impl]
-    P = rate[impl]
-    bound = "tensor" if F / (P * 1e12) >= B / (hbm * 1e9) else "hbm"
+        f, b = unit_cost(eng, i, batch)
+        tl = max(f / (rate[impl] * 1e12), b / (hbm * 1e9))
+        step_roof += tl
+        if ts.family[i] == dom:
+            F += f
+            B += b
+            t_tensor += f / (rate[impl] * 1e12)
+            t_hbm += b / (hbm * 1e9)
+        per_layer.append(round(tl * 1e6, 2))
+    Tk = fam_ms[dom] * 1e-3
+    P = rate[5] if "fp16x2" in dom else rate[2]
+    bound = "tensor" if t_tensor >= t_hbm else "hbm"
     if bound == "tensor":
         achieved, peak, unit = F / Tk / 1e12, P, "TFLOP/s"
     else:
         achieved, peak, unit = B / Tk / 1e9, hbm, "GB/s"
-    name = KERNEL_NAMES[impl]
+    n = ts.launches(dom)
+    ncu = measured_ncu(config)
     return {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": unit,
-            "frac": round(achieved / peak, 4), "traffic": measured_traffic(config, name),
-            "kernel": f"{name}: {n} launches/step, {100 * Tk / total:.1f}% of the step",
-            "algorithmic_per_launch": {"flops": F / n, "bytes": B / n},
+            "frac": round(achieved / peak, 4),
+            "traffic": (ncu or {}).get("dram_bytes_per_launch"),
+            "kernel": dom, "launches_per_step": n,
+            "kernel_ms_per_step": round(fam_ms[dom], 4),
+            "share_of_step": round(fam_ms[dom] / ms_per_step, 4),
+            "frac_tensor": round(F / Tk / 1e12 / P, 4), "frac_hbm": round(B / Tk / 1e9 / hbm, 4),
+            "algorithmic_per_launch": {"flops": F / max(n, 1), "bytes": B / max(n, 1)},
+            "timing": "device timeline of every timed graph replay (pcnn_plan_timeline), union of the "
+                      "family's launch intervals per step",
             "peak_basis": f"{basis} bf16_tflops {bf16} (tensor: /3 for fp16x2, /6 for 3xTF32); hbm_gbs {hbm}",
-            "all_conv_roofline_time_frac": round(Troof / T, 4) if T else None,
-            "conv_share_of_step": round(T / total, 4) if total else None}
+            "ncu": ncu,
+            "step": {"roofline_time_us": round(step_roof * 1e6, 1), "frac": round(step_roof * 1e3 / ms_per_step, 4),
+                     "formula": "sum over conv layers of max(FLOP/P_kernel, bytes/BW) / measured ms_per_step"},
+            "families_ms_per_step": {k: round(v, 4) for k, v in sorted(fam_ms.items(), key=lambda kv: -kv[1])}}
+
+
+def measured_ncu(config):
+    """ncu evidence for the dominant kernel from the committed capture
+    summary (profiles/ncu_summary.json, tools/summarize_profiles.py)."""
+    path = ROOT / "profiles" / "ncu_summary.json"
+    try:
+        return json.loads(path.read_text()).get(config)
+    except (OSError, ValueError):
+        return None
 
 
 # ---------------------------------------------------------------------------
@@ -376,35 +432,44 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def run_ours(args):
+def parity_of(gr, x_host, y):
+    """Max relative error of the timed batch's logits against the float64
+    oracle forward of the same (redistributed) graph, every image, over the
+    host cores (oracle/pool.py) -- the checker, not the measured path."""
+    from oracle.pool import OraclePool
+    t0 = time.perf_counter()
+    with OraclePool(gr) as pool:
+        want = pool.eval(x_host)
+    y = y.reshape(want.shape).astype(np.float64)
+    err = float(np.max(np.abs(y - want)) / max(float(np.max(np.abs(want))), 1e-30))
+    cy, cw = y - y.mean(0), want - want.mean(0)
+    cerr = float(np.max(np.abs(cy - cw)) / max(float(np.max(np.abs(cw))), 1e-30))
+    close = bool(np.allclose(y, want, rtol=1e-4, atol=1e-5))
+    return {"max_rel_err": err, "centred_rel_err": cerr, "allclose_rtol1e-4_atol1e-5": close,
+            "images": int(len(x_host)), "argmax_agree": float(np.mean(np.argmax(y, 1) == np.argmax(want, 1))),
+            "vs": "float64 oracle reference_eval restatement of the redistributed graph, every image of the "
+                  "timed batch", "oracle_s": round(time.perf_counter() - t0, 2)}
+
+
+def measure(name, args, rank, world, local, flush, options, e2e=True):
+    """Time one config's redistributed forward; returns the pieces of a line."""
     import torch
-    from paper_2509_22857_b200 import replicas
-    rank, world, local = dist_env()
-    if world > 1:
-        replicas.init_replicas("nccl")  # replicas only: the group carries the barrier and max-over-ranks
-    else:
-        torch.cuda.set_device(0)
-    from paper_2509_22857_b200 import configs
-    from paper_2509_22857_b200._lib import require_device
-    require_device()
-    cfg = configs.CONFIGS[args.config]
-    batch = args.batch or cfg.batch
-    g = build_model(args.config)
-    eng, gr, redist_info = redistributed_engine(g, cfg)
+    from paper_2509_22857_b200 import configs, replicas
+    cfg = configs.CONFIGS[name]
+    batch = (args.batch or cfg.batch) if name == args.config else cfg.batch
+    g = build_model(name)
+    eng, gr, redist_info = redistributed_engine(g, cfg, options)
     x_host = configs.make_input(cfg, batch=batch, seed=2 + rank).astype(np.float32)
     x = torch.from_numpy(x_host).cuda()
     out = torch.empty(eng.out_shape(batch), dtype=torch.float32, device="cuda")
-    flush_buf = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
-
-    def flush():
-        flush_buf.fill_(1.0)
-
     stream = torch.cuda.current_stream()
     # one checked forward: if an activation overflows the fp16 split format the
     # engine reruns it in float32 and rescales those tensors (Engine.recalibrate)
     eng.forward(x, out)
     for _ in range(max(args.warmup, 3)):
         eng.forward(x, out, check=False)
+    plan = eng.plan(batch)
+    ts = TimelineStats(eng, plan)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -424,6 +489,8 @@ def run_ours(args):
             starts[i].record(stream)
             eng.forward(x, out, check=False)
             ends[i].record(stream)
+            # the step's launch timeline (D2H after its end event; not timed)
+            ts.add(plan.timeline())
         torch.cuda.synchronize()
         t_end = time.perf_counter() + 0.3
         while time.perf_counter() < t_end:
@@ -434,7 +501,14 @@ def run_ours(args):
         torch.distributed.barrier()
     ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
     ms = replicas.max_over_ranks(ms)
-    value = world * batch * args.steps / (ms * 1e-3)
+    res = {"name": name, "cfg": cfg, "batch": batch, "g": g, "gr": gr, "eng": eng, "plan": plan, "ts": ts,
+           "x_host": x_host, "out": out, "ms": ms, "clocks": clocks.summary(), "redist_info": redist_info,
+           "value": world * batch * args.steps / (ms * 1e-3)}
+    # fp16x2 fast path valid only if no split-format activation left the fp16 range
+    assert plan.status() == 0, "fp16 range overflow: result needs the fp32 rerun"
+    assert np.all(np.isfinite(out.cpu().numpy())), "non-finite logits"
+    if not e2e:
+        return res
 
     # e2e through the C ABI with pinned host buffers
     xh = torch.from_numpy(x_host).pin_memory()
@@ -444,7 +518,6 @@ def run_ours(args):
     from paper_2509_22857_b200 import _lib as L
     import ctypes
     from paper_2509_22857_b200.runtime import _stream_handle
-    plan = eng.plan(batch)
 
     def e2e_step():
         L.check(L.lib().pcnn_forward_host(plan.handle, ctypes.c_void_p(xh.data_ptr()), ctypes.c_void_p(oh.data_ptr()),
@@ -464,7 +537,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         e_ms += s0.elapsed_time(s1)
     e_ms = replicas.max_over_ranks(e_ms)
-    e2e_serial = world * batch * args.steps / (e_ms * 1e-3)
+    res["e2e_serial"] = world * batch * args.steps / (e_ms * 1e-3)
 
     # e2e, pipelined: the same K steps through Engine.forward_host_many
     # (pcnn_forward_host_many) -- every step still copies its input in and
@@ -480,52 +553,125 @@ def run_ours(args):
     eng.forward_host_many([xh] * args.steps, outs_h, staging=staging, sync=False)
     p1.record(stream)
     torch.cuda.synchronize()
-    p_ms = p0.elapsed_time(p1)
-    p_ms = replicas.max_over_ranks(p_ms)
-    e2e_value = world * batch * args.steps / (p_ms * 1e-3)
+    p_ms = replicas.max_over_ranks(p0.elapsed_time(p1))
+    res["e2e"] = world * batch * args.steps / (p_ms * 1e-3)
+    ref = out.cpu().numpy()
     for o in outs_h:
-        np.testing.assert_allclose(o.numpy(), out.cpu().numpy(), rtol=1e-5, atol=1e-6)
+        np.testing.assert_allclose(o.numpy(), ref, rtol=1e-5, atol=1e-6)
     # fused global pools reduce with float atomics, so repeated runs agree to rounding only
-    np.testing.assert_allclose(oh.numpy(), out.cpu().numpy(), rtol=1e-5, atol=1e-6)
-    # the fp16x2 fast path is only valid if no split-format activation left the
-    # fp16 range (the status word libpcnn copies back with the logits)
-    assert plan.status() == 0 and plan.last_status() == 0, "fp16 range overflow: result needs the fp32 rerun"
-    assert np.all(np.isfinite(oh.numpy())), "non-finite logits"
+    np.testing.assert_allclose(oh.numpy(), ref, rtol=1e-5, atol=1e-6)
+    assert plan.last_status() == 0, "fp16 range overflow: result needs the fp32 rerun"
     any_split = any(plan.tensor_split(t) for t in range(len(eng.lw.tensors)))
+    res["h2d"] = int(xh.numel() * 4)
+    res["d2h"] = int(oh.numel() * 4) + (4 if any_split else 0)
+    return res
 
+
+def record(res, args, world):
+    """The per-config fields of the JSON line."""
+    eng, plan, batch, ms = res["eng"], res["plan"], res["batch"], res["ms"]
+    ms_step = ms / args.steps
+    roof = roofline(eng, plan, batch, res["ts"], ms_step, res["name"])
+    cfg = res["cfg"]
+    rec = {"value": round(res["value"], 2), "ms_per_step": round(ms_step, 4),
+           "config": {"workload": f"{res['name']}_b{batch}_redistributed_forward", "model": res["name"],
+                      "global_batch": batch * world, "input": "x".join(map(str, cfg.input_shape)),
+                      "parallelism": f"replicas{world}", "l2": "flushed (256 MiB write) between timed steps",
+                      "redistribution": res["redist_info"],
+                      "conv_impl": sorted({plan.unit_impl(i) for i, u in enumerate(eng.lw.units)
+                                           if u.get("kind") == 2}),
+                      "split_tensors": sum(plan.tensor_split(t) > 0 for t in range(len(eng.lw.tensors)))},
+           "gpu_launches": plan.launches() * args.steps,
+           "roofline": roof, "clocks": res["clocks"],
+           "device_step_span_ms": round(float(np.median(res["ts"].span_ns)) * 1e-6, 4),
+           "unit_ms": [round(float(v), 4) for v in res["ts"].unit_ms()]}
+    if "e2e" in res:
+        rec["e2e"] = {"value": round(res["e2e"], 2), "unit": UNIT, "h2d_bytes_per_step": res["h2d"],
+                      "d2h_bytes_per_step": res["d2h"],
+                      "api": "Engine.forward_host_many -> pcnn_forward_host_many (pinned host batches, "
+                             "H2D of step i+1 overlapping step i; no L2 flush inside the pipeline)",
+                      "serial_value": round(res["e2e_serial"], 2),
+                      "serial_api": "pcnn_forward_host per step (H2D, forward, D2H, sync; L2 flushed between steps)"}
+    return rec
+
+
+def time_cpu_redistribution(g, cfg, budget_s=2.0):
+    """The oracle port of the reference's per-donor sweeps (transforms.py:
+    423-485, float64 on one host core) for the same config: ms per call."""
+    from oracle import levnet_oracle as O
+    times = []
+    t_end = time.perf_counter() + budget_s
+    while not times or (time.perf_counter() < t_end and len(times) < 20):
+        t0 = time.perf_counter()
+        cur = g
+        for d in cfg.redistribution:
+            cur, _, _ = O.redistribute_sweep(cur, d, allow_negative_leading=cfg.allow_negative_leading)
+        times.append(time.perf_counter() - t0)
+    return 1e3 * float(np.median(times)), len(times)
+
+
+def run_ours(args):
+    import torch
+    from paper_2509_22857_b200 import replicas
+    from paper_2509_22857_b200 import _lib as L
+    rank, world, local = dist_env()
+    if world > 1:
+        replicas.init_replicas("nccl")  # replicas only: the group carries the barrier and max-over-ranks
+    else:
+        torch.cuda.set_device(0)
+    from paper_2509_22857_b200 import configs
+    L.require_device()
+    # default plan options; PCNN_* developer variables (tools/, profiling) are
+    # applied here explicitly and recorded in the line when they change anything
+    options = L.options_from_env()
+    flush_buf = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+
+    def flush():
+        flush_buf.fill_(1.0)
+
+    main = measure(args.config, args, rank, world, local, flush, options)
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
         return
-    unit_ms = per_unit_times(eng, x, out, reps=max(3, min(args.steps, 10)), flush=flush)
-    roof = roofline(eng, batch, unit_ms, plan, args.config)
-    roof["step"] = step_roofline(eng, batch, ms / args.steps)
-    launches = plan.launches()
-    line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-            "config": {"workload": f"{args.config}_b{batch}_redistributed_forward", "model": args.config,
-                       "global_batch": batch * world, "input": "x".join(map(str, cfg.input_shape)),
-                       "parallelism": f"replicas{world}", "l2": "flushed (256 MiB write) between timed steps",
-                       "redistribution": redist_info,
-                       "conv_impl": sorted({plan.unit_impl(i) for i, u in enumerate(eng.lw.units)
-                                            if u.get("kind") == 2}),
-                       "split_tensors": sum(plan.tensor_split(t) > 0 for t in range(len(eng.lw.tensors)))},
-            "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": int(xh.numel() * 4),
-                    "d2h_bytes_per_step": int(oh.numel() * 4) + (4 if any_split else 0),
-                    "api": "Engine.forward_host_many -> pcnn_forward_host_many (pinned host batches, "
-                           "H2D of step i+1 overlapping step i; no L2 flush inside the pipeline)",
-                    "serial_value": round(e2e_serial, 2),
-                    "serial_api": "pcnn_forward_host per step (H2D, forward, D2H, sync; L2 flushed between steps)"},
-            "gpu_launches": launches * args.steps,
-            "roofline": roof,
-            "clocks": clocks.summary(),
-            "unit_ms": [round(float(v), 4) for v in unit_ms]}
+    rec = record(main, args, world)
+    line = {"metric": METRIC, "value": rec["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": rec["ms_per_step"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic"}
+    line.update({k: v for k, v in rec.items() if k not in ("value", "ms_per_step")})
+    default = L.PlanOptions.default().as_dict()
+    changed = {k: v for k, v in options.as_dict().items() if default.get(k) != v}
+    if changed:
+        line["config"]["plan_options"] = changed
+    if not args.no_parity:
+        line["parity"] = parity_of(main["gr"], main["x_host"], main["out"].cpu().numpy())
+    cfg = main["cfg"]
     # (before the CPU baseline: its worker processes would load the host
     # thread that drives the wall-clock timing)
     if not args.no_redist_timing:
-        line["redistribution"] = time_redistribution(g, cfg)
+        red = time_redistribution(main["g"], cfg)
+        cpu_ms, n = time_cpu_redistribution(main["g"], cfg)
+        red["cpu_reference_ms_per_call"] = round(cpu_ms, 3)
+        red["cpu_reference"] = (f"oracle port of levnet redistribute_{'/'.join(cfg.redistribution)} per-donor "
+                                f"sweep (transforms.py:423-485), float64, 1 host core, median of {n}")
+        line["redistribution"] = red
+    secondary = [c for c in args.secondary.split(",") if c and c != args.config] if world == 1 else []
+    if secondary:
+        line["secondary"] = {}
+        del main
+        torch.cuda.empty_cache()
+        for name in secondary:
+            res = measure(name, args, rank, world, local, flush, options, e2e=True)
+            sub = record(res, args, world)
+            sub["metric"] = METRIC
+            sub["unit"] = UNIT
+            if not args.no_parity:
+                sub["parity"] = parity_of(res["gr"], res["x_host"], res["out"].cpu().numpy())
+            line["secondary"][name] = sub
+            del res
+            torch.cuda.empty_cache()
     if not args.no_cpu and world == 1:
+        g = build_model(args.config)
         ips, done, el, procs = cpu_reference(g, configs.make_input(cfg, batch=64), args.cpu_seconds)
         line["cpu_baseline"] = {"value": round(ips, 3), "unit": UNIT, "cores": procs, "kind": "port",
                                 "sample": f"{done} images in {el:.1f} s, float64 oracle reference_eval "
@@ -546,6 +692,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-redist-timing", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--secondary", default="resnet18",
+                    help="comma-separated configs measured after the main one (1 GPU), reported under 'secondary'")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define PCNN_ABI_VERSION 2
+#define PCNN_ABI_VERSION 3
 
 enum pcnn_status {
   PCNN_OK = 0,
@@ -207,6 +207,46 @@ typedef struct pcnn_rewrite_desc {
 /* status_dev (device, int64[4]) receives {first error code, op index, 0, 0};
  * flags_dev (device, int64[n_flags]) receives CHECK_ALLONE results.        */
 
+/* ---- plan options ----------------------------------------------------------
+ * Every tuning / diagnostic switch of a plan.  The library reads no
+ * environment variables: a plan's behaviour is fixed by its descriptors and
+ * these options.  pcnn_plan_options_default() fills the defaults (the
+ * configuration the benchmarks run); pcnn_plan_create() uses them.        */
+typedef struct pcnn_plan_options {
+  int64_t size;             /* sizeof(pcnn_plan_options), set by _default  */
+  int64_t split;            /* 1: split fp16 hi/lo tensors between fp16x2
+                               tensor-core convs; 0: every tensor float32  */
+  int64_t halo_tiles;       /* 1: halo-tile conv kernel where the shape
+                               allows; 0: the TMEM-A kernel only           */
+  int64_t fuse_projection;  /* 1: a block's 1x1 projection inside its 3x3
+                               conv's launch                               */
+  int64_t fuse_block;       /* 1: a residual block's two 3x3 convs in one
+                               launch (halo recompute) where it fits       */
+  int64_t streamk;          /* 1: stream-K for launches whose whole tiles
+                               fill < streamk_fill of the SMs              */
+  double streamk_fill;      /* default 0.3                                 */
+  int64_t flag_sync;        /* 1: per-tile completion counters instead of
+                               whole-grid ordering (experimental, off)     */
+  int64_t prezero;          /* 1: a halo-tile conv zeroes the next unit's
+                               global-pool sums in its prologue            */
+  int64_t linear_out;       /* 1: the last linear writes the logits        */
+  int64_t pdl;              /* 1: programmatic dependent launches          */
+  int64_t graph;            /* 1: pcnn_forward replays a CUDA graph when
+                               use_graph is set; 0: always eager           */
+  int64_t ss_mt;            /* halo-tile 128-row sub-tiles per tile, 0 auto*/
+  int64_t ss_share;         /* both epilogue warpgroups per tile: -1 auto  */
+  int64_t ss_psub;          /* one parity plane per stage: -1 auto         */
+  int64_t ss_wres;          /* 1: resident weights where they fit          */
+  int64_t tc_stage;         /* 1: TMA-staged input boxes (TMEM-A kernel)   */
+  int64_t timeline;         /* 1: every launch stamps %globaltimer at its
+                               first CTA's start and last CTA's exit
+                               (pcnn_plan_timeline)                        */
+  int64_t debug;            /* diagnostic bits (tests / tools only):
+                               2 skip MMAs, 4 skip epilogues, 32 CTA-0
+                               trace, 64 per-CTA stamps                    */
+  int64_t reserved[8];
+} pcnn_plan_options;
+
 /* ---- entry points --------------------------------------------------------*/
 typedef struct pcnn_plan pcnn_plan;
 
@@ -215,6 +255,8 @@ const char* pcnn_last_error(void);
 /* 1 if a device of compute capability 10.x is visible, else 0 */
 int pcnn_device_ok(void);
 
+void pcnn_plan_options_default(pcnn_plan_options* opt);
+
 size_t pcnn_workspace_bytes(const pcnn_tensor_desc* tensors, int n_tensors, int batch);
 
 int pcnn_plan_create(const pcnn_unit_desc* units, int n_units,
@@ -222,6 +264,20 @@ int pcnn_plan_create(const pcnn_unit_desc* units, int n_units,
                      int batch, int input_tensor, int output_tensor,
                      const float* params, void* workspace, size_t ws_bytes,
                      pcnn_plan** plan_out);
+/* same with explicit options (null = defaults) */
+int pcnn_plan_create_ex(const pcnn_unit_desc* units, int n_units,
+                        const pcnn_tensor_desc* tensors, int n_tensors,
+                        int batch, int input_tensor, int output_tensor,
+                        const float* params, void* workspace, size_t ws_bytes,
+                        const pcnn_plan_options* opt, pcnn_plan** plan_out);
+/* Device timeline of the last forward (options.timeline): for each unit u,
+ * ns[2u] = %globaltimer when its launch's first CTA passed its dependency
+ * wait, ns[2u + 1] = when its last CTA exited; both 0 for a unit that ran
+ * inside another unit's launch (fused) or launched nothing.  Synchronises
+ * `stream`.  Returns the number of units written (<= max_units).          */
+int pcnn_plan_timeline(pcnn_plan* plan, int64_t* ns, int max_units, void* stream);
+/* the unit whose launch computes unit u (u itself unless fused) */
+int pcnn_plan_unit_launch(const pcnn_plan* plan, int unit);
 int pcnn_plan_destroy(pcnn_plan* plan);
 /* number of kernel launches one forward issues (for gpu_launches) */
 int pcnn_plan_num_launches(const pcnn_plan* plan);

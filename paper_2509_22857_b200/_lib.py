@@ -40,7 +40,7 @@ IMPL_AUTO, IMPL_SIMT, IMPL_TF32, IMPL_F16X2, IMPL_FP32_TENSORS, IMPL_F16X2_SS = 
  OP_SQRT, OP_STORE) = range(1, 18)
 
 MAX_FACTORS = 6
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 
 class PcnnError(RuntimeError):
@@ -86,6 +86,53 @@ class RewriteDesc(ctypes.Structure):
                [("value", c_f64), ("f", Factor * MAX_FACTORS)]
 
 
+_OPT_INT_FIELDS_A = ("size", "split", "halo_tiles", "fuse_projection", "fuse_block", "streamk")
+_OPT_INT_FIELDS_B = ("flag_sync", "prezero", "linear_out", "pdl", "graph", "ss_mt", "ss_share", "ss_psub",
+                     "ss_wres", "tc_stage", "timeline", "debug")
+
+
+class PlanOptions(ctypes.Structure):
+    """pcnn_plan_options: every tuning / diagnostic switch of a plan (the
+    library reads no environment variables)."""
+    _fields_ = [(n, c_i64) for n in _OPT_INT_FIELDS_A] + [("streamk_fill", c_f64)] + \
+               [(n, c_i64) for n in _OPT_INT_FIELDS_B] + [("reserved", c_i64 * 8)]
+
+    @classmethod
+    def default(cls, **overrides) -> "PlanOptions":
+        o = cls()
+        lib().pcnn_plan_options_default(ctypes.byref(o))
+        for k, v in overrides.items():
+            if k not in dict(cls._fields_):
+                raise KeyError(f"unknown plan option {k!r}")
+            setattr(o, k, v)
+        return o
+
+    def as_dict(self) -> dict:
+        return {n: getattr(self, n) for n, _ in self._fields_ if n != "reserved"}
+
+
+# Developer / tooling switches (tools/*.py): environment variable -> option.
+# Only these helpers read the environment; Engine() uses explicit options.
+ENV_OPTIONS = {
+    "PCNN_NO_SPLIT": ("split", 0), "PCNN_NO_SS": ("halo_tiles", 0), "PCNN_NO_PROJ_FUSE": ("fuse_projection", 0),
+    "PCNN_NO_BLOCK_FUSE": ("fuse_block", 0), "PCNN_NO_STREAMK": ("streamk", 0), "PCNN_FLAGS": ("flag_sync", int),
+    "PCNN_NO_PREZERO": ("prezero", 0), "PCNN_NO_LINEAR_OUT": ("linear_out", 0), "PCNN_NO_PDL": ("pdl", 0),
+    "PCNN_NO_GRAPH": ("graph", 0), "PCNN_SS_MT": ("ss_mt", int), "PCNN_SS_SHARE": ("ss_share", int),
+    "PCNN_SS_PSUB": ("ss_psub", int), "PCNN_SS_WRES": ("ss_wres", int), "PCNN_TC_NOSTAGE": ("tc_stage", 0),
+    "PCNN_TC_DEBUG": ("debug", int), "PCNN_STREAMK_FILL": ("streamk_fill", float),
+}
+
+
+def options_from_env(**overrides) -> "PlanOptions":
+    """Defaults, then the PCNN_* developer variables of ENV_OPTIONS, then overrides."""
+    kw = {}
+    for var, (field, val) in ENV_OPTIONS.items():
+        if var in os.environ:
+            kw[field] = val(os.environ[var]) if callable(val) else val
+    kw.update(overrides)
+    return PlanOptions.default(**kw)
+
+
 _lib: Optional[ctypes.CDLL] = None
 
 SYMBOLS = {
@@ -96,6 +143,12 @@ SYMBOLS = {
     "pcnn_plan_create": ([ctypes.POINTER(UnitDesc), ctypes.c_int, ctypes.POINTER(TensorDesc), ctypes.c_int,
                           ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                           ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "pcnn_plan_create_ex": ([ctypes.POINTER(UnitDesc), ctypes.c_int, ctypes.POINTER(TensorDesc), ctypes.c_int,
+                             ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                             ctypes.c_size_t, ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "pcnn_plan_options_default": ([ctypes.c_void_p], None),
+    "pcnn_plan_timeline": ([ctypes.c_void_p, ctypes.POINTER(c_i64), ctypes.c_int, ctypes.c_void_p], ctypes.c_int),
+    "pcnn_plan_unit_launch": ([ctypes.c_void_p, ctypes.c_int], ctypes.c_int),
     "pcnn_plan_destroy": ([ctypes.c_void_p], ctypes.c_int),
     "pcnn_plan_num_launches": ([ctypes.c_void_p], ctypes.c_int),
     "pcnn_plan_unit_impl": ([ctypes.c_void_p, ctypes.c_int], ctypes.c_int),

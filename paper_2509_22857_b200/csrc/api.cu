@@ -22,6 +22,19 @@ using namespace pcnn;
 
 namespace {
 
+// Per-forward reset of a plan's small device state (status word, stream-K
+// and flag counters, launch timeline) in ONE kernel node instead of a
+// memset node per buffer.
+struct ResetRanges {
+  uint32_t* p[4];
+  int64_t n[4];  // 32-bit words
+};
+__global__ void plan_reset_kernel(ResetRanges r) {
+  for (int k = 0; k < 4; ++k)
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r.n[k]; i += (int64_t)gridDim.x * blockDim.x)
+      r.p[k][i] = 0u;
+}
+
 thread_local std::string g_last_error;
 
 int fail(int code, const std::string& msg) {
@@ -61,10 +74,11 @@ struct pcnn_plan {
   bool any_split = false;
   int* status_dev = nullptr;   // bit 0: a split-format value left the fp16 range
   int* status_host = nullptr;  // pinned copy written by pcnn_forward_host
-  // halo-tile conv units run as chains (one persistent launch per run of
-  // consecutive units): chain_of[u] = chain index or -1
-  std::vector<SsChain*> chains;
-  std::vector<int> chain_of, chain_first, chain_len;
+  pcnn_plan_options opt;
+  KOpts kopt;
+  // launch timeline (options.timeline): [n_units][2] (common.cuh tl_mark)
+  unsigned long long* tl_dev = nullptr;
+  unsigned long long* tl_host = nullptr;
   // flag-synchronised halo-tile launches (build_flags): per-tile completion
   // counters of every signalling unit, zeroed at the start of each forward
   bool flags_on = false;
@@ -135,12 +149,12 @@ void choose_formats(pcnn_plan* p) {
       ++inputs[u.in];
       if (!tc16) ok[u.in] = 0;
       const bool ss2 = tc16 && u.stride == 2 && (u.impl == 0 || u.impl == 3 || u.impl == 5) &&
-                       !getenv("PCNN_NO_SS") && conv_ss_shape_ok(p->conv_args[i]);
+                       p->opt.halo_tiles && conv_ss_shape_ok(p->conv_args[i]);
       if (!ss2) s2_only[u.in] = 0;
     }
     if (u.in2 >= 0 && !(tc16 && u.residual)) ok[u.in2] = 0;
   }
-  if (getenv("PCNN_NO_SPLIT")) ok.assign(nt, 0);
+  if (!p->opt.split) ok.assign(nt, 0);
   for (int t = 0; t < nt; ++t) {
     TensorView& v = p->views[t];
     if (!ok[t] || !produced[t] || v.is_vector || t == p->output) continue;
@@ -175,69 +189,9 @@ void choose_formats(pcnn_plan* p) {
     if (u.residual) a.epi.skip = p->views[u.in2];
     // fp16x2 convs reading a split tensor: the halo-tile kernel when the
     // shape allows (unit impl 0, 3 or 5)
-    if (p->impl[i] == 3 && (u.impl == 0 || u.impl == 3 || u.impl == 5) && !getenv("PCNN_NO_SS") &&
+    if (p->impl[i] == 3 && (u.impl == 0 || u.impl == 3 || u.impl == 5) && p->opt.halo_tiles &&
         conv_ss_supported(a))
       p->impl[i] = 5;
-  }
-}
-
-// Experimental, opt-in (PCNN_CHAIN=1): runs of consecutive halo-tile units
-// become one persistent launch each.  Measured slower than separate PDL
-// launches on RN20/RN18, so plans default to one
-// launch per unit.  A layer depends on the chain layers
-// that write its input and residual: on the tiles covering its position range
-// when both are stride-1 convs over the same shared-border grid, else on all
-// their tiles.  Runs that cannot share a launch are shortened.
-void build_chains(pcnn_plan* p) {
-  const int n = (int)p->units.size();
-  p->chain_of.assign(n, -1);
-  if (!getenv("PCNN_CHAIN")) return;
-  std::vector<int> producer(p->tensors.size(), -1);
-  for (int i = 0; i < n; ++i)
-    if (p->units[i].out >= 0) producer[p->units[i].out] = i;
-  int i = 0;
-  while (i < n) {
-    if (p->impl[i] != 5) { ++i; continue; }
-    int j = i + 1;
-    static const int cap = getenv("PCNN_CHAIN_MAX") ? atoi(getenv("PCNN_CHAIN_MAX")) : 22;
-    while (j < n && p->impl[j] == 5 && j - i < cap) ++j;
-    int end = j;
-    static const int lo = getenv("PCNN_CHAIN_SINGLE") ? 0 : 1;  // debugging: one-layer chains
-    for (; end > i + lo; --end) {
-      const int m = end - i;
-      std::vector<ConvArgs> args(m);
-      std::vector<int> din(m), dinm(m), dsk(m), dskm(m);
-      for (int k = 0; k < m; ++k) {
-        const pcnn_unit_desc& u = p->units[i + k];
-        args[k] = p->conv_args[i + k];
-        auto dep = [&](int64_t t, int& d, int& mode) {
-          d = -1;
-          mode = 0;
-          if (t < 0) return;
-          const int q = producer[t];
-          if (q < i || q >= i + k) return;  // written before the launch
-          d = q - i;
-          mode = (u.stride == 1 && p->units[q].stride == 1 && p->views[t].split == 1) ? 1 : 2;
-        };
-        dep(u.in, din[k], dinm[k]);
-        if (u.residual) {
-          dep(u.in2, dsk[k], dskm[k]);
-        } else {
-          dsk[k] = -1;
-          dskm[k] = 0;
-        }
-      }
-      SsChain* c = ss_chain_create(args.data(), m, din.data(), dinm.data(), dsk.data(), dskm.data());
-      if (c) {
-        const int id = (int)p->chains.size();
-        p->chains.push_back(c);
-        p->chain_first.push_back(i);
-        p->chain_len.push_back(m);
-        for (int k = i; k < end; ++k) p->chain_of[k] = id;
-        break;
-      }
-    }
-    i = end > i ? end : i + 1;  // a single unit keeps the one-layer kernel
   }
 }
 
@@ -304,34 +258,23 @@ int build_conv(pcnn_plan* p, int ui, ConvArgs& a) {
 
 void enqueue_unit(pcnn_plan* p, int ui, const float* x, float* logits, cudaStream_t s, bool flags) {
   const pcnn_unit_desc& u = p->units[ui];
+  unsigned long long* tl = p->tl_dev ? p->tl_dev + 2 * ui : nullptr;
   switch (u.kind) {
     case PCNN_UNIT_INGEST:
-      launch_ingest(x, p->views[u.out], p->batch, (u.flags & PCNN_FLAG_S2D) != 0, s);
+      launch_ingest(x, p->views[u.out], p->batch, (u.flags & PCNN_FLAG_S2D) != 0, s, tl);
       break;
     case PCNN_UNIT_CONV: {
-      const ConvArgs& a = p->conv_args[ui];
-      const bool chained = p->impl[ui] == 5 && p->chain_of[ui] >= 0;
-      if (chained && p->chain_first[p->chain_of[ui]] != ui) break;  // launched with its chain's first unit
       if (p->fused[ui]) break;  // computed by the previous unit's launch
+      ConvArgs a = p->conv_args[ui];
+      a.tl = tl;
       if (u.pool == PCNN_POOL_GLOBAL && !p->prezeroed[ui])
         cudaMemsetAsync(a.epi.out.base, 0, sizeof(float) * (size_t)p->batch * a.epi.out.cpad(), s);
-      if (chained) {
-        const int c = p->chain_of[ui];
-        // every global-pool output of the chain is zeroed before its launch
-        for (int j = ui + 1; j < ui + p->chain_len[c]; ++j) {
-          const pcnn_unit_desc& uj = p->units[j];
-          if (uj.pool == PCNN_POOL_GLOBAL) {
-            const ConvArgs& aj = p->conv_args[j];
-            cudaMemsetAsync(aj.epi.out.base, 0, sizeof(float) * (size_t)p->batch * aj.epi.out.cpad(), s);
-          }
-        }
-        ss_chain_launch(p->chains[c], s);
-      } else if (p->impl[ui] == 5) {
+      if (p->impl[ui] == 5) {
         if (flags || !p->flags_on) {
           launch_conv_ss(a, s);
         } else {
           // a unit run on its own: plain griddepcontrol ordering, no counters
-          ConvArgs b = a;
+          ConvArgs& b = a;
           b.sig_done = nullptr;
           b.skip_gridwait = 0;
           b.fin = FlagDep();
@@ -360,12 +303,13 @@ void enqueue_unit(pcnn_plan* p, int ui, const float* x, float* logits, cudaStrea
       a.out = p->views[u.out].base;
       a.out_stride = p->views[u.out].cpad();
       if (ui + 1 < (int)p->fused.size() && p->fused[ui + 1]) a.out2 = logits;
+      a.tl = tl;
       launch_linear(a, s);
       break;
     }
     case PCNN_UNIT_COPYOUT: {
       if (p->fused[ui]) break;  // the linear unit before it wrote the logits
-      launch_copyout(p->views[u.in], logits, p->batch, s);
+      launch_copyout(p->views[u.in], logits, p->batch, s, tl);
       break;
     }
     default: {
@@ -383,6 +327,7 @@ void enqueue_unit(pcnn_plan* p, int ui, const float* x, float* logits, cudaStrea
       a.pad = (int)u.pad;
       a.axis = (int)u.pool_order;
       a.pool = (int)u.pool;
+      a.tl = tl;
       launch_eltwise(a, s);
       break;
     }
@@ -390,9 +335,13 @@ void enqueue_unit(pcnn_plan* p, int ui, const float* x, float* logits, cudaStrea
 }
 
 void enqueue_all(pcnn_plan* p, const float* x, float* logits, cudaStream_t s) {
-  if (p->any_split) cudaMemsetAsync(p->status_dev, 0, sizeof(int), s);
-  if (p->flags_on) cudaMemsetAsync(p->flags_dev, 0, sizeof(int) * p->flags_n, s);
-  if (p->sk_flags) cudaMemsetAsync(p->sk_flags, 0, sizeof(int) * p->sk_flags_n, s);
+  ResetRanges r = {};
+  int k = 0;
+  if (p->any_split) { r.p[k] = reinterpret_cast<uint32_t*>(p->status_dev); r.n[k++] = 1; }
+  if (p->flags_on) { r.p[k] = reinterpret_cast<uint32_t*>(p->flags_dev); r.n[k++] = (int64_t)p->flags_n; }
+  if (p->sk_flags) { r.p[k] = reinterpret_cast<uint32_t*>(p->sk_flags); r.n[k++] = (int64_t)p->sk_flags_n; }
+  if (p->tl_dev) { r.p[k] = reinterpret_cast<uint32_t*>(p->tl_dev); r.n[k++] = 4 * (int64_t)p->units.size(); }
+  if (k) plan_reset_kernel<<<1, 256, 0, s>>>(r);
   for (int i = 0; i < (int)p->units.size(); ++i) enqueue_unit(p, i, x, logits, s, true);
 }
 
@@ -408,7 +357,7 @@ void fuse_projections(pcnn_plan* p) {
   for (int i = 0; i + 1 < n; ++i) {
     const pcnn_unit_desc &u = p->units[i], &v = p->units[i + 1];
     if (u.kind != PCNN_UNIT_CONV || v.kind != PCNN_UNIT_CONV || p->impl[i] != 5 || p->impl[i + 1] != 5) continue;
-    if (p->chain_of[i] >= 0 || p->chain_of[i + 1] >= 0 || p->fused[i]) continue;
+    if (p->fused[i]) continue;
     if (v.in != u.in || v.kh != 1 || v.stride != u.stride || u.kh != 3) continue;
     if (p->prezeroed[i] || p->prezeroed[i + 1] || (i + 2 < n && p->prezeroed[i + 2])) continue;
     if (p->conv_args[i].prezero || p->conv_args[i + 1].prezero) continue;
@@ -423,7 +372,7 @@ void fuse_projections(pcnn_plan* p) {
     const pcnn_unit_desc &u = p->units[i], &v = p->units[i + 1];
     if (u.kind != PCNN_UNIT_LINEAR || v.kind != PCNN_UNIT_COPYOUT || v.in != u.out) continue;
     const TensorView& t = p->views[u.out];
-    if (!t.is_vector || t.c != (int)u.cout || getenv("PCNN_NO_LINEAR_OUT")) continue;
+    if (!t.is_vector || t.c != (int)u.cout || !p->opt.linear_out) continue;
     p->fused[i + 1] = 1;
     p->launches -= 1;
   }
@@ -445,7 +394,7 @@ void plan_streamk(pcnn_plan* p) {
   std::vector<int> want(n, 0);
   size_t slot_max = 0, nflags = 0;
   for (int i = 0; i < n; ++i) {
-    if (p->units[i].kind != PCNN_UNIT_CONV || p->impl[i] != 5 || p->chain_of[i] >= 0 || p->fused[i]) continue;
+    if (p->units[i].kind != PCNN_UNIT_CONV || p->impl[i] != 5 || p->fused[i]) continue;
     size_t slot = 0;
     if (!conv_ss_streamk_wanted(p->conv_args[i], nsm, &slot)) continue;
     want[i] = 1;
@@ -490,9 +439,8 @@ void plan_streamk(pcnn_plan* p) {
 // relaxed, i.e. unordered, signal: the overlap alone gains nothing).
 void build_flags(pcnn_plan* p) {
   p->flags_on = false;
-  const char* env = getenv("PCNN_FLAGS");
-  const char* dbg = getenv("PCNN_TC_DEBUG");  // bits 2 / 4 skip the MMAs / the epilogue (no signals)
-  if (!env || atoi(env) == 0 || (dbg && (atoi(dbg) & 6))) return;
+  // debug bits 2 / 4 skip the MMAs / the epilogue (no signals)
+  if (!p->opt.flag_sync || (p->opt.debug & 6)) return;
   const int n = (int)p->units.size();
   std::vector<int> producer(p->tensors.size(), -1);
   for (int i = 0; i < n; ++i)
@@ -502,7 +450,7 @@ void build_flags(pcnn_plan* p) {
   size_t total = 0;
   std::vector<size_t> off(n, 0);
   for (int i = 0; i < n; ++i) {
-    if (p->units[i].kind != PCNN_UNIT_CONV || p->impl[i] != 5 || p->chain_of[i] >= 0 || p->fused[i]) continue;
+    if (p->units[i].kind != PCNN_UNIT_CONV || p->impl[i] != 5 || p->fused[i]) continue;
     if (!conv_ss_flag_geometry(p->conv_args[i], geo[i])) continue;
     sig[i] = 1;
     off[i] = total;
@@ -583,15 +531,62 @@ size_t pcnn_workspace_bytes(const pcnn_tensor_desc* tensors, int n_tensors, int 
   return (size_t)end * sizeof(float);
 }
 
+void pcnn_plan_options_default(pcnn_plan_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->size = sizeof(*o);
+  o->split = 1;
+  o->halo_tiles = 1;
+  o->fuse_projection = 1;
+  o->fuse_block = 1;
+  o->streamk = 1;
+  o->streamk_fill = 0.3;
+  o->flag_sync = 0;
+  o->prezero = 1;
+  o->linear_out = 1;
+  o->pdl = 1;
+  o->graph = 1;
+  o->ss_mt = 0;
+  o->ss_share = -1;
+  o->ss_psub = -1;
+  o->ss_wres = 1;
+  o->tc_stage = 1;
+  o->timeline = 1;
+  o->debug = 0;
+}
+
 int pcnn_plan_create(const pcnn_unit_desc* units, int n_units, const pcnn_tensor_desc* tensors, int n_tensors,
                      int batch, int input_tensor, int output_tensor, const float* params, void* workspace,
                      size_t ws_bytes, pcnn_plan** plan_out) {
+  return pcnn_plan_create_ex(units, n_units, tensors, n_tensors, batch, input_tensor, output_tensor, params,
+                             workspace, ws_bytes, nullptr, plan_out);
+}
+
+int pcnn_plan_create_ex(const pcnn_unit_desc* units, int n_units, const pcnn_tensor_desc* tensors, int n_tensors,
+                        int batch, int input_tensor, int output_tensor, const float* params, void* workspace,
+                        size_t ws_bytes, const pcnn_plan_options* opt, pcnn_plan** plan_out) {
   if (!units || !tensors || n_units <= 0 || n_tensors <= 0 || batch <= 0 || !plan_out || !params || !workspace)
     return fail(PCNN_ERR_INVALID, "pcnn_plan_create: null or empty argument");
+  if (input_tensor < 0 || input_tensor >= n_tensors || output_tensor < 0 || output_tensor >= n_tensors)
+    return fail(PCNN_ERR_INVALID, "pcnn_plan_create: input / output tensor id out of range");
+  if (opt && opt->size != (int64_t)sizeof(pcnn_plan_options))
+    return fail(PCNN_ERR_INVALID, "pcnn_plan_create: options size mismatch (use pcnn_plan_options_default)");
   if (!pcnn_device_ok()) return fail(PCNN_ERR_NO_DEVICE, "no compute capability 10.x device");
   if (pcnn_workspace_bytes(tensors, n_tensors, batch) > ws_bytes)
     return fail(PCNN_ERR_INVALID, "workspace too small");
   pcnn_plan* p = new pcnn_plan();
+  if (opt) p->opt = *opt;
+  else pcnn_plan_options_default(&p->opt);
+  p->kopt.pdl = (int)p->opt.pdl;
+  p->kopt.ss_mt = (int)p->opt.ss_mt;
+  p->kopt.ss_share = (int)p->opt.ss_share;
+  p->kopt.ss_psub = (int)p->opt.ss_psub;
+  p->kopt.ss_wres = (int)p->opt.ss_wres;
+  p->kopt.tc_stage = (int)p->opt.tc_stage;
+  p->kopt.proj_fuse = (int)p->opt.fuse_projection;
+  p->kopt.streamk = (int)p->opt.streamk;
+  p->kopt.streamk_fill = (float)p->opt.streamk_fill;
+  p->kopt.dbg = (int)p->opt.debug;
   p->units.assign(units, units + n_units);
   p->tensors.assign(tensors, tensors + n_tensors);
   p->batch = batch;
@@ -603,7 +598,7 @@ int pcnn_plan_create(const pcnn_unit_desc* units, int n_units, const pcnn_tensor
   for (auto& t : p->tensors) {
     if (!(t.cb == 4 || t.cb == 8 || t.cb == 16 || t.cb == 32) || t.nblk * t.cb < t.c ||
         (t.is_vector && (t.h != 1 || t.w != 1))) {
-      delete p;
+      pcnn_plan_destroy(p);
       return fail(PCNN_ERR_INVALID, "tensor block size must be 4, 8, 16 or 32");
     }
     p->views.push_back(make_view(t, p->ws));
@@ -614,13 +609,14 @@ int pcnn_plan_create(const pcnn_unit_desc* units, int n_units, const pcnn_tensor
     const pcnn_unit_desc& u = p->units[i];
     auto bad = [&](int64_t id) { return id < -1 || id >= n_tensors; };
     if (bad(u.in) || bad(u.in2) || bad(u.out)) {
-      delete p;
+      pcnn_plan_destroy(p);
       return fail(PCNN_ERR_INVALID, "unit " + std::to_string(i) + ": tensor id out of range");
     }
     if (u.kind == PCNN_UNIT_CONV) {
+      p->conv_args[i].opt = p->kopt;
       int rc = build_conv(p, i, p->conv_args[i]);
       if (rc != PCNN_OK) {
-        delete p;
+        pcnn_plan_destroy(p);
         return rc;
       }
       // auto: fp16x2 tensor cores, else 3xTF32, else SIMT; 4: auto without fp16x2
@@ -633,7 +629,7 @@ int pcnn_plan_create(const pcnn_unit_desc* units, int n_units, const pcnn_tensor
       if (p->impl[i] == 1 && (u.impl == 0 || u.impl == 2 || u.impl == 4) && a.tcw && conv_tc_supported(a))
         p->impl[i] = 2;
       if (p->impl[i] == 1 && (u.impl == 2 || u.impl == 3 || u.impl == 5)) {
-        delete p;
+        pcnn_plan_destroy(p);
         return fail(PCNN_ERR_UNSUPPORTED, "unit " + std::to_string(i) + ": tcgen05 conv requested but unsupported");
       }
     }
@@ -646,16 +642,23 @@ int pcnn_plan_create(const pcnn_unit_desc* units, int n_units, const pcnn_tensor
   }
   cudaMemset(p->status_dev, 0, sizeof(int));
   *p->status_host = 0;
+  if (p->opt.timeline) {
+    const size_t tb = sizeof(unsigned long long) * 2 * (size_t)n_units;
+    if (cudaMalloc(&p->tl_dev, tb) != cudaSuccess || cudaMallocHost(&p->tl_host, tb) != cudaSuccess) {
+      pcnn_plan_destroy(p);
+      return fail(PCNN_ERR_CUDA, "timeline allocation failed");
+    }
+    cudaMemset(p->tl_dev, 0, tb);
+  }
   choose_formats(p);
-  build_chains(p);
-  // a global-pool conv right after an unchained halo-tile conv: that kernel
-  // zeroes the sums in its prologue (keeps the launch chain free of memset
-  // nodes, which would break programmatic dependent launch)
+  // a global-pool conv right after a halo-tile conv: that kernel zeroes the
+  // sums in its prologue (keeps the launch chain free of memset nodes, which
+  // would break programmatic dependent launch)
   p->prezeroed.assign(n_units, 0);
   for (int i = 1; i < n_units; ++i) {
     const pcnn_unit_desc& u = p->units[i];
-    if (u.kind != PCNN_UNIT_CONV || u.pool != PCNN_POOL_GLOBAL || p->chain_of[i] >= 0) continue;
-    if (p->impl[i - 1] != 5 || p->chain_of[i - 1] >= 0 || getenv("PCNN_NO_PREZERO")) continue;
+    if (u.kind != PCNN_UNIT_CONV || u.pool != PCNN_POOL_GLOBAL) continue;
+    if (p->impl[i - 1] != 5 || !p->opt.prezero) continue;
     ConvArgs& prev = p->conv_args[i - 1];
     prev.prezero = p->conv_args[i].epi.out.base;
     prev.prezero_n = (int64_t)p->batch * p->conv_args[i].epi.out.cpad();
@@ -664,9 +667,8 @@ int pcnn_plan_create(const pcnn_unit_desc* units, int n_units, const pcnn_tensor
   fuse_projections(p);
   build_flags(p);
   plan_streamk(p);
-  for (int len : p->chain_len) p->launches -= len - 1;  // one kernel per chain
   if (cudaStreamCreateWithFlags(&p->capture_stream, cudaStreamNonBlocking) != cudaSuccess) {
-    delete p;
+    pcnn_plan_destroy(p);
     return fail(PCNN_ERR_CUDA, "cudaStreamCreate failed");
   }
   *plan_out = p;
@@ -677,8 +679,9 @@ int pcnn_plan_destroy(pcnn_plan* p) {
   if (!p) return PCNN_OK;
   for (auto& g : p->graphs) cudaGraphExecDestroy(g.exec);
   if (p->capture_stream) cudaStreamDestroy(p->capture_stream);
-  for (SsChain* c : p->chains) ss_chain_destroy(c);
   if (p->status_dev) cudaFree(p->status_dev);
+  if (p->tl_dev) cudaFree(p->tl_dev);
+  if (p->tl_host) cudaFreeHost(p->tl_host);
   if (p->flags_dev) cudaFree(p->flags_dev);
   if (p->sk_flags) cudaFree(p->sk_flags);
   if (p->sk_slots) cudaFree(p->sk_slots);
@@ -693,6 +696,29 @@ int pcnn_plan_destroy(pcnn_plan* p) {
   if (p->status_host) cudaFreeHost(p->status_host);
   delete p;
   return PCNN_OK;
+}
+
+int pcnn_plan_timeline(pcnn_plan* p, int64_t* ns, int max_units, void* stream) {
+  if (!p || !ns || max_units < 0) return fail(PCNN_ERR_INVALID, "pcnn_plan_timeline: null argument");
+  if (!p->tl_dev) return fail(PCNN_ERR_INVALID, "pcnn_plan_timeline: plan created without options.timeline");
+  const int n = std::min(max_units, (int)p->units.size());
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  PCNN_CUDA(cudaMemcpyAsync(p->tl_host, p->tl_dev, sizeof(unsigned long long) * 2 * (size_t)n,
+                            cudaMemcpyDeviceToHost, s));
+  PCNN_CUDA(cudaStreamSynchronize(s));
+  for (int i = 0; i < n; ++i) {
+    const unsigned long long a = p->tl_host[2 * i], b = p->tl_host[2 * i + 1];
+    ns[2 * i] = b ? (int64_t)~a : 0;
+    ns[2 * i + 1] = (int64_t)b;
+  }
+  return n;
+}
+
+int pcnn_plan_unit_launch(const pcnn_plan* p, int unit) {
+  if (!p || unit < 0 || unit >= (int)p->units.size()) return -1;
+  int u = unit;
+  while (u > 0 && p->fused[u]) --u;  // a fused unit runs in its predecessor's launch
+  return u;
 }
 
 int pcnn_plan_num_launches(const pcnn_plan* p) { return p ? p->launches : -1; }
@@ -723,10 +749,9 @@ int pcnn_plan_last_status(const pcnn_plan* p) { return p ? *p->status_host : -1;
 int pcnn_forward(pcnn_plan* p, const float* x, float* logits, void* stream, int use_graph) {
   if (!p || !x || !logits) return fail(PCNN_ERR_INVALID, "pcnn_forward: null argument");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // PCNN_NO_GRAPH=1: eager launches (ncu cannot replay the extended-launch
+  // options.graph = 0: eager launches (ncu cannot replay the extended-launch
   // kernels inside a CUDA graph)
-  static const bool no_graph = getenv("PCNN_NO_GRAPH") != nullptr;
-  if (!use_graph || no_graph) {
+  if (!use_graph || !p->opt.graph) {
     enqueue_all(p, x, logits, s);
     PCNN_CUDA(cudaGetLastError());
     return PCNN_OK;
@@ -858,6 +883,8 @@ int pcnn_forward_unit(pcnn_plan* p, int unit, const float* x, float* logits, voi
     cudaMemsetAsync(a.epi.out.base, 0, sizeof(float) * (size_t)p->batch * a.epi.out.cpad(),
                     static_cast<cudaStream_t>(stream));
   }
+  if (p->tl_dev)
+    cudaMemsetAsync(p->tl_dev + 2 * unit, 0, 2 * sizeof(unsigned long long), static_cast<cudaStream_t>(stream));
   enqueue_unit(p, unit, x, logits, static_cast<cudaStream_t>(stream), false);
   PCNN_CUDA(cudaGetLastError());
   return PCNN_OK;

@@ -325,6 +325,29 @@ struct PixelMap {
   }
 };
 
+// ---- launch timeline (pcnn_plan_timeline) ----------------------------------
+// tl[0] = max over CTAs of ~start (so ~tl[0] is the earliest start), tl[1] =
+// max over CTAs of the exit time, in %globaltimer ns; both zeroed before
+// every forward.  One fire-and-forget reduction per CTA and mark.
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void tl_mark(unsigned long long* tl, int end) {
+  if (tl && threadIdx.x == 0) {
+    const unsigned long long t = global_ns();
+    if (end) atomicMax(tl + 1, t);
+    else atomicMax(tl, ~t);
+  }
+}
+// start mark at construction, end mark when the kernel body returns (thread 0)
+struct TlScope {
+  unsigned long long* tl;
+  __device__ __forceinline__ explicit TlScope(unsigned long long* p) : tl(p) { tl_mark(tl, 0); }
+  __device__ __forceinline__ ~TlScope() { tl_mark(tl, 1); }
+};
+
 // Horner with per-channel coefficients c_k at coef[k * stride + ch].
 __device__ __forceinline__ float horner(const float* __restrict__ coef, int64_t stride, int deg,
                                         int ch, float x) {

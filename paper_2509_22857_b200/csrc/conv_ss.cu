@@ -82,12 +82,6 @@ struct SsParams {
   int fold_skip, fold_out;  // storage scales folded into the epilogue table (epi_fill_tab)
   int dbg;
   int time_slot;         // PCNN_TC_DEBUG bit 64: per-CTA globaltimer stamps slot, else -1
-  // ---- chained launches (conv_chain_kernel) ----
-  uint32_t buf_cols;        // TMEM columns between accumulator buffers
-  int dep_in, dep_in_mode;  // chain index of the layer writing the input (-1: before the launch); 1 range, 2 all
-  int dep_sk, dep_sk_mode;  // same for the residual skip
-  int* done;                // [m_tiles] finished n-tiles per m-tile, [m_tiles] all finished tiles; or null
-  const __half* zeros;      // zero source for the missing second 8-channel group (cpad 4 / 8)
   // wres: the whole weight image (one n-tile, every chunk) stays resident in
   // shared memory after the stage ring, copied once before
   // griddepcontrol.wait; the ring stages then hold activations only
@@ -104,16 +98,6 @@ struct SsParams {
   const float* pwscale;
   uint32_t pb_bytes;        // 64 * nt per chunk
   int ptoff;                // centre tap offset (toff of the projection's input position)
-};
-
-// launch-wide configuration of a chain
-struct ChainCommon {
-  int stages;
-  uint32_t stage_bytes;  // ring slot (max over the chain)
-  int acc_bufs;
-  uint32_t buf_cols;     // accumulator buffer stride (max over the chain)
-  uint32_t tmem_cols;
-  int ptab_floats;       // per-warpgroup parameter table (max over the chain)
 };
 
 // PCNN_TC_DEBUG bit 32: CTA 0 records clock64 events (see pcnn_ss_trace)
@@ -360,6 +344,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
   if (!a.skip_gridwait) ptx::griddep_wait();
   ptx::griddep_launch();
   cta_stamp(P, 1);
+  tl_mark(a.tl, 0);
 
   if (warp == kWarpProducer) {
     // ===== producer: per (tile, 16-channel chunk) one stage = the tile's
@@ -826,297 +811,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
   }
   cta_stamp(P, 2);
   __syncthreads();
+  tl_mark(a.tl, 1);
   if (warp == kWarpProducer) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, P.tmem_cols);
   }
   cta_stamp(P, 3);
-}
-
-// ---- chained layers: one persistent launch runs a run of consecutive layers.
-// Every role walks the same (layer, tile) sequence; the stage ring and the
-// accumulator ring continue across layers.  A tile's producer waits for the
-// tiles of earlier chain layers that wrote its input range / residual range
-// (per-(layer, m-tile) counters: released by the epilogue after its stores,
-// acquired by the producer before its bulk copies).  No launch gaps, one
-// prologue, and a layer's tail overlaps the next layer's head.
-__device__ __forceinline__ void wait_count(const int* c, int target) {
-  int v;
-  for (;;) {
-    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
-    if (v >= target) break;
-    __nanosleep(32);
-  }
-}
-
-__device__ __forceinline__ void wait_dep(const SsParams* layers, int dep, int mode, int64_t lo, int64_t hi) {
-  if (dep < 0) return;
-  const SsParams& Q = layers[dep];
-  if (mode == 1) {
-    const int tm = kTileM * Q.mt;
-    lo = lo < 0 ? 0 : lo;
-    hi = hi > Q.gtotal ? Q.gtotal : hi;
-    if (hi > lo) {
-      int first = (int)(lo / tm), last = (int)((hi - 1) / tm);
-      if (last >= Q.m_tiles) last = Q.m_tiles - 1;
-      for (int t = first; t <= last; ++t) wait_count(Q.done + t, Q.n_tiles);
-    }
-  } else {
-    wait_count(Q.done + Q.m_tiles, Q.m_tiles * Q.n_tiles);
-  }
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");  // the polls were relaxed
-}
-
-__device__ __forceinline__ void copy_params(SsParams* dst, const SsParams* src, int tid, int nthr) {
-  const int* s = reinterpret_cast<const int*>(src);
-  int* d = reinterpret_cast<int*>(dst);
-  for (int i = tid; i < (int)(sizeof(SsParams) / 4); i += nthr) d[i] = __ldg(s + i);
-}
-
-template <int TAPS>
-__global__ void __launch_bounds__(kThreads, 1) conv_chain_kernel(const SsParams* __restrict__ layers, const int nlayers,
-                                                                 const __grid_constant__ ChainCommon C) {
-  // each role works from its own copy of its current layer's parameters in
-  // (static, so explicitly shared-space) shared memory: producer, MMA, two
-  // epilogue warpgroups
-  __shared__ SsParams s_prm[4];
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
-  Smem* S = reinterpret_cast<Smem*>(smem + (size_t)C.stages * C.stage_bytes);
-  float* ptab_base = reinterpret_cast<float*>(smem + (size_t)C.stages * C.stage_bytes + ((sizeof(Smem) + 15) & ~size_t(15)));
-  const uint32_t base = ptx::smem_u32(smem);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int NB = C.acc_bufs;
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < C.stages; ++i) {
-      ptx::mbar_init(ptx::smem_u32(&S->full[i]), 1);
-      ptx::mbar_init(ptx::smem_u32(&S->empty[i]), 1);
-    }
-    for (int i = 0; i < kMaxAcc; ++i) {
-      ptx::mbar_init(ptx::smem_u32(&S->acc_full[i]), 1);
-      ptx::mbar_init(ptx::smem_u32(&S->acc_empty[i]), 4);
-    }
-    ptx::fence_mbar_init();
-  }
-  if (warp == kWarpProducer) ptx::tmem_alloc(ptx::smem_u32(&S->tmem_base), C.tmem_cols);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = S->tmem_base;
-  ptx::griddep_wait();
-  ptx::griddep_launch();
-
-  if (warp == kWarpProducer) {
-    int st = 0;
-    uint32_t ph = 0;
-    for (int L = 0; L < nlayers; ++L) {
-      __syncwarp();  // lane 0 is done with the previous layer's copy
-      copy_params(&s_prm[0], layers + L, lane, 32);
-      __syncwarp();
-      if (lane == 0) {
-        const SsParams& P = s_prm[0];
-        const ConvArgs& a = P.a;
-        const __half* hi = a.in.hi();
-        const __half* lo = a.in.lo();
-        const int total_tiles = P.m_tiles * P.n_tiles;
-        const int tm = kTileM * P.mt;
-        for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-          const int n_tile = tile / P.m_tiles, m_tile = tile - n_tile * P.m_tiles;
-          const int64_t gs = (int64_t)m_tile * tm - P.halo;
-          const int64_t cs = gs < 0 ? 0 : gs;
-          const int64_t ge = gs + P.span;
-          const int64_t ce = ge > P.gtotal ? P.gtotal : ge;
-          const uint32_t slot0 = (uint32_t)(cs - gs) * 16, bytes = (uint32_t)(ce - cs) * 16;
-          if (P.dep_in >= 0 || P.dep_sk >= 0) {
-            wait_dep(layers, P.dep_in, P.dep_in_mode, cs, ce);
-            wait_dep(layers, P.dep_sk, P.dep_sk_mode, (int64_t)m_tile * tm, (int64_t)m_tile * tm + tm);
-            asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> bulk-copy reads
-          }
-          for (int q = 0; q < P.nq; ++q) {
-            ptx::mbar_wait_sleep(ptx::smem_u32(&S->empty[st]), ph ^ 1);
-            const uint32_t bar = ptx::smem_u32(&S->full[st]);
-            const uint32_t sb = base + st * C.stage_bytes;
-            ptx::mbar_arrive_tx(bar, 4 * P.nplanes * bytes + P.b_bytes);
-            for (int pl = 0; pl < P.nplanes; ++pl) {
-              const uint32_t ps = sb + pl * 4 * P.a_bytes;
-              for (int g = 0; g < 2; ++g) {
-                if (q == P.nq - 1 && g >= P.last_groups) {  // cpad 4 / 8: zero second group
-                  ptx::bulk_g2s(ps + g * P.a_bytes + slot0, P.zeros, bytes, bar);
-                  ptx::bulk_g2s(ps + (2 + g) * P.a_bytes + slot0, P.zeros, bytes, bar);
-                  continue;
-                }
-                const int64_t off = (2 * q + g) * a.in.kstride + P.plane_id[pl] * a.in.pstride + cs * 8;
-                ptx::bulk_g2s(ps + g * P.a_bytes + slot0, hi + off, bytes, bar);
-                ptx::bulk_g2s(ps + (2 + g) * P.a_bytes + slot0, lo + off, bytes, bar);
-              }
-            }
-            ptx::bulk_g2s(sb + P.nplanes * 4 * P.a_bytes, P.w + ((int64_t)n_tile * P.nq + q) * P.taps * 32 * P.nt,
-                          P.b_bytes, bar);
-            if (++st == C.stages) { st = 0; ph ^= 1; }
-          }
-        }
-      }
-    }
-  } else if (warp == kWarpMma) {
-    int st = 0;
-    uint32_t ph = 0, it = 0;
-    for (int L = 0; L < nlayers; ++L) {
-      __syncwarp();
-      copy_params(&s_prm[1], layers + L, lane, 32);
-      __syncwarp();
-      const SsParams& P = s_prm[1];
-      const int total_tiles = P.m_tiles * P.n_tiles;
-      const int NP = P.partials;
-      const uint32_t set_cols = P.concat ? (uint32_t)NP * 2 * P.nt : (uint32_t)(NP + 1) * P.nt;
-      const uint32_t idesc = ptx::idesc_f16(kTileM, P.nt);
-      const uint32_t idesc2 = ptx::idesc_f16(kTileM, 2 * P.nt);
-      const uint32_t a_lbo = P.a_bytes, b_lbo = 2 * P.nt * 16;
-      const int taps = P.taps, mt = P.mt, nq = P.nq;
-      const bool concat = P.concat;
-      const uint32_t nt = P.nt, a_bytes = P.a_bytes, b_off = P.nplanes * 4 * P.a_bytes;
-      uint64_t offs[TAPS];
-#pragma unroll
-      for (int t = 0; t < TAPS; ++t) offs[t] = (uint64_t)P.toff[t < taps ? t : 0];
-      const uint64_t bstep = (uint64_t)(64 * nt) >> 4, blo = (uint64_t)(nt * 16) >> 4;
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
-        const uint32_t acc = it % NB, acc_ph = (it / NB) & 1;
-        ptx::mbar_wait(ptx::smem_u32(&S->acc_empty[acc]), acc_ph ^ 1);
-        ptx::tc_fence_after();
-        const uint32_t d_tile = tmem + acc * C.buf_cols;
-        int p = 0;
-        for (int q = 0; q < nq; ++q) {
-          ptx::mbar_wait(ptx::smem_u32(&S->full[st]), ph);
-          ptx::tc_fence_after();
-          const uint32_t sb = base + st * C.stage_bytes;
-          const uint64_t a_hi = ptx::smem_desc_noswz(sb, a_lbo, 128);
-          const uint64_t a_lo = ptx::smem_desc_noswz(sb + 2 * a_bytes, a_lbo, 128);
-          const uint64_t b0 = ptx::smem_desc_noswz(sb + b_off, b_lbo, 128);
-          const uint32_t main_acc = q >= NP ? 1u : 0u;
-          for (int sub = 0; sub < mt; ++sub) {
-            const uint32_t d_set = d_tile + sub * set_cols;
-            const uint32_t dm = concat ? d_set + p * 2 * nt : d_set + p * nt;
-            const uint32_t dc = concat ? dm + nt : d_set + NP * nt;
-            const uint64_t shift = (uint64_t)(sub * kTileM);
-            if (TAPS >= 16 && taps == 16)
-              ss_stage<16>(concat, dm, dc, a_hi + shift, a_lo + shift, b0, bstep, blo, idesc2, idesc, main_acc, q > 0, offs);
-            else if (TAPS >= 9 && taps == 9)
-              ss_stage<9>(concat, dm, dc, a_hi + shift, a_lo + shift, b0, bstep, blo, idesc2, idesc, main_acc, q > 0, offs);
-            else
-              ss_stage<1>(concat, dm, dc, a_hi + shift, a_lo + shift, b0, bstep, blo, idesc2, idesc, main_acc, q > 0, offs);
-          }
-          if (++p == NP) p = 0;
-          ptx::mma_commit_warp(ptx::smem_u32(&S->empty[st]));
-          if (++st == C.stages) { st = 0; ph ^= 1; }
-        }
-        ptx::mma_commit_warp(ptx::smem_u32(&S->acc_full[acc]));
-      }
-    }
-  } else if (warp < 8) {
-    const int ew = warp >> 2;
-    const int row = threadIdx.x & 127;
-    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    float* ptab = ptab_base + ew * C.ptab_floats;
-    uint32_t it = 0;
-    for (int L = 0; L < nlayers; ++L) {
-      // this layer's parameters and per-channel table, once per warpgroup
-      asm volatile("bar.sync %0, 128;" ::"r"(1 + ew) : "memory");
-      copy_params(&s_prm[2 + ew], layers + L, row, 128);
-      epi_fill_tab(layers[L].a.epi, layers[L].etab, ptab, row, 128);
-      asm volatile("bar.sync %0, 128;" ::"r"(1 + ew) : "memory");
-      const SsParams& P = s_prm[2 + ew];
-      const ConvArgs& a = P.a;
-      const EpiParams& e = a.epi;
-      const int total_tiles = P.m_tiles * P.n_tiles;
-      const int NP = P.partials;
-      const uint32_t set_cols = P.concat ? (uint32_t)NP * 2 * P.nt : (uint32_t)(NP + 1) * P.nt;
-      const float wsc = __ldg(P.wscale) * a.in.sload;
-      EpiTab etab = P.etab;
-      etab.ptab = ptab;
-      const int hw = P.hp * P.wp;
-      const bool early_skip = P.dep_sk < 0;
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
-        const uint32_t acc = it % NB;
-        const uint32_t acc_ph = (it / NB) & 1;
-        if ((int)(acc & 1) != ew || (NB == 1 && ew == 1)) continue;
-        const int n_tile = (int)P.div_mt.div(tile), m_tile = tile - n_tile * P.m_tiles;
-        for (int sub = 0; sub < P.mt; ++sub) {
-          const int g = (m_tile * P.mt + sub) * kTileM + row;
-          int b, gy, gx;
-          bool valid;
-          if (P.shared_grid) {
-            const int g1 = g > 0 ? g - 1 : 0;
-            const int R = (int)P.div_wp.div(g1);
-            gx = g1 - R * P.wp;
-            const int R1 = R > 0 ? R - 1 : 0;
-            b = (int)P.div_h1.div(R1);
-            gy = R1 - b * P.hp;
-            valid = g >= 1 && R >= 1 && g < P.gtotal && gx < P.vx1 && gy < P.vy1 && b < a.batch;
-          } else {
-            b = (int)P.div_hw.div(g);
-            const int r = g - b * hw;
-            gy = (int)P.div_wp.div(r);
-            gx = r - gy * P.wp;
-            valid = g < P.gtotal && gy >= P.vy0 && gy < P.vy1 && gx >= P.vx0 && gx < P.vx1;
-          }
-          const int yp = gy - P.vy0 + 1, xp = gx - P.vx0 + 1;
-          float sk[16];
-          // the skip can be loaded ahead of the accumulators unless an earlier
-          // layer of this launch writes it
-          if (early_skip) epi_load_skip(e, n_tile * P.nt, valid, b, yp - 1, xp - 1, sk);
-          if (sub == 0) {
-            ptx::mbar_wait_warp(ptx::smem_u32(&S->acc_full[acc]), acc_ph);
-            ptx::tc_fence_after();
-          }
-          if (!early_skip) epi_load_skip(e, n_tile * P.nt, valid, b, yp - 1, xp - 1, sk);
-          const uint32_t d_set = tmem + lane_off + acc * C.buf_cols + sub * set_cols;
-          for (int c0 = 0; c0 < P.nt; c0 += 16) {
-            float v[16], t[16];
-            if (P.concat) {
-              ptx::tmem_ld16x2(d_set + P.nt + c0, d_set + c0, v, t);
-#pragma unroll
-              for (int i = 0; i < 16; ++i) v[i] += t[i];
-              for (int p = 1; p < NP; ++p) {
-                float u[16];
-                ptx::tmem_ld16x2(d_set + 2 * p * P.nt + P.nt + c0, d_set + 2 * p * P.nt + c0, u, t);
-#pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] += u[i] + t[i];
-              }
-            } else {
-              ptx::tmem_ld16x2(d_set + NP * P.nt + c0, d_set + c0, v, t);
-#pragma unroll
-              for (int i = 0; i < 16; ++i) v[i] += t[i];
-              for (int p = 1; p < NP; ++p) {
-                ptx::tmem_ld16(d_set + p * P.nt + c0, t);
-#pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] += t[i];
-              }
-            }
-#pragma unroll
-            epi_chunk16(e, etab, v, wsc, sk, n_tile * P.nt + c0, valid, valid ? b : 0, yp - 1, xp - 1, lane);
-            if (c0 + 16 < P.nt) epi_load_skip(e, n_tile * P.nt + c0 + 16, valid, b, yp - 1, xp - 1, sk);
-          }
-        }
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->acc_empty[acc]));
-        if (P.done) {
-          // the warpgroup barrier orders every thread's stores before thread
-          // 0's (cumulative) release increments
-          asm volatile("bar.sync %0, 128;" ::"r"(1 + ew) : "memory");
-          if (row == 0) {
-            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(P.done + m_tile) : "memory");
-            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(P.done + P.m_tiles) : "memory");
-          }
-        }
-      }
-    }
-  }
-  __syncthreads();
-  if (warp == kWarpProducer) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, C.tmem_cols);
-  }
 }
 
 // residual staging: [2 buffers][4 words][256 epilogue threads] x 16 bytes
@@ -1153,10 +853,7 @@ static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub,
   if (P.gtotal >= (1ll << 31)) return false;
   // two 128-row sub-tiles per tile for small N: one stage, one weight copy
   // and one set of hand-offs serve 256 positions
-  const char* mt_env = getenv("PCNN_SS_MT");
-  const char* mt16_env = getenv("PCNN_SS_MT16");  // experiment: sub-tiles for NT = 16 layers only
-  P.mt = mt_env ? atoi(mt_env) : (P.nt <= 32 ? 2 : 1);
-  if (mt16_env && P.nt == 16) P.mt = atoi(mt16_env);
+  P.mt = a.opt.ss_mt ? a.opt.ss_mt : (P.nt <= 32 ? 2 : 1);
   if (force_mt) P.mt = force_mt;
   if (P.mt < 1 || P.mt > 4) P.mt = 1;
   const int tm = kTileM * P.mt;
@@ -1257,8 +954,7 @@ static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub,
   P.wres = 0;
   P.res_bytes = 0;
   {
-    static const char* wenv = getenv("PCNN_SS_WRES");
-    const bool want = wenv ? atoi(wenv) != 0 : true;
+    const bool want = a.opt.ss_wres != 0;
     const uint32_t res = (uint32_t)P.nq * P.b_bytes, sa = P.nplanes * 4 * P.a_bytes;
     if (want && allow_wres && !P.psub && !P.proj && P.b_img_nt == P.nt && P.n_tiles == 1 && P.nq <= kMaxWChunks &&
         res < budget) {
@@ -1272,8 +968,7 @@ static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub,
       }
     }
   }
-  const char* dbg = getenv("PCNN_TC_DEBUG");
-  P.dbg = dbg ? atoi(dbg) : 0;
+  P.dbg = a.opt.dbg;
   P.time_slot = -1;
   // accumulators: as many partials as accuracy asks for, then two buffers
   // main products rotate over the partials per stage (taps MMAs each)
@@ -1294,14 +989,8 @@ static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub,
       (P.concat ? P.partials * 2 * P.nt : (P.partials + 1) * P.nt) + (P.proj ? 2u * P.nt : 0u);
   const uint32_t need = P.acc_bufs * P.mt * set;
   P.tmem_cols = need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
-  P.buf_cols = P.mt * set;
   // shared epilogue when a tile has an even number of 16-column chunks
-  const char* sh = getenv("PCNN_SS_SHARE");
-  P.share_epi = sh ? atoi(sh) : ((P.mt * (P.proj ? 2 : 1) * P.nt / 16) % 2 == 0);
-  P.dep_in = P.dep_sk = -1;
-  P.dep_in_mode = P.dep_sk_mode = 0;
-  P.done = nullptr;
-  P.zeros = nullptr;
+  P.share_epi = a.opt.ss_share >= 0 ? a.opt.ss_share : ((P.mt * (P.proj ? 2 : 1) * P.nt / 16) % 2 == 0);
   P.div_hw = make_fastdiv((uint32_t)(P.hp * P.wp));
   P.div_h1 = make_fastdiv((uint32_t)P.hp);
   P.div_wp = make_fastdiv((uint32_t)P.wp);
@@ -1312,11 +1001,10 @@ static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub,
 // Staging choice: whole-chunk stages (a 16-channel chunk of every plane and
 // all taps' weights) when two fit; else, for 3x3 stride 2, one parity plane
 // per stage (measured: faster than 64-channel tiles, slower than whole-chunk
-// stages when those fit); else two 64-channel tiles.  PCNN_SS_PSUB=0/1 forces.
+// stages when those fit); else two 64-channel tiles.  Option ss_psub 0/1 forces.
 bool make_ss_params(const ConvArgs& a, SsParams& P, bool allow_wres = true) {
   const int nt = a.npad <= 128 ? a.npad : 128;
-  const char* env = getenv("PCNN_SS_PSUB");
-  const int force = env ? atoi(env) : -1;
+  const int force = a.opt.ss_psub;
   if (force == 1 && make_ss_params_nt(a, P, nt, true, allow_wres)) return true;
   if (make_ss_params_nt(a, P, nt, false, allow_wres)) return true;
   if (force != 0 && make_ss_params_nt(a, P, nt, true, allow_wres)) return true;
@@ -1379,7 +1067,7 @@ bool conv_ss_flag_geometry(const ConvArgs& a, FlagDep& d) {
 }
 
 bool conv_ss_proj_ok(const ConvArgs& a, const ConvArgs& proj) {
-  if (getenv("PCNN_NO_PROJ_FUSE")) return false;
+  if (!a.opt.proj_fuse) return false;
   ConvArgs b = a;
   b.proj = &proj;
   SsParams P;
@@ -1387,17 +1075,16 @@ bool conv_ss_proj_ok(const ConvArgs& a, const ConvArgs& proj) {
 }
 
 bool conv_ss_streamk_wanted(const ConvArgs& a, int nsm, size_t* slot_floats) {
-  if (getenv("PCNN_NO_STREAMK")) return false;
+  if (!a.opt.streamk) return false;
   SsParams P;
   if (!make_ss_params(a, P) || P.nq < 2) return false;
   const int tiles = P.m_tiles * P.n_tiles;
-  // Measured on B200 (PCNN_NO_STREAMK A/B): splitting pays only when whole
+  // Measured on B200 (streamk option A/B): splitting pays only when whole
   // tiles leave most SMs idle (VGG 2x2 layers: 36 tiles for 148 SMs);
   // for 1.1-1.5 rounds of tiles (RN20 stage 3, RN18 stages 3-4) the partial
   // round trips and shorter pipelines cost more than the balance gains
-  // (RN20 0.362 vs 0.322 ms).  PCNN_STREAMK_FILL overrides the threshold.
-  const char* fill_env = getenv("PCNN_STREAMK_FILL");
-  const double fill = fill_env ? atof(fill_env) : 0.3;
+  // (RN20 0.362 vs 0.322 ms).  Option streamk_fill sets the threshold.
+  const double fill = a.opt.streamk_fill;
   if (tiles > fill * nsm) return false;
   const int items = P.mt * (P.nt / 16) * (P.proj ? 2 : 1);
   *slot_floats = (size_t)items * 128 * 16;
@@ -1433,108 +1120,7 @@ void launch_conv_ss(const ConvArgs& a, cudaStream_t s) {
                                       : (sk ? conv_ss_kernel<1, true> : conv_ss_kernel<1, false>);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (P.dbg & 64) P.time_slot = g_time_next++ % kTimeSlots;
-  launch_pdl(k, grid, kThreads, smem, s, P);
-}
-
-struct SsChain {
-  ChainCommon C;
-  SsParams* d_layers = nullptr;
-  int* d_done = nullptr;
-  size_t done_count = 0;
-  int n = 0, grid = 0, taps_max = 1;
-  size_t smem = 0;
-};
-
-static const __half* zero_source() {
-  static void* z = nullptr;
-  if (!z) {
-    cudaMalloc(&z, 1 << 17);
-    cudaMemset(z, 0, 1 << 17);
-  }
-  return static_cast<const __half*>(z);
-}
-
-SsChain* ss_chain_create(const ConvArgs* args, int n, const int* dep_in, const int* dep_in_mode, const int* dep_sk,
-                         const int* dep_sk_mode) {
-  std::vector<SsParams> L(n);
-  uint32_t stage_max = 0, buf = 0;
-  int ptab_max = 0, tiles_max = 0, taps_max = 1;
-  std::vector<int> needed(n, 0);
-  for (int i = 0; i < n; ++i) {
-    if (!make_ss_params(args[i], L[i], false) || L[i].b_img_nt != L[i].nt || L[i].psub) return nullptr;
-    if ((size_t)L[i].span * 16 > (1u << 17)) return nullptr;
-    stage_max = stage_max > L[i].stage_bytes ? stage_max : L[i].stage_bytes;
-    buf = buf > L[i].buf_cols ? buf : L[i].buf_cols;
-    const int pt = (L[i].etab.rows * args[i].epi.npad + 3) & ~3;
-    ptab_max = ptab_max > pt ? ptab_max : pt;
-    const int tiles = L[i].m_tiles * L[i].n_tiles;
-    tiles_max = tiles_max > tiles ? tiles_max : tiles;
-    taps_max = taps_max > L[i].taps ? taps_max : L[i].taps;
-    L[i].dep_in = dep_in[i];
-    L[i].dep_in_mode = dep_in_mode[i];
-    L[i].dep_sk = dep_sk[i];
-    L[i].dep_sk_mode = dep_sk_mode[i];
-    if (dep_in[i] >= 0) needed[dep_in[i]] = 1;
-    if (dep_sk[i] >= 0) needed[dep_sk[i]] = 1;
-    L[i].zeros = zero_source();
-  }
-  ChainCommon C;
-  C.stage_bytes = stage_max;
-  C.ptab_floats = ptab_max;
-  C.buf_cols = buf;
-  C.acc_bufs = 4 * buf <= 512 ? 4 : (2 * buf <= 512 ? 2 : 1);
-  if (buf > 512) return nullptr;
-  const uint32_t need = C.acc_bufs * buf;
-  C.tmem_cols = need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
-  // dynamic budget: 227 KB minus the static parameter copies
-  const size_t aux = ((sizeof(Smem) + 15) & ~size_t(15)) + 2 * (size_t)ptab_max * 4;
-  const size_t budget = 227 * 1024 - 4 * sizeof(SsParams) - 128 - 256;
-  int stages = (int)((budget - aux) / stage_max);
-  C.stages = stages > kMaxStages ? kMaxStages : stages;
-  if (C.stages < 2) return nullptr;
-  size_t done = 0;
-  for (int i = 0; i < n; ++i) {
-    L[i].buf_cols = buf;
-    L[i].acc_bufs = C.acc_bufs;
-    if (needed[i]) done += L[i].m_tiles + 1;
-  }
-  SsChain* c = new SsChain;
-  c->C = C;
-  c->n = n;
-  c->taps_max = taps_max;
-  if (done) {
-    cudaMalloc(&c->d_done, done * sizeof(int));
-    c->done_count = done;
-    size_t off = 0;
-    for (int i = 0; i < n; ++i)
-      if (needed[i]) {
-        L[i].done = c->d_done + off;
-        off += L[i].m_tiles + 1;
-      }
-  }
-  cudaMalloc(&c->d_layers, sizeof(SsParams) * n);
-  cudaMemcpy(c->d_layers, L.data(), sizeof(SsParams) * n, cudaMemcpyHostToDevice);
-  int dev = 0, nsm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  c->grid = tiles_max < nsm ? tiles_max : nsm;
-  c->smem = 128 + (size_t)C.stages * C.stage_bytes + aux;
-  return c;
-}
-
-void ss_chain_launch(const SsChain* c, cudaStream_t s) {
-  if (c->done_count) cudaMemsetAsync(c->d_done, 0, c->done_count * sizeof(int), s);
-  void (*k)(const SsParams*, int, ChainCommon) =
-      c->taps_max >= 16 ? conv_chain_kernel<16> : c->taps_max >= 9 ? conv_chain_kernel<9> : conv_chain_kernel<1>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem);
-  launch_pdl(k, c->grid, kThreads, c->smem, s, (const SsParams*)c->d_layers, c->n, c->C);
-}
-
-void ss_chain_destroy(SsChain* c) {
-  if (!c) return;
-  cudaFree(c->d_layers);
-  if (c->d_done) cudaFree(c->d_done);
-  delete c;
+  launch_pdl(k, grid, kThreads, smem, s, a.opt.pdl, P);
 }
 
 }  // namespace pcnn

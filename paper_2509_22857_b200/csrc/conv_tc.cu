@@ -344,6 +344,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   ptx::tc_fence_after();
   ptx::griddep_wait();  // activations come from the previous kernel
   ptx::griddep_launch();
+  tl_mark(a.tl, 0);
   const uint32_t tmem = S->tmem_base;
   const uint32_t a_col0 = (uint32_t)NB * acc_set_cols;
 
@@ -720,6 +721,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     }
   }
   __syncthreads();
+  tl_mark(a.tl, 1);
   if (warp == kWarpAlloc) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, P.tmem_cols);
@@ -755,7 +757,7 @@ bool make_params(const ConvArgs& a, TcParams& P) {
   // staged input if a tile needs few boxes and everything fits
   P.staged = 0;
   staging_geometry(a, P);
-  const bool stage_ok = !(getenv("PCNN_TC_NOSTAGE")) && !a.in.split && P.pieces <= 4 && P.box_w <= 256 &&
+  const bool stage_ok = a.opt.tc_stage && !a.in.split && P.pieces <= 4 && P.box_w <= 256 &&
                         P.box_h <= 256 &&
                         (a.in.nblk == 1 || a.in.cb == 32);
   P.nbs = kBStages;
@@ -770,8 +772,7 @@ bool make_params(const ConvArgs& a, TcParams& P) {
   if (1024 + (size_t)P.b_stage_bytes * P.nbs + st + aux > budget) return false;
   P.resident = (P.n_tiles == 1 && 1024 + (size_t)P.b_stage_bytes * P.nkb + st + aux <= budget) ? 1 : 0;
   // TMEM budget (512 columns): acc_bufs x (P + 1) x NT accumulators + a_stages x 64
-  const char* dbg = getenv("PCNN_TC_DEBUG");
-  P.dbg = dbg ? atoi(dbg) : 0;
+  P.dbg = a.opt.dbg;
   const int ksteps = P.nkb * (kTcBK / 8);
   int want = (ksteps + kAddsPerPartial - 1) / kAddsPerPartial;
   want = want < 1 ? 1 : (want > kMaxPartials ? kMaxPartials : want);
@@ -901,7 +902,7 @@ void launch_conv_tc(const ConvArgs& a, cudaStream_t s) {
 #define PCNN_TC_LAUNCH(C, H, SP)                                                                              \
   case C * 4 + (H ? (SP ? 2 : 1) : 0):                                                                        \
     cudaFuncSetAttribute(conv_tc_kernel<C, H, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
-    launch_pdl(conv_tc_kernel<C, H, SP>, grid, kThreads, smem, s, P);                                         \
+    launch_pdl(conv_tc_kernel<C, H, SP>, grid, kThreads, smem, s, a.opt.pdl, P);                                         \
     break;
     PCNN_TC_LAUNCH(2, false, false)
     PCNN_TC_LAUNCH(3, false, false)

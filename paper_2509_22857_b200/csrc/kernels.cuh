@@ -20,6 +20,21 @@ struct FlagDep {
   int per_tile = 0, all = 0;  // counter values meaning "done"
 };
 
+// Per-plan kernel switches (from pcnn_plan_options; the library reads no
+// environment variables)
+struct KOpts {
+  int pdl = 1;          // programmatic dependent launch
+  int ss_mt = 0;        // halo-tile sub-tiles per tile (0 auto)
+  int ss_share = -1;    // shared epilogue (-1 auto)
+  int ss_psub = -1;     // parity-plane stages (-1 auto)
+  int ss_wres = 1;      // resident weights
+  int tc_stage = 1;     // TMA-staged input boxes (TMEM-A kernel)
+  int proj_fuse = 1;    // fused projections
+  int streamk = 1;      // stream-K
+  float streamk_fill = 0.3f;
+  int dbg = 0;          // diagnostic bits (pcnn_plan_options.debug)
+};
+
 struct ConvArgs {
   TensorView in;
   PixelMap pm;
@@ -53,6 +68,8 @@ struct ConvArgs {
   // epilogue.  null: one whole tile per CTA turn.
   int* sk_flags = nullptr;    // [grid], zeroed at the start of every forward
   float* sk_slots = nullptr;  // [grid][items][128][16]
+  KOpts opt;
+  unsigned long long* tl = nullptr;  // launch timeline slot (common.cuh tl_mark) or null
 };
 
 struct LinearArgs {
@@ -68,6 +85,7 @@ struct LinearArgs {
   int64_t out_stride;
   // also the user's [batch][n_out] logits (the copyout unit folded in), or null
   float* out2 = nullptr;
+  unsigned long long* tl = nullptr;
 };
 
 struct EltArgs {
@@ -77,6 +95,7 @@ struct EltArgs {
   int64_t stride;
   int deg, k, st, pad, axis;
   int pool = 0;  // LOCALPOOL: PCNN_POOL_BI2 = 2x2 window through two bivariate stages
+  unsigned long long* tl = nullptr;
 };
 
 inline int64_t host_pixel_count(const PixelMap& pm, int batch) {
@@ -84,19 +103,21 @@ inline int64_t host_pixel_count(const PixelMap& pm, int batch) {
 }
 
 // s2d: x is [B][C/4][2H][2W] and t holds it as 2x2 blocks, channel (dy*2+dx)*(C/4)+c
-void launch_ingest(const float* x, const TensorView& t, int batch, bool s2d, cudaStream_t s);
+void launch_ingest(const float* x, const TensorView& t, int batch, bool s2d, cudaStream_t s,
+                   unsigned long long* tl = nullptr);
 void launch_conv_simt(const ConvArgs& a, cudaStream_t s);
 void launch_linear(const LinearArgs& a, cudaStream_t s);
 void launch_eltwise(const EltArgs& a, cudaStream_t s);
-void launch_copyout(const TensorView& t, float* dst, int batch, cudaStream_t s);
+void launch_copyout(const TensorView& t, float* dst, int batch, cudaStream_t s, unsigned long long* tl = nullptr);
 
 // Launch a persistent tcgen05 kernel with programmatic stream serialization:
 // its prologue (barriers, TMEM allocation, parameter table) overlaps the tail
 // of the previous kernel, and griddep_wait() in the kernel orders the data.
-// PCNN_NO_PDL=1 launches it plainly.
+// pdl = 0 launches it plainly.
 template <typename... Params, typename... Args>
-inline void launch_pdl(void (*kernel)(Params...), int grid, int threads, size_t smem, cudaStream_t s, Args... args) {
-  static const bool off = getenv("PCNN_NO_PDL") != nullptr;
+inline void launch_pdl(void (*kernel)(Params...), int grid, int threads, size_t smem, cudaStream_t s, int pdl,
+                       Args... args) {
+  const bool off = !pdl;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(threads);
@@ -118,16 +139,6 @@ void tc_weight_image_dims(int npad, int kp, int64_t* floats);
 // fp16x2 conv with A from shared memory (conv_ss.cu): stride-1 3x3/1x1 convs
 // reading a split tensor
 bool conv_ss_supported(const ConvArgs& a);
-// A run of consecutive halo-tile conv layers in ONE persistent launch; each
-// layer's producer waits (per-tile counters) for the earlier chain layers
-// that write its input / residual: dep_* = chain index or -1, mode 1 = the
-// tiles covering the position range (stride-1 layers on the same grid), 2 =
-// all tiles.  nullptr if the layers cannot share one launch.
-struct SsChain;
-SsChain* ss_chain_create(const ConvArgs* args, int n, const int* dep_in, const int* dep_in_mode, const int* dep_sk,
-                         const int* dep_sk_mode);
-void ss_chain_launch(const SsChain* c, cudaStream_t s);
-void ss_chain_destroy(SsChain* c);
 // the shape/precision part of conv_ss_supported (input format not checked)
 bool conv_ss_shape_ok(const ConvArgs& a);
 void launch_conv_ss(const ConvArgs& a, cudaStream_t s);

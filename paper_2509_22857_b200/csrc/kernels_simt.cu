@@ -9,7 +9,9 @@ namespace pcnn {
 // ---------------------------------------------------------------------------
 // ingest: user NCHW float32 -> channel-blocked [B][nblk][H][W][cb], pad = 0
 // ---------------------------------------------------------------------------
-__global__ void ingest_kernel(const float* __restrict__ x, TensorView t, int batch, int s2d) {
+__global__ void ingest_kernel(const float* __restrict__ x, TensorView t, int batch, int s2d,
+                              unsigned long long* tl) {
+  TlScope tls(tl);
   // one thread per (image, 4-channel group, pixel); pixels fastest so the
   // NCHW reads of each channel plane are coalesced, one float4 store each
   const int64_t hw = (int64_t)t.h * t.w;
@@ -48,7 +50,8 @@ __global__ void ingest_kernel(const float* __restrict__ x, TensorView t, int bat
 // space-to-depth ingest, one thread per block position and all 16 channels:
 // per input channel two float2 row reads (coalesced across the warp), one
 // 16-channel store (whole 32-byte sectors in the split layout)
-__global__ void ingest_s2d_kernel(const float* __restrict__ x, TensorView t, int batch) {
+__global__ void ingest_s2d_kernel(const float* __restrict__ x, TensorView t, int batch, unsigned long long* tl) {
+  TlScope tls(tl);
   const int cin = t.c / 4, H = 2 * (t.h - 1), W = 2 * (t.w - 1);
   const int64_t hw = (int64_t)t.h * t.w;
   const int64_t total = (int64_t)batch * hw;
@@ -79,16 +82,17 @@ __global__ void ingest_s2d_kernel(const float* __restrict__ x, TensorView t, int
   }
 }
 
-void launch_ingest(const float* x, const TensorView& t, int batch, bool s2d, cudaStream_t s) {
+void launch_ingest(const float* x, const TensorView& t, int batch, bool s2d, cudaStream_t s,
+                   unsigned long long* tl) {
   if (s2d && t.c <= 16 && (2 * (t.w - 1)) % 2 == 0) {
     const int64_t total = (int64_t)batch * t.h * t.w;
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-    ingest_s2d_kernel<<<std::max(blocks, 1), 256, 0, s>>>(x, t, batch);
+    ingest_s2d_kernel<<<std::max(blocks, 1), 256, 0, s>>>(x, t, batch, tl);
     return;
   }
   int64_t total = (int64_t)batch * (t.cpad() / 4) * t.h * t.w;
   int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-  ingest_kernel<<<std::max(blocks, 1), 256, 0, s>>>(x, t, batch, s2d ? 1 : 0);
+  ingest_kernel<<<std::max(blocks, 1), 256, 0, s>>>(x, t, batch, s2d ? 1 : 0, tl);
 }
 
 // ---------------------------------------------------------------------------
@@ -97,6 +101,7 @@ void launch_ingest(const float* x, const TensorView& t, int batch, bool s2d, cud
 // ---------------------------------------------------------------------------
 template <int BN>
 __global__ void __launch_bounds__(256) conv_simt_kernel(ConvArgs a) {
+  TlScope tls(a.tl);
   constexpr int TN = 4, TM = 4, BK = 16;
   constexpr int NTX = BN / TN;          // threads along N
   constexpr int NTY = 256 / NTX;        // threads along M
@@ -252,6 +257,7 @@ void launch_conv_simt(const ConvArgs& a, cudaStream_t s) {
 // Block = 8 warps over 32 outputs x 16 images; X tile staged in smem.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) linear_kernel(LinearArgs a) {
+  TlScope tls(a.tl);
   extern __shared__ float xs[];  // [16][n_in]
   constexpr int BB = 16;
   const int b0 = blockIdx.y * BB;
@@ -357,6 +363,7 @@ void launch_linear(const LinearArgs& a, cudaStream_t s) {
 // standalone elementwise / pool kernels (one thread per 4-channel group)
 // ---------------------------------------------------------------------------
 __global__ void eltwise_kernel(EltArgs a) {
+  TlScope tls(a.tl);
   const TensorView& o = a.out;
   const int groups = o.cpad() / 4;
   const int64_t total = (int64_t)a.batch * groups * o.h * o.w;
@@ -432,6 +439,7 @@ __global__ void eltwise_kernel(EltArgs a) {
 
 // global pool / flatten: spatial -> vector [B][c] or [B][c*h*w]
 __global__ void to_vector_kernel(EltArgs a) {
+  TlScope tls(a.tl);
   const TensorView& in = a.in;
   const int hw = in.h * in.w;
   if (a.kind == PCNN_UNIT_GLOBALPOOL) {
@@ -474,6 +482,7 @@ __global__ void to_vector_kernel(EltArgs a) {
 // output pixel) with the channel group fastest, so a warp's loads cover whole
 // 128-byte pixel rows of the channel-blocked input; the output may be split.
 __global__ void localpool_kernel(EltArgs a) {
+  TlScope tls(a.tl);
   const TensorView& in = a.in;
   const TensorView& o = a.out;
   const int gpb = in.cb / 4;  // 4-channel groups per channel block
@@ -530,6 +539,7 @@ __global__ void localpool_kernel(EltArgs a) {
 // fp32 blocked input, output in its storage format.  Restates the BI2 pool
 // of the conv epilogue (epi_tc.cuh) as a pass of its own.
 __global__ void bipool2_kernel(EltArgs a) {
+  TlScope tls(a.tl);
   const TensorView& in = a.in;
   const TensorView& o = a.out;
   const int sub_n = o.cb / 4;
@@ -587,7 +597,8 @@ void launch_eltwise(const EltArgs& a, cudaStream_t s) {
 }
 
 // blocked tensor -> user output [B][C][H][W] (logits [B][K] when H = W = 1)
-__global__ void copyout_kernel(TensorView t, float* __restrict__ dst, int batch) {
+__global__ void copyout_kernel(TensorView t, float* __restrict__ dst, int batch, unsigned long long* tl) {
+  TlScope tls(tl);
   const int64_t hw = (int64_t)t.h * t.w;
   const int64_t n = (int64_t)batch * t.c * hw;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -597,10 +608,10 @@ __global__ void copyout_kernel(TensorView t, float* __restrict__ dst, int batch)
   }
 }
 
-void launch_copyout(const TensorView& t, float* dst, int batch, cudaStream_t s) {
+void launch_copyout(const TensorView& t, float* dst, int batch, cudaStream_t s, unsigned long long* tl) {
   int64_t n = (int64_t)batch * t.c * t.h * t.w;
   int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
-  copyout_kernel<<<std::max(blocks, 1), 256, 0, s>>>(t, dst, batch);
+  copyout_kernel<<<std::max(blocks, 1), 256, 0, s>>>(t, dst, batch, tl);
 }
 
 }  // namespace pcnn

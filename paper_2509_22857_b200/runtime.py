@@ -15,6 +15,8 @@ libpcnn.so or a B200 they raise ``PcnnError``.
 from __future__ import annotations
 
 import ctypes
+import dataclasses
+import weakref
 from typing import Dict, Optional, Tuple
 
 import numpy as np
@@ -38,7 +40,7 @@ def _stream_handle(stream=None) -> ctypes.c_void_p:
 class Plan:
     """A libpcnn plan for one batch size: workspace + unit table."""
 
-    def __init__(self, engine: "Engine", batch: int, impl: int = 0):
+    def __init__(self, engine: "Engine", batch: int, impl: int = 0, options: Optional[L.PlanOptions] = None):
         torch = _torch()
         lw = engine.lw
         self.batch = batch
@@ -46,12 +48,14 @@ class Plan:
         self.ws = torch.zeros(max(floats, 1), dtype=torch.float32, device=engine.device)
         self.units = lw.unit_descs(impl)
         self.tdescs = tdescs
+        self.options = options if options is not None else L.PlanOptions.default()
         handle = ctypes.c_void_p()
-        L.check(L.lib().pcnn_plan_create(self.units, len(lw.units), tdescs, len(lw.tensors), batch,
-                                         lw.input_tensor, lw.output_tensor,
-                                         ctypes.c_void_p(engine.packed.data_ptr()),
-                                         ctypes.c_void_p(self.ws.data_ptr()),
-                                         self.ws.numel() * 4, ctypes.byref(handle)),
+        L.check(L.lib().pcnn_plan_create_ex(self.units, len(lw.units), tdescs, len(lw.tensors), batch,
+                                            lw.input_tensor, lw.output_tensor,
+                                            ctypes.c_void_p(engine.packed.data_ptr()),
+                                            ctypes.c_void_p(self.ws.data_ptr()),
+                                            self.ws.numel() * 4, ctypes.byref(self.options),
+                                            ctypes.byref(handle)),
                 "pcnn_plan_create")
         self.handle = handle
         self.n_units = len(lw.units)
@@ -75,6 +79,21 @@ class Plan:
 
     def last_status(self) -> int:
         return L.lib().pcnn_plan_last_status(self.handle)
+
+    def unit_launch(self, i: int) -> int:
+        """The unit whose kernel launch computes unit i (i unless fused)."""
+        return L.lib().pcnn_plan_unit_launch(self.handle, i)
+
+    def timeline(self, stream=None) -> np.ndarray:
+        """(n_units, 2) int64 %globaltimer ns of the last forward: when each
+        unit's launch released its first CTA past the dependency wait, and
+        when its last CTA exited (0, 0 for units run inside another launch).
+        Synchronises the stream."""
+        buf = (L.c_i64 * (2 * self.n_units))()
+        n = L.lib().pcnn_plan_timeline(self.handle, buf, self.n_units, _stream_handle(stream))
+        if n < 0:
+            L.check(n, "pcnn_plan_timeline")
+        return np.frombuffer(buf, dtype=np.int64).reshape(self.n_units, 2).copy()
 
     def read_tensor(self, t: int) -> np.ndarray:
         """Copy tensor t out of the workspace, decoded from its storage format
@@ -120,12 +139,15 @@ class Engine:
     """One graph resident on the GPU."""
 
     def __init__(self, g: ModelGraph, device=None, use_tc: bool = True, impl: int = 0,
-                 lowered: Optional[Lowered] = None):
+                 lowered: Optional[Lowered] = None, options: Optional[L.PlanOptions] = None):
+        """options: pcnn_plan_options for every plan of this engine (None =
+        the library defaults; see _lib.PlanOptions / options_from_env)."""
         torch = _torch()
         L.require_device()
         self.device = torch.device(device or "cuda")
         self.lw = lowered or lower(g, use_tc=use_tc)
         self.impl = impl
+        self.options = options
         m = master_array(self.lw._chunks, self.lw.master_size)
         self.master = torch.from_numpy(m).to(self.device)
         self.packed = torch.zeros(self.lw.packed_size, dtype=torch.float32, device=self.device)
@@ -154,7 +176,7 @@ class Engine:
     def plan(self, batch: int) -> Plan:
         p = self.plans.get(batch)
         if p is None:
-            p = self.plans[batch] = Plan(self, batch, self.impl)
+            p = self.plans[batch] = Plan(self, batch, self.impl, self.options)
         return p
 
     def fallback_plan(self, batch: int) -> Plan:
@@ -162,7 +184,7 @@ class Engine:
         recompute path when a split-format activation left the fp16 range."""
         p = self.fallback_plans.get(batch)
         if p is None:
-            p = self.fallback_plans[batch] = Plan(self, batch, L.IMPL_FP32_TENSORS)
+            p = self.fallback_plans[batch] = Plan(self, batch, L.IMPL_FP32_TENSORS, self.options)
         return p
 
     def recalibrate(self, f: "Plan") -> bool:
@@ -219,9 +241,30 @@ class Engine:
             self.recalibrate(f)
         return out
 
+    def _check_input_shape(self, shape) -> None:
+        want = tuple(self.lw.shapes[self.lw.graph.input_id()])
+        if len(shape) != 1 + len(want) or tuple(shape[1:]) != want:
+            raise GraphError(f"input shape {tuple(shape[1:])} != graph input {want}")
+
+    @staticmethod
+    def _check_buffer(t, shape, what: str, device: bool) -> None:
+        """A caller-provided staging / output buffer must be float32,
+        contiguous, on the right side and exactly the size libpcnn copies."""
+        torch = _torch()
+        if torch.is_tensor(t):
+            ok = t.dtype == torch.float32 and t.is_contiguous() and bool(t.is_cuda) == device
+        else:
+            ok = (not device and isinstance(t, np.ndarray) and t.dtype == np.float32
+                  and t.flags["C_CONTIGUOUS"])
+        if not ok or tuple(t.shape) != tuple(shape):
+            raise GraphError(f"{what}: expected a contiguous float32 {'CUDA' if device else 'host'} buffer "
+                             f"of shape {tuple(shape)}, got {getattr(t, 'dtype', type(t))} {tuple(t.shape)}")
+
     def forward_host(self, x_host: np.ndarray, x_dev=None, out_dev=None, out_host=None, stream=None):
         """Host in, host out: H2D copy, forward, D2H copy inside libpcnn."""
         torch = _torch()
+        x_host = np.asarray(x_host)
+        self._check_input_shape(x_host.shape)
         b = x_host.shape[0]
         if x_dev is None:
             x_dev = torch.empty(x_host.shape, dtype=torch.float32, device=self.device)
@@ -229,6 +272,9 @@ class Engine:
             out_dev = torch.empty(self.out_shape(b), dtype=torch.float32, device=self.device)
         if out_host is None:
             out_host = np.empty(self.out_shape(b), dtype=np.float32)
+        self._check_buffer(x_dev, x_host.shape, "forward_host x_dev", True)
+        self._check_buffer(out_dev, self.out_shape(b), "forward_host out_dev", True)
+        self._check_buffer(out_host, self.out_shape(b), "forward_host out_host", False)
         xh = np.ascontiguousarray(x_host, dtype=np.float32)
         p = self.plan(b)
         L.check(L.lib().pcnn_forward_host(p.handle, xh.ctypes.data_as(ctypes.c_void_p),
@@ -259,15 +305,23 @@ class Engine:
               for x in xs_host]
         if not xs:
             return []
+        self._check_input_shape(xs[0].shape)
         b = xs[0].shape[0]
-        if any(tuple(x.shape) != tuple(xs[0].shape) for x in xs):
-            raise GraphError("forward_host_many: all batches must have the same shape")
+        for i, x in enumerate(xs):
+            self._check_buffer(x, xs[0].shape, f"forward_host_many batch {i}", False)
         if outs_host is None:
             outs_host = [torch.empty(self.out_shape(b), dtype=torch.float32).pin_memory() for _ in xs]
+        if len(outs_host) != len(xs):
+            raise GraphError("forward_host_many: one output buffer per input batch")
+        for i, o in enumerate(outs_host):
+            self._check_buffer(o, self.out_shape(b), f"forward_host_many output {i}", False)
         if staging is None:
             staging = (torch.empty(xs[0].shape, dtype=torch.float32, device=self.device),
                        torch.empty(xs[0].shape, dtype=torch.float32, device=self.device),
                        torch.empty(self.out_shape(b), dtype=torch.float32, device=self.device))
+        self._check_buffer(staging[0], xs[0].shape, "forward_host_many staging[0]", True)
+        self._check_buffer(staging[1], xs[0].shape, "forward_host_many staging[1]", True)
+        self._check_buffer(staging[2], self.out_shape(b), "forward_host_many staging[2]", True)
         n = len(xs)
         xp = (ctypes.c_void_p * n)(*[x.data_ptr() for x in xs])
         op = (ctypes.c_void_p * n)(*[o.data_ptr() for o in outs_host])
@@ -291,10 +345,86 @@ class Engine:
                 "pcnn_forward_unit")
 
 
+# ---------------------------------------------------------------------------
+# drop-in functions: one cached Engine per graph
+# ---------------------------------------------------------------------------
+
+def _param_fingerprint(v):
+    if isinstance(v, np.ndarray):
+        flat = v.reshape(-1)
+        step = max(1, flat.size // 61)
+        sample = flat[::step]
+        return ("a", id(v), v.shape, float(sample.sum()) if sample.size else 0.0,
+                float(flat[-1]) if flat.size else 0.0)
+    if isinstance(v, (list, tuple)):
+        return tuple(_param_fingerprint(x) for x in v)
+    return v
+
+
+def graph_signature(g: ModelGraph) -> tuple:
+    """Structure + parameter identity of a graph: node ids, kinds, scalar
+    fields, each parameter array's identity, shape and a strided sample of
+    its values, and the ordered edge list.  Cheap (O(nodes)); the reference
+    treats validated graphs as immutable (transforms return copies), so a
+    graph whose signature is unchanged reuses its Engine."""
+    nodes = tuple((nid, type(n).__name__,
+                   tuple((f.name, _param_fingerprint(getattr(n, f.name))) for f in dataclasses.fields(n)))
+                  for nid, n in g.nodes.items())
+    return nodes, tuple(g.edges)
+
+
+class _EngineCache:
+    """Engines of recently used graphs, keyed by the graph object (weakly:
+    an entry dies with its graph) and checked against graph_signature on
+    every hit, so an edited graph is lowered again."""
+
+    def __init__(self, capacity: int = 8):
+        self.capacity = capacity
+        self.entries: "weakref.WeakKeyDictionary[ModelGraph, tuple]" = weakref.WeakKeyDictionary()
+        self.order = []
+        self.hits = self.misses = 0
+
+    def get(self, g: ModelGraph, **kw) -> "Engine":
+        key_kw = tuple(sorted((k, repr(v)) for k, v in kw.items()))
+        sig = graph_signature(g)
+        e = self.entries.get(g)
+        if e is not None and e[0] == sig and e[1] == key_kw:
+            self.hits += 1
+            return e[2]
+        self.misses += 1
+        eng = Engine(g, **kw)
+        self.entries[g] = (sig, key_kw, eng)
+        self.order = [r for r in self.order if r() is not None and r() is not g] + [weakref.ref(g)]
+        while len(self.order) > self.capacity:
+            old = self.order.pop(0)()
+            if old is not None:
+                self.entries.pop(old, None)
+        return eng
+
+    def clear(self) -> None:
+        self.entries = weakref.WeakKeyDictionary()
+        self.order = []
+
+
+_ENGINES = _EngineCache()
+
+
+def cached_engine(g: ModelGraph, **kw) -> "Engine":
+    """The Engine reference_eval / forward use for g (lowered, uploaded and
+    its plans / CUDA graphs built once per graph)."""
+    return _ENGINES.get(g, **kw)
+
+
+def clear_engine_cache() -> None:
+    _ENGINES.clear()
+
+
 def forward(g: ModelGraph, x, **kw):
-    """Batched GPU forward of a graph: numpy or torch (B, C, H, W) -> same kind (B, K)."""
+    """Batched GPU forward of a graph: numpy or torch (B, C, H, W) -> same kind (B, K).
+    The graph's Engine is cached (cached_engine), so repeated calls pay the
+    lowering, upload and plan capture once."""
     torch = _torch()
-    eng = Engine(g, **kw)
+    eng = cached_engine(g, **kw)
     if isinstance(x, np.ndarray):
         xt = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(eng.device)
         return eng.forward(xt).cpu().numpy().astype(np.float64)
@@ -304,9 +434,11 @@ def forward(g: ModelGraph, x, **kw):
 def reference_eval(g: ModelGraph, image) -> np.ndarray:
     """Drop-in for levnet.graph.reference_eval (graph.py:413-426): one image
     (C, H, W) -> logits, computed by the B200 kernels (float32 compute,
-    returned as float64 like the reference)."""
-    shapes = g.validate()
+    returned as float64 like the reference).  Validation and lowering happen
+    once per graph (cached_engine), not per call as in the reference."""
+    eng = cached_engine(g)
     image = np.asarray(image, dtype=np.float64)
-    if image.shape != shapes[g.input_id()]:
-        raise GraphError(f"input shape {image.shape} != graph input {shapes[g.input_id()]}")
+    want = tuple(eng.lw.shapes[eng.lw.graph.input_id()])
+    if image.shape != want:
+        raise GraphError(f"input shape {image.shape} != graph input {want}")
     return forward(g, image[None])[0]

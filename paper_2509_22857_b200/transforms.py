@@ -1063,21 +1063,44 @@ def apply_pipeline(g: ModelGraph, strategy: str) -> Tuple[ModelGraph, PassReport
     return out, PassReport(rewrites, len(g.nodes) - len(out.nodes), before, critical_path_levels(out))
 
 
-def check_equivalence_replicas(ref: ModelGraph, candidate: ModelGraph, n_inputs: int = 100,
-                               rtol: float = 1e-4, seed: int = 0) -> EquivReport:
-    """check_equivalence with the inputs spread over the ranks of the
-    process group (one GPU each, replicas.init_replicas): each rank runs both
-    models on its shard, the per-input verdicts are gathered, every rank gets
-    the same report.  Same inputs as check_equivalence for a given seed."""
-    from . import replicas
-    from .runtime import Engine
-    import torch
+# float32 device compute: the tightest relative tolerance check_equivalence
+# can honour (north-star gate rel 1e-4).  The reference's float64 default
+# (1e-8, transforms.py:755) is below float32 resolution.
+DEVICE_RTOL = 1e-4
+FP32_RTOL_FLOOR = 1e-6
+
+
+def _resolve_rtol(rtol):
+    if rtol is None:
+        return DEVICE_RTOL
+    if rtol < FP32_RTOL_FLOOR:
+        import warnings
+        warnings.warn(f"check_equivalence: rtol={rtol:g} is below what float32 device compute can reach "
+                      f"(~{FP32_RTOL_FLOOR:g}); equivalent models may report passed=False. "
+                      f"Use rtol=None (default {DEVICE_RTOL:g}).", RuntimeWarning, stacklevel=3)
+    return rtol
+
+
+def _equivalence_inputs(ref: ModelGraph, candidate: ModelGraph, n_inputs: int, seed: int) -> np.ndarray:
     shapes = ref.validate()
     candidate.validate()
     in_shape = shapes[ref.input_id()]
     rng = np.random.default_rng(seed)
-    xs = np.stack([rng.uniform(-1.0, 1.0, in_shape) for _ in range(n_inputs)])
-    ea, eb = Engine(ref), Engine(candidate)
+    return np.stack([rng.uniform(-1.0, 1.0, in_shape) for _ in range(n_inputs)])
+
+
+def check_equivalence_replicas(ref: ModelGraph, candidate: ModelGraph, n_inputs: int = 100,
+                               rtol: Optional[float] = None, seed: int = 0) -> EquivReport:
+    """check_equivalence with the inputs spread over the ranks of the
+    process group (one GPU each, replicas.init_replicas): each rank runs both
+    models on its shard, the per-input verdicts are gathered, every rank gets
+    the same report.  Same inputs and rtol default as check_equivalence."""
+    from . import replicas
+    from .runtime import cached_engine
+    import torch
+    rtol = _resolve_rtol(rtol)
+    xs = _equivalence_inputs(ref, candidate, n_inputs, seed)
+    ea, eb = cached_engine(ref), cached_engine(candidate)
 
     def run(eng):
         return lambda x: eng.forward(torch.from_numpy(x.astype(np.float32)).cuda()).double().cpu().numpy()
@@ -1087,20 +1110,20 @@ def check_equivalence_replicas(ref: ModelGraph, candidate: ModelGraph, n_inputs:
 
 
 def check_equivalence(ref: ModelGraph, candidate: ModelGraph, n_inputs: int = 100,
-                      rtol: float = 1e-8, seed: int = 0) -> EquivReport:
-    """transforms.py:753-778 with both forwards batched on the GPU (float32
-    compute, so use rtol around 1e-4 rather than the reference's float64 1e-8).
-    Inputs are the same U(-1, 1) draws from default_rng(seed)."""
-    from .runtime import Engine
+                      rtol: Optional[float] = None, seed: int = 0) -> EquivReport:
+    """transforms.py:753-778 with both forwards batched on the GPU.  Same
+    inputs (U(-1, 1) draws from default_rng(seed)), same metric (max|a-b| /
+    max|a| per input, worst over inputs; argmax agreement).  The forwards
+    compute in float32, so rtol defaults to DEVICE_RTOL = 1e-4 instead of the
+    reference's float64 1e-8; an explicit rtol below FP32_RTOL_FLOOR warns
+    (RuntimeWarning) rather than silently failing equivalent models."""
+    from .runtime import cached_engine
     import torch
-    shapes = ref.validate()
-    candidate.validate()
-    in_shape = shapes[ref.input_id()]
-    rng = np.random.default_rng(seed)
-    xs = np.stack([rng.uniform(-1.0, 1.0, in_shape) for _ in range(n_inputs)])
+    rtol = _resolve_rtol(rtol)
+    xs = _equivalence_inputs(ref, candidate, n_inputs, seed)
     xt = torch.from_numpy(xs.astype(np.float32)).cuda()
-    a = Engine(ref).forward(xt).double().cpu().numpy().reshape(n_inputs, -1)
-    b = Engine(candidate).forward(xt).double().cpu().numpy().reshape(n_inputs, -1)
+    a = cached_engine(ref).forward(xt).double().cpu().numpy().reshape(n_inputs, -1)
+    b = cached_engine(candidate).forward(xt).double().cpu().numpy().reshape(n_inputs, -1)
     err = np.max(np.abs(a - b), axis=1) / np.maximum(np.max(np.abs(a), axis=1), 1e-12)
     worst = float(err.max())
     match = float(np.mean(np.argmax(a, axis=1) == np.argmax(b, axis=1)))

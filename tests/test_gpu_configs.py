@@ -17,10 +17,6 @@ from paper_2509_22857_b200.runtime import Engine
 
 pytestmark = pytest.mark.gpu
 
-# oracle images per config (the float64 numpy oracle is slow at 224^2)
-N_IMAGES = {"lenet5": 16, "resnet20": 8, "resnet20_deg8": 8, "vgg11": 8, "resnet18": 2}
-
-
 def _device_sweeps(g, cfg):
     eng = Engine(g)
     cur = g
@@ -40,34 +36,44 @@ def _oracle_sweeps(g, cfg):
 
 @pytest.mark.parametrize("name", list(configs.CONFIGS))
 def test_config_redistributed_forward(cuda, name):
+    """Every image of the measured batch (64 / 256 / 512 / 128 / 64) against
+    the float64 oracle: rel 1e-4 / abs 1e-5 elementwise, the reference's
+    max|a-b|/max|a| <= 1e-4 (transforms.py:768-772), and the batch-centred
+    logits within 1e-3 of their range -- the oracle runs over the host cores
+    (oracle/pool.py), so there is no reason to sample."""
     import torch
+    from oracle.pool import OraclePool
     cfg = configs.CONFIGS[name]
     g = configs.build(name)
     eng, got_g = _device_sweeps(g, cfg)
     want_g = _oracle_sweeps(g, cfg)
     assert max_param_rel_diff(got_g, want_g) <= 1e-6, name
 
-    # a batch of the measured size through the device engine; the oracle
-    # checks the first N images (batch size changes no per-image arithmetic)
     x = configs.make_input(cfg)
+    assert len(x) == cfg.batch
     y = eng.forward(torch.from_numpy(x.astype(np.float32)).cuda()).double().cpu().numpy()
     assert np.all(np.isfinite(y)), name
-    n = N_IMAGES[name]
-    want = O.eval_batch(want_g, x[:n])
-    np.testing.assert_allclose(y[:n], want, rtol=1e-4, atol=1e-5, err_msg=name)
-    assert rel_err(y[:n], want) <= 1e-4, name
-    # input-dependent part of the logits
-    cg, cw = y[:n] - y[:n].mean(0), want - want.mean(0)
+    with OraclePool(want_g) as pool:
+        want = pool.eval(x)
+    np.testing.assert_allclose(y, want, rtol=1e-4, atol=1e-5, err_msg=name)
+    assert rel_err(y, want) <= 1e-4, name
+    # input-dependent part of the logits (RN18 / VGG logits are ~99.7 % constant)
+    cg, cw = y - y.mean(0), want - want.mean(0)
     assert np.abs(cw).max() > 0, name
-    assert np.abs(cg - cw).max() <= 1e-2 * np.abs(cw).max(), name
-    # the redistributed model is the original function
-    orig = O.eval_batch(g, x[:n])
+    assert np.abs(cg - cw).max() <= 1e-3 * np.abs(cw).max(), (name, np.abs(cg - cw).max() / np.abs(cw).max())
+    # per image: the argmax agrees wherever the oracle's top-2 margin exceeds the tolerance
+    top2 = np.sort(want, axis=1)[:, -2:]
+    clear = (top2[:, 1] - top2[:, 0]) > 1e-4 * np.abs(want).max()
+    assert np.all(np.argmax(y, 1)[clear] == np.argmax(want, 1)[clear]), name
+    # the redistributed model is the original function (float64 oracle, full batch)
+    with OraclePool(g) as pool:
+        orig = pool.eval(x)
     assert rel_err(want, orig) <= 1e-8, name
 
 
 @pytest.mark.parametrize("name", ["resnet20", "resnet18", "resnet20_deg8"])
-def test_flag_synchronised_launches_match(cuda, name, monkeypatch):
-    """PCNN_FLAGS=1 (per-tile completion counters instead of whole-grid
+def test_flag_synchronised_launches_match(cuda, name):
+    """options.flag_sync = 1 (per-tile completion counters instead of whole-grid
     griddepcontrol ordering, api.cu build_flags) computes the same logits:
     every tile does the same arithmetic, only the global-pool atomics may
     add in another order."""
@@ -79,8 +85,7 @@ def test_flag_synchronised_launches_match(cuda, name, monkeypatch):
                                    allow_negative_leading=cfg.allow_negative_leading)
     x = torch.from_numpy(configs.make_input(cfg).astype(np.float32)).cuda()
     base = Engine(g).forward(x).double().cpu().numpy()
-    monkeypatch.setenv("PCNN_FLAGS", "1")
-    eng = Engine(g)
+    eng = Engine(g, options=L.PlanOptions.default(flag_sync=1))
     fn = L.lib().pcnn_plan_flags
     fn.argtypes = [ctypes.c_void_p]
     assert fn(eng.plan(cfg.batch).handle) == 1, name
@@ -117,13 +122,18 @@ def test_check_equivalence_replicas_single_rank(cuda):
     a = T.check_equivalence(g, rg, n_inputs=32, rtol=1e-4)
     b = T.check_equivalence_replicas(g, rg, n_inputs=32, rtol=1e-4)
     assert a.passed and b.passed
+    # default rtol: the float32-reachable DEVICE_RTOL, never a silent failure
+    c = T.check_equivalence(g, rg, n_inputs=32)
+    assert c.passed and c.max_rel_err == a.max_rel_err
+    with pytest.warns(RuntimeWarning):
+        T.check_equivalence(g, rg, n_inputs=8, rtol=1e-8)
     assert abs(a.max_rel_err - b.max_rel_err) <= 1e-7 and a.argmax_match_rate == b.argmax_match_rate
 
 
 @pytest.mark.parametrize("name", ["resnet20", "resnet18", "vgg11"])
-def test_streamk_matches_whole_tiles(cuda, name, monkeypatch):
+def test_streamk_matches_whole_tiles(cuda, name):
     """Stream-K forced onto every layer with <= 2 rounds of tiles
-    (PCNN_STREAMK_FILL=2: RN20 stage 3, RN18 stages 3-4, VGG's 8x8..2x2
+    (options.streamk_fill = 2: RN20 stage 3, RN18 stages 3-4, VGG's 8x8..2x2
     layers, fused projections included) computes what whole tiles compute,
     up to the summation order of the split chunks."""
     import torch
@@ -132,11 +142,9 @@ def test_streamk_matches_whole_tiles(cuda, name, monkeypatch):
     for d in cfg.redistribution:
         g, _, _ = T.redistribute_sweep(g, d, allow_negative_leading=cfg.allow_negative_leading)
     x = torch.from_numpy(configs.make_input(cfg).astype(np.float32)).cuda()
-    monkeypatch.setenv("PCNN_NO_STREAMK", "1")
-    base = Engine(g).forward(x).double().cpu().numpy()
-    monkeypatch.delenv("PCNN_NO_STREAMK")
-    monkeypatch.setenv("PCNN_STREAMK_FILL", "2")
-    eng = Engine(g)
+    from paper_2509_22857_b200 import _lib as L
+    base = Engine(g, options=L.PlanOptions.default(streamk=0)).forward(x).double().cpu().numpy()
+    eng = Engine(g, options=L.PlanOptions.default(streamk_fill=2.0))
     for _ in range(2):
         got = eng.forward(x).double().cpu().numpy()
         assert rel_err(got, base) <= 1e-5, name

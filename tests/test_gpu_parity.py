@@ -56,6 +56,56 @@ def test_reference_eval_dropin(cuda, golden):
     assert_forward_close(reference_eval(g, x), arrays["rn20_fixture/y"][0])
 
 
+def test_reference_eval_loop_reuses_engine(cuda, golden):
+    """A levnet caller looping reference_eval per image (the reference's
+    usage, transforms.py:768-769) pays the lowering / upload / plan capture
+    once: 100 calls cost far less than 100 lowerings, every result matches
+    the golden vector, and an edited graph is lowered again."""
+    import time
+    from paper_2509_22857_b200 import runtime as R
+    manifest, arrays = golden
+    case = next(c for c in manifest["cases"] if c["name"] == "rn20_fixture")
+    g = _load(case["model"])
+    xs, ys = arrays["rn20_fixture/x"], arrays["rn20_fixture/y"]
+    R.clear_engine_cache()
+    t0 = time.perf_counter()
+    assert_forward_close(reference_eval(g, xs[0]), ys[0])
+    first = time.perf_counter() - t0
+    hits0 = R._ENGINES.hits
+    t0 = time.perf_counter()
+    for i in range(100):
+        y = reference_eval(g, xs[i % len(xs)])
+    loop = time.perf_counter() - t0
+    assert_forward_close(y, ys[99 % len(xs)])
+    assert R._ENGINES.hits - hits0 == 100
+    assert loop < 20 * first, (loop, first)
+    # editing a parameter array invalidates the cached engine
+    conv = next(n for n in g.nodes.values() if isinstance(n, ConvNode))
+    conv.bias = conv.bias + 1.0
+    misses = R._ENGINES.misses
+    reference_eval(g, xs[0])
+    assert R._ENGINES.misses == misses + 1
+
+
+def test_forward_host_rejects_bad_buffers(cuda, golden):
+    """forward_host / forward_host_many check shapes, dtypes and staging
+    sizes before libpcnn copies batch * C * H * W floats."""
+    import torch
+    from paper_2509_22857_b200.graph import GraphError
+    manifest, arrays = golden
+    g = _load(next(c for c in manifest["cases"] if c["name"] == "rn20_fixture")["model"])
+    x = arrays["rn20_fixture/x"].astype(np.float32)
+    eng = Engine(g)
+    with pytest.raises(GraphError):
+        eng.forward_host(x[:, :, :-1])  # wrong spatial shape
+    with pytest.raises(GraphError):
+        eng.forward_host(x, x_dev=torch.empty(1, device="cuda"))  # staging too small
+    with pytest.raises(GraphError):
+        eng.forward_host_many([torch.from_numpy(x.astype(np.float64))])  # float64 batch
+    with pytest.raises(GraphError):
+        eng.forward_host_many([torch.from_numpy(x)[:, :, ::2]])  # strided / wrong shape
+
+
 def test_forward_host_e2e_matches_device(cuda, golden):
     import torch
     manifest, arrays = golden

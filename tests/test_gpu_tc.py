@@ -56,9 +56,10 @@ def conv_graph(rng, cin, cout, k, s, p, hw, tail=(), gain=1.0):
     return chain(nodes)
 
 
-def run(g, x, impl):
+def run(g, x, impl, **options):
     import torch
-    eng = Engine(g, impl=impl)
+    from paper_2509_22857_b200 import _lib as L
+    eng = Engine(g, impl=impl, options=L.PlanOptions.default(**options) if options else None)
     y = eng.forward(torch.from_numpy(x.astype(np.float32)).cuda())
     impls = {eng.plan(x.shape[0]).unit_impl(i) for i, u in enumerate(eng.lw.units) if u["kind"] == 2}
     return y.double().cpu().numpy(), impls
@@ -151,11 +152,10 @@ def test_tc_matches_simt_on_resnet20(cuda):
 
 
 @pytest.mark.parametrize("shape", [(16, 32, 3, 1, 1, 16, 8), (64, 128, 3, 1, 1, 8, 4)], ids=["n32", "n128"])
-def test_f16x2_overflow_rows_recomputed(cuda, shape, monkeypatch):
-    """float32 input tensors (PCNN_NO_SPLIT) into the TMEM-A fp16x2 kernel:
+def test_f16x2_overflow_rows_recomputed(cuda, shape):
+    """float32 input tensors (options.split = 0) into the TMEM-A fp16x2 kernel:
     inputs beyond the fp16 range (|x| >= 65520) poison their pixel's
     accumulator row; the epilogue redoes exactly those rows in fp32."""
-    monkeypatch.setenv("PCNN_NO_SPLIT", "1")
     cin, cout, k, s, p, hw, batch = shape
     rng = np.random.default_rng(5)
     g = conv_graph(rng, cin, cout, k, s, p, hw)
@@ -164,7 +164,7 @@ def test_f16x2_overflow_rows_recomputed(cuda, shape, monkeypatch):
     x[1, cin - 1, 0, 0] = -7.0e4
     x[batch - 1, :, hw - 1, :] = 3.0e5
     want = O.eval_batch(g, x)
-    got, impls = run(g, x, 3)
+    got, impls = run(g, x, 3, split=0)
     assert impls == {3}
     np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-5 * np.abs(want).max())
 

@@ -179,3 +179,22 @@ def test_bivariate_matches_polyval2d(rng):
         x, y = rng.uniform(-2, 2, 50), rng.uniform(-2, 2, 50)
         want = np.polynomial.polynomial.polyval2d(x, y, c)
         np.testing.assert_allclose(O.eval_bivariate(c, x, y), want, rtol=1e-12, atol=1e-12)
+
+
+def test_batched_oracle_matches_per_image(golden):
+    """eval_batch_fast (every node kernel with a batch axis; full-batch
+    checker of the GPU tests and the bench parity field) = the per-image
+    reference_eval restatement, on the reference-written golden forwards."""
+    manifest, arrays = golden
+    n = 0
+    for case in manifest["cases"]:
+        if case.get("kind") != "eval" or case["name"] + "/x" not in arrays:
+            continue
+        g = _load(case["model"])
+        x = arrays[case["name"] + "/x"]
+        want = arrays[case["name"] + "/y"]
+        got = O.eval_batch_fast(g, x).reshape(want.shape)
+        assert rel_err(got, O.eval_batch(g, x).reshape(want.shape)) <= 1e-13, case["name"]
+        assert rel_err(got, want) <= 1e-13, case["name"]
+        n += 1
+    assert n >= 10

@@ -13,9 +13,10 @@ g = configs.build(name)
 for d in cfg.redistribution:
     g, _, _ = T.redistribute_sweep(g, d, allow_negative_leading=cfg.allow_negative_leading)
 x = torch.from_numpy(configs.make_input(cfg).astype(np.float32)).cuda()
+from paper_2509_22857_b200 import _lib as _L
 ea = Engine(g); ya = ea.forward(x).cpu().numpy(); pa = ea.plan(cfg.batch)
 os.environ[k] = v
-eb = Engine(g); yb = eb.forward(x).cpu().numpy(); pb = eb.plan(cfg.batch)
+eb = Engine(g, options=_L.options_from_env()); yb = eb.forward(x).cpu().numpy(); pb = eb.plan(cfg.batch)
 print("logits max rel diff", float(np.abs(ya - yb).max() / np.abs(yb).max()))
 for i, u in enumerate(ea.lw.units):
     t = u.get("out", -1)

@@ -21,6 +21,7 @@ import numpy as np
 import torch
 
 from paper_2509_22857_b200 import _lib as L
+from paper_2509_22857_b200 import _lib as _L
 from paper_2509_22857_b200 import configs
 from paper_2509_22857_b200.runtime import Engine
 
@@ -33,7 +34,7 @@ fn.restype = ctypes.c_int
 SLOTS, CTAS = 64, 160
 fn(None, 2)
 cfg = configs.CONFIGS[name]
-eng = Engine(configs.build(name))
+eng = Engine(configs.build(name), options=_L.options_from_env())
 x = torch.from_numpy(configs.make_input(cfg).astype(np.float32)).cuda()
 for _ in range(3):
     eng.forward(x, check=False)

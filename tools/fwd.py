@@ -8,6 +8,7 @@ import numpy as np
 import torch
 
 from paper_2509_22857_b200 import configs
+from paper_2509_22857_b200 import _lib as _L
 from paper_2509_22857_b200.runtime import Engine
 
 ap = argparse.ArgumentParser()
@@ -18,7 +19,7 @@ ap.add_argument("--graph", type=int, default=0)
 args = ap.parse_args()
 cfg = configs.CONFIGS[args.config]
 g = configs.build(args.config)
-eng = Engine(g, impl=args.impl)
+eng = Engine(g, impl=args.impl, options=_L.options_from_env())
 x = torch.from_numpy(configs.make_input(cfg).astype(np.float32)).cuda()
 for _ in range(args.iters):
     y = eng.forward(x, use_graph=bool(args.graph))

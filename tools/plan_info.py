@@ -3,10 +3,11 @@ import sys, pathlib
 sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
 import numpy as np, torch
 from paper_2509_22857_b200 import configs
+from paper_2509_22857_b200 import _lib as _L
 from paper_2509_22857_b200.runtime import Engine
 name = sys.argv[1] if len(sys.argv) > 1 else "resnet20"
 cfg = configs.CONFIGS[name]
-eng = Engine(configs.build(name))
+eng = Engine(configs.build(name), options=_L.options_from_env())
 p = eng.plan(cfg.batch)
 names = {1: "ingest", 2: "conv", 3: "linear", 8: "localpool", 10: "globalpool", 11: "flatten", 12: "copyout"}
 for i, u in enumerate(eng.lw.units):

@@ -9,13 +9,14 @@ import numpy as np
 import torch
 
 from paper_2509_22857_b200 import configs
+from paper_2509_22857_b200 import _lib as _L
 from paper_2509_22857_b200 import transforms as T
 from paper_2509_22857_b200.runtime import Engine
 
 name = sys.argv[1] if len(sys.argv) > 1 else "resnet20"
 cfg = configs.CONFIGS[name]
 g = configs.build(name)
-eng = Engine(g)
+eng = Engine(g, options=_L.options_from_env())
 direction = cfg.redistribution[0]
 accepted, _ = T.plan_sweep(eng, g, direction, allow_negative_leading=cfg.allow_negative_leading)
 prog = T.compile_sweep(eng, g, direction, accepted, cfg.allow_negative_leading)

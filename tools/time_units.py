@@ -3,12 +3,13 @@ import sys, pathlib, os
 sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
 import numpy as np, torch
 from paper_2509_22857_b200 import configs
+from paper_2509_22857_b200 import _lib as _L
 from paper_2509_22857_b200.runtime import Engine
 name = sys.argv[1] if len(sys.argv) > 1 else "resnet20"
 impl = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 cfg = configs.CONFIGS[name]
 g = configs.build(name)
-eng = Engine(g, impl=impl)
+eng = Engine(g, impl=impl, options=_L.options_from_env())
 x = torch.from_numpy(configs.make_input(cfg).astype(np.float32)).cuda()
 out = eng.forward(x)
 plan = eng.plan(x.shape[0])

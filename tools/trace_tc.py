@@ -4,10 +4,11 @@ import ctypes, os, sys, pathlib
 sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
 import numpy as np, torch
 from paper_2509_22857_b200 import configs, _lib as L
+from paper_2509_22857_b200 import _lib as _L
 from paper_2509_22857_b200.runtime import Engine
 unit = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 g = configs.build(sys.argv[2] if len(sys.argv) > 2 else "resnet20")
-eng = Engine(g)
+eng = Engine(g, options=_L.options_from_env())
 cfgname = sys.argv[2] if len(sys.argv) > 2 else "resnet20"
 x = torch.from_numpy(configs.make_input(configs.CONFIGS[cfgname]).astype(np.float32)).cuda()
 out = eng.forward(x)

@@ -6,6 +6,7 @@ import sys, pathlib
 sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
 import numpy as np, torch
 from paper_2509_22857_b200 import configs
+from paper_2509_22857_b200 import _lib as _L
 from paper_2509_22857_b200.runtime import Engine
 
 name = sys.argv[1] if len(sys.argv) > 1 else "resnet20"
@@ -14,7 +15,7 @@ cfg = configs.CONFIGS[name]
 g = configs.build(name)
 B = cfg.batch
 x = torch.from_numpy(configs.make_input(cfg).astype(np.float32)).cuda()
-engs = [Engine(g) for _ in range(ns)]
+engs = [Engine(g, options=_L.options_from_env()) for _ in range(ns)]
 streams = [torch.cuda.Stream() for _ in range(ns)]
 parts = [x[i * B // ns:(i + 1) * B // ns].contiguous() for i in range(ns)]
 outs = [torch.empty(p.shape[0], 10 if cfg.name != "resnet18" else 1000, device="cuda") for p in parts]
@@ -35,7 +36,7 @@ def timed(fn, reps=20):
     return float(np.median(ts[3:]))
 
 
-full = Engine(g)
+full = Engine(g, options=_L.options_from_env())
 out = torch.empty(B, outs[0].shape[1], device="cuda")
 full.forward(x, out=out)
 print("one plan, batch", B, "ms", round(timed(lambda: full.forward(x, out=out, check=False)), 4))
