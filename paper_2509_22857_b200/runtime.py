@@ -349,28 +349,34 @@ class Engine:
 # drop-in functions: one cached Engine per graph
 # ---------------------------------------------------------------------------
 
+_FIELDS: Dict[type, Tuple[str, ...]] = {}
+
+
 def _param_fingerprint(v):
     if isinstance(v, np.ndarray):
-        flat = v.reshape(-1)
-        step = max(1, flat.size // 61)
-        sample = flat[::step]
-        return ("a", id(v), v.shape, float(sample.sum()) if sample.size else 0.0,
-                float(flat[-1]) if flat.size else 0.0)
+        n = v.size
+        return (id(v), v.shape, v.item(0), v.item(n // 2), v.item(n - 1)) if n else (id(v), v.shape)
     if isinstance(v, (list, tuple)):
         return tuple(_param_fingerprint(x) for x in v)
+    if isinstance(v, dict):
+        return tuple((k, _param_fingerprint(x)) for k, x in v.items())
     return v
 
 
 def graph_signature(g: ModelGraph) -> tuple:
     """Structure + parameter identity of a graph: node ids, kinds, scalar
-    fields, each parameter array's identity, shape and a strided sample of
-    its values, and the ordered edge list.  Cheap (O(nodes)); the reference
+    fields, each parameter array's identity, shape and three sampled
+    values, and the ordered edge list.  Cheap (O(nodes)); the reference
     treats validated graphs as immutable (transforms return copies), so a
     graph whose signature is unchanged reuses its Engine."""
-    nodes = tuple((nid, type(n).__name__,
-                   tuple((f.name, _param_fingerprint(getattr(n, f.name))) for f in dataclasses.fields(n)))
-                  for nid, n in g.nodes.items())
-    return nodes, tuple(g.edges)
+    out = []
+    for nid, n in g.nodes.items():
+        t = type(n)
+        names = _FIELDS.get(t)
+        if names is None:
+            names = _FIELDS[t] = tuple(f.name for f in dataclasses.fields(n))
+        out.append((nid, t, tuple(_param_fingerprint(getattr(n, f)) for f in names)))
+    return tuple(out), tuple(g.edges)
 
 
 class _EngineCache:
@@ -423,8 +429,11 @@ def forward(g: ModelGraph, x, **kw):
     """Batched GPU forward of a graph: numpy or torch (B, C, H, W) -> same kind (B, K).
     The graph's Engine is cached (cached_engine), so repeated calls pay the
     lowering, upload and plan capture once."""
+    return _forward_on(cached_engine(g, **kw), x)
+
+
+def _forward_on(eng: "Engine", x):
     torch = _torch()
-    eng = cached_engine(g, **kw)
     if isinstance(x, np.ndarray):
         xt = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(eng.device)
         return eng.forward(xt).cpu().numpy().astype(np.float64)
@@ -441,4 +450,4 @@ def reference_eval(g: ModelGraph, image) -> np.ndarray:
     want = tuple(eng.lw.shapes[eng.lw.graph.input_id()])
     if image.shape != want:
         raise GraphError(f"input shape {image.shape} != graph input {want}")
-    return forward(g, image[None])[0]
+    return _forward_on(eng, image[None])[0]
