@@ -643,33 +643,36 @@ def run_ours(args):
     changed = {k: v for k, v in options.as_dict().items() if default.get(k) != v}
     if changed:
         line["config"]["plan_options"] = changed
-    if not args.no_parity:
-        line["parity"] = parity_of(main["gr"], main["x_host"], main["out"].cpu().numpy())
     cfg = main["cfg"]
-    # (before the CPU baseline: its worker processes would load the host
-    # thread that drives the wall-clock timing)
-    if not args.no_redist_timing:
-        red = time_redistribution(main["g"], cfg)
-        cpu_ms, n = time_cpu_redistribution(main["g"], cfg)
-        red["cpu_reference_ms_per_call"] = round(cpu_ms, 3)
-        red["cpu_reference"] = (f"oracle port of levnet redistribute_{'/'.join(cfg.redistribution)} per-donor "
-                                f"sweep (transforms.py:423-485), float64, 1 host core, median of {n}")
-        line["redistribution"] = red
+    # every timed measurement first (main, then secondary configs); the
+    # checkers and CPU work afterwards, so their host processes never overlap
+    # a timed region
     secondary = [c for c in args.secondary.split(",") if c and c != args.config] if world == 1 else []
+    checks = [(line, main["gr"], main["x_host"], main["out"].cpu().numpy())]
+    main_g = main["g"]
+    del main
+    torch.cuda.empty_cache()
     if secondary:
         line["secondary"] = {}
-        del main
-        torch.cuda.empty_cache()
         for name in secondary:
             res = measure(name, args, rank, world, local, flush, options, e2e=True)
             sub = record(res, args, world)
             sub["metric"] = METRIC
             sub["unit"] = UNIT
-            if not args.no_parity:
-                sub["parity"] = parity_of(res["gr"], res["x_host"], res["out"].cpu().numpy())
             line["secondary"][name] = sub
+            checks.append((sub, res["gr"], res["x_host"], res["out"].cpu().numpy()))
             del res
             torch.cuda.empty_cache()
+    if not args.no_parity:
+        for dst, gr, xh, y in checks:
+            dst["parity"] = parity_of(gr, xh, y)
+    if not args.no_redist_timing:
+        red = time_redistribution(main_g, cfg)
+        cpu_ms, n = time_cpu_redistribution(main_g, cfg)
+        red["cpu_reference_ms_per_call"] = round(cpu_ms, 3)
+        red["cpu_reference"] = (f"oracle port of levnet redistribute_{'/'.join(cfg.redistribution)} per-donor "
+                                f"sweep (transforms.py:423-485), float64, 1 host core, median of {n}")
+        line["redistribution"] = red
     if not args.no_cpu and world == 1:
         g = build_model(args.config)
         ips, done, el, procs = cpu_reference(g, configs.make_input(cfg, batch=64), args.cpu_seconds)

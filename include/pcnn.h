@@ -84,7 +84,13 @@ enum pcnn_pool_kind {
   PCNN_POOL_NONE = 0,
   PCNN_POOL_SUM2 = 1,     /* 2x2/s2 window sum * divisor                    */
   PCNN_POOL_BI2 = 2,      /* two pairwise bivariate pools over a 2x2 window */
-  PCNN_POOL_GLOBAL = 3    /* sum over H*W * divisor -> vector tensor        */
+  PCNN_POOL_GLOBAL = 3,   /* sum over H*W * divisor -> vector tensor        */
+  PCNN_POOL_LOCAL = 4     /* k x k / stride s / pad p window sum * divisor
+                             (k, s, p in pool_geom), e.g. ResNet-18's 3x3/s2
+                             stem pool; the halo-tile kernel computes it in
+                             its epilogue over row bands, other conv kernels
+                             write the unpooled output to plan scratch and
+                             pool in a second launch                        */
 };
 
 /* Offsets are in floats into the packed float32 parameter buffer; -1 = none.
@@ -123,7 +129,7 @@ typedef struct pcnn_unit_desc {
   int64_t tcss_off;              /* conv fp16x2 image of the shared-memory
                                     (halo tile) kernel, or -1                */
   int64_t flags;                 /* PCNN_FLAG_*                              */
-  int64_t reserved;
+  int64_t pool_geom;             /* POOL_LOCAL: k | stride << 8 | pad << 16  */
 } pcnn_unit_desc;
 
 /* ---- parameter packing (float64 master -> float32 compute images) -------*/
@@ -220,8 +226,9 @@ typedef struct pcnn_plan_options {
                                allows; 0: the TMEM-A kernel only           */
   int64_t fuse_projection;  /* 1: a block's 1x1 projection inside its 3x3
                                conv's launch                               */
-  int64_t fuse_block;       /* 1: a residual block's two 3x3 convs in one
-                               launch (halo recompute) where it fits       */
+  int64_t band_pool;        /* 1: a conv's local / 2x2 bivariate pool in
+                               the halo-tile kernel's band epilogue; 0:
+                               conv into plan scratch, then a pool launch  */
   int64_t streamk;          /* 1: stream-K for launches whose whole tiles
                                fill < streamk_fill of the SMs              */
   double streamk_fill;      /* default 0.3                                 */

@@ -27,7 +27,7 @@ PCNN_ERR_TRANSFORM = -4
 UNIT_INGEST, UNIT_CONV, UNIT_LINEAR, UNIT_POLY, UNIT_ADD, UNIT_POLYSKIP = 1, 2, 3, 4, 5, 6
 UNIT_AFFINE, UNIT_LOCALPOOL, UNIT_BIPOOL, UNIT_GLOBALPOOL, UNIT_FLATTEN, UNIT_COPYOUT = 7, 8, 9, 10, 11, 12
 # fused pool kinds
-POOL_NONE, POOL_SUM2, POOL_BI2, POOL_GLOBAL = 0, 1, 2, 3
+POOL_NONE, POOL_SUM2, POOL_BI2, POOL_GLOBAL, POOL_LOCAL = 0, 1, 2, 3, 4
 # pack kinds
 PACK_CAST, PACK_BN_AFFINE, PACK_TC_WEIGHTS, PACK_TC16_WEIGHTS, PACK_TCSS_WEIGHTS = 1, 2, 3, 4, 5
 # conv implementations (pcnn_unit_desc.impl)
@@ -54,11 +54,11 @@ class TensorDesc(ctypes.Structure):
 _UNIT_FIELDS = ("kind", "in_", "in2", "out", "cin", "cout", "kh", "kw", "stride", "pad",
                 "w_off", "b_off", "affine_off", "residual", "res_off", "poly_deg", "poly_off",
                 "pool", "pool_off", "pool_deg", "pool_order", "in_mode", "in_div_off", "impl",
-                "tc_off", "npad", "tc16_off", "tc16_scale_off", "tcss_off", "flags")
+                "tc_off", "npad", "tc16_off", "tc16_scale_off", "tcss_off", "flags", "pool_geom")
 
 
 class UnitDesc(ctypes.Structure):
-    _fields_ = [(n, c_i64) for n in _UNIT_FIELDS] + [("reserved", c_i64)]
+    _fields_ = [(n, c_i64) for n in _UNIT_FIELDS]
 
     def __init__(self, **kw):
         defaults = {"in_": -1, "in2": -1, "out": -1, "w_off": -1, "b_off": -1, "affine_off": -1,
@@ -86,7 +86,7 @@ class RewriteDesc(ctypes.Structure):
                [("value", c_f64), ("f", Factor * MAX_FACTORS)]
 
 
-_OPT_INT_FIELDS_A = ("size", "split", "halo_tiles", "fuse_projection", "fuse_block", "streamk")
+_OPT_INT_FIELDS_A = ("size", "split", "halo_tiles", "fuse_projection", "band_pool", "streamk")
 _OPT_INT_FIELDS_B = ("flag_sync", "prezero", "linear_out", "pdl", "graph", "ss_mt", "ss_share", "ss_psub",
                      "ss_wres", "tc_stage", "timeline", "debug")
 
@@ -115,7 +115,7 @@ class PlanOptions(ctypes.Structure):
 # Only these helpers read the environment; Engine() uses explicit options.
 ENV_OPTIONS = {
     "PCNN_NO_SPLIT": ("split", 0), "PCNN_NO_SS": ("halo_tiles", 0), "PCNN_NO_PROJ_FUSE": ("fuse_projection", 0),
-    "PCNN_NO_BLOCK_FUSE": ("fuse_block", 0), "PCNN_NO_STREAMK": ("streamk", 0), "PCNN_FLAGS": ("flag_sync", int),
+    "PCNN_NO_BAND": ("band_pool", 0), "PCNN_BAND": ("band_pool", int), "PCNN_NO_STREAMK": ("streamk", 0), "PCNN_FLAGS": ("flag_sync", int),
     "PCNN_NO_PREZERO": ("prezero", 0), "PCNN_NO_LINEAR_OUT": ("linear_out", 0), "PCNN_NO_PDL": ("pdl", 0),
     "PCNN_NO_GRAPH": ("graph", 0), "PCNN_SS_MT": ("ss_mt", int), "PCNN_SS_SHARE": ("ss_share", int),
     "PCNN_SS_PSUB": ("ss_psub", int), "PCNN_SS_WRES": ("ss_wres", int), "PCNN_TC_NOSTAGE": ("tc_stage", 0),

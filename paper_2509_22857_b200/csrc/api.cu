@@ -76,6 +76,11 @@ struct pcnn_plan {
   int* status_host = nullptr;  // pinned copy written by pcnn_forward_host
   pcnn_plan_options opt;
   KOpts kopt;
+  // PCNN_POOL_LOCAL convs not run by the halo-tile band epilogue: unpooled
+  // output in plan scratch (float32), then this pooling launch
+  std::vector<EltArgs> post_pool;
+  std::vector<char> has_post_pool;
+  float* scratch = nullptr;
   // launch timeline (options.timeline): [n_units][2] (common.cuh tl_mark)
   unsigned long long* tl_dev = nullptr;
   unsigned long long* tl_host = nullptr;
@@ -224,9 +229,18 @@ int build_conv(pcnn_plan* p, int ui, ConvArgs& a) {
   EpiParams& e = a.epi;
   e.cout = (int)u.cout;
   e.npad = out.cpad();
+  e.pool_k = (int)(u.pool_geom & 0xff);
+  e.pool_s = (int)((u.pool_geom >> 8) & 0xff);
+  e.pool_pad = (int)((u.pool_geom >> 16) & 0xff);
   if (u.pool == PCNN_POOL_GLOBAL) {
     if (out.h != 1 || out.w != 1 || out.c != u.cout)
       return fail(PCNN_ERR_INVALID, "global-pool conv needs a (cout,) output");
+  } else if (u.pool == PCNN_POOL_LOCAL) {
+    if (e.pool_k < 1 || e.pool_s < 1 || e.pool_pad < 0 || e.pool_pad >= e.pool_k)
+      return fail(PCNN_ERR_INVALID, "conv unit " + std::to_string(ui) + ": bad local pool geometry");
+    if (out.h != (ho + 2 * e.pool_pad - e.pool_k) / e.pool_s + 1 ||
+        out.w != (wo + 2 * e.pool_pad - e.pool_k) / e.pool_s + 1 || out.c != u.cout)
+      return fail(PCNN_ERR_INVALID, "conv unit " + std::to_string(ui) + ": pooled output tensor shape mismatch");
   } else {
     int ho_o = a.pm.order == kWindow ? a.pm.hp : ho, wo_o = a.pm.order == kWindow ? a.pm.wp : wo;
     if (out.h != ho_o || out.w != wo_o || out.c != u.cout)
@@ -245,6 +259,14 @@ int build_conv(pcnn_plan* p, int ui, ConvArgs& a) {
   e.pool_deg = (int)u.pool_deg;
   e.pool_order = (int)u.pool_order;
   e.out = out;
+  if (u.pool == PCNN_POOL_LOCAL) {
+    // the other conv kernels see an unpooled conv: plan_local_pools either
+    // hands the pool to the halo-tile kernel's band epilogue or gives the
+    // conv a scratch output and a pooling launch
+    e.pool = PCNN_POOL_NONE;
+    e.out.h = ho;
+    e.out.w = wo;
+  }
   if (u.residual) {
     if (u.in2 < 0) return fail(PCNN_ERR_INVALID, "residual unit without skip tensor");
     e.skip = p->views[u.in2];
@@ -285,6 +307,11 @@ void enqueue_unit(pcnn_plan* p, int ui, const float* x, float* logits, cudaStrea
         launch_conv_tc(a, s);
       }
       else launch_conv_simt(a, s);
+      if (p->has_post_pool[ui]) {
+        EltArgs e = p->post_pool[ui];
+        e.tl = tl;
+        launch_eltwise(e, s);
+      }
       break;
     }
     case PCNN_UNIT_LINEAR: {
@@ -343,6 +370,88 @@ void enqueue_all(pcnn_plan* p, const float* x, float* logits, cudaStream_t s) {
   if (p->tl_dev) { r.p[k] = reinterpret_cast<uint32_t*>(p->tl_dev); r.n[k++] = 4 * (int64_t)p->units.size(); }
   if (k) plan_reset_kernel<<<1, 256, 0, s>>>(r);
   for (int i = 0; i < (int)p->units.size(); ++i) enqueue_unit(p, i, x, logits, s, true);
+}
+
+// Pooled convs (PCNN_POOL_LOCAL, e.g. ResNet-18's stem followed by its
+// 3x3/s2 pool; PCNN_POOL_BI2 on the halo-tile kernel): with options.band_pool
+// the pool runs in the halo-tile kernel's band epilogue (conv_ss.cu
+// band_item) -- the unpooled map never reaches global memory; otherwise the
+// conv writes a float32 scratch map and a pooling launch follows (BI2 on the
+// TMEM-A / SIMT kernels keeps its window-order fused epilogue).
+int plan_local_pools(pcnn_plan* p) {
+  const int n = (int)p->units.size();
+  p->post_pool.assign(n, EltArgs());
+  p->has_post_pool.assign(n, 0);
+  size_t need = 0;
+  std::vector<int> fallback;
+  for (int i = 0; i < n; ++i) {
+    const pcnn_unit_desc& u = p->units[i];
+    if (u.kind != PCNN_UNIT_CONV || !(u.pool == PCNN_POOL_LOCAL || u.pool == PCNN_POOL_BI2)) continue;
+    ConvArgs& a = p->conv_args[i];
+    if (u.pool == PCNN_POOL_BI2 && p->impl[i] != 5) continue;  // window-order epilogue of the other kernels
+    ConvArgs b = a;
+    b.epi.pool = (int)u.pool;
+    b.epi.out = p->views[u.out];
+    if (p->impl[i] == 5 && p->opt.band_pool && conv_ss_supported(b)) {
+      a = b;
+      continue;
+    }
+    if (u.pool == PCNN_POOL_LOCAL) {
+      if (p->impl[i] == 3 && !conv_tc_supported(a)) p->impl[i] = 1;
+    } else {
+      // BI2 behind a halo-tile conv: conv_ss into scratch, then the bivariate pass
+      a.pm.order = kPlain;
+      a.epi.pool = PCNN_POOL_NONE;
+      if (!conv_ss_supported(a))
+        return fail(PCNN_ERR_UNSUPPORTED, "unit " + std::to_string(i) + ": pooled halo-tile conv");
+    }
+    fallback.push_back(i);
+    const TensorView& o = p->views[u.out];
+    need += (size_t)p->batch * o.cpad() * a.pm.ho * a.pm.wo;
+  }
+  if (fallback.empty()) return PCNN_OK;
+  if (cudaMalloc(&p->scratch, need * sizeof(float)) != cudaSuccess)
+    return fail(PCNN_ERR_CUDA, "local-pool scratch allocation failed");
+  size_t off = 0;
+  for (int i : fallback) {
+    const pcnn_unit_desc& u = p->units[i];
+    ConvArgs& a = p->conv_args[i];
+    const TensorView& o = p->views[u.out];
+    TensorView t = o;
+    t.base = p->scratch + off;
+    t.h = a.pm.ho;
+    t.w = a.pm.wo;
+    t.split = 0;
+    t.flag = nullptr;
+    off += (size_t)p->batch * o.cpad() * t.h * t.w;
+    const int kind = (int)u.pool;
+    a.epi.out = t;
+    a.epi.pool = PCNN_POOL_NONE;
+    a.pm.order = kPlain;
+    EltArgs& e = p->post_pool[i];
+    e.kind = PCNN_UNIT_LOCALPOOL;
+    e.batch = p->batch;
+    e.in = t;
+    e.out = o;
+    e.p = a.epi.pool_p;
+    e.stride = o.cpad();
+    if (kind == PCNN_POOL_BI2) {  // bipool2_kernel: the 2x2 window through both bivariate stages
+      e.k = 2;
+      e.st = 2;
+      e.pad = 0;
+      e.pool = PCNN_POOL_BI2;
+      e.deg = a.epi.pool_deg;
+      e.axis = a.epi.pool_order;
+    } else {
+      e.k = a.epi.pool_k;
+      e.st = a.epi.pool_s;
+      e.pad = a.epi.pool_pad;
+      e.pool = PCNN_POOL_NONE;
+    }
+    p->has_post_pool[i] = 1;
+    p->launches += 1;
+  }
+  return PCNN_OK;
 }
 
 // A residual block's 1x1 projection (unit i + 1) reads the same input with
@@ -538,7 +647,7 @@ void pcnn_plan_options_default(pcnn_plan_options* o) {
   o->split = 1;
   o->halo_tiles = 1;
   o->fuse_projection = 1;
-  o->fuse_block = 1;
+  o->band_pool = 0;  // measured slower than conv + pool pass on RN18 / VGG
   o->streamk = 1;
   o->streamk_fill = 0.3;
   o->flag_sync = 0;
@@ -651,6 +760,13 @@ int pcnn_plan_create_ex(const pcnn_unit_desc* units, int n_units, const pcnn_ten
     cudaMemset(p->tl_dev, 0, tb);
   }
   choose_formats(p);
+  {
+    const int rc = plan_local_pools(p);
+    if (rc != PCNN_OK) {
+      pcnn_plan_destroy(p);
+      return rc;
+    }
+  }
   // a global-pool conv right after a halo-tile conv: that kernel zeroes the
   // sums in its prologue (keeps the launch chain free of memset nodes, which
   // would break programmatic dependent launch)
@@ -694,6 +810,7 @@ int pcnn_plan_destroy(pcnn_plan* p) {
   if (p->status_slots) cudaFree(p->status_slots);
   if (p->status_pinned) cudaFreeHost(p->status_pinned);
   if (p->status_host) cudaFreeHost(p->status_host);
+  if (p->scratch) cudaFree(p->scratch);
   delete p;
   return PCNN_OK;
 }

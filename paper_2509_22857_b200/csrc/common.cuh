@@ -160,6 +160,25 @@ __device__ __forceinline__ void store16_split_at(const TensorView& t, int64_t e,
   if (!ok) atomicExch(t.flag, 1);
 }
 
+// store 8 consecutive channels (ch % 8 == 0) in the tensor's format
+__device__ __forceinline__ void store8_any(const TensorView& t, int b, int ch, int y, int x, const float* v) {
+  if (!t.split) {
+    float4* o = reinterpret_cast<float4*>(t.base + t.index(b, ch, y, x));
+    o[0] = make_float4(v[0], v[1], v[2], v[3]);
+    o[1] = make_float4(v[4], v[5], v[6], v[7]);
+    return;
+  }
+  const int64_t e = t.sindex(b, ch, y, x);
+  const float s = t.sstore;
+  uint32_t hi[4], lo[4];
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) ok &= split_pair(v[2 * i] * s, v[2 * i + 1] * s, hi[i], lo[i]);
+  *reinterpret_cast<uint4*>(t.hi() + e) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+  *reinterpret_cast<uint4*>(t.lo() + e) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  if (!ok) atomicExch(t.flag, 1);
+}
+
 // store 16 consecutive channels (ch % 16 == 0; one block when fp32, cb >= 16):
 // whole 32-byte sectors per thread in both formats
 __device__ __forceinline__ void store16_any(const TensorView& t, int b, int ch, int y, int x, const float* v) {
@@ -386,6 +405,43 @@ __device__ __forceinline__ float4 bivariate4(const float* __restrict__ coef, int
                                  fmaf(acc.w, x.w, r.w));
   }
   return acc;
+}
+
+// bivariate4 with the degree a compile-time constant: the loops unroll, so
+// all coefficient loads issue up front instead of one dependent load per
+// Horner step (the band epilogue runs these on few warps)
+template <int D>
+__device__ __forceinline__ float4 bivariate4_t(const float* __restrict__ coef, int64_t stride, int ch, float4 x,
+                                               float4 y) {
+  float4 c[D + 1][D + 1];
+#pragma unroll
+  for (int i = 0; i <= D; ++i)
+#pragma unroll
+    for (int j = 0; j + i <= D; ++j)
+      c[i][j] = __ldg(reinterpret_cast<const float4*>(coef + (int64_t)(i * (D + 1) + j) * stride + ch));
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int i = D; i >= 0; --i) {
+    float4 r = c[i][D - i];
+#pragma unroll
+    for (int j = D - i - 1; j >= 0; --j)
+      r = make_float4(fmaf(r.x, y.x, c[i][j].x), fmaf(r.y, y.y, c[i][j].y), fmaf(r.z, y.z, c[i][j].z),
+                      fmaf(r.w, y.w, c[i][j].w));
+    acc = (i == D) ? r
+                   : make_float4(fmaf(acc.x, x.x, r.x), fmaf(acc.y, x.y, r.y), fmaf(acc.z, x.z, r.z),
+                                 fmaf(acc.w, x.w, r.w));
+  }
+  return acc;
+}
+__device__ __forceinline__ float4 bivariate4_any(const float* __restrict__ coef, int64_t stride, int d, int ch,
+                                                 float4 x, float4 y) {
+  switch (d) {
+    case 1: return bivariate4_t<1>(coef, stride, ch, x, y);
+    case 2: return bivariate4_t<2>(coef, stride, ch, x, y);
+    case 3: return bivariate4_t<3>(coef, stride, ch, x, y);
+    case 4: return bivariate4_t<4>(coef, stride, ch, x, y);
+    default: return bivariate4(coef, stride, d, ch, x, y);
+  }
 }
 
 // Quadratic join S(x, y) with coefficient vectors x2 y2 xy x y c.

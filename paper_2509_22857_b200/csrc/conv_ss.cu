@@ -98,6 +98,23 @@ struct SsParams {
   const float* pwscale;
   uint32_t pb_bytes;        // 64 * nt per chunk
   int ptoff;                // centre tap offset (toff of the projection's input position)
+  // band mode (a pooled epilogue, PCNN_POOL_LOCAL k x k / s / pad or
+  // PCNN_POOL_BI2 2x2 bivariate): CTA c owns the pooled rows [c R / G,
+  // (c + 1) R / G) of all R = batch * hpo pooled rows and walks the conv
+  // rows they need in order, one tile per `brows` grid rows (a pooled row
+  // whose window overlaps the previous band recomputes one conv row).  The
+  // epilogue stages each 16-channel item in shared memory, and the thread
+  // owning pooled column px folds the item's rows into a two-row ring of
+  // window partials (owned per channel chunk by one warpgroup, so no
+  // atomics) and stores each pooled row when its last conv row is in.
+  int band;
+  int brows;                // grid rows per tile (brows * wp <= 128)
+  int pk, ps, pp;           // pool window, stride, pad
+  int ho, wo;               // conv output rows / columns per image
+  int hpo, wpo;             // pooled rows / columns
+  int prows;                // batch * hpo
+  int nchunk;               // npad / 16 (ring chunks)
+  int nbands;               // bands; CTA c runs band c % nbands of n-tile c / nbands
 };
 
 // PCNN_TC_DEBUG bit 32: CTA 0 records clock64 events (see pcnn_ss_trace)
@@ -199,7 +216,59 @@ struct Seg {
   int tile, q0, q1;
   int owner;  // holds the tile's last chunk: runs the epilogue
   int c_lo;   // owner: first CTA holding earlier chunks of the tile (-1: none)
+  int n_tile;
+  int64_t g0;  // grid position of the tile's first output row
+  int r, rows;  // band mode: first grid row, grid rows in the tile
 };
+
+// band mode: this CTA's pooled rows [P0, P1) and conv grid rows [r0, r1]
+struct Band {
+  int P0, P1, r0, r1, tiles;
+};
+__device__ __forceinline__ Band band_of(const SsParams& P) {
+  Band bd;
+  const int G = P.nbands, c = (int)blockIdx.x % P.nbands;
+  bd.P0 = (int)((int64_t)c * P.prows / G);
+  bd.P1 = (int)((int64_t)(c + 1) * P.prows / G);
+  bd.tiles = 0;
+  bd.r0 = bd.r1 = 0;
+  if (bd.P1 <= bd.P0) return bd;
+  const int b0 = bd.P0 / P.hpo, py0 = bd.P0 - b0 * P.hpo;
+  const int b1 = (bd.P1 - 1) / P.hpo, py1 = bd.P1 - 1 - b1 * P.hpo;
+  const int y0 = max(0, P.ps * py0 - P.pp), y1 = min(P.ho - 1, P.ps * py1 - P.pp + P.pk - 1);
+  bd.r0 = b0 * P.hp + y0 + 1;  // shared grid: image row y of b is grid row b (H + 1) + y + 1
+  bd.r1 = b1 * P.hp + y1 + 1;
+  bd.tiles = (bd.r1 - bd.r0 + P.brows) / P.brows;
+  return bd;
+}
+
+__device__ __forceinline__ bool seg_at(int i, int total_tiles, int nq, bool streamk, Seg& s);
+
+// segment i of this CTA in any mode (whole tiles, stream-K, bands)
+template <bool BAND>
+__device__ __forceinline__ bool seg_get(const SsParams& P, const Band& bd, int i, int total_tiles, bool streamk,
+                                        Seg& s) {
+  if constexpr (BAND) {
+    if (i >= bd.tiles) return false;
+    s.n_tile = (int)blockIdx.x / P.nbands;
+    const int local = i;
+    s.tile = i;
+    s.q0 = 0;
+    s.q1 = P.nq;
+    s.owner = 1;
+    s.c_lo = -1;
+    s.r = bd.r0 + local * P.brows;
+    s.rows = min(P.brows, bd.r1 - s.r + 1);
+    s.g0 = 1 + (int64_t)s.r * P.wp;
+    return true;
+  }
+  if (!seg_at(i, total_tiles, P.nq, streamk, s)) return false;
+  s.n_tile = s.tile / P.m_tiles;
+  s.g0 = (int64_t)(s.tile - s.n_tile * P.m_tiles) * kTileM * P.mt;
+  s.r = s.rows = 0;
+  return true;
+}
+
 __device__ __forceinline__ bool seg_at(int i, int total_tiles, int nq, bool streamk, Seg& s) {
   if (!streamk) {
     s.tile = (int)blockIdx.x + i * (int)gridDim.x;
@@ -262,10 +331,223 @@ __device__ __forceinline__ void flag_wait(const FlagDep& d, int64_t lo, int64_t 
   }
 }
 
+constexpr int kStgPitch = 20;  // staged floats per row (16 + 4: conflict-free 16-byte reads)
+
+// Band mode, one item = 16 channels chb..chb+15 of the tile's grid rows
+// [r, r + rows) (v: this thread's row = tile position `row`, per-element
+// epilogue applied).  Pooled rows finish in the ring of window partials,
+// [ns slots][nchunk][wpo][16] (BI2 order 1: two such rings).
+//
+// POOL_LOCAL (s = 2; k = 3, p = 1 or k = 2, p = 0; one grid row per tile,
+//   so tile position = column x): the even lane x = 2 px sums its window
+//   row from its neighbours' registers (shuffles; the window of px = 16 w
+//   crossing a warp boundary gets lane 31's value through shared memory),
+//   then adds it to the ring slot of every pooled row the conv row feeds;
+//   the conv row finishing a pooled row scales by the divisor and stores it.
+//   The owner of (px, chunk) is always the same thread: no atomics, no
+//   other synchronisation.
+// POOL_BI2 (2 x 2, any rows per tile): the item is staged; pair (j, px)
+//   of the item goes to thread j * wpo + px; even conv rows write their
+//   first-stage result (order 0: S1(q00, q01); order 1: q00, q01) to the
+//   ring, a second barrier, odd rows finish S2 and store (epi_tc.cuh's tree).
+__device__ __forceinline__ void band_item(const SsParams& P, const EpiParams& e, const Band& bd, float* ring,
+                                          float* stg, float* bnd, int r, int rows, int row, int lane, int wq, int ew,
+                                          int chb, float* v, float pdiv) {
+  const int chunk = chb >> 4;
+  const int ns = P.brows / 2 + 2;
+  if (e.pool == PCNN_POOL_LOCAL) {
+    // lane x holds column x of the tile's conv row.  Window px (s = 2):
+    // (3, 1): columns 2px-1 .. 2px+1; (2, 0): 2px, 2px+1.  Channels 0-7 of
+    // window px belong to lane 2px, channels 8-15 to lane 2px+1, so every
+    // lane sums 8 channels of three (two) columns: even lanes x-1, x, x+1,
+    // odd lanes x-2, x-1, x (k = 2: x, x+1 / x-1, x).
+    const bool odd = row & 1;
+    if (row >= P.wo) {  // columns past the image (the shared zero border): padding
+#pragma unroll
+      for (int c = 0; c < 16; ++c) v[c] = 0.f;
+    }
+    float l1[16], h8[8];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) l1[c] = __shfl_up_sync(0xffffffffu, v[c], 1);
+    if (P.pk == 3) {
+      float r1[8], l2[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) r1[c] = __shfl_down_sync(0xffffffffu, v[c], 1);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) l2[c] = __shfl_up_sync(0xffffffffu, v[8 + c], 2);
+      // lane 31's column for lanes 0 and 1 of the next warp
+      if (lane == 31)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          *reinterpret_cast<float4*>(bnd + wq * 16 + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + ew) : "memory");
+      if (lane < 2) {
+        float pv[16];
+        if (wq > 0) {
+          lds16(bnd + (wq - 1) * 16, pv);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 16; ++c) pv[c] = 0.f;  // column -1: zero padding
+        }
+        if (lane == 0) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) l1[c] = pv[c];
+        } else {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) l2[c] = pv[8 + c];
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) h8[c] = odd ? v[8 + c] + l1[8 + c] + l2[c] : v[c] + l1[c] + r1[c];
+    } else {
+      float r1[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) r1[c] = __shfl_down_sync(0xffffffffu, v[c], 1);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) h8[c] = odd ? v[8 + c] + l1[8 + c] : v[c] + r1[c];
+    }
+    const int px = row >> 1, ch8 = chb + (odd ? 8 : 0);
+    if (px >= P.wpo || r <= 0) return;
+    const int b = (int)P.div_h1.div((uint32_t)(r - 1)), y = r - 1 - b * P.hp;
+    if (y >= P.ho) return;  // shared border row between images
+    // pooled rows fed by conv row y; ring slot = pooled row & 1 (one conv
+    // row per tile, so at most two pooled rows are open)
+    float* const ring_px = ring + (chunk * P.wpo + px) * 16 + (odd ? 8 : 0);
+    const int slot_stride = P.nchunk * P.wpo * 16;
+    auto in_band = [&](int py) { const int pr = b * P.hpo + py; return py < P.hpo && pr >= bd.P0 && pr < bd.P1; };
+    auto finish = [&](int py, const float* a) {
+      float o[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) o[c] = ch8 + c < e.cout ? (a[c] + h8[c]) * pdiv : 0.f;
+      store8_any(e.out, b, ch8, py, px, o);
+    };
+    auto keep = [&](int py, const float* a) {
+      float* sl = ring_px + ((b * P.hpo + py) & 1) * slot_stride;
+      *reinterpret_cast<float4*>(sl) = make_float4(a[0] + h8[0], a[1] + h8[1], a[2] + h8[2], a[3] + h8[3]);
+      *reinterpret_cast<float4*>(sl + 4) = make_float4(a[4] + h8[4], a[5] + h8[5], a[6] + h8[6], a[7] + h8[7]);
+    };
+    const float zero[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    auto ring_of = [&](int py, float* a) {
+      const float* sl = ring_px + ((b * P.hpo + py) & 1) * slot_stride;
+      const float4 u = *reinterpret_cast<const float4*>(sl), w = *reinterpret_cast<const float4*>(sl + 4);
+      a[0] = u.x; a[1] = u.y; a[2] = u.z; a[3] = u.w; a[4] = w.x; a[5] = w.y; a[6] = w.z; a[7] = w.w;
+    };
+    if (P.pk == 3) {
+      if (!(y & 1)) {  // rows 2py-1, [2py], 2py+1 of pooled row py = y / 2
+        const int py = y >> 1;
+        if (in_band(py)) {
+          float a[8];
+          if (py == 0) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) a[c] = 0.f;
+          } else {
+            ring_of(py, a);
+          }
+          if (y == P.ho - 1) finish(py, a);
+          else keep(py, a);
+        }
+      } else {         // last row of py0 = (y - 1) / 2, first row of py1 = (y + 1) / 2
+        const int py0 = (y - 1) >> 1, py1 = (y + 1) >> 1;
+        if (in_band(py0)) {
+          float a[8];
+          ring_of(py0, a);
+          finish(py0, a);
+        }
+        if (in_band(py1)) keep(py1, zero);
+      }
+    } else {           // (2, 0): rows 2py, 2py+1
+      const int py = y >> 1;
+      if (in_band(py)) {
+        if (!(y & 1)) {
+          keep(py, zero);
+        } else {
+          float a[8];
+          ring_of(py, a);
+          finish(py, a);
+        }
+      }
+    }
+    return;
+  }
+  // ---- POOL_BI2 ----
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    *reinterpret_cast<float4*>(stg + row * kStgPitch + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  asm volatile("bar.sync %0, 128;" ::"r"(1 + ew) : "memory");
+  const int w = row, nw = rows * P.wpo;
+  int j = 0, px = 0, b = 0, y = -1, py = 0, prow = 0;
+  bool mine = false;
+  if (w < nw) {
+    j = w / P.wpo;
+    px = w - j * P.wpo;
+    const int R = r + j;
+    if (R > 0) {
+      b = (int)P.div_h1.div((uint32_t)(R - 1));
+      y = R - 1 - b * P.hp;
+      py = y >> 1;
+      prow = b * P.hpo + py;
+      mine = y < P.ho && py < P.hpo && prow >= bd.P0 && prow < bd.P1;
+    }
+  }
+  const int64_t nc = (int64_t)(e.pool_deg + 1) * (e.pool_deg + 1) * e.npad;
+  float* sl = ring + (((prow % ns) * P.nchunk + chunk) * P.wpo + px) * 16;
+  float* sl2 = sl + ns * P.nchunk * P.wpo * 16;  // order 1: q01 of the even row
+  float q0[16], q1[16];
+  if (mine) {
+    const float* rowp = stg + (j * P.wp + 2 * px) * kStgPitch;
+    lds16(rowp, q0);
+    lds16(rowp + kStgPitch, q1);
+    if (!(y & 1)) {
+      if (e.pool_order == 0) {
+#pragma unroll
+        for (int g = 0; g < 4; ++g)
+          *reinterpret_cast<float4*>(sl + 4 * g) =
+              bivariate4_any(e.pool_p, e.npad, e.pool_deg, chb + 4 * g,
+                         make_float4(q0[4 * g], q0[4 * g + 1], q0[4 * g + 2], q0[4 * g + 3]),
+                         make_float4(q1[4 * g], q1[4 * g + 1], q1[4 * g + 2], q1[4 * g + 3]));
+      } else {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          *reinterpret_cast<float4*>(sl + 4 * g) = make_float4(q0[4 * g], q0[4 * g + 1], q0[4 * g + 2], q0[4 * g + 3]);
+          *reinterpret_cast<float4*>(sl2 + 4 * g) = make_float4(q1[4 * g], q1[4 * g + 1], q1[4 * g + 2], q1[4 * g + 3]);
+        }
+      }
+    }
+  }
+  asm volatile("bar.sync %0, 128;" ::"r"(1 + ew) : "memory");
+  if (!mine || !(y & 1)) return;
+  float o[16];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    const int ch = chb + 4 * g;
+    const float4 x0 = make_float4(q0[4 * g], q0[4 * g + 1], q0[4 * g + 2], q0[4 * g + 3]);
+    const float4 x1 = make_float4(q1[4 * g], q1[4 * g + 1], q1[4 * g + 2], q1[4 * g + 3]);
+    float4 u, ww;
+    if (e.pool_order == 0) {
+      u = *reinterpret_cast<const float4*>(sl + 4 * g);
+      ww = bivariate4_any(e.pool_p, e.npad, e.pool_deg, ch, x0, x1);
+    } else {
+      u = bivariate4_any(e.pool_p, e.npad, e.pool_deg, ch, *reinterpret_cast<const float4*>(sl + 4 * g), x0);
+      ww = bivariate4_any(e.pool_p, e.npad, e.pool_deg, ch, *reinterpret_cast<const float4*>(sl2 + 4 * g), x1);
+    }
+    const float4 r4 = bivariate4_any(e.pool_p + nc, e.npad, e.pool_deg, ch, u, ww);
+    o[4 * g] = ch < e.cout ? r4.x : 0.f;
+    o[4 * g + 1] = ch + 1 < e.cout ? r4.y : 0.f;
+    o[4 * g + 2] = ch + 2 < e.cout ? r4.z : 0.f;
+    o[4 * g + 3] = ch + 3 < e.cout ? r4.w : 0.f;
+  }
+  store16_any(e.out, b, chb, py, px, o);
+}
+
 // SK: stream-K segments (a separate instantiation: the whole-tile kernel
 // keeps its registers and its simpler item walk)
-template <int TAPS, bool SK>
+// POOL: kPoolNone (store, fused projection), kPoolGlobal, kPoolBand -- one
+// epilogue tail per instantiation keeps the epilogue loop's code short
+constexpr int kPoolNone = 0, kPoolGlobal = 1, kPoolBand = 2;
+
+template <int TAPS, bool SK, int POOL>
 __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_constant__ SsParams P) {
+  constexpr bool BAND = POOL == kPoolBand;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   const ConvArgs& a = P.a;
@@ -279,7 +561,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
   constexpr bool streamk = SK;
   const int NP = P.partials, NB = P.acc_bufs;
   const uint32_t set_a = P.concat ? (uint32_t)NP * 2 * P.nt : (uint32_t)(NP + 1) * P.nt;
-  constexpr bool kProj = TAPS == 9;  // projection fusion: 3x3 convs only (keeps the stem's registers)
+  constexpr bool kProj = TAPS == 9 && POOL == kPoolNone;  // projection fusion: 3x3 convs only
   const bool proj = kProj && P.proj;
   const uint32_t set_cols = set_a + (proj ? 2u * P.nt : 0u);  // + projection [main | corr]
   Tracer tr;
@@ -357,10 +639,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       bool fin_all = false, fsk_all = false;
       int dep_seq = 0;
       Seg sg;
-      for (int si = 0; seg_at(si, total_tiles, P.nq, streamk, sg); ++si) {
-        const int tile = sg.tile;
-        const int n_tile = tile / P.m_tiles, m_tile = tile - n_tile * P.m_tiles;
-        const int64_t gs = (int64_t)m_tile * kTileM * P.mt - P.halo;  // grid position of buffer slot 0
+      Band bd = {};
+      if constexpr (BAND) bd = band_of(P);
+      for (int si = 0; seg_get<BAND>(P, bd, si, total_tiles, streamk, sg); ++si) {
+        const int n_tile = sg.n_tile;
+        const int64_t gs = sg.g0 - P.halo;  // grid position of buffer slot 0
         const int64_t cs = gs < 0 ? 0 : gs;
         const int64_t ge = gs + P.span;
         const int64_t ce = ge > P.gtotal ? P.gtotal : ge;
@@ -370,7 +653,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
           // dep_seq hands the acquired state to the epilogue (CTA scope)
           if (a.fin.mode) flag_wait(a.fin, cs, ce, fin_all);
           if (a.fsk.mode) {
-            const int64_t r0 = (int64_t)m_tile * kTileM * P.mt;
+            const int64_t r0 = sg.g0;
             flag_wait(a.fsk, r0, r0 + kTileM * P.mt, fsk_all);
           }
           asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> bulk-copy reads
@@ -468,7 +751,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
     uint32_t ph = 0, acc = 0, acc_ph = 0;
     uint32_t w_seen = P.wres ? 0u : ~0u;  // resident chunks already waited for
     Seg sg;
-    for (int si = 0; seg_at(si, total_tiles, P.nq, streamk, sg); ++si) {
+    Band bd = {};
+    if constexpr (BAND) bd = band_of(P);
+    for (int si = 0; seg_get<BAND>(P, bd, si, total_tiles, streamk, sg); ++si) {
       ptx::mbar_wait(ptx::smem_u32(&S->acc_empty[acc]), acc_ph ^ 1);
       ptx::tc_fence_after();
       const uint32_t d_tile = tmem + acc * P.mt * set_cols;
@@ -564,19 +849,34 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
     // ([buffer][word][thread] x 16 bytes: conflict-free 16-byte reads)
     const uint32_t skq = 256 * 16;
     const uint32_t sk_slot = ptx::smem_u32(ptab + P.etab.rows * e.npad) + threadIdx.x * 16;
+    // band mode: staging [warpgroup][2][128 rows][kStgPitch] then the ring
+    // [2 slots][nchunk][wpo][16] (no residual, so the residual staging area is free)
+    float* band_stage = ptab + ((P.etab.rows * e.npad + 3) & ~3);
+    float* band_bnd = band_stage + 4 * kTileM * kStgPitch;  // [warpgroup][2][4 warps][16]
+    float* band_ring = band_bnd + 4 * 64;
+    const float band_div = (BAND && e.pool == PCNN_POOL_LOCAL) ? __ldg(e.pool_p) : 1.f;
     struct Item {
       int tile, k, n_tile, b, oy, ox, g;
       uint32_t it;  // segment index
       bool valid;
       int owner, c_lo;  // segment: runs the epilogue; first contributing CTA
       int nqs;          // segment chunks (partial accumulators beyond them were not written)
+      int tn;           // segment's n-tile
+      int64_t g0;       // segment's first grid position
+      int r, rows;      // band mode: first grid row, grid rows
     };
+    Band ebd = {};
+    if constexpr (BAND) ebd = band_of(P);
     // this thread's row of sub-tile (k >> lg_nch) of the item's tile -> image, output row / column
     auto locate = [&](Item& x) {
-      const int n_tile = (int)P.div_mt.div(x.tile), m_tile = x.tile - n_tile * P.m_tiles;
-      x.n_tile = n_tile;
-      const int g = (m_tile * P.mt + (x.k >> lg_nch)) * kTileM + row;
+      x.n_tile = x.tn;
+      const int g = (int)x.g0 + (x.k >> lg_nch) * kTileM + row;
       x.g = g;
+      if constexpr (BAND) {  // the pooled store decodes rows itself (band_pool)
+        x.valid = true;
+        x.b = x.oy = x.ox = 0;
+        return;
+      }
       int gy, gx;
       if (P.shared_grid) {
         // position 1 + R (W+1) + x, global row R = b (H+1) + y + 1
@@ -604,8 +904,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       for (;;) {
         ++x.it;
         Seg sx;
-        if (!seg_at((int)x.it, total_tiles, P.nq, streamk, sx)) return false;
+        if (!seg_get<BAND>(P, ebd, (int)x.it, total_tiles, streamk, sx)) return false;
         x.tile = sx.tile;
+        x.tn = sx.n_tile;
+        x.g0 = sx.g0;
+        x.r = sx.r;
+        x.rows = sx.rows;
         if constexpr (SK) {
           x.owner = sx.owner;
           x.c_lo = sx.c_lo;
@@ -769,12 +1073,26 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
               }
             }
           }
-          if (kProj && pj)
-            epi_chunk16(P.pe, petab, v, pwsc, sk, chan(cur), cur.valid, cur.valid ? cur.b : 0, cur.oy, cur.ox, lane,
-                        -1, P.pe.out.sstore);
-          else
-            epi_chunk16(e, etab, v, wsc, sk, chan(cur), cur.valid, cur.valid ? cur.b : 0, cur.oy, cur.ox, lane,
-                        P.out_pos ? (int64_t)cur.g * 8 : -1, P.fold_out ? 1.f : e.out.sstore);
+          // one epilogue body per instantiation: the projection item shares
+          // it with its own parameters (same code, other table / output)
+          const bool pji = kProj && pj;
+          epi_point16(pji ? P.pe : e, pji ? petab : etab, v, pji ? pwsc : wsc, sk, chan(cur));
+          if constexpr (POOL == kPoolBand) {
+            // the item's 128 conv outputs (bias / affine / poly applied):
+            // the owner of each pooled column folds them in (band_item)
+            if (lane == 0 && warp == 0) tr(P, 2, 0xA00);
+            if (!(P.dbg & 4096))
+              band_item(P, e, ebd, band_ring, band_stage + ((ew * 2 + par) * kTileM) * kStgPitch,
+                        band_bnd + (ew * 2 + par) * 64, cur.r, cur.rows, row, lane, warp & 3, ew, chan(cur), v,
+                        band_div);
+            if (lane == 0 && warp == 0) tr(P, 2, 0xC00);
+          } else if constexpr (POOL == kPoolGlobal) {
+            epi_global16(e, v, chan(cur), cur.valid, cur.valid ? cur.b : 0, lane);
+          } else {
+            epi_store16(pji ? P.pe : e, v, chan(cur), cur.valid, cur.valid ? cur.b : 0, cur.oy, cur.ox,
+                        (!pji && P.out_pos) ? (int64_t)cur.g * 8 : -1,
+                        pji ? P.pe.out.sstore : (P.fold_out ? 1.f : e.out.sstore));
+          }
         }
         if (lane == 0 && warp == 0) tr(P, 2, 0xE00 | c0);
         if (last_of_tile && a.sig_done) {
@@ -823,8 +1141,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
 constexpr uint32_t kSkipStage = 2 * 4 * 256 * 16;
 
 size_t ss_aux_bytes(const SsParams& P) {
+  const size_t band =
+      P.band ? 16 + (size_t)(4 * kTileM * kStgPitch + 4 * 64 + 2 * (P.brows / 2 + 2) * P.nchunk * P.wpo * 16) * 4 : 0;
   return ((sizeof(Smem) + 15) & ~size_t(15)) + (size_t)P.etab.rows * P.a.epi.npad * 4 +
-         (P.proj ? (size_t)P.petab.rows * P.pe.npad * 4 : 0) + (P.a.epi.residual ? kSkipStage : 0);
+         (P.proj ? (size_t)P.petab.rows * P.pe.npad * 4 : 0) + (P.a.epi.residual ? kSkipStage : 0) + band;
 }
 
 // nt: output channels per tile (the weight image is packed in tiles of
@@ -836,10 +1156,17 @@ static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub,
   if ((a.stride != 1 && a.stride != 2) || a.kh != a.kw ||
       !((a.kh == 3 && a.pad == 1) || (a.kh == 1 && a.pad == 0) || (a.kh == 4 && a.pad == 1 && a.stride == 1)))
     return false;
-  if (a.epi.pool != PCNN_POOL_NONE && a.epi.pool != PCNN_POOL_GLOBAL) return false;
+  const bool pooled = a.epi.pool == PCNN_POOL_LOCAL || a.epi.pool == PCNN_POOL_BI2;
+  if (a.epi.pool != PCNN_POOL_NONE && a.epi.pool != PCNN_POOL_GLOBAL && !pooled) return false;
   if (!(in.cpad() == 4 || in.cpad() == 8 || in.cpad() % 16 == 0) || a.npad < 16 || a.npad % 16) return false;
   // stride 1 reads the padded grid, stride 2 the parity planes
   if (in.split != (a.stride == 2 ? 2 : 1)) return false;
+  // band mode (pooled epilogue): stride-1 convs on the shared-border grid
+  // whose grid rows fit one 128-row tile, >= 32 channels per tile (an even
+  // number of 16-channel chunks: each warpgroup owns fixed chunks)
+  if (pooled && (a.stride != 1 || a.epi.residual || a.proj || nt < 32 || in.wp > kTileM || a.epi.out.w > kTileM ||
+                 !((a.kh == 3 && a.kw == 3) || (a.kh == 4 && a.kw == 4))))
+    return false;
   const int cpad = in.cpad();
   P.a = a;
   P.b_img_nt = a.npad <= 128 ? a.npad : 128;
@@ -855,6 +1182,32 @@ static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub,
   // and one set of hand-offs serve 256 positions
   P.mt = a.opt.ss_mt ? a.opt.ss_mt : (P.nt <= 32 ? 2 : 1);
   if (force_mt) P.mt = force_mt;
+  P.band = 0;
+  if (pooled) {
+    P.band = 1;
+    P.mt = 1;  // an item is a whole tile's rows (band_pool reads them from one staging buffer)
+    P.brows = a.epi.pool == PCNN_POOL_LOCAL ? 1 : kTileM / in.wp;  // LOCAL: one grid row per tile (band_item)
+    if (a.epi.pool == PCNN_POOL_LOCAL) {
+      P.pk = a.epi.pool_k;
+      P.ps = a.epi.pool_s;
+      P.pp = a.epi.pool_pad;
+    } else {
+      P.pk = 2;
+      P.ps = 2;
+      P.pp = 0;
+    }
+    // LOCAL: s = 2 with (k, p) = (3, 1) or (2, 0) -- a window row is the owner lane and its neighbours
+    if (P.ps != 2 || !((P.pk == 3 && P.pp == 1) || (P.pk == 2 && P.pp == 0))) return false;
+    P.ho = a.pm.ho;
+    P.wo = a.pm.wo;
+    P.hpo = a.epi.out.h;
+    P.wpo = a.epi.out.w;
+    if (P.hpo != (P.ho + 2 * P.pp - P.pk) / P.ps + 1 || P.wpo != (P.wo + 2 * P.pp - P.pk) / P.ps + 1) return false;
+    if (a.epi.pool == PCNN_POOL_BI2 && (2 * P.wpo > P.wo || 2 * P.hpo > P.ho)) return false;
+    P.prows = a.batch * P.hpo;
+    P.nchunk = a.npad / 16;
+    P.nbands = 1;  // set per launch (launch_conv_ss)
+  }
   if (P.mt < 1 || P.mt > 4) P.mt = 1;
   const int tm = kTileM * P.mt;
   P.m_tiles = (int)((P.gtotal + tm - 1) / tm);
@@ -948,7 +1301,6 @@ static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub,
   const size_t budget = 225 * 1024 - 128 - ss_aux_bytes(P);
   P.stages = (int)(budget / P.stage_bytes);
   if (P.stages > kMaxStages) P.stages = kMaxStages;
-  if (P.stages < 2) return false;
   // resident weights when one n-tile covers every output channel and the
   // image leaves room for at least min(4, streamed stages) activation stages
   P.wres = 0;
@@ -968,6 +1320,7 @@ static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub,
       }
     }
   }
+  if (P.stages < 2) return false;  // neither two streamed stages nor resident weights + two stages fit
   P.dbg = a.opt.dbg;
   P.time_slot = -1;
   // accumulators: as many partials as accuracy asks for, then two buffers
@@ -991,6 +1344,7 @@ static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub,
   P.tmem_cols = need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
   // shared epilogue when a tile has an even number of 16-column chunks
   P.share_epi = a.opt.ss_share >= 0 ? a.opt.ss_share : ((P.mt * (P.proj ? 2 : 1) * P.nt / 16) % 2 == 0);
+  if (P.band) P.share_epi = 1;  // chunk k always drains on warpgroup k % 2 (ring ownership)
   P.div_hw = make_fastdiv((uint32_t)(P.hp * P.wp));
   P.div_h1 = make_fastdiv((uint32_t)P.hp);
   P.div_wp = make_fastdiv((uint32_t)P.wp);
@@ -1057,7 +1411,7 @@ bool conv_ss_shape_ok(const ConvArgs& a) {
 
 bool conv_ss_flag_geometry(const ConvArgs& a, FlagDep& d) {
   SsParams P;
-  if (!make_ss_params(a, P)) return false;
+  if (!make_ss_params(a, P) || P.band) return false;
   d.tm = kTileM * P.mt;
   d.m_tiles = P.m_tiles;
   d.gtotal = P.gtotal;
@@ -1077,7 +1431,7 @@ bool conv_ss_proj_ok(const ConvArgs& a, const ConvArgs& proj) {
 bool conv_ss_streamk_wanted(const ConvArgs& a, int nsm, size_t* slot_floats) {
   if (!a.opt.streamk) return false;
   SsParams P;
-  if (!make_ss_params(a, P) || P.nq < 2) return false;
+  if (!make_ss_params(a, P) || P.nq < 2 || P.band) return false;
   const int tiles = P.m_tiles * P.n_tiles;
   // Measured on B200 (streamk option A/B): splitting pays only when whole
   // tiles leave most SMs idle (VGG 2x2 layers: 36 tiles for 148 SMs);
@@ -1108,6 +1462,14 @@ void launch_conv_ss(const ConvArgs& a, cudaStream_t s) {
   const size_t smem = 128 + (size_t)P.stages * P.stage_bytes + P.res_bytes + ss_aux_bytes(P);
   const int tiles = P.m_tiles * P.n_tiles;
   int grid = tiles < nsm ? tiles : nsm;
+  if (P.band) {
+    // bands of at least one tile's worth of pooled rows, n-tiles on separate CTAs
+    const int per_tile = P.brows / P.ps > 0 ? P.brows / P.ps : 1;
+    int nb = (P.prows + per_tile - 1) / per_tile;
+    const int cap = nsm / P.n_tiles > 0 ? nsm / P.n_tiles : 1;
+    P.nbands = nb < cap ? nb : cap;
+    grid = P.nbands * P.n_tiles;
+  }
   if (a.sk_flags) {
     // stream-K: every SM, at least two chunks each (plan_streamk sized the slots for nsm CTAs)
     const int64_t units = (int64_t)tiles * P.nq;
@@ -1115,9 +1477,18 @@ void launch_conv_ss(const ConvArgs& a, cudaStream_t s) {
     if (grid < 1) grid = 1;
   }
   const bool sk = a.sk_flags != nullptr;
-  void (*k)(SsParams) = P.taps == 16 ? (sk ? conv_ss_kernel<16, true> : conv_ss_kernel<16, false>)
-                        : P.taps == 9 ? (sk ? conv_ss_kernel<9, true> : conv_ss_kernel<9, false>)
-                                      : (sk ? conv_ss_kernel<1, true> : conv_ss_kernel<1, false>);
+  void (*k)(SsParams);
+  if (P.band) {
+    k = P.taps == 16 ? conv_ss_kernel<16, false, kPoolBand> : conv_ss_kernel<9, false, kPoolBand>;
+  } else if (a.epi.pool == PCNN_POOL_GLOBAL) {
+    k = P.taps == 16 ? (sk ? conv_ss_kernel<16, true, kPoolGlobal> : conv_ss_kernel<16, false, kPoolGlobal>)
+        : P.taps == 9 ? (sk ? conv_ss_kernel<9, true, kPoolGlobal> : conv_ss_kernel<9, false, kPoolGlobal>)
+                      : (sk ? conv_ss_kernel<1, true, kPoolGlobal> : conv_ss_kernel<1, false, kPoolGlobal>);
+  } else {
+    k = P.taps == 16 ? (sk ? conv_ss_kernel<16, true, kPoolNone> : conv_ss_kernel<16, false, kPoolNone>)
+        : P.taps == 9 ? (sk ? conv_ss_kernel<9, true, kPoolNone> : conv_ss_kernel<9, false, kPoolNone>)
+                      : (sk ? conv_ss_kernel<1, true, kPoolNone> : conv_ss_kernel<1, false, kPoolNone>);
+  }
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (P.dbg & 64) P.time_slot = g_time_next++ % kTimeSlots;
   launch_pdl(k, grid, kThreads, smem, s, a.opt.pdl, P);

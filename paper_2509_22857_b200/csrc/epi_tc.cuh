@@ -106,15 +106,16 @@ __device__ __forceinline__ void epi_skip_decode(const EpiParams& e, const Raw16&
   }
 }
 
-// v: accumulator values of channels [chb, chb + 16), times vscale in true units;
-// sk: their skip values (epi_load_skip); lanes of a warp hold consecutive
-// pixel rows (WINDOW order for 2x2 pools)
-// opos >= 0: the output is a split tensor whose row starts at half index
-// opos (+ channel-group terms), so no (b, y, x) addressing is needed; then
-// ostore is its storage scale (1 when folded into the table, epi_fill_tab)
-__device__ __forceinline__ void epi_chunk16(const EpiParams& e, const EpiTab& T, float* v, float vscale,
-                                            const float* sk, int chb, bool valid, int b, int oy, int ox, int lane,
-                                            int64_t opos = -1, float ostore = 1.f) {
+// ---- the fused epilogue in pieces: epi_point16 (per element), then one of
+// epi_store16 / epi_window16 / epi_global16; kernels instantiate only the
+// pieces their units use (the instruction cache holds one short path), and
+// epi_chunk16 dispatches on e.pool at run time.
+
+// v: accumulator values of channels [chb, chb + 16), times vscale in true
+// units; sk: their skip values (epi_load_skip).  bias -> [affine] ->
+// [residual: + skip | S(v, skip)] -> [polynomial]; padded channels -> 0.
+__device__ __forceinline__ void epi_point16(const EpiParams& e, const EpiTab& T, float* v, float vscale,
+                                            const float* sk, int chb) {
   const float* pt = T.ptab + chb;  // per-channel parameters, shared by all rows
   const int np = e.npad;
   float c[16];
@@ -168,70 +169,78 @@ __device__ __forceinline__ void epi_chunk16(const EpiParams& e, const EpiTab& T,
     for (int j = 0; j < 16; ++j)
       if (chb + j >= e.cout) v[j] = 0.f;
   }
-  if (e.pool == PCNN_POOL_NONE) {
-    // the 16 channels are contiguous (cb >= 16)
-    if (valid) {
-      if (opos >= 0) store16_split_at(e.out, (int64_t)(chb >> 3) * e.out.kstride + opos, v, ostore);
-      else store16_any(e.out, b, chb, oy, ox, v);
-    }
-    return;
+}
+
+// PCNN_POOL_NONE: the 16 channels are contiguous (cb >= 16).  opos >= 0:
+// the output is a split tensor whose row starts at half index opos (+
+// channel-group terms), so no (b, y, x) addressing is needed; then ostore is
+// its storage scale (1 when folded into the table, epi_fill_tab)
+__device__ __forceinline__ void epi_store16(const EpiParams& e, const float* v, int chb, bool valid, int b, int oy,
+                                            int ox, int64_t opos, float ostore) {
+  if (!valid) return;
+  if (opos >= 0) store16_split_at(e.out, (int64_t)(chb >> 3) * e.out.kstride + opos, v, ostore);
+  else store16_any(e.out, b, chb, oy, ox, v);
+}
+
+// SUM2 / BI2 in WINDOW order: lanes 4q..4q+3 hold the (dy, dx) = 00, 01, 10,
+// 11 pixels of window q.  Lane 4q+j pools channels [4j, 4j+4) of window q,
+// so all 32 lanes work: gather those 4 channels of the 4 pixels by shuffles.
+__device__ __forceinline__ void epi_window16(const EpiParams& e, float* v, int chb, bool valid, int b, int oy,
+                                             int ox, int lane) {
+  if (!valid) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = 0.f;
   }
-  if (e.pool != PCNN_POOL_GLOBAL) {
-    // WINDOW order: lanes 4q..4q+3 hold the (dy, dx) = 00, 01, 10, 11 pixels
-    // of window q.  Lane 4q+j pools channels [4j, 4j+4) of window q, so all
-    // 32 lanes work: gather those 4 channels of the 4 pixels by shuffles.
-    if (!valid) {
+  const int j4 = lane & 3, src = lane & ~3;
+  float4 px[4];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] = 0.f;
-    }
-    const int j4 = lane & 3, src = lane & ~3;
-    float4 px[4];
+  for (int pix = 0; pix < 4; ++pix) {
+    float4 mine = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int pix = 0; pix < 4; ++pix) {
-      float4 mine = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        const float a0 = __shfl_sync(0xffffffffu, v[4 * g], src + pix);
-        const float a1 = __shfl_sync(0xffffffffu, v[4 * g + 1], src + pix);
-        const float a2 = __shfl_sync(0xffffffffu, v[4 * g + 2], src + pix);
-        const float a3 = __shfl_sync(0xffffffffu, v[4 * g + 3], src + pix);
-        if (g == j4) mine = make_float4(a0, a1, a2, a3);
-      }
-      px[pix] = mine;
+    for (int g = 0; g < 4; ++g) {
+      const float a0 = __shfl_sync(0xffffffffu, v[4 * g], src + pix);
+      const float a1 = __shfl_sync(0xffffffffu, v[4 * g + 1], src + pix);
+      const float a2 = __shfl_sync(0xffffffffu, v[4 * g + 2], src + pix);
+      const float a3 = __shfl_sync(0xffffffffu, v[4 * g + 3], src + pix);
+      if (g == j4) mine = make_float4(a0, a1, a2, a3);
     }
-    const int ch0 = chb + 4 * j4;
-    float4 r;
-    if (e.pool == PCNN_POOL_SUM2) {
-      const float dv = __ldg(e.pool_p);
-      r = make_float4((px[0].x + px[1].x + px[2].x + px[3].x) * dv, (px[0].y + px[1].y + px[2].y + px[3].y) * dv,
-                      (px[0].z + px[1].z + px[2].z + px[3].z) * dv, (px[0].w + px[1].w + px[2].w + px[3].w) * dv);
-    } else {
-      // bivariate tree: stage 1 pairs along the first axis, stage 2 across
-      const int64_t nc = (int64_t)(e.pool_deg + 1) * (e.pool_deg + 1) * e.npad;
-      const float* s1 = e.pool_p;
-      const float* s2 = e.pool_p + nc;
-      float4 u, w;
-      if (e.pool_order == 0) {  // w first: S1(q0,q1), S1(q2,q3) then S2 along h
-        u = bivariate4(s1, e.npad, e.pool_deg, ch0, px[0], px[1]);
-        w = bivariate4(s1, e.npad, e.pool_deg, ch0, px[2], px[3]);
-      } else {                  // h first: S1(q0,q2), S1(q1,q3) then S2 along w
-        u = bivariate4(s1, e.npad, e.pool_deg, ch0, px[0], px[2]);
-        w = bivariate4(s1, e.npad, e.pool_deg, ch0, px[1], px[3]);
-      }
-      r = bivariate4(s2, e.npad, e.pool_deg, ch0, u, w);
-    }
-    // padded channels (>= cout) stay zero; rows past M are not stored
-    if (ch0 + 0 >= e.cout) r.x = 0.f;
-    if (ch0 + 1 >= e.cout) r.y = 0.f;
-    if (ch0 + 2 >= e.cout) r.z = 0.f;
-    if (ch0 + 3 >= e.cout) r.w = 0.f;
-    if (valid) store4_any(e.out, b, ch0, oy >> 1, ox >> 1, r.x, r.y, r.z, r.w);
-    return;
+    px[pix] = mine;
   }
-  // GLOBAL: a warp's 32 rows belong to at most two images unless the images
-  // are tiny.  The 16 channels x 2 images are reduced over the 32 lanes by a
-  // transposing butterfly (31 shuffles): afterwards lane L holds the sum of
-  // image lo_b + L / 16, channel chb + L % 16, and all lanes add at once.
+  const int ch0 = chb + 4 * j4;
+  float4 r;
+  if (e.pool == PCNN_POOL_SUM2) {
+    const float dv = __ldg(e.pool_p);
+    r = make_float4((px[0].x + px[1].x + px[2].x + px[3].x) * dv, (px[0].y + px[1].y + px[2].y + px[3].y) * dv,
+                    (px[0].z + px[1].z + px[2].z + px[3].z) * dv, (px[0].w + px[1].w + px[2].w + px[3].w) * dv);
+  } else {
+    // bivariate tree: stage 1 pairs along the first axis, stage 2 across
+    const int64_t nc = (int64_t)(e.pool_deg + 1) * (e.pool_deg + 1) * e.npad;
+    const float* s1 = e.pool_p;
+    const float* s2 = e.pool_p + nc;
+    float4 u, w;
+    if (e.pool_order == 0) {  // w first: S1(q0,q1), S1(q2,q3) then S2 along h
+      u = bivariate4(s1, e.npad, e.pool_deg, ch0, px[0], px[1]);
+      w = bivariate4(s1, e.npad, e.pool_deg, ch0, px[2], px[3]);
+    } else {                  // h first: S1(q0,q2), S1(q1,q3) then S2 along w
+      u = bivariate4(s1, e.npad, e.pool_deg, ch0, px[0], px[2]);
+      w = bivariate4(s1, e.npad, e.pool_deg, ch0, px[1], px[3]);
+    }
+    r = bivariate4(s2, e.npad, e.pool_deg, ch0, u, w);
+  }
+  // padded channels (>= cout) stay zero; rows past M are not stored
+  if (ch0 + 0 >= e.cout) r.x = 0.f;
+  if (ch0 + 1 >= e.cout) r.y = 0.f;
+  if (ch0 + 2 >= e.cout) r.z = 0.f;
+  if (ch0 + 3 >= e.cout) r.w = 0.f;
+  if (valid) store4_any(e.out, b, ch0, oy >> 1, ox >> 1, r.x, r.y, r.z, r.w);
+}
+
+// GLOBAL: a warp's 32 rows belong to at most two images unless the images
+// are tiny.  The 16 channels x 2 images are reduced over the 32 lanes by a
+// transposing butterfly (31 shuffles): afterwards lane L holds the sum of
+// image lo_b + L / 16, channel chb + L % 16, and all lanes add at once.
+__device__ __forceinline__ void epi_global16(const EpiParams& e, const float* v, int chb, bool valid, int b,
+                                             int lane) {
   const float div = __ldg(e.pool_p);
   const int lo_b = (int)__reduce_min_sync(0xffffffffu, valid ? (unsigned)b : 0x7fffffffu);
   const int hi_b = (int)__reduce_max_sync(0xffffffffu, valid ? (unsigned)b : 0u);
@@ -257,6 +266,16 @@ __device__ __forceinline__ void epi_chunk16(const EpiParams& e, const EpiTab& T,
 #pragma unroll
   for (int j = 0; j < 16; ++j)
     if (valid && chb + j < e.cout) atomicAdd(e.out.base + (int64_t)b * e.npad + chb + j, v[j] * div);
+}
+
+// the whole epilogue, pool kind chosen at run time (TMEM-A kernel)
+__device__ __forceinline__ void epi_chunk16(const EpiParams& e, const EpiTab& T, float* v, float vscale,
+                                            const float* sk, int chb, bool valid, int b, int oy, int ox, int lane,
+                                            int64_t opos = -1, float ostore = 1.f) {
+  epi_point16(e, T, v, vscale, sk, chb);
+  if (e.pool == PCNN_POOL_NONE) epi_store16(e, v, chb, valid, b, oy, ox, opos, ostore);
+  else if (e.pool == PCNN_POOL_GLOBAL) epi_global16(e, v, chb, valid, b, lane);
+  else epi_window16(e, v, chb, valid, b, oy, ox, lane);
 }
 
 }  // namespace pcnn

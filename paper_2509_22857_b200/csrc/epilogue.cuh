@@ -17,6 +17,7 @@ struct EpiParams {
   int pool;               // pcnn_pool_kind
   const float* pool_p;    // divisor or bivariate coeffs
   int pool_deg, pool_order;
+  int pool_k, pool_s, pool_pad;  // POOL_LOCAL window
   int npad, cout;         // padded / logical output channels
   TensorView skip;        // residual input (same geometry as the conv output)
   TensorView out;         // output tensor (pooled or vector for GLOBAL)

@@ -26,7 +26,6 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Tuple
 
-import os
 
 import numpy as np
 
@@ -567,11 +566,37 @@ class _Builder:
                     and wmeta["kh"] == wmeta["kw"] and st in (1, 2)
                     and ((k == 3 and pd == 1) or (k == 1 and pd == 0) or (k == S2D_K and pd == 1 and st == 1))
                     and ((cp := wmeta["kp"] // (k * k)) in (4, 8) or cp % 16 == 0))
-        window_ok = not ss_shape or os.environ.get("PCNN_FUSE_WINDOW_POOL") == "1"
+        window_ok = not ss_shape
+        # band epilogue of the halo-tile kernel (conv_ss.cu band_pool): a
+        # following local pool or 2x2 bivariate pool computed over row bands
+        # in the conv's epilogue when the conv is stride 1, has >= 32 output
+        # channels and its grid rows (input width + 1) fit a 128-row tile
+        # (and are >= 9 long: tiny maps keep whole tiles / stream-K and a
+        # separate pool pass)
+        band_ok = (ss_shape and st == 1 and wmeta["npad"] >= 32 and not u.get("residual")
+                   and 8 <= self.tensors[src].w and self.tensors[src].w + 1 <= 128)
         post_pool = None  # (first, second) BiPool nodes lowered as one 2x2 pool unit after the conv
         if nxt:
             pn = g.nodes[nxt[0]]
-            if not window_ok and isinstance(pn, (LocalPoolNode, BiPoolNode)):
+            nn = self.single(nxt[0]) if isinstance(pn, BiPoolNode) else None
+            bi_pair = (nn is not None and isinstance(g.nodes[nn[0]], BiPoolNode) and g.nodes[nn[0]].axis != pn.axis
+                       and g.nodes[nn[0]].degree == pn.degree and pn.degree <= 4)
+            if band_ok and isinstance(pn, LocalPoolNode) and pn.k <= 2 * pn.stride + 1 and pn.padding < pn.k:
+                cur = nxt[0]
+                chain.append(cur)
+                u["pool"] = L.POOL_LOCAL
+                u["pool_geom"] = pn.k | (pn.stride << 8) | (pn.padding << 16)
+                u["pool_off"] = self.cast(cur, "divisor")
+                out_shape = sh[cur]
+            elif band_ok and bi_pair:
+                chain += [nxt[0], nn[0]]
+                cur = nn[0]
+                u["pool"] = L.POOL_BI2
+                u["pool_deg"] = pn.degree
+                u["pool_order"] = 0 if pn.axis == "w" else 1
+                u["pool_off"] = self.cast_pair(nxt[0], nn[0])
+                out_shape = sh[cur]
+            elif not window_ok and isinstance(pn, (LocalPoolNode, BiPoolNode)):
                 nn = self.single(nxt[0]) if isinstance(pn, BiPoolNode) else None
                 if nn and isinstance(g.nodes[nn[0]], BiPoolNode) and g.nodes[nn[0]].axis != pn.axis \
                         and g.nodes[nn[0]].degree == pn.degree and pn.degree <= 4:
@@ -602,7 +627,7 @@ class _Builder:
         if self.use_tc and wmeta["npad"] % 16 == 0 and wmeta["npad"] >= 16:
             u["tc_off"] = self.tc_image(nid)
             u["tc16_off"], u["tc16_scale_off"] = self.tc16_image(nid)
-            if ss_shape and u.get("pool", 0) in (L.POOL_NONE, L.POOL_GLOBAL):
+            if ss_shape and u.get("pool", 0) in (L.POOL_NONE, L.POOL_GLOBAL, L.POOL_LOCAL, L.POOL_BI2):
                 u["tcss_off"] = self.tcss_image(nid, u["tc16_scale_off"])
         t = self.tensor(out_shape)
         u["out"] = t

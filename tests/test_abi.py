@@ -57,6 +57,7 @@ def test_plan_options_defaults_host_only():
     o = L.PlanOptions.default()
     assert o.size == ctypes.sizeof(L.PlanOptions)
     assert (o.split, o.halo_tiles, o.fuse_projection, o.streamk, o.pdl, o.graph, o.timeline) == (1,) * 7
+    assert o.band_pool == 0
     assert o.flag_sync == 0 and o.debug == 0 and abs(o.streamk_fill - 0.3) < 1e-12
     assert L.PlanOptions.default(streamk=0).streamk == 0
     with pytest.raises(KeyError):

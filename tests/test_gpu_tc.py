@@ -226,3 +226,64 @@ def test_split_tensors_and_overflow_fallback(cuda):
     got = eng.forward(torch.from_numpy(x.astype(np.float32)).cuda()).double().cpu().numpy()
     assert eng.fallbacks == 1
     np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-5 * np.abs(want).max())
+
+
+BAND_CASES = [
+    # cin, cout, k(conv), hw, batch, pool: ("local", k, s, p) | ("bi", degree, axis-first)
+    (16, 64, 3, 20, 6, ("local", 3, 2, 1)),
+    (16, 64, 3, 17, 5, ("local", 3, 2, 1)),   # odd conv rows / columns
+    (32, 128, 3, 12, 7, ("local", 2, 2, 0)),
+    (3, 64, 7, 40, 3, ("local", 3, 2, 1)),    # space-to-depth 7x7/s2 stem + 3x3/s2 pool (ResNet-18's)
+    (16, 64, 3, 16, 9, ("bi", 4, "w")),
+    (64, 128, 3, 10, 6, ("bi", 3, "h")),
+    (32, 256, 3, 8, 6, ("bi", 2, "w")),       # two n-tiles
+]
+
+
+@pytest.mark.parametrize("case", BAND_CASES, ids=[f"{c[0]}x{c[1]}k{c[2]}h{c[3]}{c[5][0]}" for c in BAND_CASES])
+def test_band_pooled_epilogue(cuda, case):
+    """A conv (+ polynomial) followed by a local k x k / s pool or a 2x2
+    bivariate pool runs as ONE halo-tile launch (conv_ss.cu band mode: the
+    unpooled map never leaves the SM) and matches the oracle; the float32
+    fallback plans (TMEM-A 3xTF32 / SIMT with a scratch map and a pooling
+    launch) compute the same."""
+    from paper_2509_22857_b200 import _lib as L
+    cin, cout, k, hw, batch, pool = case
+    rng = np.random.default_rng(31)
+    stride, pad = (2, 3) if k == 7 else (1, k // 2)
+    poly = PolyActNode("act", [rng.normal(0, 0.3, cout), rng.normal(0.6, 0.1, cout), rng.uniform(0.05, 0.3, cout)])
+    if pool[0] == "local":
+        _, pk, ps, pp = pool
+        tail = [poly, LocalPoolNode("pool", pk, ps, pp, np.float64(1.0 / (pk * pk)))]
+    else:
+        _, d, first = pool
+        second = "h" if first == "w" else "w"
+
+        def coeffs():
+            c = rng.normal(0, 0.2, (d + 1, d + 1, cout))
+            i, j = np.indices((d + 1, d + 1))
+            c[(i + j) > d] = 0.0
+            c[d, 0] = rng.uniform(0.05, 0.3, cout)
+            return c
+        tail = [poly, BiPoolNode("p1", first, coeffs()), BiPoolNode("p2", second, coeffs())]
+    g = conv_graph(rng, cin, cout, k, stride, pad, hw, tail=tail, gain=0.5)
+    x = rng.normal(0, 1, (batch, cin, hw, hw))
+    want = O.eval_batch(g, x)
+    import torch
+    eng = Engine(g, options=L.PlanOptions.default(band_pool=1))
+    got = eng.forward(torch.from_numpy(x.astype(np.float32)).cuda()).double().cpu().numpy()
+    plan = eng.plan(batch)
+    conv_units = [i for i, u in enumerate(eng.lw.units) if u["kind"] == L.UNIT_CONV]
+    assert len(conv_units) == 1 and eng.lw.units[conv_units[0]]["pool"] in (L.POOL_LOCAL, L.POOL_BI2)
+    assert plan.unit_impl(conv_units[0]) == 5
+    np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-5 * max(1.0, np.abs(want).max()))
+    # default plan: the conv into scratch, then a pooling launch
+    e0 = Engine(g)
+    y0 = e0.forward(torch.from_numpy(x.astype(np.float32)).cuda()).double().cpu().numpy()
+    assert e0.plan(batch).unit_impl(conv_units[0]) == 5 and e0.plan(batch).launches() == plan.launches() + 1
+    np.testing.assert_allclose(y0, want, rtol=1e-4, atol=1e-5 * max(1.0, np.abs(want).max()))
+    for impl in (1, 4):
+        e2 = Engine(g, impl=impl)
+        y2 = e2.forward(torch.from_numpy(x.astype(np.float32)).cuda()).double().cpu().numpy()
+        assert e2.plan(batch).unit_impl(conv_units[0]) in (1, 2)
+        np.testing.assert_allclose(y2, want, rtol=1e-4, atol=1e-5 * max(1.0, np.abs(want).max()))

@@ -25,7 +25,7 @@ torch.cuda.synchronize()
 n = fn(buf, 65536)
 ev = [(int(v) >> 48, int(v) & 0xFFFFFFFFFFFF) for v in buf[:n] if int(v)]
 t0 = min(t for _, t in ev)
-names = {13: "ep_acc", 14: "ep_math", 12: "cv_stfull", 11: "cv_aempty", 10: "mma_k4", 1: "cv_lds", 2: "cv_go", 3: "cv_done", 4: "mma_wait", 5: "mma_go", 6: "mma_done", 7: "ep_wait", 8: "ep_go", 9: "ep_done"}
+names = {10: "bp_bar", 11: "bp_go", 12: "bp_done", 13: "ep_acc", 14: "ep_math", 12: "cv_stfull", 11: "cv_aempty", 10: "mma_k4", 1: "cv_lds", 2: "cv_go", 3: "cv_done", 4: "mma_wait", 5: "mma_go", 6: "mma_done", 7: "ep_wait", 8: "ep_go", 9: "ep_done"}
 ev.sort(key=lambda e: e[1])
 for tag, t in (ev if os.environ.get("ALL") else ev[:240]):
     print(f"{t - t0:8d} {names.get(tag >> 8, tag >> 8):9s} kb={tag & 0xff}")
