@@ -567,7 +567,37 @@ def load_model(path: str) -> ModelGraph:
     return g
 
 
-def _node_from_entry(e: Dict, blob: np.ndarray) -> Node:
+def load_model_views(path: str):
+    """The neutral model as (graph, blob, specs): the base64 blob decoded
+    once into a read-only float64 array, every node tensor a zero-copy view
+    of it, specs[node id][field] = (offset, shape) of each tensor in the
+    blob (polyact fields c0..cd, polyskip its monomial keys).  The loader
+    behind lowering.load_lowered; same validation and errors as load_model."""
+    try:
+        with open(path) as f:
+            doc = json.load(f)
+    except (OSError, json.JSONDecodeError) as e:
+        raise ModelFormatError(f"cannot read model file {path!r}: {e}") from e
+    if not isinstance(doc, dict) or doc.get("version") != FORMAT_VERSION:
+        raise ModelFormatError(
+            f"unsupported model format version {doc.get('version') if isinstance(doc, dict) else None!r}")
+    specs: Dict[str, Dict[str, Tuple[int, Tuple[int, ...]]]] = {}
+    try:
+        blob = np.frombuffer(base64.b64decode(doc["weights"]), dtype="<f8")
+        blob.flags.writeable = False
+        g = ModelGraph()
+        for e in doc["nodes"]:
+            g.add(_node_from_entry(e, blob, views=True))
+            specs[e["id"]] = {k: (int(v["offset"]), tuple(v["shape"])) for k, v in e.get("tensors", {}).items()}
+        for s_, d_ in doc["edges"]:
+            g.connect(s_, d_)
+    except (KeyError, TypeError, ValueError) as e:
+        raise ModelFormatError(f"malformed model file {path!r}: {e}") from e
+    g.validate()
+    return g, blob, specs
+
+
+def _node_from_entry(e: Dict, blob: np.ndarray, views: bool = False) -> Node:
     kind = e["kind"]
     if kind not in TYPE_BY_KIND:
         raise ModelFormatError(f"unknown node kind {kind!r}")
@@ -581,7 +611,8 @@ def _node_from_entry(e: Dict, blob: np.ndarray) -> Node:
         off = int(spec["offset"])
         if off < 0 or off + n > blob.size:
             raise ValueError(f"tensor {name!r} of node {e['id']!r} overruns the blob")
-        return np.array(blob[off:off + n].reshape(shape), dtype=np.float64)
+        v = blob[off:off + n].reshape(shape)
+        return v if views else np.array(v, dtype=np.float64)
 
     nid = e["id"]
     if kind == "input":

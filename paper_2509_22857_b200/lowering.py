@@ -30,7 +30,7 @@ from typing import Dict, List, Optional, Tuple
 import numpy as np
 
 from . import _lib as L
-from .graph import (AddNode, AvgPoolNode, BatchNormNode, BiPoolNode, ConvNode, FlattenNode,
+from .graph import (load_model_views, AddNode, AvgPoolNode, BatchNormNode, BiPoolNode, ConvNode, FlattenNode,
                     GraphError, InputNode, LinearNode, LocalPoolNode, ModelGraph, OutputNode,
                     PolyActNode, PolySkipNode, PS_KEYS)
 
@@ -235,8 +235,20 @@ def s2d_weight_back(w2: np.ndarray, info: Dict) -> np.ndarray:
     return w
 
 
-def build_master(g: ModelGraph, shapes) -> Tuple[Dict[str, Dict[str, Slot]], List[np.ndarray], int, Dict]:
-    """Assign master offsets for every parameter and return the float64 chunks."""
+def build_master(g: ModelGraph, shapes, get=None) -> Tuple[Dict[str, Dict[str, Slot]], List[np.ndarray], int, Dict]:
+    """Assign master offsets for every parameter and return the float64 chunks.
+
+    get(node, field) supplies a parameter tensor (default: the node's own
+    attribute; polyact fields are c0..cd, polyskip fields its monomial keys).
+    load_lowered passes encoded blob indices instead of values, so the same
+    layout code yields the index map of the neutral-format loader."""
+    if get is None:
+        def get(node, field):
+            if isinstance(node, PolyActNode):
+                return node.coeffs[int(field[1:])]
+            if isinstance(node, PolySkipNode):
+                return node.coeffs[field]
+            return getattr(node, field)
     slots: Dict[str, Dict[str, Slot]] = {}
     chunks: List[Tuple[int, np.ndarray]] = []
     scalar: Dict[Tuple[str, str], bool] = {}
@@ -258,38 +270,43 @@ def build_master(g: ModelGraph, shapes) -> Tuple[Dict[str, Dict[str, Slot]], Lis
         cp = cpad_for(c_out)
         if isinstance(node, ConvNode):
             cin = shapes[preds[nid][0]][0]
+            w = get(node, "weight")
             if s2d_eligible(g, shapes, nid):
-                m, meta = conv_weight_to_master(s2d_weight(node.weight), cp, 4 * cin)
-                meta["s2d"] = {"cin": cin, "k": node.weight.shape[2]}
+                m, meta = conv_weight_to_master(s2d_weight(w), cp, 4 * cin)
+                meta["s2d"] = {"cin": cin, "k": w.shape[2]}
                 meta["i"] = cin
             else:
-                m, meta = conv_weight_to_master(node.weight, cp, cin)
+                m, meta = conv_weight_to_master(w, cp, cin)
             put(nid, "weight", m, **meta)
-            put(nid, "bias", _vec(node.bias, cp))
+            put(nid, "bias", _vec(get(node, "bias"), cp))
         elif isinstance(node, LinearNode):
-            k, n = node.weight.shape
-            put(nid, "weight", node.weight, k=k, n=n)
-            put(nid, "bias", _vec(node.bias, cp))
+            w = get(node, "weight")
+            k, n = w.shape
+            put(nid, "weight", w, k=k, n=n)
+            put(nid, "bias", _vec(get(node, "bias"), cp))
         elif isinstance(node, BatchNormNode):
             std = np.ones(cp)
-            std[:c_out] = node.std
-            put(nid, "bn", np.concatenate([_vec(node.gamma, cp), _vec(node.beta, cp),
-                                           _vec(node.mean, cp), std]), cpad=cp, c=c_out)
+            std[:c_out] = get(node, "std")
+            put(nid, "bn", np.concatenate([_vec(get(node, "gamma"), cp), _vec(get(node, "beta"), cp),
+                                           _vec(get(node, "mean"), cp), std]), cpad=cp, c=c_out)
         elif isinstance(node, PolyActNode):
-            put(nid, "coeffs", np.concatenate([_vec(c, cp) for c in node.coeffs]),
+            cs = [get(node, f"c{i}") for i in range(node.degree + 1)]
+            put(nid, "coeffs", np.concatenate([_vec(c, cp) for c in cs]),
                 cpad=cp, c=c_out, deg=node.degree)
-            for i, c in enumerate(node.coeffs):
+            for i, c in enumerate(cs):
                 scalar[(nid, f"c{i}")] = np.asarray(c).ndim == 0
         elif isinstance(node, PolySkipNode):
-            put(nid, "coeffs", np.concatenate([_vec(node.coeffs[k], cp) for k in PS_KEYS]),
+            cs = {k: get(node, k) for k in PS_KEYS}
+            put(nid, "coeffs", np.concatenate([_vec(cs[k], cp) for k in PS_KEYS]),
                 cpad=cp, c=c_out)
             for k in PS_KEYS:
-                scalar[(nid, k)] = np.asarray(node.coeffs[k]).ndim == 0
+                scalar[(nid, k)] = np.asarray(cs[k]).ndim == 0
         elif isinstance(node, (AvgPoolNode, LocalPoolNode)):
-            put(nid, "divisor", np.asarray([float(node.divisor)]))
-            scalar[(nid, "divisor")] = np.asarray(node.divisor).ndim == 0
+            dv = get(node, "divisor")
+            put(nid, "divisor", np.asarray([float(dv)]))
+            scalar[(nid, "divisor")] = np.asarray(dv).ndim == 0
         elif isinstance(node, BiPoolNode):
-            c = np.asarray(node.coeffs, dtype=np.float64)
+            c = np.asarray(get(node, "coeffs"), dtype=np.float64)
             d = c.shape[0] - 1
             flat = [_vec(c[i, j], cp) for i in range(d + 1) for j in range(d + 1)]
             put(nid, "coeffs", np.concatenate(flat), cpad=cp, c=c_out, deg=d)
@@ -725,9 +742,9 @@ def _schedule(units: List[Dict], unit_nodes: List[List[str]]):
     return [units[i] for i in order], [unit_nodes[i] for i in order]
 
 
-def lower(g: ModelGraph, use_tc: bool = True) -> Lowered:
+def lower(g: ModelGraph, use_tc: bool = True, _layout=None) -> Lowered:
     shapes = g.validate()
-    slots, chunks, size, scalar = build_master(g, shapes)
+    slots, chunks, size, scalar = _layout or build_master(g, shapes)
     b = _Builder(g, slots, size, use_tc).run()
     units, unit_nodes = _schedule(b.units, b.unit_nodes)
     lw = Lowered(graph=g, shapes=shapes, tensors=b.tensors, units=units, unit_nodes=unit_nodes,
@@ -736,3 +753,39 @@ def lower(g: ModelGraph, use_tc: bool = True) -> Lowered:
                  out_shape=tuple(b.output_shape), scalar=scalar)
     lw._chunks = chunks
     return lw
+
+
+# ---------------------------------------------------------------------------
+# neutral model format straight into the master layout
+# ---------------------------------------------------------------------------
+
+def load_lowered(path: str, use_tc: bool = True) -> Tuple[Lowered, np.ndarray]:
+    """levnet's neutral JSON model (reference graph.py:433-539, written by
+    exporter neutral.py:57-91 / graph.save_model) -> (Lowered, float64
+    master) without copying any parameter into per-node arrays.
+
+    The base64 blob is decoded once.  The graph the lowering walks holds
+    read-only views into the blob (graph.load_model_views), and the master
+    is ONE vectorised gather: the master layout (build_master) is computed
+    on blob indices instead of values -- element i of the blob enters as
+    the code i + 2 (exact in float64), the layout's zero padding stays 0 and
+    its BatchNorm std padding 1 -- then master = [0, 1, blob...][code].
+    Byte-identical to master_array(lower(load_model(path))) -- see
+    tests/test_loader.py."""
+    g, blob, specs = load_model_views(path)
+    shapes = g.validate()
+
+    def get(node, field):
+        off, shape = specs[node.id][field]
+        n = int(np.prod(shape)) if shape else 1
+        return np.arange(off + 2, off + 2 + n, dtype=np.float64).reshape(shape)
+
+    slots, chunks, size, scalar = build_master(g, shapes, get)
+    code = master_array(chunks, size).astype(np.int64)
+    ext = np.empty(blob.size + 2)
+    ext[0], ext[1] = 0.0, 1.0
+    ext[2:] = blob
+    master = ext[code]
+    lw = lower(g, use_tc=use_tc, _layout=(slots, chunks, size, scalar))
+    lw._chunks = None  # the chunks hold encoded indices; the master is the gathered array
+    return lw, master

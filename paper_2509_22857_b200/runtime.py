@@ -139,7 +139,8 @@ class Engine:
     """One graph resident on the GPU."""
 
     def __init__(self, g: ModelGraph, device=None, use_tc: bool = True, impl: int = 0,
-                 lowered: Optional[Lowered] = None, options: Optional[L.PlanOptions] = None):
+                 lowered: Optional[Lowered] = None, options: Optional[L.PlanOptions] = None,
+                 master: Optional[np.ndarray] = None):
         """options: pcnn_plan_options for every plan of this engine (None =
         the library defaults; see _lib.PlanOptions / options_from_env)."""
         torch = _torch()
@@ -148,8 +149,8 @@ class Engine:
         self.lw = lowered or lower(g, use_tc=use_tc)
         self.impl = impl
         self.options = options
-        m = master_array(self.lw._chunks, self.lw.master_size)
-        self.master = torch.from_numpy(m).to(self.device)
+        m = master if master is not None else master_array(self.lw._chunks, self.lw.master_size)
+        self.master = torch.from_numpy(np.ascontiguousarray(m)).to(self.device)
         self.packed = torch.zeros(self.lw.packed_size, dtype=torch.float32, device=self.device)
         self._packs = self.lw.pack_descs()
         self.repack()
@@ -159,6 +160,15 @@ class Engine:
         # per tensor: split storage keeps x * 2^scale_log2 (set from the float32
         # rerun's magnitudes when an activation left the fp16 range)
         self.scale_log2 = np.zeros(len(self.lw.tensors), dtype=np.int64)
+
+    @classmethod
+    def from_model_file(cls, path: str, **kw) -> "Engine":
+        """Neutral model file (reference graph.py:433-539) straight to a
+        device engine: the blob is decoded once and gathered into the
+        master layout (lowering.load_lowered), then uploaded."""
+        from .lowering import load_lowered
+        lw, master = load_lowered(path, use_tc=kw.pop("use_tc", True))
+        return cls(lw.graph, lowered=lw, master=master, **kw)
 
     # -- parameters -----------------------------------------------------------
     def repack(self, stream=None) -> None:

@@ -277,3 +277,19 @@ def test_extension_redistribution_matches_oracle(cuda):
             got, applied, _ = T.redistribute_sweep(g, direction, allow_negative_leading=True)
             assert applied == applied_o, (kind, direction)
             assert max_param_rel_diff(got, want) <= 1e-12, (kind, direction)
+
+
+def test_engine_from_model_file(cuda, golden, tmp_path):
+    """Engine.from_model_file (blob gathered straight into the master,
+    lowering.load_lowered) runs the same network as Engine(load_model())."""
+    import torch
+    manifest, arrays = golden
+    case = next(c for c in manifest["cases"] if c["name"] == "rn20_fixture")
+    path = str(GOLDEN / case["model"])
+    x = torch.from_numpy(arrays["rn20_fixture/x"].astype(np.float32)).cuda()
+    a = Engine(load_model(path)).forward(x).cpu().numpy()
+    e = Engine.from_model_file(path)
+    b = e.forward(x).cpu().numpy()
+    np.testing.assert_allclose(a, b, rtol=1e-6, atol=1e-7)
+    assert_forward_close(b, arrays["rn20_fixture/y"], "from_model_file")
+    assert max_param_rel_diff(e.to_graph(), load_model(path)) == 0.0
