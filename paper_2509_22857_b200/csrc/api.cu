@@ -65,6 +65,7 @@ struct pcnn_plan {
   std::vector<int> impl;  // per unit: 1 SIMT, 2 tcgen05
   std::vector<ConvArgs> conv_args;
   int batch = 0, input = 0, output = 0;
+  int64_t in_elems = 0;  // user input floats per image (NCHW; a space-to-depth ingest's image, not its tensor)
   const float* params = nullptr;
   float* ws = nullptr;
   size_t ws_bytes = 0;
@@ -712,6 +713,13 @@ int pcnn_plan_create_ex(const pcnn_unit_desc* units, int n_units, const pcnn_ten
     }
     p->views.push_back(make_view(t, p->ws));
   }
+  {
+    const pcnn_tensor_desc& ti = p->tensors[input_tensor];
+    p->in_elems = ti.c * ti.h * ti.w;
+    for (const auto& u : p->units)
+      if (u.kind == PCNN_UNIT_INGEST && u.out == input_tensor && (u.flags & PCNN_FLAG_S2D))
+        p->in_elems = (ti.c / 4) * (2 * (ti.h - 1)) * (2 * (ti.w - 1));
+  }
   p->impl.assign(n_units, 1);
   p->conv_args.resize(n_units);
   for (int i = 0; i < n_units; ++i) {
@@ -906,8 +914,7 @@ int pcnn_forward_host(pcnn_plan* p, const float* x_host, float* logits_host, flo
                       void* stream) {
   if (!p || !x_host || !logits_host || !x_dev || !logits_dev) return fail(PCNN_ERR_INVALID, "null argument");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const pcnn_tensor_desc& ti = p->tensors[p->input];
-  size_t in_bytes = sizeof(float) * (size_t)p->batch * ti.c * ti.h * ti.w;
+  const size_t in_bytes = sizeof(float) * (size_t)p->batch * p->in_elems;
   const pcnn_tensor_desc& to = p->tensors[p->output];
   size_t out_bytes = sizeof(float) * (size_t)p->batch * to.c * to.h * to.w;
   PCNN_CUDA(cudaMemcpyAsync(x_dev, x_host, in_bytes, cudaMemcpyHostToDevice, s));
@@ -923,8 +930,7 @@ int pcnn_forward_host_many(pcnn_plan* p, const float* const* x_hosts, float* con
   if (!p || (n > 0 && (!x_hosts || !logits_hosts)) || !x_dev0 || !x_dev1 || !logits_dev || n < 0)
     return fail(PCNN_ERR_INVALID, "pcnn_forward_host_many: null argument");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const pcnn_tensor_desc& ti = p->tensors[p->input];
-  const size_t in_bytes = sizeof(float) * (size_t)p->batch * ti.c * ti.h * ti.w;
+  const size_t in_bytes = sizeof(float) * (size_t)p->batch * p->in_elems;
   const pcnn_tensor_desc& to = p->tensors[p->output];
   const size_t out_bytes = sizeof(float) * (size_t)p->batch * to.c * to.h * to.w;
   if (!p->copy_stream) {

@@ -148,3 +148,29 @@ def test_streamk_matches_whole_tiles(cuda, name):
     for _ in range(2):
         got = eng.forward(x).double().cpu().numpy()
         assert rel_err(got, base) <= 1e-5, name
+
+
+@pytest.mark.parametrize("name", ["lenet5", "resnet20"])
+def test_compare_report(cuda, name, tmp_path):
+    """The GPU compare report (reference cli.py:554-629's transform-equivalence
+    check over 1000 inputs through forward_host_many, plus the per-unit
+    precision table): passes on the configs' redistributions, agrees with
+    check_equivalence on the common inputs, and the CLI writes the JSON and
+    exits 0."""
+    import json
+    from paper_2509_22857_b200 import compare
+    cfg = configs.CONFIGS[name]
+    g = configs.build(name)
+    rg = g
+    for d in cfg.redistribution:
+        rg, _, _ = T.redistribute_sweep(rg, d, allow_negative_leading=cfg.allow_negative_leading)
+    rep = compare.compare_report(g, rg, n_inputs=1000)
+    eq, prec = rep["checks"]
+    assert rep["passed"] and eq["passed"] and eq["n_inputs"] == 1000
+    assert eq["max_rel_err"] <= 1e-4 and eq["argmax_match_rate"] >= 0.99
+    small = T.check_equivalence(g, rg, n_inputs=100)
+    assert small.max_rel_err <= eq["max_rel_err"] + 1e-7  # the first 100 inputs are the same draws
+    assert len(prec["units"]) >= 3 and prec["logits_max_rel_err_vs_fp32"] <= 1e-4
+    out = tmp_path / "r.json"
+    assert compare.main(["--config", name, "--n-inputs", "300", "--json", str(out)]) == 0
+    assert json.loads(out.read_text())["passed"]

@@ -293,3 +293,20 @@ def test_engine_from_model_file(cuda, golden, tmp_path):
     np.testing.assert_allclose(a, b, rtol=1e-6, atol=1e-7)
     assert_forward_close(b, arrays["rn20_fixture/y"], "from_model_file")
     assert max_param_rel_diff(e.to_graph(), load_model(path)) == 0.0
+
+
+def test_forward_host_space_to_depth_input(cuda):
+    """A 7x7/s2 stem ingested as 2x2 space-to-depth blocks: the host-buffer
+    entry points copy the user's NCHW image (batch * C * H * W floats), not
+    the ingest tensor's (4C, H/2+1, W/2+1) size."""
+    import torch
+    from paper_2509_22857_b200 import configs
+    g = configs.build("resnet18", hw=64, calib_batch=4)
+    x = configs.make_input(configs.CONFIGS["resnet18"], batch=8, hw=64).astype(np.float32)
+    eng = Engine(g)
+    assert eng.lw.tensors[eng.lw.input_tensor].c == 12  # the space-to-depth ingest tensor
+    want = eng.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+    np.testing.assert_allclose(eng.forward_host(x), want, rtol=1e-6, atol=1e-7)
+    outs = eng.forward_host_many([x, x[::-1].copy()])
+    np.testing.assert_allclose(outs[0].numpy(), want, rtol=1e-6, atol=1e-7)
+    assert rel_err(O.eval_batch(g, x[:2]), want[:2].astype(np.float64)) <= 1e-4
