@@ -182,7 +182,8 @@ enum pcnn_scale_opcode {
   PCNN_OP_CHECK_CLOSE = 14,   /* err unless |A-B| <= atol + rtol |B|         */
   PCNN_OP_CHECK_ALLONE = 15,  /* flag[p] = all(A == 1) (no error)            */
   PCNN_OP_SQRT = 16,       /* dst = sqrt(A)                                  */
-  PCNN_OP_STORE = 17       /* master[dst + i*sa] = A[i]                      */
+  PCNN_OP_STORE = 17,      /* master[dst + i*sa] = A[i]                      */
+  PCNN_OP_ADD = 18         /* dst = A + B (node fusing, transforms.py:62-101) */
 };
 
 typedef struct pcnn_scale_op {

@@ -37,7 +37,7 @@ IMPL_AUTO, IMPL_SIMT, IMPL_TF32, IMPL_F16X2, IMPL_FP32_TENSORS, IMPL_F16X2_SS = 
 # scale opcodes
 (OP_FILL, OP_LOAD, OP_MUL, OP_DIV, OP_SUB, OP_POWI, OP_SROOT, OP_AROOT, OP_RECIP, OP_SOLVE,
  OP_CHECK_UNIFORM, OP_CHECK_NONZERO, OP_CHECK_NONNEG, OP_CHECK_CLOSE, OP_CHECK_ALLONE,
- OP_SQRT, OP_STORE) = range(1, 18)
+ OP_SQRT, OP_STORE, OP_ADD) = range(1, 19)
 
 MAX_FACTORS = 6
 ABI_VERSION = 3

@@ -1041,7 +1041,7 @@ int pcnn_redistribute(double* master, double* arena, int64_t arena_len, const pc
     return fail(PCNN_ERR_INVALID, "pcnn_redistribute: null argument");
   for (int i = 0; i < n_ops; ++i) {
     const pcnn_scale_op& o = ops[i];
-    if (o.op < PCNN_OP_FILL || o.op > PCNN_OP_STORE || o.n < 0 || o.dst < 0)
+    if (o.op < PCNN_OP_FILL || o.op > PCNN_OP_ADD || o.n < 0 || o.dst < 0)
       return fail(PCNN_ERR_INVALID, "bad scale op " + std::to_string(i));
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);

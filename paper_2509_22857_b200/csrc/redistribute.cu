@@ -44,7 +44,7 @@ __device__ void run_program(const double* __restrict__ master_ro, double* master
       double A = 0.0, B = 0.0;
       if (o.op != PCNN_OP_FILL && o.op != PCNN_OP_LOAD) A = arena[o.a + i * o.sa];
       if (o.op == PCNN_OP_MUL || o.op == PCNN_OP_DIV || o.op == PCNN_OP_SUB || o.op == PCNN_OP_SOLVE ||
-          o.op == PCNN_OP_CHECK_CLOSE)
+          o.op == PCNN_OP_CHECK_CLOSE || o.op == PCNN_OP_ADD)
         B = arena[o.b + i * o.sb];
       switch (o.op) {
         case PCNN_OP_FILL: arena[o.dst + i] = o.imm; break;
@@ -52,6 +52,7 @@ __device__ void run_program(const double* __restrict__ master_ro, double* master
         case PCNN_OP_MUL: arena[o.dst + i] = A * B; break;
         case PCNN_OP_DIV: arena[o.dst + i] = A / B; break;
         case PCNN_OP_SUB: arena[o.dst + i] = A - B; break;
+        case PCNN_OP_ADD: arena[o.dst + i] = A + B; break;
         case PCNN_OP_POWI: arena[o.dst + i] = o.p >= 0 ? ipow(A, o.p) : pow(A, (double)o.p); break;
         case PCNN_OP_SROOT: arena[o.dst + i] = copysign(pow(fabs(A), 1.0 / (double)o.p), A); break;
         case PCNN_OP_AROOT: arena[o.dst + i] = pow(fabs(A), 1.0 / (double)o.p); break;

@@ -170,6 +170,7 @@ class Program:
         self.consts: Dict[int, Tuple[int, float]] = {}
         self.from_arena: Dict[int, Tuple[int, Vec]] = {}
         self.flag_names: List[str] = []
+        self.src_of: Dict[int, int] = {}  # rewrite source offset when it is not the destination
 
     # -- raw ops ---------------------------------------------------------------
     def _op(self, op, n, dst=0, a=0, b=0, sa=1, sb=1, p=0, err=0, imm=0.0, rtol=0.0, atol=0.0):
@@ -212,6 +213,9 @@ class Program:
 
     def sub(self, a, b):
         return self._bin(L.OP_SUB, a, b)
+
+    def add(self, a, b):
+        return self._bin(L.OP_ADD, a, b)
 
     def _un(self, op, a: Vec, p: int = 0) -> Vec:
         out = self.alloc(a.n, a.alloc)
@@ -264,6 +268,12 @@ class Program:
     def set_from(self, off: int, n: int, v: Vec) -> None:
         self.from_arena[off] = (n, v)
 
+    def copy(self, off: int, n: int, src: int) -> None:
+        """master[off : off + n] = master[src : src + n] (no factors)."""
+        self.chain.setdefault(off, [])
+        self.n_of[off] = n
+        self.src_of[off] = src
+
     def current(self, off: int, n: int, alloc: int) -> Vec:
         """Value of a coefficient vector after the factors recorded so far
         (donor updates compose in order, like sequential reference calls)."""
@@ -280,7 +290,7 @@ class Program:
                 continue
             if len(chain) > L.MAX_FACTORS:
                 raise TransformError(f"tensor at {off} collects {len(chain)} factors (max {L.MAX_FACTORS})")
-            d = L.RewriteDesc(dst=off, src=off, n=self.n_of[off], n_factors=len(chain))
+            d = L.RewriteDesc(dst=off, src=self.src_of.get(off, off), n=self.n_of[off], n_factors=len(chain))
             for i, (slot, divide, d1, m1, s1, d2, m2) in enumerate(chain):
                 d.f[i] = L.Factor(slot=slot, divide=divide, d1=d1, m1=m1, s1=s1, d2=d2, m2=m2, reserved=0)
             out.append(d)
@@ -294,15 +304,21 @@ class Program:
 def run_program(engine, prog: Program, stream=None) -> np.ndarray:
     """Launch pcnn_redistribute; raise TransformError with the reference's
     message if a device-side check failed; return the flag array."""
+    flags = run_program_on(engine.master, prog, engine.device, stream)
+    engine.repack(stream)
+    return flags
+
+
+def run_program_on(master, prog: Program, dev, stream=None) -> np.ndarray:
+    """pcnn_redistribute over any float64 device buffer (no repack)."""
     import torch
     from .runtime import _stream_handle
-    dev = engine.device
     arena = torch.empty(max(prog.arena, 1), dtype=torch.float64, device=dev)
     status = torch.zeros(4, dtype=torch.int64, device=dev)
     flags = torch.zeros(max(prog.nflags, 1), dtype=torch.int64, device=dev)
     ops = L.array(L.ScaleOp, prog.ops)
     rws = prog.rewrite_descs()
-    L.check(L.lib().pcnn_redistribute(ctypes.c_void_p(engine.master.data_ptr()), ctypes.c_void_p(arena.data_ptr()),
+    L.check(L.lib().pcnn_redistribute(ctypes.c_void_p(master.data_ptr()), ctypes.c_void_p(arena.data_ptr()),
                                       prog.arena, ops, len(prog.ops), L.array(L.RewriteDesc, rws), len(rws),
                                       ctypes.c_void_p(status.data_ptr()), ctypes.c_void_p(flags.data_ptr()),
                                       _stream_handle(stream)), "pcnn_redistribute")
@@ -311,7 +327,6 @@ def run_program(engine, prog: Program, stream=None) -> np.ndarray:
         code = int(st[0])
         msg = prog.errors[code - 1] if 0 < code <= len(prog.errors) else f"device status {code}"
         raise TransformError(msg)
-    engine.repack(stream)
     return flags.cpu().numpy()[:prog.nflags]
 
 
@@ -854,154 +869,23 @@ def redistribute_pass(g: ModelGraph):
 
 
 # ---------------------------------------------------------------------------
-# node fusing (host algebra, transforms.py:62-277)
+# node fusing (transforms.py:62-277): structure on the host, parameters on
+# the device -- see fusing.py
 # ---------------------------------------------------------------------------
 
-def fuse_bn_act(bn: BatchNormNode, act: PolyActNode) -> PolyActNode:
-    """Quadratic P(B(x)) (transforms.py:62-73)."""
-    if act.degree != 2:
-        raise TransformError(f"batchnorm folds into degree-2 activations only, got degree {act.degree}")
-    s, t = bn.b1, bn.b0
-    c0, c1, c2 = (np.asarray(c, dtype=np.float64) for c in act.coeffs)
-    return PolyActNode(act.id, [t * t * c2 + t * c1 + c0, s * (2.0 * t * c2 + c1), s * s * c2])
-
-
-def fuse_bn_conv(conv: ConvNode, bn: BatchNormNode) -> ConvNode:
-    """B(C(x)) (transforms.py:76-86)."""
-    if bn.gamma.shape[0] != conv.weight.shape[0]:
-        raise TransformError(f"batchnorm width {bn.gamma.shape[0]} does not match "
-                             f"{conv.weight.shape[0]} conv output channels")
-    s, t = bn.b1, bn.b0
-    return ConvNode(conv.id, conv.weight * s[:, None, None, None], s * conv.bias + t,
-                    conv.stride, conv.padding)
-
-
-def _join_coeffs(act: PolyActNode, ax, bx, ay, by) -> Dict[str, np.ndarray]:
-    """P(ax x + bx + ay y + by) as a bivariate quadratic (transforms.py:89-101)."""
-    c0, c1, c2 = (np.asarray(c, dtype=np.float64) for c in act.coeffs)
-    k = np.asarray(bx + by, dtype=np.float64)
-    lin = 2.0 * c2 * k + c1
-    one = np.ones_like(np.asarray(ax, dtype=np.float64))
-    return {"x2": c2 * ax * ax * one, "y2": c2 * ay * ay * one, "xy": 2.0 * c2 * ax * ay * one,
-            "x": ax * lin, "y": ay * lin, "c": c2 * k * k + c1 * k + c0}
-
-
-def fuse_skip_bn_bn(bnX: BatchNormNode, bnY: BatchNormNode, act: PolyActNode) -> PolySkipNode:
-    if act.degree != 2:
-        raise TransformError(f"skip fusion needs a degree-2 activation, got degree {act.degree}")
-    return PolySkipNode(act.id, _join_coeffs(act, bnX.b1, bnX.b0, bnY.b1, bnY.b0))
-
-
-def fuse_skip_identity(bnX: BatchNormNode, act: PolyActNode) -> PolySkipNode:
-    if act.degree != 2:
-        raise TransformError(f"skip fusion needs a degree-2 activation, got degree {act.degree}")
-    return PolySkipNode(act.id, _join_coeffs(act, bnX.b1, bnX.b0, 1.0, 0.0))
-
-
-def _fusion_sites(g: ModelGraph):
-    """Disjoint claims: joins first, then conv folds, then activation folds."""
-    sites, claimed = [], set()
-    order = g.topo_order()
-    for nid in order:
-        if not isinstance(g.nodes[nid], AddNode):
-            continue
-        cons = g.consumers_of(nid)
-        if len(cons) != 1 or not isinstance(g.nodes[cons[0]], PolyActNode) or g.nodes[cons[0]].degree != 2:
-            continue
-        ins = g.inputs_of(nid)
-        only = [isinstance(g.nodes[q], BatchNormNode) and [c for c, _ in g.consumer_edges(q)] == [nid]
-                for q in ins]
-        if only[0] and only[1]:
-            sites.append(("fuse_skip_bn_bn", (ins[0], ins[1], nid, cons[0])))
-            claimed.update(ins)
-        elif only[0]:
-            sites.append(("fuse_skip_identity", (ins[0], nid, cons[0])))
-            claimed.add(ins[0])
-        elif only[1]:
-            sites.append(("fuse_skip_identity_y", (ins[1], nid, cons[0])))
-            claimed.add(ins[1])
-    folded = set()
-    for nid in order:
-        if isinstance(g.nodes[nid], ConvNode):
-            cons = g.consumers_of(nid)
-            if len(cons) == 1 and isinstance(g.nodes[cons[0]], BatchNormNode) and cons[0] not in claimed:
-                sites.append(("fuse_bn_conv", (nid, cons[0])))
-                folded.add(cons[0])
-    for nid in order:
-        if isinstance(g.nodes[nid], BatchNormNode) and nid not in claimed and nid not in folded:
-            cons = g.consumers_of(nid)
-            if len(cons) == 1 and isinstance(g.nodes[cons[0]], PolyActNode) and g.nodes[cons[0]].degree == 2:
-                sites.append(("fuse_bn_act", (nid, cons[0])))
-    return sites
-
-
-def _remove_edges(g: ModelGraph, pairs) -> None:
-    todo = list(pairs)
-    keep = []
-    for e in g.edges:
-        if e in todo:
-            todo.remove(e)
-        else:
-            keep.append(e)
-    g.edges = keep
-
-
-def _apply_site(g: ModelGraph, rule: str, ids) -> None:
-    if rule == "fuse_bn_conv":
-        conv_id, bn_id = ids
-        g.nodes[conv_id] = fuse_bn_conv(g.nodes[conv_id], g.nodes[bn_id])
-        _remove_edges(g, [(conv_id, bn_id)])
-        g.edges = [(conv_id if s == bn_id else s, d) for s, d in g.edges]
-        del g.nodes[bn_id]
-        return
-    if rule == "fuse_bn_act":
-        bn_id, act_id = ids
-        src = g.inputs_of(bn_id)[0]
-        g.nodes[act_id] = fuse_bn_act(g.nodes[bn_id], g.nodes[act_id])
-        _remove_edges(g, [(src, bn_id), (bn_id, act_id)])
-        del g.nodes[bn_id]
-        g.connect(src, act_id)
-        return
-    if rule == "fuse_skip_bn_bn":
-        bx, by, add_id, act_id = ids
-        ps = fuse_skip_bn_bn(g.nodes[bx], g.nodes[by], g.nodes[act_id])
-        xs, ys, gone = g.inputs_of(bx)[0], g.inputs_of(by)[0], [bx, by]
-    elif rule == "fuse_skip_identity":
-        bx, add_id, act_id = ids
-        ps = fuse_skip_identity(g.nodes[bx], g.nodes[act_id])
-        xs, ys, gone = g.inputs_of(bx)[0], [q for q in g.inputs_of(add_id) if q != bx][0], [bx]
-    elif rule == "fuse_skip_identity_y":
-        by, add_id, act_id = ids
-        b = g.nodes[by]
-        ps = PolySkipNode(act_id, _join_coeffs(g.nodes[act_id], 1.0, 0.0, b.b1, b.b0))
-        xs, ys, gone = [q for q in g.inputs_of(add_id) if q != by][0], g.inputs_of(by)[0], [by]
-    else:
-        raise TransformError(f"unknown fusion rule {rule!r}")
-    g.nodes[act_id] = ps
-    drop = [(add_id, act_id)]
-    for b in gone:
-        drop += [(g.inputs_of(b)[0], b), (b, add_id)]
-    drop += [(q, add_id) for q in g.inputs_of(add_id) if q not in gone]
-    _remove_edges(g, drop)
-    for b in gone:
-        del g.nodes[b]
-    del g.nodes[add_id]
-    g.connect(xs, act_id)
-    g.connect(ys, act_id)
-
-
 def fuse_pass(g: ModelGraph, rng: Optional[np.random.Generator] = None):
-    g = g.copy()
-    applied = []
-    while True:
-        sites = _fusion_sites(g)
-        if not sites:
-            return g, applied
-        if rng is not None:
-            rng.shuffle(sites)
-        for rule, ids in sites:
-            _apply_site(g, rule, ids)
-            applied.append((rule, ids))
+    from . import fusing
+    try:
+        return fusing.fuse_pass(g, rng)
+    except fusing.FusionError as e:
+        raise TransformError(str(e)) from e
+
+
+def __getattr__(name):  # the reference's single-site helpers (host algebra)
+    if name in ("fuse_bn_act", "fuse_bn_conv", "fuse_skip_bn_bn", "fuse_skip_identity"):
+        from . import fusing
+        return getattr(fusing, name)
+    raise AttributeError(name)
 
 
 # ---------------------------------------------------------------------------

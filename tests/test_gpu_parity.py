@@ -310,3 +310,20 @@ def test_forward_host_space_to_depth_input(cuda):
     outs = eng.forward_host_many([x, x[::-1].copy()])
     np.testing.assert_allclose(outs[0].numpy(), want, rtol=1e-6, atol=1e-7)
     assert rel_err(O.eval_batch(g, x[:2]), want[:2].astype(np.float64)) <= 1e-4
+
+
+@pytest.mark.parametrize("model", ["models/rn20_fixture.json", "models/rn18_poly2_s1.json",
+                                   "models/ckpt_rn20_w4_ref.json"])
+def test_device_fusing_matches_reference(cuda, model):
+    """P2F node fusing with every parameter computed by one device launch
+    (fusing.py) = the reference's host algebra (oracle fuse_pass, pinned to
+    the reference): same structure, parameters within 1e-12 relative."""
+    from paper_2509_22857_b200 import fusing
+    g = _load(model)
+    got, applied = fusing.fuse_pass(g)
+    want, applied_ref = O.fuse_pass(g)
+    assert applied and [(r, tuple(i)) for r, i in applied_ref] == applied
+    assert got.edges == want.edges
+    assert max_param_rel_diff(got, want) <= 1e-12
+    x = np.random.default_rng(4).uniform(-1, 1, (4,) + g.validate()[g.input_id()])
+    assert rel_err(O.eval_batch(got, x), O.eval_batch(g, x)) <= 1e-10
