@@ -222,6 +222,9 @@ def roofline(eng, plan, batch, ts: TimelineStats, ms_per_step, config):
     hbm, bf16, _, basis = peaks()
     rate = {3: bf16 / 3.0, 5: bf16 / 3.0, 2: bf16 / 6.0, 1: bf16 / 6.0}
     lw = eng.lw
+    if not ts.steps:
+        return {"bound": None, "achieved": None, "peak": None, "unit": None, "frac": None, "traffic": None,
+                "note": "plan created without options.timeline: no device timeline"}
     fam_ms = ts.family_ms()
     dom = max(fam_ms, key=fam_ms.get)
     F = B = t_tensor = t_hbm = 0.0
@@ -490,7 +493,8 @@ def measure(name, args, rank, world, local, flush, options, e2e=True):
             eng.forward(x, out, check=False)
             ends[i].record(stream)
             # the step's launch timeline (D2H after its end event; not timed)
-            ts.add(plan.timeline())
+            if options.timeline:
+                ts.add(plan.timeline())
         torch.cuda.synchronize()
         t_end = time.perf_counter() + 0.3
         while time.perf_counter() < t_end:
@@ -583,7 +587,7 @@ def record(res, args, world):
                       "split_tensors": sum(plan.tensor_split(t) > 0 for t in range(len(eng.lw.tensors)))},
            "gpu_launches": plan.launches() * args.steps,
            "roofline": roof, "clocks": res["clocks"],
-           "device_step_span_ms": round(float(np.median(res["ts"].span_ns)) * 1e-6, 4),
+           "device_step_span_ms": round(float(np.median(res["ts"].span_ns)) * 1e-6, 4) if res["ts"].steps else None,
            "unit_ms": [round(float(v), 4) for v in res["ts"].unit_ms()]}
     if "e2e" in res:
         rec["e2e"] = {"value": round(res["e2e"], 2), "unit": UNIT, "h2d_bytes_per_step": res["h2d"],

@@ -120,6 +120,7 @@ ENV_OPTIONS = {
     "PCNN_NO_GRAPH": ("graph", 0), "PCNN_SS_MT": ("ss_mt", int), "PCNN_SS_SHARE": ("ss_share", int),
     "PCNN_SS_PSUB": ("ss_psub", int), "PCNN_SS_WRES": ("ss_wres", int), "PCNN_TC_NOSTAGE": ("tc_stage", 0),
     "PCNN_TC_DEBUG": ("debug", int), "PCNN_STREAMK_FILL": ("streamk_fill", float),
+    "PCNN_NO_TIMELINE": ("timeline", 0),
 }
 
 

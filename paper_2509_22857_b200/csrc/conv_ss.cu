@@ -541,9 +541,12 @@ __device__ __forceinline__ void band_item(const SsParams& P, const EpiParams& e,
 
 // SK: stream-K segments (a separate instantiation: the whole-tile kernel
 // keeps its registers and its simpler item walk)
-// POOL: kPoolNone (store, fused projection), kPoolGlobal, kPoolBand -- one
-// epilogue tail per instantiation keeps the epilogue loop's code short
-constexpr int kPoolNone = 0, kPoolGlobal = 1, kPoolBand = 2;
+// POOL: kPoolNone (store or global sum, fused projection) or kPoolBand (the
+// band epilogue).  Global pools stay in the common instantiation: a kernel
+// that runs once per forward starts with a cold instruction cache (measured
+// +4.4 us on RN20's last conv as its own instantiation), while the code
+// shared by every other layer of the network is already resident.
+constexpr int kPoolNone = 0, kPoolBand = 2;
 
 template <int TAPS, bool SK, int POOL>
 __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_constant__ SsParams P) {
@@ -1073,25 +1076,20 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
               }
             }
           }
-          // one epilogue body per instantiation: the projection item shares
-          // it with its own parameters (same code, other table / output)
-          const bool pji = kProj && pj;
-          epi_point16(pji ? P.pe : e, pji ? petab : etab, v, pji ? pwsc : wsc, sk, chan(cur));
           if constexpr (POOL == kPoolBand) {
             // the item's 128 conv outputs (bias / affine / poly applied):
             // the owner of each pooled column folds them in (band_item)
-            if (lane == 0 && warp == 0) tr(P, 2, 0xA00);
+            epi_point16(e, etab, v, wsc, sk, chan(cur));
             if (!(P.dbg & 4096))
               band_item(P, e, ebd, band_ring, band_stage + ((ew * 2 + par) * kTileM) * kStgPitch,
                         band_bnd + (ew * 2 + par) * 64, cur.r, cur.rows, row, lane, warp & 3, ew, chan(cur), v,
                         band_div);
-            if (lane == 0 && warp == 0) tr(P, 2, 0xC00);
-          } else if constexpr (POOL == kPoolGlobal) {
-            epi_global16(e, v, chan(cur), cur.valid, cur.valid ? cur.b : 0, lane);
+          } else if (kProj && pj) {
+            epi_chunk16<true>(P.pe, petab, v, pwsc, sk, chan(cur), cur.valid, cur.valid ? cur.b : 0, cur.oy,
+                               cur.ox, lane, -1, P.pe.out.sstore);
           } else {
-            epi_store16(pji ? P.pe : e, v, chan(cur), cur.valid, cur.valid ? cur.b : 0, cur.oy, cur.ox,
-                        (!pji && P.out_pos) ? (int64_t)cur.g * 8 : -1,
-                        pji ? P.pe.out.sstore : (P.fold_out ? 1.f : e.out.sstore));
+            epi_chunk16<true>(e, etab, v, wsc, sk, chan(cur), cur.valid, cur.valid ? cur.b : 0, cur.oy, cur.ox,
+                               lane, P.out_pos ? (int64_t)cur.g * 8 : -1, P.fold_out ? 1.f : e.out.sstore);
           }
         }
         if (lane == 0 && warp == 0) tr(P, 2, 0xE00 | c0);
@@ -1480,10 +1478,6 @@ void launch_conv_ss(const ConvArgs& a, cudaStream_t s) {
   void (*k)(SsParams);
   if (P.band) {
     k = P.taps == 16 ? conv_ss_kernel<16, false, kPoolBand> : conv_ss_kernel<9, false, kPoolBand>;
-  } else if (a.epi.pool == PCNN_POOL_GLOBAL) {
-    k = P.taps == 16 ? (sk ? conv_ss_kernel<16, true, kPoolGlobal> : conv_ss_kernel<16, false, kPoolGlobal>)
-        : P.taps == 9 ? (sk ? conv_ss_kernel<9, true, kPoolGlobal> : conv_ss_kernel<9, false, kPoolGlobal>)
-                      : (sk ? conv_ss_kernel<1, true, kPoolGlobal> : conv_ss_kernel<1, false, kPoolGlobal>);
   } else {
     k = P.taps == 16 ? (sk ? conv_ss_kernel<16, true, kPoolNone> : conv_ss_kernel<16, false, kPoolNone>)
         : P.taps == 9 ? (sk ? conv_ss_kernel<9, true, kPoolNone> : conv_ss_kernel<9, false, kPoolNone>)

@@ -268,13 +268,15 @@ __device__ __forceinline__ void epi_global16(const EpiParams& e, const float* v,
     if (valid && chb + j < e.cout) atomicAdd(e.out.base + (int64_t)b * e.npad + chb + j, v[j] * div);
 }
 
-// the whole epilogue, pool kind chosen at run time (TMEM-A kernel)
+// the whole epilogue, pool kind chosen at run time; WINDOW = false drops the
+// 2x2 window pools (the halo-tile kernel never runs them: a shorter loop body)
+template <bool WINDOW = true>
 __device__ __forceinline__ void epi_chunk16(const EpiParams& e, const EpiTab& T, float* v, float vscale,
                                             const float* sk, int chb, bool valid, int b, int oy, int ox, int lane,
                                             int64_t opos = -1, float ostore = 1.f) {
   epi_point16(e, T, v, vscale, sk, chb);
   if (e.pool == PCNN_POOL_NONE) epi_store16(e, v, chb, valid, b, oy, ox, opos, ostore);
-  else if (e.pool == PCNN_POOL_GLOBAL) epi_global16(e, v, chb, valid, b, lane);
+  else if (!WINDOW || e.pool == PCNN_POOL_GLOBAL) epi_global16(e, v, chb, valid, b, lane);
   else epi_window16(e, v, chb, valid, b, oy, ox, lane);
 }
 
