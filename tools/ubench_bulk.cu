@@ -55,6 +55,40 @@ __global__ void bulk_kernel(const uint8_t* src, size_t span, int bytes, int copi
   cycles[blockIdx.x] = clock64() - t0;
 }
 
+// all copies of the launch issued back to back (no slot reuse), one
+// mbarrier for all: is the TMA engine pipelining independent copies?
+__global__ void burst_kernel(const uint8_t* src, size_t span, int bytes, int copies, unsigned long long* cycles,
+                             int lanes) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bar;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t b = smem_u32(&bar);
+  const unsigned long long t0 = clock64();
+  if (threadIdx.x == 0)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes * copies) : "memory");
+  __syncthreads();
+  if ((int)threadIdx.x < lanes) {
+    for (int c = threadIdx.x; c < copies; c += lanes) {
+      size_t off = ((size_t)blockIdx.x * 131 + c) * 65536 % (span - bytes);
+      off &= ~(size_t)15;
+      const uint32_t dst = smem_u32(smem + (size_t)c * bytes);
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(dst), "l"(src + off), "r"(bytes), "r"(b) : "memory");
+    }
+  }
+  if (threadIdx.x == 0) {
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                   : "=r"(ok) : "r"(b), "r"(0) : "memory");
+    cycles[blockIdx.x] = clock64() - t0;
+  }
+}
+
 int main() {
   const size_t span = 32u << 20;
   uint8_t* src;
@@ -63,27 +97,22 @@ int main() {
   unsigned long long* cyc;
   cudaMalloc(&cyc, 148 * sizeof(unsigned long long));
   unsigned long long h[148];
-  cudaFuncSetAttribute(bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  printf("grid bytes x per_stage depth copies -> cycles/stage  B/cyc/SM  chip TB/s(@1.9GHz)\n");
-  for (int grid : {148})
-    for (int per_stage : {1, 2, 4, 8, 16})
-      for (int bytes : {1024, 5248, 16384, 65536})
-        for (int depth : {1, 4}) {
-          if ((size_t)bytes * per_stage * depth > 190 * 1024) continue;
-          if (depth == 4 && bytes != 5248) continue;
-          const int copies = 64;
-          for (int rep = 0; rep < 2; ++rep)
-            bulk_kernel<<<grid, 32, 200 * 1024>>>(src, span, bytes, copies, depth, per_stage, cyc);
+  cudaFuncSetAttribute(burst_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  printf("burst: grid bytes copies lanes -> total cycles  cycles/copy  B/cyc/SM\n");
+  for (int grid : {1, 148})
+    for (int bytes : {1024, 5248, 16384})
+      for (int copies : {1, 4, 8, 16, 32})
+        for (int lanes : {1, 32}) {
+          if ((size_t)bytes * copies > 190 * 1024 || lanes > copies) continue;
+          for (int rep = 0; rep < 3; ++rep)
+            burst_kernel<<<grid, 32, 200 * 1024>>>(src, span, bytes, copies, cyc, lanes);
           cudaDeviceSynchronize();
           cudaMemcpy(h, cyc, grid * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
           double mx = 0;
           for (int i = 0; i < grid; ++i) mx = mx > h[i] ? mx : (double)h[i];
-          const double per = mx / copies;
-          const double bpc = (double)bytes * per_stage / per;
-          printf("%4d %6d x %d %3d %4d -> %8.0f  %7.1f  %6.2f\n", grid, bytes, per_stage, depth, copies, per, bpc,
-                 bpc * grid * 1.9e9 / 1e12);
+          printf("%4d %6d %3d %3d -> %8.0f  %8.1f  %7.1f\n", grid, bytes, copies, lanes, mx, mx / copies,
+                 (double)bytes * copies / mx);
         }
-  cudaError_t e = cudaGetLastError();
-  printf("%s\n", cudaGetErrorString(e));
+  printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
