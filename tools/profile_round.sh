@@ -11,10 +11,10 @@ set -e
 export PCNN_NO_PDL=1 PCNN_NO_GRAPH=1
 cfg=${1:-resnet20}; tag=${2:-r01}; kre=${3:-conv_ss_kernel}; skip=${4:-0}
 mkdir -p gpurun_out
-python bench.py --config $cfg --steps 5 --warmup 3 --no-cpu --no-redist-timing > gpurun_out/${tag}_${cfg}_plain.json 2> gpurun_out/${tag}_${cfg}_plain.err
+python bench.py --config $cfg --steps 5 --warmup 3 --no-cpu --no-redist-timing --no-parity --secondary "" > gpurun_out/${tag}_${cfg}_plain.json 2> gpurun_out/${tag}_${cfg}_plain.err
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'conv_|ingest|linear_kernel|eltwise|localpool|to_vector|copyout' \
     -c 600 --csv --log-file gpurun_out/${tag}_${cfg}_launches.csv \
-    python bench.py --config $cfg --steps 5 --warmup 3 --no-cpu --no-redist-timing > gpurun_out/${tag}_${cfg}_ncu_bench.log 2>&1
+    python bench.py --config $cfg --steps 5 --warmup 3 --no-cpu --no-redist-timing --no-parity --secondary "" > gpurun_out/${tag}_${cfg}_ncu_bench.log 2>&1
 python tools/fwd.py --config $cfg --iters 1 > gpurun_out/${tag}_${cfg}_fwd.log 2>&1
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:conv_ \
     --csv --log-file gpurun_out/${tag}_${cfg}_traffic.csv python tools/fwd.py --config $cfg --iters 1 > /dev/null 2>&1

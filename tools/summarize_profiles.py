@@ -104,15 +104,36 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__shared_mem_per_block_dynamic", "launch__grid_size", "launch__block_size"]
 
 
-def full(tag, cfg):
+NCU_SUMMARY = {
+    "tc_smem_wavefronts_pct": "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+    "mem_tensor_active_pct": "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "tc_inst_issue_pct": "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active",
+    "sm_throughput_pct": "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "dram_throughput_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "stall_no_instruction_per_issue": "smsp__average_warps_issue_stalled_no_instruction_per_issue_active.ratio",
+    "registers_per_thread": "launch__registers_per_thread",
+}
+
+
+def full(tag, cfg, summary=None):
     rep = OUT / f"{tag}_{cfg}_full.ncu-rep"
     raw = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     if len(rows) < 3:
         return
     hdr, units, vals = rows[0], rows[1], rows[2]
+    if summary is not None:
+        d = {"kernel": vals[hdr.index("Kernel Name")][:80], "source": f"profiles/{tag}_{cfg}_full_summary.txt"}
+        for k, m in NCU_SUMMARY.items():
+            if m in hdr:
+                try:
+                    d[k] = float(vals[hdr.index(m)].replace(",", ""))
+                except ValueError:
+                    pass
+        summary[cfg] = d
     out = [f"# ncu --set full of one launch ({vals[hdr.index('Kernel Name')]})"]
-    for k in KEYS + [h for h in hdr if "tensor" in h and "pct" in h][:6]:
+    for k in KEYS + list(NCU_SUMMARY.values()) + [h for h in hdr if "tensor" in h and "pct" in h][:6]:
         if k in hdr:
             i = hdr.index(k)
             out.append(f"{k}, {vals[i]}, {units[i]}")
@@ -124,14 +145,21 @@ def main():
     PROF.mkdir(exist_ok=True)
     tpath = PROF / "traffic.json"
     table = json.loads(tpath.read_text()) if tpath.exists() else {}
+    spath = PROF / "ncu_summary.json"
+    summary = json.loads(spath.read_text()) if spath.exists() else {}
     for cfg in cfgs:
         launches(tag, cfg)
         traffic(tag, cfg, table)
-        full(tag, cfg)
+        full(tag, cfg, summary)
+        conv = [k for k in table.get(cfg, {}) if "conv_ss" in k]
+        if cfg in summary and conv:
+            summary[cfg]["dram_bytes_per_launch"] = table[cfg][conv[0]]
+            summary[cfg]["dram_source"] = f"profiles/{tag}_{cfg}_traffic.csv (mean over the conv_ss launches of one forward)"
         src = OUT / f"{tag}_{cfg}_plain.json"
         if src.exists():
             shutil.copy(src, PROF / src.name)
     tpath.write_text(json.dumps(table, indent=1) + "\n")
+    spath.write_text(json.dumps(summary, indent=1) + "\n")
 
 
 if __name__ == "__main__":
