@@ -115,11 +115,35 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
 __device__ __forceinline__ float2 unpack_half2(uint32_t u) {
   return __half22float2(*reinterpret_cast<const __half2*>(&u));
 }
+// ---- packed fp32 pairs (sm_100 FFMA2 / FADD2 / FMUL2: one instruction per two lanes of work) ----
+__device__ __forceinline__ float2 f2(const float* v) { return make_float2(v[0], v[1]); }
+__device__ __forceinline__ void f2_put(float* v, float2 p) { v[0] = p.x; v[1] = p.y; }
+// v[0..n) = v * s + c (elementwise, s and c per element)
+template <int N>
+__device__ __forceinline__ void fma_n(float* v, const float* s, const float* c) {
+#pragma unroll
+  for (int i = 0; i < N; i += 2) f2_put(v + i, __ffma2_rn(f2(v + i), f2(s + i), f2(c + i)));
+}
+// v[0..n) = v * s + c with one scalar s
+template <int N>
+__device__ __forceinline__ void fma_n(float* v, float s, const float* c) {
+  const float2 ss = make_float2(s, s);
+#pragma unroll
+  for (int i = 0; i < N; i += 2) f2_put(v + i, __ffma2_rn(f2(v + i), ss, f2(c + i)));
+}
+// v[0..n) += t
+template <int N>
+__device__ __forceinline__ void add_n(float* v, const float* t) {
+#pragma unroll
+  for (int i = 0; i < N; i += 2) f2_put(v + i, __fadd2_rn(f2(v + i), f2(t + i)));
+}
+
 // hi/lo fp16 pairs of (a, b); returns false if either is outside |x| < 2^15
 __device__ __forceinline__ bool split_pair(float a, float b, uint32_t& hi, uint32_t& lo) {
   hi = pack_half2(a, b);
   const float2 h = unpack_half2(hi);
-  lo = pack_half2(a - h.x, b - h.y);
+  const float2 d = __fadd2_rn(make_float2(a, b), make_float2(-h.x, -h.y));
+  lo = pack_half2(d.x, d.y);
   return fabsf(a) < 32768.f && fabsf(b) < 32768.f;
 }
 
@@ -144,8 +168,12 @@ __device__ __forceinline__ void store4_any(const TensorView& t, int b, int ch, i
 // (s: storage scale applied here, 1 when the caller folded it into its math)
 __device__ __forceinline__ void store16_split_at(const TensorView& t, int64_t e, const float* v, float s) {
   uint32_t hi[8], lo[8];
+  const float2 ss = make_float2(s, s);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) split_pair(v[2 * i] * s, v[2 * i + 1] * s, hi[i], lo[i]);
+  for (int i = 0; i < 8; ++i) {
+    const float2 x = __fmul2_rn(f2(v + 2 * i), ss);
+    split_pair(x.x, x.y, hi[i], lo[i]);
+  }
   // range check on the packed hi halves: max |hi| (NaN-propagating) < 2^15
   __half2 m = __habs2(*reinterpret_cast<const __half2*>(&hi[0]));
 #pragma unroll
@@ -256,16 +284,14 @@ __device__ __forceinline__ void decode16_raw(const TensorView& t, const Raw16& r
     }
     return;
   }
+  const float2 ss = make_float2(s, s);
 #pragma unroll
   for (int g = 0; g < 2; ++g) {
     const uint32_t hw[4] = {r.q[2 * g].x, r.q[2 * g].y, r.q[2 * g].z, r.q[2 * g].w};
     const uint32_t lw[4] = {r.q[2 * g + 1].x, r.q[2 * g + 1].y, r.q[2 * g + 1].z, r.q[2 * g + 1].w};
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float2 a = unpack_half2(hw[i]), c = unpack_half2(lw[i]);
-      v[8 * g + 2 * i] = (a.x + c.x) * s;
-      v[8 * g + 2 * i + 1] = (a.y + c.y) * s;
-    }
+    for (int i = 0; i < 4; ++i)
+      f2_put(v + 8 * g + 2 * i, __fmul2_rn(__fadd2_rn(unpack_half2(hw[i]), unpack_half2(lw[i])), ss));
   }
 }
 

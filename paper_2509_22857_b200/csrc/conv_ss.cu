@@ -989,23 +989,20 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
         const int npi = pj ? 1 : (SK && cur.nqs < NP ? cur.nqs : NP);
         if (P.concat) {
           ptx::tmem_ld16x2(d_set + P.nt + c0, d_set + c0, v, t);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] += t[i];
+          add_n<16>(v, t);
           for (int p = 1; p < npi; ++p) {
             float u[16];
             ptx::tmem_ld16x2(d_set + 2 * p * P.nt + P.nt + c0, d_set + 2 * p * P.nt + c0, u, t);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] += u[i] + t[i];
+            add_n<16>(u, t);
+            add_n<16>(v, u);
           }
         } else {
           // correction after all NP main partials (projection: after its one)
           ptx::tmem_ld16x2(d_set + (pj ? 1 : NP) * P.nt + c0, d_set + c0, v, t);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] += t[i];
+          add_n<16>(v, t);
           for (int p = 1; p < npi; ++p) {
             ptx::tmem_ld16(d_set + p * P.nt + c0, t);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] += t[i];
+            add_n<16>(v, t);
           }
         }
         if (last_of_tile) {

@@ -118,22 +118,21 @@ __device__ __forceinline__ void epi_point16(const EpiParams& e, const EpiTab& T,
                                             const float* sk, int chb) {
   const float* pt = T.ptab + chb;  // per-channel parameters, shared by all rows
   const int np = e.npad;
+  // packed fp32 pairs throughout (FFMA2 / FADD2): half the FMA-pipe issue slots
   float c[16];
   lds16(pt, c);
-#pragma unroll
-  for (int j = 0; j < 16; ++j) v[j] = fmaf(v[j], vscale, c[j]);
+  fma_n<16>(v, vscale, c);
   if (T.row_aff >= 0) {
     float sc[16], sh[16];
     lds16(pt + T.row_aff * np, sc);
     lds16(pt + (T.row_aff + 1) * np, sh);
-#pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = fmaf(v[j], sc[j], sh[j]);
+    fma_n<16>(v, sc, sh);
   }
   if (e.residual == 1) {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] += sk[j];
+    add_n<16>(v, sk);
   } else if (e.residual >= 2) {
-    // S(x, y) = x2 x^2 + y2 y^2 + xy x y + cx x + cy y + c, 4 channels at a time
+    // S(x, y) = x2 x^2 + y2 y^2 + xy x y + cx x + cy y + c, 4 channels at a time:
+    // ((x2 x + xy y + cx) x + (y2 y + cy) y + c
     const float* rc = pt + T.row_res * np;
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
@@ -144,11 +143,15 @@ __device__ __forceinline__ void epi_point16(const EpiParams& e, const EpiTab& T,
         k[r][0] = f.x; k[r][1] = f.y; k[r][2] = f.z; k[r][3] = f.w;
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < 4; i += 2) {
         const int j = 4 * g + i;
-        const float xv = e.residual == 2 ? v[j] : sk[j], yv = e.residual == 2 ? sk[j] : v[j];
-        v[j] = fmaf(k[0][i] * xv, xv, fmaf(k[1][i] * yv, yv, fmaf(k[2][i] * xv, yv,
-               fmaf(k[3][i], xv, fmaf(k[4][i], yv, k[5][i])))));
+        const float2 xv = e.residual == 2 ? f2(v + j) : f2(sk + j), yv = e.residual == 2 ? f2(sk + j) : f2(v + j);
+        const float2 x2 = make_float2(k[0][i], k[0][i + 1]), y2 = make_float2(k[1][i], k[1][i + 1]);
+        const float2 xy = make_float2(k[2][i], k[2][i + 1]), cx = make_float2(k[3][i], k[3][i + 1]);
+        const float2 cy = make_float2(k[4][i], k[4][i + 1]), c0 = make_float2(k[5][i], k[5][i + 1]);
+        const float2 ax = __ffma2_rn(x2, xv, __ffma2_rn(xy, yv, cx));
+        const float2 ay = __ffma2_rn(y2, yv, cy);
+        f2_put(v + j, __ffma2_rn(ax, xv, __ffma2_rn(ay, yv, c0)));
       }
     }
   }
@@ -159,7 +162,7 @@ __device__ __forceinline__ void epi_point16(const EpiParams& e, const EpiTab& T,
     for (int k = e.poly_deg - 1; k >= 0; --k) {
       lds16(pc + k * np, ck);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) h[j] = fmaf(h[j], v[j], ck[j]);
+      for (int j = 0; j < 16; j += 2) f2_put(h + j, __ffma2_rn(f2(h + j), f2(v + j), f2(ck + j)));
     }
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] = h[j];
