@@ -116,7 +116,8 @@ def time_redistribution(g, cfg, reps=20):
 # ---------------------------------------------------------------------------
 
 KERNEL_NAMES = {1: "conv_simt_kernel", 2: "conv_tc_kernel (3xTF32, A in TMEM)",
-                3: "conv_tc_kernel (fp16x2, A in TMEM)", 5: "conv_ss_kernel (fp16x2, halo tiles in smem)"}
+                3: "conv_tc_kernel (fp16x2, A in TMEM)", 5: "conv_ss_kernel (fp16x2, halo tiles in smem)",
+                6: "conv_blk_kernel (fp16x2, image-resident runs)"}
 OTHER_NAMES = {1: "ingest_kernel", 3: "linear_kernel", 12: "copyout_kernel"}
 
 
@@ -220,7 +221,7 @@ def roofline(eng, plan, batch, ts: TimelineStats, ms_per_step, config):
     per-layer roofline max(F/P, B/BW) says binds.  Also the SURVEY 8(d) step
     figure sum_l max(F_l/P, B_l/BW) / ms_per_step."""
     hbm, bf16, _, basis = peaks()
-    rate = {3: bf16 / 3.0, 5: bf16 / 3.0, 2: bf16 / 6.0, 1: bf16 / 6.0}
+    rate = {3: bf16 / 3.0, 5: bf16 / 3.0, 6: bf16 / 3.0, 2: bf16 / 6.0, 1: bf16 / 6.0}
     lw = eng.lw
     if not ts.steps:
         return {"bound": None, "achieved": None, "peak": None, "unit": None, "frac": None, "traffic": None,

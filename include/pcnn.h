@@ -249,6 +249,12 @@ typedef struct pcnn_plan_options {
   int64_t timeline;         /* 1: every launch stamps %globaltimer at its
                                first CTA's start and last CTA's exit
                                (pcnn_plan_timeline)                        */
+  int64_t image_blocks;     /* >0: runs of stride-1 3x3 convs (32-64
+                               channels) on small images in ONE launch,
+                               each CTA keeping whole images' activations
+                               in shared memory between the layers; the
+                               value is the most images a CTA keeps
+                               resident (1 or 2; default 2)             */
   int64_t debug;            /* diagnostic bits (tests / tools only):
                                2 skip MMAs, 4 skip epilogues, 32 CTA-0
                                trace, 64 per-CTA stamps                    */
@@ -289,7 +295,9 @@ int pcnn_plan_unit_launch(const pcnn_plan* plan, int unit);
 int pcnn_plan_destroy(pcnn_plan* plan);
 /* number of kernel launches one forward issues (for gpu_launches) */
 int pcnn_plan_num_launches(const pcnn_plan* plan);
-/* conv implementation of unit i: 1 SIMT, 2 tcgen05 3xTF32, 3 tcgen05 fp16x2 */
+/* conv implementation of unit i: 1 SIMT, 2 tcgen05 3xTF32, 3 tcgen05 fp16x2
+ * (A in TMEM), 5 tcgen05 fp16x2 halo tiles, 6 the same inside an
+ * image-resident run (options.image_blocks) */
 int pcnn_plan_unit_impl(const pcnn_plan* plan, int unit);
 /* storage format of tensor t: 0 float32; 1 split (two fp16 planes x = hi +
  * lo on the zero-bordered grid, written by its producer for fp16x2 convs);

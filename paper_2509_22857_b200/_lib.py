@@ -88,7 +88,7 @@ class RewriteDesc(ctypes.Structure):
 
 _OPT_INT_FIELDS_A = ("size", "split", "halo_tiles", "fuse_projection", "band_pool", "streamk")
 _OPT_INT_FIELDS_B = ("flag_sync", "prezero", "linear_out", "pdl", "graph", "ss_mt", "ss_share", "ss_psub",
-                     "ss_wres", "tc_stage", "timeline", "debug")
+                     "ss_wres", "tc_stage", "timeline", "image_blocks", "debug")
 
 
 class PlanOptions(ctypes.Structure):
@@ -120,7 +120,7 @@ ENV_OPTIONS = {
     "PCNN_NO_GRAPH": ("graph", 0), "PCNN_SS_MT": ("ss_mt", int), "PCNN_SS_SHARE": ("ss_share", int),
     "PCNN_SS_PSUB": ("ss_psub", int), "PCNN_SS_WRES": ("ss_wres", int), "PCNN_TC_NOSTAGE": ("tc_stage", 0),
     "PCNN_TC_DEBUG": ("debug", int), "PCNN_STREAMK_FILL": ("streamk_fill", float),
-    "PCNN_NO_TIMELINE": ("timeline", 0),
+    "PCNN_NO_TIMELINE": ("timeline", 0), "PCNN_NO_BLOCKS": ("image_blocks", 0), "PCNN_BLOCKS": ("image_blocks", int),
 }
 
 

@@ -100,7 +100,7 @@ def precision_check(g: ModelGraph, n_inputs: int = 64, seed: int = 0, tol: float
     rows = []
     for i, (u, nodes) in enumerate(zip(fast.lw.units, fast.lw.unit_nodes)):
         t = u.get("out", -1)
-        if t is None or t < 0 or u["kind"] in (L.UNIT_INGEST, L.UNIT_COPYOUT):
+        if t is None or t < 0 or u["kind"] in (L.UNIT_INGEST, L.UNIT_COPYOUT) or not pf.materialized(i):
             continue
         a, b = pf.read_tensor(t).astype(np.float64), pr.read_tensor(t).astype(np.float64)
         scale = max(float(np.abs(b).max()), 1e-30)

@@ -82,6 +82,10 @@ struct pcnn_plan {
   std::vector<EltArgs> post_pool;
   std::vector<char> has_post_pool;
   float* scratch = nullptr;
+  // image-resident runs (build_blocks): blk_of[u] = run index or -1; a run
+  // launches with its first unit
+  std::vector<BlkRun*> blks;
+  std::vector<int> blk_of, blk_first;
   // launch timeline (options.timeline): [n_units][2] (common.cuh tl_mark)
   unsigned long long* tl_dev = nullptr;
   unsigned long long* tl_host = nullptr;
@@ -288,6 +292,19 @@ void enqueue_unit(pcnn_plan* p, int ui, const float* x, float* logits, cudaStrea
       break;
     case PCNN_UNIT_CONV: {
       if (p->fused[ui]) break;  // computed by the previous unit's launch
+      if (!p->blk_of.empty() && p->blk_of[ui] >= 0) {
+        const int r = p->blk_of[ui];
+        if (p->blk_first[r] == ui) {
+          int last = ui;
+          while (last + 1 < (int)p->units.size() && p->blk_of[last + 1] == r) ++last;
+          if (p->units[last].pool == PCNN_POOL_GLOBAL && !p->prezeroed[last]) {
+            const ConvArgs& al = p->conv_args[last];
+            cudaMemsetAsync(al.epi.out.base, 0, sizeof(float) * (size_t)p->batch * al.epi.out.cpad(), s);
+          }
+          blk_launch(p->blks[r], s, tl, p->kopt.pdl);
+        }
+        break;  // the other units of the run are computed by that launch
+      }
       ConvArgs a = p->conv_args[ui];
       a.tl = tl;
       if (u.pool == PCNN_POOL_GLOBAL && !p->prezeroed[ui])
@@ -453,6 +470,142 @@ int plan_local_pools(pcnn_plan* p) {
     p->launches += 1;
   }
   return PCNN_OK;
+}
+
+// Image-resident runs: maximal sequences of consecutive halo-tile convs, each
+// reading the previous one's output, stride 1, 3x3, C = 32 or 64 channels
+// in and out, the same small image (whole-image slots fit shared memory), no
+// pools but a global pool on the last unit, every residual either produced
+// inside the run or one of the two external tensors (the first unit's input
+// and residual), and every output but the last read only inside the run.
+// Slots are assigned greedily by liveness (a tensor's slot is free after its
+// last reader); the run then computes in ONE conv_blk_kernel launch.
+void build_blocks(pcnn_plan* p) {
+  const int n = (int)p->units.size();
+  p->blk_of.assign(n, -1);
+  if (!p->opt.image_blocks || p->flags_on) return;
+  std::vector<std::vector<int>> readers(p->tensors.size());
+  for (int i = 0; i < n; ++i) {
+    const pcnn_unit_desc& u = p->units[i];
+    if (u.in >= 0) readers[u.in].push_back(i);
+    if (u.in2 >= 0) readers[u.in2].push_back(i);
+  }
+  auto eligible = [&](int i) {
+    const pcnn_unit_desc& u = p->units[i];
+    if (u.kind != PCNN_UNIT_CONV || p->impl[i] != 5 || p->fused[i]) return false;
+    const ConvArgs& a = p->conv_args[i];
+    return a.kh == 3 && a.kw == 3 && a.stride == 1 && a.pad == 1 && !a.proj && a.in.split == 1 && !a.sk_flags &&
+           (a.npad == 32 || a.npad == 64) && a.in.cpad() == a.npad && u.cout == a.npad;
+  };
+  int i = 0;
+  while (i < n) {
+    if (!eligible(i)) { ++i; continue; }
+    const ConvArgs& a0 = p->conv_args[i];
+    int j = i + 1;
+    while (j < n && j - i < 6 && eligible(j) && p->units[j].in == p->units[j - 1].out &&
+           p->conv_args[j].in.h == a0.in.h && p->conv_args[j].in.w == a0.in.w &&
+           p->conv_args[j].npad == a0.npad && p->conv_args[j - 1].epi.pool == PCNN_POOL_NONE)
+      ++j;
+    // shrink until every condition holds
+    bool done = false;
+    for (; j - i >= 2; --j) {
+      const int m = j - i;
+      const int64_t ext_in = p->units[i].in, ext_res = p->units[i].residual ? p->units[i].in2 : -1;
+      bool ok = p->conv_args[j - 1].epi.pool == PCNN_POOL_NONE || p->conv_args[j - 1].epi.pool == PCNN_POOL_GLOBAL;
+      for (int k = i; k < j && ok; ++k) {
+        if (k < j - 1)
+          for (int rd : readers[p->units[k].out]) ok &= rd > k && rd < j;  // consumed inside the run only
+        if (k > i && p->units[k].residual) {
+          const int64_t t = p->units[k].in2;
+          bool inside = t == ext_in || t == ext_res;
+          for (int q = i; q < k; ++q) inside |= p->units[q].out == t;
+          ok &= inside;
+        }
+        if (k < j - 1) ok &= p->conv_args[k].epi.pool == PCNN_POOL_NONE;
+      }
+      if (!ok) continue;
+      // liveness: last unit (index in the run) reading each tensor
+      std::vector<int64_t> tens;
+      std::vector<int> last_use;
+      auto idx = [&](int64_t t) {
+        for (size_t q = 0; q < tens.size(); ++q)
+          if (tens[q] == t) return (int)q;
+        tens.push_back(t);
+        last_use.push_back(-1);
+        return (int)tens.size() - 1;
+      };
+      idx(ext_in);
+      if (ext_res >= 0) idx(ext_res);
+      for (int k = 0; k < m; ++k) {
+        const pcnn_unit_desc& u = p->units[i + k];
+        last_use[idx(u.in)] = k;
+        if (u.residual) last_use[idx(u.in2)] = k;
+        if (k < m - 1) idx(u.out);
+      }
+      // two slots when every residual's last reader writes over it in
+      // place (the epilogue thread reads position p's residual, then writes
+      // p), else three
+      for (int nslots = 2; nslots <= 3; ++nslots) {
+      std::vector<int64_t> holder(nslots, -1);
+      std::vector<int> slot_of(tens.size(), -1);
+      auto place = [&](int64_t t, int k) {
+        for (int sidx = 0; sidx < nslots; ++sidx) {
+          const int64_t h = holder[sidx];
+          if (h < 0 || last_use[idx(h)] < k) {
+            holder[sidx] = t;
+            slot_of[idx(t)] = sidx;
+            return sidx;
+          }
+        }
+        return -1;
+      };
+      int ext_in_slot = place(ext_in, 0), ext_res_slot = ext_res >= 0 ? place(ext_res, 0) : -1;
+      std::vector<int> in_s(m), res_s(m), out_s(m), kind(m, 0);
+      for (int k = 0; k < m; ++k) {
+        const pcnn_unit_desc& u = p->units[i + k];
+        kind[k] = (u.in == ext_in ? 1 : 0) |
+                  (u.residual ? (u.in2 == ext_in ? 1 : (u.in2 == ext_res ? 2 : 0)) << 2 : 0);
+      }
+      bool fit = ext_in_slot >= 0 && (ext_res < 0 || ext_res_slot >= 0);
+      for (int k = 0; k < m && fit; ++k) {
+        const pcnn_unit_desc& u = p->units[i + k];
+        in_s[k] = slot_of[idx(u.in)];
+        res_s[k] = u.residual ? slot_of[idx(u.in2)] : -1;
+        if (k == m - 1) {
+          out_s[k] = -1;
+        } else {
+          // the output may not take its input's slot, and takes its
+          // residual's only when this unit is the residual's last reader
+          int sl = -1;
+          for (int sidx = 0; sidx < nslots; ++sidx) {
+            const int64_t h = holder[sidx];
+            if (sidx == in_s[k]) continue;
+            if (sidx == res_s[k] ? last_use[idx(h)] == k : (h < 0 || last_use[idx(h)] < k)) { sl = sidx; break; }
+          }
+          if (sl < 0) { fit = false; break; }
+          holder[sl] = u.out;
+          slot_of[idx(u.out)] = sl;
+          out_s[k] = sl;
+        }
+      }
+      if (!fit) continue;
+      std::vector<ConvArgs> layers(p->conv_args.begin() + i, p->conv_args.begin() + j);
+      BlkRun* r = blk_create(layers.data(), m, in_s.data(), res_s.data(), out_s.data(), kind.data(), nslots, ext_in_slot,
+                             ext_res_slot, p->views[ext_in], ext_res >= 0 ? p->views[ext_res] : p->views[ext_in],
+                             p->status_dev, p->batch, (int)p->opt.image_blocks);
+      if (!r) continue;
+      const int id = (int)p->blks.size();
+      p->blks.push_back(r);
+      p->blk_first.push_back(i);
+      for (int k = i; k < j; ++k) p->blk_of[k] = id;
+      p->launches -= m - 1;
+      done = true;
+      break;
+      }
+      if (done) break;
+    }
+    i = j > i + 1 ? j : i + 1;
+  }
 }
 
 // A residual block's 1x1 projection (unit i + 1) reads the same input with
@@ -662,6 +815,7 @@ void pcnn_plan_options_default(pcnn_plan_options* o) {
   o->ss_wres = 1;
   o->tc_stage = 1;
   o->timeline = 1;
+  o->image_blocks = 2;
   o->debug = 0;
 }
 
@@ -791,6 +945,26 @@ int pcnn_plan_create_ex(const pcnn_unit_desc* units, int n_units, const pcnn_ten
   fuse_projections(p);
   build_flags(p);
   plan_streamk(p);
+  build_blocks(p);
+  // a run ending in a global pool: its sums were prezeroed by the unit before
+  // the pooled conv, which is now inside the run -- zero them before the run
+  for (size_t r = 0; r < p->blks.size(); ++r) {
+    int last = p->blk_first[r];
+    while (last + 1 < n_units && p->blk_of[last + 1] == (int)r) ++last;
+    if (p->prezeroed[last]) {
+      p->prezeroed[last] = 0;
+      p->conv_args[last - 1].prezero = nullptr;
+      const int before = p->blk_first[r] - 1;
+      int lb = before;
+      while (lb > 0 && p->fused[lb]) --lb;  // the launch that computes unit `before`
+      if (lb >= 0 && p->impl[lb] == 5 && p->units[lb].kind == PCNN_UNIT_CONV && !p->conv_args[lb].prezero &&
+          (p->blk_of[lb] < 0)) {
+        p->conv_args[lb].prezero = p->conv_args[last].epi.out.base;
+        p->conv_args[lb].prezero_n = (int64_t)p->batch * p->conv_args[last].epi.out.cpad();
+        p->prezeroed[last] = 1;
+      }
+    }
+  }
   if (cudaStreamCreateWithFlags(&p->capture_stream, cudaStreamNonBlocking) != cudaSuccess) {
     pcnn_plan_destroy(p);
     return fail(PCNN_ERR_CUDA, "cudaStreamCreate failed");
@@ -819,6 +993,7 @@ int pcnn_plan_destroy(pcnn_plan* p) {
   if (p->status_pinned) cudaFreeHost(p->status_pinned);
   if (p->status_host) cudaFreeHost(p->status_host);
   if (p->scratch) cudaFree(p->scratch);
+  for (BlkRun* b : p->blks) blk_destroy(b);
   delete p;
   return PCNN_OK;
 }
@@ -842,6 +1017,7 @@ int pcnn_plan_timeline(pcnn_plan* p, int64_t* ns, int max_units, void* stream) {
 int pcnn_plan_unit_launch(const pcnn_plan* p, int unit) {
   if (!p || unit < 0 || unit >= (int)p->units.size()) return -1;
   int u = unit;
+  if (!p->blk_of.empty() && p->blk_of[u] >= 0) return p->blk_first[p->blk_of[u]];  // an image-resident run
   while (u > 0 && p->fused[u]) --u;  // a fused unit runs in its predecessor's launch
   return u;
 }
@@ -853,6 +1029,7 @@ int pcnn_plan_flags(const pcnn_plan* p) { return p && p->flags_on ? 1 : 0; }
 
 int pcnn_plan_unit_impl(const pcnn_plan* p, int unit) {
   if (!p || unit < 0 || unit >= (int)p->units.size()) return -1;
+  if (!p->blk_of.empty() && p->blk_of[unit] >= 0) return 6;  // halo-tile arithmetic inside an image-resident run
   return p->impl[unit];
 }
 

@@ -26,6 +26,7 @@
 // epilogue warpgroups (one per accumulator buffer), warp 8 TMEM allocator +
 // bulk-copy producer, warp 9 MMA issuer.
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "epi_tc.cuh"
@@ -1360,7 +1361,479 @@ bool make_ss_params(const ConvArgs& a, SsParams& P, bool allow_wres = true) {
   return nt == 128 && make_ss_params_nt(a, P, 64, false, allow_wres);
 }
 
+// =====================================================================
+// Image-resident residual stages (conv_blk_kernel): a run of stride-1 3x3
+// convs on one grid with C = 32..128 channels (ResNet-20's identity blocks
+// and the conv that follows a downsampling block) in ONE launch.  Each CTA
+// takes whole images; an image's activations never leave shared memory
+// between the run's layers: the run's external input (and external residual)
+// are bulk-copied in, every layer's output is written by the epilogue as a
+// split hi/lo tensor into a shared-memory slot in the halo layout, and the
+// next layer's MMAs read it there (the same fixed-offset tap descriptors as
+// conv_ss).  Only the last layer stores to global memory (or into the global
+// pool sums).  Whole images need no halo recompute: the shared zero border
+// rows / columns of the grid are the padding.
+//
+// Pipelining inside the CTA.  One resident image (ni = 1): accumulators
+// alternate between two TMEM buffers by layer; the epilogue releases output
+// chunk q of layer l (16 channels, all positions) through ready[q], so the
+// MMA warp starts layer l+1's chunk q while later chunks of layer l are
+// still draining.  Two resident images (ni = 2, when both images' slots fit):
+// each image owns a slot set and a TMEM buffer, and the MMA warp alternates
+// between them layer by layer, so one image's epilogue runs under the other
+// image's MMAs (a layer's epilogue is as long as its MMAs; with one image the
+// two only overlap per chunk).  Weights stream through a ring (one stage = one
+// 16-channel chunk, all taps), in MMA order.
+//
+// Slot planes are P_img positions long: a sub-tile's A reads run past the
+// image into the next plane (or the weight ring) only for rows whose outputs
+// are discarded.
+// =====================================================================
+constexpr int kBlkMaxLayers = 6;
+constexpr int kBlkMaxChunks = 8;
+constexpr int kBlkStages = 4;
+
+struct BlkLayer {
+  EpiParams epi;       // this layer's epilogue; epi.out is the global output (last layer only)
+  EpiTab etab;
+  const __half* w;     // tcss weight image (one n-tile = all C output channels)
+  const float* wscale; // its 2^-e
+  int in_slot, res_slot, out_slot;  // res_slot -1: no residual; out_slot -1: global output
+  int ptab_off;        // floats into the CTA's parameter-table area
+  float in_sload;      // storage load scale of the input (the external input; 1 for slots)
+  float res_sload;     // same for the residual
+  int res_ext;         // the residual is an external tensor (wait for its copy)
+};
+
+struct BlkParams {
+  BlkLayer L[kBlkMaxLayers];
+  int nl, C, nq;
+  int H, W, wp;        // image, grid row pitch W + 1
+  int S;               // 128-row sub-tiles per image
+  int p_out0, nout;    // first output position (1 + wp), output positions H * wp
+  int P_img;           // positions per external copy: (H + 2) wp
+  uint32_t plane;      // bytes per (8-channel group, hi | lo) plane of a slot
+  uint32_t slot_bytes; // nq * 4 * plane
+  uint32_t set_bytes;  // nslots * slot_bytes: one resident image
+  int nslots;
+  int ni;              // resident images per CTA (1 or 2)
+  int ext_in_slot, ext_res_slot;
+  TensorView ext_in, ext_res;
+  int batch;
+  int stages;
+  uint32_t b_bytes;    // one chunk of weights: 9 taps x 64 C bytes
+  uint32_t tmem_cols;
+  uint32_t set_cols;   // accumulator columns per sub-tile: [main C | corr C]
+  int ptab_floats;
+  int toff[9];         // tap (ky, kx) -> ky wp + kx (A base = first output position - (wp + 1))
+  int* flag;           // the plan's status word (an activation left the fp16 range)
+  unsigned long long* tl;
+  int dbg;             // debug bit 32: CTA-0 event trace (built with -DPCNN_SS_TRACE)
+};
+
+// CTA-0 event trace of the block kernel (region: 0 producer, 1 MMA, 2 epilogue warp 0)
+struct BlkTracer {
+  uint32_t n = 0;
+  __device__ __forceinline__ void operator()(const BlkParams& P, int region, uint32_t tag) {
+#ifdef PCNN_SS_TRACE
+    if ((P.dbg & 32) && blockIdx.x == 0 && n < kTraceRegion)
+      g_ss_trace[region * kTraceRegion + n++] = ((unsigned long long)tag << 48) | (clock64() & 0xFFFFFFFFFFFFull);
+#else
+    (void)P; (void)region; (void)tag;
+#endif
+  }
+};
+
+struct BlkSmem {
+  uint64_t wfull[kBlkStages], wempty[kBlkStages];
+  uint64_t acc_full[2], acc_empty[2];
+  uint64_t ready[kBlkMaxChunks];
+  uint64_t ext_full[2], img_free[2];
+  uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(kThreads, 1) conv_blk_kernel(const __grid_constant__ BlkParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  const uint32_t slots = ptx::smem_u32(smem);
+  const uint32_t ring = slots + (uint32_t)P.ni * P.set_bytes;
+  BlkSmem* S = reinterpret_cast<BlkSmem*>(smem + (size_t)P.ni * P.set_bytes + (size_t)P.stages * P.b_bytes);
+  float* ptab = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(S) + ((sizeof(BlkSmem) + 15) & ~size_t(15)));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = (int)gridDim.x;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < P.stages; ++i) {
+      ptx::mbar_init(ptx::smem_u32(&S->wfull[i]), 1);
+      ptx::mbar_init(ptx::smem_u32(&S->wempty[i]), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(ptx::smem_u32(&S->acc_full[i]), 1);
+      ptx::mbar_init(ptx::smem_u32(&S->acc_empty[i]), 8);
+    }
+    for (int q = 0; q < kBlkMaxChunks; ++q) ptx::mbar_init(ptx::smem_u32(&S->ready[q]), 8);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(ptx::smem_u32(&S->ext_full[i]), 1);
+      ptx::mbar_init(ptx::smem_u32(&S->img_free[i]), 8);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == kWarpProducer) ptx::tmem_alloc(ptx::smem_u32(&S->tmem_base), P.tmem_cols);
+  // zero the activation slots (their unwritten border rows are the conv padding)
+  {
+    uint4* z = reinterpret_cast<uint4*>(smem);
+    const uint32_t n16 = (uint32_t)P.ni * P.set_bytes / 16;
+    for (uint32_t i = threadIdx.x; i < n16; i += kThreads) z[i] = make_uint4(0, 0, 0, 0);
+  }
+  for (int l = 0; l < P.nl; ++l) epi_fill_tab(P.L[l].epi, P.L[l].etab, ptab + P.L[l].ptab_off, threadIdx.x, kThreads);
+  ptx::fence_proxy_async();  // generic zero stores -> tcgen05 reads of the slots
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = S->tmem_base;
+  ptx::griddep_wait();
+  ptx::griddep_launch();
+  tl_mark(P.tl, 0);
+
+  if (warp == kWarpProducer) {
+    // ===== producer: per image the external tensors (after the previous
+    // image is drained), then every (layer, chunk) weight stage =====
+    int st = 0;
+    uint32_t ph = 0;
+    BlkTracer tr;
+    for (int g = 0;; ++g) {
+      const int b0 = blockIdx.x + G * g * P.ni;
+      if (b0 >= P.batch) break;
+      const int nv = (P.ni == 2 && b0 + G < P.batch) ? 2 : 1;
+      for (int i = 0; i < nv; ++i) {
+        const int b = b0 + G * i;
+        if (g > 0) {
+          if (lane == 0) ptx::mbar_wait_sleep(ptx::smem_u32(&S->img_free[i]), (g - 1) & 1);
+          __syncwarp();
+        }
+        const uint32_t set = slots + (uint32_t)i * P.set_bytes;
+        const int nt_ext = (P.ext_in_slot >= 0) + (P.ext_res_slot >= 0);
+        const uint32_t bytes = (uint32_t)P.P_img * 16;
+        const uint32_t eb = ptx::smem_u32(&S->ext_full[i]);
+        if (lane == 0) ptx::mbar_arrive_tx(eb, (uint32_t)nt_ext * P.nq * 4 * bytes);
+        __syncwarp();
+        // copy k: tensor k / (4 nq), chunk, group, plane -- one copy per lane per round
+        const int total = nt_ext * 4 * P.nq;
+        for (int k = lane; k < total; k += 32) {
+          const int ti = k / (4 * P.nq), r = k - ti * 4 * P.nq, q = r >> 2, gp = r & 3;
+          const bool use_in = P.ext_in_slot >= 0 && ti == 0;
+          const TensorView& t = use_in ? P.ext_in : P.ext_res;
+          const int slot = use_in ? P.ext_in_slot : P.ext_res_slot;
+          const int gg = gp & 1, lo = gp >> 1;
+          const __half* base = lo ? t.lo() : t.hi();
+          const int64_t off = (2 * q + gg) * t.kstride + (int64_t)b * (P.H + 1) * P.wp * 8;
+          ptx::bulk_g2s(set + (uint32_t)slot * P.slot_bytes + (uint32_t)(q * 4 + gp) * P.plane, base + off, bytes, eb);
+        }
+        if (lane == 0) tr(P, 0, 0x100 | g);  // externals issued
+      }
+      if (lane == 0) {
+        for (int l = 0; l < P.nl; ++l)
+          for (int i = 0; i < nv; ++i)
+            for (int q = 0; q < P.nq; ++q) {
+              ptx::mbar_wait_sleep(ptx::smem_u32(&S->wempty[st]), ph ^ 1);
+              tr(P, 0, 0x200 | (l << 4) | q);
+              const uint32_t bar = ptx::smem_u32(&S->wfull[st]);
+              ptx::mbar_arrive_tx(bar, P.b_bytes);
+              ptx::bulk_g2s(ring + (uint32_t)st * P.b_bytes, P.L[l].w + (int64_t)q * 9 * 32 * P.C, P.b_bytes, bar);
+              if (++st == P.stages) { st = 0; ph ^= 1; }
+            }
+      }
+      __syncwarp();
+    }
+  } else if (warp == kWarpMma) {
+    // ===== MMA issuer =====
+    const int nt = P.C;
+    const uint32_t idesc = ptx::idesc_f16(kTileM, nt), idesc2 = ptx::idesc_f16(kTileM, 2 * nt);
+    const uint32_t a_lbo = P.plane, b_lbo = 2 * nt * 16;
+    uint64_t offs[9];
+#pragma unroll
+    for (int t = 0; t < 9; ++t) offs[t] = (uint64_t)(P.toff[t] * 16 >> 4);
+    const uint64_t bstep = (uint64_t)(64 * nt) >> 4, blo = (uint64_t)(nt * 16) >> 4;
+    int st = 0;
+    uint32_t ph = 0;
+    uint32_t use[2] = {0u, 0u};
+    int gl = 0;
+    BlkTracer tr;
+    for (int g = 0;; ++g) {
+      const int b0 = blockIdx.x + G * g * P.ni;
+      if (b0 >= P.batch) break;
+      const int nv = (P.ni == 2 && b0 + G < P.batch) ? 2 : 1;
+      for (int l = 0; l < P.nl; ++l)
+        for (int i = 0; i < nv; ++i, ++gl) {
+          // ni = 1: buffers by layer parity; ni = 2: by image
+          const uint32_t buf = P.ni == 1 ? (uint32_t)(gl & 1) : (uint32_t)i;
+          if (lane == 0) tr(P, 1, 0x300 | (l << 4) | (i << 3));
+          // ni = 2: this also waits for the image's previous layer in its slot
+          ptx::mbar_wait(ptx::smem_u32(&S->acc_empty[buf]), (use[buf] & 1) ^ 1);
+          if (lane == 0) tr(P, 1, 0x400 | (l << 4) | (i << 3));
+          ptx::tc_fence_after();
+          const uint32_t in_base = slots + (uint32_t)i * P.set_bytes + (uint32_t)P.L[l].in_slot * P.slot_bytes;
+          for (int q = 0; q < P.nq; ++q) {
+            if (l == 0) {
+              if (q == 0) ptx::mbar_wait(ptx::smem_u32(&S->ext_full[i]), g & 1);
+            } else if (P.ni == 1) {
+              ptx::mbar_wait(ptx::smem_u32(&S->ready[q]), (gl - 1) & 1);  // layer l-1's chunk q is in the slot
+            }
+            if (lane == 0) tr(P, 1, 0x500 | (l << 4) | (i << 3) | q);  // input chunk ready
+            ptx::mbar_wait(ptx::smem_u32(&S->wfull[st]), ph);
+            if (lane == 0) tr(P, 1, 0x600 | (l << 4) | (i << 3) | q);  // weights ready
+            ptx::tc_fence_after();
+            const uint32_t cb = in_base + (uint32_t)q * 4 * P.plane;
+            const uint64_t b0d = ptx::smem_desc_noswz(ring + (uint32_t)st * P.b_bytes, b_lbo, 128);
+            for (int s = 0; s < P.S; ++s) {
+              // rows of sub-tile s: positions p_out0 + 128 s + r; tap t reads
+              // p - (wp + 1) + toff[t], and p_out0 = wp + 1
+              const uint32_t a0 = cb + (uint32_t)(128 * s) * 16;
+              const uint64_t ah = ptx::smem_desc_noswz(a0, a_lbo, 128), al = ptx::smem_desc_noswz(a0 + 2 * P.plane, a_lbo, 128);
+              const uint32_t dm = tmem + (buf * P.S + s) * P.set_cols;
+              ss_stage<9>(true, dm, dm + nt, ah, al, b0d, bstep, blo, idesc2, idesc, q > 0 ? 1u : 0u, 1u, offs);
+            }
+            ptx::mma_commit_warp(ptx::smem_u32(&S->wempty[st]));
+            if (lane == 0) tr(P, 1, 0x700 | (l << 4) | (i << 3) | q);  // issued
+            if (++st == P.stages) { st = 0; ph ^= 1; }
+          }
+          ptx::mma_commit_warp(ptx::smem_u32(&S->acc_full[buf]));
+          ++use[buf];
+        }
+    }
+  } else if (warp < 8) {
+    // ===== epilogue: every 16-channel chunk k is split between the two
+    // warpgroups (warpgroup ew: channels 16k + 8ew .. +8 of every sub-tile),
+    // chunks in order, so chunk k of a layer is complete -- and the next
+    // layer's MMAs on it can start -- after the shortest time; a layer's
+    // output goes to its slot (split hi/lo, the next layer's A operand) or,
+    // for the last layer, to global memory =====
+    const int ew = warp >> 2, row = threadIdx.x & 127;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    uint32_t use[2] = {0u, 0u};
+    int gl = 0;
+    BlkTracer tr;
+    for (int g = 0;; ++g) {
+      const int b0 = blockIdx.x + G * g * P.ni;
+      if (b0 >= P.batch) break;
+      const int nv = (P.ni == 2 && b0 + G < P.batch) ? 2 : 1;
+      for (int l = 0; l < P.nl; ++l)
+        for (int i = 0; i < nv; ++i, ++gl) {
+        const int b = b0 + G * i;
+        const uint32_t set = slots + (uint32_t)i * P.set_bytes;
+        const BlkLayer& L = P.L[l];
+        const EpiParams& e = L.epi;
+        const bool last = l == P.nl - 1;
+        if (L.res_ext) ptx::mbar_wait_warp(ptx::smem_u32(&S->ext_full[i]), g & 1);
+        const uint32_t buf = P.ni == 1 ? (uint32_t)(gl & 1) : (uint32_t)i;
+        if (threadIdx.x == 0) tr(P, 2, 0x800 | (l << 4) | (i << 3));
+        ptx::mbar_wait_warp(ptx::smem_u32(&S->acc_full[buf]), use[buf] & 1);
+        if (threadIdx.x == 0) tr(P, 2, 0x900 | (l << 4) | (i << 3));
+        ptx::tc_fence_after();
+        EpiTab tab = L.etab;
+        tab.ptab = ptab + L.ptab_off;
+        const float wsc = __ldg(L.wscale) * L.in_sload;
+        for (int k = 0; k < P.nq; ++k) {
+          const int chb = 16 * k + 8 * ew;
+          float psum[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) psum[j] = 0.f;
+          for (int s = 0; s < P.S; ++s) {
+            const int p = P.p_out0 + 128 * s + row;
+            const int y = (p - 1) / P.wp - 1, x = p - 1 - (y + 1) * P.wp;
+            const bool inside = p < P.p_out0 + P.nout, valid = inside && x < P.W;
+            float v[8], t[8];
+            const uint32_t d = tmem + lane_off + (buf * P.S + s) * P.set_cols;
+            ptx::tmem_ld8x2(d + P.C + chb, d + chb, v, t);
+            add_n<8>(v, t);
+            float sk[8];
+            if (L.res_slot >= 0) {
+              // this group's hi and lo planes: [g0 hi][g1 hi][g0 lo][g1 lo] per chunk
+              const uint32_t rb = set + (uint32_t)L.res_slot * P.slot_bytes + (uint32_t)(k * 4 + ew) * P.plane +
+                                  (uint32_t)p * 16;
+              uint4 h, q;
+              asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(h.x), "=r"(h.y), "=r"(h.z), "=r"(h.w) : "r"(rb) : "memory");
+              asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "r"(rb + 2 * P.plane) : "memory");
+              const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {q.x, q.y, q.z, q.w};
+              const float2 ss = make_float2(L.res_sload, L.res_sload);
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                f2_put(sk + 2 * i, __fmul2_rn(__fadd2_rn(unpack_half2(hw[i]), unpack_half2(lw[i])), ss));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) sk[j] = 0.f;
+            }
+            epi_point8(e, tab, v, wsc, sk, chb);
+            if (!last) {
+              if (inside) {
+                uint32_t hi[4], lo[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  if (valid) split_pair(v[2 * i], v[2 * i + 1], hi[i], lo[i]);
+                  else hi[i] = lo[i] = 0u;
+                }
+                __half2 m = __habs2(*reinterpret_cast<const __half2*>(&hi[0]));
+#pragma unroll
+                for (int i = 1; i < 4; ++i) m = __hmax2_nan(m, __habs2(*reinterpret_cast<const __half2*>(&hi[i])));
+                const float2 mf = __half22float2(m);
+                if (!(mf.x < 32768.f && mf.y < 32768.f)) atomicExch(P.flag, 1);
+                const uint32_t ob = set + (uint32_t)L.out_slot * P.slot_bytes + (uint32_t)(k * 4 + ew) * P.plane +
+                                    (uint32_t)p * 16;
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(ob), "r"(hi[0]), "r"(hi[1]), "r"(hi[2]),
+                             "r"(hi[3]) : "memory");
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(ob + 2 * P.plane), "r"(lo[0]), "r"(lo[1]),
+                             "r"(lo[2]), "r"(lo[3]) : "memory");
+              }
+            } else if (e.pool == PCNN_POOL_GLOBAL) {
+              if (valid) add_n<8>(psum, v);
+            } else if (valid) {
+              store8_any(e.out, b, chb, y, x, v);
+            }
+          }
+          if (last && e.pool == PCNN_POOL_GLOBAL) {
+            // every row of the tile is image b: reduce the warp's rows, one atomic per channel
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+#pragma unroll
+              for (int o = 16; o; o >>= 1) psum[j] += __shfl_xor_sync(0xffffffffu, psum[j], o);
+            if (lane < 8) {
+              float mine = psum[0];
+#pragma unroll
+              for (int j = 1; j < 8; ++j)
+                if (lane == j) mine = psum[j];
+              if (chb + lane < e.cout) atomicAdd(e.out.base + (int64_t)b * e.npad + chb + lane, mine * __ldg(e.pool_p));
+            }
+          }
+          if (P.ni == 1) {
+            // this warp's rows of chunk k are in the slot: hand them to the
+            // async proxy (tcgen05.mma reads) and count the warp in (8 warps)
+            ptx::fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->ready[k]));
+          }
+          if (threadIdx.x == 0) tr(P, 2, 0xA00 | (l << 4) | (i << 3) | k);
+        }
+        // ni = 2: acc_empty also hands the whole output to the image's next layer
+        if (P.ni == 2) ptx::fence_proxy_async();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->acc_empty[buf]));
+        ++use[buf];
+        if (last && lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->img_free[i]));
+      }
+    }
+  }
+  __syncthreads();
+  tl_mark(P.tl, 1);
+  if (warp == kWarpProducer) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, P.tmem_cols);
+  }
+}
+
 }  // namespace
+
+struct BlkRun {
+  BlkParams P;
+  size_t smem;
+};
+
+BlkRun* blk_create(const ConvArgs* layers, int n, const int* in_slot, const int* res_slot, const int* out_slot,
+                   const int* src_kind, int nslots, int ext_in_slot, int ext_res_slot, const TensorView& ext_in,
+                   const TensorView& ext_res, int* flag, int batch, int max_images) {
+  if (n < 2 || n > kBlkMaxLayers) return nullptr;
+  BlkRun* r = new BlkRun();
+  BlkParams& P = r->P;
+  std::memset(&P, 0, sizeof(P));
+  const ConvArgs& a0 = layers[0];
+  P.nl = n;
+  P.C = a0.npad;
+  P.nq = P.C / 16;
+  P.H = a0.in.h;
+  P.W = a0.in.w;
+  P.wp = a0.in.wp;
+  if (P.C % 32 || P.nq > kBlkMaxChunks || P.wp != P.W + 1) { delete r; return nullptr; }
+  P.nout = P.H * P.wp;
+  P.p_out0 = 1 + P.wp;
+  P.S = (P.nout + kTileM - 1) / kTileM;
+  P.P_img = (P.H + 2) * P.wp;
+  // planes hold the image (P_img positions, + 1: the bottom-right border
+  // corner the last output's taps read); A reads of the last sub-tile run
+  // up to (128 S + 2 wp + 2 - P_img - 1) positions past the last plane, into
+  // the weight ring (checked below)
+  P.plane = (uint32_t)(P.P_img + 1) * 16;
+  P.slot_bytes = (uint32_t)P.nq * 4 * P.plane;
+  P.set_bytes = (uint32_t)nslots * P.slot_bytes;
+  const int over = kTileM * P.S + 2 * (P.wp + 1) - P.P_img - 1;
+  const uint32_t overrun = over > 0 ? (uint32_t)over * 16 : 0u;
+  P.nslots = nslots;
+  P.ext_in_slot = ext_in_slot;
+  P.ext_res_slot = ext_res_slot;
+  P.ext_in = ext_in;
+  P.ext_res = ext_res;
+  P.batch = batch;
+  P.b_bytes = 9u * 64u * (uint32_t)P.C;
+  P.set_cols = 2u * (uint32_t)P.C;
+  const uint32_t need = 2u * (uint32_t)P.S * P.set_cols;
+  if (need > 512) { delete r; return nullptr; }
+  P.tmem_cols = need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
+  for (int t = 0; t < 9; ++t) P.toff[t] = (t / 3) * P.wp + t % 3;
+  P.flag = flag;
+  P.dbg = a0.opt.dbg;
+  int pt = 0;
+  for (int l = 0; l < n; ++l) {
+    const ConvArgs& a = layers[l];
+    if (a.kh != 3 || a.kw != 3 || a.stride != 1 || a.pad != 1 || a.npad != P.C || a.in.cpad() != P.C ||
+        a.in.h != P.H || a.in.w != P.W || !a.tcwss || !a.tc16_scale || a.proj || a.epi.residual > 3 ||
+        (a.epi.pool != PCNN_POOL_NONE && !(a.epi.pool == PCNN_POOL_GLOBAL && l == n - 1))) {
+      delete r;
+      return nullptr;
+    }
+    BlkLayer& L = P.L[l];
+    L.epi = a.epi;
+    L.etab = epi_tab_layout(a.epi);
+    L.w = reinterpret_cast<const __half*>(a.tcwss);
+    L.wscale = a.tc16_scale + 1;
+    L.in_slot = in_slot[l];
+    L.res_slot = res_slot[l];
+    L.out_slot = out_slot[l];
+    // src_kind: bit 0 input is the external input; bits 2-3 residual 1 = external input, 2 = external residual
+    L.in_sload = (src_kind[l] & 1) ? ext_in.sload : 1.f;
+    const int rk = (src_kind[l] >> 2) & 3;
+    L.res_sload = rk == 1 ? ext_in.sload : rk == 2 ? ext_res.sload : 1.f;
+    L.res_ext = rk != 0;
+    L.ptab_off = pt;
+    pt += (L.etab.rows * P.C + 3) & ~3;
+  }
+  P.ptab_floats = pt;
+  const size_t aux = ((sizeof(BlkSmem) + 15) & ~size_t(15)) + (size_t)pt * 4;
+  const size_t budget = 225 * 1024 - 128;
+  P.ni = max_images >= 2 ? 2 : 1;
+  if (P.ni == 2 && 2 * (size_t)P.set_bytes + aux + 2 * (size_t)P.b_bytes > budget) P.ni = 1;
+  const size_t fixed = (size_t)P.ni * P.set_bytes + aux;
+  if (fixed + 2 * (size_t)P.b_bytes > budget || overrun > 2 * P.b_bytes) { delete r; return nullptr; }
+  P.stages = (int)((budget - fixed) / P.b_bytes);
+  if (P.stages > kBlkStages) P.stages = kBlkStages;
+  r->smem = 128 + fixed + (size_t)P.stages * P.b_bytes;
+  return r;
+}
+
+void blk_launch(const BlkRun* r, cudaStream_t s, unsigned long long* tl, int pdl) {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  BlkParams P = r->P;
+  P.tl = tl;
+  const int grid = P.batch < nsm ? P.batch : nsm;
+  cudaFuncSetAttribute(conv_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)r->smem);
+  launch_pdl(conv_blk_kernel, grid, kThreads, r->smem, s, pdl, P);
+}
+
+void blk_destroy(BlkRun* r) { delete r; }
 
 // debugging aid (not part of pcnn.h): drain the CTA-0 event trace
 extern "C" int pcnn_ss_trace(unsigned long long* host, int n) {

@@ -174,6 +174,75 @@ __device__ __forceinline__ void epi_point16(const EpiParams& e, const EpiTab& T,
   }
 }
 
+// epi_point16 for 8 channels (chb % 8 == 0): the block kernel's half items
+__device__ __forceinline__ void epi_point8(const EpiParams& e, const EpiTab& T, float* v, float vscale,
+                                           const float* sk, int chb) {
+  const float* pt = T.ptab + chb;
+  const int np = e.npad;
+  float c[8];
+  {
+    const float4 f0 = lds4(pt), f1 = lds4(pt + 4);
+    c[0] = f0.x; c[1] = f0.y; c[2] = f0.z; c[3] = f0.w; c[4] = f1.x; c[5] = f1.y; c[6] = f1.z; c[7] = f1.w;
+  }
+  fma_n<8>(v, vscale, c);
+  if (T.row_aff >= 0) {
+    float sc[8], sh[8];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const float4 a = lds4(pt + T.row_aff * np + 4 * q), d = lds4(pt + (T.row_aff + 1) * np + 4 * q);
+      sc[4 * q] = a.x; sc[4 * q + 1] = a.y; sc[4 * q + 2] = a.z; sc[4 * q + 3] = a.w;
+      sh[4 * q] = d.x; sh[4 * q + 1] = d.y; sh[4 * q + 2] = d.z; sh[4 * q + 3] = d.w;
+    }
+    fma_n<8>(v, sc, sh);
+  }
+  if (e.residual == 1) {
+    add_n<8>(v, sk);
+  } else if (e.residual >= 2) {
+    const float* rc = pt + T.row_res * np;
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+      float k[6][4];
+#pragma unroll
+      for (int r = 0; r < 6; ++r) {
+        const float4 f = lds4(rc + r * np + 4 * g);
+        k[r][0] = f.x; k[r][1] = f.y; k[r][2] = f.z; k[r][3] = f.w;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; i += 2) {
+        const int j = 4 * g + i;
+        const float2 xv = e.residual == 2 ? f2(v + j) : f2(sk + j), yv = e.residual == 2 ? f2(sk + j) : f2(v + j);
+        const float2 x2 = make_float2(k[0][i], k[0][i + 1]), y2 = make_float2(k[1][i], k[1][i + 1]);
+        const float2 xy = make_float2(k[2][i], k[2][i + 1]), cx = make_float2(k[3][i], k[3][i + 1]);
+        const float2 cy = make_float2(k[4][i], k[4][i + 1]), c0 = make_float2(k[5][i], k[5][i + 1]);
+        const float2 ax = __ffma2_rn(x2, xv, __ffma2_rn(xy, yv, cx));
+        const float2 ay = __ffma2_rn(y2, yv, cy);
+        f2_put(v + j, __ffma2_rn(ax, xv, __ffma2_rn(ay, yv, c0)));
+      }
+    }
+  }
+  if (e.poly_deg) {
+    const float* pc = pt + T.row_poly * np;
+    float h[8], ck[8];
+    {
+      const float4 f0 = lds4(pc + e.poly_deg * np), f1 = lds4(pc + e.poly_deg * np + 4);
+      h[0] = f0.x; h[1] = f0.y; h[2] = f0.z; h[3] = f0.w; h[4] = f1.x; h[5] = f1.y; h[6] = f1.z; h[7] = f1.w;
+    }
+    for (int k = e.poly_deg - 1; k >= 0; --k) {
+      const float4 f0 = lds4(pc + k * np), f1 = lds4(pc + k * np + 4);
+      ck[0] = f0.x; ck[1] = f0.y; ck[2] = f0.z; ck[3] = f0.w; ck[4] = f1.x; ck[5] = f1.y; ck[6] = f1.z; ck[7] = f1.w;
+#pragma unroll
+      for (int j = 0; j < 8; j += 2) f2_put(h + j, __ffma2_rn(f2(h + j), f2(v + j), f2(ck + j)));
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = h[j];
+  }
+  if (chb + 8 > e.cout) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (chb + j >= e.cout) v[j] = 0.f;
+  }
+}
+
 // PCNN_POOL_NONE: the 16 channels are contiguous (cb >= 16).  opos >= 0:
 // the output is a split tensor whose row starts at half index opos (+
 // channel-group terms), so no (b, y, x) addressing is needed; then ostore is

@@ -139,6 +139,17 @@ void tc_weight_image_dims(int npad, int kp, int64_t* floats);
 // fp16x2 conv with A from shared memory (conv_ss.cu): stride-1 3x3/1x1 convs
 // reading a split tensor
 bool conv_ss_supported(const ConvArgs& a);
+// Image-resident residual runs (conv_ss.cu conv_blk_kernel): n consecutive
+// stride-1 3x3 convs on one grid in one launch, activations in shared-memory
+// slots; in/res/out_slot per layer (res -1: none, out -1: global), the run's
+// external input / residual bulk-copied into ext_in_slot / ext_res_slot.
+// nullptr if the layers do not fit.
+struct BlkRun;
+BlkRun* blk_create(const ConvArgs* layers, int n, const int* in_slot, const int* res_slot, const int* out_slot,
+                   const int* src_kind, int nslots, int ext_in_slot, int ext_res_slot, const TensorView& ext_in,
+                   const TensorView& ext_res, int* flag, int batch, int max_images);
+void blk_launch(const BlkRun* r, cudaStream_t s, unsigned long long* tl, int pdl);
+void blk_destroy(BlkRun* r);
 // the shape/precision part of conv_ss_supported (input format not checked)
 bool conv_ss_shape_ok(const ConvArgs& a);
 void launch_conv_ss(const ConvArgs& a, cudaStream_t s);

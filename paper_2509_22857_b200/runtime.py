@@ -66,6 +66,15 @@ class Plan:
     def unit_impl(self, i: int) -> int:
         return L.lib().pcnn_plan_unit_impl(self.handle, i)
 
+    def materialized(self, i: int) -> bool:
+        """False for a unit inside an image-resident run (options.image_blocks)
+        whose output stays in shared memory: every unit of the run but the
+        last (read_tensor of its output tensor returns stale workspace)."""
+        lib = L.lib()
+        n = len(self.units)
+        return not (self.unit_impl(i) == 6 and i + 1 < n and lib.pcnn_plan_unit_impl(self.handle, i + 1) == 6
+                    and lib.pcnn_plan_unit_launch(self.handle, i + 1) == lib.pcnn_plan_unit_launch(self.handle, i))
+
     def tensor_split(self, t: int) -> int:
         """0 float32, 1 split fp16 hi/lo (padded grid), 2 split in parity planes."""
         return L.lib().pcnn_plan_tensor_split(self.handle, t)

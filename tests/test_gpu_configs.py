@@ -174,3 +174,29 @@ def test_compare_report(cuda, name, tmp_path):
     out = tmp_path / "r.json"
     assert compare.main(["--config", name, "--n-inputs", "300", "--json", str(out)]) == 0
     assert json.loads(out.read_text())["passed"]
+
+
+@pytest.mark.parametrize("images", [1, 2])
+@pytest.mark.parametrize("name", ["resnet20", "resnet20_deg8"])
+def test_image_resident_runs_match(cuda, name, images):
+    """options.image_blocks: runs of stride-1 3x3 convs computed in one launch
+    with whole images' activations in shared memory (conv_ss.cu
+    conv_blk_kernel) give the logits of the per-layer launches (the same
+    per-element arithmetic; only the global-pool atomics may add in another
+    order) with fewer launches; images = 2 keeps two images per CTA resident
+    and alternates between them layer by layer."""
+    import torch
+    from paper_2509_22857_b200 import _lib as L
+    cfg = configs.CONFIGS[name]
+    g = configs.build(name)
+    for d in cfg.redistribution:
+        g, _, _ = T.redistribute_sweep(g, d, allow_negative_leading=cfg.allow_negative_leading)
+    x = torch.from_numpy(configs.make_input(cfg).astype(np.float32)).cuda()
+    base = Engine(g, options=L.PlanOptions.default(image_blocks=0))
+    eng = Engine(g, options=L.PlanOptions.default(image_blocks=images))
+    want = base.forward(x).double().cpu().numpy()
+    for _ in range(2):
+        got = eng.forward(x).double().cpu().numpy()
+        assert rel_err(got, want) <= 1e-5, name
+    assert eng.plan(cfg.batch).launches() < base.plan(cfg.batch).launches()
+    assert eng.fallbacks == 0

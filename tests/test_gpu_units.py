@@ -25,13 +25,18 @@ def oracle_values(g, x):
 
 
 @pytest.mark.parametrize("name", list(configs.CONFIGS))
-@pytest.mark.parametrize("impl", [0, 4], ids=["auto", "fp32_tensors"])
-def test_every_unit_matches_oracle(cuda, name, impl):
+@pytest.mark.parametrize("impl,blocks", [(0, 2), (0, 0), (4, 2)], ids=["auto", "per_layer", "fp32_tensors"])
+def test_every_unit_matches_oracle(cuda, name, impl, blocks):
+    """auto: the default plan (image-resident runs keep their inner outputs
+    in shared memory, so only the units whose outputs leave the run are
+    read); per_layer: options.image_blocks = 0, every unit's output is in the
+    workspace."""
     import torch
+    from paper_2509_22857_b200 import _lib as L
     g = configs.build(name)
     n = N_IMAGES[name]
     x = configs.make_input(configs.CONFIGS[name], batch=n)
-    eng = Engine(g, impl=impl)
+    eng = Engine(g, impl=impl, options=L.PlanOptions.default(image_blocks=blocks))
     y = eng.forward(torch.from_numpy(x.astype(np.float32)).cuda())
     torch.cuda.synchronize()
     plan = eng.plan(n)
@@ -43,7 +48,7 @@ def test_every_unit_matches_oracle(cuda, name, impl):
     splan = simt.plan(n)
     checked = 0
     for i, (u, chain) in enumerate(zip(eng.lw.units, eng.lw.unit_nodes)):
-        if u["kind"] in (1, 12) or u.get("out", -1) < 0:  # ingest / copyout
+        if u["kind"] in (1, 12) or u.get("out", -1) < 0 or not plan.materialized(i):  # ingest / copyout
             continue
         got = plan.read_tensor(u["out"]).astype(np.float64)
         ref = want[chain[-1]].reshape(got.shape)

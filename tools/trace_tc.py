@@ -25,8 +25,10 @@ torch.cuda.synchronize()
 n = fn(buf, 65536)
 ev = [(int(v) >> 48, int(v) & 0xFFFFFFFFFFFF) for v in buf[:n] if int(v)]
 t0 = min(t for _, t in ev)
-names = {10: "bp_bar", 11: "bp_go", 12: "bp_done", 13: "ep_acc", 14: "ep_math", 12: "cv_stfull", 11: "cv_aempty", 10: "mma_k4", 1: "cv_lds", 2: "cv_go", 3: "cv_done", 4: "mma_wait", 5: "mma_go", 6: "mma_done", 7: "ep_wait", 8: "ep_go", 9: "ep_done"}
+names = {13: "ep_acc", 14: "ep_math", 12: "cv_stfull", 11: "cv_aempty", 10: "mma_k4", 1: "cv_lds", 2: "cv_go", 3: "cv_done", 4: "mma_wait", 5: "mma_go", 6: "mma_done", 7: "ep_wait", 8: "ep_go", 9: "ep_done"}
+if os.environ.get("BLK"):
+    names = {1: "p_ext", 2: "p_w", 3: "m_accw", 4: "m_acc_ok", 5: "m_in_ok", 6: "m_w_ok", 7: "m_issued", 8: "e_wait", 9: "e_go", 10: "e_chunk"}
 ev.sort(key=lambda e: e[1])
 for tag, t in (ev if os.environ.get("ALL") else ev[:240]):
-    print(f"{t - t0:8d} {names.get(tag >> 8, tag >> 8):9s} kb={tag & 0xff}")
+    print(f"{t - t0:8d} {names.get(tag >> 8, tag >> 8):9s} kb={tag & 0xff:02x}")
 print("events", n, "span", max(t for _, t in ev) - t0)
