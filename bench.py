@@ -117,7 +117,11 @@ def time_redistribution(g, cfg, reps=20):
 
 KERNEL_NAMES = {1: "conv_simt_kernel", 2: "conv_tc_kernel (3xTF32, A in TMEM)",
                 3: "conv_tc_kernel (fp16x2, A in TMEM)", 5: "conv_ss_kernel (fp16x2, halo tiles in smem)",
-                6: "conv_blk_kernel (fp16x2, image-resident runs)"}
+                6: "conv_blk_kernel (fp16x2, image-resident runs)",
+                7: "net_kernel (whole network in one launch, fp32 CUDA cores)"}
+# fp32 FMA peak of the CUDA cores (148 SMs x 128 lanes x 2 FLOP x 1.965 GHz), the
+# roofline of the whole-network kernel (derived from the SM count and max clock)
+SIMT_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 OTHER_NAMES = {1: "ingest_kernel", 3: "linear_kernel", 12: "copyout_kernel"}
 
 
@@ -151,6 +155,8 @@ def unit_cost(eng, i, batch):
 
 def unit_family(eng, plan, i):
     u = eng.lw.units[i]
+    if plan.unit_impl(i) == 7:
+        return KERNEL_NAMES[7]
     if u["kind"] == 2:
         return KERNEL_NAMES[plan.unit_impl(i)]
     return OTHER_NAMES.get(u["kind"], "eltwise / pool kernels")
@@ -209,7 +215,7 @@ class TimelineStats:
 
     def launches(self, fam):
         return sum(1 for i in range(len(self.family)) if self.family[i] == fam and self.launch_of[i] == i
-                   and self.eng.lw.units[i]["kind"] == 2)
+                   and (self.eng.lw.units[i]["kind"] == 2 or fam == KERNEL_NAMES[7]))
 
 
 def roofline(eng, plan, batch, ts: TimelineStats, ms_per_step, config):
@@ -221,7 +227,7 @@ def roofline(eng, plan, batch, ts: TimelineStats, ms_per_step, config):
     per-layer roofline max(F/P, B/BW) says binds.  Also the SURVEY 8(d) step
     figure sum_l max(F_l/P, B_l/BW) / ms_per_step."""
     hbm, bf16, _, basis = peaks()
-    rate = {3: bf16 / 3.0, 5: bf16 / 3.0, 6: bf16 / 3.0, 2: bf16 / 6.0, 1: bf16 / 6.0}
+    rate = {3: bf16 / 3.0, 5: bf16 / 3.0, 6: bf16 / 3.0, 2: bf16 / 6.0, 1: bf16 / 6.0, 7: SIMT_FP32_TFLOPS}
     lw = eng.lw
     if not ts.steps:
         return {"bound": None, "achieved": None, "peak": None, "unit": None, "frac": None, "traffic": None,
@@ -245,7 +251,7 @@ def roofline(eng, plan, batch, ts: TimelineStats, ms_per_step, config):
             t_hbm += b / (hbm * 1e9)
         per_layer.append(round(tl * 1e6, 2))
     Tk = fam_ms[dom] * 1e-3
-    P = rate[5] if "fp16x2" in dom else rate[2]
+    P = rate[5] if "fp16x2" in dom else (rate[7] if dom == KERNEL_NAMES[7] else rate[2])
     bound = "tensor" if t_tensor >= t_hbm else "hbm"
     if bound == "tensor":
         achieved, peak, unit = F / Tk / 1e12, P, "TFLOP/s"
@@ -263,7 +269,8 @@ def roofline(eng, plan, batch, ts: TimelineStats, ms_per_step, config):
             "algorithmic_per_launch": {"flops": F / max(n, 1), "bytes": B / max(n, 1)},
             "timing": "device timeline of every timed graph replay (pcnn_plan_timeline), union of the "
                       "family's launch intervals per step",
-            "peak_basis": f"{basis} bf16_tflops {bf16} (tensor: /3 for fp16x2, /6 for 3xTF32); hbm_gbs {hbm}",
+            "peak_basis": f"{basis} bf16_tflops {bf16} (tensor: /3 for fp16x2, /6 for 3xTF32); hbm_gbs {hbm}"
+                          + (f"; fp32 CUDA-core FMA peak {SIMT_FP32_TFLOPS:.1f} (derived)" if dom == KERNEL_NAMES[7] else ""),
             "ncu": ncu,
             "step": {"roofline_time_us": round(step_roof * 1e6, 1), "frac": round(step_roof * 1e3 / ms_per_step, 4),
                      "formula": "sum over conv layers of max(FLOP/P_kernel, bytes/BW) / measured ms_per_step"},

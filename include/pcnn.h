@@ -258,7 +258,12 @@ typedef struct pcnn_plan_options {
   int64_t debug;            /* diagnostic bits (tests / tools only):
                                2 skip MMAs, 4 skip epilogues, 32 CTA-0
                                trace, 64 per-CTA stamps                    */
-  int64_t reserved[8];
+  int64_t fused_net;        /* 1: a small sequential network (ingest, convs
+                               with fused epilogue and pool, dense layers,
+                               copyout; <= 2 M MACs per image) runs as ONE
+                               launch, every CTA keeping whole images in
+                               shared memory between the units            */
+  int64_t reserved[7];
 } pcnn_plan_options;
 
 /* ---- entry points --------------------------------------------------------*/

@@ -86,6 +86,10 @@ struct pcnn_plan {
   // launches with its first unit
   std::vector<BlkRun*> blks;
   std::vector<int> blk_of, blk_first;
+  // whole-network launch (build_net): every unit in one net_kernel launch
+  bool net_on = false;
+  NetParams net = {};
+  int net_grid = 0;
   // launch timeline (options.timeline): [n_units][2] (common.cuh tl_mark)
   unsigned long long* tl_dev = nullptr;
   unsigned long long* tl_host = nullptr;
@@ -387,6 +391,14 @@ void enqueue_all(pcnn_plan* p, const float* x, float* logits, cudaStream_t s) {
   if (p->sk_flags) { r.p[k] = reinterpret_cast<uint32_t*>(p->sk_flags); r.n[k++] = (int64_t)p->sk_flags_n; }
   if (p->tl_dev) { r.p[k] = reinterpret_cast<uint32_t*>(p->tl_dev); r.n[k++] = 4 * (int64_t)p->units.size(); }
   if (k) plan_reset_kernel<<<1, 256, 0, s>>>(r);
+  if (p->net_on) {
+    NetParams P = p->net;
+    P.x = x;
+    P.logits = logits;
+    P.tl = p->tl_dev;  // unit 0's slot: the launch covers every unit
+    net_launch(P, s, p->net_grid);
+    return;
+  }
   for (int i = 0; i < (int)p->units.size(); ++i) enqueue_unit(p, i, x, logits, s, true);
 }
 
@@ -614,6 +626,131 @@ void build_blocks(pcnn_plan* p) {
 // computes it too (two more MMAs per chunk, its own epilogue items and
 // output) and the projection's launch -- mostly fill / drain latency at
 // these sizes -- disappears.  PCNN_NO_PROJ_FUSE=1 keeps separate launches.
+// Small sequential networks (LeNet-5-shaped) as ONE launch (net_fused.cu):
+// ingest, then convs (no residual; any kernel / stride / pad; fused poly and
+// SUM2 / BI2 / local / global pools) and dense layers each reading the unit
+// before it, then copyout.  Only where the launch chain, not arithmetic,
+// bounds the forward: <= 2 M conv + dense MACs per image, and an image's
+// activations fit in shared memory.
+void build_net(pcnn_plan* p) {
+  if (!p->opt.fused_net) return;
+  const int n = (int)p->units.size();
+  if (n < 3 || p->units[0].kind != PCNN_UNIT_INGEST || (p->units[0].flags & PCNN_FLAG_S2D) ||
+      p->units[n - 1].kind != PCNN_UNIT_COPYOUT || n - 2 > kNetMaxOps)
+    return;
+  NetParams& NP = p->net;
+  NP = NetParams();
+  int64_t top = 0;
+  bool ok = true;
+  auto alloc = [&](int64_t floats) {
+    const int64_t off = top;
+    top += (floats + 3) & ~int64_t(3);
+    return (int)off;
+  };
+  // a parameter block staged into shared memory by the kernel's prologue
+  auto stage = [&](const float* src, int64_t floats) -> int {
+    if (!src) return -1;
+    if (NP.ncopies == kNetMaxCopies) {
+      ok = false;
+      return -1;
+    }
+    if (reinterpret_cast<uintptr_t>(src) & 15) {
+      ok = false;
+      return -1;
+    }
+    const int off = alloc(floats);
+    NP.cp[NP.ncopies++] = NetCopy{src, off, (int)floats, NP.nops - 1};
+    return off;
+  };
+  const pcnn_tensor_desc& ti = p->tensors[p->units[0].out];
+  NP.in_elems = (int)(ti.c * ti.h * ti.w);
+  NP.act_off = alloc(NP.in_elems);
+  int cur_t = (int)p->units[0].out, cur_off = NP.act_off;
+  double macs = 0;
+  for (int i = 1; i < n - 1; ++i) {
+    const pcnn_unit_desc& u = p->units[i];
+    if (u.in != cur_t) return;  // not a chain
+    NetOp& o = NP.op[NP.nops++];
+    o = NetOp();
+    const pcnn_tensor_desc& tin = p->tensors[u.in];
+    const pcnn_tensor_desc& tout = p->tensors[u.out];
+    o.in_off = cur_off;
+    o.aff = o.poly = o.pool_p = o.in_div = -1;
+    if (u.kind == PCNN_UNIT_CONV) {
+      const ConvArgs& a = p->conv_args[i];
+      if (u.residual || u.impl != 0) return;  // a requested kernel keeps its own launch
+      o.kind = kNetConv;
+      o.c = (int)tin.c; o.h = (int)tin.h; o.w = (int)tin.w;
+      o.kh = a.kh; o.kw = a.kw; o.stride = a.stride; o.pad = a.pad;
+      o.cb = a.in.cb; o.kp = a.kp;
+      o.co = (int)u.cout;
+      o.ho = a.pm.ho; o.wo = a.pm.wo;
+      o.npad = a.epi.npad; o.poly_deg = a.epi.poly_deg; o.poly_stride = a.epi.npad;
+      o.pool = (int)u.pool;
+      o.pool_deg = a.epi.pool_deg; o.pool_order = a.epi.pool_order;
+      o.pool_k = a.epi.pool_k; o.pool_s = a.epi.pool_s; o.pool_pad = a.epi.pool_pad;
+      o.ph = (int)tout.h; o.pw = (int)tout.w;
+      if (o.pool == PCNN_POOL_SUM2 || o.pool == PCNN_POOL_BI2) {
+        if (o.ph != o.ho / 2 || o.pw != o.wo / 2) return;
+      } else if (o.pool == PCNN_POOL_GLOBAL) {
+        if (!tout.is_vector) return;
+      } else if (o.pool != PCNN_POOL_NONE && o.pool != PCNN_POOL_LOCAL) {
+        return;
+      }
+      o.wt = stage(a.w, (int64_t)o.co * o.kp);
+      o.bias = stage(a.epi.bias, o.co);
+      if (a.epi.aff) o.aff = stage(a.epi.aff, 2 * (int64_t)o.npad);
+      if (o.poly_deg) o.poly = stage(a.epi.poly, (int64_t)(o.poly_deg + 1) * o.npad);
+      if (o.pool)
+        o.pool_p = stage(a.epi.pool_p, o.pool == PCNN_POOL_BI2 ? 2 * (int64_t)(o.pool_deg + 1) * (o.pool_deg + 1) * o.npad : 1);
+      const int hwo = o.ho * o.wo;
+      o.cpi = ((o.co + 3) / 4) * hwo >= kNetThreads ? 4 : ((o.co + 1) / 2) * hwo >= kNetThreads ? 2 : 1;
+      if (o.pool) o.scratch_off = alloc((int64_t)o.co * o.ho * o.wo);
+      o.out_off = alloc(o.pool == PCNN_POOL_GLOBAL ? o.co : (int64_t)o.co * o.ph * o.pw);
+      macs += (double)o.co * o.ho * o.wo * o.c * o.kh * o.kw;
+    } else if (u.kind == PCNN_UNIT_LINEAR) {
+      o.kind = kNetLinear;
+      o.in_mode = (int)u.in_mode;
+      if (o.in_mode < 0 || o.in_mode > 2) return;
+      o.c = (int)tin.c; o.h = (int)tin.h; o.w = (int)tin.w;
+      o.n_in = (int)u.cin; o.n_out = (int)u.cout;
+      if (o.in_mode == 1 && o.n_in != o.c * o.h * o.w) return;
+      if (o.in_mode != 1 && o.n_in != o.c) return;
+      if (!P(p, u.w_off) || !P(p, u.b_off)) return;
+      o.poly_deg = (int)u.poly_deg;
+      o.poly_stride = p->views[u.out].cpad();
+      o.wt = stage(P(p, u.w_off), (int64_t)o.n_in * o.n_out);
+      o.bias = stage(P(p, u.b_off), o.n_out);
+      if (o.poly_deg) o.poly = stage(P(p, u.poly_off), (int64_t)(o.poly_deg + 1) * o.poly_stride);
+      if (o.in_mode == 2) o.in_div = stage(P(p, u.in_div_off), 1);
+      if (o.in_mode == 2) o.scratch_off = alloc(o.n_in);
+      o.out_off = alloc(o.n_out);
+      macs += (double)o.n_in * o.n_out;
+    } else {
+      return;
+    }
+    cur_t = (int)u.out;
+    cur_off = o.out_off;
+  }
+  if (!ok || p->units[n - 1].in != cur_t || !p->tensors[cur_t].is_vector) return;
+  if (macs > 2e6 || (size_t)top * sizeof(float) > 220 * 1024) return;
+  NP.out_off = cur_off;
+  NP.n_out = (int)p->tensors[cur_t].c;
+  NP.out_pad = p->views[cur_t].cpad();
+  NP.out_ws = p->views[cur_t].base;
+  NP.batch = p->batch;
+  NP.smem_floats = (int)top;
+  int nsm = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  p->net_grid = std::min(p->batch, nsm);
+  p->net_on = true;
+  p->launches = 1;
+}
+
 void fuse_projections(pcnn_plan* p) {
   const int n = (int)p->units.size();
   p->fused.assign(n, 0);
@@ -817,6 +954,7 @@ void pcnn_plan_options_default(pcnn_plan_options* o) {
   o->timeline = 1;
   o->image_blocks = 2;
   o->debug = 0;
+  o->fused_net = 1;
 }
 
 int pcnn_plan_create(const pcnn_unit_desc* units, int n_units, const pcnn_tensor_desc* tensors, int n_tensors,
@@ -965,6 +1103,7 @@ int pcnn_plan_create_ex(const pcnn_unit_desc* units, int n_units, const pcnn_ten
       }
     }
   }
+  build_net(p);
   if (cudaStreamCreateWithFlags(&p->capture_stream, cudaStreamNonBlocking) != cudaSuccess) {
     pcnn_plan_destroy(p);
     return fail(PCNN_ERR_CUDA, "cudaStreamCreate failed");
@@ -1017,6 +1156,7 @@ int pcnn_plan_timeline(pcnn_plan* p, int64_t* ns, int max_units, void* stream) {
 int pcnn_plan_unit_launch(const pcnn_plan* p, int unit) {
   if (!p || unit < 0 || unit >= (int)p->units.size()) return -1;
   int u = unit;
+  if (p->net_on) return 0;  // one whole-network launch
   if (!p->blk_of.empty() && p->blk_of[u] >= 0) return p->blk_first[p->blk_of[u]];  // an image-resident run
   while (u > 0 && p->fused[u]) --u;  // a fused unit runs in its predecessor's launch
   return u;
@@ -1029,6 +1169,7 @@ int pcnn_plan_flags(const pcnn_plan* p) { return p && p->flags_on ? 1 : 0; }
 
 int pcnn_plan_unit_impl(const pcnn_plan* p, int unit) {
   if (!p || unit < 0 || unit >= (int)p->units.size()) return -1;
+  if (p->net_on) return 7;  // whole-network kernel (fp32 CUDA cores)
   if (!p->blk_of.empty() && p->blk_of[unit] >= 0) return 6;  // halo-tile arithmetic inside an image-resident run
   return p->impl[unit];
 }

@@ -162,4 +162,40 @@ bool conv_ss_proj_ok(const ConvArgs& a, const ConvArgs& proj);
 // last round mostly idle); slot_floats: the slot size it needs per CTA
 bool conv_ss_streamk_wanted(const ConvArgs& a, int nsm, size_t* slot_floats);
 
+
+// Whole-network kernel (net_fused.cu) for small sequential networks: every
+// unit of the plan in one launch, each CTA keeping whole images in shared
+// memory (dense CHW fp32) and every parameter staged into shared memory once.
+// Offsets are floats into a CTA's shared memory (-1: absent).
+constexpr int kNetThreads = 512, kNetMaxOps = 16, kNetMaxCopies = 96, kNetConv = 1, kNetLinear = 2;
+struct NetOp {
+  int kind;
+  int in_off, out_off, scratch_off;  // scratch: a pooled conv's unpooled map / a global-sum view
+  int c, h, w;                       // input (conv, in_mode 2 linear)
+  int co, ho, wo, cpi;               // conv output before its pool; output channels per work item
+  int kh, kw, stride, pad, cb, kp;   // conv weights [co][kp], k = (ci/cb) kh kw cb + (ky kw + kx) cb + ci%cb
+  int pool, pool_k, pool_s, pool_pad, pool_deg, pool_order, ph, pw;
+  int npad, poly_deg, poly_stride;
+  int n_in, n_out, in_mode;          // linear
+  int wt, bias, aff, poly, pool_p, in_div;  // parameter offsets in shared memory
+};
+struct NetCopy {
+  const float* src;  // 16-byte aligned
+  int dst, n, op;    // shared-memory float offset, floats, the op that first reads it
+};
+struct NetParams {
+  int nops, ncopies;
+  NetOp op[kNetMaxOps];
+  NetCopy cp[kNetMaxCopies];
+  const float* x;          // user NCHW input
+  int in_elems, batch;
+  int out_off, n_out, out_pad;
+  float* logits;           // user [batch][n_out]
+  float* out_ws;           // the plan's output vector tensor [batch][out_pad]
+  int act_off;             // first activation float (parameters below it)
+  int smem_floats;
+  unsigned long long* tl;
+};
+void net_launch(const NetParams& P, cudaStream_t s, int grid);
+
 }  // namespace pcnn

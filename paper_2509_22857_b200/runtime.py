@@ -72,6 +72,8 @@ class Plan:
         last (read_tensor of its output tensor returns stale workspace)."""
         lib = L.lib()
         n = len(self.units)
+        if self.unit_impl(i) == 7:  # whole-network launch: only the output vector is stored
+            return self.units[i].out == self.units[n - 1].in_
         return not (self.unit_impl(i) == 6 and i + 1 < n and lib.pcnn_plan_unit_impl(self.handle, i + 1) == 6
                     and lib.pcnn_plan_unit_launch(self.handle, i + 1) == lib.pcnn_plan_unit_launch(self.handle, i))
 

@@ -36,7 +36,8 @@ def test_every_unit_matches_oracle(cuda, name, impl, blocks):
     g = configs.build(name)
     n = N_IMAGES[name]
     x = configs.make_input(configs.CONFIGS[name], batch=n)
-    eng = Engine(g, impl=impl, options=L.PlanOptions.default(image_blocks=blocks))
+    # per_layer also runs small networks unit by unit (options.fused_net = 0)
+    eng = Engine(g, impl=impl, options=L.PlanOptions.default(image_blocks=blocks, fused_net=int(blocks > 0)))
     y = eng.forward(torch.from_numpy(x.astype(np.float32)).cuda())
     torch.cuda.synchronize()
     plan = eng.plan(n)
@@ -63,5 +64,6 @@ def test_every_unit_matches_oracle(cuda, name, impl, blocks):
         assert err <= max(1e-4, 4 * err_simt), (name, i, chain, plan.unit_impl(i), plan.tensor_split(u["out"]),
                                                  err, err_simt)
         checked += 1
-    assert checked >= 3
+    # a whole-network launch (impl 7) stores only the logits vector
+    assert checked >= (1 if plan.unit_impl(1) == 7 else 3)
     np.testing.assert_allclose(y.double().cpu().numpy(), want[g.output_id()].reshape(n, -1), rtol=1e-4, atol=1e-5)
