@@ -97,18 +97,25 @@ def time_redistribution(g, cfg, reps=20):
     accepted, _ = T.plan_sweep(eng, g, direction, allow_negative_leading=cfg.allow_negative_leading)
     prog = T.compile_sweep(eng, g, direction, accepted, cfg.allow_negative_leading)
     saved = eng.master.clone()
-    times = []
+    times, dev_us, pack_us = [], [], []
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     for i in range(reps + 3):
         eng.master.copy_(saved)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        T.run_program(eng, prog)  # includes the status read-back and the repack
+        T.run_program_on(eng.master, prog, eng.device, events=(ev[0], ev[1]))  # status read-back included
+        eng.repack()
+        ev[2].record()
         torch.cuda.synchronize()
         if i >= 3:
             times.append(time.perf_counter() - t0)
-    return {"us_per_call": 1e6 * float(np.median(times)), "direction": direction, "donors": len(accepted),
-            "ops": len(prog.ops), "rewrites": len(prog.rewrite_descs()),
-            "note": "wall time of pcnn_redistribute (one cooperative launch) + status read + repack"}
+            dev_us.append(ev[0].elapsed_time(ev[1]) * 1e3)
+            pack_us.append(ev[1].elapsed_time(ev[2]) * 1e3)
+    return {"us_per_call": 1e6 * float(np.median(times)), "device_us": round(float(np.median(dev_us)), 1),
+            "repack_device_us": round(float(np.median(pack_us)), 1), "direction": direction,
+            "donors": len(accepted), "ops": len(prog.ops), "rewrites": len(prog.rewrite_descs()),
+            "note": "us_per_call: wall time of pcnn_redistribute (one cooperative launch) + status read + repack; "
+                    "device_us: CUDA events around the launch; repack_device_us: status read to repack end"}
 
 
 # ---------------------------------------------------------------------------

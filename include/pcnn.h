@@ -344,6 +344,25 @@ int pcnn_redistribute(double* master, double* arena, int64_t arena_len,
                       const pcnn_rewrite_desc* rewrites, int n_rewrites,
                       int64_t* status_dev, int64_t* flags_dev, void* stream);
 
+/* Device-resident forms of pcnn_redistribute / pcnn_pack for repeated runs
+ * (an engine repacking after every transform, a redistribution program run
+ * again on new weights): the descriptor tables are uploaded once at create;
+ * run is stream-ordered launches only -- no allocation, no host copy, no
+ * synchronisation.  A program owns its arena.  Same semantics per run as
+ * the one-shot calls above (reference transforms.py:287-705). */
+typedef struct pcnn_program pcnn_program;
+int pcnn_program_create(const pcnn_scale_op* ops, int n_ops,
+                        const pcnn_rewrite_desc* rewrites, int n_rewrites,
+                        int64_t arena_len, pcnn_program** program_out);
+int pcnn_program_run(pcnn_program* program, double* master, int64_t* status_dev,
+                     int64_t* flags_dev, void* stream);
+int pcnn_program_destroy(pcnn_program* program);
+
+typedef struct pcnn_packer pcnn_packer;
+int pcnn_packer_create(const pcnn_pack_desc* ops, int n_ops, pcnn_packer** packer_out);
+int pcnn_packer_run(pcnn_packer* packer, const double* master, float* packed, void* stream);
+int pcnn_packer_destroy(pcnn_packer* packer);
+
 #ifdef __cplusplus
 }
 #endif

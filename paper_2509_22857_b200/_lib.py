@@ -169,7 +169,55 @@ SYMBOLS = {
     "pcnn_redistribute": ([ctypes.c_void_p, ctypes.c_void_p, c_i64, ctypes.POINTER(ScaleOp), ctypes.c_int,
                            ctypes.POINTER(RewriteDesc), ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                            ctypes.c_void_p], ctypes.c_int),
+    "pcnn_program_create": ([ctypes.POINTER(ScaleOp), ctypes.c_int, ctypes.POINTER(RewriteDesc), ctypes.c_int, c_i64,
+                             ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "pcnn_program_run": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p],
+                         ctypes.c_int),
+    "pcnn_program_destroy": ([ctypes.c_void_p], ctypes.c_int),
+    "pcnn_packer_create": ([ctypes.POINTER(PackDesc), ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "pcnn_packer_run": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "pcnn_packer_destroy": ([ctypes.c_void_p], ctypes.c_int),
 }
+
+
+class DeviceProgram:
+    """A redistribution program resident on the device (pcnn_program_*): its
+    op and rewrite tables uploaded once, every run launches only."""
+
+    def __init__(self, ops, n_ops: int, rws, n_rws: int, arena_len: int):
+        h = ctypes.c_void_p()
+        check(lib().pcnn_program_create(ops, n_ops, rws, n_rws, arena_len, ctypes.byref(h)), "pcnn_program_create")
+        self.handle = h
+
+    def run(self, master_ptr: int, status_ptr: int, flags_ptr: int, stream) -> None:
+        check(lib().pcnn_program_run(self.handle, ctypes.c_void_p(master_ptr), ctypes.c_void_p(status_ptr),
+                                     ctypes.c_void_p(flags_ptr), stream), "pcnn_program_run")
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and _lib is not None:
+            _lib.pcnn_program_destroy(h)
+            self.handle = None
+
+
+class DevicePacker:
+    """The float64 master -> compute images step with its pack tables on the
+    device (pcnn_packer_*)."""
+
+    def __init__(self, packs, n: int):
+        h = ctypes.c_void_p()
+        check(lib().pcnn_packer_create(packs, n, ctypes.byref(h)), "pcnn_packer_create")
+        self.handle = h
+
+    def run(self, master_ptr: int, packed_ptr: int, stream) -> None:
+        check(lib().pcnn_packer_run(self.handle, ctypes.c_void_p(master_ptr), ctypes.c_void_p(packed_ptr), stream),
+              "pcnn_packer_run")
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and _lib is not None:
+            _lib.pcnn_packer_destroy(h)
+            self.handle = None
 
 
 def lib() -> ctypes.CDLL:

@@ -12,9 +12,9 @@
 #include "tc_layout.cuh"
 
 namespace pcnn {
-__global__ void redistribute_kernel(double*, double*, const pcnn_scale_op*, int, const pcnn_rewrite_desc*,
-                                    int, int64_t*, int64_t*);
-__global__ void pack_kernel(const double*, float*, const pcnn_pack_desc*, int);
+__global__ void redistribute_kernel(double*, double*, int64_t, int, const pcnn_scale_op*, int,
+                                    const pcnn_rewrite_desc*, int, const int2*, int, int64_t*, int64_t*);
+__global__ void pack_kernel(const double*, float*, const pcnn_pack_desc*, int, const int*);
 __global__ void pack_amax_kernel(const double*, float*, const pcnn_pack_desc*, int, int);
 }  // namespace pcnn
 
@@ -1331,24 +1331,165 @@ int pcnn_forward_unit(pcnn_plan* p, int unit, const float* x, float* logits, voi
   return PCNN_OK;
 }
 
+struct pcnn_packer {
+  pcnn_pack_desc* d_ops = nullptr;
+  int* d_first = nullptr;
+  int n_ops = 0, blocks = 0;
+  bool tc16 = false;
+};
+
+struct pcnn_program {
+  char* d_tables = nullptr;  // ops then rewrites
+  pcnn_scale_op* d_ops = nullptr;
+  pcnn_rewrite_desc* d_rw = nullptr;
+  int2* d_chunks = nullptr;  // phase-(b) work chunks {rewrite, first element}
+  double* arena = nullptr;
+  int64_t arena_len = 0;
+  int n_ops = 0, n_rw = 0, n_chunks = 0;
+  int smem_arena = 0, blocks = 0;
+  size_t smem = 0;
+};
+
+int pcnn_packer_create(const pcnn_pack_desc* ops, int n_ops, pcnn_packer** out) {
+  if (!out || (!ops && n_ops) || n_ops < 0) return fail(PCNN_ERR_INVALID, "pcnn_packer_create: bad argument");
+  pcnn_packer* k = new pcnn_packer();
+  k->n_ops = n_ops;
+  std::vector<int> first(n_ops + 1, 0);
+  for (int i = 0; i < n_ops; ++i) {
+    k->tc16 |= ops[i].kind == PCNN_PACK_TC16_WEIGHTS;
+    // work items of the op (the padded weight images cover rows x padded k)
+    const int64_t work = std::max<int64_t>(std::max<int64_t>(ops[i].n, ops[i].rows * ops[i].k), 1);
+    const int64_t nb = std::min<int64_t>((work + 256 * 8 - 1) / (256 * 8), 512);
+    first[i + 1] = first[i] + (int)nb;
+  }
+  k->blocks = first[n_ops];
+  if (n_ops) {
+    if (cudaMalloc(&k->d_ops, sizeof(pcnn_pack_desc) * n_ops) != cudaSuccess ||
+        cudaMalloc(&k->d_first, sizeof(int) * (n_ops + 1)) != cudaSuccess) {
+      pcnn_packer_destroy(k);
+      return fail(PCNN_ERR_CUDA, "pcnn_packer_create: allocation failed");
+    }
+    cudaMemcpy(k->d_ops, ops, sizeof(pcnn_pack_desc) * n_ops, cudaMemcpyHostToDevice);
+    cudaMemcpy(k->d_first, first.data(), sizeof(int) * (n_ops + 1), cudaMemcpyHostToDevice);
+  }
+  *out = k;
+  return PCNN_OK;
+}
+
+int pcnn_packer_run(pcnn_packer* k, const double* master, float* packed, void* stream) {
+  if (!k || !master || !packed) return fail(PCNN_ERR_INVALID, "pcnn_packer_run: null argument");
+  if (!k->n_ops) return PCNN_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (k->tc16) {
+    // max|w| of every fp16x2 image first (its power-of-two scale)
+    pack_amax_kernel<<<k->n_ops, 1024, 0, s>>>(master, packed, k->d_ops, k->n_ops, 0);
+    pack_amax_kernel<<<dim3(k->n_ops, 64), 256, 0, s>>>(master, packed, k->d_ops, k->n_ops, 1);
+  }
+  pack_kernel<<<k->blocks, 256, 0, s>>>(master, packed, k->d_ops, k->n_ops, k->d_first);
+  cudaError_t le = cudaGetLastError();
+  if (le != cudaSuccess) return fail(PCNN_ERR_CUDA, std::string("pack_kernel: ") + cudaGetErrorString(le));
+  return PCNN_OK;
+}
+
+int pcnn_packer_destroy(pcnn_packer* k) {
+  if (!k) return PCNN_OK;
+  if (k->d_ops) cudaFree(k->d_ops);
+  if (k->d_first) cudaFree(k->d_first);
+  delete k;
+  return PCNN_OK;
+}
+
 int pcnn_pack(const double* master, float* packed, const pcnn_pack_desc* ops, int n_ops, void* stream) {
   if (!master || !packed || (!ops && n_ops)) return fail(PCNN_ERR_INVALID, "pcnn_pack: null argument");
   if (n_ops == 0) return PCNN_OK;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  pcnn_pack_desc* d_ops = nullptr;
-  PCNN_CUDA(cudaMallocAsync(&d_ops, sizeof(pcnn_pack_desc) * n_ops, s));
-  PCNN_CUDA(cudaMemcpyAsync(d_ops, ops, sizeof(pcnn_pack_desc) * n_ops, cudaMemcpyHostToDevice, s));
-  bool tc16 = false;
-  for (int i = 0; i < n_ops; ++i) tc16 |= ops[i].kind == PCNN_PACK_TC16_WEIGHTS;
-  if (tc16) {
-    // max|w| of every fp16x2 image first (its power-of-two scale)
-    pack_amax_kernel<<<n_ops, 1024, 0, s>>>(master, packed, d_ops, n_ops, 0);
-    pack_amax_kernel<<<dim3(n_ops, 64), 256, 0, s>>>(master, packed, d_ops, n_ops, 1);
+  pcnn_packer* k = nullptr;
+  int rc = pcnn_packer_create(ops, n_ops, &k);
+  if (rc != PCNN_OK) return rc;
+  rc = pcnn_packer_run(k, master, packed, stream);
+  cudaStreamSynchronize(static_cast<cudaStream_t>(stream));  // the tables are freed below
+  pcnn_packer_destroy(k);
+  return rc;
+}
+
+int pcnn_program_create(const pcnn_scale_op* ops, int n_ops, const pcnn_rewrite_desc* rewrites, int n_rewrites,
+                        int64_t arena_len, pcnn_program** out) {
+  if (!out || (!ops && n_ops) || (!rewrites && n_rewrites) || n_ops < 0 || n_rewrites < 0 || arena_len < 0)
+    return fail(PCNN_ERR_INVALID, "pcnn_program_create: bad argument");
+  for (int i = 0; i < n_ops; ++i) {
+    const pcnn_scale_op& o = ops[i];
+    if (o.op < PCNN_OP_FILL || o.op > PCNN_OP_ADD || o.n < 0 || o.dst < 0)
+      return fail(PCNN_ERR_INVALID, "bad scale op " + std::to_string(i));
   }
-  pack_kernel<<<148 * 4, 256, 0, s>>>(master, packed, d_ops, n_ops);
-  cudaError_t le = cudaGetLastError();
-  PCNN_CUDA(cudaFreeAsync(d_ops, s));
-  if (le != cudaSuccess) return fail(PCNN_ERR_CUDA, std::string("pack_kernel: ") + cudaGetErrorString(le));
+  pcnn_program* g = new pcnn_program();
+  g->n_ops = n_ops;
+  g->n_rw = n_rewrites;
+  g->arena_len = arena_len;
+  std::vector<int2> chunks;
+  for (int i = 0; i < n_rewrites; ++i) {
+    const pcnn_rewrite_desc& r = rewrites[i];
+    bool ok = r.n >= 0 && r.n < (int64_t(1) << 31) && r.n_factors >= 0 && r.n_factors <= PCNN_MAX_FACTORS;
+    for (int f = 0; ok && f < (int)r.n_factors; ++f) {
+      const pcnn_factor& F = r.f[f];
+      ok = F.d1 > 0 && F.m1 > 0 && F.d2 > 0 && F.m2 > 0 && F.d1 < (int64_t(1) << 31) && F.m1 < (int64_t(1) << 31) &&
+           F.d2 < (int64_t(1) << 31) && F.m2 < (int64_t(1) << 31) && F.s1 >= 0 &&
+           (F.m1 - 1) * F.s1 + F.m2 < (int64_t(1) << 32);
+    }
+    if (!ok) {
+      delete g;
+      return fail(PCNN_ERR_INVALID, "bad rewrite descriptor " + std::to_string(i));
+    }
+    for (int64_t e = 0; e < r.n; e += 4096) chunks.push_back(make_int2(i, (int)e));
+  }
+  g->n_chunks = (int)chunks.size();
+  const size_t ob = sizeof(pcnn_scale_op) * (size_t)std::max(n_ops, 1);
+  const size_t rb = sizeof(pcnn_rewrite_desc) * (size_t)std::max(n_rewrites, 1);
+  const size_t cb = sizeof(int2) * std::max<size_t>(chunks.size(), 1);
+  if (cudaMalloc(&g->d_tables, ob + rb + cb) != cudaSuccess ||
+      cudaMalloc(&g->arena, sizeof(double) * (size_t)std::max<int64_t>(arena_len, 1)) != cudaSuccess) {
+    pcnn_program_destroy(g);
+    return fail(PCNN_ERR_CUDA, "pcnn_program_create: allocation failed");
+  }
+  g->d_ops = reinterpret_cast<pcnn_scale_op*>(g->d_tables);
+  g->d_rw = reinterpret_cast<pcnn_rewrite_desc*>(g->d_tables + ob);
+  g->d_chunks = reinterpret_cast<int2*>(g->d_tables + ob + rb);
+  if (!chunks.empty()) cudaMemcpy(g->d_chunks, chunks.data(), sizeof(int2) * chunks.size(), cudaMemcpyHostToDevice);
+  if (n_ops) cudaMemcpy(g->d_ops, ops, sizeof(pcnn_scale_op) * n_ops, cudaMemcpyHostToDevice);
+  if (n_rewrites) cudaMemcpy(g->d_rw, rewrites, sizeof(pcnn_rewrite_desc) * n_rewrites, cudaMemcpyHostToDevice);
+  // the arena and the op table in block 0's shared memory when they fit
+  const size_t need = sizeof(double) * (size_t)((arena_len + 1) & ~int64_t(1)) + sizeof(pcnn_scale_op) * (size_t)n_ops;
+  g->smem_arena = arena_len > 0 && need <= 200 * 1024 ? 1 : 0;
+  g->smem = g->smem_arena ? need : 0;
+  if (g->smem > 48 * 1024)
+    cudaFuncSetAttribute(redistribute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g->smem);
+  int dev = 0, nsm = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, redistribute_kernel, 256, g->smem);
+  g->blocks = std::max(1, nsm * std::max(1, std::min(per_sm, 4)));
+  *out = g;
+  return PCNN_OK;
+}
+
+int pcnn_program_run(pcnn_program* g, double* master, int64_t* status_dev, int64_t* flags_dev, void* stream) {
+  if (!g || !master || !status_dev) return fail(PCNN_ERR_INVALID, "pcnn_program_run: null argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  PCNN_CUDA(cudaMemsetAsync(status_dev, 0, 4 * sizeof(int64_t), s));
+  int64_t* flags = flags_dev ? flags_dev : status_dev + 2;
+  double* arena = g->arena;
+  int64_t arena_len = g->arena_len;
+  int smem_arena = g->smem_arena;
+  void* args[] = {&master, &arena, &arena_len, &smem_arena, &g->d_ops, &g->n_ops, &g->d_rw, &g->n_rw,
+                  &g->d_chunks, &g->n_chunks, &status_dev, &flags};
+  cudaError_t le = cudaLaunchCooperativeKernel((void*)redistribute_kernel, dim3(g->blocks), dim3(256), args, g->smem, s);
+  if (le != cudaSuccess) return fail(PCNN_ERR_CUDA, std::string("redistribute_kernel: ") + cudaGetErrorString(le));
+  return PCNN_OK;
+}
+
+int pcnn_program_destroy(pcnn_program* g) {
+  if (!g) return PCNN_OK;
+  if (g->d_tables) cudaFree(g->d_tables);
+  if (g->arena) cudaFree(g->arena);
+  delete g;
   return PCNN_OK;
 }
 
@@ -1357,34 +1498,17 @@ int pcnn_redistribute(double* master, double* arena, int64_t arena_len, const pc
                       void* stream) {
   if (!master || !arena || !status_dev || (!ops && n_ops) || (!rewrites && n_rewrites))
     return fail(PCNN_ERR_INVALID, "pcnn_redistribute: null argument");
-  for (int i = 0; i < n_ops; ++i) {
-    const pcnn_scale_op& o = ops[i];
-    if (o.op < PCNN_OP_FILL || o.op > PCNN_OP_ADD || o.n < 0 || o.dst < 0)
-      return fail(PCNN_ERR_INVALID, "bad scale op " + std::to_string(i));
-  }
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  size_t ob = sizeof(pcnn_scale_op) * (size_t)std::max(n_ops, 1);
-  size_t rb = sizeof(pcnn_rewrite_desc) * (size_t)std::max(n_rewrites, 1);
-  char* d = nullptr;
-  PCNN_CUDA(cudaMallocAsync((void**)&d, ob + rb, s));
-  pcnn_scale_op* d_ops = reinterpret_cast<pcnn_scale_op*>(d);
-  pcnn_rewrite_desc* d_rw = reinterpret_cast<pcnn_rewrite_desc*>(d + ob);
-  if (n_ops) PCNN_CUDA(cudaMemcpyAsync(d_ops, ops, sizeof(pcnn_scale_op) * n_ops, cudaMemcpyHostToDevice, s));
-  if (n_rewrites)
-    PCNN_CUDA(cudaMemcpyAsync(d_rw, rewrites, sizeof(pcnn_rewrite_desc) * n_rewrites, cudaMemcpyHostToDevice, s));
-  PCNN_CUDA(cudaMemsetAsync(status_dev, 0, 4 * sizeof(int64_t), s));
-  int dev = 0, nsm = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, redistribute_kernel, 256, 0);
-  int blocks = std::max(1, nsm * std::min(per_sm, 4));
-  int64_t* flags = flags_dev ? flags_dev : status_dev + 2;
-  void* args[] = {&master, &arena, &d_ops, &n_ops, &d_rw, &n_rewrites, &status_dev, &flags};
-  cudaError_t le = cudaLaunchCooperativeKernel((void*)redistribute_kernel, dim3(blocks), dim3(256), args, 0, s);
-  cudaFreeAsync(d, s);
-  if (le != cudaSuccess) return fail(PCNN_ERR_CUDA, std::string("redistribute_kernel: ") + cudaGetErrorString(le));
-  (void)arena_len;
-  return PCNN_OK;
+  pcnn_program* g = nullptr;
+  int rc = pcnn_program_create(ops, n_ops, rewrites, n_rewrites, arena_len, &g);
+  if (rc != PCNN_OK) return rc;
+  // the caller's arena, not the program's own
+  cudaFree(g->arena);
+  g->arena = arena;
+  rc = pcnn_program_run(g, master, status_dev, flags_dev, stream);
+  cudaStreamSynchronize(static_cast<cudaStream_t>(stream));  // the tables are freed below
+  g->arena = nullptr;
+  pcnn_program_destroy(g);
+  return rc;
 }
 
 }  // extern "C"

@@ -21,6 +21,8 @@ namespace cg = cooperative_groups;
 
 namespace pcnn {
 
+constexpr int kRwChunk = 4096;  // rewrite elements per phase-(b) work chunk
+
 __device__ __forceinline__ double ipow(double x, long long p) {
   // exact repeated squaring for small positive p matches x*x*... closely;
   // use pow() like numpy for the general case
@@ -99,32 +101,59 @@ __device__ void run_program(const double* __restrict__ master_ro, double* master
   }
 }
 
-__global__ void redistribute_kernel(double* master, double* arena, const pcnn_scale_op* ops, int n_ops,
-                                    const pcnn_rewrite_desc* rw, int n_rw, int64_t* status,
-                                    int64_t* flags) {
+// smem_arena: phase (a) keeps the arena and the op table in block 0's shared
+// memory (every op is then a few shared-memory accesses and two block
+// barriers instead of dependent L2 round trips) and publishes the arena to
+// global memory for phase (b)
+__global__ void redistribute_kernel(double* master, double* arena, int64_t arena_len, int smem_arena,
+                                    const pcnn_scale_op* ops, int n_ops, const pcnn_rewrite_desc* rw, int n_rw,
+                                    const int2* chunks, int n_chunks, int64_t* status, int64_t* flags) {
+  extern __shared__ double sarena[];
   cg::grid_group grid = cg::this_grid();
-  if (blockIdx.x == 0) run_program(master, master, arena, ops, n_ops, status, flags);
+  if (blockIdx.x == 0) {
+    const pcnn_scale_op* pops = ops;
+    if (smem_arena) {
+      // the op table after the arena (16-byte aligned)
+      pcnn_scale_op* sops = reinterpret_cast<pcnn_scale_op*>(sarena + ((arena_len + 1) & ~int64_t(1)));
+      const int64_t words = (int64_t)n_ops * (int64_t)(sizeof(pcnn_scale_op) / 8);
+      const int64_t* src = reinterpret_cast<const int64_t*>(ops);
+      int64_t* dst = reinterpret_cast<int64_t*>(sops);
+      for (int64_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+      __syncthreads();
+      pops = sops;
+    }
+    run_program(master, master, smem_arena ? sarena : arena, pops, n_ops, status, flags);
+    if (smem_arena) {
+      __syncthreads();
+      for (int64_t i = threadIdx.x; i < arena_len; i += blockDim.x) arena[i] = sarena[i];
+    }
+  }
   grid.sync();
   if (status[0] != 0) return;
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
-  for (int d = 0; d < n_rw; ++d) {
-    const pcnn_rewrite_desc& r = rw[d];
+  // phase (b): the rewrites cut into chunks of kRwChunk elements, chunks
+  // spread over the blocks (every rewrite in parallel; a block pays one
+  // descriptor load per chunk, not one per rewrite); factor indices in
+  // 32-bit arithmetic (every extent < 2^31, checked at create)
+  for (int c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+    const int2 ch = chunks[c];
+    const pcnn_rewrite_desc& r = rw[ch.x];
+    const int n = (int)r.n, e1 = min(ch.y + kRwChunk, n), nf = (int)r.n_factors;
     const double* src = r.src_arena ? arena + r.src : master + r.src;
-    for (int64_t e = tid; e < r.n; e += nthreads) {
-      double v;
-      if (r.set_const) {
-        v = r.value;
-      } else {
-        v = src[e];
-        for (int f = 0; f < r.n_factors; ++f) {
-          const pcnn_factor& F = r.f[f];
-          int64_t idx = ((e / F.d1) % F.m1) * F.s1 + (e / F.d2) % F.m2;
-          double fv = arena[F.slot + idx];
-          v = F.divide ? v / fv : v * fv;
-        }
+    double* dst = master + r.dst;
+    if (r.set_const) {
+      for (int e = ch.y + threadIdx.x; e < e1; e += blockDim.x) dst[e] = r.value;
+      continue;
+    }
+    for (int e = ch.y + threadIdx.x; e < e1; e += blockDim.x) {
+      double v = src[e];
+      for (int f = 0; f < nf; ++f) {
+        const pcnn_factor& F = r.f[f];
+        const unsigned idx = (((unsigned)e / (unsigned)F.d1) % (unsigned)F.m1) * (unsigned)F.s1 +
+                             ((unsigned)e / (unsigned)F.d2) % (unsigned)F.m2;
+        const double fv = arena[F.slot + idx];
+        v = F.divide ? v / fv : v * fv;
       }
-      master[r.dst + e] = v;
+      dst[e] = v;
     }
   }
 }
@@ -154,11 +183,27 @@ __global__ void pack_amax_kernel(const double* __restrict__ master, float* __res
   }
 }
 
+// first_block (n_ops + 1 entries, or null): op k is packed by blocks
+// [first_block[k], first_block[k + 1]) -- every op in parallel, each by a
+// block count proportional to its size; null: all blocks walk every op.
 __global__ void pack_kernel(const double* __restrict__ master, float* __restrict__ packed,
-                            const pcnn_pack_desc* ops, int n_ops) {
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
-  for (int k = 0; k < n_ops; ++k) {
+                            const pcnn_pack_desc* ops, int n_ops, const int* __restrict__ first_block) {
+  int k0 = 0, k1 = n_ops;
+  int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  if (first_block) {
+    int lo = 0, hi = n_ops - 1;  // last op whose first block <= blockIdx.x
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (first_block[mid] <= (int)blockIdx.x) lo = mid;
+      else hi = mid - 1;
+    }
+    k0 = lo;
+    k1 = lo + 1;
+    tid = (blockIdx.x - first_block[lo]) * (int64_t)blockDim.x + threadIdx.x;
+    nthreads = (int64_t)(first_block[lo + 1] - first_block[lo]) * blockDim.x;
+  }
+  for (int k = k0; k < k1; ++k) {
     const pcnn_pack_desc o = ops[k];
     if (o.kind == PCNN_PACK_CAST) {
       for (int64_t i = tid; i < o.n; i += nthreads) packed[o.dst + i] = (float)master[o.src + i];

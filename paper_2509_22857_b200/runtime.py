@@ -164,6 +164,7 @@ class Engine:
         self.master = torch.from_numpy(np.ascontiguousarray(m)).to(self.device)
         self.packed = torch.zeros(self.lw.packed_size, dtype=torch.float32, device=self.device)
         self._packs = self.lw.pack_descs()
+        self._packer = L.DevicePacker(self._packs, len(self.lw.pack_ops))
         self.repack()
         self.plans: Dict[int, Plan] = {}
         self.fallback_plans: Dict[int, Plan] = {}
@@ -183,9 +184,7 @@ class Engine:
 
     # -- parameters -----------------------------------------------------------
     def repack(self, stream=None) -> None:
-        L.check(L.lib().pcnn_pack(ctypes.c_void_p(self.master.data_ptr()),
-                                  ctypes.c_void_p(self.packed.data_ptr()),
-                                  self._packs, len(self.lw.pack_ops), _stream_handle(stream)), "pcnn_pack")
+        self._packer.run(self.master.data_ptr(), self.packed.data_ptr(), _stream_handle(stream))
 
     def master_numpy(self) -> np.ndarray:
         return self.master.cpu().numpy()

@@ -309,19 +309,34 @@ def run_program(engine, prog: Program, stream=None) -> np.ndarray:
     return flags
 
 
-def run_program_on(master, prog: Program, dev, stream=None) -> np.ndarray:
-    """pcnn_redistribute over any float64 device buffer (no repack)."""
+def _program_buffers(prog: Program, dev):
+    """The program's ctypes op / rewrite tables and its device scratch (arena,
+    status, flags), built once per program and reused by every call."""
     import torch
+    key = (len(prog.ops), prog.arena, prog.nflags, str(dev))
+    cached = getattr(prog, "_buffers", None)
+    if cached is None or cached[0] != key:
+        rws = prog.rewrite_descs()
+        dprog = L.DeviceProgram(L.array(L.ScaleOp, prog.ops), len(prog.ops), L.array(L.RewriteDesc, rws), len(rws),
+                                prog.arena)
+        cached = (key, dprog, torch.zeros(4, dtype=torch.int64, device=dev),
+                  torch.zeros(max(prog.nflags, 1), dtype=torch.int64, device=dev))
+        prog._buffers = cached
+    return cached[1:]
+
+
+def run_program_on(master, prog: Program, dev, stream=None, events=None) -> np.ndarray:
+    """Run the program (pcnn_program_run: one cooperative launch, tables and
+    arena resident on the device since its first run) over any float64
+    device buffer (no repack).  events: an optional (start, end) CUDA event
+    pair recorded around the launch."""
     from .runtime import _stream_handle
-    arena = torch.empty(max(prog.arena, 1), dtype=torch.float64, device=dev)
-    status = torch.zeros(4, dtype=torch.int64, device=dev)
-    flags = torch.zeros(max(prog.nflags, 1), dtype=torch.int64, device=dev)
-    ops = L.array(L.ScaleOp, prog.ops)
-    rws = prog.rewrite_descs()
-    L.check(L.lib().pcnn_redistribute(ctypes.c_void_p(master.data_ptr()), ctypes.c_void_p(arena.data_ptr()),
-                                      prog.arena, ops, len(prog.ops), L.array(L.RewriteDesc, rws), len(rws),
-                                      ctypes.c_void_p(status.data_ptr()), ctypes.c_void_p(flags.data_ptr()),
-                                      _stream_handle(stream)), "pcnn_redistribute")
+    dprog, status, flags = _program_buffers(prog, dev)
+    if events is not None:
+        events[0].record()
+    dprog.run(master.data_ptr(), status.data_ptr(), flags.data_ptr(), _stream_handle(stream))
+    if events is not None:
+        events[1].record()
     st = status.cpu().numpy()
     if st[0] != 0:
         code = int(st[0])
