@@ -263,7 +263,10 @@ typedef struct pcnn_plan_options {
                                copyout; <= 2 M MACs per image) runs as ONE
                                launch, every CTA keeping whole images in
                                shared memory between the units            */
-  int64_t reserved[7];
+  int64_t ss_wide;          /* 1: the halo-tile producer warp issues a
+                               stage's bulk copies from several lanes at
+                               once (one lane pays ~300 cycles per copy)   */
+  int64_t reserved[6];
 } pcnn_plan_options;
 
 /* ---- entry points --------------------------------------------------------*/

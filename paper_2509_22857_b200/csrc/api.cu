@@ -507,7 +507,7 @@ void build_blocks(pcnn_plan* p) {
     if (u.kind != PCNN_UNIT_CONV || p->impl[i] != 5 || p->fused[i]) return false;
     const ConvArgs& a = p->conv_args[i];
     return a.kh == 3 && a.kw == 3 && a.stride == 1 && a.pad == 1 && !a.proj && a.in.split == 1 && !a.sk_flags &&
-           (a.npad == 32 || a.npad == 64) && a.in.cpad() == a.npad && u.cout == a.npad;
+           (a.npad == 16 || a.npad == 32 || a.npad == 64) && a.in.cpad() == a.npad && u.cout == a.npad;
   };
   int i = 0;
   while (i < n) {
@@ -955,6 +955,7 @@ void pcnn_plan_options_default(pcnn_plan_options* o) {
   o->image_blocks = 2;
   o->debug = 0;
   o->fused_net = 1;
+  o->ss_wide = 1;
 }
 
 int pcnn_plan_create(const pcnn_unit_desc* units, int n_units, const pcnn_tensor_desc* tensors, int n_tensors,
@@ -984,6 +985,7 @@ int pcnn_plan_create_ex(const pcnn_unit_desc* units, int n_units, const pcnn_ten
   p->kopt.ss_share = (int)p->opt.ss_share;
   p->kopt.ss_psub = (int)p->opt.ss_psub;
   p->kopt.ss_wres = (int)p->opt.ss_wres;
+  p->kopt.ss_wide = (int)p->opt.ss_wide;
   p->kopt.tc_stage = (int)p->opt.tc_stage;
   p->kopt.proj_fuse = (int)p->opt.fuse_projection;
   p->kopt.streamk = (int)p->opt.streamk;

@@ -81,6 +81,7 @@ struct SsParams {
   int out_pos, skip_pos; // output / residual row of grid position g starts at half index 8 g (split,
                          // same shared-border geometry as the input grid)
   int fold_skip, fold_out;  // storage scales folded into the epilogue table (epi_fill_tab)
+  int wide;  // producer: the warp's lanes issue a stage's bulk copies in parallel
   int dbg;
   int time_slot;         // PCNN_TC_DEBUG bit 64: per-CTA globaltimer stamps slot, else -1
   // wres: the whole weight image (one n-tile, every chunk) stays resident in
@@ -635,7 +636,61 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
   if (warp == kWarpProducer) {
     // ===== producer: per (tile, 16-channel chunk) one stage = the tile's
     // input range for both planes and both 8-channel groups + the weights =====
-    if (lane == 0) {
+    if (!BAND && P.wide) {
+      // the whole warp walks the stages; lane 0 waits for the slot and posts
+      // the byte count, then lane j issues copy j of the stage (a single
+      // thread pays ~300 cycles per cp.async.bulk, tools/ubench_bulk.cu)
+      const __half* hi = a.in.hi();
+      const __half* lo = a.in.lo();
+      int st = 0;
+      uint32_t ph = 0;
+      Seg sg;
+      Band bd = {};
+      for (int si = 0; seg_get<false>(P, bd, si, total_tiles, streamk, sg); ++si) {
+        const int n_tile = sg.n_tile;
+        const int64_t gs = sg.g0 - P.halo;
+        const int64_t cs = gs < 0 ? 0 : gs;
+        const int64_t ge = gs + P.span;
+        const int64_t ce = ge > P.gtotal ? P.gtotal : ge;
+        const uint32_t slot0 = (uint32_t)(cs - gs) * 16, bytes = (uint32_t)(ce - cs) * 16;
+        for (int q = sg.q0; q < sg.q1; ++q) {
+          const uint32_t bar = ptx::smem_u32(&S->full[st]);
+          const uint32_t sb = base + st * P.stage_bytes;
+          const int ng = q == P.nq - 1 ? P.last_groups : 2;
+          if (lane == 0) {
+            ptx::mbar_wait_sleep(ptx::smem_u32(&S->empty[st]), ph ^ 1);
+            ptx::mbar_arrive_tx(bar, 2 * ng * P.nplanes * bytes + (P.wres ? 0u : P.b_bytes) + P.pb_bytes);
+          }
+          __syncwarp();
+          const int na = 2 * ng * P.nplanes;  // activation copies: (plane, group, hi / lo)
+          if (lane < na) {
+            const int pl = lane / (2 * ng), r = lane - pl * 2 * ng, g = r >> 1, hl = r & 1;
+            const int64_t off = (2 * q + g) * a.in.kstride + P.plane_id[pl] * a.in.pstride + cs * 8;
+            ptx::bulk_g2s(sb + pl * 4 * P.a_bytes + (hl * 2 + g) * P.a_bytes + slot0, (hl ? lo : hi) + off, bytes,
+                          bar);
+          } else if (lane == na && P.proj) {
+            ptx::bulk_g2s(sb + P.nplanes * 4 * P.a_bytes + P.b_bytes, P.pw + ((int64_t)n_tile * P.nq + q) * 32 * P.nt,
+                          P.pb_bytes, bar);
+          } else if (lane == na + 1 && !P.wres && P.b_img_nt == P.nt) {
+            ptx::bulk_g2s(sb + P.nplanes * 4 * P.a_bytes, P.w + ((int64_t)n_tile * P.nq + q) * P.taps * 32 * P.nt,
+                          P.b_bytes, bar);
+          }
+          if (!P.wres && P.b_img_nt != P.nt) {
+            // nt of the image's b_img_nt rows: per (tap, group) the hi and lo row ranges
+            const int INT = P.b_img_nt, row0 = n_tile * P.nt, it = row0 / INT, r0 = row0 - it * INT;
+            const uint32_t rows_bytes = (uint32_t)P.nt * 16;
+            for (int j = lane; j < P.taps * 4; j += 32) {
+              const int t = j >> 2, g = (j >> 1) & 1, hl = j & 1;
+              const __half* blk = P.w + (((int64_t)it * P.nq + q) * P.taps + t) * 32 * INT;
+              const uint32_t dst = sb + P.nplanes * 4 * P.a_bytes + (uint32_t)(t * 32 * P.nt + g * 16 * P.nt) * 2;
+              ptx::bulk_g2s(dst + hl * rows_bytes, blk + g * 16 * INT + (hl * INT + r0) * 8, rows_bytes, bar);
+            }
+          }
+          __syncwarp();
+          if (++st == P.stages) { st = 0; ph ^= 1; }
+        }
+      }
+    } else if (lane == 0) {
       const __half* hi = a.in.hi();
       const __half* lo = a.in.lo();
       int st = 0;
@@ -1318,6 +1373,7 @@ static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub,
   }
   if (P.stages < 2) return false;  // neither two streamed stages nor resident weights + two stages fit
   P.dbg = a.opt.dbg;
+  P.wide = a.opt.ss_wide && !P.psub && !P.band && !a.fin.mode && !a.fsk.mode;
   P.time_slot = -1;
   // accumulators: as many partials as accuracy asks for, then two buffers
   // main products rotate over the partials per stage (taps MMAs each)
@@ -1429,6 +1485,9 @@ struct BlkParams {
   int* flag;           // the plan's status word (an activation left the fp16 range)
   unsigned long long* tl;
   int dbg;             // debug bit 32: CTA-0 event trace (built with -DPCNN_SS_TRACE)
+  // wave mode (conv_wave_kernel, C = 16): one image per CTA, every layer's
+  // weights resident, accumulators in a ring of R sub-tile buffers
+  int wave, R;
 };
 
 // CTA-0 event trace of the block kernel (region: 0 producer, 1 MMA, 2 epilogue warp 0)
@@ -1732,6 +1791,254 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk_kernel(const __grid_cons
   }
 }
 
+// =====================================================================
+// Image-resident runs of 16-channel layers (conv_wave_kernel; ResNet-20's
+// stage 1: 32 x 32 images, six 3x3 convs).  A 16-channel image needs 72 KB
+// per slot, so a CTA keeps ONE image (two slots: the ping-pong output and
+// the in-place residual) plus every layer's weights (9 KB each) resident.
+// Without a second image to alternate with, the MMA and epilogue overlap
+// across sub-tiles instead of across images: job (layer l, sub-tile s)
+// needs only sub-tiles s-1..s+1 of layer l-1 (the taps reach one grid row,
+// 33 positions, past a 128-row sub-tile), so the MMA warp runs a wavefront
+// one layer ahead of the epilogue, through a ring of R TMEM accumulators
+// (32 columns each: [main | corr] of the concatenated hi/lo weights).
+// ready[s] counts the epilogue warps that stored sub-tile s of the current
+// layer (one phase per layer); a job waits for its three neighbours, which
+// can never be more than one phase ahead (their next phase needs a later
+// job of the in-order MMA warp).
+// =====================================================================
+constexpr int kWaveMaxSub = 16;
+// four epilogue warpgroups (pairs 0 / 1 take even / odd jobs, each pair's
+// two warpgroups split a job's 16 channels): one 8-channel item is a long
+// dependent chain (accumulator wait, TMEM load, table reads, shared stores,
+// proxy fence, arrive), so twice the warps per sub-partition hide it
+constexpr int kWaveThreads = 576, kWaveProducer = 16, kWaveMma = 17;
+
+struct WaveSmem {
+  uint64_t wfull, ext_full, img_done;
+  uint64_t acc_full[kWaveMaxSub], acc_empty[kWaveMaxSub];
+  uint64_t ready[kWaveMaxSub];
+  uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(kWaveThreads, 1) conv_wave_kernel(const __grid_constant__ BlkParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  const uint32_t slots = ptx::smem_u32(smem);
+  const uint32_t wres = slots + P.set_bytes;
+  WaveSmem* S = reinterpret_cast<WaveSmem*>(smem + (size_t)P.set_bytes + (size_t)P.nl * P.b_bytes);
+  float* ptab = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(S) + ((sizeof(WaveSmem) + 15) & ~size_t(15)));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = (int)gridDim.x, R = P.R, NS = P.S, NL = P.nl;
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(ptx::smem_u32(&S->wfull), 1);
+    ptx::mbar_init(ptx::smem_u32(&S->ext_full), 1);
+    ptx::mbar_init(ptx::smem_u32(&S->img_done), 16);
+    for (int i = 0; i < R; ++i) {
+      ptx::mbar_init(ptx::smem_u32(&S->acc_full[i]), 1);
+      ptx::mbar_init(ptx::smem_u32(&S->acc_empty[i]), 8);
+    }
+    for (int i = 0; i < NS; ++i) ptx::mbar_init(ptx::smem_u32(&S->ready[i]), 8);
+    ptx::fence_mbar_init();
+  }
+  if (warp == kWaveProducer) ptx::tmem_alloc(ptx::smem_u32(&S->tmem_base), P.tmem_cols);
+  {
+    uint4* z = reinterpret_cast<uint4*>(smem);
+    for (uint32_t i = threadIdx.x; i < P.set_bytes / 16; i += kWaveThreads) z[i] = make_uint4(0, 0, 0, 0);
+  }
+  for (int l = 0; l < NL; ++l) epi_fill_tab(P.L[l].epi, P.L[l].etab, ptab + P.L[l].ptab_off, threadIdx.x, kWaveThreads);
+  ptx::fence_proxy_async();
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = S->tmem_base;
+  // weights are parameters: their copy overlaps the previous kernel's tail
+  if (warp == kWaveProducer && lane == 0) {
+    const uint32_t wb = ptx::smem_u32(&S->wfull);
+    ptx::mbar_arrive_tx(wb, (uint32_t)NL * P.b_bytes);
+    for (int l = 0; l < NL; ++l) ptx::bulk_g2s(wres + (uint32_t)l * P.b_bytes, P.L[l].w, P.b_bytes, wb);
+  }
+  ptx::griddep_wait();
+  ptx::griddep_launch();
+  tl_mark(P.tl, 0);
+
+  if (warp == kWaveProducer) {
+    // ===== producer: each image's external input (+ residual) after the
+    // previous image is fully drained =====
+    for (int g = 0;; ++g) {
+      const int b = blockIdx.x + G * g;
+      if (b >= P.batch) break;
+      if (g > 0) {
+        if (lane == 0) ptx::mbar_wait_sleep(ptx::smem_u32(&S->img_done), (g - 1) & 1);
+        __syncwarp();
+      }
+      const int nt_ext = (P.ext_in_slot >= 0) + (P.ext_res_slot >= 0);
+      const uint32_t bytes = (uint32_t)P.P_img * 16;
+      const uint32_t eb = ptx::smem_u32(&S->ext_full);
+      if (lane == 0) ptx::mbar_arrive_tx(eb, (uint32_t)nt_ext * 4 * bytes);
+      __syncwarp();
+      if (lane < 4 * nt_ext) {
+        const int ti = lane >> 2, gp = lane & 3;
+        const bool use_in = P.ext_in_slot >= 0 && ti == 0;
+        const TensorView& t = use_in ? P.ext_in : P.ext_res;
+        const int slot = use_in ? P.ext_in_slot : P.ext_res_slot;
+        const int gg = gp & 1, lo = gp >> 1;
+        const __half* base = lo ? t.lo() : t.hi();
+        const int64_t off = gg * t.kstride + (int64_t)b * (P.H + 1) * P.wp * 8;
+        ptx::bulk_g2s(slots + (uint32_t)slot * P.slot_bytes + (uint32_t)gp * P.plane, base + off, bytes, eb);
+      }
+      __syncwarp();
+    }
+  } else if (warp == kWaveMma) {
+    // ===== MMA issuer: jobs (image, layer, sub-tile) in order =====
+    const int nt = 16;
+    const uint32_t idesc = ptx::idesc_f16(kTileM, nt), idesc2 = ptx::idesc_f16(kTileM, 2 * nt);
+    const uint32_t a_lbo = P.plane, b_lbo = 2 * nt * 16;
+    uint64_t offs[9];
+#pragma unroll
+    for (int t = 0; t < 9; ++t) offs[t] = (uint64_t)P.toff[t];
+    const uint64_t bstep = (uint64_t)(64 * nt) >> 4, blo = (uint64_t)(nt * 16) >> 4;
+    ptx::mbar_wait(ptx::smem_u32(&S->wfull), 0);
+    uint32_t j = 0;  // job counter (ring slot j % R, use j / R)
+    for (int g = 0;; ++g) {
+      const int b = blockIdx.x + G * g;
+      if (b >= P.batch) break;
+      ptx::mbar_wait(ptx::smem_u32(&S->ext_full), g & 1);
+      for (int l = 0; l < NL; ++l) {
+        const uint32_t in_base = slots + (uint32_t)P.L[l].in_slot * P.slot_bytes;
+        const uint64_t b0d = ptx::smem_desc_noswz(wres + (uint32_t)l * P.b_bytes, b_lbo, 128);
+        const uint32_t rph = (uint32_t)(g * NL + l - 1) & 1u;  // phase of layer l-1's ready
+        for (int s = 0; s < NS; ++s, ++j) {
+          if (l > 0) {
+            if (s == 0) {
+              ptx::mbar_wait(ptx::smem_u32(&S->ready[0]), rph);
+              if (NS > 1) ptx::mbar_wait(ptx::smem_u32(&S->ready[1]), rph);
+            } else if (s + 1 < NS) {
+              ptx::mbar_wait(ptx::smem_u32(&S->ready[s + 1]), rph);
+            }
+          }
+          const uint32_t r = j % (uint32_t)R;
+          ptx::mbar_wait(ptx::smem_u32(&S->acc_empty[r]), ((j / (uint32_t)R) & 1u) ^ 1u);
+          ptx::tc_fence_after();
+          const uint32_t a0 = in_base + (uint32_t)(128 * s) * 16;
+          const uint64_t ah = ptx::smem_desc_noswz(a0, a_lbo, 128), al = ptx::smem_desc_noswz(a0 + 2 * P.plane, a_lbo, 128);
+          const uint32_t dm = tmem + r * 32u;
+          ss_stage<9>(true, dm, dm + nt, ah, al, b0d, bstep, blo, idesc2, idesc, 0u, 1u, offs);
+          ptx::mma_commit_warp(ptx::smem_u32(&S->acc_full[r]));
+        }
+      }
+    }
+  } else if (warp < 16) {
+    // ===== epilogue: warpgroup pair jp = wg / 2 drains the jobs j = jp
+    // (mod 2); warpgroup ew = wg % 2 of the pair takes channels 8 ew .. +7 =====
+    const int wg = warp >> 2, ew = wg & 1, jp = wg >> 1, row = threadIdx.x & 127, chb = 8 * ew;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    uint32_t j = 0;
+    for (int g = 0;; ++g) {
+      const int b = blockIdx.x + G * g;
+      if (b >= P.batch) break;
+      for (int l = 0; l < NL; ++l) {
+        const BlkLayer& L = P.L[l];
+        const EpiParams& e = L.epi;
+        const bool last = l == NL - 1;
+        if (L.res_ext) ptx::mbar_wait_warp(ptx::smem_u32(&S->ext_full), g & 1);
+        EpiTab tab = L.etab;
+        tab.ptab = ptab + L.ptab_off;
+        const float wsc = __ldg(L.wscale) * L.in_sload;
+        float psum[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) psum[q] = 0.f;
+        for (int s = 0; s < NS; ++s, ++j) {
+          if ((int)(j & 1u) != jp) continue;
+          const uint32_t r = j % (uint32_t)R;
+          const int p = P.p_out0 + 128 * s + row;
+          const int y = (p - 1) / P.wp - 1, x = p - 1 - (y + 1) * P.wp;
+          const bool inside = p < P.p_out0 + P.nout, valid = inside && x < P.W;
+          float sk[8];
+          if (L.res_slot >= 0) {
+            const uint32_t rb = slots + (uint32_t)L.res_slot * P.slot_bytes + (uint32_t)ew * P.plane + (uint32_t)p * 16;
+            uint4 h, q;
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(h.x), "=r"(h.y), "=r"(h.z), "=r"(h.w) : "r"(rb) : "memory");
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "r"(rb + 2 * P.plane) : "memory");
+            const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {q.x, q.y, q.z, q.w};
+            const float2 ss = make_float2(L.res_sload, L.res_sload);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              f2_put(sk + 2 * i, __fmul2_rn(__fadd2_rn(unpack_half2(hw[i]), unpack_half2(lw[i])), ss));
+          } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) sk[q] = 0.f;
+          }
+          ptx::mbar_wait_warp(ptx::smem_u32(&S->acc_full[r]), (j / (uint32_t)R) & 1u);
+          ptx::tc_fence_after();
+          float v[8], t[8];
+          const uint32_t d = tmem + lane_off + r * 32u;
+          ptx::tmem_ld8x2(d + 16 + chb, d + chb, v, t);
+          // the accumulator is in registers: hand the ring slot back
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->acc_empty[r]));
+          add_n<8>(v, t);
+          epi_point8(e, tab, v, wsc, sk, chb);
+          if (!last) {
+            if (inside) {
+              uint32_t hi[4], lo[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                if (valid) split_pair(v[2 * i], v[2 * i + 1], hi[i], lo[i]);
+                else hi[i] = lo[i] = 0u;
+              }
+              __half2 m = __habs2(*reinterpret_cast<const __half2*>(&hi[0]));
+#pragma unroll
+              for (int i = 1; i < 4; ++i) m = __hmax2_nan(m, __habs2(*reinterpret_cast<const __half2*>(&hi[i])));
+              const float2 mf = __half22float2(m);
+              if (!(mf.x < 32768.f && mf.y < 32768.f)) atomicExch(P.flag, 1);
+              const uint32_t ob = slots + (uint32_t)L.out_slot * P.slot_bytes + (uint32_t)ew * P.plane + (uint32_t)p * 16;
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(ob), "r"(hi[0]), "r"(hi[1]), "r"(hi[2]),
+                           "r"(hi[3]) : "memory");
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(ob + 2 * P.plane), "r"(lo[0]), "r"(lo[1]),
+                           "r"(lo[2]), "r"(lo[3]) : "memory");
+            }
+          } else if (e.pool == PCNN_POOL_GLOBAL) {
+            if (valid) add_n<8>(psum, v);
+          } else if (valid) {
+            store8_any(e.out, b, chb, y, x, v);
+          }
+          // this warp's rows of sub-tile s are stored: to the async proxy
+          // (the next layer's tcgen05 reads), then count the warp in
+          ptx::fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->ready[s]));
+        }
+        if (last && e.pool == PCNN_POOL_GLOBAL) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+#pragma unroll
+            for (int o = 16; o; o >>= 1) psum[q] += __shfl_xor_sync(0xffffffffu, psum[q], o);
+          if (lane < 8) {
+            float mine = psum[0];
+#pragma unroll
+            for (int q = 1; q < 8; ++q)
+              if (lane == q) mine = psum[q];
+            if (chb + lane < e.cout) atomicAdd(e.out.base + (int64_t)b * e.npad + chb + lane, mine * __ldg(e.pool_p));
+          }
+        }
+      }
+      // the image is drained (its last layer's residual reads included)
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->img_done));
+    }
+  }
+  __syncthreads();
+  tl_mark(P.tl, 1);
+  if (warp == kWaveProducer) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, P.tmem_cols);
+  }
+}
+
 }  // namespace
 
 struct BlkRun {
@@ -1753,7 +2060,8 @@ BlkRun* blk_create(const ConvArgs* layers, int n, const int* in_slot, const int*
   P.H = a0.in.h;
   P.W = a0.in.w;
   P.wp = a0.in.wp;
-  if (P.C % 32 || P.nq > kBlkMaxChunks || P.wp != P.W + 1) { delete r; return nullptr; }
+  P.wave = P.C == 16;  // 16 channels: one image per CTA, sub-tile wavefront (conv_wave_kernel)
+  if ((P.C % 32 && !P.wave) || P.nq > kBlkMaxChunks || P.wp != P.W + 1) { delete r; return nullptr; }
   P.nout = P.H * P.wp;
   P.p_out0 = 1 + P.wp;
   P.S = (P.nout + kTileM - 1) / kTileM;
@@ -1775,8 +2083,9 @@ BlkRun* blk_create(const ConvArgs* layers, int n, const int* in_slot, const int*
   P.batch = batch;
   P.b_bytes = 9u * 64u * (uint32_t)P.C;
   P.set_cols = 2u * (uint32_t)P.C;
-  const uint32_t need = 2u * (uint32_t)P.S * P.set_cols;
-  if (need > 512) { delete r; return nullptr; }
+  const uint32_t need = P.wave ? 512u : 2u * (uint32_t)P.S * P.set_cols;
+  if (need > 512 || (P.wave && P.S > kWaveMaxSub)) { delete r; return nullptr; }
+  P.R = P.wave ? 512 / (int)P.set_cols : 0;
   P.tmem_cols = need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
   for (int t = 0; t < 9; ++t) P.toff[t] = (t / 3) * P.wp + t % 3;
   P.flag = flag;
@@ -1807,8 +2116,19 @@ BlkRun* blk_create(const ConvArgs* layers, int n, const int* in_slot, const int*
     pt += (L.etab.rows * P.C + 3) & ~3;
   }
   P.ptab_floats = pt;
-  const size_t aux = ((sizeof(BlkSmem) + 15) & ~size_t(15)) + (size_t)pt * 4;
   const size_t budget = 225 * 1024 - 128;
+  if (P.wave) {
+    // one image, every layer's weights resident; A over-reads of the last
+    // sub-tile land in the weights (discarded rows)
+    P.ni = 1;
+    const size_t fixed = (size_t)P.set_bytes + (size_t)n * P.b_bytes + ((sizeof(WaveSmem) + 15) & ~size_t(15)) +
+                         (size_t)pt * 4;
+    if (fixed > budget || overrun > (size_t)n * P.b_bytes) { delete r; return nullptr; }
+    P.stages = 0;
+    r->smem = 128 + fixed;
+    return r;
+  }
+  const size_t aux = ((sizeof(BlkSmem) + 15) & ~size_t(15)) + (size_t)pt * 4;
   P.ni = max_images >= 2 ? 2 : 1;
   if (P.ni == 2 && 2 * (size_t)P.set_bytes + aux + 2 * (size_t)P.b_bytes > budget) P.ni = 1;
   const size_t fixed = (size_t)P.ni * P.set_bytes + aux;
@@ -1829,6 +2149,11 @@ void blk_launch(const BlkRun* r, cudaStream_t s, unsigned long long* tl, int pdl
   BlkParams P = r->P;
   P.tl = tl;
   const int grid = P.batch < nsm ? P.batch : nsm;
+  if (P.wave) {
+    cudaFuncSetAttribute(conv_wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)r->smem);
+    launch_pdl(conv_wave_kernel, grid, kWaveThreads, r->smem, s, pdl, P);
+    return;
+  }
   cudaFuncSetAttribute(conv_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)r->smem);
   launch_pdl(conv_blk_kernel, grid, kThreads, r->smem, s, pdl, P);
 }
