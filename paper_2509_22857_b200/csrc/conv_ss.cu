@@ -1446,6 +1446,11 @@ bool make_ss_params(const ConvArgs& a, SsParams& P, bool allow_wres = true) {
 // are discarded.
 // =====================================================================
 constexpr int kBlkMaxLayers = 6;
+// the image-resident kernels run four epilogue warpgroups (warps 0-15), the
+// producer (16) and the MMA warp (17): an epilogue item is a long dependent
+// chain (accumulator wait, TMEM load, table reads, stores, proxy fence,
+// arrive), and twice the warps per sub-partition hide it
+constexpr int kWaveThreads = 576, kWaveProducer = 16, kWaveMma = 17;
 constexpr int kBlkMaxChunks = 8;
 constexpr int kBlkStages = 4;
 
@@ -1511,7 +1516,7 @@ struct BlkSmem {
   uint32_t tmem_base;
 };
 
-__global__ void __launch_bounds__(kThreads, 1) conv_blk_kernel(const __grid_constant__ BlkParams P) {
+__global__ void __launch_bounds__(kWaveThreads, 1) conv_blk_kernel(const __grid_constant__ BlkParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   const uint32_t slots = ptx::smem_u32(smem);
@@ -1527,23 +1532,23 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk_kernel(const __grid_cons
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(ptx::smem_u32(&S->acc_full[i]), 1);
-      ptx::mbar_init(ptx::smem_u32(&S->acc_empty[i]), 8);
+      ptx::mbar_init(ptx::smem_u32(&S->acc_empty[i]), 16);
     }
     for (int q = 0; q < kBlkMaxChunks; ++q) ptx::mbar_init(ptx::smem_u32(&S->ready[q]), 8);
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(ptx::smem_u32(&S->ext_full[i]), 1);
-      ptx::mbar_init(ptx::smem_u32(&S->img_free[i]), 8);
+      ptx::mbar_init(ptx::smem_u32(&S->img_free[i]), 16);
     }
     ptx::fence_mbar_init();
   }
-  if (warp == kWarpProducer) ptx::tmem_alloc(ptx::smem_u32(&S->tmem_base), P.tmem_cols);
+  if (warp == kWaveProducer) ptx::tmem_alloc(ptx::smem_u32(&S->tmem_base), P.tmem_cols);
   // zero the activation slots (their unwritten border rows are the conv padding)
   {
     uint4* z = reinterpret_cast<uint4*>(smem);
     const uint32_t n16 = (uint32_t)P.ni * P.set_bytes / 16;
-    for (uint32_t i = threadIdx.x; i < n16; i += kThreads) z[i] = make_uint4(0, 0, 0, 0);
+    for (uint32_t i = threadIdx.x; i < n16; i += kWaveThreads) z[i] = make_uint4(0, 0, 0, 0);
   }
-  for (int l = 0; l < P.nl; ++l) epi_fill_tab(P.L[l].epi, P.L[l].etab, ptab + P.L[l].ptab_off, threadIdx.x, kThreads);
+  for (int l = 0; l < P.nl; ++l) epi_fill_tab(P.L[l].epi, P.L[l].etab, ptab + P.L[l].ptab_off, threadIdx.x, kWaveThreads);
   ptx::fence_proxy_async();  // generic zero stores -> tcgen05 reads of the slots
   ptx::tc_fence_before();
   __syncthreads();
@@ -1553,7 +1558,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk_kernel(const __grid_cons
   ptx::griddep_launch();
   tl_mark(P.tl, 0);
 
-  if (warp == kWarpProducer) {
+  if (warp == kWaveProducer) {
     // ===== producer: per image the external tensors (after the previous
     // image is drained), then every (layer, chunk) weight stage =====
     int st = 0;
@@ -1603,7 +1608,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk_kernel(const __grid_cons
       }
       __syncwarp();
     }
-  } else if (warp == kWarpMma) {
+  } else if (warp == kWaveMma) {
     // ===== MMA issuer =====
     const int nt = P.C;
     const uint32_t idesc = ptx::idesc_f16(kTileM, nt), idesc2 = ptx::idesc_f16(kTileM, 2 * nt);
@@ -1659,14 +1664,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk_kernel(const __grid_cons
           ++use[buf];
         }
     }
-  } else if (warp < 8) {
+  } else if (warp < 16) {
     // ===== epilogue: every 16-channel chunk k is split between the two
     // warpgroups (warpgroup ew: channels 16k + 8ew .. +8 of every sub-tile),
     // chunks in order, so chunk k of a layer is complete -- and the next
     // layer's MMAs on it can start -- after the shortest time; a layer's
     // output goes to its slot (split hi/lo, the next layer's A operand) or,
     // for the last layer, to global memory =====
-    const int ew = warp >> 2, row = threadIdx.x & 127;
+    // four warpgroups: pair jp = wg / 2 drains chunks k = jp (mod 2), warpgroup
+    // ew = wg % 2 of the pair channels 16 k + 8 ew .. +7 (a 16-channel chunk's
+    // ready count stays the 8 warps of its pair)
+    const int wg = warp >> 2, ew = wg & 1, jp = wg >> 1, row = threadIdx.x & 127;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     uint32_t use[2] = {0u, 0u};
     int gl = 0;
@@ -1691,7 +1699,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk_kernel(const __grid_cons
         EpiTab tab = L.etab;
         tab.ptab = ptab + L.ptab_off;
         const float wsc = __ldg(L.wscale) * L.in_sload;
-        for (int k = 0; k < P.nq; ++k) {
+        for (int k = jp; k < P.nq; k += 2) {
           const int chb = 16 * k + 8 * ew;
           float psum[8];
 #pragma unroll
@@ -1785,7 +1793,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk_kernel(const __grid_cons
   }
   __syncthreads();
   tl_mark(P.tl, 1);
-  if (warp == kWarpProducer) {
+  if (warp == kWaveProducer) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, P.tmem_cols);
   }
@@ -1807,12 +1815,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_blk_kernel(const __grid_cons
 // can never be more than one phase ahead (their next phase needs a later
 // job of the in-order MMA warp).
 // =====================================================================
-constexpr int kWaveMaxSub = 16;
-// four epilogue warpgroups (pairs 0 / 1 take even / odd jobs, each pair's
-// two warpgroups split a job's 16 channels): one 8-channel item is a long
-// dependent chain (accumulator wait, TMEM load, table reads, shared stores,
-// proxy fence, arrive), so twice the warps per sub-partition hide it
-constexpr int kWaveThreads = 576, kWaveProducer = 16, kWaveMma = 17;
+constexpr int kWaveMaxSub = 16;  // pairs of epilogue warpgroups take even / odd jobs
 
 struct WaveSmem {
   uint64_t wfull, ext_full, img_done;
@@ -2155,7 +2158,7 @@ void blk_launch(const BlkRun* r, cudaStream_t s, unsigned long long* tl, int pdl
     return;
   }
   cudaFuncSetAttribute(conv_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)r->smem);
-  launch_pdl(conv_blk_kernel, grid, kThreads, r->smem, s, pdl, P);
+  launch_pdl(conv_blk_kernel, grid, kWaveThreads, r->smem, s, pdl, P);
 }
 
 void blk_destroy(BlkRun* r) { delete r; }
