@@ -266,7 +266,10 @@ typedef struct pcnn_plan_options {
   int64_t ss_wide;          /* 1: the halo-tile producer warp issues a
                                stage's bulk copies from several lanes at
                                once (one lane pays ~300 cycles per copy)   */
-  int64_t reserved[6];
+  int64_t epi_pairs;        /* halo-tile kernel epilogue warpgroup pairs:
+                               2 (four warpgroups, pairs alternate tiles)
+                               or 1                                        */
+  int64_t reserved[5];
 } pcnn_plan_options;
 
 /* ---- entry points --------------------------------------------------------*/

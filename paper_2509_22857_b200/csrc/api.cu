@@ -956,6 +956,7 @@ void pcnn_plan_options_default(pcnn_plan_options* o) {
   o->debug = 0;
   o->fused_net = 1;
   o->ss_wide = 1;
+  o->epi_pairs = 2;
 }
 
 int pcnn_plan_create(const pcnn_unit_desc* units, int n_units, const pcnn_tensor_desc* tensors, int n_tensors,
@@ -986,6 +987,7 @@ int pcnn_plan_create_ex(const pcnn_unit_desc* units, int n_units, const pcnn_ten
   p->kopt.ss_psub = (int)p->opt.ss_psub;
   p->kopt.ss_wres = (int)p->opt.ss_wres;
   p->kopt.ss_wide = (int)p->opt.ss_wide;
+  p->kopt.epi_pairs = (int)p->opt.epi_pairs;
   p->kopt.tc_stage = (int)p->opt.tc_stage;
   p->kopt.proj_fuse = (int)p->opt.fuse_projection;
   p->kopt.streamk = (int)p->opt.streamk;

@@ -72,6 +72,7 @@ struct SsParams {
   uint32_t tmem_cols;
   FastDiv div_hw, div_wp, div_mt;  // grid position decode, tile -> n_tile
   int share_epi;         // both epilogue warpgroups drain every tile (alternate chunks)
+  int epi_pairs;         // warpgroup pairs draining tiles (2: pairs alternate tiles, 4 warpgroups)
   int b_img_nt;          // rows per tile of the packed weight image (nt, or 128 when nt = 64)
   // psub: 3x3 stride-2 conv staged one parity plane at a time (4 sub-stages
   // per 16-channel chunk, each with that plane's taps): smaller stages, more
@@ -550,9 +551,17 @@ __device__ __forceinline__ void band_item(const SsParams& P, const EpiParams& e,
 // shared by every other layer of the network is already resident.
 constexpr int kPoolNone = 0, kPoolBand = 2;
 
-template <int TAPS, bool SK, int POOL>
-__global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_constant__ SsParams P) {
+// threads: PAIRS pairs of epilogue warpgroups, the producer and the MMA
+// warp.  Two pairs (576 threads, <= 112 registers) hide the epilogue's
+// latency on narrow layers; wide layers keep one pair and 168 registers
+template <int PAIRS>
+constexpr int ss_threads() { return PAIRS == 2 ? 576 : 320; }
+
+template <int TAPS, bool SK, int POOL, int PAIRS = 1>
+__global__ void __launch_bounds__(ss_threads<PAIRS>(), 1) conv_ss_kernel(const __grid_constant__ SsParams P) {
   constexpr bool BAND = POOL == kPoolBand;
+  constexpr int kThreads = ss_threads<PAIRS>();
+  constexpr int kWarpProducer = kThreads / 32 - 2, kWarpMma = kThreads / 32 - 1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   const ConvArgs& a = P.a;
@@ -884,14 +893,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
       ptx::mma_commit_warp(ptx::smem_u32(&S->acc_full[acc]));
       if (++acc == (uint32_t)NB) { acc = 0; acc_ph ^= 1; }
     }
-  } else if (warp < 8) {
+  } else if (warp < 8 * PAIRS) {
     // ===== epilogue: a tile's 16-column chunks (sub-tile, channel chunk)
     // k = 0 .. mt * nt / 16 - 1.  Unshared: warpgroup (buffer % 2) drains
     // the whole buffer; shared: both warpgroups drain every buffer, warpgroup
     // ew taking the chunks k = ew (mod 2), halving a tile's epilogue latency.
     // The warpgroup walks its (tile, chunk) items in order and issues the
     // next item's residual loads (across tiles too) before this item's math. =====
-    const int ew = warp >> 2;
+    // pairs (two pairs: 4 warpgroups): pair jp drains the tiles it = jp
+    // (mod 2) -- consecutive tiles sit in different accumulator buffers --
+    // and within a pair everything runs as with one pair of warpgroups
+    const int wg = warp >> 2, ew = wg & 1, jp = wg >> 1, nwg = 2 * PAIRS;
     const EpiParams& e = a.epi;
     const int row = threadIdx.x & 127;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
@@ -906,7 +918,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
     const int lg_nb = __ffs(NB) - 1;
     // residual rows are staged in shared memory by cp.async one item ahead
     // ([buffer][word][thread] x 16 bytes: conflict-free 16-byte reads)
-    const uint32_t skq = 256 * 16;
+    const uint32_t skq = (uint32_t)nwg * 128 * 16;
     const uint32_t sk_slot = ptx::smem_u32(ptab + P.etab.rows * e.npad) + threadIdx.x * 16;
     // band mode: staging [warpgroup][2][128 rows][kStgPitch] then the ring
     // [2 slots][nchunk][wpo][16] (no residual, so the residual staging area is free)
@@ -974,7 +986,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
           x.c_lo = sx.c_lo;
           x.nqs = sx.q1 - sx.q0;
         }
-        if (P.share_epi || ((int)((x.it & (NB - 1)) & 1) == ew && !(NB == 1 && ew == 1))) break;
+        if (P.share_epi ? (NB == 1 ? jp == 0 : (int)(x.it & (uint32_t)(PAIRS - 1)) == jp)
+                        : (int)((x.it & (uint32_t)(NB - 1)) % (uint32_t)nwg) == wg)
+          break;
       }
       x.k = k0;
       return true;
@@ -1188,21 +1202,22 @@ __global__ void __launch_bounds__(kThreads, 1) conv_ss_kernel(const __grid_const
   cta_stamp(P, 3);
 }
 
-// residual staging: [2 buffers][4 words][256 epilogue threads] x 16 bytes
-constexpr uint32_t kSkipStage = 2 * 4 * 256 * 16;
+// residual staging: [2 buffers][4 words][epilogue threads] x 16 bytes
+inline uint32_t ss_skip_stage(int pairs) { return 2u * 4u * 256u * 16u * (uint32_t)pairs; }
 
 size_t ss_aux_bytes(const SsParams& P) {
   const size_t band =
       P.band ? 16 + (size_t)(4 * kTileM * kStgPitch + 4 * 64 + 2 * (P.brows / 2 + 2) * P.nchunk * P.wpo * 16) * 4 : 0;
   return ((sizeof(Smem) + 15) & ~size_t(15)) + (size_t)P.etab.rows * P.a.epi.npad * 4 +
-         (P.proj ? (size_t)P.petab.rows * P.pe.npad * 4 : 0) + (P.a.epi.residual ? kSkipStage : 0) + band;
+         (P.proj ? (size_t)P.petab.rows * P.pe.npad * 4 : 0) + (P.a.epi.residual ? ss_skip_stage(P.epi_pairs) : 0) + band;
 }
 
 // nt: output channels per tile (the weight image is packed in tiles of
 // min(npad, 128) rows; a smaller nt copies its rows out of that image)
 static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub, bool allow_wres, int force_mt = 0,
-                              int max_np = 0) {
+                              int max_np = 0, int pairs = 1) {
   const TensorView& in = a.in;
+  P.epi_pairs = pairs;
   if (!a.f16 || !a.tcwss || !a.tc16_scale) return false;
   if ((a.stride != 1 && a.stride != 2) || a.kh != a.kw ||
       !((a.kh == 3 && a.pad == 1) || (a.kh == 1 && a.pad == 0) || (a.kh == 4 && a.pad == 1 && a.stride == 1)))
@@ -1397,6 +1412,7 @@ static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub,
   // shared epilogue when a tile has an even number of 16-column chunks
   P.share_epi = a.opt.ss_share >= 0 ? a.opt.ss_share : ((P.mt * (P.proj ? 2 : 1) * P.nt / 16) % 2 == 0);
   if (P.band) P.share_epi = 1;  // chunk k always drains on warpgroup k % 2 (ring ownership)
+  if (P.band) P.epi_pairs = 1;
   P.div_hw = make_fastdiv((uint32_t)(P.hp * P.wp));
   P.div_h1 = make_fastdiv((uint32_t)P.hp);
   P.div_wp = make_fastdiv((uint32_t)P.wp);
@@ -1408,13 +1424,35 @@ static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub,
 // all taps' weights) when two fit; else, for 3x3 stride 2, one parity plane
 // per stage (measured: faster than 64-channel tiles, slower than whole-chunk
 // stages when those fit); else two 64-channel tiles.  Option ss_psub 0/1 forces.
-bool make_ss_params(const ConvArgs& a, SsParams& P, bool allow_wres = true) {
+static bool make_ss_params_pairs(const ConvArgs& a, SsParams& P, bool allow_wres, int pairs) {
   const int nt = a.npad <= 128 ? a.npad : 128;
   const int force = a.opt.ss_psub;
-  if (force == 1 && make_ss_params_nt(a, P, nt, true, allow_wres)) return true;
-  if (make_ss_params_nt(a, P, nt, false, allow_wres)) return true;
-  if (force != 0 && make_ss_params_nt(a, P, nt, true, allow_wres)) return true;
-  return nt == 128 && make_ss_params_nt(a, P, 64, false, allow_wres);
+  if (force == 1 && make_ss_params_nt(a, P, nt, true, allow_wres, 0, 0, pairs)) return true;
+  if (make_ss_params_nt(a, P, nt, false, allow_wres, 0, 0, pairs)) return true;
+  if (force != 0 && make_ss_params_nt(a, P, nt, true, allow_wres, 0, 0, pairs)) return true;
+  return nt == 128 && make_ss_params_nt(a, P, 64, false, allow_wres, 0, 0, pairs);
+}
+
+// Two epilogue pairs (four warpgroups) for narrow layers (<= 32 output
+// channels, or <= 64 with a fused projection, whose tiles carry twice the
+// epilogue items): measured per unit, RN20's downsampling convs with their
+// projections 17.8 -> 15.3 us and 17.0 -> 14.8 us, while RN18's 64-channel
+// 56 x 56 layers and its stem run slower at the 112-register budget (50 ->
+// 54 us, 204 -> 234 us).  Only when the same staging choice still holds
+// with the larger residual staging area and keeps its pipeline depth.
+bool make_ss_params(const ConvArgs& a, SsParams& P, bool allow_wres = true) {
+  SsParams P1 = P;
+  if (!make_ss_params_pairs(a, P1, allow_wres, 1)) return false;
+  if (a.opt.epi_pairs >= 2 && (P1.nt <= 32 || (P1.nt <= 64 && P1.proj)) && !P1.band && !a.sk_flags) {
+    SsParams Q = P;
+    if (make_ss_params_nt(a, Q, P1.nt, P1.psub != 0, allow_wres, 0, 0, 2) && Q.wres == P1.wres &&
+        Q.mt == P1.mt && Q.stages >= (P1.stages < 3 ? P1.stages : 3)) {
+      P = Q;
+      return true;
+    }
+  }
+  P = P1;
+  return true;
 }
 
 // =====================================================================
@@ -2276,6 +2314,9 @@ void launch_conv_ss(const ConvArgs& a, cudaStream_t s) {
   void (*k)(SsParams);
   if (P.band) {
     k = P.taps == 16 ? conv_ss_kernel<16, false, kPoolBand> : conv_ss_kernel<9, false, kPoolBand>;
+  } else if (P.epi_pairs == 2) {
+    k = P.taps == 16 ? conv_ss_kernel<16, false, kPoolNone, 2>
+        : P.taps == 9 ? conv_ss_kernel<9, false, kPoolNone, 2> : conv_ss_kernel<1, false, kPoolNone, 2>;
   } else {
     k = P.taps == 16 ? (sk ? conv_ss_kernel<16, true, kPoolNone> : conv_ss_kernel<16, false, kPoolNone>)
         : P.taps == 9 ? (sk ? conv_ss_kernel<9, true, kPoolNone> : conv_ss_kernel<9, false, kPoolNone>)
@@ -2283,7 +2324,7 @@ void launch_conv_ss(const ConvArgs& a, cudaStream_t s) {
   }
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (P.dbg & 64) P.time_slot = g_time_next++ % kTimeSlots;
-  launch_pdl(k, grid, kThreads, smem, s, a.opt.pdl, P);
+  launch_pdl(k, grid, P.epi_pairs == 2 ? ss_threads<2>() : ss_threads<1>(), smem, s, a.opt.pdl, P);
 }
 
 }  // namespace pcnn

@@ -29,6 +29,7 @@ struct KOpts {
   int ss_psub = -1;     // parity-plane stages (-1 auto)
   int ss_wres = 1;      // resident weights
   int ss_wide = 1;      // halo-tile producer issues a stage's copies from many lanes
+  int epi_pairs = 2;    // halo-tile epilogue warpgroup pairs (1 or 2)
   int tc_stage = 1;     // TMA-staged input boxes (TMEM-A kernel)
   int proj_fuse = 1;    // fused projections
   int streamk = 1;      // stream-K
