@@ -1854,15 +1854,18 @@ __global__ void __launch_bounds__(kWaveThreads, 1) conv_blk_kernel(const __grid_
 // job of the in-order MMA warp).
 // =====================================================================
 constexpr int kWaveMaxSub = 16;  // pairs of epilogue warpgroups take even / odd jobs
+// two MMA warps (even / odd jobs): one warp's dependency waits (~200-300
+// cycles per mbarrier test) overlap the other warp's MMA issue
+constexpr int kWaveThreads2 = 608, kWaveMma2 = 18;
 
 struct WaveSmem {
   uint64_t wfull, ext_full, img_done;
   uint64_t acc_full[kWaveMaxSub], acc_empty[kWaveMaxSub];
-  uint64_t ready[kWaveMaxSub];
+  uint64_t ready[2][kWaveMaxSub];  // by layer parity: [global layer & 1][sub-tile]
   uint32_t tmem_base;
 };
 
-__global__ void __launch_bounds__(kWaveThreads, 1) conv_wave_kernel(const __grid_constant__ BlkParams P) {
+__global__ void __launch_bounds__(kWaveThreads2, 1) conv_wave_kernel(const __grid_constant__ BlkParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   const uint32_t slots = ptx::smem_u32(smem);
@@ -1879,15 +1882,18 @@ __global__ void __launch_bounds__(kWaveThreads, 1) conv_wave_kernel(const __grid
       ptx::mbar_init(ptx::smem_u32(&S->acc_full[i]), 1);
       ptx::mbar_init(ptx::smem_u32(&S->acc_empty[i]), 8);
     }
-    for (int i = 0; i < NS; ++i) ptx::mbar_init(ptx::smem_u32(&S->ready[i]), 8);
+    for (int i = 0; i < NS; ++i) {
+      ptx::mbar_init(ptx::smem_u32(&S->ready[0][i]), 8);
+      ptx::mbar_init(ptx::smem_u32(&S->ready[1][i]), 8);
+    }
     ptx::fence_mbar_init();
   }
   if (warp == kWaveProducer) ptx::tmem_alloc(ptx::smem_u32(&S->tmem_base), P.tmem_cols);
   {
     uint4* z = reinterpret_cast<uint4*>(smem);
-    for (uint32_t i = threadIdx.x; i < P.set_bytes / 16; i += kWaveThreads) z[i] = make_uint4(0, 0, 0, 0);
+    for (uint32_t i = threadIdx.x; i < P.set_bytes / 16; i += kWaveThreads2) z[i] = make_uint4(0, 0, 0, 0);
   }
-  for (int l = 0; l < NL; ++l) epi_fill_tab(P.L[l].epi, P.L[l].etab, ptab + P.L[l].ptab_off, threadIdx.x, kWaveThreads);
+  for (int l = 0; l < NL; ++l) epi_fill_tab(P.L[l].epi, P.L[l].etab, ptab + P.L[l].ptab_off, threadIdx.x, kWaveThreads2);
   ptx::fence_proxy_async();
   ptx::tc_fence_before();
   __syncthreads();
@@ -1930,8 +1936,13 @@ __global__ void __launch_bounds__(kWaveThreads, 1) conv_wave_kernel(const __grid
       }
       __syncwarp();
     }
-  } else if (warp == kWaveMma) {
-    // ===== MMA issuer: jobs (image, layer, sub-tile) in order =====
+  } else if (warp == kWaveMma || warp == kWaveMma2) {
+    // ===== MMA issuers: warp kWaveMma the even jobs, kWaveMma2 the odd ones
+    // (jobs (image, layer, sub-tile) in order).  A job waits for all three
+    // of its input sub-tiles (the other warp may have issued the neighbours)
+    // on ready[layer & 1]: a neighbour's barrier cannot run a phase ahead,
+    // since layer l+1 at sub-tiles s-1 .. s+1 needs this job's output.
+    const uint32_t mine = warp == kWaveMma ? 0u : 1u;
     const int nt = 16;
     const uint32_t idesc = ptx::idesc_f16(kTileM, nt), idesc2 = ptx::idesc_f16(kTileM, 2 * nt);
     const uint32_t a_lbo = P.plane, b_lbo = 2 * nt * 16;
@@ -1948,15 +1959,14 @@ __global__ void __launch_bounds__(kWaveThreads, 1) conv_wave_kernel(const __grid
       for (int l = 0; l < NL; ++l) {
         const uint32_t in_base = slots + (uint32_t)P.L[l].in_slot * P.slot_bytes;
         const uint64_t b0d = ptx::smem_desc_noswz(wres + (uint32_t)l * P.b_bytes, b_lbo, 128);
-        const uint32_t rph = (uint32_t)(g * NL + l - 1) & 1u;  // phase of layer l-1's ready
+        const int gl = g * NL + l - 1;  // global index of the input's layer
+        const uint32_t rb = ptx::smem_u32(&S->ready[gl & 1][0]), rph = (uint32_t)(gl >> 1) & 1u;
         for (int s = 0; s < NS; ++s, ++j) {
+          if ((j & 1u) != mine) continue;
           if (l > 0) {
-            if (s == 0) {
-              ptx::mbar_wait(ptx::smem_u32(&S->ready[0]), rph);
-              if (NS > 1) ptx::mbar_wait(ptx::smem_u32(&S->ready[1]), rph);
-            } else if (s + 1 < NS) {
-              ptx::mbar_wait(ptx::smem_u32(&S->ready[s + 1]), rph);
-            }
+            if (s > 0) ptx::mbar_wait(rb + 8u * (uint32_t)(s - 1), rph);
+            ptx::mbar_wait(rb + 8u * (uint32_t)s, rph);
+            if (s + 1 < NS) ptx::mbar_wait(rb + 8u * (uint32_t)(s + 1), rph);
           }
           const uint32_t r = j % (uint32_t)R;
           ptx::mbar_wait(ptx::smem_u32(&S->acc_empty[r]), ((j / (uint32_t)R) & 1u) ^ 1u);
@@ -2051,7 +2061,7 @@ __global__ void __launch_bounds__(kWaveThreads, 1) conv_wave_kernel(const __grid
           // (the next layer's tcgen05 reads), then count the warp in
           ptx::fence_proxy_async();
           __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->ready[s]));
+          if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->ready[(g * NL + l) & 1][s]));
         }
         if (last && e.pool == PCNN_POOL_GLOBAL) {
 #pragma unroll
@@ -2192,7 +2202,7 @@ void blk_launch(const BlkRun* r, cudaStream_t s, unsigned long long* tl, int pdl
   const int grid = P.batch < nsm ? P.batch : nsm;
   if (P.wave) {
     cudaFuncSetAttribute(conv_wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)r->smem);
-    launch_pdl(conv_wave_kernel, grid, kWaveThreads, r->smem, s, pdl, P);
+    launch_pdl(conv_wave_kernel, grid, kWaveThreads2, r->smem, s, pdl, P);
     return;
   }
   cudaFuncSetAttribute(conv_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)r->smem);
