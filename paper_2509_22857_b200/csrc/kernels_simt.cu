@@ -3,6 +3,7 @@
 // dense layer, and standalone elementwise/pool kernels so every node kind of
 // the graph IR runs on the GPU even when it is not fused.
 #include "kernels.cuh"
+#include "tc_ptx.cuh"
 
 namespace pcnn {
 
@@ -254,107 +255,141 @@ void launch_conv_simt(const ConvArgs& a, cudaStream_t s) {
 // ---------------------------------------------------------------------------
 // dense layer: out[b][k] = W[k] . view(b) + bias[k]  [-> poly]
 // view: vector, flatten of a blocked spatial tensor (C-major), or global sum.
-// Block = 8 warps over 32 outputs x 16 images; X tile staged in smem.
+// Block = 16 outputs x 16 images (one thread each); the block's 16 weight
+// rows and 16 input views are staged in shared memory with every thread's
+// loads in flight at once (the layer is a few latency-bound round trips, not
+// arithmetic: 512 -> 1000 for 64 images is 33 M MACs), then each thread runs
+// its dot product from shared memory (rows padded by one float: the 16
+// images a half-warp reads sit in different banks).
 // ---------------------------------------------------------------------------
+constexpr int kLinO = 16, kLinB = 16, kLinK = 1024;  // K staged in chunks of kLinK
+
+__device__ __forceinline__ float linear_view(const LinearArgs& a, int b, int j, float div) {
+  const TensorView& in = a.in;
+  if (a.in_mode == 0) return __ldg(in.base + (int64_t)b * in.cpad() + j);
+  const int hw = in.h * in.w;
+  if (a.in_mode == 1) {
+    const int c = j / hw, r = j - c * hw;
+    return __ldg(in.at(b, c, r / in.w, r % in.w));
+  }
+  const float* p = in.at(b, j, 0, 0);
+  float s = 0.f;
+  for (int q = 0; q < hw; ++q) s += __ldg(p + (int64_t)q * in.cb);
+  return s * div;
+}
+
 __global__ void __launch_bounds__(256) linear_kernel(LinearArgs a) {
   TlScope tls(a.tl);
-  extern __shared__ float xs[];  // [16][n_in]
-  constexpr int BB = 16;
-  const int b0 = blockIdx.y * BB;
-  const int n = a.n_in;
-  const TensorView& in = a.in;
-  const int hw = in.h * in.w;
+  extern __shared__ __align__(16) float sm[];
+  __shared__ __align__(8) uint64_t bar;
+  const int n = a.n_in, kc = n < kLinK ? n : kLinK, ld = (kc + 4) & ~3;  // rows 16-byte aligned
+  float* ws = sm;                 // [kLinO][ld]
+  float* xs = sm + kLinO * ld;    // [kLinB][ld]
+  const int o0 = blockIdx.x * kLinO, b0 = blockIdx.y * kLinB;
   const float div = a.in_div ? __ldg(a.in_div) : 1.f;
-  if (a.in_mode == 0) {
-    // vector input: eight loads per thread in flight, then the stores
-    for (int e0 = threadIdx.x; e0 < BB * n; e0 += 8 * blockDim.x) {
-      float v8[8];
+  // contiguous rows (vector input or a 1 x 1 flatten, whole K in one chunk,
+  // 16-byte aligned rows): every weight row and input row is one bulk copy,
+  // all in flight at once -- one memory round trip for the block
+  const bool vec = a.in_mode == 0 || (a.in_mode == 1 && a.in.h * a.in.w == 1);
+  const bool bulk = vec && kc == n && (n % 4) == 0 && (a.in.cpad() % 4) == 0 &&
+                    ((reinterpret_cast<uintptr_t>(a.w) | reinterpret_cast<uintptr_t>(a.in.base)) & 15) == 0;
+  // thread (output ko, image bi): bi fastest, so a warp is 2 outputs x 16 images
+  const int bi = threadIdx.x & (kLinB - 1), ko = threadIdx.x >> 4;
+  float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
+  if (bulk) {
+    const int no = a.n_out - o0 < kLinO ? a.n_out - o0 : kLinO;
+    const int nb = a.batch - b0 < kLinB ? a.batch - b0 : kLinB;
+    if (threadIdx.x == 0) {
+      ptx::mbar_init(ptx::smem_u32(&bar), 1);
+      ptx::fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const uint32_t rb = (uint32_t)n * 4u;
+      if (threadIdx.x == 0) ptx::mbar_arrive_tx(ptx::smem_u32(&bar), (uint32_t)((no > 0 ? no : 0) + nb) * rb);
+      __syncwarp();
+      const int r = threadIdx.x;
+      if (r < kLinO && r < no)
+        ptx::bulk_g2s(ptx::smem_u32(ws + r * ld), a.w + (int64_t)(o0 + r) * n, rb, ptx::smem_u32(&bar));
+      else if (r >= kLinO && r - kLinO < nb)
+        ptx::bulk_g2s(ptx::smem_u32(xs + (r - kLinO) * ld), a.in.base + (int64_t)(b0 + r - kLinO) * a.in.cpad(), rb,
+                      ptx::smem_u32(&bar));
+    }
+    // rows past n_out / the batch: zeros
+    for (int e = threadIdx.x; e < (kLinO - (no > 0 ? no : 0)) * ld; e += blockDim.x) ws[(no > 0 ? no : 0) * ld + e] = 0.f;
+    for (int e = threadIdx.x; e < (kLinB - nb) * ld; e += blockDim.x) xs[nb * ld + e] = 0.f;
+    ptx::mbar_wait(ptx::smem_u32(&bar), 0);
+    __syncthreads();
+    const float* wr = ws + ko * ld;
+    const float* xr = xs + bi * ld;
+    for (int j = 0; j + 4 <= n; j += 4) {
+      const float4 w4 = *reinterpret_cast<const float4*>(wr + j), x4 = *reinterpret_cast<const float4*>(xr + j);
+      acc0 = fmaf(w4.x, x4.x, acc0);
+      acc1 = fmaf(w4.y, x4.y, acc1);
+      acc2 = fmaf(w4.z, x4.z, acc2);
+      acc3 = fmaf(w4.w, x4.w, acc3);
+    }
+  } else
+  for (int k0 = 0; k0 < n; k0 += kc) {
+    const int m = n - k0 < kc ? n - k0 : kc;
+    if (k0) __syncthreads();
+    // weights: rows o0 .. o0 + 15 (zero past n_out), eight loads in flight per thread
+    for (int e0 = threadIdx.x; e0 < kLinO * m; e0 += 8 * blockDim.x) {
+      float v[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int e = e0 + u * blockDim.x;
-        const int bb = e / n, j = e - bb * n;
-        v8[u] = (e < BB * n && b0 + bb < a.batch) ? __ldg(in.base + (int64_t)(b0 + bb) * in.cpad() + j) : 0.f;
+        const int r = e / m, j = e - r * m;
+        v[u] = (e < kLinO * m && o0 + r < a.n_out) ? __ldg(a.w + (int64_t)(o0 + r) * n + k0 + j) : 0.f;
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int e = e0 + u * blockDim.x;
-        if (e < BB * n) xs[e] = v8[u];
+        if (e < kLinO * m) ws[(e / m) * ld + e % m] = v[u];
       }
     }
-  }
-  for (int e = threadIdx.x; e < BB * n && a.in_mode != 0; e += blockDim.x) {
-    int bb = e / n, j = e - bb * n;
-    int b = b0 + bb;
-    float v = 0.f;
-    if (b < a.batch) {
-      if (a.in_mode == 1) {
-        int c = j / hw, r = j - c * hw;
-        int y = r / in.w, xw = r - y * in.w;
-        v = *in.at(b, c, y, xw);
-      } else {
-        const float* p = in.at(b, j, 0, 0);
-        float s = 0.f;
-        for (int q = 0; q < hw; ++q) s += p[(int64_t)q * in.cb];
-        v = s * div;
-      }
-    }
-    xs[e] = v;
-  }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int kk = warp; kk < 32; kk += 8) {
-    int k = blockIdx.x * 32 + kk;
-    if (k >= a.out_stride) break;
-    if (k >= a.n_out) {  // zero the padded channels
-      if (lane < BB && b0 + lane < a.batch) a.out[(int64_t)(b0 + lane) * a.out_stride + k] = 0.f;
-      continue;
-    }
-    const float* wr = a.w + (int64_t)k * n;
-    float acc[BB];
-#pragma unroll
-    for (int i = 0; i < BB; ++i) acc[i] = 0.f;
-    // eight weights per lane in flight before the FMAs (the loop was bound by
-    // one dependent global load per 16 FMAs)
-    for (int j0 = 0; j0 < n; j0 += 32 * 8) {
-      float wv[8];
+    // inputs: images b0 .. b0 + 15 (zero past the batch)
+    for (int e0 = threadIdx.x; e0 < kLinB * m; e0 += 8 * blockDim.x) {
+      float v[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int j = j0 + u * 32 + lane;
-        wv[u] = j < n ? __ldg(wr + j) : 0.f;
+        const int e = e0 + u * blockDim.x;
+        const int bb = e / m, j = e - bb * m;
+        v[u] = (e < kLinB * m && b0 + bb < a.batch) ? linear_view(a, b0 + bb, k0 + j, div) : 0.f;
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int j = j0 + u * 32 + lane;
-        if (j < n) {
-#pragma unroll
-          for (int i = 0; i < BB; ++i) acc[i] = fmaf(wv[u], xs[i * n + j], acc[i]);
-        }
+        const int e = e0 + u * blockDim.x;
+        if (e < kLinB * m) xs[(e / m) * ld + e % m] = v[u];
       }
     }
-#pragma unroll
-    for (int i = 0; i < BB; ++i) {
-#pragma unroll
-      for (int o = 16; o; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+    __syncthreads();
+    const float* wr = ws + ko * ld;
+    const float* xr = xs + bi * ld;
+    int j = 0;
+    for (; j + 4 <= m; j += 4) {
+      acc0 = fmaf(wr[j], xr[j], acc0);
+      acc1 = fmaf(wr[j + 1], xr[j + 1], acc1);
+      acc2 = fmaf(wr[j + 2], xr[j + 2], acc2);
+      acc3 = fmaf(wr[j + 3], xr[j + 3], acc3);
     }
-    if (lane < BB) {
-      float v = acc[0];
-#pragma unroll
-      for (int i = 1; i < BB; ++i)
-        if (lane == i) v = acc[i];
-      int b = b0 + lane;
-      if (b < a.batch) {
-        v += __ldg(a.bias + k);
-        if (a.poly_deg) v = horner(a.poly, a.poly_stride, a.poly_deg, k, v);
-        a.out[(int64_t)b * a.out_stride + k] = v;
-        if (a.out2) a.out2[(int64_t)b * a.n_out + k] = v;
-      }
-    }
+    for (; j < m; ++j) acc0 = fmaf(wr[j], xr[j], acc0);
   }
+  const int k = o0 + ko, b = b0 + bi;
+  if (b >= a.batch || k >= a.out_stride) return;
+  if (k >= a.n_out) {  // zero the padded channels
+    a.out[(int64_t)b * a.out_stride + k] = 0.f;
+    return;
+  }
+  float v = (acc0 + acc1) + (acc2 + acc3) + __ldg(a.bias + k);
+  if (a.poly_deg) v = horner(a.poly, a.poly_stride, a.poly_deg, k, v);
+  a.out[(int64_t)b * a.out_stride + k] = v;
+  if (a.out2) a.out2[(int64_t)b * a.n_out + k] = v;
 }
 
 void launch_linear(const LinearArgs& a, cudaStream_t s) {
-  dim3 grid((unsigned)((a.out_stride + 31) / 32), (unsigned)((a.batch + 15) / 16));
-  size_t smem = (size_t)16 * a.n_in * sizeof(float);
+  dim3 grid((unsigned)((a.out_stride + kLinO - 1) / kLinO), (unsigned)((a.batch + kLinB - 1) / kLinB));
+  const size_t smem = (size_t)(kLinO + kLinB) * ((((a.n_in < kLinK ? a.n_in : kLinK) + 4) & ~3)) * sizeof(float);
   if (smem > 48 * 1024) cudaFuncSetAttribute(linear_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   linear_kernel<<<grid, 256, smem, s>>>(a);
 }
