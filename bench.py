@@ -279,6 +279,10 @@ def roofline(eng, plan, batch, ts: TimelineStats, ms_per_step, config):
             "peak_basis": f"{basis} bf16_tflops {bf16} (tensor: /3 for fp16x2, /6 for 3xTF32); hbm_gbs {hbm}"
                           + (f"; fp32 CUDA-core FMA peak {SIMT_FP32_TFLOPS:.1f} (derived)" if dom == KERNEL_NAMES[7] else ""),
             "ncu": ncu,
+            "note": ("image-resident runs: the bytes term above counts every layer's input and output once "
+                     "(SURVEY 8d), but the run keeps intermediate tensors in shared memory -- ncu DRAM traffic per "
+                     "launch is 'traffic'; frac_tensor is the binding measure for this family")
+            if dom == KERNEL_NAMES[6] else None,
             "step": {"roofline_time_us": round(step_roof * 1e6, 1), "frac": round(step_roof * 1e3 / ms_per_step, 4),
                      "formula": "sum over conv layers of max(FLOP/P_kernel, bytes/BW) / measured ms_per_step"},
             "families_ms_per_step": {k: round(v, 4) for k, v in sorted(fam_ms.items(), key=lambda kv: -kv[1])}}

@@ -10,9 +10,7 @@ python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_o
 python bench.py > gpurun_out/${tag}_default_bench.json 2> gpurun_out/${tag}_default_bench.err; tail -c 400 gpurun_out/${tag}_default_bench.json
 python bench.py --impl reference > gpurun_out/${tag}_reference_bench.json 2> gpurun_out/${tag}_reference_bench.err
 for c in lenet5 resnet20_deg8 vgg11 resnet18; do
-  python bench.py --config $c > gpurun_out/${tag}_${c}_bench.json 2> gpurun_out/${tag}_${c}_bench.err
+  python bench.py --config $c --secondary "" > gpurun_out/${tag}_${c}_bench.json 2> gpurun_out/${tag}_${c}_bench.err
 done
-PCNN_TC_DEBUG=64 python tools/cta_times.py resnet20 > gpurun_out/${tag}_resnet20_cta_times.txt 2>&1
-PCNN_TC_DEBUG=64 python tools/cta_times.py resnet18 > gpurun_out/${tag}_resnet18_cta_times.txt 2>&1
-bash tools/profile_round.sh resnet20 $tag conv_ss 2 > gpurun_out/${tag}_prof20.log 2>&1; tail -1 gpurun_out/${tag}_prof20.log
+bash tools/profile_round.sh resnet20 $tag conv_wave 0 > gpurun_out/${tag}_prof20.log 2>&1; tail -1 gpurun_out/${tag}_prof20.log
 bash tools/profile_round.sh resnet18 $tag conv_ss 14 > gpurun_out/${tag}_prof18.log 2>&1; tail -1 gpurun_out/${tag}_prof18.log

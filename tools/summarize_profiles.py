@@ -24,6 +24,10 @@ PROF = ROOT / "profiles"
 
 # ncu kernel name -> bench.py KERNEL_NAMES display name
 def display(name):
+    if "conv_blk_kernel" in name or "conv_wave_kernel" in name:
+        return "conv_blk_kernel (fp16x2, image-resident runs)"
+    if "net_kernel" in name:
+        return "net_kernel (whole network in one launch, fp32 CUDA cores)"
     if "conv_ss_kernel" in name:
         return "conv_ss_kernel (fp16x2, halo tiles in smem)"
     if "conv_tc_kernel" in name:
@@ -49,7 +53,8 @@ def launches(tag, cfg):
     by = defaultdict(lambda: [0, 0.0])
     for r in rows:
         k = r["Kernel Name"].split("(")[0].strip()
-        if "conv_tc_kernel" in r["Kernel Name"] or "conv_ss_kernel" in r["Kernel Name"]:
+        if any(t in r["Kernel Name"] for t in ("conv_tc_kernel", "conv_ss_kernel", "conv_blk_kernel", "conv_wave_kernel",
+                                                "net_kernel")):
             k = display(r["Kernel Name"])
         v = float(r["Metric Value"].replace(",", ""))
         unit = r["Metric Unit"]
@@ -151,10 +156,13 @@ def main():
         launches(tag, cfg)
         traffic(tag, cfg, table)
         full(tag, cfg, summary)
-        conv = [k for k in table.get(cfg, {}) if "conv_ss" in k]
+        # the family of the fully captured launch (the config's dominant kernel)
+        fam = display(summary.get(cfg, {}).get("kernel", "conv_ss_kernel"))
+        conv = [k for k in table.get(cfg, {}) if k == fam]
         if cfg in summary and conv:
             summary[cfg]["dram_bytes_per_launch"] = table[cfg][conv[0]]
-            summary[cfg]["dram_source"] = f"profiles/{tag}_{cfg}_traffic.csv (mean over the conv_ss launches of one forward)"
+            summary[cfg]["dram_source"] = (f"profiles/{tag}_{cfg}_traffic.csv (mean over the {fam.split(' ')[0]} "
+                                           "launches of one forward)")
         src = OUT / f"{tag}_{cfg}_plain.json"
         if src.exists():
             shutil.copy(src, PROF / src.name)
