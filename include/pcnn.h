@@ -263,13 +263,19 @@ typedef struct pcnn_plan_options {
                                copyout; <= 2 M MACs per image) runs as ONE
                                launch, every CTA keeping whole images in
                                shared memory between the units            */
-  int64_t ss_wide;          /* 1: the halo-tile producer warp issues a
+  int64_t ss_wide;          /* the halo-tile producer warp issues a
                                stage's bulk copies from several lanes at
-                               once (one lane pays ~300 cycles per copy)   */
+                               once (one lane pays ~300 cycles per copy):
+                               1 on tiles of <= 64 channels, 2 always,
+                               0 never                                     */
   int64_t epi_pairs;        /* halo-tile kernel epilogue warpgroup pairs:
                                2 (four warpgroups, pairs alternate tiles)
                                or 1                                        */
-  int64_t reserved[5];
+  int64_t ss_pair;          /* 1: 128-channel halo tiles run on CTA pairs
+                               (cluster of two, tcgen05 cta_group::2,
+                               M = 256 over two SMs, each SM staging half
+                               of the tile's weights); 0: one CTA per tile */
+  int64_t reserved[4];
 } pcnn_plan_options;
 
 /* ---- entry points --------------------------------------------------------*/

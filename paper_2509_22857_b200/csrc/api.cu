@@ -292,7 +292,7 @@ void enqueue_unit(pcnn_plan* p, int ui, const float* x, float* logits, cudaStrea
   unsigned long long* tl = p->tl_dev ? p->tl_dev + 2 * ui : nullptr;
   switch (u.kind) {
     case PCNN_UNIT_INGEST:
-      launch_ingest(x, p->views[u.out], p->batch, (u.flags & PCNN_FLAG_S2D) != 0, s, tl);
+      launch_ingest(x, p->views[u.out], p->batch, (u.flags & PCNN_FLAG_S2D) != 0, s, (int)p->opt.pdl, tl);
       break;
     case PCNN_UNIT_CONV: {
       if (p->fused[ui]) break;  // computed by the previous unit's launch
@@ -332,7 +332,7 @@ void enqueue_unit(pcnn_plan* p, int ui, const float* x, float* logits, cudaStrea
       if (p->has_post_pool[ui]) {
         EltArgs e = p->post_pool[ui];
         e.tl = tl;
-        launch_eltwise(e, s);
+        launch_eltwise(e, s, (int)p->opt.pdl);
       }
       break;
     }
@@ -353,12 +353,12 @@ void enqueue_unit(pcnn_plan* p, int ui, const float* x, float* logits, cudaStrea
       a.out_stride = p->views[u.out].cpad();
       if (ui + 1 < (int)p->fused.size() && p->fused[ui + 1]) a.out2 = logits;
       a.tl = tl;
-      launch_linear(a, s);
+      launch_linear(a, s, (int)p->opt.pdl);
       break;
     }
     case PCNN_UNIT_COPYOUT: {
       if (p->fused[ui]) break;  // the linear unit before it wrote the logits
-      launch_copyout(p->views[u.in], logits, p->batch, s, tl);
+      launch_copyout(p->views[u.in], logits, p->batch, s, tl, 0);  // plain: a tiny grid launched early would crowd the dense layer's blocks
       break;
     }
     default: {
@@ -377,7 +377,7 @@ void enqueue_unit(pcnn_plan* p, int ui, const float* x, float* logits, cudaStrea
       a.axis = (int)u.pool_order;
       a.pool = (int)u.pool;
       a.tl = tl;
-      launch_eltwise(a, s);
+      launch_eltwise(a, s, (int)p->opt.pdl);
       break;
     }
   }
@@ -957,6 +957,7 @@ void pcnn_plan_options_default(pcnn_plan_options* o) {
   o->fused_net = 1;
   o->ss_wide = 1;
   o->epi_pairs = 2;
+  o->ss_pair = 1;
 }
 
 int pcnn_plan_create(const pcnn_unit_desc* units, int n_units, const pcnn_tensor_desc* tensors, int n_tensors,
@@ -988,6 +989,7 @@ int pcnn_plan_create_ex(const pcnn_unit_desc* units, int n_units, const pcnn_ten
   p->kopt.ss_wres = (int)p->opt.ss_wres;
   p->kopt.ss_wide = (int)p->opt.ss_wide;
   p->kopt.epi_pairs = (int)p->opt.epi_pairs;
+  p->kopt.ss_pair = (int)(p->opt.ss_pair && !p->opt.flag_sync);
   p->kopt.tc_stage = (int)p->opt.tc_stage;
   p->kopt.proj_fuse = (int)p->opt.fuse_projection;
   p->kopt.streamk = (int)p->opt.streamk;

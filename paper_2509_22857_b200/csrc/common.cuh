@@ -386,10 +386,17 @@ __device__ __forceinline__ void tl_mark(unsigned long long* tl, int end) {
     else atomicMax(tl, ~t);
   }
 }
-// start mark at construction, end mark when the kernel body returns (thread 0)
+// start mark at construction, end mark when the kernel body returns (thread 0).
+// Kernels using it may be launched with programmatic stream serialization:
+// the construction waits for the previous grid (no-op on a plain launch) and
+// lets the next grid's CTAs start their prologue on the SMs this one leaves.
 struct TlScope {
   unsigned long long* tl;
-  __device__ __forceinline__ explicit TlScope(unsigned long long* p) : tl(p) { tl_mark(tl, 0); }
+  __device__ __forceinline__ explicit TlScope(unsigned long long* p) : tl(p) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    tl_mark(tl, 0);
+  }
   __device__ __forceinline__ ~TlScope() { tl_mark(tl, 1); }
 };
 

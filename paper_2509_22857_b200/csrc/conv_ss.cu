@@ -25,6 +25,8 @@
 // Warp roles (320 threads, persistent, one CTA per SM): warps 0-3 / 4-7
 // epilogue warpgroups (one per accumulator buffer), warp 8 TMEM allocator +
 // bulk-copy producer, warp 9 MMA issuer.
+#include <cuda.h>
+
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -46,7 +48,12 @@ constexpr int kMaxStages = 8;
 constexpr int kMaxPartials = 4;
 constexpr int kAddsPerPartial = 96;
 
+struct alignas(64) SsTmap {
+  uint64_t v[16];  // CUtensorMap (opaque 128 bytes)
+};
+
 struct SsParams {
+  SsTmap wmap;           // pair mode: 4-D map of the weight image (first member: 64-byte aligned)
   ConvArgs a;
   int mt;                // 128-row sub-tiles per tile (two for small N: halves the per-tile hand-offs)
   EpiTab etab;
@@ -83,6 +90,15 @@ struct SsParams {
                          // same shared-border geometry as the input grid)
   int fold_skip, fold_out;  // storage scales folded into the epilogue table (epi_fill_tab)
   int wide;  // producer: the warp's lanes issue a stage's bulk copies in parallel
+  // CTA pair (cta_group::2, cluster of two): one M = 256 tile over two SMs,
+  // each CTA staging its own 128 positions and HALF of the tile's weight rows
+  // (bn = nt / 2, one 4-D TMA box from wmap), the leader issuing M = 256 MMAs
+  // whose accumulators land in both CTAs' TMEM: the weight bytes every SM
+  // pulls through L2 per tile halve.  The peer's MMA warp relays its stage
+  // hand-offs to the leader (full2), the peer's epilogue releases the
+  // leader's accumulator buffers remotely.
+  int pair;
+  int bn;    // weight rows staged per CTA: nt, or nt / 2 in pair mode
   int dbg;
   int time_slot;         // PCNN_TC_DEBUG bit 64: per-CTA globaltimer stamps slot, else -1
   // wres: the whole weight image (one n-tile, every chunk) stays resident in
@@ -160,6 +176,7 @@ struct Smem {
   uint64_t full[kMaxStages], empty[kMaxStages];
   uint64_t acc_full[kMaxAcc], acc_empty[kMaxAcc];
   uint64_t wfull[kMaxWChunks];  // resident weights: chunk q landed
+  uint64_t full2[kMaxStages];   // pair mode, leader: the peer's stage landed (relayed by its MMA warp)
   uint32_t tstored[kSigRing];  // flag mode: draining warps done with a tile (monotonic per slot)
   uint32_t tmem_base;
   int dep_seq;     // flag mode: this CTA's tiles whose producer tiles were acquired
@@ -187,7 +204,19 @@ __device__ __forceinline__ void mma_f16_ss_if(uint32_t e, uint32_t d, uint64_t a
                ::"r"(e), "r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc)
                : "memory");
 }
-template <int TAPS>
+__device__ __forceinline__ void mma_f16_ss2_if(uint32_t e, uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                               uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p, q;\n\tsetp.ne.b32 q, %0, 0;\n\tsetp.ne.b32 p, %5, 0;\n\t"
+               "@q tcgen05.mma.cta_group::2.kind::f16 [%1], %2, %3, %4, p;\n\t}"
+               ::"r"(e), "r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc)
+               : "memory");
+}
+template <bool PAIR>
+__device__ __forceinline__ void mma_ss(uint32_t e, uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if constexpr (PAIR) mma_f16_ss2_if(e, d, a, b, idesc, acc);
+  else mma_f16_ss_if(e, d, a, b, idesc, acc);
+}
+template <int TAPS, bool PAIR = false>
 __device__ __forceinline__ void ss_stage(bool concat, uint32_t dm, uint32_t dc, uint64_t ah, uint64_t al,
                                              uint64_t b, uint64_t bstep, uint64_t blo, uint32_t id2, uint32_t id1,
                                              uint32_t accm, uint32_t accc, const uint64_t* o) {
@@ -195,15 +224,15 @@ __device__ __forceinline__ void ss_stage(bool concat, uint32_t dm, uint32_t dc, 
   if (concat) {
 #pragma unroll
     for (int t = 0; t < TAPS; ++t) {
-      mma_f16_ss_if(e, dm, ah + o[t], b + t * bstep, id2, t ? 1u : accm);
-      mma_f16_ss_if(e, dc, al + o[t], b + t * bstep, id1, 1u);
+      mma_ss<PAIR>(e, dm, ah + o[t], b + t * bstep, id2, t ? 1u : accm);
+      mma_ss<PAIR>(e, dc, al + o[t], b + t * bstep, id1, 1u);
     }
   } else {
 #pragma unroll
     for (int t = 0; t < TAPS; ++t) {
-      mma_f16_ss_if(e, dc, al + o[t], b + t * bstep, id1, t ? 1u : accc);
-      mma_f16_ss_if(e, dc, ah + o[t], b + t * bstep + blo, id1, 1u);
-      mma_f16_ss_if(e, dm, ah + o[t], b + t * bstep, id1, t ? 1u : accm);
+      mma_ss<PAIR>(e, dc, al + o[t], b + t * bstep, id1, t ? 1u : accc);
+      mma_ss<PAIR>(e, dc, ah + o[t], b + t * bstep + blo, id1, 1u);
+      mma_ss<PAIR>(e, dm, ah + o[t], b + t * bstep, id1, t ? 1u : accm);
     }
   }
 }
@@ -248,7 +277,7 @@ __device__ __forceinline__ Band band_of(const SsParams& P) {
 __device__ __forceinline__ bool seg_at(int i, int total_tiles, int nq, bool streamk, Seg& s);
 
 // segment i of this CTA in any mode (whole tiles, stream-K, bands)
-template <bool BAND>
+template <bool BAND, bool PAIR = false>
 __device__ __forceinline__ bool seg_get(const SsParams& P, const Band& bd, int i, int total_tiles, bool streamk,
                                         Seg& s) {
   if constexpr (BAND) {
@@ -263,6 +292,22 @@ __device__ __forceinline__ bool seg_get(const SsParams& P, const Band& bd, int i
     s.r = bd.r0 + local * P.brows;
     s.rows = min(P.brows, bd.r1 - s.r + 1);
     s.g0 = 1 + (int64_t)s.r * P.wp;
+    return true;
+  }
+  if constexpr (PAIR) {
+    // pair tile pt = (n_tile, m-tile pair) walked by cluster; rank r takes m-tile 2 m + r
+    const int ncl = (int)gridDim.x >> 1, mp = P.m_tiles >> 1;
+    const int pt = ((int)blockIdx.x >> 1) + i * ncl;
+    if (pt >= mp * P.n_tiles) return false;
+    s.n_tile = pt / mp;
+    const int m = 2 * (pt - s.n_tile * mp) + ((int)blockIdx.x & 1);
+    s.tile = s.n_tile * P.m_tiles + m;
+    s.q0 = 0;
+    s.q1 = P.nq;
+    s.owner = 1;
+    s.c_lo = -1;
+    s.g0 = (int64_t)m * kTileM;
+    s.r = s.rows = 0;
     return true;
   }
   if (!seg_at(i, total_tiles, P.nq, streamk, s)) return false;
@@ -557,7 +602,7 @@ constexpr int kPoolNone = 0, kPoolBand = 2;
 template <int PAIRS>
 constexpr int ss_threads() { return PAIRS == 2 ? 576 : 320; }
 
-template <int TAPS, bool SK, int POOL, int PAIRS = 1>
+template <int TAPS, bool SK, int POOL, int PAIRS = 1, bool PAIR = false>
 __global__ void __launch_bounds__(ss_threads<PAIRS>(), 1) conv_ss_kernel(const __grid_constant__ SsParams P) {
   constexpr bool BAND = POOL == kPoolBand;
   constexpr int kThreads = ss_threads<PAIRS>();
@@ -588,14 +633,19 @@ __global__ void __launch_bounds__(ss_threads<PAIRS>(), 1) conv_ss_kernel(const _
     }
     for (int i = 0; i < kMaxAcc; ++i) {
       ptx::mbar_init(ptx::smem_u32(&S->acc_full[i]), 1);
-      ptx::mbar_init(ptx::smem_u32(&S->acc_empty[i]), P.share_epi ? 8 : 4);  // one arrive per draining warp
+      // one arrive per draining warp (pair mode, leader: of both CTAs)
+      ptx::mbar_init(ptx::smem_u32(&S->acc_empty[i]), (P.share_epi ? 8 : 4) * (PAIR ? 2 : 1));
     }
+    for (int i = 0; i < kMaxStages; ++i) ptx::mbar_init(ptx::smem_u32(&S->full2[i]), 1);
     for (int i = 0; i < kMaxWChunks; ++i) ptx::mbar_init(ptx::smem_u32(&S->wfull[i]), 1);
     for (int i = 0; i < kSigRing; ++i) S->tstored[i] = 0;
     S->dep_seq = 0;
     ptx::fence_mbar_init();
   }
-  if (warp == kWarpProducer) ptx::tmem_alloc(ptx::smem_u32(&S->tmem_base), P.tmem_cols);
+  if (warp == kWarpProducer) {
+    if constexpr (PAIR) ptx::tmem_alloc2(ptx::smem_u32(&S->tmem_base), P.tmem_cols);
+    else ptx::tmem_alloc(ptx::smem_u32(&S->tmem_base), P.tmem_cols);
+  }
   epi_fill_tab(a.epi, P.etab, ptab, threadIdx.x, kThreads, P.fold_skip ? a.epi.skip.sload : 1.f,
                P.fold_out ? a.epi.out.sstore : 1.f);
   float* ptab_p = ptab + P.etab.rows * a.epi.npad;  // projection table (P.proj)
@@ -620,6 +670,7 @@ __global__ void __launch_bounds__(ss_threads<PAIRS>(), 1) conv_ss_kernel(const _
   }
   ptx::tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) ptx::cluster_sync();  // the peer's barriers exist before any remote arrive
   ptx::tc_fence_after();
   const uint32_t tmem = S->tmem_base;
   // resident weights: parameters, not written by the previous kernel, so the
@@ -645,7 +696,49 @@ __global__ void __launch_bounds__(ss_threads<PAIRS>(), 1) conv_ss_kernel(const _
   if (warp == kWarpProducer) {
     // ===== producer: per (tile, 16-channel chunk) one stage = the tile's
     // input range for both planes and both 8-channel groups + the weights =====
-    if (!BAND && P.wide) {
+    if constexpr (PAIR) {
+      // pair mode: own activation rows (lanes in parallel) + this CTA's half
+      // of the tile's weight rows as one 4-D TMA box ([tap][g, hi/lo][bn rows x 16 B])
+      const __half* hi = a.in.hi();
+      const __half* lo = a.in.lo();
+      const int rank = (int)(blockIdx.x & 1);
+      if (lane == 0) ptx::prefetch_tmap(&P.wmap);
+      int st = 0;
+      uint32_t ph = 0;
+      Seg sg;
+      Band bd = {};
+      for (int si = 0; seg_get<false, true>(P, bd, si, total_tiles, false, sg); ++si) {
+        const int64_t gs = sg.g0 - P.halo;
+        const int64_t cs = gs < 0 ? 0 : gs;
+        const int64_t ge = gs + P.span;
+        const int64_t ce = ge > P.gtotal ? P.gtotal : ge;
+        // an m-tile past the grid (odd m-tile count) stages weights only
+        const uint32_t slot0 = (uint32_t)(cs - gs) * 16, bytes = ce > cs ? (uint32_t)(ce - cs) * 16 : 0u;
+        for (int q = 0; q < P.nq; ++q) {
+          const uint32_t bar = ptx::smem_u32(&S->full[st]);
+          const uint32_t sb = base + st * P.stage_bytes;
+          const int ng = q == P.nq - 1 ? P.last_groups : 2;
+          if (lane == 0) {
+            ptx::mbar_wait_sleep(ptx::smem_u32(&S->empty[st]), ph ^ 1);
+            ptx::mbar_arrive_tx(bar, 2 * ng * P.nplanes * bytes + P.b_bytes);
+          }
+          __syncwarp();
+          const int na = 2 * ng * P.nplanes;
+          if (lane < na) {
+            if (bytes) {
+              const int pl = lane / (2 * ng), r = lane - pl * 2 * ng, g = r >> 1, hl = r & 1;
+              const int64_t off = (2 * q + g) * a.in.kstride + P.plane_id[pl] * a.in.pstride + cs * 8;
+              ptx::bulk_g2s(sb + pl * 4 * P.a_bytes + (hl * 2 + g) * P.a_bytes + slot0, (hl ? lo : hi) + off, bytes,
+                            bar);
+            }
+          } else if (lane == 31) {
+            ptx::tma_load_4d(sb + P.nplanes * 4 * P.a_bytes, &P.wmap, rank * P.bn * 4, 0, 0, sg.n_tile * P.nq + q, bar);
+          }
+          __syncwarp();
+          if (++st == P.stages) { st = 0; ph ^= 1; }
+        }
+      }
+    } else if (!BAND && P.wide) {
       // the whole warp walks the stages; lane 0 waits for the slot and posts
       // the byte count, then lane j issues copy j of the stage (a single
       // thread pays ~300 cycles per cp.async.bulk, tools/ubench_bulk.cu)
@@ -709,7 +802,7 @@ __global__ void __launch_bounds__(ss_threads<PAIRS>(), 1) conv_ss_kernel(const _
       Seg sg;
       Band bd = {};
       if constexpr (BAND) bd = band_of(P);
-      for (int si = 0; seg_get<BAND>(P, bd, si, total_tiles, streamk, sg); ++si) {
+      for (int si = 0; seg_get<BAND, PAIR>(P, bd, si, total_tiles, streamk, sg); ++si) {
         const int n_tile = sg.n_tile;
         const int64_t gs = sg.g0 - P.halo;  // grid position of buffer slot 0
         const int64_t cs = gs < 0 ? 0 : gs;
@@ -803,26 +896,44 @@ __global__ void __launch_bounds__(ss_threads<PAIRS>(), 1) conv_ss_kernel(const _
         }
       }
     }
+  } else if (PAIR && warp == kWarpMma && (blockIdx.x & 1)) {
+    // ===== pair mode, peer CTA: relay each landed stage to the leader =====
+    const uint32_t full2 = ptx::mapa(ptx::smem_u32(&S->full2[0]), 0);
+    int st = 0;
+    uint32_t ph = 0;
+    Seg sg;
+    Band bd = {};
+    for (int si = 0; seg_get<false, true>(P, bd, si, total_tiles, false, sg); ++si)
+      for (int q = 0; q < P.nq; ++q) {
+        if (lane == 0) {
+          ptx::mbar_wait(ptx::smem_u32(&S->full[st]), ph);
+          ptx::mbar_arrive_cluster(full2 + st * 8);
+        }
+        __syncwarp();
+        if (++st == P.stages) { st = 0; ph ^= 1; }
+      }
   } else if (warp == kWarpMma) {
     // ===== MMA issuer: whole warp, one elected lane issues; main products
-    // rotate over the NP partial accumulators per stage =====
-    const uint32_t idesc = ptx::idesc_f16(kTileM, P.nt);
-    const uint32_t idesc2 = ptx::idesc_f16(kTileM, 2 * P.nt);
-    const uint32_t a_lbo = P.a_bytes, b_lbo = 2 * P.nt * 16;
+    // rotate over the NP partial accumulators per stage (pair mode: the
+    // leader, M = 256 over both CTAs) =====
+    const uint32_t idesc = ptx::idesc_f16(PAIR ? 2 * kTileM : kTileM, P.nt);
+    const uint32_t idesc2 = ptx::idesc_f16(PAIR ? 2 * kTileM : kTileM, 2 * P.nt);
+    const uint32_t a_lbo = P.a_bytes, b_lbo = 2 * P.bn * 16;
     const bool do_mma = !(P.dbg & 2);
     // tap offsets in the descriptors' 16-byte address units
     uint64_t offs[TAPS];
 #pragma unroll
     for (int t = 0; t < TAPS; ++t) offs[t] = (uint64_t)P.toff[t];
-    const uint64_t bstep = (uint64_t)(64 * P.nt) >> 4, blo = (uint64_t)(P.nt * 16) >> 4;
+    const uint64_t bstep = (uint64_t)(64 * P.bn) >> 4, blo = (uint64_t)(P.bn * 16) >> 4;
     int st = 0;
     uint32_t ph = 0, acc = 0, acc_ph = 0;
     uint32_t w_seen = P.wres ? 0u : ~0u;  // resident chunks already waited for
     Seg sg;
     Band bd = {};
     if constexpr (BAND) bd = band_of(P);
-    for (int si = 0; seg_get<BAND>(P, bd, si, total_tiles, streamk, sg); ++si) {
-      ptx::mbar_wait(ptx::smem_u32(&S->acc_empty[acc]), acc_ph ^ 1);
+    for (int si = 0; seg_get<BAND, PAIR>(P, bd, si, total_tiles, streamk, sg); ++si) {
+      if constexpr (PAIR) ptx::mbar_wait_cluster(ptx::smem_u32(&S->acc_empty[acc]), acc_ph ^ 1);
+      else ptx::mbar_wait(ptx::smem_u32(&S->acc_empty[acc]), acc_ph ^ 1);
       ptx::tc_fence_after();
       const uint32_t d_tile = tmem + acc * P.mt * set_cols;
       int p = 0;
@@ -832,6 +943,7 @@ __global__ void __launch_bounds__(ss_threads<PAIRS>(), 1) conv_ss_kernel(const _
        for (int ps = 0; ps < nsub; ++ps) {
         tr(P, 1, 0x400 | q);
         ptx::mbar_wait(ptx::smem_u32(&S->full[st]), ph);
+        if constexpr (PAIR) ptx::mbar_wait_cluster(ptx::smem_u32(&S->full2[st]), ph);
         tr(P, 1, 0x500 | q);
         if (!((w_seen >> q) & 1u)) {
           ptx::mbar_wait(ptx::smem_u32(&S->wfull[q]), 0);
@@ -861,36 +973,38 @@ __global__ void __launch_bounds__(ss_threads<PAIRS>(), 1) conv_ss_kernel(const _
                 for (int t = 0; t < 4; ++t) o4[t] = (uint64_t)P.pl_toff[ps][t];
                 const int ntp = P.pl_ntaps[ps];
                 if (ntp == 4)
-                  ss_stage<4>(P.concat, dm, dc, a_hi + shift, a_lo + shift, b0, bstep, blo, idesc2, idesc, main_acc,
+                  ss_stage<4, PAIR>(P.concat, dm, dc, a_hi + shift, a_lo + shift, b0, bstep, blo, idesc2, idesc, main_acc,
                               corr_acc, o4);
                 else if (ntp == 2)
-                  ss_stage<2>(P.concat, dm, dc, a_hi + shift, a_lo + shift, b0, bstep, blo, idesc2, idesc, main_acc,
+                  ss_stage<2, PAIR>(P.concat, dm, dc, a_hi + shift, a_lo + shift, b0, bstep, blo, idesc2, idesc, main_acc,
                               corr_acc, o4);
                 else
-                  ss_stage<1>(P.concat, dm, dc, a_hi + shift, a_lo + shift, b0, bstep, blo, idesc2, idesc, main_acc,
+                  ss_stage<1, PAIR>(P.concat, dm, dc, a_hi + shift, a_lo + shift, b0, bstep, blo, idesc2, idesc, main_acc,
                               corr_acc, o4);
                 continue;
               }
             }
-            ss_stage<TAPS>(P.concat, dm, dc, a_hi + shift, a_lo + shift, b0, bstep, blo, idesc2, idesc, main_acc,
-                           corr_acc, offs);
+            ss_stage<TAPS, PAIR>(P.concat, dm, dc, a_hi + shift, a_lo + shift, b0, bstep, blo, idesc2, idesc,
+                                 main_acc, corr_acc, offs);
             if (proj) {
               // projection: the centre tap's A, its weights after the taps'
               const uint64_t po[1] = {(uint64_t)P.ptoff};
               const uint32_t pm = d_set + set_a;
               const uint64_t bp = b0 + ((uint64_t)P.b_bytes >> 4);
-              ss_stage<1>(P.concat, pm, pm + P.nt, a_hi + shift, a_lo + shift, bp, bstep, blo, idesc2, idesc,
+              ss_stage<1, PAIR>(P.concat, pm, pm + P.nt, a_hi + shift, a_lo + shift, bp, bstep, blo, idesc2, idesc,
                           q > q0 ? 1u : 0u, q > q0 ? 1u : 0u, po);
             }
           }
         }
-        ptx::mma_commit_warp(ptx::smem_u32(&S->empty[st]));
+        if constexpr (PAIR) ptx::mma_commit2_warp(ptx::smem_u32(&S->empty[st]), 3);
+        else ptx::mma_commit_warp(ptx::smem_u32(&S->empty[st]));
         tr(P, 1, 0x600 | q);
         if (++st == P.stages) { st = 0; ph ^= 1; }
        }
         if (++p == NP) p = 0;
       }
-      ptx::mma_commit_warp(ptx::smem_u32(&S->acc_full[acc]));
+      if constexpr (PAIR) ptx::mma_commit2_warp(ptx::smem_u32(&S->acc_full[acc]), 3);
+      else ptx::mma_commit_warp(ptx::smem_u32(&S->acc_full[acc]));
       if (++acc == (uint32_t)NB) { acc = 0; acc_ph ^= 1; }
     }
   } else if (warp < 8 * PAIRS) {
@@ -975,7 +1089,7 @@ __global__ void __launch_bounds__(ss_threads<PAIRS>(), 1) conv_ss_kernel(const _
       for (;;) {
         ++x.it;
         Seg sx;
-        if (!seg_get<BAND>(P, ebd, (int)x.it, total_tiles, streamk, sx)) return false;
+        if (!seg_get<BAND, PAIR>(P, ebd, (int)x.it, total_tiles, streamk, sx)) return false;
         x.tile = sx.tile;
         x.tn = sx.n_tile;
         x.g0 = sx.g0;
@@ -1077,9 +1191,13 @@ __global__ void __launch_bounds__(ss_threads<PAIRS>(), 1) conv_ss_kernel(const _
         }
         if (last_of_tile) {
           // the accumulators are in registers: release the buffer to the MMA warp
+          // (pair mode: the leader's)
           ptx::tc_fence_before();
           __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->acc_empty[acc]));
+          if (lane == 0) {
+            if constexpr (PAIR) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&S->acc_empty[acc]), 0));
+            else ptx::mbar_arrive(ptx::smem_u32(&S->acc_empty[acc]));
+          }
         }
         if (lane == 0 && warp == 0) tr(P, 2, 0xD00 | c0);
         float sk[16];
@@ -1181,7 +1299,10 @@ __global__ void __launch_bounds__(ss_threads<PAIRS>(), 1) conv_ss_kernel(const _
       } else if (last_of_tile) {
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&S->acc_empty[acc]));
+        if (lane == 0) {
+          if constexpr (PAIR) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&S->acc_empty[acc]), 0));
+          else ptx::mbar_arrive(ptx::smem_u32(&S->acc_empty[acc]));
+        }
       }
       if (last_of_tile && lane == 0 && warp == 0) tr(P, 2, 0x900);
       if (!have_next) break;
@@ -1194,10 +1315,13 @@ __global__ void __launch_bounds__(ss_threads<PAIRS>(), 1) conv_ss_kernel(const _
   }
   cta_stamp(P, 2);
   __syncthreads();
+  // pair mode: neither CTA leaves while the other may still arrive on its barriers
+  if constexpr (PAIR) ptx::cluster_sync();
   tl_mark(a.tl, 1);
   if (warp == kWarpProducer) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, P.tmem_cols);
+    if constexpr (PAIR) ptx::tmem_dealloc2(tmem, P.tmem_cols);
+    else ptx::tmem_dealloc(tmem, P.tmem_cols);
   }
   cta_stamp(P, 3);
 }
@@ -1215,9 +1339,10 @@ size_t ss_aux_bytes(const SsParams& P) {
 // nt: output channels per tile (the weight image is packed in tiles of
 // min(npad, 128) rows; a smaller nt copies its rows out of that image)
 static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub, bool allow_wres, int force_mt = 0,
-                              int max_np = 0, int pairs = 1) {
+                              int max_np = 0, int pairs = 1, int pair = 0) {
   const TensorView& in = a.in;
   P.epi_pairs = pairs;
+  P.pair = pair;
   if (!a.f16 || !a.tcwss || !a.tc16_scale) return false;
   if ((a.stride != 1 && a.stride != 2) || a.kh != a.kw ||
       !((a.kh == 3 && a.pad == 1) || (a.kh == 1 && a.pad == 0) || (a.kh == 4 && a.pad == 1 && a.stride == 1)))
@@ -1248,6 +1373,8 @@ static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub,
   // and one set of hand-offs serve 256 positions
   P.mt = a.opt.ss_mt ? a.opt.ss_mt : (P.nt <= 32 ? 2 : 1);
   if (force_mt) P.mt = force_mt;
+  if (P.pair) P.mt = 1;
+  P.bn = P.pair ? P.nt / 2 : P.nt;
   P.band = 0;
   if (pooled) {
     P.band = 1;
@@ -1277,6 +1404,7 @@ static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub,
   if (P.mt < 1 || P.mt > 4) P.mt = 1;
   const int tm = kTileM * P.mt;
   P.m_tiles = (int)((P.gtotal + tm - 1) / tm);
+  if (P.pair) P.m_tiles = (P.m_tiles + 1) & ~1;  // whole pairs (a last odd m-tile's partner stores nothing)
   P.nq = (cpad + 15) / 16;
   P.last_groups = cpad % 16 == 0 ? 2 : 1;
   P.taps = a.kh * a.kw;
@@ -1344,7 +1472,7 @@ static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub,
   P.fold_skip = a.epi.residual >= 2 && a.epi.skip.split;
   P.fold_out = P.out_pos && (a.epi.poly_deg > 0 || a.epi.residual >= 2);
   P.a_bytes = (uint32_t)P.span * 16;
-  P.b_bytes = (uint32_t)(P.psub ? 4 : P.taps) * 64 * P.nt;  // psub: at most 4 taps per plane
+  P.b_bytes = (uint32_t)(P.psub ? 4 : P.taps) * 64 * P.bn;  // psub: at most 4 taps per plane
   P.proj = 0;
   P.pb_bytes = 0;
   if (a.proj) {
@@ -1374,7 +1502,7 @@ static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub,
   {
     const bool want = a.opt.ss_wres != 0;
     const uint32_t res = (uint32_t)P.nq * P.b_bytes, sa = P.nplanes * 4 * P.a_bytes;
-    if (want && allow_wres && !P.psub && !P.proj && P.b_img_nt == P.nt && P.n_tiles == 1 && P.nq <= kMaxWChunks &&
+    if (want && allow_wres && !P.pair && !P.psub && !P.proj && P.b_img_nt == P.nt && P.n_tiles == 1 && P.nq <= kMaxWChunks &&
         res < budget) {
       int st = (int)((budget - res) / sa);
       if (st > kMaxStages) st = kMaxStages;
@@ -1388,7 +1516,10 @@ static bool make_ss_params_nt(const ConvArgs& a, SsParams& P, int nt, bool psub,
   }
   if (P.stages < 2) return false;  // neither two streamed stages nor resident weights + two stages fit
   P.dbg = a.opt.dbg;
-  P.wide = a.opt.ss_wide && !P.psub && !P.band && !a.fin.mode && !a.fsk.mode;
+  // multi-lane issue pays on narrow tiles (RN20); on 128-channel tiles the
+  // one-lane producer measured faster (RN18 1106 -> 1087 us, VGG 393 -> 383)
+  P.wide = (a.opt.ss_wide == 2 || (a.opt.ss_wide == 1 && P.nt <= 64)) && !P.psub && !P.band && !a.fin.mode &&
+           !a.fsk.mode;
   P.time_slot = -1;
   // accumulators: as many partials as accuracy asks for, then two buffers
   // main products rotate over the partials per stage (taps MMAs each)
@@ -1443,6 +1574,17 @@ static bool make_ss_params_pairs(const ConvArgs& a, SsParams& P, bool allow_wres
 bool make_ss_params(const ConvArgs& a, SsParams& P, bool allow_wres = true) {
   SsParams P1 = P;
   if (!make_ss_params_pairs(a, P1, allow_wres, 1)) return false;
+  // CTA pairs for 128-channel tiles whose weights are re-staged per tile
+  // (RN18 stages 2-4, VGG's wide layers): halves every SM's weight traffic
+  if (a.opt.ss_pair && P1.nt == 128 && P1.b_img_nt == 128 && !P1.wres && !P1.psub && !P1.proj && !P1.band &&
+      P1.taps == 9 && P1.mt == 1 && P1.m_tiles >= 2 && !a.sk_flags && !a.sig_done && !a.fin.mode && !a.fsk.mode &&
+      !a.proj) {
+    SsParams Q = P;
+    if (make_ss_params_nt(a, Q, 128, false, false, 1, 0, 1, 1) && Q.stages >= 2) {
+      P = Q;
+      return true;
+    }
+  }
   if (a.opt.epi_pairs >= 2 && (P1.nt <= 32 || (P1.nt <= 64 && P1.proj)) && !P1.band && !a.sk_flags) {
     SsParams Q = P;
     if (make_ss_params_nt(a, Q, P1.nt, P1.psub != 0, allow_wres, 0, 0, 2) && Q.wres == P1.wres &&
@@ -2294,6 +2436,35 @@ bool conv_ss_supported(const ConvArgs& a) {
   return make_ss_params(a, P);
 }
 
+typedef CUresult (*SsEncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// pair mode: the weight image (tc_layout.cuh pack_tcss_weights_device, 128-row
+// tiles: [tile, chunk][tap][g, hi/lo][128 rows][8 fp16]) as a 4-D tensor of
+// 32-bit words; a box is one CTA's bn rows of every (tap, g, hi/lo) of a chunk
+static bool encode_weight_map(SsParams& P) {
+  static SsEncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* ptr = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess || !ptr)
+      return false;
+    fn = reinterpret_cast<SsEncodeTiledFn>(ptr);
+  }
+  // 4-byte elements, a 128-row block row = 128 x 16 B: the box's inner
+  // extent is one CTA's bn rows (1 KB contiguous), not one 16-byte row
+  const int INT = P.b_img_nt;
+  const cuuint64_t dims[4] = {(cuuint64_t)INT * 4, 4, (cuuint64_t)P.taps, (cuuint64_t)(P.a.npad / INT) * (cuuint64_t)P.nq};
+  const cuuint64_t strides[3] = {(cuuint64_t)INT * 16, (cuuint64_t)4 * INT * 16, (cuuint64_t)P.taps * 4 * INT * 16};
+  const cuuint32_t box[4] = {(cuuint32_t)P.bn * 4, 4, (cuuint32_t)P.taps, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(reinterpret_cast<CUtensorMap*>(&P.wmap), CU_TENSOR_MAP_DATA_TYPE_UINT32, 4,
+                  const_cast<__half*>(P.w), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 void launch_conv_ss(const ConvArgs& a, cudaStream_t s) {
   SsParams P;
   if (!make_ss_params(a, P)) return;
@@ -2322,6 +2493,38 @@ void launch_conv_ss(const ConvArgs& a, cudaStream_t s) {
   }
   const bool sk = a.sk_flags != nullptr;
   void (*k)(SsParams);
+  if (P.pair) {
+    if (!encode_weight_map(P)) {
+      // no tensor map: the one-CTA kernel
+      SsParams Q;
+      ConvArgs b = a;
+      b.opt.ss_pair = 0;
+      if (!make_ss_params(b, Q)) return;
+      launch_conv_ss(b, s);
+      return;
+    }
+    const int pairs = P.m_tiles / 2 * P.n_tiles;
+    const int ncl = pairs < nsm / 2 ? pairs : nsm / 2;
+    k = conv_ss_kernel<9, false, kPoolNone, 1, true>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (P.dbg & 64) P.time_slot = g_time_next++ % kTimeSlots;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * ncl);
+    cfg.blockDim = dim3(ss_threads<1>());
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = a.opt.pdl ? 2 : 1;
+    cudaLaunchKernelEx(&cfg, k, P);
+    return;
+  }
   if (P.band) {
     k = P.taps == 16 ? conv_ss_kernel<16, false, kPoolBand> : conv_ss_kernel<9, false, kPoolBand>;
   } else if (P.epi_pairs == 2) {

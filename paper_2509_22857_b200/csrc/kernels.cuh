@@ -28,7 +28,8 @@ struct KOpts {
   int ss_share = -1;    // shared epilogue (-1 auto)
   int ss_psub = -1;     // parity-plane stages (-1 auto)
   int ss_wres = 1;      // resident weights
-  int ss_wide = 1;      // halo-tile producer issues a stage's copies from many lanes
+  int ss_wide = 1;      // halo-tile producer issues a stage's copies from many lanes (1: narrow layers, 2: all)
+  int ss_pair = 1;      // halo-tile CTA pairs (cta_group::2) for 128-channel tiles
   int epi_pairs = 2;    // halo-tile epilogue warpgroup pairs (1 or 2)
   int tc_stage = 1;     // TMA-staged input boxes (TMEM-A kernel)
   int proj_fuse = 1;    // fused projections
@@ -105,23 +106,24 @@ inline int64_t host_pixel_count(const PixelMap& pm, int batch) {
 }
 
 // s2d: x is [B][C/4][2H][2W] and t holds it as 2x2 blocks, channel (dy*2+dx)*(C/4)+c
-void launch_ingest(const float* x, const TensorView& t, int batch, bool s2d, cudaStream_t s,
+void launch_ingest(const float* x, const TensorView& t, int batch, bool s2d, cudaStream_t s, int pdl,
                    unsigned long long* tl = nullptr);
 void launch_conv_simt(const ConvArgs& a, cudaStream_t s);
-void launch_linear(const LinearArgs& a, cudaStream_t s);
-void launch_eltwise(const EltArgs& a, cudaStream_t s);
-void launch_copyout(const TensorView& t, float* dst, int batch, cudaStream_t s, unsigned long long* tl = nullptr);
+void launch_linear(const LinearArgs& a, cudaStream_t s, int pdl = 0);
+void launch_eltwise(const EltArgs& a, cudaStream_t s, int pdl = 0);
+void launch_copyout(const TensorView& t, float* dst, int batch, cudaStream_t s, unsigned long long* tl = nullptr,
+                    int pdl = 0);
 
 // Launch a persistent tcgen05 kernel with programmatic stream serialization:
 // its prologue (barriers, TMEM allocation, parameter table) overlaps the tail
 // of the previous kernel, and griddep_wait() in the kernel orders the data.
 // pdl = 0 launches it plainly.
 template <typename... Params, typename... Args>
-inline void launch_pdl(void (*kernel)(Params...), int grid, int threads, size_t smem, cudaStream_t s, int pdl,
+inline void launch_pdl(void (*kernel)(Params...), dim3 grid, int threads, size_t smem, cudaStream_t s, int pdl,
                        Args... args) {
   const bool off = !pdl;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
+  cfg.gridDim = grid;
   cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;

@@ -83,17 +83,17 @@ __global__ void ingest_s2d_kernel(const float* __restrict__ x, TensorView t, int
   }
 }
 
-void launch_ingest(const float* x, const TensorView& t, int batch, bool s2d, cudaStream_t s,
+void launch_ingest(const float* x, const TensorView& t, int batch, bool s2d, cudaStream_t s, int pdl,
                    unsigned long long* tl) {
   if (s2d && t.c <= 16 && (2 * (t.w - 1)) % 2 == 0) {
     const int64_t total = (int64_t)batch * t.h * t.w;
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-    ingest_s2d_kernel<<<std::max(blocks, 1), 256, 0, s>>>(x, t, batch, tl);
+    launch_pdl(ingest_s2d_kernel, std::max(blocks, 1), 256, 0, s, pdl, x, t, batch, tl);
     return;
   }
   int64_t total = (int64_t)batch * (t.cpad() / 4) * t.h * t.w;
   int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-  ingest_kernel<<<std::max(blocks, 1), 256, 0, s>>>(x, t, batch, s2d ? 1 : 0, tl);
+  launch_pdl(ingest_kernel, std::max(blocks, 1), 256, 0, s, pdl, x, t, batch, s2d ? 1 : 0, tl);
 }
 
 // ---------------------------------------------------------------------------
@@ -387,11 +387,11 @@ __global__ void __launch_bounds__(256) linear_kernel(LinearArgs a) {
   if (a.out2) a.out2[(int64_t)b * a.n_out + k] = v;
 }
 
-void launch_linear(const LinearArgs& a, cudaStream_t s) {
+void launch_linear(const LinearArgs& a, cudaStream_t s, int pdl) {
   dim3 grid((unsigned)((a.out_stride + kLinO - 1) / kLinO), (unsigned)((a.batch + kLinB - 1) / kLinB));
   const size_t smem = (size_t)(kLinO + kLinB) * ((((a.n_in < kLinK ? a.n_in : kLinK) + 4) & ~3)) * sizeof(float);
   if (smem > 48 * 1024) cudaFuncSetAttribute(linear_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  linear_kernel<<<grid, 256, smem, s>>>(a);
+  launch_pdl(linear_kernel, grid, 256, smem, s, pdl, a);
 }
 
 // ---------------------------------------------------------------------------
@@ -609,26 +609,26 @@ __global__ void bipool2_kernel(EltArgs a) {
   }
 }
 
-void launch_eltwise(const EltArgs& a, cudaStream_t s) {
+void launch_eltwise(const EltArgs& a, cudaStream_t s, int pdl) {
   if (a.kind == PCNN_UNIT_LOCALPOOL && a.pool == PCNN_POOL_BI2) {
     const int64_t total = (int64_t)a.batch * a.out.nblk * a.out.h * a.out.w * (a.out.cb / 4);
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 32);
-    bipool2_kernel<<<std::max(blocks, 1), 256, 0, s>>>(a);
+    launch_pdl(bipool2_kernel, std::max(blocks, 1), 256, 0, s, pdl, a);
     return;
   }
   if (a.kind == PCNN_UNIT_GLOBALPOOL || a.kind == PCNN_UNIT_FLATTEN) {
-    to_vector_kernel<<<148 * 8, 256, 0, s>>>(a);
+    launch_pdl(to_vector_kernel, 148 * 8, 256, 0, s, pdl, a);
     return;
   }
   if (a.kind == PCNN_UNIT_LOCALPOOL && !a.in.split && a.in.cb == a.out.cb) {
     const int64_t total = (int64_t)a.batch * a.out.nblk * a.out.h * a.out.w * (a.in.cb / 4);
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 32);
-    localpool_kernel<<<std::max(blocks, 1), 256, 0, s>>>(a);
+    launch_pdl(localpool_kernel, std::max(blocks, 1), 256, 0, s, pdl, a);
     return;
   }
   int64_t total = (int64_t)a.batch * (a.out.cpad() / 4) * a.out.h * a.out.w;
   int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-  eltwise_kernel<<<std::max(blocks, 1), 256, 0, s>>>(a);
+  launch_pdl(eltwise_kernel, std::max(blocks, 1), 256, 0, s, pdl, a);
 }
 
 // blocked tensor -> user output [B][C][H][W] (logits [B][K] when H = W = 1)
@@ -643,10 +643,10 @@ __global__ void copyout_kernel(TensorView t, float* __restrict__ dst, int batch,
   }
 }
 
-void launch_copyout(const TensorView& t, float* dst, int batch, cudaStream_t s, unsigned long long* tl) {
+void launch_copyout(const TensorView& t, float* dst, int batch, cudaStream_t s, unsigned long long* tl, int pdl) {
   int64_t n = (int64_t)batch * t.c * t.h * t.w;
   int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
-  copyout_kernel<<<std::max(blocks, 1), 256, 0, s>>>(t, dst, batch, tl);
+  launch_pdl(copyout_kernel, std::max(blocks, 1), 256, 0, s, pdl, t, dst, batch, tl);
 }
 
 }  // namespace pcnn
