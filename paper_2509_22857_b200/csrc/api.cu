@@ -353,7 +353,7 @@ void enqueue_unit(pcnn_plan* p, int ui, const float* x, float* logits, cudaStrea
       a.out_stride = p->views[u.out].cpad();
       if (ui + 1 < (int)p->fused.size() && p->fused[ui + 1]) a.out2 = logits;
       a.tl = tl;
-      launch_linear(a, s, (int)p->opt.pdl);
+      launch_linear(a, s, 0);  // plain launch: measured faster than PDL (RN18 9.3 vs 12.9 us)
       break;
     }
     case PCNN_UNIT_COPYOUT: {

@@ -719,7 +719,8 @@ __global__ void __launch_bounds__(ss_threads<PAIRS>(), 1) conv_ss_kernel(const _
           const uint32_t sb = base + st * P.stage_bytes;
           const int ng = q == P.nq - 1 ? P.last_groups : 2;
           if (lane == 0) {
-            ptx::mbar_wait_sleep(ptx::smem_u32(&S->empty[st]), ph ^ 1);
+            if (P.dbg & 2048) ptx::mbar_wait_nohint(ptx::smem_u32(&S->empty[st]), ph ^ 1);
+            else ptx::mbar_wait_sleep(ptx::smem_u32(&S->empty[st]), ph ^ 1);
             ptx::mbar_arrive_tx(bar, 2 * ng * P.nplanes * bytes + P.b_bytes);
           }
           __syncwarp();
@@ -760,7 +761,8 @@ __global__ void __launch_bounds__(ss_threads<PAIRS>(), 1) conv_ss_kernel(const _
           const uint32_t sb = base + st * P.stage_bytes;
           const int ng = q == P.nq - 1 ? P.last_groups : 2;
           if (lane == 0) {
-            ptx::mbar_wait_sleep(ptx::smem_u32(&S->empty[st]), ph ^ 1);
+            if (P.dbg & 2048) ptx::mbar_wait_nohint(ptx::smem_u32(&S->empty[st]), ph ^ 1);
+            else ptx::mbar_wait_sleep(ptx::smem_u32(&S->empty[st]), ph ^ 1);
             ptx::mbar_arrive_tx(bar, 2 * ng * P.nplanes * bytes + (P.wres ? 0u : P.b_bytes) + P.pb_bytes);
           }
           __syncwarp();
