@@ -466,6 +466,34 @@ __device__ __forceinline__ float4 bivariate4_t(const float* __restrict__ coef, i
   }
   return acc;
 }
+// two evaluations sharing one coefficient load: (u, w) = (S(x0, y0), S(x1, y1))
+template <int D>
+__device__ __forceinline__ void bivariate4x2_t(const float* __restrict__ coef, int64_t stride, int ch, float4 x0,
+                                               float4 y0, float4 x1, float4 y1, float4& u, float4& w) {
+  float4 c[D + 1][D + 1];
+#pragma unroll
+  for (int i = 0; i <= D; ++i)
+#pragma unroll
+    for (int j = 0; j + i <= D; ++j)
+      c[i][j] = __ldg(reinterpret_cast<const float4*>(coef + (int64_t)(i * (D + 1) + j) * stride + ch));
+  auto ev = [&](float4 x, float4 y) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int i = D; i >= 0; --i) {
+      float4 r = c[i][D - i];
+#pragma unroll
+      for (int j = D - i - 1; j >= 0; --j)
+        r = make_float4(fmaf(r.x, y.x, c[i][j].x), fmaf(r.y, y.y, c[i][j].y), fmaf(r.z, y.z, c[i][j].z),
+                        fmaf(r.w, y.w, c[i][j].w));
+      acc = (i == D) ? r
+                     : make_float4(fmaf(acc.x, x.x, r.x), fmaf(acc.y, x.y, r.y), fmaf(acc.z, x.z, r.z),
+                                   fmaf(acc.w, x.w, r.w));
+    }
+    return acc;
+  };
+  u = ev(x0, y0);
+  w = ev(x1, y1);
+}
 __device__ __forceinline__ float4 bivariate4_any(const float* __restrict__ coef, int64_t stride, int d, int ch,
                                                  float4 x, float4 y) {
   switch (d) {

@@ -580,6 +580,9 @@ __global__ void localpool_kernel(EltArgs a) {
 // consecutive threads on consecutive memory (channel sub-group, then x);
 // fp32 blocked input, output in its storage format.  Restates the BI2 pool
 // of the conv epilogue (epi_tc.cuh) as a pass of its own.
+// D > 0: the degree at compile time (every coefficient load issued up
+// front, one load shared by the two first-axis evaluations); D = 0 any degree
+template <int D>
 __global__ void bipool2_kernel(EltArgs a) {
   TlScope tls(a.tl);
   const TensorView& in = a.in;
@@ -599,15 +602,21 @@ __global__ void bipool2_kernel(EltArgs a) {
     const float4 q01 = __ldg(reinterpret_cast<const float4*>(in.pix(b, ch0, 2 * y, 2 * x + 1)));
     const float4 q10 = __ldg(reinterpret_cast<const float4*>(in.pix(b, ch0, 2 * y + 1, 2 * x)));
     const float4 q11 = __ldg(reinterpret_cast<const float4*>(in.pix(b, ch0, 2 * y + 1, 2 * x + 1)));
-    float4 u, w;
-    if (a.axis == 0) {
-      u = bivariate4(a.p, a.stride, a.deg, ch0, q00, q01);
-      w = bivariate4(a.p, a.stride, a.deg, ch0, q10, q11);
+    float4 u, w, v;
+    if constexpr (D > 0) {
+      if (a.axis == 0) bivariate4x2_t<D>(a.p, a.stride, ch0, q00, q01, q10, q11, u, w);
+      else bivariate4x2_t<D>(a.p, a.stride, ch0, q00, q10, q01, q11, u, w);
+      v = bivariate4_t<D>(a.p + nc, a.stride, ch0, u, w);
     } else {
-      u = bivariate4(a.p, a.stride, a.deg, ch0, q00, q10);
-      w = bivariate4(a.p, a.stride, a.deg, ch0, q01, q11);
+      if (a.axis == 0) {
+        u = bivariate4(a.p, a.stride, a.deg, ch0, q00, q01);
+        w = bivariate4(a.p, a.stride, a.deg, ch0, q10, q11);
+      } else {
+        u = bivariate4(a.p, a.stride, a.deg, ch0, q00, q10);
+        w = bivariate4(a.p, a.stride, a.deg, ch0, q01, q11);
+      }
+      v = bivariate4(a.p + nc, a.stride, a.deg, ch0, u, w);
     }
-    float4 v = bivariate4(a.p + nc, a.stride, a.deg, ch0, u, w);
     if (ch0 + 0 >= o.c) v.x = 0.f;
     if (ch0 + 1 >= o.c) v.y = 0.f;
     if (ch0 + 2 >= o.c) v.z = 0.f;
@@ -620,7 +629,11 @@ void launch_eltwise(const EltArgs& a, cudaStream_t s, int pdl) {
   if (a.kind == PCNN_UNIT_LOCALPOOL && a.pool == PCNN_POOL_BI2) {
     const int64_t total = (int64_t)a.batch * a.out.nblk * a.out.h * a.out.w * (a.out.cb / 4);
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 32);
-    launch_pdl(bipool2_kernel, std::max(blocks, 1), 256, 0, s, pdl, a);
+    void (*k)(EltArgs) = a.deg == 2   ? bipool2_kernel<2>
+                         : a.deg == 3 ? bipool2_kernel<3>
+                         : a.deg == 4 ? bipool2_kernel<4>
+                                      : bipool2_kernel<0>;
+    launch_pdl(k, std::max(blocks, 1), 256, 0, s, pdl, a);
     return;
   }
   if (a.kind == PCNN_UNIT_GLOBALPOOL || a.kind == PCNN_UNIT_FLATTEN) {
