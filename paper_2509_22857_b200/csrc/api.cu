@@ -989,7 +989,7 @@ int pcnn_plan_create_ex(const pcnn_unit_desc* units, int n_units, const pcnn_ten
   p->kopt.ss_wres = (int)p->opt.ss_wres;
   p->kopt.ss_wide = (int)p->opt.ss_wide;
   p->kopt.epi_pairs = (int)p->opt.epi_pairs;
-  p->kopt.ss_pair = (int)(p->opt.ss_pair && !p->opt.flag_sync);
+  p->kopt.ss_pair = p->opt.flag_sync ? 0 : (int)p->opt.ss_pair;
   p->kopt.tc_stage = (int)p->opt.tc_stage;
   p->kopt.proj_fuse = (int)p->opt.fuse_projection;
   p->kopt.streamk = (int)p->opt.streamk;
