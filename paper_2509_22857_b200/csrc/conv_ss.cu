@@ -1668,6 +1668,8 @@ struct BlkParams {
   uint32_t tmem_cols;
   uint32_t set_cols;   // accumulator columns per sub-tile: [main C | corr C]
   int ptab_floats;
+  int pos_off;         // floats into the table area: [S][128] packed (inside, valid, y, x) of each
+                       // epilogue row of each sub-tile (blk_pos_fill; same for every layer and image)
   int toff[9];         // tap (ky, kx) -> ky wp + kx (A base = first output position - (wp + 1))
   int* flag;           // the plan's status word (an activation left the fp16 range)
   unsigned long long* tl;
@@ -1676,6 +1678,26 @@ struct BlkParams {
   // weights resident, accumulators in a ring of R sub-tile buffers
   int wave, R;
 };
+
+// position table of the image-resident kernels' epilogue: row `row` of
+// sub-tile s is grid position p = p_out0 + 128 s + row, image row y and
+// column x; bit 31 = inside the output rows, bit 30 = a real output column
+__device__ __forceinline__ void blk_pos_fill(const BlkParams& P, int* tab, int tid, int nthreads) {
+  for (int i = tid; i < P.S * 128; i += nthreads) {
+    const int p = P.p_out0 + i;
+    const int y = (p - 1) / P.wp - 1, x = p - 1 - (y + 1) * P.wp;
+    const bool inside = p < P.p_out0 + P.nout, valid = inside && x < P.W;
+    tab[i] = (inside ? (1 << 31) : 0) | (valid ? (1 << 30) : 0) | ((y & 0x7FFF) << 15) | (x & 0x7FFF);
+  }
+}
+__device__ __forceinline__ void blk_pos_get(const int* tab, int s, int row, bool& inside, bool& valid, int& y,
+                                            int& x) {
+  const int v = tab[s * 128 + row];
+  inside = v < 0;
+  valid = (v >> 30) & 1;
+  y = (v >> 15) & 0x7FFF;
+  x = v & 0x7FFF;
+}
 
 // CTA-0 event trace of the block kernel (region: 0 producer, 1 MMA, 2 epilogue warp 0)
 struct BlkTracer {
@@ -1731,6 +1753,7 @@ __global__ void __launch_bounds__(kWaveThreads, 1) conv_blk_kernel(const __grid_
     for (uint32_t i = threadIdx.x; i < n16; i += kWaveThreads) z[i] = make_uint4(0, 0, 0, 0);
   }
   for (int l = 0; l < P.nl; ++l) epi_fill_tab(P.L[l].epi, P.L[l].etab, ptab + P.L[l].ptab_off, threadIdx.x, kWaveThreads);
+  blk_pos_fill(P, reinterpret_cast<int*>(ptab + P.pos_off), threadIdx.x, kWaveThreads);
   ptx::fence_proxy_async();  // generic zero stores -> tcgen05 reads of the slots
   ptx::tc_fence_before();
   __syncthreads();
@@ -1858,6 +1881,7 @@ __global__ void __launch_bounds__(kWaveThreads, 1) conv_blk_kernel(const __grid_
     // ready count stays the 8 warps of its pair)
     const int wg = warp >> 2, ew = wg & 1, jp = wg >> 1, row = threadIdx.x & 127;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const int* postab = reinterpret_cast<const int*>(ptab + P.pos_off);
     uint32_t use[2] = {0u, 0u};
     int gl = 0;
     BlkTracer tr;
@@ -1888,8 +1912,9 @@ __global__ void __launch_bounds__(kWaveThreads, 1) conv_blk_kernel(const __grid_
           for (int j = 0; j < 8; ++j) psum[j] = 0.f;
           for (int s = 0; s < P.S; ++s) {
             const int p = P.p_out0 + 128 * s + row;
-            const int y = (p - 1) / P.wp - 1, x = p - 1 - (y + 1) * P.wp;
-            const bool inside = p < P.p_out0 + P.nout, valid = inside && x < P.W;
+            bool inside, valid;
+            int y, x;
+            blk_pos_get(postab, s, row, inside, valid, y, x);
             float v[8], t[8];
             const uint32_t d = tmem + lane_off + (buf * P.S + s) * P.set_cols;
             ptx::tmem_ld8x2(d + P.C + chb, d + chb, v, t);
@@ -2038,6 +2063,7 @@ __global__ void __launch_bounds__(kWaveThreads2, 1) conv_wave_kernel(const __gri
     for (uint32_t i = threadIdx.x; i < P.set_bytes / 16; i += kWaveThreads2) z[i] = make_uint4(0, 0, 0, 0);
   }
   for (int l = 0; l < NL; ++l) epi_fill_tab(P.L[l].epi, P.L[l].etab, ptab + P.L[l].ptab_off, threadIdx.x, kWaveThreads2);
+  blk_pos_fill(P, reinterpret_cast<int*>(ptab + P.pos_off), threadIdx.x, kWaveThreads2);
   ptx::fence_proxy_async();
   ptx::tc_fence_before();
   __syncthreads();
@@ -2128,6 +2154,8 @@ __global__ void __launch_bounds__(kWaveThreads2, 1) conv_wave_kernel(const __gri
     // (mod 2); warpgroup ew = wg % 2 of the pair takes channels 8 ew .. +7 =====
     const int wg = warp >> 2, ew = wg & 1, jp = wg >> 1, row = threadIdx.x & 127, chb = 8 * ew;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const int* postab = reinterpret_cast<const int*>(ptab + P.pos_off);
+    const uint32_t rmask = (uint32_t)R - 1u, lg_r = (uint32_t)(__ffs(R) - 1);  // R: a power of two
     uint32_t j = 0;
     for (int g = 0;; ++g) {
       const int b = blockIdx.x + G * g;
@@ -2143,12 +2171,16 @@ __global__ void __launch_bounds__(kWaveThreads2, 1) conv_wave_kernel(const __gri
         float psum[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) psum[q] = 0.f;
-        for (int s = 0; s < NS; ++s, ++j) {
-          if ((int)(j & 1u) != jp) continue;
-          const uint32_t r = j % (uint32_t)R;
+        // jobs j0 + s of this layer; this pair's are those with (j0 + s) % 2 == jp
+        const uint32_t j0 = j;
+        j += (uint32_t)NS;
+        for (int s = (int)(((uint32_t)jp ^ j0) & 1u); s < NS; s += 2) {
+          const uint32_t jj = j0 + (uint32_t)s;
+          const uint32_t r = jj & rmask;
           const int p = P.p_out0 + 128 * s + row;
-          const int y = (p - 1) / P.wp - 1, x = p - 1 - (y + 1) * P.wp;
-          const bool inside = p < P.p_out0 + P.nout, valid = inside && x < P.W;
+          bool inside, valid;
+          int y, x;
+          blk_pos_get(postab, s, row, inside, valid, y, x);
           float sk[8];
           if (L.res_slot >= 0) {
             const uint32_t rb = slots + (uint32_t)L.res_slot * P.slot_bytes + (uint32_t)ew * P.plane + (uint32_t)p * 16;
@@ -2166,7 +2198,7 @@ __global__ void __launch_bounds__(kWaveThreads2, 1) conv_wave_kernel(const __gri
 #pragma unroll
             for (int q = 0; q < 8; ++q) sk[q] = 0.f;
           }
-          ptx::mbar_wait_warp(ptx::smem_u32(&S->acc_full[r]), (j / (uint32_t)R) & 1u);
+          ptx::mbar_wait_warp(ptx::smem_u32(&S->acc_full[r]), (jj >> lg_r) & 1u);
           ptx::tc_fence_after();
           float v[8], t[8];
           const uint32_t d = tmem + lane_off + r * 32u;
@@ -2281,6 +2313,7 @@ BlkRun* blk_create(const ConvArgs* layers, int n, const int* in_slot, const int*
   const uint32_t need = P.wave ? 512u : 2u * (uint32_t)P.S * P.set_cols;
   if (need > 512 || (P.wave && P.S > kWaveMaxSub)) { delete r; return nullptr; }
   P.R = P.wave ? 512 / (int)P.set_cols : 0;
+  if (P.wave && (P.R & (P.R - 1))) { delete r; return nullptr; }  // the epilogue indexes the ring by masks
   P.tmem_cols = need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
   for (int t = 0; t < 9; ++t) P.toff[t] = (t / 3) * P.wp + t % 3;
   P.flag = flag;
@@ -2310,6 +2343,8 @@ BlkRun* blk_create(const ConvArgs* layers, int n, const int* in_slot, const int*
     L.ptab_off = pt;
     pt += (L.etab.rows * P.C + 3) & ~3;
   }
+  P.pos_off = pt;
+  pt += P.S * 128;
   P.ptab_floats = pt;
   const size_t budget = 225 * 1024 - 128;
   if (P.wave) {
