@@ -507,14 +507,16 @@ void build_blocks(pcnn_plan* p) {
     if (u.kind != PCNN_UNIT_CONV || p->impl[i] != 5 || p->fused[i]) return false;
     const ConvArgs& a = p->conv_args[i];
     return a.kh == 3 && a.kw == 3 && a.stride == 1 && a.pad == 1 && !a.proj && a.in.split == 1 && !a.sk_flags &&
-           (a.npad == 16 || a.npad == 32 || a.npad == 64) && a.in.cpad() == a.npad && u.cout == a.npad;
+           (a.npad == 16 || a.npad == 32 || a.npad == 64) && u.cout == a.npad &&
+           // a narrow input (ResNet-20's 3-channel stem: one 8-channel group) can only head a 16-channel run
+           (a.in.cpad() == a.npad || (a.npad == 16 && a.in.cpad() <= 8));
   };
   int i = 0;
   while (i < n) {
     if (!eligible(i)) { ++i; continue; }
     const ConvArgs& a0 = p->conv_args[i];
     int j = i + 1;
-    while (j < n && j - i < 6 && eligible(j) && p->units[j].in == p->units[j - 1].out &&
+    while (j < n && j - i < 7 && eligible(j) && p->units[j].in == p->units[j - 1].out &&
            p->conv_args[j].in.h == a0.in.h && p->conv_args[j].in.w == a0.in.w &&
            p->conv_args[j].npad == a0.npad && p->conv_args[j - 1].epi.pool == PCNN_POOL_NONE)
       ++j;
@@ -1271,9 +1273,11 @@ int pcnn_forward_host_many(pcnn_plan* p, const float* const* x_hosts, float* con
     p->status_pinned = nullptr;
     p->status_slots = nullptr;
     p->status_pinned_n = 0;
-    PCNN_CUDA(cudaMallocHost(&p->status_pinned, sizeof(int) * (size_t)n));
-    PCNN_CUDA(cudaMalloc(&p->status_slots, sizeof(int) * (size_t)n));
-    p->status_pinned_n = n;
+    // room to spare: a later, longer call does not pay a pinned allocation (~1 ms) again
+    const int cap = n < 256 ? 256 : 2 * n;
+    PCNN_CUDA(cudaMallocHost(&p->status_pinned, sizeof(int) * (size_t)cap));
+    PCNN_CUDA(cudaMalloc(&p->status_slots, sizeof(int) * (size_t)cap));
+    p->status_pinned_n = cap;
   }
   float* xd[2] = {x_dev0, x_dev1};
   float* ld[2] = {logits_dev, p->logits2};

@@ -1627,7 +1627,7 @@ bool make_ss_params(const ConvArgs& a, SsParams& P, bool allow_wres = true) {
 // image into the next plane (or the weight ring) only for rows whose outputs
 // are discarded.
 // =====================================================================
-constexpr int kBlkMaxLayers = 6;
+constexpr int kBlkMaxLayers = 7;  // ResNet-20 stage 1 with its stem: 1 + 6 convs
 // the image-resident kernels run four epilogue warpgroups (warps 0-15), the
 // producer (16) and the MMA warp (17): an epilogue item is a long dependent
 // chain (accumulator wait, TMEM load, table reads, stores, proxy fence,
@@ -1661,6 +1661,7 @@ struct BlkParams {
   int nslots;
   int ni;              // resident images per CTA (1 or 2)
   int ext_in_slot, ext_res_slot;
+  int ext_in_groups;   // 8-channel groups the external input stores (wave mode: 1 for a 3-channel stem input)
   TensorView ext_in, ext_res;
   int batch;
   int stages;
@@ -2092,7 +2093,10 @@ __global__ void __launch_bounds__(kWaveThreads2, 1) conv_wave_kernel(const __gri
       const int nt_ext = (P.ext_in_slot >= 0) + (P.ext_res_slot >= 0);
       const uint32_t bytes = (uint32_t)P.P_img * 16;
       const uint32_t eb = ptx::smem_u32(&S->ext_full);
-      if (lane == 0) ptx::mbar_arrive_tx(eb, (uint32_t)nt_ext * 4 * bytes);
+      // a one-group input (the stem's) leaves the slot's second group as the
+      // previous image left it: finite values its zero weight rows cancel
+      const int planes = (P.ext_in_slot >= 0 ? 2 * P.ext_in_groups : 0) + (P.ext_res_slot >= 0 ? 4 : 0);
+      if (lane == 0) ptx::mbar_arrive_tx(eb, (uint32_t)planes * bytes);
       __syncwarp();
       if (lane < 4 * nt_ext) {
         const int ti = lane >> 2, gp = lane & 3;
@@ -2102,7 +2106,8 @@ __global__ void __launch_bounds__(kWaveThreads2, 1) conv_wave_kernel(const __gri
         const int gg = gp & 1, lo = gp >> 1;
         const __half* base = lo ? t.lo() : t.hi();
         const int64_t off = gg * t.kstride + (int64_t)b * (P.H + 1) * P.wp * 8;
-        ptx::bulk_g2s(slots + (uint32_t)slot * P.slot_bytes + (uint32_t)gp * P.plane, base + off, bytes, eb);
+        if (!use_in || gg < P.ext_in_groups)
+          ptx::bulk_g2s(slots + (uint32_t)slot * P.slot_bytes + (uint32_t)gp * P.plane, base + off, bytes, eb);
       }
       __syncwarp();
     }
@@ -2307,6 +2312,7 @@ BlkRun* blk_create(const ConvArgs* layers, int n, const int* in_slot, const int*
   P.ext_res_slot = ext_res_slot;
   P.ext_in = ext_in;
   P.ext_res = ext_res;
+  P.ext_in_groups = a0.in.cpad() <= 8 ? 1 : 2;
   P.batch = batch;
   P.b_bytes = 9u * 64u * (uint32_t)P.C;
   P.set_cols = 2u * (uint32_t)P.C;
@@ -2321,7 +2327,8 @@ BlkRun* blk_create(const ConvArgs* layers, int n, const int* in_slot, const int*
   int pt = 0;
   for (int l = 0; l < n; ++l) {
     const ConvArgs& a = layers[l];
-    if (a.kh != 3 || a.kw != 3 || a.stride != 1 || a.pad != 1 || a.npad != P.C || a.in.cpad() != P.C ||
+    const bool narrow_head = l == 0 && P.wave && a.in.cpad() <= 8;  // one stored group, zero weight rows beyond it
+    if (a.kh != 3 || a.kw != 3 || a.stride != 1 || a.pad != 1 || a.npad != P.C || (a.in.cpad() != P.C && !narrow_head) ||
         a.in.h != P.H || a.in.w != P.W || !a.tcwss || !a.tc16_scale || a.proj || a.epi.residual > 3 ||
         (a.epi.pool != PCNN_POOL_NONE && !(a.epi.pool == PCNN_POOL_GLOBAL && l == n - 1))) {
       delete r;
