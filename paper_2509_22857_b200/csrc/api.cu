@@ -509,7 +509,7 @@ void build_blocks(pcnn_plan* p) {
     return a.kh == 3 && a.kw == 3 && a.stride == 1 && a.pad == 1 && !a.proj && a.in.split == 1 && !a.sk_flags &&
            (a.npad == 16 || a.npad == 32 || a.npad == 64) && u.cout == a.npad &&
            // a narrow input (ResNet-20's 3-channel stem: one 8-channel group) can only head a 16-channel run
-           (a.in.cpad() == a.npad || (a.npad == 16 && a.in.cpad() <= 8));
+           (a.in.cpad() == a.npad || (a.npad == 16 && a.in.cpad() <= 8 && !(p->opt.debug & 16384)));
   };
   int i = 0;
   while (i < n) {

@@ -1671,6 +1671,7 @@ struct BlkParams {
   int ptab_floats;
   int pos_off;         // floats into the table area: [S][128] packed (inside, valid, y, x) of each
                        // epilogue row of each sub-tile (blk_pos_fill; same for every layer and image)
+  int wsc_off;         // floats into the table area: every layer's weight scale x input load scale
   int toff[9];         // tap (ky, kx) -> ky wp + kx (A base = first output position - (wp + 1))
   int* flag;           // the plan's status word (an activation left the fp16 range)
   unsigned long long* tl;
@@ -1689,6 +1690,36 @@ __device__ __forceinline__ void blk_pos_fill(const BlkParams& P, int* tab, int t
     const int y = (p - 1) / P.wp - 1, x = p - 1 - (y + 1) * P.wp;
     const bool inside = p < P.p_out0 + P.nout, valid = inside && x < P.W;
     tab[i] = (inside ? (1 << 31) : 0) | (valid ? (1 << 30) : 0) | ((y & 0x7FFF) << 15) | (x & 0x7FFF);
+  }
+}
+// Every layer's epilogue table and weight scale in one pass: a thread issues
+// all of its (read-only) global loads before its first store, so a cold
+// start pays one memory round trip, not one per layer (measured after an L2
+// flush: ~0.8 us per layer of launch gap)
+__device__ __forceinline__ void blk_fill_tabs(const BlkParams& P, float* ptab, int tid, int nthreads) {
+  const int total = P.pos_off;  // the layers' tables (each padded to 4 floats)
+  for (int base = tid; base < total + P.nl; base += 4 * nthreads) {
+    float v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = base + k * nthreads;
+      v[k] = 0.f;
+      if (i < total) {
+        int l = 0;
+        for (int q = 1; q < P.nl; ++q)
+          if (i >= P.L[q].ptab_off) l = q;
+        const int j = i - P.L[l].ptab_off;
+        if (j < P.L[l].etab.rows * P.C) v[k] = epi_tab_value(P.L[l].epi, P.L[l].etab, j, 1.f, 1.f);
+      } else if (i < total + P.nl) {
+        v[k] = __ldg(P.L[i - total].wscale) * P.L[i - total].in_sload;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = base + k * nthreads;
+      if (i < total) ptab[i] = v[k];
+      else if (i < total + P.nl) ptab[P.wsc_off + i - total] = v[k];
+    }
   }
 }
 __device__ __forceinline__ void blk_pos_get(const int* tab, int s, int row, bool& inside, bool& valid, int& y,
@@ -1753,7 +1784,7 @@ __global__ void __launch_bounds__(kWaveThreads, 1) conv_blk_kernel(const __grid_
     const uint32_t n16 = (uint32_t)P.ni * P.set_bytes / 16;
     for (uint32_t i = threadIdx.x; i < n16; i += kWaveThreads) z[i] = make_uint4(0, 0, 0, 0);
   }
-  for (int l = 0; l < P.nl; ++l) epi_fill_tab(P.L[l].epi, P.L[l].etab, ptab + P.L[l].ptab_off, threadIdx.x, kWaveThreads);
+  blk_fill_tabs(P, ptab, threadIdx.x, kWaveThreads);
   blk_pos_fill(P, reinterpret_cast<int*>(ptab + P.pos_off), threadIdx.x, kWaveThreads);
   ptx::fence_proxy_async();  // generic zero stores -> tcgen05 reads of the slots
   ptx::tc_fence_before();
@@ -1905,7 +1936,7 @@ __global__ void __launch_bounds__(kWaveThreads, 1) conv_blk_kernel(const __grid_
         ptx::tc_fence_after();
         EpiTab tab = L.etab;
         tab.ptab = ptab + L.ptab_off;
-        const float wsc = __ldg(L.wscale) * L.in_sload;
+        const float wsc = ptab[P.wsc_off + l];
         for (int k = jp; k < P.nq; k += 2) {
           const int chb = 16 * k + 8 * ew;
           float psum[8];
@@ -2063,7 +2094,7 @@ __global__ void __launch_bounds__(kWaveThreads2, 1) conv_wave_kernel(const __gri
     uint4* z = reinterpret_cast<uint4*>(smem);
     for (uint32_t i = threadIdx.x; i < P.set_bytes / 16; i += kWaveThreads2) z[i] = make_uint4(0, 0, 0, 0);
   }
-  for (int l = 0; l < NL; ++l) epi_fill_tab(P.L[l].epi, P.L[l].etab, ptab + P.L[l].ptab_off, threadIdx.x, kWaveThreads2);
+  blk_fill_tabs(P, ptab, threadIdx.x, kWaveThreads2);
   blk_pos_fill(P, reinterpret_cast<int*>(ptab + P.pos_off), threadIdx.x, kWaveThreads2);
   ptx::fence_proxy_async();
   ptx::tc_fence_before();
@@ -2172,7 +2203,7 @@ __global__ void __launch_bounds__(kWaveThreads2, 1) conv_wave_kernel(const __gri
         if (L.res_ext) ptx::mbar_wait_warp(ptx::smem_u32(&S->ext_full), g & 1);
         EpiTab tab = L.etab;
         tab.ptab = ptab + L.ptab_off;
-        const float wsc = __ldg(L.wscale) * L.in_sload;
+        const float wsc = ptab[P.wsc_off + l];
         float psum[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) psum[q] = 0.f;
@@ -2352,6 +2383,8 @@ BlkRun* blk_create(const ConvArgs* layers, int n, const int* in_slot, const int*
   }
   P.pos_off = pt;
   pt += P.S * 128;
+  P.wsc_off = pt;
+  pt += (kBlkMaxLayers + 3) & ~3;
   P.ptab_floats = pt;
   const size_t budget = 225 * 1024 - 128;
   if (P.wave) {

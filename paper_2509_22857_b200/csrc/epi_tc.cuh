@@ -35,27 +35,31 @@ inline EpiTab epi_tab_layout(const EpiParams& e) {
 // scale; oscale multiplies the rows of the last stage (poly, else S), so the
 // result comes out already in storage units.  Both are powers of two: the
 // folded arithmetic is exact.
+// the value epi_fill_tab stores at table index i (read-only loads: callers
+// may batch several before their first store)
+__device__ __forceinline__ float epi_tab_value(const EpiParams& ep, const EpiTab& T, int i, float yscale, float oscale) {
+  const int np = ep.npad;
+  const int r = i / np, c = i - r * np;
+  float v;
+  if (r == 0) v = __ldg(ep.bias + c);
+  else if (T.row_aff >= 0 && r < T.row_aff + 2 && r >= T.row_aff) v = __ldg(ep.aff + (r - T.row_aff) * np + c);
+  else if (T.row_poly >= 0 && r >= T.row_poly && r <= T.row_poly + ep.poly_deg) {
+    v = __ldg(ep.poly + (r - T.row_poly) * np + c) * oscale;
+  } else {
+    // S rows: x2 y2 xy x y c; the skip is y for residual 2, x for residual 3
+    const int k = r - T.row_res;
+    v = __ldg(ep.res + k * np + c);
+    const int sq = ep.residual == 2 ? 1 : 0, lin = ep.residual == 2 ? 4 : 3;
+    if (k == sq) v *= yscale * yscale;
+    else if (k == 2 || k == lin) v *= yscale;
+    if (!ep.poly_deg) v *= oscale;
+  }
+  return v;
+}
+
 __device__ __forceinline__ void epi_fill_tab(const EpiParams& ep, const EpiTab& T, float* ptab, int tid, int nthreads,
                                              float yscale = 1.f, float oscale = 1.f) {
-  const int np = ep.npad;
-  for (int i = tid; i < T.rows * np; i += nthreads) {
-    const int r = i / np, c = i - r * np;
-    float v;
-    if (r == 0) v = ep.bias[c];
-    else if (T.row_aff >= 0 && r < T.row_aff + 2 && r >= T.row_aff) v = ep.aff[(r - T.row_aff) * np + c];
-    else if (T.row_poly >= 0 && r >= T.row_poly && r <= T.row_poly + ep.poly_deg) {
-      v = ep.poly[(r - T.row_poly) * np + c] * oscale;
-    } else {
-      // S rows: x2 y2 xy x y c; the skip is y for residual 2, x for residual 3
-      const int k = r - T.row_res;
-      v = ep.res[k * np + c];
-      const int sq = ep.residual == 2 ? 1 : 0, lin = ep.residual == 2 ? 4 : 3;
-      if (k == sq) v *= yscale * yscale;
-      else if (k == 2 || k == lin) v *= yscale;
-      if (!ep.poly_deg) v *= oscale;
-    }
-    ptab[i] = v;
-  }
+  for (int i = tid; i < T.rows * ep.npad; i += nthreads) ptab[i] = epi_tab_value(ep, T, i, yscale, oscale);
 }
 
 __device__ __forceinline__ void epi_store4(const EpiParams& e, int b, int ch, int y, int x, const float* o) {
