@@ -454,14 +454,66 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def parity_of(gr, x_host, y):
+def oracle_logits(gr, x_host):
+    """float64 oracle forward of every image over the host cores (oracle/pool.py)."""
+    from oracle.pool import OraclePool
+    with OraclePool(gr) as pool:
+        return pool.eval(x_host)
+
+
+def precision_table(gr, x_host, want, flush, steps=5):
+    """The same redistributed graph and batch under each arithmetic scheme the
+    library has: device ms per forward (CUDA events, L2 flushed, graph replay)
+    and max relative error of the logits against the float64 oracle on every
+    image.  Rows: the default fp16x2 fast path (three fp16 products, fp32
+    accumulation), forced 3xTF32 (kind::tf32, A from TMEM), the all-float32
+    tensor plan (the rerun target when an activation leaves the fp16 range)
+    and plain fp32 FFMA (conv_simt_kernel)."""
+    import torch
+    from paper_2509_22857_b200 import _lib as L
+    from paper_2509_22857_b200.runtime import Engine
+    x = torch.from_numpy(x_host).cuda()
+    rows = []
+    for label, impl in (("fp16x2 (default plan)", L.IMPL_AUTO), ("3xTF32 forced", L.IMPL_TF32),
+                        ("float32 tensors (3xTF32 / SIMT)", L.IMPL_FP32_TENSORS), ("fp32 FFMA (SIMT)", L.IMPL_SIMT)):
+        row = {"scheme": label, "impl": impl}
+        try:
+            eng = Engine(gr, impl=impl)
+            out = torch.empty(eng.out_shape(len(x_host)), dtype=torch.float32, device="cuda")
+            eng.forward(x, out)
+            for _ in range(3):
+                eng.forward(x, out, check=False)
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+            stream = torch.cuda.current_stream()
+            for a, b in ev:
+                flush()
+                a.record(stream)
+                eng.forward(x, out, check=False)
+                b.record(stream)
+            torch.cuda.synchronize()
+            y = out.cpu().numpy().reshape(want.shape).astype(np.float64)
+            plan = eng.plan(len(x_host))
+            row.update({"ms_per_step": round(sum(a.elapsed_time(b) for a, b in ev) / steps, 4),
+                        "max_rel_err": float(np.max(np.abs(y - want)) / max(float(np.max(np.abs(want))), 1e-30)),
+                        "allclose_rtol1e-4_atol1e-5": bool(np.allclose(y, want, rtol=1e-4, atol=1e-5)),
+                        "fp32_reruns": int(eng.fallbacks),
+                        "conv_impl": sorted({plan.unit_impl(i) for i, u in enumerate(eng.lw.units)
+                                             if u.get("kind") == 2})})
+            del eng, out
+            torch.cuda.empty_cache()
+        except Exception as e:  # a scheme a shape class does not support is reported, not hidden
+            row["error"] = f"{type(e).__name__}: {e}"[:200]
+        rows.append(row)
+    return rows
+
+
+def parity_of(gr, x_host, y, want=None):
     """Max relative error of the timed batch's logits against the float64
     oracle forward of the same (redistributed) graph, every image, over the
     host cores (oracle/pool.py) -- the checker, not the measured path."""
-    from oracle.pool import OraclePool
     t0 = time.perf_counter()
-    with OraclePool(gr) as pool:
-        want = pool.eval(x_host)
+    if want is None:
+        want = oracle_logits(gr, x_host)
     y = y.reshape(want.shape).astype(np.float64)
     err = float(np.max(np.abs(y - want)) / max(float(np.max(np.abs(want))), 1e-30))
     cy, cw = y - y.mean(0), want - want.mean(0)
@@ -688,7 +740,13 @@ def run_ours(args):
             torch.cuda.empty_cache()
     if not args.no_parity:
         for dst, gr, xh, y in checks:
-            dst["parity"] = parity_of(gr, xh, y)
+            t0 = time.perf_counter()
+            want = oracle_logits(gr, xh)
+            oracle_s = round(time.perf_counter() - t0, 2)
+            dst["parity"] = parity_of(gr, xh, y, want)
+            dst["parity"]["oracle_s"] = oracle_s
+            if not args.no_precision and world == 1:
+                dst["precision"] = precision_table(gr, xh, want, flush)
     if not args.no_redist_timing:
         red = time_redistribution(main_g, cfg)
         cpu_ms, n = time_cpu_redistribution(main_g, cfg)
@@ -719,6 +777,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-redist-timing", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-precision", action="store_true",
+                    help="skip the per-scheme precision / time table (fp16x2, 3xTF32, float32 tensors, SIMT)")
     ap.add_argument("--secondary", default="resnet18",
                     help="comma-separated configs measured after the main one (1 GPU), reported under 'secondary'")
     args = ap.parse_args()

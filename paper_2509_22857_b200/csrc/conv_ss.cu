@@ -1587,7 +1587,8 @@ bool make_ss_params(const ConvArgs& a, SsParams& P, bool allow_wres = true) {
       return true;
     }
   }
-  if (a.opt.epi_pairs >= 2 && (P1.nt <= 32 || (P1.nt <= 64 && P1.proj)) && !P1.band && !a.sk_flags) {
+  if (a.opt.epi_pairs >= 2 && (P1.nt <= 32 || (P1.nt <= 64 && (P1.proj || a.opt.epi_pairs >= 3)) || a.opt.epi_pairs >= 4) &&
+      !P1.band && !a.sk_flags) {
     SsParams Q = P;
     if (make_ss_params_nt(a, Q, P1.nt, P1.psub != 0, allow_wres, 0, 0, 2) && Q.wres == P1.wres &&
         Q.mt == P1.mt && Q.stages >= (P1.stages < 3 ? P1.stages : 3)) {
