@@ -230,3 +230,32 @@ def test_whole_network_launch_matches(cuda, batch):
     assert rel_err(fused.forward(xt, use_graph=True).double().cpu().numpy(), got) <= 1e-7
     outs = fused.forward_host_many([torch.from_numpy(x.astype(np.float32))])
     assert rel_err(outs[0].double().numpy(), got) <= 1e-7
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("opts", [{"epi_pairs": 1}, {"epi_pairs": 3}, {"epi_pairs": 4}, {"ss_pair": 0},
+                                  {"ss_wide": 0}, {"ss_wide": 2}],
+                         ids=lambda o: ",".join(f"{k}={v}" for k, v in o.items()))
+@pytest.mark.parametrize("name", ["resnet18", "vgg11"])
+def test_halo_tile_option_variants_match(cuda, name, opts):
+    """Every halo-tile scheduling option ships tested: epilogue warpgroup
+    pairs on no / 64-channel / every tile (options.epi_pairs 1 / 3 / 4),
+    CTA-pair tiles off (options.ss_pair) and the producer's single- or
+    multi-lane bulk-copy issue (options.ss_wide) change who drains or stages
+    a tile, never its arithmetic: logits equal the default plan's (the
+    global-pool atomics may add in another order)."""
+    import torch
+    from paper_2509_22857_b200 import _lib as L
+    cfg = configs.CONFIGS[name]
+    g = configs.build(name)
+    for d in cfg.redistribution:
+        g, _, _ = T.redistribute_sweep(g, d, allow_negative_leading=cfg.allow_negative_leading)
+    x = torch.from_numpy(configs.make_input(cfg).astype(np.float32)).cuda()
+    base = Engine(g)
+    want = base.forward(x).double().cpu().numpy()
+    eng = Engine(g, options=L.PlanOptions.default(**opts))
+    for _ in range(2):
+        got = eng.forward(x).double().cpu().numpy()
+        assert rel_err(got, want) <= 1e-5, (name, opts)
+    # the fp16-range rescue (one float32 rerun + rescale on VGG's first batch) is the plan's, not the option's
+    assert eng.fallbacks == base.fallbacks
