@@ -275,7 +275,12 @@ typedef struct pcnn_plan_options {
                                (cluster of two, tcgen05 cta_group::2,
                                M = 256 over two SMs, each SM staging half
                                of the tile's weights); 0: one CTA per tile */
-  int64_t reserved[4];
+  int64_t scratch_cb4;      /* 1: the float32 scratch map between a halo-tile
+                               conv and its local-pool pass in 4-channel
+                               blocks (a warp's row-per-lane stores become
+                               contiguous); 0 (default; measured equal): the
+                               tensor's own block width                    */
+  int64_t reserved[3];
 } pcnn_plan_options;
 
 /* ---- entry points --------------------------------------------------------*/

@@ -89,14 +89,14 @@ class RewriteDesc(ctypes.Structure):
 _OPT_INT_FIELDS_A = ("size", "split", "halo_tiles", "fuse_projection", "band_pool", "streamk")
 _OPT_INT_FIELDS_B = ("flag_sync", "prezero", "linear_out", "pdl", "graph", "ss_mt", "ss_share", "ss_psub",
                      "ss_wres", "tc_stage", "timeline", "image_blocks", "debug", "fused_net", "ss_wide", "epi_pairs",
-                     "ss_pair")
+                     "ss_pair", "scratch_cb4")
 
 
 class PlanOptions(ctypes.Structure):
     """pcnn_plan_options: every tuning / diagnostic switch of a plan (the
     library reads no environment variables)."""
     _fields_ = [(n, c_i64) for n in _OPT_INT_FIELDS_A] + [("streamk_fill", c_f64)] + \
-               [(n, c_i64) for n in _OPT_INT_FIELDS_B] + [("reserved", c_i64 * 4)]
+               [(n, c_i64) for n in _OPT_INT_FIELDS_B] + [("reserved", c_i64 * 3)]
 
     @classmethod
     def default(cls, **overrides) -> "PlanOptions":
@@ -121,7 +121,7 @@ ENV_OPTIONS = {
     "PCNN_NO_GRAPH": ("graph", 0), "PCNN_SS_MT": ("ss_mt", int), "PCNN_SS_SHARE": ("ss_share", int),
     "PCNN_SS_PSUB": ("ss_psub", int), "PCNN_SS_WRES": ("ss_wres", int), "PCNN_TC_NOSTAGE": ("tc_stage", 0),
     "PCNN_TC_DEBUG": ("debug", int), "PCNN_STREAMK_FILL": ("streamk_fill", float),
-    "PCNN_NO_TIMELINE": ("timeline", 0), "PCNN_NO_NET": ("fused_net", 0), "PCNN_WIDE": ("ss_wide", int), "PCNN_PAIRS": ("epi_pairs", int), "PCNN_PAIR": ("ss_pair", int), "PCNN_NO_BLOCKS": ("image_blocks", 0), "PCNN_BLOCKS": ("image_blocks", int),
+    "PCNN_NO_TIMELINE": ("timeline", 0), "PCNN_NO_NET": ("fused_net", 0), "PCNN_WIDE": ("ss_wide", int), "PCNN_PAIRS": ("epi_pairs", int), "PCNN_PAIR": ("ss_pair", int), "PCNN_SCRATCH_CB4": ("scratch_cb4", int), "PCNN_NO_BLOCKS": ("image_blocks", 0), "PCNN_BLOCKS": ("image_blocks", int),
 }
 
 

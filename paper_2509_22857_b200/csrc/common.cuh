@@ -209,11 +209,17 @@ __device__ __forceinline__ void store8_any(const TensorView& t, int b, int ch, i
 
 // store 16 consecutive channels (ch % 16 == 0; one block when fp32, cb >= 16):
 // whole 32-byte sectors per thread in both formats
+// cb = 4 (pooled convs' scratch maps): four channel blocks, each 16 bytes per
+// position with consecutive positions adjacent, so a warp whose lanes hold
+// consecutive positions writes 512 contiguous bytes per store instruction
+// (cb >= 16 puts a lane's 64 bytes together and the lanes 64 bytes apart:
+// 32 wavefronts of the LSU data pipe per instruction instead of 4)
 __device__ __forceinline__ void store16_any(const TensorView& t, int b, int ch, int y, int x, const float* v) {
   if (!t.split) {
     float4* o = reinterpret_cast<float4*>(t.base + t.index(b, ch, y, x));
+    const int64_t qs = t.cb == 4 ? (int64_t)t.h * t.w : 1;  // float4 stride between 4-channel groups
 #pragma unroll
-    for (int q = 0; q < 4; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    for (int q = 0; q < 4; ++q) o[q * qs] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     return;
   }
   store16_split_at(t, t.sindex(b, ch, y, x), v, t.sstore);

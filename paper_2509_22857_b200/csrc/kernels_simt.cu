@@ -575,6 +575,70 @@ __global__ void localpool_kernel(EltArgs a) {
   }
 }
 
+// k x k / stride local sum pool * divisor over a scratch map in 4-channel
+// blocks (in.cb = 4, plan_local_pools): one thread per (8-channel group,
+// output pixel), x fastest -- a warp reads runs of adjacent 16-byte pixels
+// and writes whole 16-byte hi / lo groups of a split output.
+__global__ void localpool_cb4_kernel(EltArgs a) {
+  TlScope tls(a.tl);
+  const TensorView& in = a.in;
+  const TensorView& o = a.out;
+  const int ng = o.cpad() / 8;
+  const int64_t total = (int64_t)a.batch * ng * o.h * o.w;
+  const float dv = __ldg(a.p);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int xw = (int)(i % o.w);
+    int64_t r = i / o.w;
+    const int y = (int)(r % o.h);
+    r /= o.h;
+    const int g = (int)(r % ng);
+    const int b = (int)(r / ng);
+    const int ch0 = g * 8;
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+    if (a.k == 3) {
+      // all eighteen loads in flight at once
+      float4 t9[2][9];
+#pragma unroll
+      for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) {
+          const int iy = y * a.st - a.pad + dy, ix = xw * a.st - a.pad + dx;
+          const bool ok = iy >= 0 && iy < in.h && ix >= 0 && ix < in.w;
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            t9[h][dy * 3 + dx] = ok ? __ldg(reinterpret_cast<const float4*>(in.at(b, ch0 + 4 * h, iy, ix)))
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+      for (int q = 0; q < 9; ++q)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          acc[4 * h] += t9[h][q].x; acc[4 * h + 1] += t9[h][q].y; acc[4 * h + 2] += t9[h][q].z; acc[4 * h + 3] += t9[h][q].w;
+        }
+    } else {
+      for (int dy = 0; dy < a.k; ++dy) {
+        const int iy = y * a.st - a.pad + dy;
+        if (iy < 0 || iy >= in.h) continue;
+        for (int dx = 0; dx < a.k; ++dx) {
+          const int ix = xw * a.st - a.pad + dx;
+          if (ix < 0 || ix >= in.w) continue;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(in.at(b, ch0 + 4 * h, iy, ix)));
+            acc[4 * h] += v.x; acc[4 * h + 1] += v.y; acc[4 * h + 2] += v.z; acc[4 * h + 3] += v.w;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] *= dv;
+    store8_any(o, b, ch0, y, xw, acc);
+  }
+}
+
 // 2x2 / stride-2 window through two bivariate polynomials (axis 0: along w,
 // then across rows; 1: along h, then across columns), 4 channels per thread,
 // consecutive threads on consecutive memory (channel sub-group, then x);
@@ -638,6 +702,12 @@ void launch_eltwise(const EltArgs& a, cudaStream_t s, int pdl) {
   }
   if (a.kind == PCNN_UNIT_GLOBALPOOL || a.kind == PCNN_UNIT_FLATTEN) {
     launch_pdl(to_vector_kernel, 148 * 8, 256, 0, s, pdl, a);
+    return;
+  }
+  if (a.kind == PCNN_UNIT_LOCALPOOL && !a.in.split && a.in.cb == 4 && a.out.cb >= 8 && a.pool == 0) {
+    const int64_t total = (int64_t)a.batch * (a.out.cpad() / 8) * a.out.h * a.out.w;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 32);
+    launch_pdl(localpool_cb4_kernel, std::max(blocks, 1), 256, 0, s, pdl, a);
     return;
   }
   if (a.kind == PCNN_UNIT_LOCALPOOL && !a.in.split && a.in.cb == a.out.cb) {

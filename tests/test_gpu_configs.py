@@ -234,15 +234,17 @@ def test_whole_network_launch_matches(cuda, batch):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("opts", [{"epi_pairs": 1}, {"epi_pairs": 3}, {"epi_pairs": 4}, {"ss_pair": 0},
-                                  {"ss_wide": 0}, {"ss_wide": 2}],
+                                  {"ss_wide": 0}, {"ss_wide": 2}, {"scratch_cb4": 1}],
                          ids=lambda o: ",".join(f"{k}={v}" for k, v in o.items()))
 @pytest.mark.parametrize("name", ["resnet18", "vgg11"])
 def test_halo_tile_option_variants_match(cuda, name, opts):
     """Every halo-tile scheduling option ships tested: epilogue warpgroup
     pairs on no / 64-channel / every tile (options.epi_pairs 1 / 3 / 4),
     CTA-pair tiles off (options.ss_pair) and the producer's single- or
-    multi-lane bulk-copy issue (options.ss_wide) change who drains or stages
-    a tile, never its arithmetic: logits equal the default plan's (the
+    multi-lane bulk-copy issue (options.ss_wide) and the 4-channel-block
+    scratch map between a conv and its local pool (options.scratch_cb4)
+    change who drains or stages a tile or where a scratch value lives, never
+    the arithmetic: logits equal the default plan's (the
     global-pool atomics may add in another order)."""
     import torch
     from paper_2509_22857_b200 import _lib as L
