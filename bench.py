@@ -130,6 +130,54 @@ KERNEL_NAMES = {1: "conv_simt_kernel", 2: "conv_tc_kernel (3xTF32, A in TMEM)",
 # roofline of the whole-network kernel (derived from the SM count and max clock)
 SIMT_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 OTHER_NAMES = {1: "ingest_kernel", 3: "linear_kernel", 12: "copyout_kernel"}
+POOL_PASS = "pool pass behind a conv (localpool_kernel / bipool2_kernel)"
+
+
+def unfused_stages(eng, plan, batch, ts, hbm_gbs):
+    """North star: 'achieved HBM GB/s for unfused elementwise and pooling
+    stages, each against B200 peak'.  Every launch of the timed plan that is
+    not a tensor-core conv -- the NCHW ingest, a pooling pass behind a pooled
+    conv (conv into a float32 scratch map, then the pool launch), standalone
+    pool / elementwise units, dense layers -- with its algorithmic bytes
+    (float32 input read once + output written once [+ weights]; the ingest's
+    and the pools' split fp16 hi/lo outputs are 4 bytes per element too), its
+    in-graph device time (Plan.timeline_passes) and the fraction of the
+    measured HBM peak that makes."""
+    lw = eng.lw
+    n = plan.n_units
+    um, pm = ts.unit_ms(), ts.pass_ms()
+
+    def numel(t):
+        d = lw.tensors[t]
+        return batch * d.c * d.h * d.w
+
+    rows = []
+    for i, u in enumerate(lw.units):
+        kind = u["kind"]
+        if plan.unit_impl(i) == 7:
+            continue
+        if kind == 2:
+            if pm[i] > 0:
+                # the conv wrote its unpooled map; the pass reads it and writes the unit's output
+                g, shapes = lw.graph, lw.shapes
+                from paper_2509_22857_b200.graph import ConvNode
+                conv = next(nid for nid in lw.unit_nodes[i] if isinstance(g.nodes[nid], ConvNode))
+                co, ho, wo = shapes[conv]
+                byts = 4.0 * (batch * co * ho * wo + numel(u["out"]))
+                rows.append(("pool pass of unit %d" % i, pm[i], byts))
+            continue
+        if um[i] <= 0 or kind == 12:
+            continue
+        if kind == 3:
+            byts = 4.0 * (batch * u["cin"] + batch * u["cout"] + u["cin"] * u["cout"] + u["cout"])
+            name = "linear_kernel (unit %d)" % i
+        else:
+            byts = 4.0 * ((numel(u["in_"]) if u.get("in_", -1) >= 0 else numel(u["out"])) + numel(u["out"]))
+            name = "%s (unit %d)" % (OTHER_NAMES.get(kind, "eltwise / pool kernel"), i)
+        rows.append((name, um[i], byts))
+    return [{"stage": nm, "us": round(ms * 1e3, 2), "algorithmic_bytes": int(b),
+             "achieved_gbs": round(b / (ms * 1e-3) / 1e9, 1), "frac_hbm": round(b / (ms * 1e-3) / 1e9 / hbm_gbs, 3)}
+            for nm, ms, b in rows]
 
 
 def unit_cost(eng, i, batch):
@@ -193,11 +241,13 @@ class TimelineStats:
 
     def __init__(self, eng, plan):
         self.eng, self.plan = eng, plan
-        n = plan.n_units
+        n = self.n = plan.n_units
         self.launch_of = [plan.unit_launch(i) for i in range(n)]
         self.family = [unit_family(eng, plan, self.launch_of[i]) for i in range(n)]
+        # rows n + u of Plan.timeline_passes: the pooling pass behind pooled conv unit u
+        self.family += [POOL_PASS] * n
         self.fam_ns = {}
-        self.unit_ns = np.zeros(n)
+        self.unit_ns = np.zeros(2 * n)
         self.span_ns = []
         self.steps = 0
 
@@ -218,10 +268,13 @@ class TimelineStats:
         return {f: t / self.steps * 1e-6 for f, t in self.fam_ns.items()}
 
     def unit_ms(self):
-        return self.unit_ns / max(self.steps, 1) * 1e-6
+        return self.unit_ns[:self.n] / max(self.steps, 1) * 1e-6
+
+    def pass_ms(self):
+        return self.unit_ns[self.n:] / max(self.steps, 1) * 1e-6
 
     def launches(self, fam):
-        return sum(1 for i in range(len(self.family)) if self.family[i] == fam and self.launch_of[i] == i
+        return sum(1 for i in range(self.n) if self.family[i] == fam and self.launch_of[i] == i
                    and (self.eng.lw.units[i]["kind"] == 2 or fam == KERNEL_NAMES[7]))
 
 
@@ -565,7 +618,7 @@ def measure(name, args, rank, world, local, flush, options, e2e=True):
             ends[i].record(stream)
             # the step's launch timeline (D2H after its end event; not timed)
             if options.timeline:
-                ts.add(plan.timeline())
+                ts.add(plan.timeline_passes())
         torch.cuda.synchronize()
         t_end = time.perf_counter() + 0.3
         while time.perf_counter() < t_end:
@@ -660,6 +713,8 @@ def record(res, args, world):
            "roofline": roof, "clocks": res["clocks"],
            "device_step_span_ms": round(float(np.median(res["ts"].span_ns)) * 1e-6, 4) if res["ts"].steps else None,
            "unit_ms": [round(float(v), 4) for v in res["ts"].unit_ms()]}
+    if res["ts"].steps:
+        rec["unfused_stages"] = unfused_stages(eng, plan, batch, res["ts"], peaks()[0])
     if "e2e" in res:
         rec["e2e"] = {"value": round(res["e2e"], 2), "unit": UNIT, "h2d_bytes_per_step": res["h2d"],
                       "d2h_bytes_per_step": res["d2h"],

@@ -309,8 +309,11 @@ int pcnn_plan_create_ex(const pcnn_unit_desc* units, int n_units,
 /* Device timeline of the last forward (options.timeline): for each unit u,
  * ns[2u] = %globaltimer when its launch's first CTA passed its dependency
  * wait, ns[2u + 1] = when its last CTA exited; both 0 for a unit that ran
- * inside another unit's launch (fused) or launched nothing.  Synchronises
- * `stream`.  Returns the number of units written (<= max_units).          */
+ * inside another unit's launch (fused) or launched nothing.  Entries
+ * n_units + u (max_units up to 2 n_units) hold the pooling pass that follows
+ * a pooled conv unit u (conv into plan scratch, then the pool launch), 0 when
+ * the unit has none.  Synchronises `stream`.  Returns the number of entries
+ * written (<= max_units).                                                  */
 int pcnn_plan_timeline(pcnn_plan* plan, int64_t* ns, int max_units, void* stream);
 /* the unit whose launch computes unit u (u itself unless fused) */
 int pcnn_plan_unit_launch(const pcnn_plan* plan, int unit);

@@ -331,7 +331,7 @@ void enqueue_unit(pcnn_plan* p, int ui, const float* x, float* logits, cudaStrea
       else launch_conv_simt(a, s);
       if (p->has_post_pool[ui]) {
         EltArgs e = p->post_pool[ui];
-        e.tl = tl;
+        e.tl = tl ? tl + 2 * p->units.size() : nullptr;  // the pass has its own timeline slot
         launch_eltwise(e, s, (int)p->opt.pdl);
       }
       break;
@@ -389,7 +389,7 @@ void enqueue_all(pcnn_plan* p, const float* x, float* logits, cudaStream_t s) {
   if (p->any_split) { r.p[k] = reinterpret_cast<uint32_t*>(p->status_dev); r.n[k++] = 1; }
   if (p->flags_on) { r.p[k] = reinterpret_cast<uint32_t*>(p->flags_dev); r.n[k++] = (int64_t)p->flags_n; }
   if (p->sk_flags) { r.p[k] = reinterpret_cast<uint32_t*>(p->sk_flags); r.n[k++] = (int64_t)p->sk_flags_n; }
-  if (p->tl_dev) { r.p[k] = reinterpret_cast<uint32_t*>(p->tl_dev); r.n[k++] = 4 * (int64_t)p->units.size(); }
+  if (p->tl_dev) { r.p[k] = reinterpret_cast<uint32_t*>(p->tl_dev); r.n[k++] = 8 * (int64_t)p->units.size(); }
   if (k) plan_reset_kernel<<<1, 256, 0, s>>>(r);
   if (p->net_on) {
     NetParams P = p->net;
@@ -1069,7 +1069,8 @@ int pcnn_plan_create_ex(const pcnn_unit_desc* units, int n_units, const pcnn_ten
   cudaMemset(p->status_dev, 0, sizeof(int));
   *p->status_host = 0;
   if (p->opt.timeline) {
-    const size_t tb = sizeof(unsigned long long) * 2 * (size_t)n_units;
+    // slots [0, n): the units' launches; [n, 2n): a pooled conv's pooling pass
+    const size_t tb = sizeof(unsigned long long) * 4 * (size_t)n_units;
     if (cudaMalloc(&p->tl_dev, tb) != cudaSuccess || cudaMallocHost(&p->tl_host, tb) != cudaSuccess) {
       pcnn_plan_destroy(p);
       return fail(PCNN_ERR_CUDA, "timeline allocation failed");
@@ -1157,7 +1158,7 @@ int pcnn_plan_destroy(pcnn_plan* p) {
 int pcnn_plan_timeline(pcnn_plan* p, int64_t* ns, int max_units, void* stream) {
   if (!p || !ns || max_units < 0) return fail(PCNN_ERR_INVALID, "pcnn_plan_timeline: null argument");
   if (!p->tl_dev) return fail(PCNN_ERR_INVALID, "pcnn_plan_timeline: plan created without options.timeline");
-  const int n = std::min(max_units, (int)p->units.size());
+  const int n = std::min(max_units, 2 * (int)p->units.size());
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   PCNN_CUDA(cudaMemcpyAsync(p->tl_host, p->tl_dev, sizeof(unsigned long long) * 2 * (size_t)n,
                             cudaMemcpyDeviceToHost, s));
@@ -1344,7 +1345,8 @@ int pcnn_forward_unit(pcnn_plan* p, int unit, const float* x, float* logits, voi
                     static_cast<cudaStream_t>(stream));
   }
   if (p->tl_dev)
-    cudaMemsetAsync(p->tl_dev + 2 * unit, 0, 2 * sizeof(unsigned long long), static_cast<cudaStream_t>(stream));
+    for (size_t slot : {(size_t)unit, p->units.size() + (size_t)unit})
+      cudaMemsetAsync(p->tl_dev + 2 * slot, 0, 2 * sizeof(unsigned long long), static_cast<cudaStream_t>(stream));
   enqueue_unit(p, unit, x, logits, static_cast<cudaStream_t>(stream), false);
   PCNN_CUDA(cudaGetLastError());
   return PCNN_OK;

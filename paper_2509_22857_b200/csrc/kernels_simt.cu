@@ -639,6 +639,58 @@ __global__ void localpool_cb4_kernel(EltArgs a) {
   }
 }
 
+// k x k / stride local sum pool over row bands: a block takes kPoolBandRows
+// pooled rows of one (image, channel block); the input rows they need are one
+// contiguous piece of the channel-blocked map ((rows - 1) * stride + k rows
+// of w * cb floats), fetched by ONE bulk copy into shared memory -- every
+// input element leaves L2 once per band (9 rows for 4 pooled rows of a
+// 3x3/s2 pool instead of 2.25 reads per element through L1), in long
+// contiguous reads.  Same per-window summation order as localpool_kernel.
+constexpr int kPoolBandRows = 4;  // most pooled rows per block
+__global__ void localpool_band_kernel(EltArgs a, int bands, int brows) {
+  TlScope tls(a.tl);
+  extern __shared__ __align__(128) float pool_sm[];
+  __shared__ uint64_t bar;
+  const TensorView& in = a.in;
+  const TensorView& o = a.out;
+  const int cb = in.cb, gpb = cb / 4, rowf = in.w * cb;
+  int id = blockIdx.x;
+  const int band = id % bands;
+  id /= bands;
+  const int blk = id % o.nblk, b = id / o.nblk;
+  const int y0 = band * brows, y1 = min(y0 + brows, o.h);
+  const int r0 = max(y0 * a.st - a.pad, 0), r1 = min((y1 - 1) * a.st - a.pad + a.k, in.h);  // input rows [r0, r1)
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(ptx::smem_u32(&bar), 1);
+    ptx::fence_mbar_init();
+    const uint32_t bytes = (uint32_t)(r1 - r0) * (uint32_t)rowf * 4u;
+    ptx::mbar_arrive_tx(ptx::smem_u32(&bar), bytes);
+    ptx::bulk_g2s(ptx::smem_u32(pool_sm), in.at(b, blk * cb, r0, 0), bytes, ptx::smem_u32(&bar));
+  }
+  __syncthreads();
+  const float dv = __ldg(a.p);
+  ptx::mbar_wait(ptx::smem_u32(&bar), 0);
+  const int per = (y1 - y0) * o.w * gpb;
+  for (int i = threadIdx.x; i < per; i += blockDim.x) {
+    const int gi = i % gpb;
+    const int r = i / gpb;
+    const int xw = r % o.w, y = y0 + r / o.w;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int dy = 0; dy < a.k; ++dy) {
+      const int iy = y * a.st - a.pad + dy;
+      if (iy < r0 || iy >= r1) continue;
+      const float* row = pool_sm + (size_t)(iy - r0) * rowf + gi * 4;
+      for (int dx = 0; dx < a.k; ++dx) {
+        const int ix = xw * a.st - a.pad + dx;
+        if (ix < 0 || ix >= in.w) continue;
+        const float4 v = *reinterpret_cast<const float4*>(row + ix * cb);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
+    }
+    store4_any(o, b, blk * cb + gi * 4, y, xw, acc.x * dv, acc.y * dv, acc.z * dv, acc.w * dv);
+  }
+}
+
 // 2x2 / stride-2 window through two bivariate polynomials (axis 0: along w,
 // then across rows; 1: along h, then across columns), 4 channels per thread,
 // consecutive threads on consecutive memory (channel sub-group, then x);
@@ -709,6 +761,23 @@ void launch_eltwise(const EltArgs& a, cudaStream_t s, int pdl) {
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 32);
     launch_pdl(localpool_cb4_kernel, std::max(blocks, 1), 256, 0, s, pdl, a);
     return;
+  }
+  if (a.kind == PCNN_UNIT_LOCALPOOL && !a.in.split && a.in.cb == a.out.cb && a.pool == 0 &&
+      (reinterpret_cast<uintptr_t>(a.in.base) & 15) == 0) {
+    // row bands through shared memory: the most pooled rows per block (4, 2
+    // or 1) whose input rows fit 72 KB, so three blocks share an SM
+    for (int brows = kPoolBandRows; brows >= 1; brows >>= 1) {
+      const size_t smem = (size_t)((brows - 1) * a.st + a.k) * a.in.w * a.in.cb * sizeof(float);
+      if (smem > 72 * 1024 || brows > a.out.h) continue;
+      static bool attr_set = false;
+      if (!attr_set) {
+        cudaFuncSetAttribute(localpool_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 72 * 1024);
+        attr_set = true;
+      }
+      const int bands = (a.out.h + brows - 1) / brows;
+      launch_pdl(localpool_band_kernel, a.batch * a.out.nblk * bands, 256, smem, s, pdl, a, bands, brows);
+      return;
+    }
   }
   if (a.kind == PCNN_UNIT_LOCALPOOL && !a.in.split && a.in.cb == a.out.cb) {
     const int64_t total = (int64_t)a.batch * a.out.nblk * a.out.h * a.out.w * (a.in.cb / 4);

@@ -106,6 +106,16 @@ class Plan:
             L.check(n, "pcnn_plan_timeline")
         return np.frombuffer(buf, dtype=np.int64).reshape(self.n_units, 2).copy()
 
+    def timeline_passes(self, stream=None) -> np.ndarray:
+        """(2 n_units, 2): rows [0, n) as `timeline`, row n + u the pooling
+        pass launched after pooled conv unit u (0, 0 when it has none)."""
+        m = 2 * self.n_units
+        buf = (L.c_i64 * (2 * m))()
+        n = L.lib().pcnn_plan_timeline(self.handle, buf, m, _stream_handle(stream))
+        if n < 0:
+            L.check(n, "pcnn_plan_timeline")
+        return np.frombuffer(buf, dtype=np.int64).reshape(m, 2).copy()
+
     def read_tensor(self, t: int) -> np.ndarray:
         """Copy tensor t out of the workspace, decoded from its storage format
         (csrc/common.cuh) to float32 (B, C, H, W), or (B, C) for vectors.
