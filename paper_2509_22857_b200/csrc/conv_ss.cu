@@ -222,11 +222,14 @@ __device__ __forceinline__ void ss_stage(bool concat, uint32_t dm, uint32_t dc, 
                                              uint32_t accm, uint32_t accc, const uint64_t* o) {
   const uint32_t e = elect_one_sync();
   if (concat) {
+    // same-shape MMAs back to back (all N = 2 NT products, then all N = NT):
+    // alternating the two shapes tap by tap cost the image-resident kernels
+    // 3-5 % (RN20 span 230 -> 223 us, A/B on one box); each accumulator
+    // still sees its products in tap order
 #pragma unroll
-    for (int t = 0; t < TAPS; ++t) {
-      mma_ss<PAIR>(e, dm, ah + o[t], b + t * bstep, id2, t ? 1u : accm);
-      mma_ss<PAIR>(e, dc, al + o[t], b + t * bstep, id1, 1u);
-    }
+    for (int t = 0; t < TAPS; ++t) mma_ss<PAIR>(e, dm, ah + o[t], b + t * bstep, id2, t ? 1u : accm);
+#pragma unroll
+    for (int t = 0; t < TAPS; ++t) mma_ss<PAIR>(e, dc, al + o[t], b + t * bstep, id1, 1u);
   } else {
 #pragma unroll
     for (int t = 0; t < TAPS; ++t) {
