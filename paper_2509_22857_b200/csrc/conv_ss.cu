@@ -2086,7 +2086,14 @@ constexpr int kWaveMaxSub = 16;  // pairs of epilogue warpgroups take even / odd
 // two MMA warps (even / odd jobs): one warp's dependency waits (~200-300
 // cycles per mbarrier test) overlap the other warp's MMA issue
 #ifndef PCNN_WAVE_MMA_WARPS
-#define PCNN_WAVE_MMA_WARPS 2  // 3 warps: stage-1 run 77.9 -> 75.4 us, but the rn20_fixture golden forward fails (deterministic 2.5e-4 deviation): not shipped
+#define PCNN_WAVE_MMA_WARPS 2
+// Two, not more: ready[layer & 1][s] is reused every second layer and waited
+// on by parity.  A warp's previous job (l+1, s-2) waited for layer l at
+// s-3 .. s-1, which implies layer l-2 complete at s-5 .. s+1 -- every barrier
+// job (l+1, s) tests has finished its previous phase.  With three warps the
+// previous job is (l+1, s-3), layer l-2 at s+1 may still be pending, the
+// parity aliases and the job reads a stale sub-tile (3 warps: stage-1 run
+// 77.9 -> 75.4 us, rn20_fixture golden forward off by 2.5e-4).
 #endif
 constexpr int kWaveMmaWarps = PCNN_WAVE_MMA_WARPS;  // MMA-issuing warps kWaveMma .. kWaveMma + kWaveMmaWarps - 1
 constexpr int kWaveThreads2 = 32 * (kWaveMma + kWaveMmaWarps);
